@@ -1,0 +1,114 @@
+"""ctypes binding of libdpipe.so (the C ABI declared in include/dpipe.h).
+
+The library is built in-tree by ``make`` (see ``__graft_entry__.build``).
+There is no fallback: if the shared object is missing or a call fails, the
+caller gets an exception.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdpipe.so")
+
+DP_F32 = 0
+DP_BF16 = 1
+DP_OUT_STORE = 0
+DP_OUT_ATOMIC_ADD = 1
+
+c_int, c_i64, c_float, c_void_p = ctypes.c_int, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p
+
+
+class DpGemmArgs(ctypes.Structure):
+    _fields_ = [
+        ("M", c_int), ("N", c_int), ("K", c_int),
+        ("batch1", c_int), ("batch2", c_int),
+        ("dtype", c_int),
+        ("A", c_void_p), ("a_ld", c_i64), ("a_bs1", c_i64), ("a_bs2", c_i64), ("a_mn_major", c_int),
+        ("B", c_void_p), ("b_ld", c_i64), ("b_bs1", c_i64), ("b_bs2", c_i64), ("b_mn_major", c_int),
+        ("D", c_void_p), ("d_dtype", c_int), ("d_ld", c_i64), ("d_bs1", c_i64), ("d_bs2", c_i64),
+        ("out_mode", c_int),
+        ("bias", c_void_p),
+        ("Res", c_void_p), ("r_ld", c_i64), ("r_bs1", c_i64), ("r_bs2", c_i64),
+        ("alpha", c_float),
+        ("split_k", c_int),
+    ]
+
+
+class DpConvArgs(ctypes.Structure):
+    _fields_ = [
+        ("dtype", c_int),
+        ("N", c_int), ("H", c_int), ("W", c_int), ("C", c_int),
+        ("K", c_int), ("R", c_int), ("S", c_int),
+        ("stride", c_int), ("pad_h", c_int), ("pad_w", c_int),
+        ("P", c_int), ("Q", c_int),
+        ("x", c_void_p), ("w", c_void_p), ("y", c_void_p),
+        ("bias", c_void_p), ("Res", c_void_p),
+        ("alpha", c_float),
+        ("out_mode", c_int),
+        ("split_k", c_int),
+    ]
+
+
+# name -> argtypes (restype is always c_int unless listed in _RESTYPES)
+_SIGNATURES = {
+    "dp_gemm": [ctypes.POINTER(DpGemmArgs), c_void_p],
+    "dp_conv_fwd": [ctypes.POINTER(DpConvArgs), c_void_p],
+    "dp_conv_wgrad": [ctypes.POINTER(DpConvArgs), c_void_p],
+    "dp_im2col": [c_int, c_void_p, c_void_p] + [c_int] * 11 + [c_void_p],
+    "dp_col2im": [c_int, c_void_p, c_void_p] + [c_int] * 11 + [c_void_p],
+    "dp_conv_weight_flip": [c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p],
+    "dp_dilate": [c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p],
+    "dp_last_error": [],
+    "dp_version": [],
+}
+_RESTYPES = {"dp_last_error": ctypes.c_char_p}
+
+_lib = None
+
+
+class DpipeError(RuntimeError):
+    pass
+
+
+def exported_symbols() -> list[str]:
+    return sorted(_SIGNATURES)
+
+
+def register(name: str, argtypes: list, restype=ctypes.c_int) -> None:
+    """Declare an additional C-ABI entry point (used by kernel-family modules)."""
+    _SIGNATURES[name] = argtypes
+    if restype is not ctypes.c_int:
+        _RESTYPES[name] = restype
+    if _lib is not None:
+        _bind(_lib, name)
+
+
+def _bind(lib, name):
+    fn = getattr(lib, name)
+    fn.argtypes = _SIGNATURES[name]
+    fn.restype = _RESTYPES.get(name, ctypes.c_int)
+
+
+def lib():
+    """Load libdpipe.so once; raise loudly when it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DpipeError(
+                f"{LIB_PATH} not found: build the CUDA extension first "
+                "(python -c 'import __graft_entry__ as g; g.build()' or `make`)"
+            )
+        handle = ctypes.CDLL(LIB_PATH)
+        for name in _SIGNATURES:
+            _bind(handle, name)
+        _lib = handle
+    return _lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = lib().dp_last_error().decode(errors="replace")
+        raise DpipeError(f"{what} failed (code {rc}): {msg}")

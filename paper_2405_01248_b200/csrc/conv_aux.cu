@@ -1,0 +1,179 @@
+// Convolution lowering helpers: im2col / col2im (generic path for small-channel
+// convs and the fp32 configuration), dgrad weight flip, and zero-dilation of
+// the output gradient (dgrad of strided convs as a stride-1 conv).
+#include <string>
+#include "common.cuh"
+#include "dpipe.h"
+
+namespace dp {
+void set_error(const std::string& s);
+
+template <typename T>
+__global__ void im2col_kernel(const T* __restrict__ x, T* __restrict__ cols, int N, int H, int W,
+                              int C, int R, int S, int stride, int ph, int pw, int P, int Q,
+                              int64_t total) {
+  const int64_t ncol = (int64_t)R * S * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / ncol;
+    const int col = static_cast<int>(i - row * ncol);
+    const int c = col % C;
+    const int tap = col / C;
+    const int s = tap % S, r = tap / S;
+    const int q = static_cast<int>(row % Q);
+    const int64_t t = row / Q;
+    const int p = static_cast<int>(t % P);
+    const int n = static_cast<int>(t / P);
+    const int h = p * stride + r - ph, w = q * stride + s - pw;
+    T v = from_f<T>(0.f);
+    if (h >= 0 && h < H && w >= 0 && w < W) v = x[(((int64_t)n * H + h) * W + w) * C + c];
+    cols[i] = v;
+  }
+}
+
+// Gather form of col2im (deterministic): each input element sums the columns that read it.
+template <typename T>
+__global__ void col2im_kernel(const T* __restrict__ cols, T* __restrict__ dx, int N, int H, int W,
+                              int C, int R, int S, int stride, int ph, int pw, int P, int Q,
+                              int64_t total) {
+  const int64_t ncol = (int64_t)R * S * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = static_cast<int>(i % C);
+    int64_t t = i / C;
+    const int w = static_cast<int>(t % W);
+    t /= W;
+    const int h = static_cast<int>(t % H);
+    const int n = static_cast<int>(t / H);
+    float acc = 0.f;
+    for (int r = 0; r < R; ++r) {
+      const int hp = h + ph - r;
+      if (hp < 0 || hp % stride) continue;
+      const int p = hp / stride;
+      if (p >= P) continue;
+      for (int s = 0; s < S; ++s) {
+        const int wq = w + pw - s;
+        if (wq < 0 || wq % stride) continue;
+        const int q = wq / stride;
+        if (q >= Q) continue;
+        const int64_t row = ((int64_t)n * P + p) * Q + q;
+        acc += to_f<T>(cols[row * ncol + (r * S + s) * C + c]);
+      }
+    }
+    dx[i] = from_f<T>(to_f<T>(dx[i]) + acc);
+  }
+}
+
+template <typename T>
+__global__ void flip_kernel(const T* __restrict__ w, T* __restrict__ wt, int K, int R, int S,
+                            int C) {
+  const int64_t total = (int64_t)K * R * S * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    // i indexes w[k][r][s][c]
+    const int c = static_cast<int>(i % C);
+    int64_t t = i / C;
+    const int s = static_cast<int>(t % S);
+    t /= S;
+    const int r = static_cast<int>(t % R);
+    const int k = static_cast<int>(t / R);
+    wt[(((int64_t)c * R + (R - 1 - r)) * S + (S - 1 - s)) * K + k] = w[i];
+  }
+}
+
+template <typename T>
+__global__ void dilate_kernel(const T* __restrict__ dy, T* __restrict__ out, int N, int P, int Q,
+                              int C, int stride) {
+  const int Ho = P * stride, Wo = Q * stride;
+  const int64_t total = (int64_t)N * Ho * Wo * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = static_cast<int>(i % C);
+    int64_t t = i / C;
+    const int w = static_cast<int>(t % Wo);
+    t /= Wo;
+    const int h = static_cast<int>(t % Ho);
+    const int n = static_cast<int>(t / Ho);
+    T v = from_f<T>(0.f);
+    if (h % stride == 0 && w % stride == 0)
+      v = dy[(((int64_t)n * P + h / stride) * Q + w / stride) * C + c];
+    out[i] = v;
+  }
+}
+
+static inline int grid_for(int64_t total) {
+  int64_t g = (total + 255) / 256;
+  const int64_t cap = (int64_t)kNumSMs * 16;
+  return static_cast<int>(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+static int check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return e;
+}
+
+}  // namespace dp
+
+using namespace dp;
+
+extern "C" {
+
+int dp_im2col(int dtype, const void* x, void* cols, int N, int H, int W, int C, int R, int S,
+              int stride, int pad_h, int pad_w, int P, int Q, dp_stream_t stream) {
+  const int64_t total = (int64_t)N * P * Q * R * S * C;
+  if (total == 0) return 0;
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  if (dtype == DP_F32)
+    im2col_kernel<float><<<grid_for(total), 256, 0, st>>>(
+        (const float*)x, (float*)cols, N, H, W, C, R, S, stride, pad_h, pad_w, P, Q, total);
+  else
+    im2col_kernel<__nv_bfloat16><<<grid_for(total), 256, 0, st>>>(
+        (const __nv_bfloat16*)x, (__nv_bfloat16*)cols, N, H, W, C, R, S, stride, pad_h, pad_w, P,
+        Q, total);
+  return check("im2col");
+}
+
+int dp_col2im(int dtype, const void* cols, void* dx, int N, int H, int W, int C, int R, int S,
+              int stride, int pad_h, int pad_w, int P, int Q, dp_stream_t stream) {
+  const int64_t total = (int64_t)N * H * W * C;
+  if (total == 0) return 0;
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  if (dtype == DP_F32)
+    col2im_kernel<float><<<grid_for(total), 256, 0, st>>>(
+        (const float*)cols, (float*)dx, N, H, W, C, R, S, stride, pad_h, pad_w, P, Q, total);
+  else
+    col2im_kernel<__nv_bfloat16><<<grid_for(total), 256, 0, st>>>(
+        (const __nv_bfloat16*)cols, (__nv_bfloat16*)dx, N, H, W, C, R, S, stride, pad_h, pad_w, P,
+        Q, total);
+  return check("col2im");
+}
+
+int dp_conv_weight_flip(int dtype, const void* w, void* wt, int K, int R, int S, int C,
+                        dp_stream_t stream) {
+  const int64_t total = (int64_t)K * R * S * C;
+  if (total == 0) return 0;
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  if (dtype == DP_F32)
+    flip_kernel<float><<<grid_for(total), 256, 0, st>>>((const float*)w, (float*)wt, K, R, S, C);
+  else
+    flip_kernel<__nv_bfloat16><<<grid_for(total), 256, 0, st>>>(
+        (const __nv_bfloat16*)w, (__nv_bfloat16*)wt, K, R, S, C);
+  return check("conv_weight_flip");
+}
+
+int dp_dilate(int dtype, const void* dy, void* out, int N, int P, int Q, int C, int stride,
+              dp_stream_t stream) {
+  const int64_t total = (int64_t)N * P * stride * Q * stride * C;
+  if (total == 0) return 0;
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  if (dtype == DP_F32)
+    dilate_kernel<float><<<grid_for(total), 256, 0, st>>>((const float*)dy, (float*)out, N, P, Q,
+                                                           C, stride);
+  else
+    dilate_kernel<__nv_bfloat16><<<grid_for(total), 256, 0, st>>>(
+        (const __nv_bfloat16*)dy, (__nv_bfloat16*)out, N, P, Q, C, stride);
+  return check("dilate");
+}
+
+}  // extern "C"

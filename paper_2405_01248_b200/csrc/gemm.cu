@@ -1,0 +1,793 @@
+// Tensor-core GEMM / implicit-GEMM convolution for sm_100a (tcgen05 + TMEM + TMA),
+// plus the fp32 SIMT GEMM used by the fp32 (parity) configuration.
+//
+// One persistent, warp-specialised kernel serves every contraction of the
+// training step:
+//   warp 0 (1 thread)   TMA producer: fills a STAGES-deep smem ring (A 128x64, B BNx64)
+//   warp 1 (1 thread)   MMA issuer: 4 x tcgen05.mma (128 x BN x 16) per k-block into TMEM
+//   warp 2              TMEM allocator (2 accumulator buffers of BN fp32 columns)
+//   warps 4-7           epilogue: tcgen05.ld -> alpha/bias/residual -> global store or
+//                       fp32 atomic accumulate (split-K, gradient accumulation)
+// Operand "modes" only change how the producer addresses global memory:
+//   A_KMAJ / B_KMAJ     row-major [rows][K]                      (linear fwd, QK^T)
+//   A_MNMAJ / B_MNMAJ   [K][rows]                                (dgrad/wgrad, P.V)
+//   A_CONV              NHWC activations, implicit im2col: one 4-D TMA box per
+//                       (tap, 64-channel block); padding comes from TMA OOB zero fill,
+//                       stride-2 from TMA element strides
+//   A_WG_DY / B_WG_X    conv weight gradient: K runs over 64-pixel tiles of dY / shifted X
+#include <cstdio>
+#include <mutex>
+#include <string>
+#include <cudaTypedefs.h>
+#include "common.cuh"
+#include "dpipe.h"
+
+namespace dp {
+
+thread_local std::string g_last_error;
+void set_error(const std::string& s) { g_last_error = s; }
+
+enum { A_KMAJ = 0, A_MNMAJ = 1, A_CONV = 2, A_WG_DY = 3 };
+enum { B_KMAJ = 0, B_MNMAJ = 1, B_WG_X = 2 };
+
+struct TcParams {
+  int M, N;
+  int num_kb;
+  int tiles_m, tiles_n, batch1, nbatch, splits, kb_per_split;
+  int a_mode, b_mode;
+  int P, Q;        // output spatial dims (conv modes)
+  int tw, th, tn;  // pixel box (128 pixels for A_CONV, 64 for the wgrad modes)
+  int stride, pad_h, pad_w, S, cblk, C;
+  void* D;
+  int64_t d_ld, d_bs1, d_bs2;
+  int d_f32, out_mode, vec_ok;
+  const float* bias;
+  const void* R;
+  int64_t r_ld, r_bs1, r_bs2;
+  float alpha;
+};
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr uint32_t A_STAGE_BYTES = BM * BK * 2;
+
+template <int BN>
+struct TcCfg {
+  static constexpr uint32_t B_STAGE_BYTES = BN * BK * 2;
+  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256 ? 256 : 512);
+  static constexpr size_t SMEM = 1024 + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 256;
+};
+
+DP_DEV void pixel_origin(int pix0, int P, int Q, int& n, int& h, int& w) {
+  const int pq = P * Q;
+  n = pix0 / pq;
+  const int rem = pix0 - n * pq;
+  h = rem / Q;
+  w = rem - h * Q;
+}
+
+template <int BN>
+DP_DEV void epilogue_store(const TcParams& p, int row, int n, int z1, int z2, const uint32_t (&v)[32]) {
+  float f[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * p.alpha;
+  const int nvalid = min(32, p.N - n);
+  if (p.bias) {
+    if (nvalid == 32) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) f[i] += __ldg(p.bias + n + i);
+    } else {
+      for (int i = 0; i < nvalid; ++i) f[i] += __ldg(p.bias + n + i);
+    }
+  }
+  if (p.R) {
+    const int64_t roff = z1 * p.r_bs1 + z2 * p.r_bs2 + (int64_t)row * p.r_ld + n;
+    if (p.d_f32) {
+      const float* r = reinterpret_cast<const float*>(p.R) + roff;
+      for (int i = 0; i < nvalid; ++i) f[i] += r[i];
+    } else {
+      const __nv_bfloat16* r = reinterpret_cast<const __nv_bfloat16*>(p.R) + roff;
+      if (nvalid == 32 && p.vec_ok) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u = *reinterpret_cast<const uint4*>(r + q * 8);
+          const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) f[q * 8 + i] += __bfloat162float(b[i]);
+        }
+      } else {
+        for (int i = 0; i < nvalid; ++i) f[i] += __bfloat162float(r[i]);
+      }
+    }
+  }
+  const int64_t doff = z1 * p.d_bs1 + z2 * p.d_bs2 + (int64_t)row * p.d_ld + n;
+  if (p.d_f32) {
+    float* d = reinterpret_cast<float*>(p.D) + doff;
+    if (p.out_mode == DP_OUT_ATOMIC_ADD) {
+      if (nvalid == 32 && p.vec_ok) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          atomicAdd(reinterpret_cast<float4*>(d + 4 * q),
+                    make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]));
+      } else {
+        for (int i = 0; i < nvalid; ++i) atomicAdd(d + i, f[i]);
+      }
+    } else {
+      if (nvalid == 32 && p.vec_ok) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(d + 4 * q) =
+              make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+      } else {
+        for (int i = 0; i < nvalid; ++i) d[i] = f[i];
+      }
+    }
+  } else {
+    __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(p.D) + doff;
+    if (nvalid == 32 && p.vec_ok) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 u;
+        u.x = pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]);
+        u.y = pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]);
+        u.z = pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]);
+        u.w = pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]);
+        *reinterpret_cast<uint4*>(d + q * 8) = u;
+      }
+    } else {
+      for (int i = 0; i < nvalid; ++i) d[i] = __float2bfloat16_rn(f[i]);
+    }
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(256, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const TcParams p) {
+  using Cfg = TcCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int total = p.tiles_m * p.tiles_n * p.splits * p.nbatch;
+
+  if (threadIdx.x == 0) {
+    // ------------------------------------------------------------ TMA producer
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      int r = w;
+      const int m_blk = r % p.tiles_m;
+      r /= p.tiles_m;
+      const int n_blk = r % p.tiles_n;
+      r /= p.tiles_n;
+      const int split = r % p.splits;
+      const int z = r / p.splits;
+      const int z1 = z % p.batch1, z2 = z / p.batch1;
+      const int kb0 = split * p.kb_per_split;
+      const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+      const int m0 = m_blk * BM, n0 = n_blk * BN;
+      int cn = 0, ch = 0, cw = 0;
+      if (p.a_mode == A_CONV) {
+        pixel_origin(m0, p.P, p.Q, cn, ch, cw);
+        ch = ch * p.stride - p.pad_h;
+        cw = cw * p.stride - p.pad_w;
+      }
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_expect_tx(&full[stage], A_STAGE_BYTES + Cfg::B_STAGE_BYTES);
+        uint8_t* a_dst = sA + stage * A_STAGE_BYTES;
+        uint8_t* b_dst = sB + stage * Cfg::B_STAGE_BYTES;
+        int pn = 0, ph = 0, pw = 0;
+        if (p.a_mode == A_WG_DY || p.b_mode == B_WG_X) pixel_origin(kb * BK, p.P, p.Q, pn, ph, pw);
+        switch (p.a_mode) {
+          case A_KMAJ:
+            tma_load_4d(&tmA, &full[stage], a_dst, kb * BK, m0, z1, z2);
+            break;
+          case A_MNMAJ:
+            tma_load_4d(&tmA, &full[stage], a_dst, m0, kb * BK, z1, z2);
+            tma_load_4d(&tmA, &full[stage], a_dst + 8192, m0 + 64, kb * BK, z1, z2);
+            break;
+          case A_CONV: {
+            const int tap = kb / p.cblk;
+            const int cb = kb - tap * p.cblk;
+            const int rr = tap / p.S, ss = tap - (tap / p.S) * p.S;
+            tma_load_4d(&tmA, &full[stage], a_dst, cb * BK, cw + ss, ch + rr, cn);
+            break;
+          }
+          default:  // A_WG_DY
+            tma_load_4d(&tmA, &full[stage], a_dst, m0, pw, ph, pn);
+            tma_load_4d(&tmA, &full[stage], a_dst + 8192, m0 + 64, pw, ph, pn);
+            break;
+        }
+        switch (p.b_mode) {
+          case B_KMAJ:
+            tma_load_4d(&tmB, &full[stage], b_dst, kb * BK, n0, z1, z2);
+            break;
+          case B_MNMAJ:
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_4d(&tmB, &full[stage], b_dst + j * 8192, n0 + 64 * j, kb * BK, z1, z2);
+            break;
+          default: {  // B_WG_X
+            const int hin = ph * p.stride - p.pad_h, win = pw * p.stride - p.pad_w;
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) {
+              const int nn = n0 + 64 * j;
+              const int tap = nn / p.C;
+              const int ci = nn - tap * p.C;
+              const int rr = tap / p.S, ss = tap - (tap / p.S) * p.S;
+              tma_load_4d(&tmB, &full[stage], b_dst + j * 8192, ci, win + ss, hin + rr, pn);
+            }
+            break;
+          }
+        }
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (threadIdx.x == 32) {
+    // ------------------------------------------------------------ MMA issuer
+    const int a_mn = (p.a_mode == A_MNMAJ || p.a_mode == A_WG_DY) ? 1 : 0;
+    const int b_mn = (p.b_mode != B_KMAJ) ? 1 : 0;
+    const uint32_t idesc = idesc_bf16_f32(BM, BN, a_mn, b_mn);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      const int split = (w / (p.tiles_m * p.tiles_n)) % p.splits;
+      const int kb0 = split * p.kb_per_split;
+      const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t a_addr = smem_u32(sA + stage * A_STAGE_BYTES);
+        const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_STAGE_BYTES);
+#pragma unroll
+        for (int j = 0; j < BK / 16; ++j) {
+          const uint64_t adesc = a_mn ? smem_desc_sw128(a_addr + j * 2048, 8192, 1024)
+                                      : smem_desc_sw128(a_addr + j * 32, 16, 1024);
+          const uint64_t bdesc = b_mn ? smem_desc_sw128(b_addr + j * 2048, 8192, 1024)
+                                      : smem_desc_sw128(b_addr + j * 32, 16, 1024);
+          tc_mma_bf16(d_tmem, adesc, bdesc, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
+        }
+        tc_commit(&empty[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      tc_commit(&tfull[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int wq = warp - 4;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      int r = w;
+      const int m_blk = r % p.tiles_m;
+      r /= p.tiles_m;
+      const int n_blk = r % p.tiles_n;
+      r /= p.tiles_n;
+      const int z = r / p.splits;
+      const int z1 = z % p.batch1, z2 = z / p.batch1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = m_blk * BM + wq * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32(tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + acc * BN + c * 32, v);
+        tmem_ld_wait();
+        const int n = n_blk * BN + c * 32;
+        if (row < p.M && n < p.N) epilogue_store<BN>(p, row, n, z1, z2, v);
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+  }
+}
+
+// ====================================================================== host side
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// 4-D bf16 map. dims innermost-first; strides in ELEMENTS for dims 1..3.
+static int make_map(CUtensorMap* map, const void* base, const uint64_t dims[4],
+                    const int64_t strides_el[3], const uint32_t box[4], const uint32_t estr[4]) {
+  auto fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return DP_ERR_DRIVER;
+  }
+  cuuint64_t gdim[4];
+  cuuint64_t gstr[3];
+  for (int i = 0; i < 4; ++i) gdim[i] = dims[i] ? dims[i] : 1;
+  for (int i = 0; i < 3; ++i) {
+    int64_t s = strides_el[i] * 2;
+    if (gdim[i + 1] == 1 && (s <= 0 || s % 16)) {
+      // degenerate dimension: any legal stride works
+      s = 16;
+    }
+    if (s <= 0 || s % 16) {
+      set_error("TMA stride not a positive multiple of 16 bytes");
+      return DP_ERR_UNSUPPORTED;
+    }
+    gstr[i] = static_cast<cuuint64_t>(s);
+  }
+  if (reinterpret_cast<uintptr_t>(base) % 16) {
+    set_error("TMA base pointer not 16-byte aligned");
+    return DP_ERR_UNSUPPORTED;
+  }
+  cuuint32_t bx[4], es[4];
+  for (int i = 0; i < 4; ++i) {
+    bx[i] = box[i];
+    es[i] = estr[i];
+  }
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), gdim, gstr,
+                  bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[256];
+    snprintf(buf, sizeof(buf),
+             "cuTensorMapEncodeTiled failed (%d): dims %llu,%llu,%llu,%llu box %u,%u,%u,%u", (int)r,
+             (unsigned long long)gdim[0], (unsigned long long)gdim[1],
+             (unsigned long long)gdim[2], (unsigned long long)gdim[3], bx[0], bx[1], bx[2], bx[3]);
+    set_error(buf);
+    return DP_ERR_DRIVER;
+  }
+  return 0;
+}
+
+template <int BN>
+static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, TcParams p, int max_ctas,
+                     cudaStream_t st) {
+  using Cfg = TcCfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(Cfg::SMEM));
+    if (e != cudaSuccess) {
+      set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+      return e;
+    }
+    attr_set = true;
+  }
+  const int total = p.tiles_m * p.tiles_n * p.splits * p.nbatch;
+  const int grid = total < max_ctas ? total : max_ctas;
+  if (grid <= 0) return 0;
+  tc_gemm_kernel<BN><<<grid, 256, Cfg::SMEM, st>>>(ma, mb, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("tc_gemm launch: ") + cudaGetErrorString(e));
+    return e;
+  }
+  return 0;
+}
+
+static int pick_bn(int N) {
+  if (N <= 64) return 64;
+  if (N <= 128) return 128;
+  const int t256 = (N + 255) / 256, t128 = (N + 127) / 128;
+  return (t256 * 256 - N <= t128 * 128 - N + 32) ? 256 : 128;
+}
+
+static int launch_bn(int bn, const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& p,
+                     cudaStream_t st) {
+  switch (bn) {
+    case 64: return launch_tc<64>(ma, mb, p, kNumSMs, st);
+    case 128: return launch_tc<128>(ma, mb, p, kNumSMs, st);
+    default: return launch_tc<256>(ma, mb, p, kNumSMs, st);
+  }
+}
+
+static void choose_split(TcParams& p, int requested, bool allowed) {
+  const int tiles = p.tiles_m * p.tiles_n * p.nbatch;
+  int splits = 1;
+  if (allowed) {
+    if (requested > 0) {
+      splits = requested;
+    } else if (tiles < kNumSMs && p.num_kb >= 8) {
+      splits = (2 * kNumSMs + tiles - 1) / tiles;
+      const int max_split = p.num_kb / 4;
+      if (splits > max_split) splits = max_split;
+      if (splits < 1) splits = 1;
+    }
+  }
+  p.kb_per_split = (p.num_kb + splits - 1) / splits;
+  p.splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
+}
+
+static void fill_epilogue(TcParams& p, void* D, int d_dtype, int64_t d_ld, int64_t d_bs1,
+                          int64_t d_bs2, int out_mode, const float* bias, const void* R,
+                          int64_t r_ld, int64_t r_bs1, int64_t r_bs2, float alpha) {
+  p.D = D;
+  p.d_f32 = d_dtype == DP_F32;
+  p.d_ld = d_ld;
+  p.d_bs1 = d_bs1;
+  p.d_bs2 = d_bs2;
+  p.out_mode = out_mode;
+  p.bias = bias;
+  p.R = R;
+  p.r_ld = r_ld;
+  p.r_bs1 = r_bs1;
+  p.r_bs2 = r_bs2;
+  p.alpha = alpha;
+  const int esz = p.d_f32 ? 4 : 2;
+  bool ok = (reinterpret_cast<uintptr_t>(D) % 16 == 0) && ((d_ld * esz) % 16 == 0) &&
+            ((d_bs1 * esz) % 16 == 0) && ((d_bs2 * esz) % 16 == 0);
+  if (R)
+    ok = ok && (reinterpret_cast<uintptr_t>(R) % 16 == 0) && ((r_ld * esz) % 16 == 0) &&
+         ((r_bs1 * esz) % 16 == 0) && ((r_bs2 * esz) % 16 == 0);
+  p.vec_ok = ok ? 1 : 0;
+}
+
+int tc_gemm(const DpGemmArgs* a, cudaStream_t st) {
+  if (a->M <= 0 || a->N <= 0 || a->K <= 0) return 0;
+  if (a->out_mode == DP_OUT_ATOMIC_ADD && a->d_dtype != DP_F32) {
+    set_error("atomic accumulation needs an fp32 output");
+    return DP_ERR_ARGS;
+  }
+  const int bn = pick_bn(a->N);
+  TcParams p{};
+  p.M = a->M;
+  p.N = a->N;
+  p.num_kb = (a->K + BK - 1) / BK;
+  p.tiles_m = (a->M + BM - 1) / BM;
+  p.tiles_n = (a->N + bn - 1) / bn;
+  p.batch1 = a->batch1 > 0 ? a->batch1 : 1;
+  const int batch2 = a->batch2 > 0 ? a->batch2 : 1;
+  p.nbatch = p.batch1 * batch2;
+  p.a_mode = a->a_mn_major ? A_MNMAJ : A_KMAJ;
+  p.b_mode = a->b_mn_major ? B_MNMAJ : B_KMAJ;
+  choose_split(p, a->split_k, a->out_mode == DP_OUT_ATOMIC_ADD);
+  fill_epilogue(p, a->D, a->d_dtype, a->d_ld, a->d_bs1, a->d_bs2, a->out_mode, a->bias, a->Res,
+                a->r_ld, a->r_bs1, a->r_bs2, a->alpha);
+  CUtensorMap ma, mb;
+  const uint32_t ones[4] = {1, 1, 1, 1};
+  {
+    const int64_t s[3] = {a->a_ld, a->a_bs1, a->a_bs2};
+    if (a->a_mn_major) {
+      const uint64_t d[4] = {(uint64_t)a->M, (uint64_t)a->K, (uint64_t)p.batch1, (uint64_t)batch2};
+      const uint32_t box[4] = {64, BK, 1, 1};
+      if (int e = make_map(&ma, a->A, d, s, box, ones)) return e;
+    } else {
+      const uint64_t d[4] = {(uint64_t)a->K, (uint64_t)a->M, (uint64_t)p.batch1, (uint64_t)batch2};
+      const uint32_t box[4] = {BK, BM, 1, 1};
+      if (int e = make_map(&ma, a->A, d, s, box, ones)) return e;
+    }
+  }
+  {
+    const int64_t s[3] = {a->b_ld, a->b_bs1, a->b_bs2};
+    if (a->b_mn_major) {
+      const uint64_t d[4] = {(uint64_t)a->N, (uint64_t)a->K, (uint64_t)p.batch1, (uint64_t)batch2};
+      const uint32_t box[4] = {64, BK, 1, 1};
+      if (int e = make_map(&mb, a->B, d, s, box, ones)) return e;
+    } else {
+      const uint64_t d[4] = {(uint64_t)a->K, (uint64_t)a->N, (uint64_t)p.batch1, (uint64_t)batch2};
+      const uint32_t box[4] = {BK, (uint32_t)bn, 1, 1};
+      if (int e = make_map(&mb, a->B, d, s, box, ones)) return e;
+    }
+  }
+  return launch_bn(bn, ma, mb, p, st);
+}
+
+// Tile the output pixels (P x Q per image, N images) with boxes of `pixels`
+// pixels that are contiguous in NHWC order. Returns false when the geometry
+// does not tile (caller must lower through im2col instead).
+static bool pixel_box(int P, int Q, int pixels, int& tw, int& th, int& tn) {
+  if (Q >= pixels) {
+    if (Q % pixels) return false;
+    tw = pixels;
+    th = 1;
+    tn = 1;
+    return true;
+  }
+  if (pixels % Q) return false;
+  tw = Q;
+  if (P * Q >= pixels) {
+    if ((P * Q) % pixels) return false;
+    th = pixels / Q;
+    tn = 1;
+    return true;
+  }
+  if (pixels % (P * Q)) return false;
+  th = P;
+  tn = pixels / (P * Q);
+  return true;
+}
+
+int tc_conv_fwd(const DpConvArgs* a, cudaStream_t st) {
+  if (a->C % 64) {
+    set_error("implicit conv needs C % 64 == 0");
+    return DP_ERR_UNSUPPORTED;
+  }
+  if (a->stride < 1 || a->stride > 2) {
+    set_error("implicit conv supports stride 1 or 2");
+    return DP_ERR_UNSUPPORTED;
+  }
+  TcParams p{};
+  if (!pixel_box(a->P, a->Q, BM, p.tw, p.th, p.tn)) {
+    set_error("output spatial size does not tile into 128-pixel boxes");
+    return DP_ERR_UNSUPPORTED;
+  }
+  const int bn = pick_bn(a->K);
+  p.M = a->N * a->P * a->Q;
+  p.N = a->K;
+  p.cblk = a->C / 64;
+  p.num_kb = a->R * a->S * p.cblk;
+  p.tiles_m = (p.M + BM - 1) / BM;
+  p.tiles_n = (a->K + bn - 1) / bn;
+  p.batch1 = 1;
+  p.nbatch = 1;
+  p.a_mode = A_CONV;
+  p.b_mode = B_KMAJ;
+  p.P = a->P;
+  p.Q = a->Q;
+  p.stride = a->stride;
+  p.pad_h = a->pad_h;
+  p.pad_w = a->pad_w;
+  p.S = a->S;
+  p.C = a->C;
+  choose_split(p, a->split_k, a->out_mode == DP_OUT_ATOMIC_ADD);
+  fill_epilogue(p, a->y, a->dtype == DP_BF16 && a->out_mode != DP_OUT_ATOMIC_ADD ? DP_BF16 : DP_F32,
+                a->K, 0, 0, a->out_mode, a->bias, a->Res, a->K, 0, 0, a->alpha);
+  CUtensorMap ma, mb;
+  {
+    const uint64_t d[4] = {(uint64_t)a->C, (uint64_t)a->W, (uint64_t)a->H, (uint64_t)a->N};
+    const int64_t s[3] = {a->C, (int64_t)a->W * a->C, (int64_t)a->H * a->W * a->C};
+    const uint32_t box[4] = {64, (uint32_t)(p.tw * a->stride), (uint32_t)(p.th * a->stride),
+                             (uint32_t)p.tn};
+    const uint32_t es[4] = {1, (uint32_t)a->stride, (uint32_t)a->stride, 1};
+    if (int e = make_map(&ma, a->x, d, s, box, es)) return e;
+  }
+  {
+    const int64_t Kdim = (int64_t)a->R * a->S * a->C;
+    const uint64_t d[4] = {(uint64_t)Kdim, (uint64_t)a->K, 1, 1};
+    const int64_t s[3] = {Kdim, 0, 0};
+    const uint32_t box[4] = {BK, (uint32_t)bn, 1, 1};
+    const uint32_t ones[4] = {1, 1, 1, 1};
+    if (int e = make_map(&mb, a->w, d, s, box, ones)) return e;
+  }
+  return launch_bn(bn, ma, mb, p, st);
+}
+
+// dW[k][r][s][c] += sum_{n,p,q} dy[n][p][q][k] * x[n][p*stride+r-pad][q*stride+s-pad][c]
+int tc_conv_wgrad(const DpConvArgs* a, cudaStream_t st) {
+  if (a->C % 64 || a->K % 64) {
+    set_error("implicit wgrad needs C % 64 == 0 and K % 64 == 0");
+    return DP_ERR_UNSUPPORTED;
+  }
+  TcParams p{};
+  if (!pixel_box(a->P, a->Q, BK, p.tw, p.th, p.tn)) {
+    set_error("output spatial size does not tile into 64-pixel boxes");
+    return DP_ERR_UNSUPPORTED;
+  }
+  const int Ntot = a->R * a->S * a->C;
+  const int bn = (Ntot % 256 == 0) ? 256 : (Ntot % 128 == 0 ? 128 : 64);
+  p.M = a->K;
+  p.N = Ntot;
+  p.num_kb = (a->N * a->P * a->Q + BK - 1) / BK;
+  p.tiles_m = (a->K + BM - 1) / BM;
+  p.tiles_n = (Ntot + bn - 1) / bn;
+  p.batch1 = 1;
+  p.nbatch = 1;
+  p.a_mode = A_WG_DY;
+  p.b_mode = B_WG_X;
+  p.P = a->P;
+  p.Q = a->Q;
+  p.stride = a->stride;
+  p.pad_h = a->pad_h;
+  p.pad_w = a->pad_w;
+  p.S = a->S;
+  p.C = a->C;
+  choose_split(p, a->split_k, true);
+  fill_epilogue(p, a->y, DP_F32, Ntot, 0, 0, DP_OUT_ATOMIC_ADD, nullptr, nullptr, 0, 0, 0,
+                a->alpha);
+  CUtensorMap ma, mb;
+  {  // dy as [K][pixels] MN-major, pixel tiles as 3-D boxes
+    const uint64_t d[4] = {(uint64_t)a->K, (uint64_t)a->Q, (uint64_t)a->P, (uint64_t)a->N};
+    const int64_t s[3] = {a->K, (int64_t)a->Q * a->K, (int64_t)a->P * a->Q * a->K};
+    const uint32_t box[4] = {64, (uint32_t)p.tw, (uint32_t)p.th, (uint32_t)p.tn};
+    const uint32_t ones[4] = {1, 1, 1, 1};
+    if (int e = make_map(&ma, a->w, d, s, box, ones)) return e;
+  }
+  {
+    const uint64_t d[4] = {(uint64_t)a->C, (uint64_t)a->W, (uint64_t)a->H, (uint64_t)a->N};
+    const int64_t s[3] = {a->C, (int64_t)a->W * a->C, (int64_t)a->H * a->W * a->C};
+    const uint32_t box[4] = {64, (uint32_t)(p.tw * a->stride), (uint32_t)(p.th * a->stride),
+                             (uint32_t)p.tn};
+    const uint32_t es[4] = {1, (uint32_t)a->stride, (uint32_t)a->stride, 1};
+    if (int e = make_map(&mb, a->x, d, s, box, es)) return e;
+  }
+  return launch_bn(bn, ma, mb, p, st);
+}
+
+// ====================================================================== fp32 / generic SIMT GEMM
+// 64x64 output tile, 256 threads x (4x4) outputs, K staged 16 at a time through smem.
+// Arbitrary strides on both operands (any major), batch, epilogue identical to the TC path.
+template <typename TI>
+__global__ void __launch_bounds__(256) simt_gemm_kernel(DpGemmArgs a) {
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  const int z = blockIdx.z;
+  const int z1 = z % a.batch1, z2 = z / a.batch1;
+  const TI* A = reinterpret_cast<const TI*>(a.A) + z1 * a.a_bs1 + z2 * a.a_bs2;
+  const TI* B = reinterpret_cast<const TI*>(a.B) + z1 * a.b_bs1 + z2 * a.b_bs2;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < a.K; k0 += 16) {
+    for (int i = threadIdx.x; i < 16 * 64; i += 256) {
+      int kk, mm;
+      if (a.a_mn_major) { mm = i % 64; kk = i / 64; } else { kk = i % 16; mm = i / 16; }
+      const int m = m0 + mm, k = k0 + kk;
+      float v = 0.f;
+      if (m < a.M && k < a.K)
+        v = to_f<TI>(a.a_mn_major ? A[(int64_t)k * a.a_ld + m] : A[(int64_t)m * a.a_ld + k]);
+      As[kk][mm] = v;
+    }
+    for (int i = threadIdx.x; i < 16 * 64; i += 256) {
+      int kk, nn;
+      if (a.b_mn_major) { nn = i % 64; kk = i / 64; } else { kk = i % 16; nn = i / 16; }
+      const int n = n0 + nn, k = k0 + kk;
+      float v = 0.f;
+      if (n < a.N && k < a.K)
+        v = to_f<TI>(a.b_mn_major ? B[(int64_t)k * a.b_ld + n] : B[(int64_t)n * a.b_ld + k]);
+      Bs[kk][nn] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= a.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= a.N) continue;
+      float v = acc[i][j] * a.alpha;
+      if (a.bias) v += a.bias[n];
+      if (a.Res) {
+        const int64_t ro = z1 * a.r_bs1 + z2 * a.r_bs2 + (int64_t)m * a.r_ld + n;
+        v += a.d_dtype == DP_F32 ? reinterpret_cast<const float*>(a.Res)[ro]
+                                 : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(a.Res)[ro]);
+      }
+      const int64_t o = z1 * a.d_bs1 + z2 * a.d_bs2 + (int64_t)m * a.d_ld + n;
+      if (a.d_dtype == DP_F32) {
+        float* d = reinterpret_cast<float*>(a.D) + o;
+        if (a.out_mode == DP_OUT_ATOMIC_ADD) atomicAdd(d, v); else *d = v;
+      } else {
+        reinterpret_cast<__nv_bfloat16*>(a.D)[o] = __float2bfloat16_rn(v);
+      }
+    }
+  }
+}
+
+int simt_gemm(const DpGemmArgs* in, cudaStream_t st) {
+  DpGemmArgs a = *in;
+  if (a.M <= 0 || a.N <= 0) return 0;
+  if (a.batch1 <= 0) a.batch1 = 1;
+  if (a.batch2 <= 0) a.batch2 = 1;
+  dim3 grid((a.N + 63) / 64, (a.M + 63) / 64, a.batch1 * a.batch2);
+  if (a.dtype == DP_F32)
+    simt_gemm_kernel<float><<<grid, 256, 0, st>>>(a);
+  else
+    simt_gemm_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) set_error(std::string("simt_gemm: ") + cudaGetErrorString(e));
+  return e;
+}
+
+}  // namespace dp
+
+extern "C" {
+
+int dp_gemm(const DpGemmArgs* a, dp_stream_t stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (a->dtype == DP_BF16) {
+    // TMA needs 16-byte aligned strides; otherwise use the generic kernel.
+    const bool ok = (a->a_ld % 8 == 0) && (a->b_ld % 8 == 0) && (a->a_bs1 % 8 == 0) &&
+                    (a->a_bs2 % 8 == 0) && (a->b_bs1 % 8 == 0) && (a->b_bs2 % 8 == 0) &&
+                    (reinterpret_cast<uintptr_t>(a->A) % 16 == 0) &&
+                    (reinterpret_cast<uintptr_t>(a->B) % 16 == 0) &&
+                    ((a->batch1 <= 1 || a->a_bs1 != 0) && (a->batch1 <= 1 || a->b_bs1 != 0)) &&
+                    ((a->batch2 <= 1 || a->a_bs2 != 0) && (a->batch2 <= 1 || a->b_bs2 != 0));
+    if (ok) return dp::tc_gemm(a, st);
+  }
+  return dp::simt_gemm(a, st);
+}
+
+int dp_conv_fwd(const DpConvArgs* a, dp_stream_t stream) {
+  if (a->dtype != DP_BF16) {
+    dp::set_error("dp_conv_fwd is the bf16 tensor-core path; lower fp32 convs via dp_im2col");
+    return DP_ERR_UNSUPPORTED;
+  }
+  return dp::tc_conv_fwd(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int dp_conv_wgrad(const DpConvArgs* a, dp_stream_t stream) {
+  if (a->dtype != DP_BF16) {
+    dp::set_error("dp_conv_wgrad is the bf16 tensor-core path");
+    return DP_ERR_UNSUPPORTED;
+  }
+  return dp::tc_conv_wgrad(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
+const char* dp_last_error(void) { return dp::g_last_error.c_str(); }
+int dp_version(void) { return 1; }
+
+}  // extern "C"

@@ -1,0 +1,232 @@
+"""Torch-facing wrappers over the libdpipe C ABI (no autograd here).
+
+Every function takes/returns torch CUDA tensors, launches on the current
+torch stream, and raises when the native library is missing: there is no
+eager-PyTorch or CPU fallback on the product path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import DP_BF16, DP_F32, DP_OUT_ATOMIC_ADD, DP_OUT_STORE, DpConvArgs, DpGemmArgs, check
+
+_DT = {torch.float32: DP_F32, torch.bfloat16: DP_BF16}
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise TypeError(f"unsupported dtype {t.dtype}") from None
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("libdpipe ops need CUDA tensors (no CPU fallback on the product path)")
+
+
+# ---------------------------------------------------------------------------- GEMM
+
+def gemm(A, B, D, *, M, N, K, a_ld, b_ld, d_ld, a_mn=False, b_mn=False,
+         batch=(1, 1), a_bs=(0, 0), b_bs=(0, 0), d_bs=(0, 0),
+         bias=None, residual=None, r_ld=None, r_bs=None, alpha=1.0, accumulate=False,
+         split_k=0):
+    """D[z](m,n) = alpha * sum_k A[z](m,k) B[z](n,k) (+bias[n]) (+residual[z](m,n)).
+
+    Raw-stride interface mirroring DpGemmArgs; A and B must share a dtype
+    (bf16 -> tcgen05 tensor cores, fp32 -> fp32 SIMT path).
+    """
+    _require_cuda(A, B, D, bias, residual)
+    if A.dtype != B.dtype:
+        raise TypeError("A and B must share a dtype")
+    if bias is not None and bias.dtype != torch.float32:
+        raise TypeError("bias must be fp32")
+    args = DpGemmArgs()
+    args.M, args.N, args.K = M, N, K
+    args.batch1, args.batch2 = batch
+    args.dtype = dtype_code(A)
+    args.A, args.a_ld, (args.a_bs1, args.a_bs2), args.a_mn_major = _ptr(A), a_ld, a_bs, int(a_mn)
+    args.B, args.b_ld, (args.b_bs1, args.b_bs2), args.b_mn_major = _ptr(B), b_ld, b_bs, int(b_mn)
+    args.D, args.d_dtype, args.d_ld, (args.d_bs1, args.d_bs2) = _ptr(D), dtype_code(D), d_ld, d_bs
+    args.out_mode = DP_OUT_ATOMIC_ADD if accumulate else DP_OUT_STORE
+    args.bias = _ptr(bias)
+    args.Res = _ptr(residual)
+    args.r_ld = d_ld if r_ld is None else r_ld
+    args.r_bs1, args.r_bs2 = d_bs if r_bs is None else r_bs
+    args.alpha = alpha
+    args.split_k = split_k
+    check(_lib.lib().dp_gemm(ctypes.byref(args), _stream()), "dp_gemm")
+    return D
+
+
+def linear(x, w, bias=None, residual=None, out=None):
+    """y[M,N] = x[M,K] @ w[N,K]^T (+bias) (+residual)."""
+    M, K = x.shape
+    N = w.shape[0]
+    if out is None:
+        out = torch.empty(M, N, device=x.device, dtype=x.dtype)
+    return gemm(x, w, out, M=M, N=N, K=K, a_ld=x.stride(0), b_ld=w.stride(0), d_ld=out.stride(0),
+                bias=bias, residual=residual)
+
+
+def linear_dgrad(dy, w, out=None):
+    """dx[M,K] = dy[M,N] @ w[N,K]."""
+    M, N = dy.shape
+    K = w.shape[1]
+    if out is None:
+        out = torch.empty(M, K, device=dy.device, dtype=dy.dtype)
+    return gemm(dy, w, out, M=M, N=K, K=N, a_ld=dy.stride(0), b_ld=w.stride(0), b_mn=True,
+                d_ld=out.stride(0))
+
+
+def linear_wgrad(dy, x, dw):
+    """dw[N,K] (fp32) += dy[M,N]^T @ x[M,K]."""
+    M, N = dy.shape
+    K = x.shape[1]
+    return gemm(dy, x, dw, M=N, N=K, K=M, a_ld=dy.stride(0), a_mn=True, b_ld=x.stride(0),
+                b_mn=True, d_ld=dw.stride(0), accumulate=True)
+
+
+# ---------------------------------------------------------------------------- conv (NHWC)
+
+def conv_out_size(H, R, stride, pad_lo, pad_hi):
+    return (H + pad_lo + pad_hi - R) // stride + 1
+
+
+def _conv_args(x, w, y, stride, pad, P, Q, bias=None, residual=None, accumulate=False,
+               alpha=1.0):
+    N, H, W, C = x.shape
+    K, R, S, _ = w.shape
+    a = DpConvArgs()
+    a.dtype = dtype_code(x)
+    a.N, a.H, a.W, a.C = N, H, W, C
+    a.K, a.R, a.S = K, R, S
+    a.stride, a.pad_h, a.pad_w = stride, pad[0], pad[1]
+    a.P, a.Q = P, Q
+    a.x, a.w, a.y = _ptr(x), _ptr(w), _ptr(y)
+    a.bias, a.Res = _ptr(bias), _ptr(residual)
+    a.alpha = alpha
+    a.out_mode = DP_OUT_ATOMIC_ADD if accumulate else DP_OUT_STORE
+    a.split_k = 0
+    return a
+
+
+def implicit_ok(x, w, P, Q, stride):
+    """Can the tcgen05 implicit-GEMM path run this conv (else im2col lowering)."""
+    if x.dtype != torch.bfloat16:
+        return False
+    C = x.shape[3]
+    if C % 64 or stride not in (1, 2):
+        return False
+    return _tiles(P, Q, 128) and _tiles(P, Q, 64)
+
+
+def _tiles(P, Q, pixels):
+    if Q >= pixels:
+        return Q % pixels == 0
+    if pixels % Q:
+        return False
+    if P * Q >= pixels:
+        return (P * Q) % pixels == 0
+    return pixels % (P * Q) == 0
+
+
+def conv2d(x, w, *, stride=1, pad=(1, 1), out_hw=None, bias=None, residual=None, out=None):
+    """NHWC conv: x [N,H,W,C], w [K,R,S,C] -> y [N,P,Q,K].
+
+    pad is (top, left); bottom/right padding is implied by out_hw (default:
+    symmetric padding).
+    """
+    _require_cuda(x, w, bias, residual)
+    N, H, W, C = x.shape
+    K, R, S, C2 = w.shape
+    assert C == C2, (x.shape, w.shape)
+    if out_hw is None:
+        out_hw = (conv_out_size(H, R, stride, pad[0], pad[0]), conv_out_size(W, S, stride, pad[1], pad[1]))
+    P, Q = out_hw
+    if out is None:
+        out = torch.empty(N, P, Q, K, device=x.device, dtype=x.dtype)
+    if R == 1 and S == 1 and stride == 1 and pad == (0, 0):
+        return linear(x.reshape(-1, C), w.reshape(K, C), bias=bias,
+                      residual=None if residual is None else residual.reshape(-1, K),
+                      out=out.view(-1, K)).view(N, P, Q, K)
+    if implicit_ok(x, w, P, Q, stride):
+        a = _conv_args(x, w, out, stride, pad, P, Q, bias, residual)
+        check(_lib.lib().dp_conv_fwd(ctypes.byref(a), _stream()), "dp_conv_fwd")
+        return out
+    cols = im2col(x, R, S, stride, pad, P, Q)
+    linear(cols, w.reshape(K, -1), bias=bias,
+           residual=None if residual is None else residual.reshape(-1, K), out=out.view(-1, K))
+    return out
+
+
+def im2col(x, R, S, stride, pad, P, Q):
+    N, H, W, C = x.shape
+    cols = torch.empty(N * P * Q, R * S * C, device=x.device, dtype=x.dtype)
+    check(_lib.lib().dp_im2col(dtype_code(x), _ptr(x), _ptr(cols), N, H, W, C, R, S, stride,
+                               pad[0], pad[1], P, Q, _stream()), "dp_im2col")
+    return cols
+
+
+def col2im(cols, dx, R, S, stride, pad, P, Q):
+    N, H, W, C = dx.shape
+    check(_lib.lib().dp_col2im(dtype_code(dx), _ptr(cols), _ptr(dx), N, H, W, C, R, S, stride,
+                               pad[0], pad[1], P, Q, _stream()), "dp_col2im")
+    return dx
+
+
+def conv2d_dgrad(dy, w, x_shape, *, stride=1, pad=(1, 1)):
+    """dx [N,H,W,C] of y = conv2d(x, w)."""
+    _require_cuda(dy, w)
+    N, P, Q, K = dy.shape
+    K2, R, S, C = w.shape
+    _, H, W, _ = x_shape
+    if R == 1 and S == 1 and stride == 1 and pad == (0, 0):
+        return linear_dgrad(dy.reshape(-1, K), w.reshape(K, C)).view(N, H, W, C)
+    if dy.dtype == torch.bfloat16 and K % 64 == 0 and _tiles(H, W, 128) and _tiles(H, W, 64):
+        wt = torch.empty(C, R, S, K, device=w.device, dtype=w.dtype)
+        check(_lib.lib().dp_conv_weight_flip(dtype_code(w), _ptr(w), _ptr(wt), K, R, S, C,
+                                             _stream()), "dp_conv_weight_flip")
+        src = dy
+        if stride > 1:
+            src = torch.empty(N, P * stride, Q * stride, K, device=dy.device, dtype=dy.dtype)
+            check(_lib.lib().dp_dilate(dtype_code(dy), _ptr(dy), _ptr(src), N, P, Q, K, stride,
+                                       _stream()), "dp_dilate")
+        dx = torch.empty(N, H, W, C, device=dy.device, dtype=dy.dtype)
+        a = _conv_args(src, wt, dx, 1, (R - 1 - pad[0], S - 1 - pad[1]), H, W)
+        check(_lib.lib().dp_conv_fwd(ctypes.byref(a), _stream()), "dp_conv_fwd(dgrad)")
+        return dx
+    dcols = linear_dgrad(dy.reshape(-1, K), w.reshape(K, -1))
+    dx = torch.zeros(N, H, W, C, device=dy.device, dtype=dy.dtype)
+    return col2im(dcols, dx, R, S, stride, pad, P, Q)
+
+
+def conv2d_wgrad(dy, x, dw, *, stride=1, pad=(1, 1)):
+    """dw [K,R,S,C] (fp32, accumulated) += wgrad of y = conv2d(x, w)."""
+    _require_cuda(dy, x, dw)
+    N, P, Q, K = dy.shape
+    _, H, W, C = x.shape
+    _, R, S, _ = dw.shape
+    if R == 1 and S == 1 and stride == 1 and pad == (0, 0):
+        return linear_wgrad(dy.reshape(-1, K), x.reshape(-1, C), dw.view(K, C))
+    if dy.dtype == torch.bfloat16 and C % 64 == 0 and K % 64 == 0 and _tiles(P, Q, 64):
+        a = _conv_args(x, dw, dw, stride, pad, P, Q, accumulate=True)
+        a.w = _ptr(dy)  # wgrad reads dy through the `w` slot (see dpipe.h)
+        a.K, a.R, a.S = K, R, S
+        check(_lib.lib().dp_conv_wgrad(ctypes.byref(a), _stream()), "dp_conv_wgrad")
+        return dw
+    cols = im2col(x, R, S, stride, pad, P, Q)
+    return linear_wgrad(dy.reshape(-1, K), cols, dw.view(K, -1))

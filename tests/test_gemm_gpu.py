@@ -1,0 +1,147 @@
+"""GEMM / implicit-conv kernels vs a plain PyTorch fp32 reference (GPU)."""
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+
+def _ops():
+    from paper_2405_01248_b200 import ops
+
+    return ops
+
+
+def _rel(a, b):
+    return ((a.float() - b.float()).norm() / (b.float().norm() + 1e-12)).item()
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (300, 200, 136), (1024, 1024, 1024),
+                                   (4096, 320, 2880), (77, 1024, 1024), (512, 1280, 5120)])
+def test_linear_bf16(M, N, K):
+    ops = _ops()
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    x = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    w = torch.randn(N, K, device="cuda", generator=g).bfloat16()
+    b = torch.randn(N, device="cuda", generator=g)
+    y = ops.linear(x, w, bias=b)
+    ref = x.float() @ w.float().t() + b
+    assert _rel(y, ref) < 1e-2
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 192, 320), (300, 200, 136), (2048, 640, 640)])
+def test_linear_grads_bf16(M, N, K):
+    ops = _ops()
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    w = torch.randn(N, K, device="cuda", generator=g).bfloat16()
+    dy = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    dx = ops.linear_dgrad(dy, w)
+    assert _rel(dx, dy.float() @ w.float()) < 1e-2
+    dw = torch.zeros(N, K, device="cuda")
+    ops.linear_wgrad(dy, x, dw)
+    ops.linear_wgrad(dy, x, dw)  # accumulates
+    assert _rel(dw, 2 * dy.float().t() @ x.float()) < 1e-2
+
+
+def test_residual_epilogue():
+    ops = _ops()
+    x = torch.randn(256, 128, device="cuda").bfloat16()
+    w = torch.randn(64, 128, device="cuda").bfloat16()
+    r = torch.randn(256, 64, device="cuda").bfloat16()
+    y = ops.linear(x, w, residual=r)
+    assert _rel(y, x.float() @ w.float().t() + r.float()) < 1e-2
+
+
+@pytest.mark.parametrize("B,H,N,Nk", [(2, 5, 1024, 1024), (3, 4, 256, 77)])
+def test_batched_attention_shapes(B, H, N, Nk):
+    ops = _ops()
+    C = H * 64
+    q = torch.randn(B, N, C, device="cuda").bfloat16()
+    k = torch.randn(B, Nk, C, device="cuda").bfloat16()
+    v = torch.randn(B, Nk, C, device="cuda").bfloat16()
+    s = torch.empty(B, H, N, Nk, device="cuda", dtype=torch.float32)
+    # S[b,h] = Q_bh K_bh^T : z1 = head, z2 = batch
+    ops.gemm(q, k, s, M=N, N=Nk, K=64, a_ld=C, b_ld=C, d_ld=Nk, batch=(H, B),
+             a_bs=(64, N * C), b_bs=(64, Nk * C), d_bs=(N * Nk, H * N * Nk), alpha=0.125)
+    qh = q.float().view(B, N, H, 64).transpose(1, 2)
+    kh = k.float().view(B, Nk, H, 64).transpose(1, 2)
+    vh = v.float().view(B, Nk, H, 64).transpose(1, 2)
+    ref = qh @ kh.transpose(-1, -2) * 0.125
+    assert _rel(s, ref) < 1e-2
+    p = torch.softmax(ref, -1).bfloat16().contiguous()
+    o = torch.empty(B, N, C, device="cuda", dtype=torch.bfloat16)
+    if Nk % 8 == 0:
+        # O[b, n, h*64:] = P_bh V_bh  (V is MN-major: [Nk][64] with row stride C)
+        ops.gemm(p, v, o, M=N, N=64, K=Nk, a_ld=Nk, b_ld=C, b_mn=True, d_ld=C, batch=(H, B),
+                 a_bs=(N * Nk, H * N * Nk), b_bs=(64, Nk * C), d_bs=(64, N * C))
+        ref_o = (p.float() @ vh).transpose(1, 2).reshape(B, N, C)
+        assert _rel(o, ref_o) < 1e-2
+
+
+def test_fp32_simt_gemm():
+    ops = _ops()
+    x = torch.randn(77, 96, device="cuda")
+    w = torch.randn(50, 96, device="cuda")
+    y = ops.linear(x, w)
+    assert _rel(y, x @ w.t()) < 1e-5
+    dw = torch.zeros(50, 96, device="cuda")
+    dy = torch.randn(77, 50, device="cuda")
+    ops.linear_wgrad(dy, x, dw)
+    assert _rel(dw, dy.t() @ x) < 1e-5
+
+
+def _conv_ref(x, w, stride, pad, out_hw):
+    # x NHWC, w KRSC -> NHWC, using explicit asymmetric padding
+    N, H, W, C = x.shape
+    K, R, S, _ = w.shape
+    P, Q = out_hw
+    pad_b = (P - 1) * stride + R - H - pad[0]
+    pad_r = (Q - 1) * stride + S - W - pad[1]
+    xp = F.pad(x.permute(0, 3, 1, 2).float(), (pad[1], max(pad_r, 0), pad[0], max(pad_b, 0)))
+    y = F.conv2d(xp, w.permute(0, 3, 1, 2).float(), stride=stride)
+    return y[:, :, :P, :Q].permute(0, 2, 3, 1)
+
+
+@pytest.mark.parametrize("N,H,C,K,stride,pad", [
+    (2, 32, 64, 128, 1, (1, 1)),
+    (4, 32, 320, 320, 1, (1, 1)),
+    (8, 16, 128, 192, 1, (1, 1)),
+    (16, 8, 128, 64, 1, (1, 1)),
+    (32, 4, 64, 128, 1, (1, 1)),
+    (2, 32, 128, 128, 2, (1, 1)),
+    (2, 64, 128, 128, 2, (0, 0)),
+    (1, 256, 64, 64, 1, (1, 1)),
+])
+def test_conv_implicit(N, H, C, K, stride, pad):
+    ops = _ops()
+    g = torch.Generator(device="cuda").manual_seed(H + C)
+    x = torch.randn(N, H, H, C, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(K, 3, 3, C, device="cuda", generator=g) * 0.05).bfloat16()
+    P = ops.conv_out_size(H, 3, stride, pad[0], 1 if stride == 2 else pad[0])
+    out_hw = (P, P)
+    y = ops.conv2d(x, w, stride=stride, pad=pad, out_hw=out_hw)
+    ref = _conv_ref(x, w, stride, pad, out_hw)
+    assert _rel(y, ref) < 1e-2
+    # backward
+    dy = torch.randn_like(y)
+    xr = x.float().permute(0, 3, 1, 2).requires_grad_(True)
+    wr = w.float().permute(0, 3, 1, 2).requires_grad_(True)
+    pad_b = (P - 1) * stride + 3 - H - pad[0]
+    yr = F.conv2d(F.pad(xr, (pad[1], max(pad_b, 0), pad[0], max(pad_b, 0))), wr, stride=stride)
+    yr = yr[:, :, :P, :P]
+    yr.backward(dy.float().permute(0, 3, 1, 2))
+    dx = ops.conv2d_dgrad(dy, w, x.shape, stride=stride, pad=pad)
+    assert _rel(dx, xr.grad.permute(0, 2, 3, 1)) < 1e-2
+    dw = torch.zeros(K, 3, 3, C, device="cuda")
+    ops.conv2d_wgrad(dy, x, dw, stride=stride, pad=pad)
+    assert _rel(dw, wr.grad.permute(0, 2, 3, 1)) < 1e-2
+
+
+def test_conv_small_channels_fp32():
+    ops = _ops()
+    x = torch.randn(2, 16, 16, 8, device="cuda")
+    w = torch.randn(32, 3, 3, 8, device="cuda")
+    y = ops.conv2d(x, w, stride=1, pad=(1, 1))
+    assert _rel(y, _conv_ref(x, w, 1, (1, 1), (16, 16))) < 1e-5
