@@ -9,7 +9,7 @@ LIB := $(PKG)/libdpipe.so
 NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
            -Xcompiler -fPIC -Iinclude -I$(PKG)/csrc --expt-relaxed-constexpr -Xptxas -v
 
-all: $(LIB) oracle
+all: $(LIB)
 
 build/%.o: $(PKG)/csrc/%.cu $(HDR)
 	@mkdir -p build
@@ -18,11 +18,7 @@ build/%.o: $(PKG)/csrc/%.cu $(HDR)
 $(LIB): $(OBJ)
 	$(NVCC) -shared -gencode arch=compute_100a,code=sm_100a -o $@ $(OBJ)
 
-oracle:
-	$(MAKE) -C oracle
-
 clean:
 	rm -rf build $(LIB)
-	$(MAKE) -C oracle clean
 
-.PHONY: all clean oracle
+.PHONY: all clean

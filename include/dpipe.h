@@ -41,6 +41,7 @@ typedef struct CUstream_st* dp_stream_t; /* == cudaStream_t */
 enum { DP_F32 = 0, DP_BF16 = 1 };
 enum { DP_OUT_STORE = 0, DP_OUT_ATOMIC_ADD = 1 };
 enum { DP_ERR_ARGS = 1001, DP_ERR_UNSUPPORTED = 1002, DP_ERR_DRIVER = 1003 };
+enum { DP_ACT_NONE = 0, DP_ACT_GELU = 1, DP_ACT_GELU_TANH = 2, DP_ACT_SILU = 3 };
 
 /* D[z](m,n) = alpha * sum_k A[z](m,k) * B[z](n,k)  (+ bias[n]) (+ Res[z](m,n))
  * z = z1 + batch1 * z2.  A is "K-major" when A(m,k) = A[m*a_ld + k] and
@@ -106,6 +107,100 @@ int dp_conv_weight_flip(int dtype, const void* w, void* wt, int K, int R, int S,
 /* out[n][p*stride][q*stride][c] = dy[n][p][q][c]; other positions 0. out: [N][P*stride][Q*stride][C] */
 int dp_dilate(int dtype, const void* dy, void* out, int N, int P, int Q, int C, int stride,
               dp_stream_t stream);
+
+
+/* ---- elementwise (eltwise.cu); dtype DP_F32 / DP_BF16, n in elements ---- */
+/* y = act(x); dx (+)= dy * act'(x). 16-byte aligned pointers. */
+int dp_act_fwd(int op, int dtype, const void* x, void* y, int64_t n, dp_stream_t stream);
+int dp_act_bwd(int op, int dtype, const void* x, const void* dy, void* dx, int64_t n,
+               int accumulate, dp_stream_t stream);
+/* x [rows][2F] = [a | g] -> y [rows][F] = a * gelu(g)   (SD GEGLU feed-forward) */
+int dp_geglu_fwd(int dtype, const void* x, void* y, int64_t rows, int F, dp_stream_t stream);
+int dp_geglu_bwd(int dtype, const void* x, const void* dy, void* dx, int64_t rows, int F,
+                 dp_stream_t stream);
+/* y = alpha*a + beta*b  (b may be NULL) */
+int dp_axpby(int dtype, const void* a, const void* b, void* y, int64_t n, float alpha, float beta,
+             dp_stream_t stream);
+/* adaLN-Zero gated residual: y[r] = x[r] + g[r/rps] * h[r]; backward gives dh and dg[B][C] */
+int dp_gate_residual_fwd(int dtype, const void* x, const void* g, int64_t g_ld, const void* h,
+                         void* y, int64_t rows, int C, int rows_per_sample, dp_stream_t stream);
+int dp_gate_residual_bwd(int dtype, const void* dy, const void* g, int64_t g_ld, const void* h,
+                         void* dh, void* dg, int64_t dg_ld, int B, int C, int rows_per_sample,
+                         dp_stream_t stream);
+/* x_t = sqrt_ab[t] x0 + sqrt_1mab[t] noise ; x0_hat = (x_t - sqrt_1mab[t] eps) / sqrt_ab[t] */
+int dp_q_sample(int dtype, const void* x0, const void* noise, const int64_t* t,
+                const float* sqrt_ab, const float* sqrt_1mab, void* xt, int64_t n,
+                int64_t per_sample, dp_stream_t stream);
+int dp_pred_x0(int dtype, const void* xt, const void* eps, const int64_t* t, const float* sqrt_ab,
+               const float* sqrt_1mab, void* out, int64_t n, int64_t per_sample,
+               dp_stream_t stream);
+/* *loss_acc += scale * sum (pred - target)^2 ; dpred = 2 scale (pred - target) (dpred may be NULL) */
+int dp_mse(int dtype, const void* pred, const void* target, void* dpred, float* loss_acc,
+           int64_t n, float scale, dp_stream_t stream);
+/* sinusoidal embedding [B][dim], cos half first */
+int dp_timestep_embed(int dtype, const int64_t* t, void* out, int B, int dim, float max_period,
+                      dp_stream_t stream);
+/* out[r] = table[ids[r]] (+ pos[r % L]) */
+int dp_embed(int dtype, const int64_t* ids, const void* table, const void* pos, void* out,
+             int64_t rows, int L, int C, dp_stream_t stream);
+/* channel concat of row-major [rows][Ca] and [rows][Cb] (b NULL -> zeros) and its adjoint */
+int dp_concat(int dtype, const void* a, const void* b, void* dst, int64_t rows, int Ca, int Cb,
+              dp_stream_t stream);
+int dp_split(int dtype, const void* src, void* a, void* b, int64_t rows, int Ca, int Cb,
+             int acc_a, int acc_b, dp_stream_t stream);
+/* NHWC nearest 2x upsample and its adjoint (sum of the 4 copies) */
+int dp_upsample2x(int dtype, const void* x, void* y, int N, int H, int W, int C,
+                  dp_stream_t stream);
+int dp_upsample2x_bwd(int dtype, const void* dy, void* dx, int N, int H, int W, int C,
+                      dp_stream_t stream);
+/* per-sample channel bias: y[r] = x[r] + e[r / rows_per_sample]; de[b] = sum of dy over sample b */
+int dp_row_bias_fwd(int dtype, const void* x, const void* e, int64_t e_ld, void* y, int64_t rows,
+                    int C, int rows_per_sample, dp_stream_t stream);
+int dp_row_bias_bwd(int dtype, const void* dy, void* de, int64_t de_ld, int B, int C,
+                    int rows_per_sample, dp_stream_t stream);
+/* NHWC image [N][H][W][C] <-> patches [N][H/p][W/p][p*p*C] (DiT patchify/unpatchify);
+   H, W, C describe the image side in both directions */
+int dp_space_to_depth(int dtype, const void* x, void* y, int N, int H, int W, int C, int p,
+                      int inverse, dp_stream_t stream);
+/* db[c] += sum_r dy[r][c]  (bias gradient, fp32 accumulate) */
+int dp_bias_grad(int dtype, const void* dy, float* db, int64_t rows, int C, dp_stream_t stream);
+int dp_cast(int src_dtype, int dst_dtype, const void* x, void* y, int64_t n, dp_stream_t stream);
+/* AdamW (torch.optim.AdamW semantics) over a flat fp32 master buffer; optionally refreshes the
+   bf16 compute copy. grad_scale multiplies the gradient first. */
+int dp_adamw(float* param, const float* grad, float* exp_avg, float* exp_avg_sq,
+             void* param_bf16, int64_t n, float lr, float beta1, float beta2, float eps,
+             float weight_decay, int step, float grad_scale, dp_stream_t stream);
+
+/* ---- normalisation and softmax (norm.cu) ---- */
+/* GroupNorm(+SiLU) over NHWC [N][HW][C]; gamma/beta fp32 (NULL = no affine); mean/rstd fp32
+   [N][G] saved for backward; workspace of dp_group_norm_workspace() bytes. */
+size_t dp_group_norm_workspace(int N, int HW, int G);
+int dp_group_norm_fwd(int dtype, const void* x, const float* gamma, const float* beta, void* y,
+                      float* mean, float* rstd, int N, int HW, int C, int G, float eps, int silu,
+                      float* workspace, dp_stream_t stream);
+/* dx (+)= ..., dgamma/dbeta fp32 accumulated (may be NULL) */
+int dp_group_norm_bwd(int dtype, const void* x, const void* dy, const float* gamma,
+                      const float* beta, const float* mean, const float* rstd, void* dx,
+                      float* dgamma, float* dbeta, int N, int HW, int C, int G, int silu,
+                      int accumulate, float* workspace, dp_stream_t stream);
+/* LayerNorm over rows of C (C <= 2048). Either per-channel affine gamma/beta (fp32) or per-sample
+   adaLN modulation y = xhat*(1+mod[b][scale_off+c]) + mod[b][shift_off+c], b = row/rows_per_sample */
+int dp_layer_norm_fwd(int dtype, const void* x, const float* gamma, const float* beta,
+                      const void* mod, int64_t mod_ld, int shift_off, int scale_off,
+                      int rows_per_sample, void* y, float* mean, float* rstd, int64_t rows, int C,
+                      float eps, dp_stream_t stream);
+int dp_layer_norm_bwd(int dtype, const void* x, const void* dy, const float* gamma,
+                      const void* mod, int64_t mod_ld, int shift_off, int scale_off,
+                      int rows_per_sample, const float* mean, const float* rstd, void* dx,
+                      float* dgamma, float* dbeta, void* dmod, int64_t dmod_ld, int64_t rows,
+                      int C, int accumulate, dp_stream_t stream);
+/* P = softmax(scale * S) over rows of fp32 scores, row stride ld for S and P
+   (causal: col j masked when j > row % Lq) */
+int dp_softmax_fwd(int dtype, const float* S, void* P, int64_t rows, int cols, int ld,
+                   float scale, int causal, int Lq, dp_stream_t stream);
+/* dS = scale * P * (dP - rowsum(dP * P)), row stride ld for P, dP, dS */
+int dp_softmax_bwd(int dtype, const void* P, const float* dP, void* dS, int64_t rows, int cols,
+                   int ld, float scale, dp_stream_t stream);
 
 const char* dp_last_error(void);
 int dp_version(void);

@@ -17,6 +17,7 @@ DP_F32 = 0
 DP_BF16 = 1
 DP_OUT_STORE = 0
 DP_OUT_ATOMIC_ADD = 1
+DP_ACT_NONE, DP_ACT_GELU, DP_ACT_GELU_TANH, DP_ACT_SILU = 0, 1, 2, 3
 
 c_int, c_i64, c_float, c_void_p = ctypes.c_int, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p
 
@@ -61,10 +62,52 @@ _SIGNATURES = {
     "dp_col2im": [c_int, c_void_p, c_void_p] + [c_int] * 11 + [c_void_p],
     "dp_conv_weight_flip": [c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p],
     "dp_dilate": [c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p],
+    # eltwise.cu
+    "dp_act_fwd": [c_int, c_int, c_void_p, c_void_p, c_i64, c_void_p],
+    "dp_act_bwd": [c_int, c_int, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_void_p],
+    "dp_geglu_fwd": [c_int, c_void_p, c_void_p, c_i64, c_int, c_void_p],
+    "dp_geglu_bwd": [c_int, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_void_p],
+    "dp_axpby": [c_int, c_void_p, c_void_p, c_void_p, c_i64, c_float, c_float, c_void_p],
+    "dp_gate_residual_fwd": [c_int, c_void_p, c_void_p, c_i64, c_void_p, c_void_p, c_i64, c_int,
+                             c_int, c_void_p],
+    "dp_gate_residual_bwd": [c_int, c_void_p, c_void_p, c_i64, c_void_p, c_void_p, c_void_p, c_i64,
+                             c_int, c_int, c_int, c_void_p],
+    "dp_q_sample": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i64,
+                    c_void_p],
+    "dp_pred_x0": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i64,
+                   c_void_p],
+    "dp_mse": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_float, c_void_p],
+    "dp_timestep_embed": [c_int, c_void_p, c_void_p, c_int, c_int, c_float, c_void_p],
+    "dp_embed": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_int, c_void_p],
+    "dp_concat": [c_int, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_int, c_void_p],
+    "dp_split": [c_int, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_int, c_int, c_int, c_void_p],
+    "dp_upsample2x": [c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p],
+    "dp_upsample2x_bwd": [c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p],
+    "dp_row_bias_fwd": [c_int, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_int, c_int, c_void_p],
+    "dp_row_bias_bwd": [c_int, c_void_p, c_void_p, c_i64, c_int, c_int, c_int, c_void_p],
+    "dp_space_to_depth": [c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p],
+    "dp_bias_grad": [c_int, c_void_p, c_void_p, c_i64, c_int, c_void_p],
+    "dp_cast": [c_int, c_int, c_void_p, c_void_p, c_i64, c_void_p],
+    "dp_adamw": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_float, c_float, c_float,
+                 c_float, c_float, c_int, c_float, c_void_p],
+    # norm.cu
+    "dp_group_norm_workspace": [c_int, c_int, c_int],
+    "dp_group_norm_fwd": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
+                          c_int, c_int, c_int, c_float, c_int, c_void_p, c_void_p],
+    "dp_group_norm_bwd": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                          c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
+                          c_void_p, c_void_p],
+    "dp_layer_norm_fwd": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_int, c_int,
+                          c_void_p, c_void_p, c_void_p, c_i64, c_int, c_float, c_void_p],
+    "dp_layer_norm_bwd": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_int, c_int,
+                          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i64,
+                          c_int, c_int, c_void_p],
+    "dp_softmax_fwd": [c_int, c_void_p, c_void_p, c_i64, c_int, c_int, c_float, c_int, c_int, c_void_p],
+    "dp_softmax_bwd": [c_int, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_int, c_float, c_void_p],
     "dp_last_error": [],
     "dp_version": [],
 }
-_RESTYPES = {"dp_last_error": ctypes.c_char_p}
+_RESTYPES = {"dp_last_error": ctypes.c_char_p, "dp_group_norm_workspace": ctypes.c_size_t}
 
 _lib = None
 

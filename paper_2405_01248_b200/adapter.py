@@ -1,0 +1,276 @@
+"""Plan adapter: the planner's outputs -> per-rank instruction programs.
+
+This is the executor-side half of the paper's "instruction generation" step
+(Fig. 6 step 6), which the reference leaves out.
+Input is exactly what the reference API returns (planner.evaluate_point,
+reference planner.py:141-187): the PartitionPlan, the simulated Schedule
+(scheduler.py:320-332) and the FillPlan (filler.py:245-276). Output, per
+group-local device:
+
+  ("fwd" | "fwd_sc" | "bwd", micro, stage)   compute tasks in simulated start order
+  ("fill", bubble_idx)                       frozen work of one bubble, placed after the
+                                             device's last compute task ending <= bubble.start
+  ("sync", stage)                            per-stage gradient allreduce + AdamW, right after
+                                             the stage's final backward (scheduler.py:202-207)
+  ("tail",)                                  leftover frozen work over all D devices
+  ("deliver",)                               frozen outputs -> stage-0 consumers (next iteration)
+
+plus the sample-range bookkeeping the reference only tracks as counts
+(filler.py:89,240): every frozen (component, layer) piece gets
+a concrete [lo, hi) range of the group batch on a concrete device, processed in
+ascending sample order, split contiguously and near-evenly over the bubble's
+sorted idle devices. From the pieces the adapter
+derives every frozen-activation transfer (src, dst, component, layer, range)
+in global production order, which both endpoints enumerate identically.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from .pipefill.scheduler import group_device_ranges
+
+EPS = 1e-12
+
+
+def split_range(lo, hi, parts):
+    """Contiguous near-even split of [lo, hi) into `parts` ranges (possibly empty)."""
+    n = hi - lo
+    return [(lo + (k * n) // parts, lo + ((k + 1) * n) // parts) for k in range(parts)]
+
+
+@dataclass(frozen=True)
+class Piece:
+    """Frozen work item: layer `layer` of frozen component `comp` over samples [lo, hi) on `device`."""
+
+    comp: int
+    layer: int
+    lo: int
+    hi: int
+    device: int
+    phase: int          # production order: index of the fill (bubble) or len(fills) for the tail
+
+
+@dataclass(frozen=True)
+class Transfer:
+    src: int
+    dst: int
+    comp: int
+    layer: int          # producer layer (its outputs move)
+    lo: int
+    hi: int
+    seq: int            # global production order
+
+
+@dataclass
+class DeviceProgram:
+    device: int
+    stage: int | None
+    replica: int | None
+    instrs: list = field(default_factory=list)
+
+
+@dataclass
+class GroupProgram:
+    """Everything one pipeline group (D devices) executes in one iteration."""
+
+    D: int
+    S: int
+    M: int
+    group_batch: int
+    micro_batch: int
+    stage_ranges: list          # stage -> (lo, hi) backbone layers
+    stage_devices: list         # stage -> (first, last+1) group-local devices
+    devices: list               # DeviceProgram per group-local device
+    fills: list                 # per bubble: list[Piece] in execution order
+    tail: list                  # list[Piece]
+    transfers: list             # list[Transfer] in production order
+    deliveries: list            # list[Transfer] (layer = last layer) final outputs -> stage 0
+    frozen_layers: list         # per frozen component: number of layers
+    selfcond: bool
+
+    def device_program(self, dev):
+        return self.devices[dev]
+
+    def micro_range(self, m):
+        return m * self.micro_batch, (m + 1) * self.micro_batch
+
+    def replica_range(self, stage, m, replica):
+        first, last = self.stage_devices[stage]
+        lo, hi = self.micro_range(m)
+        return split_range(lo, hi, last - first)[replica]
+
+    def stage_of(self, dev):
+        for s, (a, b) in enumerate(self.stage_devices):
+            if a <= dev < b:
+                return s, dev - a
+        raise ValueError(dev)
+
+
+def _stage_layout(plan):
+    stages = plan.stages_down
+    if plan.stages_up:
+        raise NotImplementedError("bidirectional (two-backbone) plans are not executed yet")
+    ranges = [tuple(st.layer_range) for st in stages]
+    return ranges, group_device_ranges(plan)
+
+
+def build_group_program(result, frozen_layer_counts, selfcond=None):
+    """Adapt one `evaluate_point` result (or an equivalent dict with plan/schedule/fill
+    built for the non-activated self-conditioning iterations) into a GroupProgram."""
+    plan = result["plan"]
+    schedule = result["pre_fill_schedule"]
+    fill = result["fill"]
+    cfg = plan.config
+    D, S, M, B = cfg.group_size, cfg.num_stages, cfg.num_microbatches, cfg.global_batch
+    stage_ranges, stage_devices = _stage_layout(plan)
+    sc = cfg.selfcond if selfcond is None else selfcond
+
+    devices = []
+    for dev in range(D):
+        stage = rep = None
+        for s, (a, b) in enumerate(stage_devices):
+            if a <= dev < b:
+                stage, rep = s, dev - a
+        devices.append(DeviceProgram(dev, stage, rep))
+
+    # ---- compute tasks per device, in the simulator's per-device order
+    compute = {dev: [] for dev in range(D)}
+    for t in schedule.tasks:  # sorted by (device, start, end, kind, micro)
+        if t.kind in ("fwd", "bwd", "fwd_sc"):
+            compute[t.device].append(t)
+    for dev in range(D):
+        compute[dev].sort(key=lambda t: (t.start, t.end, t.kind, t.micro_batch))
+
+    # ---- frozen pieces with concrete sample ranges (ascending per (comp, layer))
+    done = [[0] * n for n in frozen_layer_counts]
+    fills = []
+    for bi, f in enumerate(fill.fills):
+        pieces = []
+        if f.fill_time > 0:
+            idle = sorted(f.bubble.idle_devices)
+            work = []
+            for c in sorted(f.full_layers):
+                for layer in f.full_layers[c]:
+                    n = f.full_samples[(c, layer)]
+                    work.append((c, layer, n))
+            if f.partial is not None:
+                work.append((f.partial.component, f.partial.layer, f.partial.samples))
+            for c, layer, n in work:
+                lo = done[c][layer]
+                hi = lo + n
+                done[c][layer] = hi
+                for dev, (a, b) in zip(idle, split_range(lo, hi, len(idle))):
+                    if b > a:
+                        pieces.append(Piece(c, layer, a, b, dev, bi))
+        fills.append(pieces)
+    tail = []
+    tail_phase = len(fill.fills)
+    for tw in _topo_tail(fill.tail, frozen_layer_counts):
+        lo = done[tw.component][tw.layer]
+        hi = lo + tw.samples
+        done[tw.component][tw.layer] = hi
+        for dev, (a, b) in enumerate(split_range(lo, hi, D)):
+            if b > a:
+                tail.append(Piece(tw.component, tw.layer, a, b, dev, tail_phase))
+    for c, n in enumerate(frozen_layer_counts):
+        for layer in range(n):
+            if done[c][layer] != B:
+                raise RuntimeError(f"frozen component {c} layer {layer}: {done[c][layer]} of {B} samples "
+                                   "covered by the fill plan")
+
+    # ---- instruction placement
+    for dev in range(D):
+        prog = devices[dev]
+        items = []  # (sort_time, tiebreak, instr)
+        for t in compute[dev]:
+            items.append((t.start, 1, (t.kind, t.micro_batch, t.stage)))
+        for bi, f in enumerate(fill.fills):
+            if any(p.device == dev for p in fills[bi]):
+                # after every compute task ending <= bubble.start; before those starting >= it
+                items.append((f.bubble.start, 0, ("fill", bi)))
+        items.sort(key=lambda x: (x[0], x[1]))
+        instrs = [it[2] for it in items]
+        if prog.stage is not None:
+            last_bwd = max(i for i, ins in enumerate(instrs) if ins[0] == "bwd" and ins[2] == prog.stage)
+            instrs.insert(last_bwd + 1, ("sync", prog.stage))
+        if any(p.device == dev for p in tail):
+            instrs.append(("tail",))
+        instrs.append(("deliver",))
+        prog.instrs = instrs
+
+    transfers, deliveries = _data_plan(fills, tail, frozen_layer_counts, B, M, stage_devices)
+    return GroupProgram(D=D, S=S, M=M, group_batch=B, micro_batch=B // M, stage_ranges=stage_ranges,
+                        stage_devices=stage_devices, devices=devices, fills=fills, tail=tail,
+                        transfers=transfers, deliveries=deliveries,
+                        frozen_layers=list(frozen_layer_counts), selfcond=sc)
+
+
+def _topo_tail(tail, counts):
+    """Tail work in (component, layer) order; components are independent here (the configs
+    run have no frozen dependency edges), so index order is a valid topological order."""
+    return sorted(tail, key=lambda t: (t.component, t.layer))
+
+
+def _overlaps(pieces, lo, hi):
+    for p in pieces:
+        a, b = max(lo, p.lo), min(hi, p.hi)
+        if b > a:
+            yield p, a, b
+
+
+def _data_plan(fills, tail, counts, B, M, stage_devices):
+    """Frozen-activation transfers in production order, and final-output deliveries."""
+    produced = {}  # (comp, layer) -> list[Piece]
+    order = [p for ps in fills for p in ps] + list(tail)
+    transfers = []
+    seq = 0
+    for p in order:
+        if p.layer > 0:
+            for src, a, b in _overlaps(produced.get((p.comp, p.layer - 1), ()), p.lo, p.hi):
+                if src.device != p.device:
+                    transfers.append(Transfer(src.device, p.device, p.comp, p.layer - 1, a, b, seq))
+                    seq += 1
+        produced.setdefault((p.comp, p.layer), []).append(p)
+    # transfers are discovered in consumption order; re-sort by producer order so that both
+    # ends post them in the order the producer can send them
+    pos = {(p.comp, p.layer, p.lo, p.hi, p.device): i for i, p in enumerate(order)}
+
+    def prod_index(t):
+        for src, a, b in _overlaps(produced[(t.comp, t.layer)], t.lo, t.hi):
+            if src.device == t.src and a == t.lo and b == t.hi:
+                return pos[(src.comp, src.layer, src.lo, src.hi, src.device)]
+        raise AssertionError(t)
+
+    transfers.sort(key=lambda t: (prod_index(t), t.seq))
+    transfers = [Transfer(t.src, t.dst, t.comp, t.layer, t.lo, t.hi, i) for i, t in enumerate(transfers)]
+    deliveries = []
+    first, last = stage_devices[0]
+    r0 = last - first
+    mb = B // M
+    k = 0
+    for c, n in enumerate(counts):
+        final = produced.get((c, n - 1), [])
+        for m in range(M):
+            for rep, (lo, hi) in enumerate(split_range(m * mb, (m + 1) * mb, r0)):
+                for src, a, b in _overlaps(final, lo, hi):
+                    deliveries.append(Transfer(src.device, first + rep, c, n - 1, a, b, k))
+                    k += 1
+    return transfers, deliveries
+
+
+def backbone_transfers(prog: GroupProgram, stage, m):
+    """Live-set pieces crossing the cut stage -> stage+1 for micro-batch m:
+    [(src_replica, dst_replica, lo, hi)] (the reverse for gradients)."""
+    out = []
+    a0, a1 = prog.stage_devices[stage]
+    b0, b1 = prog.stage_devices[stage + 1]
+    lo, hi = prog.micro_range(m)
+    src = split_range(lo, hi, a1 - a0)
+    dst = split_range(lo, hi, b1 - b0)
+    for i, (sa, sb) in enumerate(src):
+        for j, (da, db) in enumerate(dst):
+            a, b = max(sa, da), min(sb, db)
+            if b > a:
+                out.append((i, j, a, b))
+    return out

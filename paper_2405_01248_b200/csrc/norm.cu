@@ -1,0 +1,691 @@
+// Normalisation kernels (K5/K6 in SURVEY §2.4) and the attention softmax.
+//
+// GroupNorm(+SiLU) over NHWC [N][HW][C] activations, G groups of C/G
+// contiguous channels. Forward = 2 launches:
+//   gn_partial   grid (chunks, N): each CTA streams a pixel range with 16-byte
+//                loads, keeps per-channel Welford (count, mean, M2) per thread,
+//                merges them (Chan) per channel then per group, and writes one
+//                partial per (n, chunk, g)  -> no atomics, deterministic
+//   gn_apply     merges the chunk partials of its sample in shared memory and
+//                normalises (+affine, +SiLU) its pixel range.
+// Backward = 2 launches with the same split (per-group sums of g*dy0 and
+// g*dy0*xhat, and per-channel dgamma/dbeta accumulated into fp32 buffers).
+//
+// LayerNorm over rows of C (one warp per row, two-pass in registers), with
+// either a per-channel affine or a per-sample adaLN modulation
+// y = xhat * (1 + scale[b]) + shift[b] (b = row / rows_per_sample).
+// Softmax over fp32 score rows (scale, optional causal mask) -> P in T, and its
+// backward dS = scale * P * (dP - rowsum(dP * P)).
+#include <string>
+#include "common.cuh"
+#include "dpipe.h"
+
+namespace dp {
+void set_error(const std::string& s);
+int ew_check(const char* what);
+
+template <typename T>
+struct NV {
+  static constexpr int V = 16 / sizeof(T);
+};
+
+template <typename T>
+DP_DEV void ld16(const T* p, float* f) {
+  uint4 u = *reinterpret_cast<const uint4*>(p);
+  if constexpr (sizeof(T) == 4) {
+    f[0] = __uint_as_float(u.x);
+    f[1] = __uint_as_float(u.y);
+    f[2] = __uint_as_float(u.z);
+    f[3] = __uint_as_float(u.w);
+  } else {
+    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = __bfloat162float(b[i]);
+  }
+}
+template <typename T>
+DP_DEV void st16(T* p, const float* f) {
+  uint4 u;
+  if constexpr (sizeof(T) == 4) {
+    u.x = __float_as_uint(f[0]);
+    u.y = __float_as_uint(f[1]);
+    u.z = __float_as_uint(f[2]);
+    u.w = __float_as_uint(f[3]);
+  } else {
+    u.x = pack_bf16x2(f[0], f[1]);
+    u.y = pack_bf16x2(f[2], f[3]);
+    u.z = pack_bf16x2(f[4], f[5]);
+    u.w = pack_bf16x2(f[6], f[7]);
+  }
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+struct Welford {
+  float n, mean, m2;
+};
+DP_DEV Welford wf_merge(Welford a, Welford b) {
+  const float n = a.n + b.n;
+  if (n == 0.f) return a;
+  const float d = b.mean - a.mean;
+  const float fb = b.n / n;
+  Welford r;
+  r.n = n;
+  r.mean = a.mean + d * fb;
+  r.m2 = a.m2 + b.m2 + d * d * a.n * fb;
+  return r;
+}
+
+constexpr int GN_THREADS = 256;
+constexpr int GN_MAX_C = 2560;
+
+// pixels [p0, p1) of sample n; thread layout: cv = tid % CV (channel vector), rl = tid / CV
+template <typename T>
+__global__ void __launch_bounds__(GN_THREADS) gn_partial_kernel(const T* __restrict__ x, int HW,
+                                                                int C, int G, int pix_per_chunk,
+                                                                float* __restrict__ part) {
+  constexpr int V = NV<T>::V;
+  const int CV = C / V;
+  const int n = blockIdx.y, chunk = blockIdx.x, nchunks = gridDim.x;
+  const int p0 = chunk * pix_per_chunk;
+  const int p1 = min(HW, p0 + pix_per_chunk);
+  __shared__ float s_n[GN_MAX_C], s_mean[GN_MAX_C], s_m2[GN_MAX_C];
+  for (int c = threadIdx.x; c < C; c += GN_THREADS) {
+    s_n[c] = 0.f;
+    s_mean[c] = 0.f;
+    s_m2[c] = 0.f;
+  }
+  __syncthreads();
+  const T* xs = x + (int64_t)n * HW * C;
+  // Threads loop over channel vectors in rounds so every vector gets covered even when CV > threads.
+  for (int cv0 = 0; cv0 < CV; cv0 += GN_THREADS) {
+    const int width = min(GN_THREADS, CV - cv0);
+    const int rows_par = GN_THREADS / width;
+    const int cv = cv0 + threadIdx.x % width;
+    const int rl = threadIdx.x / width;
+    if (rl < rows_par) {
+      float cnt = 0.f, mean[V], m2[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) mean[j] = m2[j] = 0.f;
+      for (int p = p0 + rl; p < p1; p += rows_par) {
+        float f[V];
+        ld16(xs + (int64_t)p * C + cv * V, f);
+        cnt += 1.f;
+        const float inv = 1.f / cnt;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          const float d = f[j] - mean[j];
+          mean[j] += d * inv;
+          m2[j] += d * (f[j] - mean[j]);
+        }
+      }
+      // merge rows_par lanes of the same channel through shared memory (serialised per lane row)
+      for (int r = 0; r < rows_par; ++r) {
+        if (rl == r && cnt > 0.f) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            const int c = cv * V + j;
+            Welford a{s_n[c], s_mean[c], s_m2[c]};
+            Welford b{cnt, mean[j], m2[j]};
+            a = wf_merge(a, b);
+            s_n[c] = a.n;
+            s_mean[c] = a.mean;
+            s_m2[c] = a.m2;
+          }
+        }
+        __syncthreads();
+      }
+    } else {
+      for (int r = 0; r < rows_par; ++r) __syncthreads();
+    }
+  }
+  __syncthreads();
+  const int cg = C / G;
+  for (int g = threadIdx.x; g < G; g += GN_THREADS) {
+    Welford a{0.f, 0.f, 0.f};
+    for (int c = g * cg; c < (g + 1) * cg; ++c) a = wf_merge(a, Welford{s_n[c], s_mean[c], s_m2[c]});
+    float* o = part + (((int64_t)n * nchunks + chunk) * G + g) * 3;
+    o[0] = a.n;
+    o[1] = a.mean;
+    o[2] = a.m2;
+  }
+}
+
+// merge the chunk partials of sample n into s_mean/s_rstd [G]
+DP_DEV void gn_merge_stats(const float* part, int n, int nchunks, int G, float eps, float* s_mean,
+                           float* s_rstd) {
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    Welford a{0.f, 0.f, 0.f};
+    for (int k = 0; k < nchunks; ++k) {
+      const float* q = part + (((int64_t)n * nchunks + k) * G + g) * 3;
+      a = wf_merge(a, Welford{q[0], q[1], q[2]});
+    }
+    s_mean[g] = a.mean;
+    s_rstd[g] = rsqrtf(a.m2 / fmaxf(a.n, 1.f) + eps);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(GN_THREADS)
+    gn_apply_kernel(const T* __restrict__ x, const float* __restrict__ gamma,
+                    const float* __restrict__ beta, T* __restrict__ y,
+                    float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                    const float* __restrict__ part, int HW, int C, int G, int pix_per_chunk,
+                    float eps, int silu_on) {
+  constexpr int V = NV<T>::V;
+  const int n = blockIdx.y, chunk = blockIdx.x, nchunks = gridDim.x;
+  __shared__ float s_mean[64 * 4], s_rstd[64 * 4];
+  gn_merge_stats(part, n, nchunks, G, eps, s_mean, s_rstd);
+  __syncthreads();
+  if (chunk == 0)
+    for (int g = threadIdx.x; g < G; g += GN_THREADS) {
+      mean_out[n * G + g] = s_mean[g];
+      rstd_out[n * G + g] = s_rstd[g];
+    }
+  const int cg = C / G;
+  const int CV = C / V;
+  const int p0 = chunk * pix_per_chunk;
+  const int p1 = min(HW, p0 + pix_per_chunk);
+  const int64_t base = (int64_t)n * HW * C;
+  const int64_t total = (int64_t)(p1 - p0) * CV;
+  for (int64_t i = threadIdx.x; i < total; i += GN_THREADS) {
+    const int64_t p = p0 + i / CV;
+    const int cv = static_cast<int>(i % CV);
+    float f[V];
+    ld16(x + base + p * C + cv * V, f);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int c = cv * V + j;
+      const int g = c / cg;
+      float v = (f[j] - s_mean[g]) * s_rstd[g];
+      if (gamma) v = v * gamma[c] + beta[c];
+      if (silu_on) v = v / (1.f + __expf(-v));
+      f[j] = v;
+    }
+    st16(y + base + p * C + cv * V, f);
+  }
+}
+
+// backward pass 1: per-channel sums of dy0*xhat and dy0 (-> dgamma, dbeta atomics) and
+// per-group partials A = sum gamma*dy0, B = sum gamma*dy0*xhat
+template <typename T>
+__global__ void __launch_bounds__(GN_THREADS)
+    gn_bwd_partial_kernel(const T* __restrict__ x, const T* __restrict__ dy,
+                          const float* __restrict__ gamma, const float* __restrict__ beta,
+                          const float* __restrict__ mean, const float* __restrict__ rstd, int HW,
+                          int C, int G, int pix_per_chunk, int silu_on, float* __restrict__ dgamma,
+                          float* __restrict__ dbeta, float* __restrict__ part) {
+  constexpr int V = NV<T>::V;
+  const int CV = C / V;
+  const int n = blockIdx.y, chunk = blockIdx.x, nchunks = gridDim.x;
+  const int p0 = chunk * pix_per_chunk;
+  const int p1 = min(HW, p0 + pix_per_chunk);
+  const int cg = C / G;
+  __shared__ float s_a[GN_MAX_C], s_b[GN_MAX_C];
+  for (int c = threadIdx.x; c < C; c += GN_THREADS) s_a[c] = s_b[c] = 0.f;
+  __syncthreads();
+  const int64_t base = (int64_t)n * HW * C;
+  for (int cv0 = 0; cv0 < CV; cv0 += GN_THREADS) {
+    const int width = min(GN_THREADS, CV - cv0);
+    const int rows_par = GN_THREADS / width;
+    const int cv = cv0 + threadIdx.x % width;
+    const int rl = threadIdx.x / width;
+    float sa[V], sb[V];  // sum dy0, sum dy0*xhat
+#pragma unroll
+    for (int j = 0; j < V; ++j) sa[j] = sb[j] = 0.f;
+    if (rl < rows_par) {
+      float mu[V], rs[V], ga[V], be[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const int c = cv * V + j;
+        mu[j] = mean[n * G + c / cg];
+        rs[j] = rstd[n * G + c / cg];
+        ga[j] = gamma ? gamma[c] : 1.f;
+        be[j] = gamma ? beta[c] : 0.f;
+      }
+      for (int p = p0 + rl; p < p1; p += rows_par) {
+        float fx[V], fd[V];
+        ld16(x + base + (int64_t)p * C + cv * V, fx);
+        ld16(dy + base + (int64_t)p * C + cv * V, fd);
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          const float xh = (fx[j] - mu[j]) * rs[j];
+          float d = fd[j];
+          if (silu_on) {
+            const float y0 = xh * ga[j] + be[j];
+            const float s = 1.f / (1.f + __expf(-y0));
+            d *= s * (1.f + y0 * (1.f - s));
+          }
+          sa[j] += d;
+          sb[j] += d * xh;
+        }
+      }
+    }
+    for (int r = 0; r < rows_par; ++r) {
+      if (rl == r) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          s_a[cv * V + j] += sa[j];
+          s_b[cv * V + j] += sb[j];
+        }
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  if (dgamma)
+    for (int c = threadIdx.x; c < C; c += GN_THREADS) {
+      atomicAdd(dgamma + c, s_b[c]);
+      atomicAdd(dbeta + c, s_a[c]);
+    }
+  for (int g = threadIdx.x; g < G; g += GN_THREADS) {
+    float A = 0.f, B = 0.f;
+    for (int c = g * cg; c < (g + 1) * cg; ++c) {
+      const float ga = gamma ? gamma[c] : 1.f;
+      A += ga * s_a[c];
+      B += ga * s_b[c];
+    }
+    float* o = part + (((int64_t)n * nchunks + chunk) * G + g) * 2;
+    o[0] = A;
+    o[1] = B;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(GN_THREADS)
+    gn_bwd_apply_kernel(const T* __restrict__ x, const T* __restrict__ dy,
+                        const float* __restrict__ gamma, const float* __restrict__ beta,
+                        const float* __restrict__ mean, const float* __restrict__ rstd,
+                        const float* __restrict__ part, int HW, int C, int G, int pix_per_chunk,
+                        int silu_on, T* __restrict__ dx, int accumulate) {
+  constexpr int V = NV<T>::V;
+  const int n = blockIdx.y, chunk = blockIdx.x, nchunks = gridDim.x;
+  const int cg = C / G;
+  __shared__ float s_A[256], s_B[256];
+  const float inv_m = 1.f / (static_cast<float>(HW) * cg);
+  for (int g = threadIdx.x; g < G; g += GN_THREADS) {
+    float A = 0.f, B = 0.f;
+    for (int k = 0; k < nchunks; ++k) {
+      const float* q = part + (((int64_t)n * nchunks + k) * G + g) * 2;
+      A += q[0];
+      B += q[1];
+    }
+    s_A[g] = A * inv_m;
+    s_B[g] = B * inv_m;
+  }
+  __syncthreads();
+  const int CV = C / V;
+  const int p0 = chunk * pix_per_chunk;
+  const int p1 = min(HW, p0 + pix_per_chunk);
+  const int64_t base = (int64_t)n * HW * C;
+  const int64_t total = (int64_t)(p1 - p0) * CV;
+  for (int64_t i = threadIdx.x; i < total; i += GN_THREADS) {
+    const int64_t p = p0 + i / CV;
+    const int cv = static_cast<int>(i % CV);
+    const int64_t off = base + p * C + cv * V;
+    float fx[V], fd[V], fo[V];
+    ld16(x + off, fx);
+    ld16(dy + off, fd);
+    if (accumulate) ld16(dx + off, fo);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int c = cv * V + j;
+      const int g = c / cg;
+      const float mu = mean[n * G + g], rs = rstd[n * G + g];
+      const float xh = (fx[j] - mu) * rs;
+      const float ga = gamma ? gamma[c] : 1.f;
+      float d = fd[j];
+      if (silu_on) {
+        const float y0 = xh * ga + (gamma ? beta[c] : 0.f);
+        const float s = 1.f / (1.f + __expf(-y0));
+        d *= s * (1.f + y0 * (1.f - s));
+      }
+      const float v = rs * (ga * d - s_A[g] - xh * s_B[g]);
+      fo[j] = accumulate ? fo[j] + v : v;
+    }
+    st16(dx + off, fo);
+  }
+}
+
+static void gn_split(int N, int HW, int& chunks, int& ppc) {
+  int target = (4 * kNumSMs + N - 1) / N;
+  if (target < 1) target = 1;
+  // keep >= 64 pixels per chunk so partials stay cheap
+  int maxc = (HW + 63) / 64;
+  chunks = target < maxc ? target : maxc;
+  if (chunks < 1) chunks = 1;
+  ppc = (HW + chunks - 1) / chunks;
+  chunks = (HW + ppc - 1) / ppc;
+}
+
+// ------------------------------------------------------------------ LayerNorm
+// one warp per row; per-lane strided elements (coalesced across the warp)
+template <typename T, int PER>
+__global__ void __launch_bounds__(256)
+    ln_fwd_kernel(const T* __restrict__ x, const float* __restrict__ gamma,
+                  const float* __restrict__ beta, const T* __restrict__ mod,
+                  int64_t mod_ld, int shift_off, int scale_off, int rps, T* __restrict__ y,
+                  float* __restrict__ mean_out, float* __restrict__ rstd_out, int64_t rows, int C,
+                  float eps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = blockIdx.x * 8LL + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const T* xr = x + row * C;
+  float v[PER];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int c = lane + 32 * k;
+    v[k] = c < C ? to_f(xr[c]) : 0.f;
+    s += v[k];
+  }
+  const float mu = warp_sum(s) / C;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int c = lane + 32 * k;
+    const float d = c < C ? v[k] - mu : 0.f;
+    q += d * d;
+  }
+  const float rs = rsqrtf(warp_sum(q) / C + eps);
+  if (lane == 0) {
+    mean_out[row] = mu;
+    rstd_out[row] = rs;
+  }
+  T* yr = y + row * C;
+  const T* mr = mod ? mod + (row / rps) * mod_ld : nullptr;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int c = lane + 32 * k;
+    if (c < C) {
+      float o = (v[k] - mu) * rs;
+      if (gamma) o = o * gamma[c] + beta[c];
+      if (mr) o = o * (1.f + to_f(mr[scale_off + c])) + to_f(mr[shift_off + c]);
+      yr[c] = from_f<T>(o);
+    }
+  }
+}
+
+template <typename T, int PER>
+__global__ void __launch_bounds__(256)
+    ln_bwd_kernel(const T* __restrict__ x, const T* __restrict__ dy,
+                  const float* __restrict__ gamma, const T* __restrict__ mod, int64_t mod_ld,
+                  int scale_off, int rps, const float* __restrict__ mean,
+                  const float* __restrict__ rstd, T* __restrict__ dx, int64_t rows, int C,
+                  int accumulate) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = blockIdx.x * 8LL + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const float mu = mean[row], rs = rstd[row];
+  const T* xr = x + row * C;
+  const T* dr = dy + row * C;
+  const T* mr = mod ? mod + (row / rps) * mod_ld : nullptr;
+  float xh[PER], g[PER];
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int c = lane + 32 * k;
+    if (c < C) {
+      xh[k] = (to_f(xr[c]) - mu) * rs;
+      float d = to_f(dr[c]);
+      if (gamma) d *= gamma[c];
+      if (mr) d *= 1.f + to_f(mr[scale_off + c]);
+      g[k] = d;
+    } else {
+      xh[k] = g[k] = 0.f;
+    }
+    s1 += g[k];
+    s2 += g[k] * xh[k];
+  }
+  s1 = warp_sum(s1) / C;
+  s2 = warp_sum(s2) / C;
+  T* xo = dx + row * C;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int c = lane + 32 * k;
+    if (c < C) {
+      float o = rs * (g[k] - s1 - xh[k] * s2);
+      if (accumulate) o += to_f(xo[c]);
+      xo[c] = from_f<T>(o);
+    }
+  }
+}
+
+// Parameter gradients of LayerNorm: grid (ceil(C/32), nseg). Segment = rows_per_seg rows.
+// affine: dgamma[c] += sum dy*xhat, dbeta[c] += sum dy (fp32 atomics)
+// mod:    dmod[b][scale_off+c] = sum_{rows of b} dy*gamma?*xhat_aff, dmod[b][shift_off+c] = sum dy
+//         (segment = sample b; stored, not accumulated)
+template <typename T>
+__global__ void __launch_bounds__(256)
+    ln_param_grad_kernel(const T* __restrict__ x, const T* __restrict__ dy,
+                         const float* __restrict__ mean, const float* __restrict__ rstd,
+                         int64_t rows, int C, int rows_per_seg, float* __restrict__ dgamma,
+                         float* __restrict__ dbeta, T* __restrict__ dmod, int64_t dmod_ld,
+                         int shift_off, int scale_off) {
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int ry = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_seg;
+  const int64_t r1 = min(rows, r0 + rows_per_seg);
+  float a = 0.f, b = 0.f;
+  if (c < C) {
+    for (int64_t r = r0 + ry; r < r1; r += 8) {
+      const float xh = (to_f(x[r * C + c]) - mean[r]) * rstd[r];
+      const float d = to_f(dy[r * C + c]);
+      a += d * xh;
+      b += d;
+    }
+  }
+  __shared__ float ra[8][33], rb[8][33];
+  ra[ry][threadIdx.x & 31] = a;
+  rb[ry][threadIdx.x & 31] = b;
+  __syncthreads();
+  if (ry == 0 && c < C) {
+    float sa = 0.f, sb = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      sa += ra[k][threadIdx.x];
+      sb += rb[k][threadIdx.x];
+    }
+    if (dmod) {
+      dmod[blockIdx.y * dmod_ld + scale_off + c] = from_f<T>(sa);
+      dmod[blockIdx.y * dmod_ld + shift_off + c] = from_f<T>(sb);
+    } else {
+      atomicAdd(dgamma + c, sa);
+      atomicAdd(dbeta + c, sb);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ softmax (attention)
+// P[r][j] = softmax_j(scale * S[r][j]) with causal mask j > (r % Lq) + causal_off when causal.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    softmax_fwd_kernel(const float* __restrict__ S, T* __restrict__ P, int64_t rows, int cols,
+                       int ld, float scale, int causal, int Lq) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = blockIdx.x * 8LL + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const float* sr = S + row * ld;
+  T* pr = P + row * ld;
+  const int lim = causal ? static_cast<int>(row % Lq) + 1 : cols;
+  float mx = -INFINITY;
+  for (int j = lane; j < lim; j += 32) mx = fmaxf(mx, sr[j] * scale);
+  mx = warp_max(mx);
+  float sum = 0.f;
+  for (int j = lane; j < lim; j += 32) sum += __expf(sr[j] * scale - mx);
+  sum = warp_sum(sum);
+  const float inv = 1.f / sum;
+  for (int j = lane; j < cols; j += 32) pr[j] = from_f<T>(j < lim ? __expf(sr[j] * scale - mx) * inv : 0.f);
+}
+
+// dS[r][j] = scale * P * (dP - sum_k dP*P)   (dP fp32 from the dO V^T GEMM)
+template <typename T>
+__global__ void __launch_bounds__(256)
+    softmax_bwd_kernel(const T* __restrict__ P, const float* __restrict__ dP, T* __restrict__ dS,
+                       int64_t rows, int cols, int ld, float scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = blockIdx.x * 8LL + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const T* pr = P + row * ld;
+  const float* dr = dP + row * ld;
+  float s = 0.f;
+  for (int j = lane; j < cols; j += 32) s += to_f(pr[j]) * dr[j];
+  s = warp_sum(s);
+  T* o = dS + row * ld;
+  for (int j = lane; j < cols; j += 32) o[j] = from_f<T>(scale * to_f(pr[j]) * (dr[j] - s));
+}
+
+}  // namespace dp
+
+using namespace dp;
+
+#define DISPATCH_T(dtype, ...)        \
+  do {                                \
+    if ((dtype) == DP_F32) {          \
+      using T = float;                \
+      __VA_ARGS__;                    \
+    } else {                          \
+      using T = __nv_bfloat16;        \
+      __VA_ARGS__;                    \
+    }                                 \
+  } while (0)
+
+#define ST reinterpret_cast<cudaStream_t>(stream)
+template <typename T>
+static const T* cp(const void* p) {
+  return reinterpret_cast<const T*>(p);
+}
+template <typename T>
+static T* mp(void* p) {
+  return reinterpret_cast<T*>(p);
+}
+
+static int gn_validate(int dtype, int C, int G) {
+  const int V = dtype == DP_F32 ? 4 : 8;
+  if (G <= 0 || C % G || C % V || C > GN_MAX_C || G > 256) {
+    set_error("group_norm: need C % G == 0, C % 8 == 0 (bf16) / 4 (fp32), C <= 2560, G <= 256");
+    return DP_ERR_ARGS;
+  }
+  return 0;
+}
+
+extern "C" {
+
+size_t dp_group_norm_workspace(int N, int HW, int G) {
+  int chunks, ppc;
+  gn_split(N, HW, chunks, ppc);
+  return sizeof(float) * 3 * (size_t)N * chunks * G;
+}
+
+int dp_group_norm_fwd(int dtype, const void* x, const float* gamma, const float* beta, void* y,
+                      float* mean, float* rstd, int N, int HW, int C, int G, float eps, int silu,
+                      float* workspace, dp_stream_t stream) {
+  if (N <= 0 || HW <= 0) return 0;
+  if (int e = gn_validate(dtype, C, G)) return e;
+  int chunks, ppc;
+  gn_split(N, HW, chunks, ppc);
+  dim3 grid(chunks, N);
+  DISPATCH_T(dtype, gn_partial_kernel<T><<<grid, GN_THREADS, 0, ST>>>(cp<T>(x), HW, C, G, ppc,
+                                                                        workspace));
+  DISPATCH_T(dtype, gn_apply_kernel<T><<<grid, GN_THREADS, 0, ST>>>(
+                        cp<T>(x), gamma, beta, mp<T>(y), mean, rstd, workspace, HW, C, G, ppc,
+                        eps, silu));
+  return ew_check("group_norm_fwd");
+}
+
+int dp_group_norm_bwd(int dtype, const void* x, const void* dy, const float* gamma,
+                      const float* beta, const float* mean, const float* rstd, void* dx,
+                      float* dgamma, float* dbeta, int N, int HW, int C, int G, int silu,
+                      int accumulate, float* workspace, dp_stream_t stream) {
+  if (N <= 0 || HW <= 0) return 0;
+  if (int e = gn_validate(dtype, C, G)) return e;
+  int chunks, ppc;
+  gn_split(N, HW, chunks, ppc);
+  dim3 grid(chunks, N);
+  DISPATCH_T(dtype, gn_bwd_partial_kernel<T><<<grid, GN_THREADS, 0, ST>>>(
+                        cp<T>(x), cp<T>(dy), gamma, beta, mean, rstd, HW, C, G, ppc, silu, dgamma,
+                        dbeta, workspace));
+  DISPATCH_T(dtype, gn_bwd_apply_kernel<T><<<grid, GN_THREADS, 0, ST>>>(
+                        cp<T>(x), cp<T>(dy), gamma, beta, mean, rstd, workspace, HW, C, G, ppc,
+                        silu, mp<T>(dx), accumulate));
+  return ew_check("group_norm_bwd");
+}
+
+#define LN_PER_DISPATCH(C, KERNEL, ...)                                               \
+  do {                                                                                \
+    if ((C) <= 256) {                                                                 \
+      KERNEL<T, 8><<<grid, 256, 0, ST>>>(__VA_ARGS__);                                \
+    } else if ((C) <= 512) {                                                          \
+      KERNEL<T, 16><<<grid, 256, 0, ST>>>(__VA_ARGS__);                               \
+    } else if ((C) <= 1024) {                                                         \
+      KERNEL<T, 32><<<grid, 256, 0, ST>>>(__VA_ARGS__);                               \
+    } else {                                                                          \
+      KERNEL<T, 64><<<grid, 256, 0, ST>>>(__VA_ARGS__);                               \
+    }                                                                                 \
+  } while (0)
+
+int dp_layer_norm_fwd(int dtype, const void* x, const float* gamma, const float* beta,
+                      const void* mod, int64_t mod_ld, int shift_off, int scale_off,
+                      int rows_per_sample, void* y, float* mean, float* rstd, int64_t rows, int C,
+                      float eps, dp_stream_t stream) {
+  if (rows <= 0) return 0;
+  if (C > 2048 || (gamma && mod)) {
+    set_error("layer_norm: C <= 2048 and affine/modulation are exclusive");
+    return DP_ERR_ARGS;
+  }
+  const dim3 grid(static_cast<unsigned>((rows + 7) / 8));
+  DISPATCH_T(dtype, LN_PER_DISPATCH(C, ln_fwd_kernel, cp<T>(x), gamma, beta, cp<T>(mod), mod_ld,
+                                    shift_off, scale_off, rows_per_sample > 0 ? rows_per_sample : 1,
+                                    mp<T>(y), mean, rstd, rows, C, eps));
+  return ew_check("layer_norm_fwd");
+}
+
+int dp_layer_norm_bwd(int dtype, const void* x, const void* dy, const float* gamma,
+                      const void* mod, int64_t mod_ld, int shift_off, int scale_off,
+                      int rows_per_sample, const float* mean, const float* rstd, void* dx,
+                      float* dgamma, float* dbeta, void* dmod, int64_t dmod_ld, int64_t rows,
+                      int C, int accumulate, dp_stream_t stream) {
+  if (rows <= 0) return 0;
+  if (C > 2048 || (gamma && mod)) {
+    set_error("layer_norm: C <= 2048 and affine/modulation are exclusive");
+    return DP_ERR_ARGS;
+  }
+  const int rps = rows_per_sample > 0 ? rows_per_sample : 1;
+  const dim3 grid(static_cast<unsigned>((rows + 7) / 8));
+  DISPATCH_T(dtype, LN_PER_DISPATCH(C, ln_bwd_kernel, cp<T>(x), cp<T>(dy), gamma, cp<T>(mod),
+                                    mod_ld, scale_off, rps, mean, rstd, mp<T>(dx), rows, C,
+                                    accumulate));
+  if (gamma && dgamma) {
+    const int seg = 256;
+    dim3 g2((C + 31) / 32, static_cast<unsigned>((rows + seg - 1) / seg));
+    DISPATCH_T(dtype, ln_param_grad_kernel<T><<<g2, 256, 0, ST>>>(
+                          cp<T>(x), cp<T>(dy), mean, rstd, rows, C, seg, dgamma, dbeta, nullptr, 0,
+                          0, 0));
+  }
+  if (mod && dmod) {
+    dim3 g2((C + 31) / 32, static_cast<unsigned>(rows / rps));
+    DISPATCH_T(dtype, ln_param_grad_kernel<T><<<g2, 256, 0, ST>>>(
+                          cp<T>(x), cp<T>(dy), mean, rstd, rows, C, rps, nullptr, nullptr,
+                          mp<T>(dmod), dmod_ld, shift_off, scale_off));
+  }
+  return ew_check("layer_norm_bwd");
+}
+
+int dp_softmax_fwd(int dtype, const float* S, void* P, int64_t rows, int cols, int ld,
+                   float scale, int causal, int Lq, dp_stream_t stream) {
+  if (rows <= 0) return 0;
+  const dim3 grid(static_cast<unsigned>((rows + 7) / 8));
+  DISPATCH_T(dtype, softmax_fwd_kernel<T><<<grid, 256, 0, ST>>>(S, mp<T>(P), rows, cols, ld, scale,
+                                                                  causal, Lq > 0 ? Lq : 1));
+  return ew_check("softmax_fwd");
+}
+
+int dp_softmax_bwd(int dtype, const void* P, const float* dP, void* dS, int64_t rows, int cols,
+                   int ld, float scale, dp_stream_t stream) {
+  if (rows <= 0) return 0;
+  const dim3 grid(static_cast<unsigned>((rows + 7) / 8));
+  DISPATCH_T(dtype, softmax_bwd_kernel<T><<<grid, 256, 0, ST>>>(cp<T>(P), dP, mp<T>(dS), rows,
+                                                                  cols, ld, scale));
+  return ew_check("softmax_bwd");
+}
+
+}  // extern "C"

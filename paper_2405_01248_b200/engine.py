@@ -1,0 +1,206 @@
+"""Public API of the executor: build a configuration's TrainModel, plan it with
+the reference planner API (pipefill.planner.evaluate_point, unchanged), adapt
+the plan into per-rank programs and run training iterations.
+
+    trainer = engine.Trainer.create("c1", world=1, rank=0, S=1, M=1, D=1)
+    loss = trainer.step()          # one pipelined training iteration (host batch -> loss)
+
+Configurations (BASELINE.json configs):
+  c1  tiny DiT (4 blocks, d=256) + tiny VAE encoder + tiny text encoder, 128 px, fp32,
+      self-conditioning p=0.5
+  c2  SD v2.1 U-Net + OpenCLIP ViT-H text (23 layers) + SD VAE encoder, 256 px, bf16
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass, replace
+
+import torch
+
+from . import ops as kops
+from .adapter import build_group_program
+from .diffusion import DataSpec, make_batch, noise_schedule
+from .networks import (CLIPTextEncoder, SDUNet, SDVAEEncoder, TinyDiT, TinyTextEncoder,
+                       TinyVAEEncoder)
+from .nn import grad_anchor
+from .pipefill import filler, planner, profile as pprof, scheduler
+from .profiler import probe_specs, synthetic_profile
+from .runtime import FrozenSpec, PipelineExecutor, TrainModel
+
+
+@dataclass(frozen=True)
+class ConfigSpec:
+    name: str
+    dtype: torch.dtype
+    image: int
+    latent: int
+    text_len: int
+    vocab: int
+    selfcond_p: float
+    config_id: int
+
+
+CONFIGS = {
+    "c1": ConfigSpec("c1", torch.float32, 128, 32, 16, 1000, 0.5, 1),
+    "c2": ConfigSpec("c2", torch.bfloat16, 256, 32, 77, 49408, 0.0, 2),
+}
+
+
+def _attach_grad_context(comp, device):
+    comp.grad_context = lambda: grad_anchor(True, device)
+    return comp
+
+
+def build_model(cfg: str | ConfigSpec, device="cuda", seed=0, states=None, small=False):
+    """Materialise the components of a configuration on `device` (deterministic init).
+    `states` optionally maps component name -> parameter dict (e.g. for parity tests)."""
+    c = CONFIGS[cfg] if isinstance(cfg, str) else cfg
+    states = states or {}
+    if c.name == "c1":
+        bb = TinyDiT(c.dtype, img=c.latent, cin=8, cout=4)
+        vae = TinyVAEEncoder(c.dtype)
+        txt = TinyTextEncoder(c.dtype)
+        sc_ch = 4
+    elif c.name == "c2":
+        bb = SDUNet(c.dtype)
+        vae = SDVAEEncoder(c.dtype)
+        txt = CLIPTextEncoder(c.dtype, layers=2 if small else 23)
+        sc_ch = 0
+    else:
+        raise KeyError(c.name)
+    for comp in (bb, vae, txt):
+        comp.materialize(device, seed, states.get(comp.name))
+    _attach_grad_context(bb, device)
+    sab, s1m = noise_schedule()
+    model = TrainModel(bb, [FrozenSpec(vae, ("images",)), FrozenSpec(txt, ("ids",))], kops,
+                       sab.to(device), s1m.to(device), selfcond_channels=sc_ch,
+                       adamw=dict(lr=1e-4, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01))
+    model.selfcond_p = c.selfcond_p
+    model.cfg = c
+    return model
+
+
+class InputFeed:
+    """Batch fields for one iteration. mode 'device': the whole world batch is resident on
+    the device (bench `value`); mode 'host': slices are copied from pinned host memory
+    when used (bench `e2e`), and the copied bytes are counted."""
+
+    def __init__(self, batch, device, dtype, mode="device"):
+        self.device = torch.device(device)
+        self.dtype = dtype
+        self.mode = mode
+        self.h2d_bytes = 0
+        fields = dict(images=batch.images, ids=batch.ids, t=batch.t, noise=batch.noise)
+        if mode == "device":
+            self.f = {k: self._cast(k, v.to(self.device, non_blocking=True)) for k, v in fields.items()}
+        else:
+            self.f = {k: (v.pin_memory() if self.device.type == "cuda" else v) for k, v in fields.items()}
+        self.selfcond = batch.selfcond
+
+    def _cast(self, k, v):
+        if k in ("images", "noise") and v.dtype != self.dtype:
+            return v.to(self.dtype)
+        return v
+
+    def get(self, k, lo, hi):
+        v = self.f[k][lo:hi]
+        if self.mode == "host":
+            v = v.to(self.device, non_blocking=True)
+            self.h2d_bytes += v.numel() * v.element_size()
+            v = self._cast(k, v)
+        return v
+
+    def t(self, lo, hi):
+        return self.get("t", lo, hi)
+
+    def noise(self, lo, hi):
+        return self.get("noise", lo, hi)
+
+
+def plan_programs(prof, world, S, M, D, world_batch, frozen_counts, bubble_min_len=0.010,
+                  cluster_comm=None):
+    """Reference planner calls -> {selfcond: GroupProgram} plus the warm-up program."""
+    comm = cluster_comm or pprof.CommCosts(2.0e11, 2e-5, 3.0e11, 1e-5)
+    cluster = pprof.ClusterConfig(world, comm)
+    res = planner.evaluate_point(prof, cluster, S, M, D, world_batch, bubble_min_len=bubble_min_len)
+    plan = res["plan"]
+    group_batch = plan.config.global_batch
+    programs = {}
+    if res["mode"] == planner.MODE_SELFCOND:
+        programs[True] = build_group_program(res, frozen_counts, selfcond=True)
+        pre = scheduler.build_schedule(plan, prof, cluster, selfcond=False)
+        fill = filler.fill_all(scheduler.extract_bubbles(pre, bubble_min_len), prof, group_batch, pre)
+        programs[False] = build_group_program(dict(plan=plan, pre_fill_schedule=pre, fill=fill),
+                                              frozen_counts, selfcond=False)
+    else:
+        programs[False] = build_group_program(res, frozen_counts, selfcond=False)
+        programs[True] = programs[False]
+    pre = res["pre_fill_schedule"]
+    warm = filler.fill_all([], prof, group_batch, pre)
+    warm_prog = build_group_program(dict(plan=plan, pre_fill_schedule=pre, fill=warm), frozen_counts,
+                                    selfcond=False)
+    unfilled = build_group_program(dict(plan=plan, pre_fill_schedule=pre, fill=warm), frozen_counts,
+                                   selfcond=False)
+    return res, programs, warm_prog, unfilled
+
+
+class Trainer:
+    """One rank of a pipelined training job."""
+
+    def __init__(self, model, cfg, executor, data_spec, device, feed_mode="device"):
+        self.model, self.cfg, self.ex, self.data_spec = model, cfg, executor, data_spec
+        self.device = device
+        self.it = 0
+        self.feed_mode = feed_mode
+        self._next = None
+
+    @classmethod
+    def create(cls, cfg="c1", *, world=1, rank=0, S=1, M=1, D=1, world_batch=None, device=None,
+               seed=0, states=None, profile=None, filled=True, feed_mode="device", small=False,
+               bubble_min_len=0.010):
+        c = CONFIGS[cfg] if isinstance(cfg, str) else cfg
+        device = device or (f"cuda:{torch.cuda.current_device()}" if torch.cuda.is_available() else "cpu")
+        model = build_model(c, device, seed, states, small=small)
+        world_batch = world_batch or 8 * world
+        ds = DataSpec(c.config_id, world_batch, c.image, c.latent, 4, c.text_len, c.vocab, 1000,
+                      c.selfcond_p)
+        probe = make_batch(replace(ds, world_batch=1), 10 ** 6)
+        pfeed = InputFeed(probe, device, c.dtype)
+        live, fspecs = probe_specs(model, lambda k: pfeed.get(k, 0, 1), device)
+        counts = [len(f.component.layers) for f in model.frozen]
+        if profile is None:
+            profile = synthetic_profile(model, live, fspecs, group_batch=world_batch * D // world, D=D, M=M)
+        res, programs, warm, unfilled = plan_programs(profile, world, S, M, D, world_batch, counts,
+                                                      bubble_min_len)
+        if not filled:
+            programs = {False: unfilled, True: unfilled}
+        elems = c.latent * c.latent * 4
+        ex = PipelineExecutor(model, programs, rank=rank, world=world, device=device, live_specs=live,
+                              frozen_specs=fspecs, loss_scale=1.0 / (world_batch * elems))
+        ex.warm_program = warm
+        ex.plan_result = res
+        t = cls(model, c, ex, ds, device, feed_mode)
+        t.profile = profile
+        return t
+
+    def _feed(self, i):
+        return InputFeed(make_batch(self.data_spec, i), self.device, self.cfg.dtype, self.feed_mode)
+
+    def warmup_frozen(self):
+        self._cur = self._feed(self.it)
+        self.ex.warmup(lambda f, lo, hi: self._cur.get(f, self.ex.gb_of() + lo, self.ex.gb_of() + hi))
+
+    def step(self, has_next=True):
+        """One iteration: train on batch `it` (frozen outputs ready), fill batch it+1."""
+        if self.it == 0 and not self.ex.frozen_ready:
+            self.warmup_frozen()
+        cur = self._cur
+        nxt = self._feed(self.it + 1) if has_next else None
+        self.ex.inputs = cur
+        gb = self.ex.gb_of()
+        raw = (lambda f, lo, hi: nxt.get(f, gb + lo, gb + hi)) if nxt is not None else None
+        loss = self.ex.run_iteration(raw, cur.selfcond, has_next=has_next)
+        self._cur = nxt
+        self.it += 1
+        return loss

@@ -1,0 +1,661 @@
+"""Layer library of the executor: flat parameter stores and autograd Functions
+whose forward/backward run only libdpipe kernels (ops.py).
+
+Design (B200-first, not a port):
+* Every trainable stage owns ONE flat fp32 master buffer, one flat fp32 grad
+  buffer and the AdamW moments; the compute copy (bf16 for the SD configs,
+  the master itself for fp32) is a second flat buffer. Weight gradients are
+  accumulated by the wgrad GEMM epilogue straight into the fp32 grad views,
+  so gradient allreduce and AdamW are single flat launches per stage.
+* Weights are therefore not torch leaves; each Function receives its layer
+  and writes `param.g` itself. A per-stage "grad anchor" (a 1-element tensor
+  with requires_grad) is threaded into every parameterised Function so that
+  torch's autograd engine records branches whose activations carry no grad
+  (time embedding from t, cross-attention K/V from the frozen context).
+* Activations: NHWC for convolutions, [B, L, C] rows for transformers (the
+  NHWC tensor viewed as [B, H*W, C] — no permutes on the hot path).
+
+Reference semantics: the paper trains diffusion backbones with frozen
+encoders; layer shapes follow SD v2.1 / DiT.
+"""
+
+from __future__ import annotations
+
+import math
+import threading
+import zlib
+
+import torch
+
+from . import ops
+from ._lib import DP_ACT_GELU, DP_ACT_GELU_TANH, DP_ACT_SILU
+
+_ALIGN = 64  # elements; keeps every view 128-byte aligned for TMA
+
+
+# ============================================================================ parameters
+
+class Param:
+    __slots__ = ("name", "shape", "fp32", "init", "offset", "numel", "w", "g", "master")
+
+    def __init__(self, name, shape, fp32, init):
+        self.name = name
+        self.shape = tuple(shape)
+        self.fp32 = fp32
+        self.init = init
+        self.numel = math.prod(self.shape)
+        self.offset = None
+        self.w = None       # compute view (bf16 weights, or fp32)
+        self.g = None       # fp32 grad view (None when frozen)
+        self.master = None  # fp32 master view
+
+
+class ParamStore:
+    """Flat parameter storage for one stage (trainable) or one frozen component."""
+
+    def __init__(self, dtype=torch.float32, trainable=True):
+        self.dtype = dtype
+        self.trainable = trainable
+        self.params: dict[str, Param] = {}
+        self.master = self.grad = self.compute = self.exp_avg = self.exp_avg_sq = None
+        self.step = 0
+
+    def add(self, name, shape, fp32=False, init="w"):
+        if name in self.params:
+            raise KeyError(f"duplicate parameter {name}")
+        p = Param(name, shape, fp32 or self.dtype == torch.float32, init)
+        self.params[name] = p
+        return p
+
+    def numel(self):
+        return sum(p.numel for p in self.params.values())
+
+    def materialize(self, device, seed=0, state=None, order_key=None):
+        """Allocate the flat buffers and fill them: from `state` (name -> fp32 tensor) when
+        given, else from the deterministic initialiser (same values the CPU oracle uses).
+        `order_key(param)` orders the flat layout (stable), e.g. by owning layer."""
+        off = 0
+        plist = list(self.params.values())
+        if order_key is not None:
+            plist = sorted(plist, key=order_key)
+        for p in plist:
+            p.offset = off
+            off += -(-p.numel // _ALIGN) * _ALIGN
+        total = max(off, _ALIGN)
+        self.master = torch.zeros(total, device=device, dtype=torch.float32)
+        if self.dtype != torch.float32:
+            self.compute = torch.zeros(total, device=device, dtype=self.dtype)
+        else:
+            self.compute = self.master
+        if self.trainable:
+            self.grad = torch.zeros(total, device=device, dtype=torch.float32)
+            self.exp_avg = torch.zeros(total, device=device, dtype=torch.float32)
+            self.exp_avg_sq = torch.zeros(total, device=device, dtype=torch.float32)
+        init = state if state is not None else init_state(self.param_specs(), seed)
+        for p in self.params.values():
+            sl = slice(p.offset, p.offset + p.numel)
+            p.master = self.master[sl].view(p.shape)
+            p.master.copy_(init[p.name].reshape(p.shape))
+            p.w = p.master if p.fp32 else self.compute[sl].view(p.shape)
+            p.g = self.grad[sl].view(p.shape) if self.trainable else None
+        if self.compute is not self.master:
+            ops.cast(self.master, self.dtype, out=self.compute)
+        return self
+
+    def param_specs(self):
+        return [(p.name, p.shape, p.init) for p in self.params.values()]
+
+    def state_dict(self):
+        return {p.name: p.master.detach().float().cpu().clone() for p in self.params.values()}
+
+    def grads(self):
+        return {p.name: p.g.detach().float().cpu().clone() for p in self.params.values()}
+
+    def zero_grad(self, rng=None):
+        if self.grad is not None:
+            lo, hi = rng if rng is not None else (0, self.grad.numel())
+            self.grad[lo:hi].zero_()
+
+    def adamw_step(self, lr=1e-4, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01, grad_scale=1.0,
+                   rng=None):
+        """One AdamW step over the flat slice `rng` (default: everything)."""
+        self.step += 1
+        lo, hi = rng if rng is not None else (0, self.master.numel())
+        if hi <= lo:
+            return
+        ops.adamw(self.master[lo:hi], self.grad[lo:hi], self.exp_avg[lo:hi], self.exp_avg_sq[lo:hi],
+                  None if self.compute is self.master else self.compute[lo:hi],
+                  lr, betas[0], betas[1], eps, weight_decay, self.step, grad_scale)
+
+
+def _name_seed(name: str, seed: int) -> int:
+    return (zlib.crc32(name.encode()) * 1000003 + seed) & 0x7FFFFFFF
+
+
+def init_state(specs, seed=0):
+    """Deterministic CPU initialiser shared by the executor and the CPU oracle.
+
+    w: N(0, 1/fan_in); b: 0.02 N(0,1); g (norm scale): 1 + 0.02 N(0,1); e (embedding): 0.02 N(0,1).
+    Zero-initialised layers of the original recipes (adaLN-Zero, zero convs) get the small
+    random init too so that their gradients are non-trivial in parity tests.
+    """
+    out = {}
+    for name, shape, kind in specs:
+        g = torch.Generator().manual_seed(_name_seed(name, seed))
+        t = torch.randn(*shape, generator=g, dtype=torch.float32)
+        if kind == "w":
+            fan_in = math.prod(shape[1:]) if len(shape) > 1 else shape[0]
+            t = t / math.sqrt(fan_in)
+        elif kind == "b":
+            t = t * 0.02
+        elif kind == "g":
+            t = 1.0 + 0.02 * t
+        elif kind == "e":
+            t = t * 0.02
+        elif kind == "z":
+            t = t * 1e-3
+        out[name] = t
+    return out
+
+
+# ============================================================================ grad anchor
+
+_tls = threading.local()
+
+
+def current_anchor():
+    return getattr(_tls, "anchor", None)
+
+
+class grad_anchor:
+    """Context manager installing the per-stage grad anchor (see module doc)."""
+
+    def __init__(self, enabled=True, device="cuda"):
+        self.enabled = enabled
+        self.device = device
+
+    def __enter__(self):
+        self.prev = current_anchor()
+        _tls.anchor = (torch.zeros(1, device=self.device, requires_grad=True)
+                       if self.enabled else None)
+        return _tls.anchor
+
+    def __exit__(self, *exc):
+        _tls.anchor = self.prev
+        return False
+
+
+def _c(t):
+    return t if t.is_contiguous() else t.contiguous()
+
+
+# ============================================================================ Functions
+
+class _LinearFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, anchor, residual, layer):
+        K = x.shape[-1]
+        x2 = _c(x).view(-1, K)
+        W = layer.weight
+        N = W.shape[0]
+        out = torch.empty(*x.shape[:-1], N, device=x.device, dtype=x.dtype)
+        ops.linear(x2, W.w, bias=None if layer.bias is None else layer.bias.w,
+                   residual=None if residual is None else _c(residual).view(-1, N),
+                   out=out.view(-1, N))
+        ctx.save_for_backward(x2)
+        ctx.layer = layer
+        ctx.has_res = residual is not None
+        return out
+
+    @staticmethod
+    def backward(ctx, dy):
+        (x2,) = ctx.saved_tensors
+        layer = ctx.layer
+        W = layer.weight
+        N = W.shape[0]
+        dy2 = _c(dy).view(-1, N)
+        dx = None
+        if ctx.needs_input_grad[0]:
+            dx = ops.linear_dgrad(dy2, W.w).view(*dy.shape[:-1], W.shape[1])
+        if W.g is not None:
+            ops.linear_wgrad(dy2, x2, W.g)
+        if layer.bias is not None and layer.bias.g is not None:
+            ops.bias_grad(dy2, layer.bias.g)
+        return dx, None, (dy if ctx.has_res else None), None
+
+
+class _ConvFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, anchor, residual, layer):
+        x = _c(x)
+        y = ops.conv2d(x, layer.weight.w, stride=layer.stride, pad=layer.pad, out_hw=layer.out_hw(x),
+                       bias=None if layer.bias is None else layer.bias.w,
+                       residual=None if residual is None else _c(residual))
+        ctx.save_for_backward(x)
+        ctx.layer = layer
+        ctx.has_res = residual is not None
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        (x,) = ctx.saved_tensors
+        layer = ctx.layer
+        dy = _c(dy)
+        dx = None
+        if ctx.needs_input_grad[0]:
+            dx = ops.conv2d_dgrad(dy, layer.weight.w, x.shape, stride=layer.stride, pad=layer.pad)
+        if layer.weight.g is not None:
+            ops.conv2d_wgrad(dy, x, layer.weight.g, stride=layer.stride, pad=layer.pad)
+        if layer.bias is not None and layer.bias.g is not None:
+            ops.bias_grad(dy, layer.bias.g)
+        return dx, None, (dy if ctx.has_res else None), None
+
+
+class _GroupNormFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, anchor, layer):
+        x = _c(x)
+        y, mean, rstd = ops.group_norm(x, layer.gamma.w, layer.beta.w, layer.groups, layer.eps, layer.silu)
+        ctx.save_for_backward(x, mean, rstd)
+        ctx.layer = layer
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, mean, rstd = ctx.saved_tensors
+        L = ctx.layer
+        dx = ops.group_norm_bwd(x, _c(dy), L.gamma.w, L.beta.w, mean, rstd, L.groups, L.silu,
+                                dgamma=L.gamma.g, dbeta=L.beta.g)
+        return dx, None, None
+
+
+class _LayerNormFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, anchor, layer):
+        x = _c(x)
+        g = None if layer.gamma is None else layer.gamma.w
+        b = None if layer.beta is None else layer.beta.w
+        y, mean, rstd = ops.layer_norm(x, g, b, layer.eps)
+        ctx.save_for_backward(x, mean, rstd)
+        ctx.layer = layer
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, mean, rstd = ctx.saved_tensors
+        L = ctx.layer
+        dx = ops.layer_norm_bwd(x, _c(dy), None if L.gamma is None else L.gamma.w, mean, rstd,
+                                dgamma=None if L.gamma is None else L.gamma.g,
+                                dbeta=None if L.beta is None else L.beta.g)
+        return dx, None, None
+
+
+class _LayerNormModFn(torch.autograd.Function):
+    """adaLN: y = LN(x) * (1 + mod[b, scale_off:+C]) + mod[b, shift_off:+C]."""
+
+    @staticmethod
+    def forward(ctx, x, mod, shift_off, scale_off, eps):
+        x = _c(x)
+        B = mod.shape[0]
+        rps = x.numel() // x.shape[-1] // B
+        y, mean, rstd = ops.layer_norm(x, None, None, eps, mod=mod, mod_ld=mod.stride(0),
+                                       shift_off=shift_off, scale_off=scale_off, rows_per_sample=rps)
+        ctx.save_for_backward(x, mod, mean, rstd)
+        ctx.meta = (shift_off, scale_off, rps)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, mod, mean, rstd = ctx.saved_tensors
+        shift_off, scale_off, rps = ctx.meta
+        dmod = torch.zeros_like(mod)
+        dx = ops.layer_norm_bwd(x, _c(dy), None, mean, rstd, mod=mod, mod_ld=mod.stride(0),
+                                shift_off=shift_off, scale_off=scale_off, rows_per_sample=rps,
+                                dmod=dmod, dmod_ld=dmod.stride(0))
+        return dx, dmod, None, None, None
+
+
+class _GateResidualFn(torch.autograd.Function):
+    """y = x + mod[b, off:off+C] * h   (adaLN-Zero gate)."""
+
+    @staticmethod
+    def forward(ctx, x, mod, off, h):
+        x, h = _c(x), _c(h)
+        B = mod.shape[0]
+        rps = x.numel() // x.shape[-1] // B
+        g = mod[:, off:]
+        y = ops.gate_residual(x, g, mod.stride(0), h, rps)
+        ctx.save_for_backward(mod, h)
+        ctx.meta = (off, rps)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        mod, h = ctx.saved_tensors
+        off, rps = ctx.meta
+        dy = _c(dy)
+        dmod = torch.zeros_like(mod)
+        dh = ops.gate_residual_bwd(dy, mod[:, off:], mod.stride(0), h, dmod[:, off:], dmod.stride(0),
+                                   mod.shape[0], rps)
+        return dy, dmod, None, dh
+
+
+class _ActFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, op):
+        x = _c(x)
+        ctx.save_for_backward(x)
+        ctx.op = op
+        return ops.act(x, op)
+
+    @staticmethod
+    def backward(ctx, dy):
+        (x,) = ctx.saved_tensors
+        return ops.act_bwd(x, _c(dy), ctx.op), None
+
+
+class _GegluFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x):
+        x = _c(x)
+        ctx.save_for_backward(x)
+        return ops.geglu(x)
+
+    @staticmethod
+    def backward(ctx, dy):
+        (x,) = ctx.saved_tensors
+        return ops.geglu_bwd(x, _c(dy))
+
+
+class _AddFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, a, b):
+        return ops.axpby(_c(a), _c(b))
+
+    @staticmethod
+    def backward(ctx, dy):
+        return dy, dy
+
+
+class _RowBiasFn(torch.autograd.Function):
+    """y = x + e[b] broadcast over the pixels/tokens of sample b."""
+
+    @staticmethod
+    def forward(ctx, x, e):
+        x = _c(x)
+        B = e.shape[0]
+        rps = x.numel() // x.shape[-1] // B
+        ctx.meta = (B, rps)
+        return ops.row_bias(x, e, rps)
+
+    @staticmethod
+    def backward(ctx, dy):
+        B, rps = ctx.meta
+        dy = _c(dy)
+        return dy, ops.row_bias_bwd(dy, B, rps)
+
+
+class _ConcatFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, a, b):
+        ctx.Ca = a.shape[-1]
+        return ops.concat_last(_c(a), _c(b))
+
+    @staticmethod
+    def backward(ctx, dy):
+        dy = _c(dy)
+        Ca = ctx.Ca
+        da = torch.empty(*dy.shape[:-1], Ca, device=dy.device, dtype=dy.dtype)
+        db = torch.empty(*dy.shape[:-1], dy.shape[-1] - Ca, device=dy.device, dtype=dy.dtype)
+        ops.split_last(dy, Ca, da, db)
+        return da, db
+
+
+class _AddConstFn(torch.autograd.Function):
+    """y[b] = x[b] + const (const broadcast over the batch; e.g. fixed 2-D sin-cos positions)."""
+
+    @staticmethod
+    def forward(ctx, x, const):
+        x = _c(x)
+        B = x.shape[0]
+        flat = x.view(B, -1)
+        y = ops.row_bias(flat, const.view(1, -1).expand(1, flat.shape[1]), B)
+        return y.view(x.shape)
+
+    @staticmethod
+    def backward(ctx, dy):
+        return dy, None
+
+
+class _SpaceToDepthFn(torch.autograd.Function):
+    """NHWC [B,H,W,C] <-> [B,H/p,W/p,p*p*C] with patch channel order (i, j, c)."""
+
+    @staticmethod
+    def forward(ctx, x, p, inverse):
+        ctx.meta = (p, inverse)
+        return ops.space_to_depth(_c(x), p, inverse)
+
+    @staticmethod
+    def backward(ctx, dy):
+        p, inverse = ctx.meta
+        return ops.space_to_depth(_c(dy), p, not inverse), None, None
+
+
+class _Upsample2xFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x):
+        return ops.upsample2x(_c(x))
+
+    @staticmethod
+    def backward(ctx, dy):
+        return ops.upsample2x_bwd(_c(dy))
+
+
+class _AttentionFn(torch.autograd.Function):
+    """Multi-head attention composed of batched tensor-core GEMMs and the softmax kernel.
+
+    self-attention: q_t is a fused [B, N, 3C] qkv tensor and kv_t is None;
+    cross-attention: q_t is [B, N, C], kv_t a fused [B, Nk, 2C] tensor.
+    Scores/probabilities live in [B, h, N, ld] buffers with ld = Nk rounded up to 8
+    (TMA row-stride alignment; the padding columns are never read).
+    """
+
+    @staticmethod
+    def forward(ctx, q_t, kv_t, heads, causal):
+        q_t = _c(q_t)
+        kv_t = None if kv_t is None else _c(kv_t)
+        B, N = q_t.shape[0], q_t.shape[1]
+        if kv_t is None:
+            C = q_t.shape[2] // 3
+            src_k, Nk, k_off, v_off, kv_ld = q_t, N, C, 2 * C, 3 * C
+            q_ld = 3 * C
+        else:
+            C = q_t.shape[2]
+            src_k, Nk, k_off, v_off, kv_ld = kv_t, kv_t.shape[1], 0, C, 2 * C
+            q_ld = C
+        hd = C // heads
+        scale = 1.0 / math.sqrt(hd)
+        ld = -(-Nk // 8) * 8
+        dev, dt = q_t.device, q_t.dtype
+        S = torch.empty(B, heads, N, ld, device=dev, dtype=torch.float32)
+        P = torch.empty(B, heads, N, ld, device=dev, dtype=dt)
+        o = torch.empty(B, N, C, device=dev, dtype=dt)
+        qp = q_t  # q at offset 0 in both layouts
+        kp = src_k.view(-1)[k_off:]
+        vp = src_k.view(-1)[v_off:]
+        # S[b,h] = Q_bh K_bh^T (unscaled; the softmax applies `scale`)
+        ops.gemm(qp, kp, S, M=N, N=Nk, K=hd, a_ld=q_ld, b_ld=kv_ld, d_ld=ld, batch=(heads, B),
+                 a_bs=(hd, N * q_ld), b_bs=(hd, Nk * kv_ld), d_bs=(N * ld, heads * N * ld))
+        ops.softmax(S, P, scale, Nk, causal=causal, Lq=N)
+        # O[b, :, h*hd:] = P_bh V_bh   (V MN-major)
+        ops.gemm(P, vp, o, M=N, N=hd, K=Nk, a_ld=ld, b_ld=kv_ld, b_mn=True, d_ld=C, batch=(heads, B),
+                 a_bs=(N * ld, heads * N * ld), b_bs=(hd, Nk * kv_ld), d_bs=(hd, N * C))
+        ctx.save_for_backward(q_t, src_k if kv_t is not None else q_t, P)
+        ctx.meta = (kv_t is None, heads, B, N, Nk, C, hd, ld, q_ld, kv_ld, k_off, v_off, scale)
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q_t, src_k, P = ctx.saved_tensors
+        self_attn, heads, B, N, Nk, C, hd, ld, q_ld, kv_ld, k_off, v_off, scale = ctx.meta
+        do = _c(do)
+        dev, dt = do.device, do.dtype
+        dq_t = torch.empty_like(q_t)
+        dkv_t = dq_t if self_attn else torch.empty_like(src_k)
+        kp = src_k.view(-1)[k_off:]
+        vp = src_k.view(-1)[v_off:]
+        dkp = dkv_t.view(-1)[k_off:]
+        dvp = dkv_t.view(-1)[v_off:]
+        # dV = P^T dO : M=Nk, N=hd, K=N
+        ops.gemm(P, do, dvp, M=Nk, N=hd, K=N, a_ld=ld, a_mn=True, b_ld=C, b_mn=True, d_ld=kv_ld,
+                 batch=(heads, B), a_bs=(N * ld, heads * N * ld), b_bs=(hd, N * C), d_bs=(hd, Nk * kv_ld))
+        # dP = dO V^T : M=N, N=Nk, K=hd (fp32)
+        dP = torch.empty(B, heads, N, ld, device=dev, dtype=torch.float32)
+        ops.gemm(do, vp, dP, M=N, N=Nk, K=hd, a_ld=C, b_ld=kv_ld, d_ld=ld, batch=(heads, B),
+                 a_bs=(hd, N * C), b_bs=(hd, Nk * kv_ld), d_bs=(N * ld, heads * N * ld))
+        dS = torch.empty(B, heads, N, ld, device=dev, dtype=dt)
+        ops.softmax_bwd(P, dP, dS, scale, Nk)
+        del dP
+        # dQ = dS K : M=N, N=hd, K=Nk (K MN-major)
+        ops.gemm(dS, kp, dq_t, M=N, N=hd, K=Nk, a_ld=ld, b_ld=kv_ld, b_mn=True, d_ld=q_ld,
+                 batch=(heads, B), a_bs=(N * ld, heads * N * ld), b_bs=(hd, Nk * kv_ld), d_bs=(hd, N * q_ld))
+        # dK = dS^T Q : M=Nk, N=hd, K=N
+        ops.gemm(dS, q_t, dkp, M=Nk, N=hd, K=N, a_ld=ld, a_mn=True, b_ld=q_ld, b_mn=True, d_ld=kv_ld,
+                 batch=(heads, B), a_bs=(N * ld, heads * N * ld), b_bs=(hd, N * q_ld), d_bs=(hd, Nk * kv_ld))
+        if self_attn:
+            return dq_t, None, None, None
+        return dq_t, dkv_t, None, None
+
+
+# ============================================================================ layer API
+
+def _anchor():
+    return current_anchor()
+
+
+class Linear:
+    def __init__(self, store, name, fin, fout, bias=True, init="w"):
+        self.weight = store.add(f"{name}.weight", (fout, fin), init=init)
+        self.bias = store.add(f"{name}.bias", (fout,), fp32=True, init="b") if bias else None
+
+    def __call__(self, x, residual=None):
+        return _LinearFn.apply(x, _anchor(), residual, self)
+
+
+class Conv2d:
+    """NHWC conv, weights [K, R, S, C]; `pad` = (top, left); symmetric unless out_hw given."""
+
+    def __init__(self, store, name, cin, cout, k=3, stride=1, pad=None, bias=True, init="w",
+                 asym=False):
+        self.k, self.stride = k, stride
+        self.pad = (0, 0) if asym else ((k // 2, k // 2) if pad is None else pad)
+        self.asym = asym
+        self.weight = store.add(f"{name}.weight", (cout, k, k, cin), init=init)
+        self.bias = store.add(f"{name}.bias", (cout,), fp32=True, init="b") if bias else None
+
+    def out_hw(self, x):
+        H, W = x.shape[1], x.shape[2]
+        if self.asym:  # SD-VAE downsample: pad (0,1,0,1) then 3x3 stride 2
+            return ((H + 1 - self.k) // 2 + 1, (W + 1 - self.k) // 2 + 1)
+        return (ops.conv_out_size(H, self.k, self.stride, self.pad[0], self.pad[0]),
+                ops.conv_out_size(W, self.k, self.stride, self.pad[1], self.pad[1]))
+
+    def __call__(self, x, residual=None):
+        return _ConvFn.apply(x, _anchor(), residual, self)
+
+
+class GroupNorm:
+    def __init__(self, store, name, C, groups=32, eps=1e-6, silu=False):
+        self.groups, self.eps, self.silu = groups, eps, silu
+        self.gamma = store.add(f"{name}.weight", (C,), fp32=True, init="g")
+        self.beta = store.add(f"{name}.bias", (C,), fp32=True, init="b")
+
+    def __call__(self, x):
+        return _GroupNormFn.apply(x, _anchor(), self)
+
+
+class LayerNorm:
+    def __init__(self, store, name, C, eps=1e-5, affine=True):
+        self.eps = eps
+        self.gamma = store.add(f"{name}.weight", (C,), fp32=True, init="g") if affine else None
+        self.beta = store.add(f"{name}.bias", (C,), fp32=True, init="b") if affine else None
+
+    def __call__(self, x):
+        return _LayerNormFn.apply(x, _anchor(), self)
+
+
+def ln_modulate(x, mod, shift_off, scale_off, eps=1e-6):
+    return _LayerNormModFn.apply(x, mod, shift_off, scale_off, eps)
+
+
+def gate_residual(x, mod, off, h):
+    return _GateResidualFn.apply(x, mod, off, h)
+
+
+def silu(x):
+    return _ActFn.apply(x, DP_ACT_SILU)
+
+
+def gelu(x, tanh=False):
+    return _ActFn.apply(x, DP_ACT_GELU_TANH if tanh else DP_ACT_GELU)
+
+
+def geglu(x):
+    return _GegluFn.apply(x)
+
+
+def add(a, b):
+    return _AddFn.apply(a, b)
+
+
+def add_row_bias(x, e):
+    return _RowBiasFn.apply(x, e)
+
+
+def concat(a, b):
+    return _ConcatFn.apply(a, b)
+
+
+def upsample2x(x):
+    return _Upsample2xFn.apply(x)
+
+
+def add_const(x, const):
+    return _AddConstFn.apply(x, const)
+
+
+def space_to_depth(x, p):
+    return _SpaceToDepthFn.apply(x, p, False)
+
+
+def depth_to_space(x, p):
+    return _SpaceToDepthFn.apply(x, p, True)
+
+
+def attention(q_t, kv_t, heads, causal=False):
+    return _AttentionFn.apply(q_t, kv_t, heads, causal)
+
+
+class SelfAttention:
+    """Fused qkv projection -> attention -> out projection (+ residual in the epilogue)."""
+
+    def __init__(self, store, name, C, heads, qkv_bias=False, causal=False):
+        self.heads, self.causal = heads, causal
+        self.qkv = Linear(store, f"{name}.qkv", C, 3 * C, bias=qkv_bias)
+        self.out = Linear(store, f"{name}.out", C, C)
+
+    def __call__(self, x, residual=None):
+        o = attention(self.qkv(x), None, self.heads, self.causal)
+        return self.out(o, residual=residual)
+
+
+class CrossAttention:
+    def __init__(self, store, name, C, ctx_dim, heads):
+        self.heads = heads
+        self.q = Linear(store, f"{name}.q", C, C, bias=False)
+        self.kv = Linear(store, f"{name}.kv", ctx_dim, 2 * C, bias=False)
+        self.out = Linear(store, f"{name}.out", C, C)
+
+    def __call__(self, x, ctx, residual=None):
+        o = attention(self.q(x), self.kv(ctx), self.heads)
+        return self.out(o, residual=residual)

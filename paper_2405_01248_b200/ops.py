@@ -230,3 +230,258 @@ def conv2d_wgrad(dy, x, dw, *, stride=1, pad=(1, 1)):
         return dw
     cols = im2col(x, R, S, stride, pad, P, Q)
     return linear_wgrad(dy.reshape(-1, K), cols, dw.view(K, -1))
+
+
+# ---------------------------------------------------------------------------- elementwise / norm
+
+def _L():
+    return _lib.lib()
+
+
+def act(x, op, out=None):
+    out = torch.empty_like(x) if out is None else out
+    check(_L().dp_act_fwd(op, dtype_code(x), _ptr(x), _ptr(out), x.numel(), _stream()), "dp_act_fwd")
+    return out
+
+
+def act_bwd(x, dy, op, dx=None, accumulate=False):
+    dx = torch.empty_like(x) if dx is None else dx
+    check(_L().dp_act_bwd(op, dtype_code(x), _ptr(x), _ptr(dy), _ptr(dx), x.numel(), int(accumulate),
+                          _stream()), "dp_act_bwd")
+    return dx
+
+
+def geglu(x):
+    rows, F2 = x.numel() // x.shape[-1], x.shape[-1]
+    y = torch.empty(*x.shape[:-1], F2 // 2, device=x.device, dtype=x.dtype)
+    check(_L().dp_geglu_fwd(dtype_code(x), _ptr(x), _ptr(y), rows, F2 // 2, _stream()), "dp_geglu_fwd")
+    return y
+
+
+def geglu_bwd(x, dy):
+    rows, F2 = x.numel() // x.shape[-1], x.shape[-1]
+    dx = torch.empty_like(x)
+    check(_L().dp_geglu_bwd(dtype_code(x), _ptr(x), _ptr(dy), _ptr(dx), rows, F2 // 2, _stream()),
+          "dp_geglu_bwd")
+    return dx
+
+
+def axpby(a, b, alpha=1.0, beta=1.0, out=None):
+    out = torch.empty_like(a) if out is None else out
+    check(_L().dp_axpby(dtype_code(a), _ptr(a), _ptr(b), _ptr(out), a.numel(), alpha, beta, _stream()),
+          "dp_axpby")
+    return out
+
+
+def gate_residual(x, g, g_ld, h, rows_per_sample):
+    C = x.shape[-1]
+    y = torch.empty_like(x)
+    check(_L().dp_gate_residual_fwd(dtype_code(x), _ptr(x), _ptr(g), g_ld, _ptr(h), _ptr(y),
+                                    x.numel() // C, C, rows_per_sample, _stream()), "dp_gate_residual_fwd")
+    return y
+
+
+def gate_residual_bwd(dy, g, g_ld, h, dg, dg_ld, B, rows_per_sample):
+    C = dy.shape[-1]
+    dh = torch.empty_like(dy)
+    check(_L().dp_gate_residual_bwd(dtype_code(dy), _ptr(dy), _ptr(g), g_ld, _ptr(h), _ptr(dh), _ptr(dg),
+                                    dg_ld, B, C, rows_per_sample, _stream()), "dp_gate_residual_bwd")
+    return dh
+
+
+def q_sample(x0, noise, t, sqrt_ab, sqrt_1mab, out=None):
+    out = torch.empty_like(x0) if out is None else out
+    check(_L().dp_q_sample(dtype_code(x0), _ptr(x0), _ptr(noise), _ptr(t), _ptr(sqrt_ab), _ptr(sqrt_1mab),
+                           _ptr(out), x0.numel(), x0.numel() // x0.shape[0], _stream()), "dp_q_sample")
+    return out
+
+
+def pred_x0(xt, eps, t, sqrt_ab, sqrt_1mab, out=None):
+    out = torch.empty_like(xt) if out is None else out
+    check(_L().dp_pred_x0(dtype_code(xt), _ptr(xt), _ptr(eps), _ptr(t), _ptr(sqrt_ab), _ptr(sqrt_1mab),
+                          _ptr(out), xt.numel(), xt.numel() // xt.shape[0], _stream()), "dp_pred_x0")
+    return out
+
+
+def mse(pred, target, loss_acc, scale, dpred=None):
+    check(_L().dp_mse(dtype_code(pred), _ptr(pred), _ptr(target), _ptr(dpred), _ptr(loss_acc), pred.numel(),
+                      scale, _stream()), "dp_mse")
+    return dpred
+
+
+def timestep_embed(t, dim, dtype, max_period=10000.0):
+    out = torch.empty(t.shape[0], dim, device=t.device, dtype=dtype)
+    check(_L().dp_timestep_embed(_DT[dtype], _ptr(t), _ptr(out), t.shape[0], dim, max_period, _stream()),
+          "dp_timestep_embed")
+    return out
+
+
+def embed(ids, table, pos=None):
+    B, L = ids.shape
+    C = table.shape[1]
+    out = torch.empty(B, L, C, device=ids.device, dtype=table.dtype)
+    check(_L().dp_embed(dtype_code(table), _ptr(ids), _ptr(table), _ptr(pos), _ptr(out), B * L, L, C,
+                        _stream()), "dp_embed")
+    return out
+
+
+def concat_last(a, b, Cb=None):
+    """cat([a, b], -1) over row-major tensors; b None -> zeros of width Cb."""
+    Ca = a.shape[-1]
+    Cb = b.shape[-1] if b is not None else Cb
+    rows = a.numel() // Ca
+    out = torch.empty(*a.shape[:-1], Ca + Cb, device=a.device, dtype=a.dtype)
+    check(_L().dp_concat(dtype_code(a), _ptr(a), _ptr(b), _ptr(out), rows, Ca, Cb, _stream()), "dp_concat")
+    return out
+
+
+def split_last(src, Ca, a=None, b=None, acc_a=False, acc_b=False):
+    C = src.shape[-1]
+    rows = src.numel() // C
+    check(_L().dp_split(dtype_code(src), _ptr(src), _ptr(a), _ptr(b), rows, Ca, C - Ca, int(acc_a),
+                        int(acc_b), _stream()), "dp_split")
+    return a, b
+
+
+def upsample2x(x):
+    N, H, W, C = x.shape
+    y = torch.empty(N, 2 * H, 2 * W, C, device=x.device, dtype=x.dtype)
+    check(_L().dp_upsample2x(dtype_code(x), _ptr(x), _ptr(y), N, H, W, C, _stream()), "dp_upsample2x")
+    return y
+
+
+def upsample2x_bwd(dy):
+    N, H2, W2, C = dy.shape
+    dx = torch.empty(N, H2 // 2, W2 // 2, C, device=dy.device, dtype=dy.dtype)
+    check(_L().dp_upsample2x_bwd(dtype_code(dy), _ptr(dy), _ptr(dx), N, H2 // 2, W2 // 2, C, _stream()),
+          "dp_upsample2x_bwd")
+    return dx
+
+
+def cast(x, dtype, out=None):
+    out = torch.empty(x.shape, device=x.device, dtype=dtype) if out is None else out
+    check(_L().dp_cast(dtype_code(x), _DT[dtype], _ptr(x), _ptr(out), x.numel(), _stream()), "dp_cast")
+    return out
+
+
+def bias_grad(dy, db):
+    C = dy.shape[-1]
+    check(_L().dp_bias_grad(dtype_code(dy), _ptr(dy), _ptr(db), dy.numel() // C, C, _stream()),
+          "dp_bias_grad")
+
+
+def adamw(param, grad, exp_avg, exp_avg_sq, param_bf16, lr, beta1, beta2, eps, weight_decay, step,
+          grad_scale=1.0):
+    check(_L().dp_adamw(_ptr(param), _ptr(grad), _ptr(exp_avg), _ptr(exp_avg_sq), _ptr(param_bf16),
+                        param.numel(), lr, beta1, beta2, eps, weight_decay, step, grad_scale, _stream()),
+          "dp_adamw")
+
+
+_GN_WS = {}
+
+
+def _gn_ws(device, nbytes):
+    ws = _GN_WS.get(device)
+    if ws is None or ws.numel() * 4 < nbytes:
+        ws = torch.empty((nbytes + 3) // 4 + 1024, device=device, dtype=torch.float32)
+        _GN_WS[device] = ws
+    return ws
+
+
+def group_norm(x, gamma, beta, G, eps, silu):
+    """x NHWC [N,H,W,C] (or [N,L,C]); returns y, mean, rstd."""
+    N, C = x.shape[0], x.shape[-1]
+    HW = x.numel() // (N * C)
+    y = torch.empty_like(x)
+    mean = torch.empty(N, G, device=x.device, dtype=torch.float32)
+    rstd = torch.empty_like(mean)
+    ws = _gn_ws(x.device, _L().dp_group_norm_workspace(N, HW, G))
+    check(_L().dp_group_norm_fwd(dtype_code(x), _ptr(x), _ptr(gamma), _ptr(beta), _ptr(y), _ptr(mean),
+                                 _ptr(rstd), N, HW, C, G, eps, int(silu), _ptr(ws), _stream()),
+          "dp_group_norm_fwd")
+    return y, mean, rstd
+
+
+def group_norm_bwd(x, dy, gamma, beta, mean, rstd, G, silu, dgamma=None, dbeta=None):
+    N, C = x.shape[0], x.shape[-1]
+    HW = x.numel() // (N * C)
+    dx = torch.empty_like(x)
+    ws = _gn_ws(x.device, _L().dp_group_norm_workspace(N, HW, G))
+    check(_L().dp_group_norm_bwd(dtype_code(x), _ptr(x), _ptr(dy), _ptr(gamma), _ptr(beta), _ptr(mean),
+                                 _ptr(rstd), _ptr(dx), _ptr(dgamma), _ptr(dbeta), N, HW, C, G, int(silu), 0,
+                                 _ptr(ws), _stream()), "dp_group_norm_bwd")
+    return dx
+
+
+def layer_norm(x, gamma, beta, eps, mod=None, mod_ld=0, shift_off=0, scale_off=0, rows_per_sample=1):
+    C = x.shape[-1]
+    rows = x.numel() // C
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device=x.device, dtype=torch.float32)
+    rstd = torch.empty_like(mean)
+    check(_L().dp_layer_norm_fwd(dtype_code(x), _ptr(x), _ptr(gamma), _ptr(beta), _ptr(mod), mod_ld,
+                                 shift_off, scale_off, rows_per_sample, _ptr(y), _ptr(mean), _ptr(rstd),
+                                 rows, C, eps, _stream()), "dp_layer_norm_fwd")
+    return y, mean, rstd
+
+
+def layer_norm_bwd(x, dy, gamma, mean, rstd, dgamma=None, dbeta=None, mod=None, mod_ld=0, shift_off=0,
+                   scale_off=0, rows_per_sample=1, dmod=None, dmod_ld=0):
+    C = x.shape[-1]
+    rows = x.numel() // C
+    dx = torch.empty_like(x)
+    check(_L().dp_layer_norm_bwd(dtype_code(x), _ptr(x), _ptr(dy), _ptr(gamma), _ptr(mod), mod_ld,
+                                 shift_off, scale_off, rows_per_sample, _ptr(mean), _ptr(rstd), _ptr(dx),
+                                 _ptr(dgamma), _ptr(dbeta), _ptr(dmod), dmod_ld, rows, C, 0, _stream()),
+          "dp_layer_norm_bwd")
+    return dx
+
+
+def softmax(S, P, scale, cols, causal=False, Lq=1):
+    """S fp32 / P [..., ld] row-major with `cols` valid columns per row."""
+    ld = S.shape[-1]
+    rows = S.numel() // ld
+    check(_L().dp_softmax_fwd(dtype_code(P), _ptr(S), _ptr(P), rows, cols, ld, scale, int(causal), Lq,
+                              _stream()), "dp_softmax_fwd")
+    return P
+
+
+def softmax_bwd(P, dP, dS, scale, cols):
+    ld = dP.shape[-1]
+    rows = dP.numel() // ld
+    check(_L().dp_softmax_bwd(dtype_code(P), _ptr(P), _ptr(dP), _ptr(dS), rows, cols, ld, scale, _stream()),
+          "dp_softmax_bwd")
+    return dS
+
+
+def row_bias(x, e, rows_per_sample):
+    """y = x + e[b] broadcast over the rows of sample b (e [B, >=C] with row stride e.stride(0))."""
+    C = x.shape[-1]
+    y = torch.empty_like(x)
+    check(_L().dp_row_bias_fwd(dtype_code(x), _ptr(x), _ptr(e), e.stride(0), _ptr(y), x.numel() // C, C,
+                               rows_per_sample, _stream()), "dp_row_bias_fwd")
+    return y
+
+
+def row_bias_bwd(dy, B, rows_per_sample):
+    C = dy.shape[-1]
+    de = torch.empty(B, C, device=dy.device, dtype=dy.dtype)
+    check(_L().dp_row_bias_bwd(dtype_code(dy), _ptr(dy), _ptr(de), C, B, C, rows_per_sample, _stream()),
+          "dp_row_bias_bwd")
+    return de
+
+
+def space_to_depth(x, p, inverse=False):
+    """NHWC space-to-depth by p (patch channel order (i, j, c)); inverse = depth-to-space."""
+    if not inverse:
+        N, H, W, C = x.shape
+        out = torch.empty(N, H // p, W // p, p * p * C, device=x.device, dtype=x.dtype)
+        Hs, Ws, Cs = H, W, C
+    else:
+        N, h, w, PC = x.shape
+        C = PC // (p * p)
+        out = torch.empty(N, h * p, w * p, C, device=x.device, dtype=x.dtype)
+        Hs, Ws, Cs = h * p, w * p, C
+    check(_L().dp_space_to_depth(dtype_code(x), _ptr(x), _ptr(out), N, Hs, Ws, Cs, p, int(inverse), _stream()),
+          "dp_space_to_depth")
+    return out

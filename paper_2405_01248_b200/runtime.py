@@ -1,0 +1,577 @@
+"""Pipelined training executor: replays the planner's schedule on real devices.
+
+One process per GPU (torch.distributed; NCCL on B200, gloo for CPU tests).
+Rank r = group * D + local device; group g is one pipeline replica of the
+planner's D-device group (reference planner.py:10-15,151-158).
+
+Per iteration i (cross-iteration filling):
+  * the backbone trains on batch i, whose frozen outputs (latents, context) were
+    computed during iteration i-1 (iteration 0 is preceded by a warm-up frozen pass);
+  * every rank executes its DeviceProgram (adapter.py) in order:
+      fwd / fwd_sc / bwd  on the high-priority compute stream, live sets moving by P2P
+      fill                on the low-priority fill stream, gated on the event of the
+                          compute task that precedes the bubble; frozen work for batch i+1
+      sync                per-stage flat-gradient allreduce + flat AdamW
+      tail, deliver       leftover frozen work, then frozen outputs -> stage-0 owners.
+
+P2P uses one 2-rank process group per (kind, src, dst) so that every link is a FIFO
+whose send and receive orders agree by construction: forward activations, backward
+gradients, self-conditioning feedback and frozen transfers never share a queue.
+
+Compute is abstracted by `TrainModel` (backbone + frozen components with layer lists);
+the executor itself never touches kernels, so the same control plane runs on CPU/gloo in
+tests with torch-op layers and on B200 with the libdpipe components.
+"""
+
+from __future__ import annotations
+
+import contextlib
+import time
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from .adapter import GroupProgram, backbone_transfers, split_range
+
+# ============================================================================ model bundle
+
+
+@dataclass
+class FrozenSpec:
+    component: object            # networks.Component (or a test double): .layers, .run
+    inputs: tuple                # raw batch fields consumed by layer 0 ("images" / "ids")
+
+
+class TrainModel:
+    """Backbone + frozen components + diffusion glue, independent of placement.
+
+    `ops` provides the few fused kernels the glue needs (q_sample, pred_x0, mse,
+    concat); on B200 it is paper_2405_01248_b200.ops, in CPU tests a torch stand-in.
+    """
+
+    def __init__(self, backbone, frozen, ops, sqrt_ab, sqrt_1mab, selfcond_channels=0,
+                 grad_scale=1.0, adamw=None):
+        self.backbone = backbone
+        self.frozen = frozen
+        self.ops = ops
+        self.sqrt_ab = sqrt_ab
+        self.sqrt_1mab = sqrt_1mab
+        self.sc_ch = selfcond_channels
+        self.adamw = adamw or {}
+
+    # -- stage 0 input construction ------------------------------------------------------
+    def stage0_inputs(self, frozen_out, t, noise, x0_sc=None):
+        """frozen_out: merged dict of frozen outputs (latent, ctx, pooled) for these samples."""
+        o = self.ops
+        x0 = frozen_out["latent"]
+        xt = o.q_sample(x0, noise, t, self.sqrt_ab, self.sqrt_1mab)
+        if self.sc_ch:
+            sc = x0_sc if x0_sc is not None else torch.zeros_like(xt)
+            x = o.concat_last(xt, sc)
+        else:
+            x = xt
+        st = {"x": x, "t": t, "noise": noise}
+        for k, v in frozen_out.items():
+            if k != "latent":
+                st[k] = v
+        return st, xt
+
+
+# ============================================================================ helpers
+
+
+def _cat(parts):
+    parts = [p for p in parts if p is not None]
+    if len(parts) == 1:
+        return parts[0]
+    return torch.cat(parts, 0)
+
+
+class _Streams:
+    def __init__(self, device):
+        self.cuda = device.type == "cuda"
+        if self.cuda:
+            self.compute = torch.cuda.Stream(device=device, priority=-1)
+            self.fill = torch.cuda.Stream(device=device, priority=0)
+        else:
+            self.compute = self.fill = None
+
+    def on(self, which):
+        if not self.cuda:
+            return contextlib.nullcontext()
+        return torch.cuda.stream(self.compute if which == "compute" else self.fill)
+
+    def event(self, which):
+        if not self.cuda:
+            return None
+        ev = torch.cuda.Event()
+        ev.record(self.compute if which == "compute" else self.fill)
+        return ev
+
+    def wait(self, which, ev):
+        if ev is None or not self.cuda:
+            return
+        (self.compute if which == "compute" else self.fill).wait_event(ev)
+
+    def join(self):
+        if self.cuda:
+            self.compute.wait_stream(self.fill)
+
+    def record(self, t, which):
+        if self.cuda and t is not None and t.is_cuda:
+            t.record_stream(self.compute if which == "compute" else self.fill)
+
+
+class Links:
+    """2-rank process groups per (kind, src, dst); kinds: fwd, bwd, fb (self-cond feedback), frz."""
+
+    def __init__(self, rank, world, needed):
+        self.rank = rank
+        self.pg = {}
+        if world == 1:
+            return
+        for key in sorted(needed):
+            kind, a, b = key
+            g = dist.new_group(ranks=sorted({a, b}))
+            self.pg[key] = g
+
+    def isend(self, kind, t, dst):
+        return dist.isend(t.contiguous(), dst=dst, group=self.pg[(kind, self.rank, dst)])
+
+    def irecv(self, kind, t, src):
+        return dist.irecv(t, src=src, group=self.pg[(kind, src, self.rank)])
+
+
+# ============================================================================ executor
+
+
+class PipelineExecutor:
+    def __init__(self, model: TrainModel, programs: dict, *, rank=0, world=1, device="cuda",
+                 live_specs=None, frozen_specs=None, loss_scale=1.0, inputs=None):
+        """programs: {False: GroupProgram, True: GroupProgram (self-cond activated)} built from
+        the same partition; `inputs` provides host/device batch slices (InputFeed)."""
+        self.model = model
+        self.programs = programs
+        self.prog0 = programs[False]
+        self.rank, self.world = rank, world
+        self.D = self.prog0.D
+        self.group, self.dev = divmod(rank, self.D)
+        self.device = torch.device(device)
+        self.streams = _Streams(self.device)
+        self.live_specs = live_specs      # list per layer boundary: {name: (shape, dtype, grad)}
+        self.frozen_specs = frozen_specs  # [comp][layer] -> {name: (shape, dtype)}
+        self.loss_scale = loss_scale
+        self.inputs = inputs
+        p = self.prog0.device_program(self.dev)
+        self.stage, self.replica = p.stage, p.replica
+        if self.stage is not None:
+            lo, hi = self.prog0.stage_ranges[self.stage]
+            self.param_range = model.backbone.stage_slice(lo, hi)
+        self.links = Links(rank, world, self._needed_links())
+        self._stage_pg = self._make_stage_groups()
+        self.frozen_ready = {}   # for the NEXT iteration: comp -> list[(lo, hi, state)] on stage-0 owners
+        self.loss_buf = torch.zeros(1, device=self.device, dtype=torch.float32)
+        self.timeline = []       # (kind, micro, stage, ev_start, ev_end) when tracing
+        self.trace = False
+        self.grad_snapshots = None  # list -> flat grad slices captured before each AdamW
+
+    # ---------------------------------------------------------------- setup
+    def gb_of(self):
+        """Offset of this rank's pipeline group in the world batch."""
+        return self.group * self.prog0.group_batch
+
+    def _grank(self, dev):
+        return self.group * self.D + dev
+
+    def _needed_links(self):
+        need = set()
+        for g in range(self.world // self.D):
+            base = g * self.D
+            for prog in self.programs.values():
+                for s in range(prog.S - 1):
+                    for m in range(prog.M):
+                        for i, j, a, b in backbone_transfers(prog, s, m):
+                            src = base + prog.stage_devices[s][0] + i
+                            dst = base + prog.stage_devices[s + 1][0] + j
+                            need.add(("fwd", src, dst))
+                            need.add(("bwd", dst, src))
+                if prog.selfcond and prog.S > 1:
+                    for m in range(prog.M):
+                        for i, j, a, b in self._feedback_pieces(prog, m):
+                            need.add(("fb", base + prog.stage_devices[-1][0] + i,
+                                      base + prog.stage_devices[0][0] + j))
+                for t in list(prog.transfers) + list(prog.deliveries):
+                    if t.src != t.dst:
+                        need.add(("frz", base + t.src, base + t.dst))
+        return need
+
+    def _make_stage_groups(self):
+        if self.world == 1:
+            return None
+        mine = None
+        for s in range(self.prog0.S):
+            a, b = self.prog0.stage_devices[s]
+            ranks = [g * self.D + d for g in range(self.world // self.D) for d in range(a, b)]
+            pg = dist.new_group(ranks=ranks) if len(ranks) > 1 else None
+            if s == self.stage:
+                mine = pg
+        return mine
+
+    @staticmethod
+    def _feedback_pieces(prog, m):
+        lo, hi = prog.micro_range(m)
+        a0, a1 = prog.stage_devices[-1]
+        b0, b1 = prog.stage_devices[0]
+        out = []
+        for i, (sa, sb) in enumerate(split_range(lo, hi, a1 - a0)):
+            for j, (da, db) in enumerate(split_range(lo, hi, b1 - b0)):
+                a, b = max(sa, da), min(sb, db)
+                if b > a:
+                    out.append((i, j, a, b))
+        return out
+
+    # ---------------------------------------------------------------- frozen work
+    def _alloc_like(self, spec, n):
+        return {k: torch.empty((n,) + tuple(shape), device=self.device, dtype=dt)
+                for k, (shape, dt) in sorted(spec.items())}
+
+    def _run_frozen_piece(self, piece, store, raw):
+        comp = self.model.frozen[piece.comp]
+        if piece.layer == 0:
+            st = {f: raw(f, piece.lo, piece.hi) for f in comp.inputs}
+        else:
+            st = self._gather_frozen(store, piece.comp, piece.layer - 1, piece.lo, piece.hi)
+        with torch.no_grad():
+            out = comp.component.layers[piece.layer](st)
+        store.setdefault((piece.comp, piece.layer), []).append((piece.lo, piece.hi, out))
+        return out
+
+    def _gather_frozen(self, store, comp, layer, lo, hi):
+        parts = []
+        for a, b, st in store.get((comp, layer), []):
+            x, y = max(a, lo), min(b, hi)
+            if y > x:
+                parts.append((x, {k: v[x - a:y - a] for k, v in st.items()}))
+        parts.sort(key=lambda q: q[0])
+        cov = sum(next(iter(p[1].values())).shape[0] for p in parts)
+        if cov != hi - lo:
+            raise RuntimeError(f"frozen comp {comp} layer {layer} [{lo},{hi}) missing on device "
+                               f"{self.dev} (have {cov})")
+        keys = parts[0][1].keys()
+        return {k: _cat([p[1][k] for p in parts]) for k in keys}
+
+    def _post_frozen_sends(self, prog, piece, out, sent):
+        """Send every transfer this piece's output feeds (production order)."""
+        for t in prog.transfers:
+            if (t.src == self.dev and t.comp == piece.comp and t.layer == piece.layer
+                    and piece.lo <= t.lo and t.hi <= piece.hi and t.dst != self.dev):
+                for k in sorted(out):
+                    self.links.isend("frz", out[k][t.lo - piece.lo:t.hi - piece.lo], self._grank(t.dst))
+                sent.add(t.seq)
+
+    def _recv_frozen_upto(self, prog, store, need_seq, posted, stream_which):
+        """Post receives (in production order) for every transfer to this device up to
+        `need_seq`, wait for them, and add them to `store`."""
+        for t in prog.transfers:
+            if t.seq > need_seq:
+                break
+            if t.dst != self.dev or t.src == self.dev or t.seq in posted:
+                continue
+            spec = self.frozen_specs[t.comp][t.layer]
+            bufs = self._alloc_like(spec, t.hi - t.lo)
+            works = [self.links.irecv("frz", bufs[k], self._grank(t.src)) for k in sorted(bufs)]
+            posted[t.seq] = (t, bufs, works)
+        for seq, (t, bufs, works) in list(posted.items()):
+            if works is not None and seq <= need_seq:
+                for w in works:
+                    w.wait()
+                store.setdefault((t.comp, t.layer), []).append((t.lo, t.hi, bufs))
+                posted[seq] = (t, bufs, None)
+
+    def _run_pieces(self, prog, pieces, store, raw, posted, sent):
+        for piece in pieces:
+            if piece.device != self.dev:
+                continue
+            if piece.layer > 0:
+                need = [t.seq for t in prog.transfers
+                        if t.dst == self.dev and t.comp == piece.comp and t.layer == piece.layer - 1
+                        and t.lo < piece.hi and piece.lo < t.hi]
+                if need:
+                    self._recv_frozen_upto(prog, store, max(need), posted, "fill")
+            out = self._run_frozen_piece(piece, store, raw)
+            self._post_frozen_sends(prog, piece, out, sent)
+
+    def _deliver(self, prog, store, posted):
+        """Final frozen outputs -> stage-0 owners (who use them next iteration)."""
+        if prog.transfers:
+            self._recv_frozen_upto(prog, store, prog.transfers[-1].seq, posted, "compute")
+        ready = {}
+        sends = []
+        recvs = []
+        for t in prog.deliveries:
+            if t.src == self.dev:
+                comp_out = self._gather_frozen(store, t.comp, t.layer, t.lo, t.hi)
+                if t.dst == self.dev:
+                    ready.setdefault(t.comp, []).append((t.lo, t.hi, comp_out))
+                else:
+                    for k in sorted(comp_out):
+                        sends.append(self.links.isend("frz", comp_out[k], self._grank(t.dst)))
+            elif t.dst == self.dev:
+                bufs = self._alloc_like(self.frozen_specs[t.comp][t.layer], t.hi - t.lo)
+                for k in sorted(bufs):
+                    recvs.append(self.links.irecv("frz", bufs[k], self._grank(t.src)))
+                ready.setdefault(t.comp, []).append((t.lo, t.hi, bufs))
+        for w in recvs:
+            w.wait()
+        for w in sends:
+            w.wait()
+        return ready
+
+    def frozen_for(self, frozen_ready, lo, hi):
+        """Merged frozen outputs of samples [lo, hi) (group-local) on this stage-0 device."""
+        merged = {}
+        for c, pieces in frozen_ready.items():
+            parts = []
+            for a, b, st in pieces:
+                x, y = max(a, lo), min(b, hi)
+                if y > x:
+                    parts.append((x, {k: v[x - a:y - a] for k, v in st.items()}))
+            parts.sort(key=lambda q: q[0])
+            for k in parts[0][1]:
+                merged[k] = _cat([p[1][k] for p in parts])
+        return merged
+
+    # ---------------------------------------------------------------- backbone
+    def _live_recv(self, boundary, n):
+        spec = self.live_specs[boundary]
+        return {k: torch.empty((n,) + tuple(shape), device=self.device, dtype=dt)
+                for k, (shape, dt, g) in sorted(spec.items())}
+
+    def _stage_forward(self, st_in, grad):
+        lo, hi = self.prog.stage_ranges[self.stage]
+        bb = self.model.backbone
+        if grad:
+            from . import nn as _nn  # noqa: F401  (anchor helper is optional for test doubles)
+            anchor_ctx = getattr(bb, "grad_context", None)
+            ctx = anchor_ctx() if anchor_ctx else contextlib.nullcontext()
+            with ctx:
+                return bb.run(st_in, lo, hi)
+        with torch.no_grad():
+            return bb.run(st_in, lo, hi)
+
+    def _fwd(self, m, sc_pass):
+        prog = self.prog
+        S = prog.S
+        s = self.stage
+        lo_r, hi_r = prog.replica_range(s, m, self.replica)
+        n = hi_r - lo_r
+        key = (m, sc_pass)
+        if s == 0:
+            fro = self.frozen_for(self.frozen_cur, lo_r, hi_r)
+            t, noise = self.inputs.t(self.gb + lo_r, self.gb + hi_r), self.inputs.noise(self.gb + lo_r,
+                                                                                         self.gb + hi_r)
+            x0_sc = None
+            if not sc_pass and prog.selfcond:
+                eps_sc = self._feedback_in.pop(m)
+                x0_sc = self.model.ops.pred_x0(self._xt[m], eps_sc, t, self.model.sqrt_ab,
+                                               self.model.sqrt_1mab)
+            st_in, xt = self.model.stage0_inputs(fro, t, noise, x0_sc)
+            if sc_pass:
+                self._xt[m] = xt
+        else:
+            st_in = self._recv_live(s, m, n, lo_r, "fwd_sc" if sc_pass else "fwd")
+        if not sc_pass:
+            for k, v in st_in.items():
+                if v.is_floating_point() and self.live_specs[prog.stage_ranges[s][0]].get(k, (0, 0, False))[2]:
+                    v.requires_grad_(True)
+        out = self._stage_forward(st_in, grad=not sc_pass)
+        if s == S - 1:
+            if sc_pass:
+                eps = out["out"].detach()
+                self._send_feedback(m, eps, lo_r)
+            else:
+                pred = out["out"]
+                dpred = torch.empty_like(pred)
+                self.model.ops.mse(pred.detach(), out["noise"], self.loss_buf, self.loss_scale, dpred)
+                self._saved[key] = (st_in, [pred], [dpred])
+        else:
+            if not sc_pass:
+                self._saved[key] = (st_in, out, None)
+            self._send_live(s, m, out, lo_r, "fwd_sc" if sc_pass else "fwd")
+
+    def _bwd(self, m):
+        prog = self.prog
+        s = self.stage
+        st_in, outs, grads = self._saved.pop((m, False))
+        if s == prog.S - 1:
+            torch.autograd.backward(outs, grads)
+        else:
+            lo_r, hi_r = prog.replica_range(s, m, self.replica)
+            spec = self.live_specs[prog.stage_ranges[s][1]]
+            names = [k for k in sorted(spec) if spec[k][2]]
+            gin = self._recv_grads(s, m, hi_r - lo_r, lo_r, names)
+            ts = [outs[k] for k in names if outs[k].requires_grad]
+            gs = [gin[k] for k in names if outs[k].requires_grad]
+            if ts:
+                torch.autograd.backward(ts, gs)
+        if s > 0:
+            spec = self.live_specs[prog.stage_ranges[s][0]]
+            names = [k for k in sorted(spec) if spec[k][2]]
+            grads_in = {k: (st_in[k].grad if st_in[k].grad is not None else torch.zeros_like(st_in[k]))
+                        for k in names}
+            lo_r, _ = prog.replica_range(s, m, self.replica)
+            self._send_grads(s, m, grads_in, lo_r)
+
+    # live-set P2P -------------------------------------------------------------------------
+    def _pieces(self, s, m, as_src):
+        """(peer_replica, lo, hi) pieces of micro m crossing cut s -> s+1 for this device."""
+        out = []
+        for i, j, a, b in backbone_transfers(self.prog, s, m):
+            if as_src and i == self.replica:
+                out.append((j, a, b))
+            if not as_src and j == self.replica:
+                out.append((i, a, b))
+        return out
+
+    def _send_live(self, s, m, out, lo_r, kind):
+        spec = self.live_specs[self.prog.stage_ranges[s][1]]
+        dst0 = self.prog.stage_devices[s + 1][0]
+        for j, a, b in self._pieces(s, m, True):
+            for k in sorted(spec):
+                self._pending.append(self.links.isend("fwd", out[k].detach()[a - lo_r:b - lo_r],
+                                                      self._grank(dst0 + j)))
+
+    def _recv_live(self, s, m, n, lo_r, kind):
+        spec_b = self.prog.stage_ranges[s][0]
+        bufs = self._live_recv(spec_b, n)
+        src0 = self.prog.stage_devices[s - 1][0]
+        works = []
+        for i, a, b in self._pieces(s - 1, m, False):
+            for k in sorted(bufs):
+                works.append(self.links.irecv("fwd", bufs[k][a - lo_r:b - lo_r], self._grank(src0 + i)))
+        for w in works:
+            w.wait()
+        return bufs
+
+    def _send_grads(self, s, m, grads, lo_r):
+        src0 = self.prog.stage_devices[s - 1][0]
+        for i, a, b in self._pieces(s - 1, m, False):
+            for k in sorted(grads):
+                self._pending.append(self.links.isend("bwd", grads[k][a - lo_r:b - lo_r],
+                                                      self._grank(src0 + i)))
+
+    def _recv_grads(self, s, m, n, lo_r, names):
+        spec = self.live_specs[self.prog.stage_ranges[s][1]]
+        bufs = {k: torch.empty((n,) + tuple(spec[k][0]), device=self.device, dtype=spec[k][1]) for k in names}
+        dst0 = self.prog.stage_devices[s + 1][0]
+        works = []
+        for j, a, b in self._pieces(s, m, True):
+            for k in names:
+                works.append(self.links.irecv("bwd", bufs[k][a - lo_r:b - lo_r], self._grank(dst0 + j)))
+        for w in works:
+            w.wait()
+        return bufs
+
+    def _send_feedback(self, m, eps, lo_r):
+        prog = self.prog
+        if prog.S == 1:
+            self._feedback_in[m] = eps
+            return
+        b0 = prog.stage_devices[0][0]
+        for i, j, a, b in self._feedback_pieces(prog, m):
+            if i == self.replica:
+                self._pending.append(self.links.isend("fb", eps[a - lo_r:b - lo_r], self._grank(b0 + j)))
+
+    def _recv_feedback(self, m):
+        prog = self.prog
+        lo_r, hi_r = prog.replica_range(0, m, self.replica)
+        spec = self.live_specs[-1]["out"]
+        buf = torch.empty((hi_r - lo_r,) + tuple(spec[0]), device=self.device, dtype=spec[1])
+        a0 = prog.stage_devices[-1][0]
+        works = [self.links.irecv("fb", buf[a - lo_r:b - lo_r], self._grank(a0 + i))
+                 for i, j, a, b in self._feedback_pieces(prog, m) if j == self.replica]
+        for w in works:
+            w.wait()
+        self._feedback_in[m] = buf
+
+    # ---------------------------------------------------------------- sync
+    def _sync(self):
+        store = self.model.backbone.store
+        lo, hi = self.param_range
+        if hasattr(store, "pre_allreduce"):
+            store.pre_allreduce()
+        if self._stage_pg is not None and hi > lo:
+            dist.all_reduce(store.grad[lo:hi], group=self._stage_pg)
+        if self.grad_snapshots is not None:
+            self.grad_snapshots.append((lo, hi, store.grad[lo:hi].detach().clone()))
+        store.adamw_step(rng=(lo, hi), **self.model.adamw)
+        store.zero_grad((lo, hi))
+
+    # ---------------------------------------------------------------- iteration
+    def warmup(self, raw_next):
+        """Iteration-0 warm-up: the frozen part of batch 0 alone, run as a
+        data-parallel tail over the group's D devices."""
+        prog = self.warm_program
+        store, posted, sent = {}, {}, set()
+        with self.streams.on("fill"):
+            self._run_pieces(prog, prog.tail, store, raw_next, posted, sent)
+        self.streams.join()
+        with self.streams.on("compute"):
+            self.frozen_ready = self._deliver(prog, store, posted)
+
+    def run_iteration(self, raw_next, selfcond, has_next=True):
+        """One training iteration on the current batch; fills compute batch i+1 (`raw_next`)."""
+        self.prog = prog = self.programs[bool(selfcond)]
+        self.frozen_cur = self.frozen_ready
+        self.frozen_ready = {}
+        self.gb = self.group * prog.group_batch
+        self._saved, self._xt, self._feedback_in, self._pending = {}, {}, {}, []
+        store, posted, sent = {}, {}, set()
+        self.loss_buf.zero_()
+        last_compute_ev = None
+        instrs = prog.device_program(self.dev).instrs
+        for ins in instrs:
+            kind = ins[0]
+            if kind in ("fwd", "fwd_sc", "bwd"):
+                _, m, s = ins
+                with self.streams.on("compute"):
+                    if kind == "fwd" and s == 0 and prog.selfcond:
+                        if prog.S > 1:
+                            self._recv_feedback(m)
+                    if kind == "bwd":
+                        self._bwd(m)
+                    else:
+                        self._fwd(m, kind == "fwd_sc")
+                    last_compute_ev = self.streams.event("compute")
+            elif kind == "fill":
+                if not has_next:
+                    continue
+                self.streams.wait("fill", last_compute_ev)
+                with self.streams.on("fill"):
+                    self._run_pieces(prog, prog.fills[ins[1]], store, raw_next, posted, sent)
+            elif kind == "sync":
+                with self.streams.on("compute"):
+                    self._sync()
+            elif kind == "tail":
+                if not has_next:
+                    continue
+                self.streams.join()
+                with self.streams.on("compute"):
+                    self._run_pieces(prog, prog.tail, store, raw_next, posted, sent)
+            elif kind == "deliver":
+                self.streams.join()
+                with self.streams.on("compute"):
+                    if has_next:
+                        self.frozen_ready = self._deliver(prog, store, posted)
+                    for w in self._pending:
+                        w.wait()
+        if self.streams.cuda:
+            torch.cuda.current_stream(self.device).wait_stream(self.streams.compute)
+        return self.loss_buf
+
+    def total_loss(self):
+        """Sum of the loss over all ranks (only last-stage ranks contribute)."""
+        if self.world > 1:
+            dist.all_reduce(self.loss_buf)
+        return self.loss_buf
