@@ -102,10 +102,11 @@ __global__ void __launch_bounds__(GN_THREADS) gn_partial_kernel(const T* __restr
     const int rows_par = GN_THREADS / width;
     const int cv = cv0 + threadIdx.x % width;
     const int rl = threadIdx.x / width;
-    if (rl < rows_par) {
-      float cnt = 0.f, mean[V], m2[V];
+    const bool active = rl < rows_par;
+    float cnt = 0.f, mean[V], m2[V];
 #pragma unroll
-      for (int j = 0; j < V; ++j) mean[j] = m2[j] = 0.f;
+    for (int j = 0; j < V; ++j) mean[j] = m2[j] = 0.f;
+    if (active) {
       for (int p = p0 + rl; p < p1; p += rows_par) {
         float f[V];
         ld16(xs + (int64_t)p * C + cv * V, f);
@@ -118,24 +119,23 @@ __global__ void __launch_bounds__(GN_THREADS) gn_partial_kernel(const T* __restr
           m2[j] += d * (f[j] - mean[j]);
         }
       }
-      // merge rows_par lanes of the same channel through shared memory (serialised per lane row)
-      for (int r = 0; r < rows_par; ++r) {
-        if (rl == r && cnt > 0.f) {
+    }
+    // merge the rows_par lanes of each channel through shared memory, one lane row at a
+    // time; every thread executes the same barriers (bar.sync is warp-aligned)
+    for (int r = 0; r < rows_par; ++r) {
+      if (active && rl == r && cnt > 0.f) {
 #pragma unroll
-          for (int j = 0; j < V; ++j) {
-            const int c = cv * V + j;
-            Welford a{s_n[c], s_mean[c], s_m2[c]};
-            Welford b{cnt, mean[j], m2[j]};
-            a = wf_merge(a, b);
-            s_n[c] = a.n;
-            s_mean[c] = a.mean;
-            s_m2[c] = a.m2;
-          }
+        for (int j = 0; j < V; ++j) {
+          const int c = cv * V + j;
+          Welford a{s_n[c], s_mean[c], s_m2[c]};
+          Welford b{cnt, mean[j], m2[j]};
+          a = wf_merge(a, b);
+          s_n[c] = a.n;
+          s_mean[c] = a.mean;
+          s_m2[c] = a.m2;
         }
-        __syncthreads();
       }
-    } else {
-      for (int r = 0; r < rows_par; ++r) __syncthreads();
+      __syncthreads();
     }
   }
   __syncthreads();

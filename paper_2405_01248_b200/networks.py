@@ -247,7 +247,7 @@ class VAEEncoderBase(Component):
         self.pad_in = pad_in
 
     def _conv_in(self, st):
-        img = st["img"].to(self.dtype)
+        img = st["images"].to(self.dtype)
         if self.pad_in:
             img = ops.concat_last(img, torch.zeros(*img.shape[:-1], self.pad_in, device=img.device,
                                                    dtype=img.dtype))

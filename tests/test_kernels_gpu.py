@@ -1,0 +1,202 @@
+"""libdpipe norm / elementwise / attention / optimizer kernels vs plain PyTorch fp32
+references of the same ops (GPU). Tolerances: fp32 1e-5 relative, bf16 2e-2."""
+
+import math
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+DT = [torch.float32, torch.bfloat16]
+
+
+def _tol(dt):
+    return 2e-5 if dt == torch.float32 else 2e-2
+
+
+def _rel(a, b):
+    return ((a.float() - b.float()).norm() / (b.float().norm() + 1e-12)).item()
+
+
+@pytest.mark.parametrize("dt", DT)
+@pytest.mark.parametrize("N,H,C,G,silu", [(2, 16, 64, 32, False), (3, 8, 320, 32, True),
+                                          (2, 32, 128, 32, True), (1, 4, 2560, 32, True)])
+def test_group_norm(dt, N, H, C, G, silu):
+    from paper_2405_01248_b200 import ops
+    x = (torch.randn(N, H, H, C, device="cuda") * 2 + 0.5).to(dt)
+    g = torch.randn(C, device="cuda") * 0.1 + 1
+    b = torch.randn(C, device="cuda") * 0.1
+    y, mean, rstd = ops.group_norm(x, g, b, G, 1e-6, silu)
+    xr = x.float().permute(0, 3, 1, 2).requires_grad_(True)
+    gr, br = g.clone().requires_grad_(True), b.clone().requires_grad_(True)
+    yr = F.group_norm(xr, G, gr, br, 1e-6)
+    if silu:
+        yr = F.silu(yr)
+    assert _rel(y, yr.permute(0, 2, 3, 1)) < _tol(dt)
+    dy = torch.randn_like(y)
+    yr.backward(dy.float().permute(0, 3, 1, 2))
+    dg = torch.zeros(C, device="cuda")
+    db = torch.zeros(C, device="cuda")
+    dx = ops.group_norm_bwd(x, dy, g, b, mean, rstd, G, silu, dg, db)
+    tol = _tol(dt) * (1 if dt == torch.float32 else 2)
+    assert _rel(dx, xr.grad.permute(0, 2, 3, 1)) < tol
+    assert _rel(dg, gr.grad) < tol
+    assert _rel(db, br.grad) < tol
+
+
+@pytest.mark.parametrize("dt", DT)
+@pytest.mark.parametrize("rows,C", [(77, 1024), (300, 320), (64, 256), (10, 1280)])
+def test_layer_norm_affine(dt, rows, C):
+    from paper_2405_01248_b200 import ops
+    x = (torch.randn(rows, C, device="cuda") * 3 - 1).to(dt)
+    g = torch.randn(C, device="cuda") * 0.1 + 1
+    b = torch.randn(C, device="cuda") * 0.1
+    y, mean, rstd = ops.layer_norm(x, g, b, 1e-5)
+    xr = x.float().requires_grad_(True)
+    gr, br = g.clone().requires_grad_(True), b.clone().requires_grad_(True)
+    yr = F.layer_norm(xr, (C,), gr, br, 1e-5)
+    assert _rel(y, yr) < _tol(dt)
+    dy = torch.randn_like(y)
+    yr.backward(dy.float())
+    dg = torch.zeros(C, device="cuda")
+    db = torch.zeros(C, device="cuda")
+    dx = ops.layer_norm_bwd(x, dy, g, mean, rstd, dgamma=dg, dbeta=db)
+    assert _rel(dx, xr.grad) < 2 * _tol(dt)
+    assert _rel(dg, gr.grad) < 2 * _tol(dt)
+    assert _rel(db, br.grad) < 2 * _tol(dt)
+
+
+@pytest.mark.parametrize("dt", DT)
+def test_layer_norm_modulated(dt):
+    from paper_2405_01248_b200 import nn
+    B, L, D = 3, 64, 256
+    x = torch.randn(B, L, D, device="cuda").to(dt).requires_grad_(True)
+    mod = (torch.randn(B, 6 * D, device="cuda") * 0.3).to(dt).requires_grad_(True)
+    y = nn.ln_modulate(x, mod, 3 * D, 4 * D)
+    xr = x.detach().float().requires_grad_(True)
+    mr = mod.detach().float().requires_grad_(True)
+    yr = F.layer_norm(xr, (D,), eps=1e-6) * (1 + mr[:, None, 4 * D:5 * D]) + mr[:, None, 3 * D:4 * D]
+    assert _rel(y, yr) < _tol(dt)
+    dy = torch.randn_like(y)
+    y.backward(dy)
+    yr.backward(dy.float())
+    assert _rel(x.grad, xr.grad) < 2 * _tol(dt)
+    assert _rel(mod.grad, mr.grad) < 2 * _tol(dt)
+
+
+@pytest.mark.parametrize("dt", DT)
+@pytest.mark.parametrize("B,N,Nk,C,heads,causal,cross", [(2, 256, 256, 256, 4, False, False),
+                                                          (2, 77, 77, 128, 2, True, False),
+                                                          (2, 256, 77, 320, 5, False, True),
+                                                          (1, 64, 16, 512, 1, False, True)])
+def test_attention(dt, B, N, Nk, C, heads, causal, cross):
+    from paper_2405_01248_b200 import nn
+    if cross:
+        q = (torch.randn(B, N, C, device="cuda")).to(dt).requires_grad_(True)
+        kv = (torch.randn(B, Nk, 2 * C, device="cuda")).to(dt).requires_grad_(True)
+        o = nn.attention(q, kv, heads)
+        qr, kvr = q.detach().float().requires_grad_(True), kv.detach().float().requires_grad_(True)
+        Q, K, V = qr, kvr[..., :C], kvr[..., C:]
+    else:
+        q = (torch.randn(B, N, 3 * C, device="cuda")).to(dt).requires_grad_(True)
+        o = nn.attention(q, None, heads, causal)
+        qr = q.detach().float().requires_grad_(True)
+        Q, K, V = qr[..., :C], qr[..., C:2 * C], qr[..., 2 * C:]
+    hd = C // heads
+
+    def sp(t, n):
+        return t.reshape(B, n, heads, hd).transpose(1, 2)
+
+    ref = F.scaled_dot_product_attention(sp(Q, N), sp(K, Nk), sp(V, Nk), is_causal=causal)
+    ref = ref.transpose(1, 2).reshape(B, N, C)
+    assert _rel(o, ref) < _tol(dt) * 2
+    do = torch.randn_like(o)
+    o.backward(do)
+    ref.backward(do.float())
+    assert _rel(q.grad, qr.grad) < _tol(dt) * 3
+    if cross:
+        assert _rel(kv.grad, kvr.grad) < _tol(dt) * 3
+
+
+@pytest.mark.parametrize("dt", DT)
+def test_eltwise_family(dt):
+    from paper_2405_01248_b200 import nn, ops
+    x = torch.randn(4, 33, 64, device="cuda").to(dt).requires_grad_(True)
+    for fn, ref in [(nn.silu, F.silu), (lambda t: nn.gelu(t), F.gelu),
+                    (lambda t: nn.gelu(t, tanh=True), lambda t: F.gelu(t, approximate="tanh"))]:
+        y = fn(x)
+        xr = x.detach().float().requires_grad_(True)
+        yr = ref(xr)
+        assert _rel(y, yr) < _tol(dt)
+        dy = torch.randn_like(y)
+        x.grad = None
+        y.backward(dy)
+        yr.backward(dy.float())
+        assert _rel(x.grad, xr.grad) < 2 * _tol(dt)
+    g = torch.randn(4, 10, 128, device="cuda").to(dt).requires_grad_(True)
+    y = nn.geglu(g)
+    gr = g.detach().float().requires_grad_(True)
+    a, b = gr.chunk(2, -1)
+    yr = a * F.gelu(b)
+    assert _rel(y, yr) < _tol(dt)
+    dy = torch.randn_like(y)
+    y.backward(dy)
+    yr.backward(dy.float())
+    assert _rel(g.grad, gr.grad) < 2 * _tol(dt)
+    # per-sample bias and its gradient
+    h = torch.randn(3, 8, 8, 64, device="cuda").to(dt).requires_grad_(True)
+    e = torch.randn(3, 64, device="cuda").to(dt).requires_grad_(True)
+    y = nn.add_row_bias(h, e)
+    assert _rel(y, h.float() + e.float()[:, None, None, :]) < _tol(dt)
+    y.backward(torch.ones_like(y))
+    assert _rel(e.grad, torch.full((3, 64), 64.0, device="cuda")) < _tol(dt)
+    # space_to_depth round trip
+    z = torch.randn(2, 8, 8, 4, device="cuda").to(dt)
+    assert torch.equal(ops.space_to_depth(ops.space_to_depth(z, 2), 2, inverse=True), z)
+    ref = z.view(2, 4, 2, 4, 2, 4).permute(0, 1, 3, 2, 4, 5).reshape(2, 4, 4, 16)
+    assert torch.equal(ops.space_to_depth(z, 2), ref)
+    # upsample
+    u = torch.randn(2, 4, 4, 64, device="cuda").to(dt)
+    up = ops.upsample2x(u)
+    assert torch.equal(up, u.repeat_interleave(2, 1).repeat_interleave(2, 2))
+    assert _rel(ops.upsample2x_bwd(up), 4 * u.float()) < _tol(dt)
+
+
+def test_adamw_matches_torch():
+    from paper_2405_01248_b200 import ops
+    n = 1000003
+    p = torch.randn(n, device="cuda")
+    g = torch.randn(n, device="cuda")
+    m = torch.zeros(n, device="cuda")
+    v = torch.zeros(n, device="cuda")
+    pb = torch.empty(n, device="cuda", dtype=torch.bfloat16)
+    pr = p.clone().requires_grad_(True)
+    opt = torch.optim.AdamW([pr], lr=1e-3, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01)
+    for step in range(1, 4):
+        ops.adamw(p, g, m, v, pb, 1e-3, 0.9, 0.999, 1e-8, 0.01, step)
+        pr.grad = g.clone()
+        opt.step()
+    assert _rel(p, pr.detach()) < 1e-6
+    assert torch.equal(pb, p.bfloat16())
+
+
+@pytest.mark.parametrize("dt", DT)
+def test_q_sample_mse(dt):
+    from paper_2405_01248_b200 import diffusion, ops
+    sab, s1m = [t.cuda() for t in diffusion.noise_schedule()]
+    x0 = torch.randn(4, 8, 8, 4, device="cuda").to(dt)
+    nz = torch.randn_like(x0)
+    t = torch.tensor([0, 10, 500, 999], device="cuda")
+    xt = ops.q_sample(x0, nz, t, sab, s1m)
+    ref = sab[t][:, None, None, None] * x0.float() + s1m[t][:, None, None, None] * nz.float()
+    assert _rel(xt, ref) < _tol(dt)
+    back = ops.pred_x0(xt, nz, t, sab, s1m)
+    assert _rel(back, x0.float()) < 5 * _tol(dt)
+    loss = torch.zeros(1, device="cuda")
+    dp = torch.empty_like(x0)
+    ops.mse(xt, nz, loss, 0.25, dp)
+    refl = 0.25 * ((xt.float() - nz.float()) ** 2).sum()
+    assert abs(loss.item() - refl.item()) <= 1e-4 * refl.item()
+    assert _rel(dp, 0.5 * (xt.float() - nz.float())) < _tol(dt)
