@@ -1,0 +1,327 @@
+"""Benchmark: pipelined diffusion training step (BASELINE.json metric
+"train samples/sec at 1/2/4/8 B200; bubble ratio; speedup vs unfilled 1F1B").
+
+    python bench.py --gpus N --steps K --warmup W [--impl ours|reference] [--config c2]
+    (N > 1: torchrun --nproc-per-node N ... bench.py --gpus N ...)
+
+Workload (configs[1] of BASELINE.json): SD v2.1 U-Net (865M, trainable) + frozen
+OpenCLIP ViT-H text encoder (23 layers) + frozen SD VAE encoder, 256 px, bf16
+compute with fp32 master weights / AdamW, synthetic data and random init.
+Per GPU 32 samples per iteration (weak scaling): world batch 32 N; N = 1 -> S = D = 1;
+N = 2 -> S = D = 2, M = 4; N = 4 -> S = D = 4, M = 4; N = 8 -> S = D = 4, M = 4, 2 groups.
+
+value  : world samples/s, inputs resident in HBM, device-timed (CUDA events) over exactly K
+         iterations after W warm-ups, max over ranks.
+e2e    : same metric through the public Trainer API with inputs in pinned host memory:
+         every step copies its batch slices H2D and reads the loss D2H (.item()).
+Every iteration also runs the frozen encoders for the next batch (cross-iteration fill /
+tail) and the AdamW step: nothing is skipped inside the timed region.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+METRIC = "train samples/sec"
+WORKLOAD = ("c2: SD v2.1 U-Net (trainable, 865M) + OpenCLIP ViT-H text (23 layers, frozen) + "
+            "SD VAE encoder (frozen), 256px, 32 samples/GPU/iteration")
+
+
+def layout(n):
+    if n == 1:
+        return dict(S=1, D=1, M=1)
+    if n == 2:
+        return dict(S=2, D=2, M=4)
+    if n == 4:
+        return dict(S=4, D=4, M=4)
+    if n == 8:
+        return dict(S=4, D=4, M=4)
+    S = min(n, 4)
+    return dict(S=S, D=S, M=4)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        load = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(n):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n:
+        raise SystemExit(f"--gpus {n} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return rank, world, local
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    t = torch.tensor([x], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.item()
+
+
+def barrier(world):
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def timed_steps(trainer, K, world, *, read_loss=False, kernel_timer=False):
+    from paper_2405_01248_b200 import telemetry
+
+    barrier(world)
+    telemetry.reset()
+    if kernel_timer:
+        telemetry.timer.start()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    losses = []
+    for _ in range(K):
+        loss = trainer.step()
+        if read_loss:
+            losses.append(trainer.ex.total_loss().item())
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    kstats = telemetry.timer.stop() if kernel_timer else None
+    launches = telemetry.total_launches()
+    barrier(world)
+    return max_over_ranks(ms, world), kstats, launches, losses
+
+
+def cpu_reference(steps, warmup, sample=1):
+    """The reference's CPU path for this workload: the sequential fp32 oracle training step
+    (oracle/train_step.py) on host cores, `sample` samples per step."""
+    from oracle import train_step
+    from paper_2405_01248_b200 import diffusion, networks, nn
+
+    torch.set_num_threads(os.cpu_count() or 1)
+    params = {}
+    for C in (networks.SDUNet, networks.SDVAEEncoder, networks.CLIPTextEncoder):
+        c = C()
+        params[c.name] = nn.init_state(c.store.param_specs(), 0)
+    ds = diffusion.DataSpec(2, sample, 256, 32, 4, 77, 49408, 1000, 0.0)
+    sab, s1m = diffusion.noise_schedule()
+    times = []
+    for i in range(warmup + steps):
+        batch = diffusion.make_batch(ds, i)
+        t0 = time.perf_counter()
+        train_step.train("c2", params, [batch], sab, s1m)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    return sample * len(times) / sum(times), torch.get_num_threads()
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    # bounded: each step is one sample (~20 s on 8 cores); cap the run at ~4 minutes
+    steps = max(1, min(args.steps, 8))
+    warm = 1 if args.warmup > 0 else 0
+    v, cores = cpu_reference(steps, warm)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
+            "steps": steps, "warmup": warm, "ms_per_step": 1000.0 / v, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "cpu_sample": "1 sample per step"},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
+                             "sample": f"{steps} steps x 1 sample of the c2 step (oracle/train_step.py, fp32)"},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--per-gpu-batch", type=int, default=32)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+    args.warmup = max(args.warmup, 3)
+
+    rank, world, local = dist_setup(args.gpus)
+    from paper_2405_01248_b200 import engine
+
+    lay = layout(world)
+    wb = args.per_gpu_batch * world
+    profile = None
+    if lay["S"] > 1:
+        from paper_2405_01248_b200 import profiling_run
+        profile = profiling_run.shared_profile("c2", world, rank, wb, **lay)
+    trainer = engine.Trainer.create("c2", world=world, rank=rank, world_batch=wb, profile=profile,
+                                    device=f"cuda:{local}", **lay)
+    W, K = args.warmup, args.steps
+    trainer.prefetch(W + K + 1, mode="device")
+    for _ in range(W):
+        trainer.step()
+    with Clocks(local) as clk:
+        ms, kstats, launches, _ = timed_steps(trainer, K, world, kernel_timer=True)
+    value = wb * K / (ms / 1000.0)
+
+    # speedup vs the same executor's unfilled pipeline (frozen part data-parallel, un-overlapped)
+    speedup = 1.0
+    if lay["S"] > 1:
+        unf = engine.Trainer.create("c2", world=world, rank=rank, world_batch=wb, profile=profile,
+                                    device=f"cuda:{local}", filled=False, **lay)
+        unf.prefetch(W + K + 1, mode="device")
+        for _ in range(W):
+            unf.step()
+        ms_u, _, _, _ = timed_steps(unf, K, world)
+        speedup = ms_u / ms
+        del unf
+
+    e2e = None
+    if not args.no_e2e:
+        trainer.feed_mode = "host"
+        trainer.prefetch(W + K + 1, mode="host")
+        for _ in range(2):
+            trainer.step()
+            trainer.ex.total_loss().item()
+        ms_e, _, _, _ = timed_steps(trainer, K, world, read_loss=True)
+        h2d = _h2d_bytes_per_step(trainer)
+        e2e = {"value": wb * K / (ms_e / 1000.0), "unit": "samples/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": 4}
+
+    pk, pk_kind = peaks()
+    roof = None
+    if kstats:
+        fam = max(kstats, key=lambda f: kstats[f]["ms"])
+        st = kstats[fam]
+        ach = st["flops"] / (st["ms"] / 1000.0) / 1e12
+        peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+        roof = {"bound": "tensor", "kernel": fam, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                "frac": ach / peak, "peak_kind": f"{pk_kind} bf16_tflops_sustained",
+                "traffic": _ncu_traffic(fam), "share_of_step": st["ms"] / ms,
+                "launches_per_step": st["launches"] / K,
+                "flops_per_launch": st["flops"] / max(1, st["launches"]),
+                "all_kernels": {f: {"ms_per_step": v["ms"] / K, "tflops": v["flops"] / max(v["ms"], 1e-9) / 1e9}
+                                for f, v in kstats.items()}}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores = cpu_reference(1, 0)
+        cpu = {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
+               "sample": "1 sample of the c2 training step on the CPU oracle (oracle/train_step.py, fp32)"}
+
+    if rank == 0:
+        res = trainer.ex.plan_result
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded), random init",
+            "config": {"workload": WORKLOAD, "world_batch": wb, "group_batch": wb * lay["D"] // world,
+                       "S": lay["S"], "M": lay["M"], "D": lay["D"], "groups": world // lay["D"],
+                       "parallelism": f"pp{lay['S']}xdp{world // lay['S']}",
+                       "l2": "working set (weights 1.7 GB bf16 + activations) >> 126 MB L2"},
+            "bubble_ratio_predicted_before": res["bubble_ratio_before"],
+            "bubble_ratio_predicted_after": res["bubble_ratio_after"],
+            "speedup_vs_unfilled": speedup,
+            "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _h2d_bytes_per_step(trainer):
+    """Bytes this rank copies host->device in one steady-state step (counted from the copies)."""
+    from paper_2405_01248_b200.engine import InputFeed
+
+    trainer.prefetch(2, mode="host")
+    before = InputFeed.h2d_total
+    trainer.step()
+    torch.cuda.synchronize()
+    return int(InputFeed.h2d_total - before)
+
+
+def _ncu_traffic(fam):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(fam)
+    except (OSError, ValueError):
+        return None
+
+
+if __name__ == "__main__":
+    main()

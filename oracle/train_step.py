@@ -39,22 +39,42 @@ def c1_forward(P, batch, sab, s1m):
     return loss, eps, dict(latent=x0, ctx=ctx, pooled=pooled)
 
 
+def c2_forward(P, batch, sab, s1m, clip_layers=23):
+    """Config c2 (SD v2.1 U-Net, frozen OpenCLIP-H text + SD VAE encoder, no self-cond)."""
+    Pu, Pv, Pt = P["unet"], P["vae"], P["text"]
+    img = batch.images.float()
+    img = torch.cat([img, torch.zeros(*img.shape[:-1], 5)], -1)  # RGB zero-padded to 8 channels
+    x0 = nets.vae_encoder(Pv, img, ch=128, mult=(1, 2, 4, 4), n_res=2)
+    ctx, _ = nets.text_encoder(Pt, batch.ids, heads=16, layers=clip_layers)
+    t = batch.t
+    a = sab[t][:, None, None, None]
+    b = s1m[t][:, None, None, None]
+    noise = batch.noise.float()
+    xt = a * x0 + b * noise
+    eps = nets.sd_unet(Pu, xt, t, ctx)
+    loss = ((eps - noise) ** 2).mean()
+    return loss, eps, dict(latent=x0, ctx=ctx)
+
+
+FORWARDS = {"c1": ("dit", c1_forward), "c2": ("unet", c2_forward)}
+
+
 def train(config, params, batches, sab, s1m, adamw=dict(lr=1e-4, betas=(0.9, 0.999), eps=1e-8,
-                                                         weight_decay=0.01)):
-    """Run len(batches) sequential iterations. params: {"dit"|"vae"|"text": {name: fp32}}.
+                                                         weight_decay=0.01), **kw):
+    """Run len(batches) sequential iterations. params: {backbone|"vae"|"text": {name: fp32}}.
     Returns per-iteration losses, the backbone gradients of every iteration and the final
     backbone parameters."""
-    assert config == "c1", config
+    bb, fwd = FORWARDS[config]
     P = {k: {n: v.detach().clone().float() for n, v in d.items()} for k, d in params.items()}
-    for v in P["dit"].values():
+    for v in P[bb].values():
         v.requires_grad_(True)
-    opt = torch.optim.AdamW(list(P["dit"].values()), **adamw)
+    opt = torch.optim.AdamW(list(P[bb].values()), **adamw)
     losses, grads = [], []
     for batch in batches:
         opt.zero_grad(set_to_none=False)
-        loss, _, _ = c1_forward(P, batch, sab, s1m)
+        loss, _, _ = fwd(P, batch, sab, s1m, **kw)
         loss.backward()
         losses.append(loss.item())
-        grads.append({n: v.grad.detach().clone() for n, v in P["dit"].items()})
+        grads.append({n: v.grad.detach().clone() for n, v in P[bb].items()})
         opt.step()
-    return losses, grads, {n: v.detach().clone() for n, v in P["dit"].items()}
+    return losses, grads, {n: v.detach().clone() for n, v in P[bb].items()}

@@ -151,7 +151,10 @@ def lib():
     return _lib
 
 
-def check(rc: int, what: str) -> None:
+def check(rc: int, what: str, kernels: int = 1) -> None:
+    from . import telemetry
+
+    telemetry.count(what, kernels)
     if rc != 0:
         msg = lib().dp_last_error().decode(errors="replace")
         raise DpipeError(f"{what} failed (code {rc}): {msg}")

@@ -84,7 +84,10 @@ def build_model(cfg: str | ConfigSpec, device="cuda", seed=0, states=None, small
 class InputFeed:
     """Batch fields for one iteration. mode 'device': the whole world batch is resident on
     the device (bench `value`); mode 'host': slices are copied from pinned host memory
-    when used (bench `e2e`), and the copied bytes are counted."""
+    when used (bench `e2e`), and the copied bytes are counted (per feed and globally in
+    InputFeed.h2d_total)."""
+
+    h2d_total = 0
 
     def __init__(self, batch, device, dtype, mode="device"):
         self.device = torch.device(device)
@@ -108,6 +111,7 @@ class InputFeed:
         if self.mode == "host":
             v = v.to(self.device, non_blocking=True)
             self.h2d_bytes += v.numel() * v.element_size()
+            InputFeed.h2d_total += v.numel() * v.element_size()
             v = self._cast(k, v)
         return v
 
@@ -184,7 +188,17 @@ class Trainer:
         t.profile = profile
         return t
 
+    def prefetch(self, n, mode=None):
+        """Pre-build the feeds of iterations [it, it + n] (device-resident or pinned host)
+        so that no batch synthesis happens inside a timed region."""
+        mode = mode or self.feed_mode
+        self._prefetched = {i: InputFeed(make_batch(self.data_spec, i), self.device, self.cfg.dtype, mode)
+                            for i in range(self.it, self.it + n + 1)}
+
     def _feed(self, i):
+        pre = getattr(self, "_prefetched", None)
+        if pre and i in pre:
+            return pre.pop(i)
         return InputFeed(make_batch(self.data_spec, i), self.device, self.cfg.dtype, self.feed_mode)
 
     def warmup_frozen(self):

@@ -11,7 +11,7 @@ import ctypes
 
 import torch
 
-from . import _lib
+from . import _lib, telemetry
 from ._lib import DP_BF16, DP_F32, DP_OUT_ATOMIC_ADD, DP_OUT_STORE, DpConvArgs, DpGemmArgs, check
 
 _DT = {torch.float32: DP_F32, torch.bfloat16: DP_BF16}
@@ -68,7 +68,9 @@ def gemm(A, B, D, *, M, N, K, a_ld, b_ld, d_ld, a_mn=False, b_mn=False,
     args.r_bs1, args.r_bs2 = d_bs if r_bs is None else r_bs
     args.alpha = alpha
     args.split_k = split_k
-    check(_lib.lib().dp_gemm(ctypes.byref(args), _stream()), "dp_gemm")
+    fam = "tcgen05_gemm" if A.dtype == torch.bfloat16 else "simt_gemm"
+    flops = 2.0 * M * N * K * max(1, batch[0]) * max(1, batch[1])
+    telemetry.timed(fam, flops, lambda: check(_lib.lib().dp_gemm(ctypes.byref(args), _stream()), "dp_gemm"))
     return D
 
 
@@ -165,7 +167,8 @@ def conv2d(x, w, *, stride=1, pad=(1, 1), out_hw=None, bias=None, residual=None,
                       out=out.view(-1, K)).view(N, P, Q, K)
     if implicit_ok(x, w, P, Q, stride):
         a = _conv_args(x, w, out, stride, pad, P, Q, bias, residual)
-        check(_lib.lib().dp_conv_fwd(ctypes.byref(a), _stream()), "dp_conv_fwd")
+        telemetry.timed("tcgen05_gemm", 2.0 * N * P * Q * K * R * S * C,
+                        lambda: check(_lib.lib().dp_conv_fwd(ctypes.byref(a), _stream()), "dp_conv_fwd"))
         return out
     cols = im2col(x, R, S, stride, pad, P, Q)
     linear(cols, w.reshape(K, -1), bias=bias,
@@ -207,7 +210,8 @@ def conv2d_dgrad(dy, w, x_shape, *, stride=1, pad=(1, 1)):
                                        _stream()), "dp_dilate")
         dx = torch.empty(N, H, W, C, device=dy.device, dtype=dy.dtype)
         a = _conv_args(src, wt, dx, 1, (R - 1 - pad[0], S - 1 - pad[1]), H, W)
-        check(_lib.lib().dp_conv_fwd(ctypes.byref(a), _stream()), "dp_conv_fwd(dgrad)")
+        telemetry.timed("tcgen05_gemm", 2.0 * N * H * W * C * R * S * K,
+                        lambda: check(_lib.lib().dp_conv_fwd(ctypes.byref(a), _stream()), "dp_conv_fwd(dgrad)"))
         return dx
     dcols = linear_dgrad(dy.reshape(-1, K), w.reshape(K, -1))
     dx = torch.zeros(N, H, W, C, device=dy.device, dtype=dy.dtype)
@@ -226,7 +230,8 @@ def conv2d_wgrad(dy, x, dw, *, stride=1, pad=(1, 1)):
         a = _conv_args(x, dw, dw, stride, pad, P, Q, accumulate=True)
         a.w = _ptr(dy)  # wgrad reads dy through the `w` slot (see dpipe.h)
         a.K, a.R, a.S = K, R, S
-        check(_lib.lib().dp_conv_wgrad(ctypes.byref(a), _stream()), "dp_conv_wgrad")
+        telemetry.timed("tcgen05_gemm", 2.0 * N * P * Q * K * R * S * C,
+                        lambda: check(_lib.lib().dp_conv_wgrad(ctypes.byref(a), _stream()), "dp_conv_wgrad"))
         return dw
     cols = im2col(x, R, S, stride, pad, P, Q)
     return linear_wgrad(dy.reshape(-1, K), cols, dw.view(K, -1))
@@ -398,7 +403,7 @@ def group_norm(x, gamma, beta, G, eps, silu):
     ws = _gn_ws(x.device, _L().dp_group_norm_workspace(N, HW, G))
     check(_L().dp_group_norm_fwd(dtype_code(x), _ptr(x), _ptr(gamma), _ptr(beta), _ptr(y), _ptr(mean),
                                  _ptr(rstd), N, HW, C, G, eps, int(silu), _ptr(ws), _stream()),
-          "dp_group_norm_fwd")
+          "dp_group_norm_fwd", 2)
     return y, mean, rstd
 
 
@@ -409,7 +414,7 @@ def group_norm_bwd(x, dy, gamma, beta, mean, rstd, G, silu, dgamma=None, dbeta=N
     ws = _gn_ws(x.device, _L().dp_group_norm_workspace(N, HW, G))
     check(_L().dp_group_norm_bwd(dtype_code(x), _ptr(x), _ptr(dy), _ptr(gamma), _ptr(beta), _ptr(mean),
                                  _ptr(rstd), _ptr(dx), _ptr(dgamma), _ptr(dbeta), N, HW, C, G, int(silu), 0,
-                                 _ptr(ws), _stream()), "dp_group_norm_bwd")
+                                 _ptr(ws), _stream()), "dp_group_norm_bwd", 2)
     return dx
 
 
@@ -433,7 +438,7 @@ def layer_norm_bwd(x, dy, gamma, mean, rstd, dgamma=None, dbeta=None, mod=None, 
     check(_L().dp_layer_norm_bwd(dtype_code(x), _ptr(x), _ptr(dy), _ptr(gamma), _ptr(mod), mod_ld,
                                  shift_off, scale_off, rows_per_sample, _ptr(mean), _ptr(rstd), _ptr(dx),
                                  _ptr(dgamma), _ptr(dbeta), _ptr(dmod), dmod_ld, rows, C, 0, _stream()),
-          "dp_layer_norm_bwd")
+          "dp_layer_norm_bwd", 1 + int(gamma is not None and dgamma is not None) + int(mod is not None and dmod is not None))
     return dx
 
 

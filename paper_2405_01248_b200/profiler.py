@@ -128,16 +128,15 @@ def _param_bytes(component, layer_idx):
 
 
 def measure_profile(model, live_specs, frozen_specs, make_state, *, group_batch, D, M, reps=3,
-                    device="cuda", key_filter=None):
+                    device="cuda", bb_keys=None, frozen_keys=None):
     """Measured per-layer costs on this GPU (CUDA events, median of `reps` after a warm-up).
 
     make_state(component_index or 'backbone', layer, batch) -> input state dict for that layer
     (random tensors of the probed shapes). Backward time of a backbone layer = time of
     torch.autograd.backward over its grad-carrying outputs with unit-random gradients.
     """
-    keys = _keys(group_batch, D, M)
-    if key_filter is not None:
-        keys = [k for k in keys if key_filter(k)]
+    keys = bb_keys or _keys(group_batch, D, M)
+    fkeys = frozen_keys or _keys(group_batch, D, M)
 
     def timed(fn):
         fn()
@@ -193,16 +192,16 @@ def measure_profile(model, live_specs, frozen_specs, make_state, *, group_batch,
         fl = []
         for j, fn in enumerate(f.component.layers):
             fwd = {}
-            for k in keys:
+            for k in fkeys:
                 st = make_state(c, j, k)
                 with torch.no_grad():
                     fwd[k] = timed(lambda: fn(dict(st)))
             spec = frozen_specs[c][j]
             ob = sum(math.prod(s) * torch.tensor([], dtype=dt).element_size() for s, dt in spec.values())
-            fl.append(LayerCost(fwd_time=fwd, bwd_time={k: 0.0 for k in keys},
-                                fwd_comm_bytes={k: ob * k for k in keys},
-                                bwd_comm_bytes={k: 0 for k in keys}, grad_bytes={k: 0 for k in keys},
-                                out_bytes={k: ob * k for k in keys}))
+            fl.append(LayerCost(fwd_time=fwd, bwd_time={k: 0.0 for k in fkeys},
+                                fwd_comm_bytes={k: ob * k for k in fkeys},
+                                bwd_comm_bytes={k: 0 for k in fkeys}, grad_bytes={k: 0 for k in fkeys},
+                                out_bytes={k: ob * k for k in fkeys}))
         frozen.append(ComponentProfile(name=getattr(f.component, "name", f"frozen{c}"), layers=fl,
                                        trainable=False))
     return ModelProfile(backbones=(backbone,), frozen=tuple(frozen), frozen_deps=(),
