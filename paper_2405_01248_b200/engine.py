@@ -169,22 +169,31 @@ class Trainer:
         world_batch = world_batch or 8 * world
         ds = DataSpec(c.config_id, world_batch, c.image, c.latent, 4, c.text_len, c.vocab, 1000,
                       c.selfcond_p)
+        return cls.from_model(model, c, ds, world=world, rank=rank, S=S, M=M, D=D, device=device,
+                              profile=profile, filled=filled, feed_mode=feed_mode,
+                              bubble_min_len=bubble_min_len)
+
+    @classmethod
+    def from_model(cls, model, cfg, ds, *, world=1, rank=0, S=1, M=1, D=1, device="cuda", profile=None,
+                   filled=True, feed_mode="device", bubble_min_len=0.010, comm=None):
+        """Plan and wire an already-built TrainModel (any component implementation)."""
+        world_batch = ds.world_batch
         probe = make_batch(replace(ds, world_batch=1), 10 ** 6)
-        pfeed = InputFeed(probe, device, c.dtype)
+        pfeed = InputFeed(probe, device, cfg.dtype)
         live, fspecs = probe_specs(model, lambda k: pfeed.get(k, 0, 1), device)
         counts = [len(f.component.layers) for f in model.frozen]
         if profile is None:
             profile = synthetic_profile(model, live, fspecs, group_batch=world_batch * D // world, D=D, M=M)
         res, programs, warm, unfilled = plan_programs(profile, world, S, M, D, world_batch, counts,
-                                                      bubble_min_len)
+                                                      bubble_min_len, comm)
         if not filled:
             programs = {False: unfilled, True: unfilled}
-        elems = c.latent * c.latent * 4
+        elems = ds.latent * ds.latent * ds.zc
         ex = PipelineExecutor(model, programs, rank=rank, world=world, device=device, live_specs=live,
                               frozen_specs=fspecs, loss_scale=1.0 / (world_batch * elems))
         ex.warm_program = warm
         ex.plan_result = res
-        t = cls(model, c, ex, ds, device, feed_mode)
+        t = cls(model, cfg, ex, ds, device, feed_mode)
         t.profile = profile
         return t
 

@@ -137,10 +137,17 @@ class Links:
             self.pg[key] = g
 
     def isend(self, kind, t, dst):
+        if _DEBUG:
+            print(f"[r{self.rank}] send {kind} -> {dst} {tuple(t.shape)}", flush=True)
         return dist.isend(t.contiguous(), dst=dst, group=self.pg[(kind, self.rank, dst)])
 
     def irecv(self, kind, t, src):
+        if _DEBUG:
+            print(f"[r{self.rank}] recv {kind} <- {src} {tuple(t.shape)}", flush=True)
         return dist.irecv(t, src=src, group=self.pg[(kind, src, self.rank)])
+
+
+_DEBUG = bool(int(__import__("os").environ.get("DP_DEBUG_P2P", "0")))
 
 
 # ============================================================================ executor
@@ -175,6 +182,7 @@ class PipelineExecutor:
         self.timeline = []       # (kind, micro, stage, ev_start, ev_end) when tracing
         self.trace = False
         self.grad_snapshots = None  # list -> flat grad slices captured before each AdamW
+        self._frz_sends = []        # in-flight frozen-activation sends (kept alive until deliver)
 
     # ---------------------------------------------------------------- setup
     def gb_of(self):
@@ -267,7 +275,8 @@ class PipelineExecutor:
             if (t.src == self.dev and t.comp == piece.comp and t.layer == piece.layer
                     and piece.lo <= t.lo and t.hi <= piece.hi and t.dst != self.dev):
                 for k in sorted(out):
-                    self.links.isend("frz", out[k][t.lo - piece.lo:t.hi - piece.lo], self._grank(t.dst))
+                    self._frz_sends.append(self.links.isend("frz", out[k][t.lo - piece.lo:t.hi - piece.lo],
+                                                            self._grank(t.dst)))
                 sent.add(t.seq)
 
     def _recv_frozen_upto(self, prog, store, need_seq, posted, stream_which):
@@ -324,8 +333,9 @@ class PipelineExecutor:
                 ready.setdefault(t.comp, []).append((t.lo, t.hi, bufs))
         for w in recvs:
             w.wait()
-        for w in sends:
+        for w in sends + self._frz_sends:
             w.wait()
+        self._frz_sends = []
         return ready
 
     def frozen_for(self, frozen_ready, lo, hi):

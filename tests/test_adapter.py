@@ -1,0 +1,91 @@
+"""Plan adapter (CPU): the per-device programs replay the reference planner's Schedule and
+FillPlan exactly — every simulated compute task once, in simulated order; every frozen
+(component, layer) covered over the whole group batch exactly once; fills placed in their
+bubbles; transfers and deliveries consistent with the pieces."""
+
+import random
+
+import pytest
+
+from paper_2405_01248_b200.adapter import build_group_program, split_range
+from paper_2405_01248_b200.pipefill import filler, planner, profile, scheduler
+
+
+def _profile(seed, L=8, frozen=(5, 3), p=0.0, keys=(1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64, 96, 128)):
+    rnd = random.Random(seed)
+
+    def layer(f, b, frozen_layer=False):
+        return profile.LayerCost(
+            fwd_time={k: f * k for k in keys}, bwd_time={k: (0.0 if frozen_layer else b * k) for k in keys},
+            fwd_comm_bytes={k: 1000 * k for k in keys}, bwd_comm_bytes={k: (0 if frozen_layer else 1000 * k) for k in keys},
+            grad_bytes={k: 0 if frozen_layer else 4000 for k in keys}, out_bytes={k: 100 * k for k in keys})
+
+    bb = profile.ComponentProfile("bb", [layer(rnd.uniform(0.5, 2) * 1e-3, rnd.uniform(1, 4) * 1e-3)
+                                         for _ in range(L)], True)
+    fr = [profile.ComponentProfile(f"f{i}", [layer(rnd.uniform(0.2, 1.5) * 1e-3, 0, True) for _ in range(n)],
+                                   False) for i, n in enumerate(frozen)]
+    return profile.ModelProfile((bb,), tuple(fr), (), p)
+
+
+@pytest.mark.parametrize("seed,S,M,D,p", [(0, 2, 4, 2, 0.0), (1, 4, 4, 4, 0.0), (2, 4, 8, 4, 0.0),
+                                          (3, 2, 4, 4, 0.0), (4, 4, 4, 4, 0.5), (5, 3, 6, 3, 0.0)])
+def test_programs_replay_schedule_and_fill(seed, S, M, D, p):
+    prof = _profile(seed, p=p)
+    cluster = profile.ClusterConfig(D, profile.CommCosts(2e11, 1e-5, 3e11, 1e-5))
+    res = planner.evaluate_point(prof, cluster, S, M, D, 64 * M // 4)
+    counts = [len(c.layers) for c in prof.frozen]
+    prog = build_group_program(res, counts)
+    B = prog.group_batch
+    # 1. compute tasks: exactly the schedule's, per device, in start order
+    sched = res["pre_fill_schedule"]
+    for dev in range(D):
+        want = [(t.kind, t.micro_batch, t.stage) for t in sorted(
+            (t for t in sched.tasks if t.device == dev and t.kind in ("fwd", "bwd", "fwd_sc")),
+            key=lambda t: (t.start, t.end))]
+        got = [i for i in prog.devices[dev].instrs if i[0] in ("fwd", "bwd", "fwd_sc")]
+        assert got == want
+        kinds = [i[0] for i in prog.devices[dev].instrs]
+        assert kinds[-1] == "deliver" and kinds.count("sync") == 1
+        last_bwd = max(k for k, i in enumerate(prog.devices[dev].instrs) if i[0] == "bwd")
+        assert prog.devices[dev].instrs[last_bwd + 1][0] == "sync"
+    # 2. frozen coverage: each (comp, layer) sample range covered exactly once
+    for c, n in enumerate(counts):
+        for layer in range(n):
+            cov = [0] * B
+            for ps in prog.fills + [prog.tail]:
+                for pc in ps:
+                    if pc.comp == c and pc.layer == layer:
+                        for s in range(pc.lo, pc.hi):
+                            cov[s] += 1
+            assert cov == [1] * B, (c, layer)
+    # 3. fill pieces run on the bubble's idle devices, sample counts match the FillPlan
+    for f, pieces in zip(res["fill"].fills, prog.fills):
+        assert {pc.device for pc in pieces} <= set(f.bubble.idle_devices)
+        per = {}
+        for pc in pieces:
+            per[(pc.comp, pc.layer)] = per.get((pc.comp, pc.layer), 0) + pc.hi - pc.lo
+        want = dict(f.full_samples)
+        if f.partial is not None:
+            key = (f.partial.component, f.partial.layer)
+            want[key] = want.get(key, 0) + f.partial.samples
+        assert per == {k: v for k, v in want.items() if v}
+    # 4. every fill instruction sits before compute tasks starting after its bubble
+    for dev in range(D):
+        tasks = sorted((t for t in sched.tasks if t.device == dev and t.kind in ("fwd", "bwd", "fwd_sc")),
+                       key=lambda t: (t.start, t.end))
+        k = 0
+        for ins in prog.devices[dev].instrs:
+            if ins[0] in ("fwd", "bwd", "fwd_sc"):
+                k += 1
+            if ins[0] == "fill":
+                b = res["fill"].fills[ins[1]].bubble
+                assert all(t.end <= b.start + 1e-12 for t in tasks[:k])
+                assert all(t.start >= b.end - 1e-12 for t in tasks[k:])
+    # 5. transfers move data between different devices, ordered by production
+    assert [t.seq for t in prog.transfers] == list(range(len(prog.transfers)))
+    assert all(t.src != t.dst for t in prog.transfers)
+
+
+def test_split_range():
+    assert split_range(0, 10, 3) == [(0, 3), (3, 6), (6, 10)]
+    assert split_range(5, 7, 4) == [(5, 5), (5, 6), (6, 6), (6, 7)]
