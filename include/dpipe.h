@@ -92,6 +92,10 @@ typedef struct DpConvArgs {
 int dp_gemm(const DpGemmArgs* args, dp_stream_t stream);
 /* y = conv(x, w) (+bias) (+Res); bf16 tensor-core implicit GEMM, needs C % 64 == 0 */
 int dp_conv_fwd(const DpConvArgs* args, dp_stream_t stream);
+/* input gradient of a stride-1 conv, weights read tap-flipped in place (no transposed copy):
+   N,H,W,C describe dx (= args->y), P,Q describe dy (= args->x), w the forward weights
+   [K][R][S][C], pad_h/pad_w the forward paddings; needs C % 64 == 0 and K % 64 == 0 */
+int dp_conv_dgrad(const DpConvArgs* args, dp_stream_t stream);
 /* w-grad: y is dW fp32 [K][R][S][C] (accumulated), x the layer input, w := dy [N][P][Q][K] */
 int dp_conv_wgrad(const DpConvArgs* args, dp_stream_t stream);
 

@@ -58,6 +58,7 @@ _SIGNATURES = {
     "dp_gemm": [ctypes.POINTER(DpGemmArgs), c_void_p],
     "dp_conv_fwd": [ctypes.POINTER(DpConvArgs), c_void_p],
     "dp_conv_wgrad": [ctypes.POINTER(DpConvArgs), c_void_p],
+    "dp_conv_dgrad": [ctypes.POINTER(DpConvArgs), c_void_p],
     "dp_im2col": [c_int, c_void_p, c_void_p] + [c_int] * 11 + [c_void_p],
     "dp_col2im": [c_int, c_void_p, c_void_p] + [c_int] * 11 + [c_void_p],
     "dp_conv_weight_flip": [c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p],

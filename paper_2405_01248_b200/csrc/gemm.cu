@@ -28,7 +28,7 @@ thread_local std::string g_last_error;
 void set_error(const std::string& s) { g_last_error = s; }
 
 enum { A_KMAJ = 0, A_MNMAJ = 1, A_CONV = 2, A_WG_DY = 3 };
-enum { B_KMAJ = 0, B_MNMAJ = 1, B_WG_X = 2 };
+enum { B_KMAJ = 0, B_MNMAJ = 1, B_WG_X = 2, B_DGRAD = 3 };
 
 struct TcParams {
   int M, N;
@@ -38,6 +38,7 @@ struct TcParams {
   int P, Q;        // output spatial dims (conv modes)
   int tw, th, tn;  // pixel box (128 pixels for A_CONV, 64 for the wgrad modes)
   int stride, pad_h, pad_w, S, cblk, C;
+  int Rf;          // filter height (B_DGRAD flips taps)
   void* D;
   int64_t d_ld, d_bs1, d_bs2;
   int d_f32, out_mode, vec_ok;
@@ -54,7 +55,9 @@ constexpr uint32_t A_STAGE_BYTES = BM * BK * 2;
 template <int BN>
 struct TcCfg {
   static constexpr uint32_t B_STAGE_BYTES = BN * BK * 2;
-  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  // as many 64-deep k-stages as fit in ~200 KB of shared memory (4 at BN=256, 8 at BN=64)
+  static constexpr int STAGES_FIT = 200 * 1024 / (A_STAGE_BYTES + B_STAGE_BYTES);
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256 ? 256 : 512);
   static constexpr size_t SMEM = 1024 + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 256;
 };
@@ -239,6 +242,18 @@ __global__ void __launch_bounds__(256, 1)
             for (int j = 0; j < BN / 64; ++j)
               tma_load_4d(&tmB, &full[stage], b_dst + j * 8192, n0 + 64 * j, kb * BK, z1, z2);
             break;
+          case B_DGRAD: {
+            // B(n = input channel c, k = (tap, filter kk)) = w[kk][R-1-r][S-1-s][c]: the conv
+            // weights [K][R][S][C] read tap-flipped in place (no transposed copy)
+            const int tap = kb / p.cblk;
+            const int kk = kb - tap * p.cblk;
+            const int rr = tap / p.S, ss = tap - (tap / p.S) * p.S;
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_4d(&tmB, &full[stage], b_dst + j * 8192, n0 + 64 * j, p.S - 1 - ss,
+                          p.Rf - 1 - rr, kk * BK);
+            break;
+          }
           default: {  // B_WG_X
             const int hin = ph * p.stride - p.pad_h, win = pw * p.stride - p.pad_w;
 #pragma unroll
@@ -425,18 +440,37 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, TcParams p, i
   return 0;
 }
 
-static int pick_bn(int N) {
-  if (N <= 64) return 64;
-  if (N <= 128) return 128;
-  const int t256 = (N + 255) / 256, t128 = (N + 127) / 128;
-  return (t256 * 256 - N <= t128 * 128 - N + 32) ? 256 : 128;
+// Tile width: minimise padded columns plus a per-tile overhead, e.g. N=320 -> 2 x 160,
+// N=2880 -> 13 x 224, N=1280 -> 5 x 256. MN-major B operands are loaded in 64-column TMA
+// boxes, so they only use multiples of 64.
+static int pick_bn(int N, bool b_mn_major) {
+  static const int kAll[] = {64, 96, 128, 160, 192, 224, 256};
+  static const int kMn[] = {64, 128, 192, 256};
+  const int* cand = b_mn_major ? kMn : kAll;
+  const int ncand = b_mn_major ? 4 : 7;
+  int best = 64;
+  long best_cost = -1;
+  for (int i = 0; i < ncand; ++i) {
+    const int bn = cand[i];
+    const long tiles = (N + bn - 1) / bn;
+    const long cost = tiles * bn + 24 * tiles;
+    if (best_cost < 0 || cost < best_cost || (cost == best_cost && bn > best)) {
+      best = bn;
+      best_cost = cost;
+    }
+  }
+  return best;
 }
 
 static int launch_bn(int bn, const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& p,
                      cudaStream_t st) {
   switch (bn) {
     case 64: return launch_tc<64>(ma, mb, p, kNumSMs, st);
+    case 96: return launch_tc<96>(ma, mb, p, kNumSMs, st);
     case 128: return launch_tc<128>(ma, mb, p, kNumSMs, st);
+    case 160: return launch_tc<160>(ma, mb, p, kNumSMs, st);
+    case 192: return launch_tc<192>(ma, mb, p, kNumSMs, st);
+    case 224: return launch_tc<224>(ma, mb, p, kNumSMs, st);
     default: return launch_tc<256>(ma, mb, p, kNumSMs, st);
   }
 }
@@ -488,7 +522,7 @@ int tc_gemm(const DpGemmArgs* a, cudaStream_t st) {
     set_error("atomic accumulation needs an fp32 output");
     return DP_ERR_ARGS;
   }
-  const int bn = pick_bn(a->N);
+  const int bn = pick_bn(a->N, a->b_mn_major != 0);
   TcParams p{};
   p.M = a->M;
   p.N = a->N;
@@ -571,7 +605,7 @@ int tc_conv_fwd(const DpConvArgs* a, cudaStream_t st) {
     set_error("output spatial size does not tile into 128-pixel boxes");
     return DP_ERR_UNSUPPORTED;
   }
-  const int bn = pick_bn(a->K);
+  const int bn = pick_bn(a->K, false);
   p.M = a->N * a->P * a->Q;
   p.N = a->K;
   p.cblk = a->C / 64;
@@ -612,6 +646,64 @@ int tc_conv_fwd(const DpConvArgs* a, cudaStream_t st) {
   return launch_bn(bn, ma, mb, p, st);
 }
 
+// Input gradient of a stride-1 convolution as an implicit GEMM over dy with the weights read
+// tap-flipped in place (B_DGRAD): dx[n][h][w][c] = sum_{kk,r,s} dy[n][h+r-(R-1-pad_h)]
+// [w+s-(S-1-pad_w)][kk] * w[kk][R-1-r][S-1-s][c]. Args: N,H,W,C describe dx, P,Q dy, x := dy,
+// w := weights [K][R][S][C], y := dx. Strided convolutions zero-dilate dy first (dp_dilate).
+int tc_conv_dgrad(const DpConvArgs* a, cudaStream_t st) {
+  if (a->C % 64 || a->K % 64) {
+    set_error("implicit dgrad needs C % 64 == 0 and K % 64 == 0");
+    return DP_ERR_UNSUPPORTED;
+  }
+  if (a->stride != 1) {
+    set_error("implicit dgrad is stride 1 (dilate dy for strided convolutions)");
+    return DP_ERR_UNSUPPORTED;
+  }
+  TcParams p{};
+  if (!pixel_box(a->H, a->W, BM, p.tw, p.th, p.tn)) {
+    set_error("input spatial size does not tile into 128-pixel boxes");
+    return DP_ERR_UNSUPPORTED;
+  }
+  const int bn = pick_bn(a->C, true);
+  p.M = a->N * a->H * a->W;
+  p.N = a->C;
+  p.cblk = a->K / 64;
+  p.num_kb = a->R * a->S * p.cblk;
+  p.tiles_m = (p.M + BM - 1) / BM;
+  p.tiles_n = (a->C + bn - 1) / bn;
+  p.batch1 = 1;
+  p.nbatch = 1;
+  p.a_mode = A_CONV;
+  p.b_mode = B_DGRAD;
+  p.P = a->H;
+  p.Q = a->W;
+  p.stride = 1;
+  p.pad_h = a->R - 1 - a->pad_h;
+  p.pad_w = a->S - 1 - a->pad_w;
+  p.S = a->S;
+  p.Rf = a->R;
+  p.C = a->C;
+  choose_split(p, a->split_k, a->out_mode == DP_OUT_ATOMIC_ADD);
+  fill_epilogue(p, a->y, a->dtype == DP_BF16 && a->out_mode != DP_OUT_ATOMIC_ADD ? DP_BF16 : DP_F32,
+                a->C, 0, 0, a->out_mode, nullptr, a->Res, a->C, 0, 0, a->alpha);
+  CUtensorMap ma, mb;
+  {
+    const uint64_t d[4] = {(uint64_t)a->K, (uint64_t)a->Q, (uint64_t)a->P, (uint64_t)a->N};
+    const int64_t s[3] = {a->K, (int64_t)a->Q * a->K, (int64_t)a->P * a->Q * a->K};
+    const uint32_t box[4] = {64, (uint32_t)p.tw, (uint32_t)p.th, (uint32_t)p.tn};
+    const uint32_t ones[4] = {1, 1, 1, 1};
+    if (int e = make_map(&ma, a->x, d, s, box, ones)) return e;
+  }
+  {
+    const uint64_t d[4] = {(uint64_t)a->C, (uint64_t)a->S, (uint64_t)a->R, (uint64_t)a->K};
+    const int64_t s[3] = {a->C, (int64_t)a->S * a->C, (int64_t)a->R * a->S * a->C};
+    const uint32_t box[4] = {64, 1, 1, BK};
+    const uint32_t ones[4] = {1, 1, 1, 1};
+    if (int e = make_map(&mb, a->w, d, s, box, ones)) return e;
+  }
+  return launch_bn(bn, ma, mb, p, st);
+}
+
 // dW[k][r][s][c] += sum_{n,p,q} dy[n][p][q][k] * x[n][p*stride+r-pad][q*stride+s-pad][c]
 int tc_conv_wgrad(const DpConvArgs* a, cudaStream_t st) {
   if (a->C % 64 || a->K % 64) {
@@ -624,7 +716,7 @@ int tc_conv_wgrad(const DpConvArgs* a, cudaStream_t st) {
     return DP_ERR_UNSUPPORTED;
   }
   const int Ntot = a->R * a->S * a->C;
-  const int bn = (Ntot % 256 == 0) ? 256 : (Ntot % 128 == 0 ? 128 : 64);
+  const int bn = pick_bn(Ntot, true);
   p.M = a->K;
   p.N = Ntot;
   p.num_kb = (a->N * a->P * a->Q + BK - 1) / BK;
@@ -779,6 +871,14 @@ int dp_conv_fwd(const DpConvArgs* a, dp_stream_t stream) {
   return dp::tc_conv_fwd(a, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int dp_conv_dgrad(const DpConvArgs* a, dp_stream_t stream) {
+  if (a->dtype != DP_BF16) {
+    dp::set_error("dp_conv_dgrad is the bf16 tensor-core path");
+    return DP_ERR_UNSUPPORTED;
+  }
+  return dp::tc_conv_dgrad(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
 int dp_conv_wgrad(const DpConvArgs* a, dp_stream_t stream) {
   if (a->dtype != DP_BF16) {
     dp::set_error("dp_conv_wgrad is the bf16 tensor-core path");
@@ -788,6 +888,6 @@ int dp_conv_wgrad(const DpConvArgs* a, dp_stream_t stream) {
 }
 
 const char* dp_last_error(void) { return dp::g_last_error.c_str(); }
-int dp_version(void) { return 1; }
+int dp_version(void) { return 2; }
 
 }  // extern "C"

@@ -126,16 +126,6 @@ def _conv_args(x, w, y, stride, pad, P, Q, bias=None, residual=None, accumulate=
     return a
 
 
-def implicit_ok(x, w, P, Q, stride):
-    """Can the tcgen05 implicit-GEMM path run this conv (else im2col lowering)."""
-    if x.dtype != torch.bfloat16:
-        return False
-    C = x.shape[3]
-    if C % 64 or stride not in (1, 2):
-        return False
-    return _tiles(P, Q, 128) and _tiles(P, Q, 64)
-
-
 def _tiles(P, Q, pixels):
     if Q >= pixels:
         return Q % pixels == 0
@@ -146,11 +136,41 @@ def _tiles(P, Q, pixels):
     return pixels % (P * Q) == 0
 
 
+def _pad_last(t, mult=64):
+    """Zero-pad the channel (last) dim to a multiple of `mult` (small convs such as the U-Net's
+    4-channel conv_in/conv_out go through the same tensor-core implicit GEMM)."""
+    C = t.shape[-1]
+    pad = -C % mult
+    if not pad:
+        return t
+    z = torch.zeros(*t.shape[:-1], pad, device=t.device, dtype=t.dtype)
+    return concat_last(t.contiguous(), z)
+
+
+def _pad_first(w, mult=64):
+    K = w.shape[0]
+    pad = -K % mult
+    if not pad:
+        return w
+    out = torch.zeros(K + pad, *w.shape[1:], device=w.device, dtype=w.dtype)
+    out[:K].copy_(w)
+    return out
+
+
+def _take_last(t, C):
+    if t.shape[-1] == C:
+        return t
+    out = torch.empty(*t.shape[:-1], C, device=t.device, dtype=t.dtype)
+    split_last(t, C, out, None)
+    return out
+
+
 def conv2d(x, w, *, stride=1, pad=(1, 1), out_hw=None, bias=None, residual=None, out=None):
     """NHWC conv: x [N,H,W,C], w [K,R,S,C] -> y [N,P,Q,K].
 
     pad is (top, left); bottom/right padding is implied by out_hw (default:
-    symmetric padding).
+    symmetric padding). bf16: tcgen05 implicit GEMM (channels zero-padded to 64 when
+    needed); fp32 (parity config): im2col + fp32 GEMM.
     """
     _require_cuda(x, w, bias, residual)
     N, H, W, C = x.shape
@@ -165,8 +185,10 @@ def conv2d(x, w, *, stride=1, pad=(1, 1), out_hw=None, bias=None, residual=None,
         return linear(x.reshape(-1, C), w.reshape(K, C), bias=bias,
                       residual=None if residual is None else residual.reshape(-1, K),
                       out=out.view(-1, K)).view(N, P, Q, K)
-    if implicit_ok(x, w, P, Q, stride):
-        a = _conv_args(x, w, out, stride, pad, P, Q, bias, residual)
+    if x.dtype == torch.bfloat16 and stride in (1, 2) and _tiles(P, Q, 128):
+        xp, wp = _pad_last(x), _pad_last(w)
+        Cp = xp.shape[-1]
+        a = _conv_args(xp, wp, out, stride, pad, P, Q, bias, residual)
         telemetry.timed("tcgen05_gemm", 2.0 * N * P * Q * K * R * S * C,
                         lambda: check(_lib.lib().dp_conv_fwd(ctypes.byref(a), _stream()), "dp_conv_fwd"))
         return out
@@ -192,27 +214,30 @@ def col2im(cols, dx, R, S, stride, pad, P, Q):
 
 
 def conv2d_dgrad(dy, w, x_shape, *, stride=1, pad=(1, 1)):
-    """dx [N,H,W,C] of y = conv2d(x, w)."""
+    """dx [N,H,W,C] of y = conv2d(x, w). bf16: implicit GEMM over dy (zero-dilated for
+    stride 2) with the weights read tap-flipped in place (dp_conv_dgrad)."""
     _require_cuda(dy, w)
     N, P, Q, K = dy.shape
     K2, R, S, C = w.shape
     _, H, W, _ = x_shape
     if R == 1 and S == 1 and stride == 1 and pad == (0, 0):
         return linear_dgrad(dy.reshape(-1, K), w.reshape(K, C)).view(N, H, W, C)
-    if dy.dtype == torch.bfloat16 and K % 64 == 0 and _tiles(H, W, 128) and _tiles(H, W, 64):
-        wt = torch.empty(C, R, S, K, device=w.device, dtype=w.dtype)
-        check(_lib.lib().dp_conv_weight_flip(dtype_code(w), _ptr(w), _ptr(wt), K, R, S, C,
-                                             _stream()), "dp_conv_weight_flip")
-        src = dy
+    if dy.dtype == torch.bfloat16 and _tiles(H, W, 128):
+        src = _pad_last(dy)
+        Kp = src.shape[-1]
+        wp = _pad_first(_pad_last(w))
+        Cp = wp.shape[-1]
         if stride > 1:
-            src = torch.empty(N, P * stride, Q * stride, K, device=dy.device, dtype=dy.dtype)
-            check(_lib.lib().dp_dilate(dtype_code(dy), _ptr(dy), _ptr(src), N, P, Q, K, stride,
+            dil = torch.empty(N, P * stride, Q * stride, Kp, device=dy.device, dtype=dy.dtype)
+            check(_lib.lib().dp_dilate(dtype_code(dy), _ptr(src), _ptr(dil), N, P, Q, Kp, stride,
                                        _stream()), "dp_dilate")
-        dx = torch.empty(N, H, W, C, device=dy.device, dtype=dy.dtype)
-        a = _conv_args(src, wt, dx, 1, (R - 1 - pad[0], S - 1 - pad[1]), H, W)
+            src = dil
+        dx = torch.empty(N, H, W, Cp, device=dy.device, dtype=dy.dtype)
+        a = _conv_args(dx, wp, dx, 1, pad, src.shape[1], src.shape[2])
+        a.x = _ptr(src)
         telemetry.timed("tcgen05_gemm", 2.0 * N * H * W * C * R * S * K,
-                        lambda: check(_lib.lib().dp_conv_fwd(ctypes.byref(a), _stream()), "dp_conv_fwd(dgrad)"))
-        return dx
+                        lambda: check(_lib.lib().dp_conv_dgrad(ctypes.byref(a), _stream()), "dp_conv_dgrad"))
+        return _take_last(dx, C)
     dcols = linear_dgrad(dy.reshape(-1, K), w.reshape(K, -1))
     dx = torch.zeros(N, H, W, C, device=dy.device, dtype=dy.dtype)
     return col2im(dcols, dx, R, S, stride, pad, P, Q)
@@ -226,12 +251,18 @@ def conv2d_wgrad(dy, x, dw, *, stride=1, pad=(1, 1)):
     _, R, S, _ = dw.shape
     if R == 1 and S == 1 and stride == 1 and pad == (0, 0):
         return linear_wgrad(dy.reshape(-1, K), x.reshape(-1, C), dw.view(K, C))
-    if dy.dtype == torch.bfloat16 and C % 64 == 0 and K % 64 == 0 and _tiles(P, Q, 64):
-        a = _conv_args(x, dw, dw, stride, pad, P, Q, accumulate=True)
-        a.w = _ptr(dy)  # wgrad reads dy through the `w` slot (see dpipe.h)
-        a.K, a.R, a.S = K, R, S
+    if dy.dtype == torch.bfloat16 and _tiles(P, Q, 64):
+        dyp, xp = _pad_last(dy), _pad_last(x)
+        Kp, Cp = dyp.shape[-1], xp.shape[-1]
+        tgt = dw if (Kp == K and Cp == C) else torch.zeros(Kp, R, S, Cp, device=dw.device,
+                                                           dtype=torch.float32)
+        a = _conv_args(xp, tgt, tgt, stride, pad, P, Q, accumulate=True)
+        a.w = _ptr(dyp)  # wgrad reads dy through the `w` slot (see dpipe.h)
+        a.K, a.R, a.S = Kp, R, S
         telemetry.timed("tcgen05_gemm", 2.0 * N * P * Q * K * R * S * C,
                         lambda: check(_lib.lib().dp_conv_wgrad(ctypes.byref(a), _stream()), "dp_conv_wgrad"))
+        if tgt is not dw:
+            dw.add_(tgt[:K, :, :, :C])
         return dw
     cols = im2col(x, R, S, stride, pad, P, Q)
     return linear_wgrad(dy.reshape(-1, K), cols, dw.view(K, -1))

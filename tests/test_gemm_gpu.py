@@ -113,6 +113,10 @@ def _conv_ref(x, w, stride, pad, out_hw):
     (2, 32, 128, 128, 2, (1, 1)),
     (2, 64, 128, 128, 2, (0, 0)),
     (1, 256, 64, 64, 1, (1, 1)),
+    (4, 32, 4, 320, 1, (1, 1)),      # U-Net conv_in (channels zero-padded to 64)
+    (4, 32, 320, 4, 1, (1, 1)),      # U-Net conv_out (4 filters)
+    (2, 64, 8, 128, 1, (1, 1)),      # VAE conv_in (RGB padded to 8)
+    (2, 16, 192, 320, 1, (1, 1)),    # C not a multiple of 64
 ])
 def test_conv_implicit(N, H, C, K, stride, pad):
     ops = _ops()
