@@ -89,7 +89,32 @@ typedef struct DpConvArgs {
   int split_k;
 } DpConvArgs;
 
+/* Multi-head attention over strided [B][N][heads*head_dim] activations (q, k, v may be
+   column slices of one fused qkv / kv tensor). Strides in elements: *_ld between tokens,
+   *_bs between batch entries. lse (optional) receives [B][heads][N] log2-domain
+   log-sum-exp (m + log2 l) of the scaled scores. */
+typedef struct DpAttnArgs {
+  int dtype;
+  int B, N, Nk, heads, head_dim;
+  const void* q;
+  const void* k;
+  const void* v;
+  void* o;
+  int64_t q_ld, q_bs, kv_ld, kv_bs, o_ld, o_bs;
+  float scale;
+  float* lse;
+} DpAttnArgs;
+
 int dp_gemm(const DpGemmArgs* args, dp_stream_t stream);
+/* fused attention forward (tcgen05 S = QK^T and O = PV, online softmax from TMEM);
+   bf16, head_dim 64 */
+int dp_flash_attn_fwd(const DpAttnArgs* args, dp_stream_t stream);
+/* fused attention backward (recomputes P from args->lse): dq (token stride dq_ld), dk/dv
+   (token stride dkv_ld) for the o written by dp_flash_attn_fwd; workspace holds
+   B*heads*N + B*N*heads*64 floats */
+int dp_flash_attn_bwd(const DpAttnArgs* args, const void* dout, int64_t do_ld, void* dq,
+                      int64_t dq_ld, void* dk, void* dv, int64_t dkv_ld, float* workspace,
+                      dp_stream_t stream);
 /* y = conv(x, w) (+bias) (+Res); bf16 tensor-core implicit GEMM, needs C % 64 == 0 */
 int dp_conv_fwd(const DpConvArgs* args, dp_stream_t stream);
 /* input gradient of a stride-1 conv, weights read tap-flipped in place (no transposed copy):

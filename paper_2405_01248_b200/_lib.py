@@ -53,12 +53,24 @@ class DpConvArgs(ctypes.Structure):
     ]
 
 
+class DpAttnArgs(ctypes.Structure):
+    _fields_ = [
+        ("dtype", c_int), ("B", c_int), ("N", c_int), ("Nk", c_int), ("heads", c_int), ("head_dim", c_int),
+        ("q", c_void_p), ("k", c_void_p), ("v", c_void_p), ("o", c_void_p),
+        ("q_ld", c_i64), ("q_bs", c_i64), ("kv_ld", c_i64), ("kv_bs", c_i64), ("o_ld", c_i64), ("o_bs", c_i64),
+        ("scale", c_float), ("lse", c_void_p),
+    ]
+
+
 # name -> argtypes (restype is always c_int unless listed in _RESTYPES)
 _SIGNATURES = {
     "dp_gemm": [ctypes.POINTER(DpGemmArgs), c_void_p],
     "dp_conv_fwd": [ctypes.POINTER(DpConvArgs), c_void_p],
     "dp_conv_wgrad": [ctypes.POINTER(DpConvArgs), c_void_p],
     "dp_conv_dgrad": [ctypes.POINTER(DpConvArgs), c_void_p],
+    "dp_flash_attn_fwd": [ctypes.POINTER(DpAttnArgs), c_void_p],
+    "dp_flash_attn_bwd": [ctypes.POINTER(DpAttnArgs), c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_void_p,
+                          c_i64, c_void_p, c_void_p],
     "dp_im2col": [c_int, c_void_p, c_void_p] + [c_int] * 11 + [c_void_p],
     "dp_col2im": [c_int, c_void_p, c_void_p] + [c_int] * 11 + [c_void_p],
     "dp_conv_weight_flip": [c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p],
@@ -137,8 +149,15 @@ def _bind(lib, name):
 
 
 def lib():
-    """Load libdpipe.so once; raise loudly when it is missing."""
+    """Load libdpipe.so once; raise loudly when it is missing. While the bench's kernel timer
+    is active, calls go through a proxy that brackets each launch with CUDA events."""
     global _lib
+    if _lib is not None:
+        from . import telemetry
+
+        if telemetry.timer.active:
+            return telemetry.TimedLib(_lib)
+        return _lib
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise DpipeError(

@@ -1,0 +1,620 @@
+// Fused multi-head attention forward for sm_100a (head dim 64), K4 in SURVEY §2.4.
+//
+// One CTA = one 128-query tile of one (batch, head); 4 warps, thread t owns query row t.
+//   * TMA loads Q once and streams 128-key K/V tiles (K double-buffered, V single-buffered)
+//     from the strided [B, N, heads*64] activations (fused qkv / kv tensors, no copies);
+//   * thread 0 issues tcgen05.mma: S = Q K^T into TMEM (128 fp32 columns), then
+//     O_j = P V_j into TMEM (64 columns) with P read from shared memory;
+//   * all 128 threads run the online softmax on their S row straight from TMEM
+//     (tcgen05.ld), write P = exp2(S*scale*log2e - m) as bf16 into the SWIZZLE_128B K-major
+//     layout the MMA reads, and accumulate O in registers with the running rescale;
+//   * epilogue: O / l staged through shared memory and written by one TMA tensor store,
+//     log-sum-exp saved for the backward pass.
+// Two CTAs fit per SM (96 KB shared memory, 256 TMEM columns each), so one CTA's softmax
+// overlaps the other's MMAs. Keys beyond N_k (cross-attention, 77 tokens) are masked.
+#include <string>
+#include <cudaTypedefs.h>
+#include "common.cuh"
+#include "dpipe.h"
+
+namespace dp {
+void set_error(const std::string& s);
+
+namespace fa {
+
+constexpr int BQ = 128, BKV = 128, HD = 64;
+constexpr uint32_t TILE_BYTES = BQ * HD * 2;  // 16 KB: Q, K or V tile (128 rows x 128 B)
+
+struct Params {
+  int N, Nk, heads;
+  float scale_log2;  // softmax scale * log2(e)
+  float* lse;        // [B][heads][N] (log2 domain: m + log2(l))
+};
+
+DP_DEV float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+DP_DEV void tma_load_4d_(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2,
+                         int c3) {
+  tma_load_4d(map, bar, dst, c0, c1, c2, c3);
+}
+
+__global__ void __launch_bounds__(128, 2)
+    fa_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                  const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + TILE_BYTES;          // 2 buffers
+  uint8_t* sV = sK + 2 * TILE_BYTES;      // 1 buffer
+  uint8_t* sP = sV + TILE_BYTES;          // 2 x 16 KB (keys 0-63, 64-127)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 2 * TILE_BYTES);
+  uint64_t* bar_q = bar;
+  uint64_t* bar_k = bar + 1;  // [2]
+  uint64_t* bar_v = bar + 3;
+  uint64_t* bar_s = bar + 4;
+  uint64_t* bar_o = bar + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 6);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int q0 = qt * BQ;
+  const int ntiles = (p.Nk + BKV - 1) / BKV;
+
+  if (tid == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    for (int i = 0; i < 6; ++i) mbar_init(&bar[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s = tmem;          // S: columns [0, 128)
+  const uint32_t t_o = tmem + 128;    // O_j: columns [128, 192)
+  const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+
+  if (tid == 0) {
+    mbar_expect_tx(bar_q, TILE_BYTES);
+    tma_load_4d_(&tmQ, bar_q, sQ, 0, q0, h, b);
+    mbar_expect_tx(&bar_k[0], TILE_BYTES);
+    tma_load_4d_(&tmK, &bar_k[0], sK, 0, 0, h, b);
+    mbar_expect_tx(bar_v, TILE_BYTES);
+    tma_load_4d_(&tmV, bar_v, sV, 0, 0, h, b);
+    if (ntiles > 1) {
+      mbar_expect_tx(&bar_k[1], TILE_BYTES);
+      tma_load_4d_(&tmK, &bar_k[1], sK + TILE_BYTES, 0, BKV, h, b);
+    }
+  }
+  const uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, 0, 0);
+  const uint32_t idesc_o = idesc_bf16_f32(BQ, HD, 0, 1);
+
+  float o[HD];
+#pragma unroll
+  for (int i = 0; i < HD; ++i) o[i] = 0.f;
+  float m_run = -INFINITY, l_run = 0.f;
+  const int row = tid;  // query row inside the tile
+
+  for (int j = 0; j < ntiles; ++j) {
+    const int kb = j & 1;
+    if (tid == 0) {
+      if (j == 0) mbar_wait(bar_q, 0);
+      mbar_wait(&bar_k[kb], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t qa = smem_u32(sQ), ka = smem_u32(sK + kb * TILE_BYTES);
+#pragma unroll
+      for (int k = 0; k < HD / 16; ++k)
+        tc_mma_bf16(t_s, smem_desc_sw128(qa + k * 32, 16, 1024), smem_desc_sw128(ka + k * 32, 16, 1024),
+                    idesc_s, k > 0 ? 1u : 0u);
+      tc_commit(bar_s);
+    }
+    mbar_wait(bar_s, j & 1);
+    tc_fence_after();
+    const int valid = min(BKV, p.Nk - j * BKV);
+    // pass 1: row max of the scaled scores
+    float mx = -INFINITY;
+#pragma unroll 1
+    for (int c = 0; c < BKV / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32(t_s + lane_off + c * 32, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (c * 32 + i < valid) mx = fmaxf(mx, __uint_as_float(v[i]));
+    }
+    const float m_new = fmaxf(m_run, mx * p.scale_log2);
+    const float alpha = ex2(m_run - m_new);
+    // pass 2: P = exp2(s*scale - m) -> bf16 -> shared (SWIZZLE_128B K-major rows)
+    float lsum = 0.f;
+#pragma unroll 1
+    for (int c = 0; c < BKV / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32(t_s + lane_off + c * 32, v);
+      tmem_ld_wait();
+      float pv[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float e = (c * 32 + i < valid) ? ex2(fmaf(__uint_as_float(v[i]), p.scale_log2, -m_new)) : 0.f;
+        pv[i] = e;
+        lsum += e;
+      }
+      uint8_t* blk = sP + (c >> 1) * TILE_BYTES + row * 128;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int chunk = (c & 1) * 4 + q;  // 16-byte chunk of the 128-byte row
+        uint4 u;
+        u.x = pack_bf16x2(pv[q * 8 + 0], pv[q * 8 + 1]);
+        u.y = pack_bf16x2(pv[q * 8 + 2], pv[q * 8 + 3]);
+        u.z = pack_bf16x2(pv[q * 8 + 4], pv[q * 8 + 5]);
+        u.w = pack_bf16x2(pv[q * 8 + 6], pv[q * 8 + 7]);
+        *reinterpret_cast<uint4*>(blk + ((chunk ^ (row & 7)) * 16)) = u;
+      }
+    }
+    fence_async_shared();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      // S MMA of tile j has completed (bar_s), so K buffer kb can be refilled
+      if (j + 2 < ntiles) {
+        mbar_expect_tx(&bar_k[kb], TILE_BYTES);
+        tma_load_4d_(&tmK, &bar_k[kb], sK + kb * TILE_BYTES, 0, (j + 2) * BKV, h, b);
+      }
+      mbar_wait(bar_v, j & 1);
+      tc_fence_after();
+      const uint32_t pa = smem_u32(sP), va = smem_u32(sV);
+#pragma unroll
+      for (int k = 0; k < BKV / 16; ++k) {
+        const uint64_t ad = smem_desc_sw128(pa + (k >> 2) * TILE_BYTES + (k & 3) * 32, 16, 1024);
+        const uint64_t bd = smem_desc_sw128(va + k * 2048, 8192, 1024);
+        tc_mma_bf16(t_o, ad, bd, idesc_o, k > 0 ? 1u : 0u);
+      }
+      tc_commit(bar_o);
+    }
+    mbar_wait(bar_o, j & 1);
+    tc_fence_after();
+    if (tid == 0 && j + 1 < ntiles) {
+      mbar_expect_tx(bar_v, TILE_BYTES);
+      tma_load_4d_(&tmV, bar_v, sV, 0, (j + 1) * BKV, h, b);
+    }
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32(t_o + lane_off + c * 32, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[c * 32 + i] = fmaf(o[c * 32 + i], alpha, __uint_as_float(v[i]));
+    }
+    l_run = l_run * alpha + lsum;
+    m_run = m_new;
+    tc_fence_before();
+    __syncthreads();
+  }
+
+  // epilogue: O / l -> shared (SWIZZLE_128B rows of 64 bf16) -> one TMA store
+  const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+  uint8_t* so = sP;  // the P buffer is free: the last PV MMA completed
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    uint4 u;
+    u.x = pack_bf16x2(o[q * 8 + 0] * inv, o[q * 8 + 1] * inv);
+    u.y = pack_bf16x2(o[q * 8 + 2] * inv, o[q * 8 + 3] * inv);
+    u.z = pack_bf16x2(o[q * 8 + 4] * inv, o[q * 8 + 5] * inv);
+    u.w = pack_bf16x2(o[q * 8 + 6] * inv, o[q * 8 + 7] * inv);
+    *reinterpret_cast<uint4*>(so + row * 128 + ((q ^ (row & 7)) * 16)) = u;
+  }
+  if (p.lse && q0 + row < p.N)
+    p.lse[((int64_t)b * p.heads + h) * p.N + q0 + row] = m_run + log2f(l_run);
+  fence_async_shared();
+  __syncthreads();
+  if (tid == 0) {
+    tma_store_4d(&tmO, so, 0, q0, h, b);
+    bulk_commit();
+    bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
+constexpr size_t SMEM = 1024 + 6 * TILE_BYTES + 64;
+
+// ------------------------------------------------------------------ backward
+// D[b][h][n] = sum_d dO[b][n][h*64+d] * O[b][n][h*64+d]   (one warp per (b, n, h) row)
+__global__ void fa_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                                   float* __restrict__ Dv, int B, int N, int heads, int64_t o_ld,
+                                   int64_t do_ld) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = blockIdx.x * 8LL + (threadIdx.x >> 5);  // (b, h, n) flattened
+  const int64_t total = (int64_t)B * heads * N;
+  if (r >= total) return;
+  const int n = static_cast<int>(r % N);
+  const int64_t bh = r / N;
+  const int h = static_cast<int>(bh % heads);
+  const int b = static_cast<int>(bh / heads);
+  const __nv_bfloat16* op = o + ((int64_t)b * N + n) * o_ld + h * HD;
+  const __nv_bfloat16* dp = dout + ((int64_t)b * N + n) * do_ld + h * HD;
+  const __nv_bfloat162 a = reinterpret_cast<const __nv_bfloat162*>(op)[lane];
+  const __nv_bfloat162 c = reinterpret_cast<const __nv_bfloat162*>(dp)[lane];
+  float s = __bfloat162float(a.x) * __bfloat162float(c.x) + __bfloat162float(a.y) * __bfloat162float(c.y);
+  s = warp_sum(s);
+  if (lane == 0) Dv[r] = s;
+}
+
+// out[b][n][h*64+d] (bf16, token stride out_ld) = alpha * acc[b][n][h][d] (fp32, dense)
+__global__ void fa_dq_cast_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ out,
+                                  int64_t rows, int C, int64_t out_ld, float alpha) {
+  const int64_t n = rows * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n / 2;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = 2 * i;
+    const int64_t r = e / C;
+    const int c = static_cast<int>(e - r * C);
+    const float2 v = reinterpret_cast<const float2*>(acc)[i];
+    reinterpret_cast<__nv_bfloat162*>(out + r * out_ld + c)[0] = __floats2bfloat162_rn(alpha * v.x, alpha * v.y);
+  }
+}
+
+struct BwdParams {
+  int N, Nk, heads;
+  float scale_log2;   // softmax scale * log2(e)
+  float scale;        // softmax scale (dS -> dS_raw)
+  const float* lse;   // [B][heads][N]
+  const float* Dv;    // [B][heads][N]
+  float* dq_acc;      // [B][N][heads][64] fp32, zero-initialised
+};
+
+// One CTA = one 128-key tile of one (batch, head); thread t owns key row t (S^T, dP^T rows).
+// Per 128-query tile: S^T = K Q^T, dP^T = V dO^T (TMEM); P^T = exp2(S^T*sl - lse),
+// dS^T = P^T (dP^T - D) -> shared (bf16, K-major over queries); dV += P^T dO, dK += dS^T Q
+// (TMEM accumulators across query tiles), dQ_i = dS K (TMEM) -> fp32 atomics into dq_acc.
+constexpr uint32_t BWD_SMEM_TILES = 10;  // K, V, Q[2], dO[2], P^T (2), dS^T (2)
+
+__global__ void __launch_bounds__(128, 1)
+    fa_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                  const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmDV,
+                  const BwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + TILE_BYTES;
+  uint8_t* sQ = sV + TILE_BYTES;        // [2]
+  uint8_t* sDO = sQ + 2 * TILE_BYTES;   // [2]
+  uint8_t* sPT = sDO + 2 * TILE_BYTES;  // 2 blocks (queries 0-63, 64-127)
+  uint8_t* sDST = sPT + 2 * TILE_BYTES; // 2 blocks
+  float* sLse = reinterpret_cast<float*>(sDST + 2 * TILE_BYTES);  // [2][128]
+  float* sD = sLse + 256;                                          // [2][128]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sD + 256);
+  uint64_t* bar_kv = bar;
+  uint64_t* bar_q = bar + 1;   // [2]
+  uint64_t* bar_sp = bar + 3;
+  uint64_t* bar_acc = bar + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 5);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int kt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int k0 = kt * BKV;
+  const int nq = (p.N + BQ - 1) / BQ;
+  const int64_t bh = (int64_t)b * p.heads + h;
+
+  if (tid == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmDO);
+    for (int i = 0; i < 5; ++i) mbar_init(&bar[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_st = tmem, t_dpt = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 320, t_dq = tmem + 384;
+  const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+
+  auto load_q = [&](int i, int buf) {
+    mbar_expect_tx(&bar_q[buf], 2 * TILE_BYTES);
+    tma_load_4d(&tmQ, &bar_q[buf], sQ + buf * TILE_BYTES, 0, i * BQ, h, b);
+    tma_load_4d(&tmDO, &bar_q[buf], sDO + buf * TILE_BYTES, 0, i * BQ, h, b);
+  };
+  if (tid == 0) {
+    mbar_expect_tx(bar_kv, 2 * TILE_BYTES);
+    tma_load_4d(&tmK, bar_kv, sK, 0, k0, h, b);
+    tma_load_4d(&tmV, bar_kv, sV, 0, k0, h, b);
+    load_q(0, 0);
+    if (nq > 1) load_q(1, 1);
+  }
+  // lse / D of the first query tile (rows >= N: lse = +inf -> P = 0)
+  auto load_rows = [&](int i, int buf) {
+    const int q = i * BQ + tid;
+    sLse[buf * 128 + tid] = q < p.N ? p.lse[bh * p.N + q] : INFINITY;
+    sD[buf * 128 + tid] = q < p.N ? p.Dv[bh * p.N + q] : 0.f;
+  };
+  load_rows(0, 0);
+  const uint32_t id_sq = idesc_bf16_f32(BKV, BQ, 0, 0);  // S^T / dP^T: M=keys, N=queries, K=64
+  const uint32_t id_acc = idesc_bf16_f32(BKV, HD, 0, 1); // dV / dK: M=keys, N=64, K=queries
+  const uint32_t id_dq = idesc_bf16_f32(BQ, HD, 1, 1);   // dQ: M=queries (A MN-major), N=64
+  const bool key_valid = k0 + tid < p.Nk;
+
+  for (int i = 0; i < nq; ++i) {
+    const int qb = i & 1;
+    __syncthreads();  // sLse/sD of tile i visible; previous tile's smem/TMEM consumers done
+    if (tid == 0) {
+      if (i == 0) mbar_wait(bar_kv, 0);
+      mbar_wait(&bar_q[qb], (i >> 1) & 1);
+      tc_fence_after();
+      const uint32_t ka = smem_u32(sK), va = smem_u32(sV);
+      const uint32_t qa = smem_u32(sQ + qb * TILE_BYTES), da = smem_u32(sDO + qb * TILE_BYTES);
+#pragma unroll
+      for (int k = 0; k < HD / 16; ++k) {
+        tc_mma_bf16(t_st, smem_desc_sw128(ka + k * 32, 16, 1024), smem_desc_sw128(qa + k * 32, 16, 1024),
+                    id_sq, k > 0 ? 1u : 0u);
+        tc_mma_bf16(t_dpt, smem_desc_sw128(va + k * 32, 16, 1024), smem_desc_sw128(da + k * 32, 16, 1024),
+                    id_sq, k > 0 ? 1u : 0u);
+      }
+      tc_commit(bar_sp);
+    }
+    if (i + 1 < nq) load_rows(i + 1, qb ^ 1);
+    mbar_wait(bar_sp, i & 1);
+    tc_fence_after();
+    const float* lse = sLse + qb * 128;
+    const float* Dq = sD + qb * 128;
+#pragma unroll 1
+    for (int c = 0; c < BQ / 32; ++c) {
+      uint32_t sv[32], dv[32];
+      tmem_ld_32x32(t_st + lane_off + c * 32, sv);
+      tmem_ld_32x32(t_dpt + lane_off + c * 32, dv);
+      tmem_ld_wait();
+      float pt[32], dst[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int q = c * 32 + j;
+        const float pp = key_valid ? ex2(fmaf(__uint_as_float(sv[j]), p.scale_log2, -lse[q])) : 0.f;
+        pt[j] = pp;
+        dst[j] = pp * (__uint_as_float(dv[j]) - Dq[q]);
+      }
+      const int blk = c >> 1;
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const int chunk = (c & 1) * 4 + q4;
+        const int off = blk * TILE_BYTES + tid * 128 + ((chunk ^ (tid & 7)) * 16);
+        uint4 u;
+        u.x = pack_bf16x2(pt[q4 * 8 + 0], pt[q4 * 8 + 1]);
+        u.y = pack_bf16x2(pt[q4 * 8 + 2], pt[q4 * 8 + 3]);
+        u.z = pack_bf16x2(pt[q4 * 8 + 4], pt[q4 * 8 + 5]);
+        u.w = pack_bf16x2(pt[q4 * 8 + 6], pt[q4 * 8 + 7]);
+        *reinterpret_cast<uint4*>(sPT + off) = u;
+        u.x = pack_bf16x2(dst[q4 * 8 + 0], dst[q4 * 8 + 1]);
+        u.y = pack_bf16x2(dst[q4 * 8 + 2], dst[q4 * 8 + 3]);
+        u.z = pack_bf16x2(dst[q4 * 8 + 4], dst[q4 * 8 + 5]);
+        u.w = pack_bf16x2(dst[q4 * 8 + 6], dst[q4 * 8 + 7]);
+        *reinterpret_cast<uint4*>(sDST + off) = u;
+      }
+    }
+    fence_async_shared();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t pta = smem_u32(sPT), dsa = smem_u32(sDST), ka = smem_u32(sK);
+      const uint32_t qa = smem_u32(sQ + qb * TILE_BYTES), da = smem_u32(sDO + qb * TILE_BYTES);
+#pragma unroll
+      for (int k = 0; k < BQ / 16; ++k) {
+        const uint32_t aoff = (k >> 2) * TILE_BYTES + (k & 3) * 32;  // K-major over queries
+        // dV += P^T dO    (B(n=d, k=q) = dO[q][d]: MN-major)
+        tc_mma_bf16(t_dv, smem_desc_sw128(pta + aoff, 16, 1024), smem_desc_sw128(da + k * 2048, 8192, 1024),
+                    id_acc, (i > 0 || k > 0) ? 1u : 0u);
+        // dK += dS^T Q    (B(n=d, k=q) = Q[q][d]: MN-major)
+        tc_mma_bf16(t_dk, smem_desc_sw128(dsa + aoff, 16, 1024), smem_desc_sw128(qa + k * 2048, 8192, 1024),
+                    id_acc, (i > 0 || k > 0) ? 1u : 0u);
+      }
+#pragma unroll
+      for (int k = 0; k < BKV / 16; ++k) {
+        // dQ_i = dS K: A(m=q, k=key) = dS^T[key][q] (MN-major, 64-query chunks 16 KB apart),
+        //              B(n=d, k=key) = K[key][d] (MN-major)
+        tc_mma_bf16(t_dq, smem_desc_sw128(dsa + k * 2048, TILE_BYTES, 1024),
+                    smem_desc_sw128(ka + k * 2048, 8192, 1024), id_dq, k > 0 ? 1u : 0u);
+      }
+      tc_commit(bar_acc);
+    }
+    mbar_wait(bar_acc, i & 1);
+    tc_fence_after();
+    if (tid == 0 && i + 2 < nq) load_q(i + 2, qb);  // Q/dO buffer qb is free again
+    // dQ rows of this query tile -> fp32 atomics (thread = query row)
+    const int q = i * BQ + tid;
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32(t_dq + lane_off + c * 32, v);
+      tmem_ld_wait();
+      if (q < p.N) {
+        float* dst = p.dq_acc + (((int64_t)b * p.N + q) * p.heads + h) * HD + c * 32;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          atomicAdd(reinterpret_cast<float4*>(dst + j),
+                    make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                                __uint_as_float(v[j + 3])));
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  tc_fence_after();
+  // dK (scaled), dV -> bf16 -> shared (reuse the Q buffers) -> TMA stores (thread = key row)
+  uint8_t* sdk = sQ;
+  uint8_t* sdv = sQ + TILE_BYTES;
+#pragma unroll
+  for (int c = 0; c < HD / 32; ++c) {
+    uint32_t vk[32], vv[32];
+    tmem_ld_32x32(t_dk + lane_off + c * 32, vk);
+    tmem_ld_32x32(t_dv + lane_off + c * 32, vv);
+    tmem_ld_wait();
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+      const int chunk = c * 4 + q4;
+      const int off = tid * 128 + ((chunk ^ (tid & 7)) * 16);
+      uint4 u;
+      u.x = pack_bf16x2(p.scale * __uint_as_float(vk[q4 * 8 + 0]), p.scale * __uint_as_float(vk[q4 * 8 + 1]));
+      u.y = pack_bf16x2(p.scale * __uint_as_float(vk[q4 * 8 + 2]), p.scale * __uint_as_float(vk[q4 * 8 + 3]));
+      u.z = pack_bf16x2(p.scale * __uint_as_float(vk[q4 * 8 + 4]), p.scale * __uint_as_float(vk[q4 * 8 + 5]));
+      u.w = pack_bf16x2(p.scale * __uint_as_float(vk[q4 * 8 + 6]), p.scale * __uint_as_float(vk[q4 * 8 + 7]));
+      *reinterpret_cast<uint4*>(sdk + off) = u;
+      u.x = pack_bf16x2(__uint_as_float(vv[q4 * 8 + 0]), __uint_as_float(vv[q4 * 8 + 1]));
+      u.y = pack_bf16x2(__uint_as_float(vv[q4 * 8 + 2]), __uint_as_float(vv[q4 * 8 + 3]));
+      u.z = pack_bf16x2(__uint_as_float(vv[q4 * 8 + 4]), __uint_as_float(vv[q4 * 8 + 5]));
+      u.w = pack_bf16x2(__uint_as_float(vv[q4 * 8 + 6]), __uint_as_float(vv[q4 * 8 + 7]));
+      *reinterpret_cast<uint4*>(sdv + off) = u;
+    }
+  }
+  fence_async_shared();
+  __syncthreads();
+  if (tid == 0) {
+    tma_store_4d(&tmDK, sdk, 0, k0, h, b);
+    tma_store_4d(&tmDV, sdv, 0, k0, h, b);
+    bulk_commit();
+    bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+constexpr size_t BWD_SMEM = 1024 + BWD_SMEM_TILES * TILE_BYTES + 4 * 256 * 4 + 64;
+
+}  // namespace fa
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
+
+// 4-D bf16 map over a [B][N][heads*64] view: dims {64, N, heads, B}, box {64, 128, 1, 1}.
+static int fa_map(CUtensorMap* map, const void* base, int N, int heads, int B, int64_t ld,
+                  int64_t bstride) {
+  auto fn = tensor_map_encoder();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return DP_ERR_DRIVER;
+  }
+  if (reinterpret_cast<uintptr_t>(base) % 16 || (ld * 2) % 16 || (bstride * 2) % 16) {
+    set_error("flash attention: 16-byte aligned base and strides required");
+    return DP_ERR_ARGS;
+  }
+  cuuint64_t gdim[4] = {64, (cuuint64_t)N, (cuuint64_t)heads, (cuuint64_t)B};
+  cuuint64_t gstr[3] = {(cuuint64_t)(ld * 2), 128, (cuuint64_t)(bstride * 2)};
+  cuuint32_t box[4] = {64, 128, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), gdim, gstr, box,
+                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("flash attention: cuTensorMapEncodeTiled failed");
+    return DP_ERR_DRIVER;
+  }
+  return 0;
+}
+
+}  // namespace dp
+
+extern "C" int dp_flash_attn_fwd(const DpAttnArgs* a, dp_stream_t stream) {
+  using namespace dp;
+  if (a->head_dim != 64 || a->dtype != DP_BF16) {
+    set_error("dp_flash_attn_fwd: bf16, head_dim 64 only");
+    return DP_ERR_UNSUPPORTED;
+  }
+  if (a->B <= 0 || a->N <= 0 || a->Nk <= 0) return 0;
+  CUtensorMap mq, mk, mv, mo;
+  if (int e = fa_map(&mq, a->q, a->N, a->heads, a->B, a->q_ld, a->q_bs)) return e;
+  if (int e = fa_map(&mk, a->k, a->Nk, a->heads, a->B, a->kv_ld, a->kv_bs)) return e;
+  if (int e = fa_map(&mv, a->v, a->Nk, a->heads, a->B, a->kv_ld, a->kv_bs)) return e;
+  if (int e = fa_map(&mo, a->o, a->N, a->heads, a->B, a->o_ld, a->o_bs)) return e;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fa::fa_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(fa::SMEM));
+    if (e != cudaSuccess) {
+      set_error(std::string("flash attention attr: ") + cudaGetErrorString(e));
+      return e;
+    }
+    attr = true;
+  }
+  fa::Params p{a->N, a->Nk, a->heads, a->scale * 1.4426950408889634f, a->lse};
+  dim3 grid((a->N + fa::BQ - 1) / fa::BQ, a->heads, a->B);
+  fa::fa_fwd_kernel<<<grid, 128, fa::SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(mq, mk, mv, mo, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("flash attention launch: ") + cudaGetErrorString(e));
+    return e;
+  }
+  return 0;
+}
+
+extern "C" int dp_flash_attn_bwd(const DpAttnArgs* a, const void* dout, int64_t do_ld, void* dq,
+                                 int64_t dq_ld, void* dk, void* dv, int64_t dkv_ld, float* workspace,
+                                 dp_stream_t stream) {
+  using namespace dp;
+  if (a->head_dim != 64 || a->dtype != DP_BF16) {
+    set_error("dp_flash_attn_bwd: bf16, head_dim 64 only");
+    return DP_ERR_UNSUPPORTED;
+  }
+  if (a->B <= 0 || a->N <= 0 || a->Nk <= 0) return 0;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int C = a->heads * 64;
+  const int64_t rows = (int64_t)a->B * a->N;
+  float* Dv = workspace;                                   // [B][heads][N]
+  float* dq_acc = workspace + (int64_t)a->B * a->heads * a->N;  // [B][N][heads][64]
+  cudaMemsetAsync(dq_acc, 0, sizeof(float) * rows * C, st);
+  {
+    const int64_t total = (int64_t)a->B * a->heads * a->N;
+    fa::fa_bwd_prep_kernel<<<static_cast<unsigned>((total + 7) / 8), 256, 0, st>>>(
+        reinterpret_cast<const __nv_bfloat16*>(a->o), reinterpret_cast<const __nv_bfloat16*>(dout), Dv, a->B,
+        a->N, a->heads, a->o_ld, do_ld);
+  }
+  CUtensorMap mq, mk, mv, mdo, mdk, mdv;
+  if (int e = fa_map(&mq, a->q, a->N, a->heads, a->B, a->q_ld, a->q_bs)) return e;
+  if (int e = fa_map(&mk, a->k, a->Nk, a->heads, a->B, a->kv_ld, a->kv_bs)) return e;
+  if (int e = fa_map(&mv, a->v, a->Nk, a->heads, a->B, a->kv_ld, a->kv_bs)) return e;
+  if (int e = fa_map(&mdo, dout, a->N, a->heads, a->B, do_ld, a->N * do_ld)) return e;
+  if (int e = fa_map(&mdk, dk, a->Nk, a->heads, a->B, dkv_ld, a->Nk * dkv_ld)) return e;
+  if (int e = fa_map(&mdv, dv, a->Nk, a->heads, a->B, dkv_ld, a->Nk * dkv_ld)) return e;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fa::fa_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(fa::BWD_SMEM));
+    if (e != cudaSuccess) {
+      set_error(std::string("flash attention bwd attr: ") + cudaGetErrorString(e));
+      return e;
+    }
+    attr = true;
+  }
+  fa::BwdParams p{a->N, a->Nk, a->heads, a->scale * 1.4426950408889634f, a->scale, a->lse, Dv, dq_acc};
+  dim3 grid((a->Nk + fa::BKV - 1) / fa::BKV, a->heads, a->B);
+  fa::fa_bwd_kernel<<<grid, 128, fa::BWD_SMEM, st>>>(mq, mk, mv, mdo, mdk, mdv, p);
+  const int64_t n2 = rows * C / 2;
+  int g = static_cast<int>((n2 + 255) / 256);
+  if (g > 148 * 8) g = 148 * 8;
+  fa::fa_dq_cast_kernel<<<g, 256, 0, st>>>(dq_acc, reinterpret_cast<__nv_bfloat16*>(dq), rows, C, dq_ld,
+                                           a->scale);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("flash attention bwd launch: ") + cudaGetErrorString(e));
+    return e;
+  }
+  return 0;
+}

@@ -39,6 +39,8 @@ struct TcParams {
   int tw, th, tn;  // pixel box (128 pixels for A_CONV, 64 for the wgrad modes)
   int stride, pad_h, pad_w, S, cblk, C;
   int Rf;          // filter height (B_DGRAD flips taps)
+  int stream_k;    // 1: contiguous k-iteration ranges per CTA (fp32 atomic outputs)
+  int d_tma;       // 1: bf16 output written by TMA tensor stores (tmD)
   void* D;
   int64_t d_ld, d_bs1, d_bs2;
   int d_f32, out_mode, vec_ok;
@@ -56,10 +58,10 @@ template <int BN>
 struct TcCfg {
   static constexpr uint32_t B_STAGE_BYTES = BN * BK * 2;
   // as many 64-deep k-stages as fit in ~200 KB of shared memory (4 at BN=256, 8 at BN=64)
-  static constexpr int STAGES_FIT = 200 * 1024 / (A_STAGE_BYTES + B_STAGE_BYTES);
+  static constexpr int STAGES_FIT = 209 * 1024 / (A_STAGE_BYTES + B_STAGE_BYTES);
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256 ? 256 : 512);
-  static constexpr size_t SMEM = 1024 + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 256;
+  static constexpr size_t SMEM = 1024 + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 8 * 2048 + 256;
 };
 
 DP_DEV void pixel_origin(int pix0, int P, int Q, int& n, int& h, int& w) {
@@ -81,14 +83,18 @@ DP_DEV void epilogue_store(const TcParams& p, int row, int n, int z1, int z2, co
 #pragma unroll
       for (int i = 0; i < 32; ++i) f[i] += __ldg(p.bias + n + i);
     } else {
-      for (int i = 0; i < nvalid; ++i) f[i] += __ldg(p.bias + n + i);
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i < nvalid) f[i] += __ldg(p.bias + n + i);
     }
   }
   if (p.R) {
     const int64_t roff = z1 * p.r_bs1 + z2 * p.r_bs2 + (int64_t)row * p.r_ld + n;
     if (p.d_f32) {
       const float* r = reinterpret_cast<const float*>(p.R) + roff;
-      for (int i = 0; i < nvalid; ++i) f[i] += r[i];
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i < nvalid) f[i] += r[i];
     } else {
       const __nv_bfloat16* r = reinterpret_cast<const __nv_bfloat16*>(p.R) + roff;
       if (nvalid == 32 && p.vec_ok) {
@@ -100,7 +106,9 @@ DP_DEV void epilogue_store(const TcParams& p, int row, int n, int z1, int z2, co
           for (int i = 0; i < 8; ++i) f[q * 8 + i] += __bfloat162float(b[i]);
         }
       } else {
-        for (int i = 0; i < nvalid; ++i) f[i] += __bfloat162float(r[i]);
+  #pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i < nvalid) f[i] += __bfloat162float(r[i]);
       }
     }
   }
@@ -114,7 +122,9 @@ DP_DEV void epilogue_store(const TcParams& p, int row, int n, int z1, int z2, co
           atomicAdd(reinterpret_cast<float4*>(d + 4 * q),
                     make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]));
       } else {
-        for (int i = 0; i < nvalid; ++i) atomicAdd(d + i, f[i]);
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i < nvalid) atomicAdd(d + i, f[i]);
       }
     } else {
       if (nvalid == 32 && p.vec_ok) {
@@ -123,7 +133,9 @@ DP_DEV void epilogue_store(const TcParams& p, int row, int n, int z1, int z2, co
           *reinterpret_cast<float4*>(d + 4 * q) =
               make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
       } else {
-        for (int i = 0; i < nvalid; ++i) d[i] = f[i];
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i < nvalid) d[i] = f[i];
       }
     }
   } else {
@@ -139,15 +151,129 @@ DP_DEV void epilogue_store(const TcParams& p, int row, int n, int z1, int z2, co
         *reinterpret_cast<uint4*>(d + q * 8) = u;
       }
     } else {
-      for (int i = 0; i < nvalid; ++i) d[i] = __float2bfloat16_rn(f[i]);
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i < nvalid) d[i] = __float2bfloat16_rn(f[i]);
     }
   }
 }
 
+// ---------------------------------------------------------------- work decomposition
+// Shared by the producer, MMA and epilogue roles (each walks the same sequence).
+//  * tiled mode: items = tiles x splits, CTA b takes items b, b+G, ...; tiles are rastered
+//    in bands of GM m-tiles (n fastest inside a band) so the CTAs of one wave share A
+//    tiles and a band's B tiles stay L2 resident.
+//  * stream-K mode (fp32 atomic outputs only): the tiles x num_kb k-iterations are cut
+//    into gridDim.x equal contiguous ranges; a range may cover parts of several tiles and
+//    each part is reduced with fp32 atomics (perfect wave balance for skinny wgrads).
+struct Work {
+  int m_blk, n_blk, z1, z2, kb0, kb1;
+};
+constexpr int GM = 8;
+
+DP_DEV void tile_coords(const TcParams& p, int t, Work& w) {
+  const int per_batch = p.tiles_m * p.tiles_n;
+  const int z = t / per_batch;
+  t -= z * per_batch;
+  const int band_items = GM * p.tiles_n;
+  const int band = t / band_items;
+  const int within = t - band * band_items;
+  const int gm = min(GM, p.tiles_m - band * GM);
+  w.m_blk = band * GM + within % gm;
+  w.n_blk = within / gm;
+  w.z1 = z % p.batch1;
+  w.z2 = z / p.batch1;
+}
+
+struct WorkIter {
+  int cursor, end;
+  DP_DEV void init(const TcParams& p) {
+    if (p.stream_k) {
+      const long long tot = (long long)p.tiles_m * p.tiles_n * p.nbatch * p.num_kb;
+      cursor = static_cast<int>(tot * blockIdx.x / gridDim.x);
+      end = static_cast<int>(tot * (blockIdx.x + 1) / gridDim.x);
+    } else {
+      cursor = blockIdx.x;
+      end = p.tiles_m * p.tiles_n * p.nbatch * p.splits;
+    }
+  }
+  DP_DEV bool next(const TcParams& p, Work& w) {
+    if (cursor >= end) return false;
+    if (p.stream_k) {
+      const int t = cursor / p.num_kb;
+      w.kb0 = cursor - t * p.num_kb;
+      w.kb1 = min(p.num_kb, w.kb0 + (end - cursor));
+      tile_coords(p, t, w);
+      cursor += w.kb1 - w.kb0;
+    } else {
+      const int tiles = p.tiles_m * p.tiles_n * p.nbatch;
+      const int split = cursor / tiles;
+      tile_coords(p, cursor - split * tiles, w);
+      w.kb0 = split * p.kb_per_split;
+      w.kb1 = min(p.num_kb, w.kb0 + p.kb_per_split);
+      cursor += gridDim.x;
+    }
+    return true;
+  }
+};
+
+// Epilogue of one 32x32 chunk through shared memory and a TMA tensor store (bf16 outputs):
+// lane = row; the 64-byte row is written in the SWIZZLE_64B layout the D map expects
+// (16-byte chunk index XOR ((row >> 1) & 3)), which also spreads the 32 lanes over all banks.
+DP_DEV void stage_row_bf16(uint8_t* buf, int lane, const float (&f)[32]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u;
+    u.x = pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]);
+    u.y = pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]);
+    u.z = pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]);
+    u.w = pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]);
+    const int qs = q ^ ((lane >> 1) & 3);
+    *reinterpret_cast<uint4*>(buf + lane * 64 + qs * 16) = u;
+  }
+}
+
+template <int BN>
+DP_DEV void epilogue_math(const TcParams& p, int row, int n, int z1, int z2, const uint32_t (&v)[32],
+                          float (&f)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * p.alpha;
+  const int nvalid = min(32, p.N - n);
+  if (p.bias) {
+    if (nvalid == 32) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) f[i] += __ldg(p.bias + n + i);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i < nvalid) f[i] += __ldg(p.bias + n + i);
+    }
+  }
+  if (p.R && row < p.M) {
+    const int64_t roff = z1 * p.r_bs1 + z2 * p.r_bs2 + (int64_t)row * p.r_ld + n;
+    const __nv_bfloat16* r = reinterpret_cast<const __nv_bfloat16*>(p.R) + roff;
+    if (nvalid == 32 && p.vec_ok) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 u = *reinterpret_cast<const uint4*>(r + q * 8);
+        const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[q * 8 + i] += __bfloat162float(b[i]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i < nvalid) f[i] += __bfloat162float(r[i]);
+    }
+  }
+}
+
+constexpr int EPI_STAGE_BYTES = 32 * 64;  // one 32 x 32 bf16 chunk
+
 template <int BN>
 __global__ void __launch_bounds__(256, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const TcParams p) {
+                   const __grid_constant__ CUtensorMap tmD, const TcParams p) {
   using Cfg = TcCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -155,7 +281,8 @@ __global__ void __launch_bounds__(256, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_STAGE_BYTES);
+  uint8_t* sE = sB + STAGES * Cfg::B_STAGE_BYTES;            // 4 warps x 2 x 2 KB, 1 KB aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(sE + 8 * EPI_STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -166,6 +293,7 @@ __global__ void __launch_bounds__(256, 1)
   if (threadIdx.x == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if (p.d_tma) tma_prefetch(&tmD);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -182,31 +310,23 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int total = p.tiles_m * p.tiles_n * p.splits * p.nbatch;
-
   if (threadIdx.x == 0) {
     // ------------------------------------------------------------ TMA producer
     int stage = 0;
     uint32_t phase = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x) {
-      int r = w;
-      const int m_blk = r % p.tiles_m;
-      r /= p.tiles_m;
-      const int n_blk = r % p.tiles_n;
-      r /= p.tiles_n;
-      const int split = r % p.splits;
-      const int z = r / p.splits;
-      const int z1 = z % p.batch1, z2 = z / p.batch1;
-      const int kb0 = split * p.kb_per_split;
-      const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
-      const int m0 = m_blk * BM, n0 = n_blk * BN;
+    WorkIter it;
+    it.init(p);
+    Work wk;
+    while (it.next(p, wk)) {
+      const int z1 = wk.z1, z2 = wk.z2;
+      const int m0 = wk.m_blk * BM, n0 = wk.n_blk * BN;
       int cn = 0, ch = 0, cw = 0;
       if (p.a_mode == A_CONV) {
         pixel_origin(m0, p.P, p.Q, cn, ch, cw);
         ch = ch * p.stride - p.pad_h;
         cw = cw * p.stride - p.pad_w;
       }
-      for (int kb = kb0; kb < kb1; ++kb) {
+      for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         mbar_expect_tx(&full[stage], A_STAGE_BYTES + Cfg::B_STAGE_BYTES);
         uint8_t* a_dst = sA + stage * A_STAGE_BYTES;
@@ -282,14 +402,14 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x) {
-      const int split = (w / (p.tiles_m * p.tiles_n)) % p.splits;
-      const int kb0 = split * p.kb_per_split;
-      const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+    WorkIter it;
+    it.init(p);
+    Work wk;
+    while (it.next(p, wk)) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = kb0; kb < kb1; ++kb) {
+      for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         const uint32_t a_addr = smem_u32(sA + stage * A_STAGE_BYTES);
@@ -300,7 +420,7 @@ __global__ void __launch_bounds__(256, 1)
                                       : smem_desc_sw128(a_addr + j * 32, 16, 1024);
           const uint64_t bdesc = b_mn ? smem_desc_sw128(b_addr + j * 2048, 8192, 1024)
                                       : smem_desc_sw128(b_addr + j * 32, 16, 1024);
-          tc_mma_bf16(d_tmem, adesc, bdesc, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
+          tc_mma_bf16(d_tmem, adesc, bdesc, idesc, (kb > wk.kb0 || j > 0) ? 1u : 0u);
         }
         tc_commit(&empty[stage]);
         if (++stage == STAGES) {
@@ -317,30 +437,49 @@ __global__ void __launch_bounds__(256, 1)
     const int wq = warp - 4;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x) {
-      int r = w;
-      const int m_blk = r % p.tiles_m;
-      r /= p.tiles_m;
-      const int n_blk = r % p.tiles_n;
-      r /= p.tiles_n;
-      const int z = r / p.splits;
-      const int z1 = z % p.batch1, z2 = z / p.batch1;
+    uint8_t* ebuf = sE + wq * 2 * EPI_STAGE_BYTES;
+    int chunk_seq = 0;
+    WorkIter it;
+    it.init(p);
+    Work wk;
+    while (it.next(p, wk)) {
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = m_blk * BM + wq * 32 + lane;
+      const int row0 = wk.m_blk * BM + wq * 32;
+      const int row = row0 + lane;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
+        const int n = wk.n_blk * BN + c * 32;
+        if (n >= p.N) break;  // warp-uniform
         uint32_t v[32];
         tmem_ld_32x32(tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + acc * BN + c * 32, v);
         tmem_ld_wait();
-        const int n = n_blk * BN + c * 32;
-        if (row < p.M && n < p.N) epilogue_store<BN>(p, row, n, z1, z2, v);
+        if (p.d_tma) {
+          float f[32];
+          epilogue_math<BN>(p, row, n, wk.z1, wk.z2, v, f);
+          uint8_t* buf = ebuf + (chunk_seq & 1) * EPI_STAGE_BYTES;
+          if (chunk_seq >= 2) {
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+          }
+          stage_row_bf16(buf, lane, f);
+          fence_async_shared();
+          __syncwarp();
+          if (lane == 0 && row0 < p.M) {
+            tma_store_4d(&tmD, buf, n, row0, wk.z1, wk.z2);
+            bulk_commit();
+          }
+          ++chunk_seq;
+        } else if (row < p.M) {
+          epilogue_store<BN>(p, row, n, wk.z1, wk.z2, v);
+        }
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (p.d_tma && lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -366,9 +505,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() { return encode_fn(); }
+
 // 4-D bf16 map. dims innermost-first; strides in ELEMENTS for dims 1..3.
 static int make_map(CUtensorMap* map, const void* base, const uint64_t dims[4],
-                    const int64_t strides_el[3], const uint32_t box[4], const uint32_t estr[4]) {
+                    const int64_t strides_el[3], const uint32_t box[4], const uint32_t estr[4],
+                    CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -399,7 +541,7 @@ static int make_map(CUtensorMap* map, const void* base, const uint64_t dims[4],
     es[i] = estr[i];
   }
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), gdim, gstr,
-                  bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     char buf[256];
@@ -414,8 +556,8 @@ static int make_map(CUtensorMap* map, const void* base, const uint64_t dims[4],
 }
 
 template <int BN>
-static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, TcParams p, int max_ctas,
-                     cudaStream_t st) {
+static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
+                     TcParams p, int max_ctas, cudaStream_t st) {
   using Cfg = TcCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -428,10 +570,11 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, TcParams p, i
     }
     attr_set = true;
   }
-  const int total = p.tiles_m * p.tiles_n * p.splits * p.nbatch;
-  const int grid = total < max_ctas ? total : max_ctas;
+  const long long total = p.stream_k ? (long long)p.tiles_m * p.tiles_n * p.nbatch * p.num_kb
+                                     : (long long)p.tiles_m * p.tiles_n * p.splits * p.nbatch;
+  const int grid = static_cast<int>(total < max_ctas ? total : max_ctas);
   if (grid <= 0) return 0;
-  tc_gemm_kernel<BN><<<grid, 256, Cfg::SMEM, st>>>(ma, mb, p);
+  tc_gemm_kernel<BN><<<grid, 256, Cfg::SMEM, st>>>(ma, mb, md, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("tc_gemm launch: ") + cudaGetErrorString(e));
@@ -462,22 +605,46 @@ static int pick_bn(int N, bool b_mn_major) {
   return best;
 }
 
-static int launch_bn(int bn, const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& p,
-                     cudaStream_t st) {
+// bf16 STORE outputs with TMA-legal strides are written by tensor stores (box 32 x 32,
+// SWIZZLE_64B); fp32 / atomic outputs keep the direct per-thread path.
+static int make_dmap(CUtensorMap* md, TcParams& p, int M, int N, int b1, int b2) {
+  p.d_tma = 0;
+  if (p.d_f32 || p.out_mode != DP_OUT_STORE || !p.vec_ok) return 0;
+  const uint64_t d[4] = {(uint64_t)N, (uint64_t)M, (uint64_t)b1, (uint64_t)b2};
+  const int64_t s[3] = {p.d_ld, b1 > 1 ? p.d_bs1 : (int64_t)M * p.d_ld,
+                        b2 > 1 ? p.d_bs2 : (int64_t)M * p.d_ld * b1};
+  const uint32_t box[4] = {32, 32, 1, 1};
+  const uint32_t ones[4] = {1, 1, 1, 1};
+  if (make_map(md, p.D, d, s, box, ones, CU_TENSOR_MAP_SWIZZLE_64B) == 0) p.d_tma = 1;
+  return 0;
+}
+
+static int launch_bn(int bn, const CUtensorMap& ma, const CUtensorMap& mb, TcParams& p, int M, int N,
+                     int b1, int b2, cudaStream_t st) {
+  CUtensorMap md = ma;
+  make_dmap(&md, p, M, N, b1, b2);
   switch (bn) {
-    case 64: return launch_tc<64>(ma, mb, p, kNumSMs, st);
-    case 96: return launch_tc<96>(ma, mb, p, kNumSMs, st);
-    case 128: return launch_tc<128>(ma, mb, p, kNumSMs, st);
-    case 160: return launch_tc<160>(ma, mb, p, kNumSMs, st);
-    case 192: return launch_tc<192>(ma, mb, p, kNumSMs, st);
-    case 224: return launch_tc<224>(ma, mb, p, kNumSMs, st);
-    default: return launch_tc<256>(ma, mb, p, kNumSMs, st);
+    case 64: return launch_tc<64>(ma, mb, md, p, kNumSMs, st);
+    case 96: return launch_tc<96>(ma, mb, md, p, kNumSMs, st);
+    case 128: return launch_tc<128>(ma, mb, md, p, kNumSMs, st);
+    case 160: return launch_tc<160>(ma, mb, md, p, kNumSMs, st);
+    case 192: return launch_tc<192>(ma, mb, md, p, kNumSMs, st);
+    case 224: return launch_tc<224>(ma, mb, md, p, kNumSMs, st);
+    default: return launch_tc<256>(ma, mb, md, p, kNumSMs, st);
   }
 }
 
 static void choose_split(TcParams& p, int requested, bool allowed) {
   const int tiles = p.tiles_m * p.tiles_n * p.nbatch;
   int splits = 1;
+  p.stream_k = 0;
+  if (allowed && requested <= 0 && tiles < 2 * kNumSMs && (long long)tiles * p.num_kb >= 4 * kNumSMs) {
+    // fp32 atomic output: balance k-iterations over all SMs (stream-K)
+    p.stream_k = 1;
+    p.splits = 1;
+    p.kb_per_split = p.num_kb;
+    return;
+  }
   if (allowed) {
     if (requested > 0) {
       splits = requested;
@@ -563,7 +730,7 @@ int tc_gemm(const DpGemmArgs* a, cudaStream_t st) {
       if (int e = make_map(&mb, a->B, d, s, box, ones)) return e;
     }
   }
-  return launch_bn(bn, ma, mb, p, st);
+  return launch_bn(bn, ma, mb, p, a->M, a->N, p.batch1, batch2, st);
 }
 
 // Tile the output pixels (P x Q per image, N images) with boxes of `pixels`
@@ -643,7 +810,7 @@ int tc_conv_fwd(const DpConvArgs* a, cudaStream_t st) {
     const uint32_t ones[4] = {1, 1, 1, 1};
     if (int e = make_map(&mb, a->w, d, s, box, ones)) return e;
   }
-  return launch_bn(bn, ma, mb, p, st);
+  return launch_bn(bn, ma, mb, p, p.M, p.N, 1, 1, st);
 }
 
 // Input gradient of a stride-1 convolution as an implicit GEMM over dy with the weights read
@@ -701,7 +868,7 @@ int tc_conv_dgrad(const DpConvArgs* a, cudaStream_t st) {
     const uint32_t ones[4] = {1, 1, 1, 1};
     if (int e = make_map(&mb, a->w, d, s, box, ones)) return e;
   }
-  return launch_bn(bn, ma, mb, p, st);
+  return launch_bn(bn, ma, mb, p, p.M, p.N, 1, 1, st);
 }
 
 // dW[k][r][s][c] += sum_{n,p,q} dy[n][p][q][k] * x[n][p*stride+r-pad][q*stride+s-pad][c]
@@ -752,7 +919,7 @@ int tc_conv_wgrad(const DpConvArgs* a, cudaStream_t st) {
     const uint32_t es[4] = {1, (uint32_t)a->stride, (uint32_t)a->stride, 1};
     if (int e = make_map(&mb, a->x, d, s, box, es)) return e;
   }
-  return launch_bn(bn, ma, mb, p, st);
+  return launch_bn(bn, ma, mb, p, p.M, p.N, 1, 1, st);
 }
 
 // ====================================================================== fp32 / generic SIMT GEMM

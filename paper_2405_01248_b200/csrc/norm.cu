@@ -164,6 +164,8 @@ DP_DEV void gn_merge_stats(const float* part, int n, int nchunks, int G, float e
   }
 }
 
+// Apply: each thread owns one 16-byte channel vector for the whole pixel range (no index
+// arithmetic in the streaming loop) with its per-channel affine folded into y = x*a + b.
 template <typename T>
 __global__ void __launch_bounds__(GN_THREADS)
     gn_apply_kernel(const T* __restrict__ x, const float* __restrict__ gamma,
@@ -173,7 +175,8 @@ __global__ void __launch_bounds__(GN_THREADS)
                     float eps, int silu_on) {
   constexpr int V = NV<T>::V;
   const int n = blockIdx.y, chunk = blockIdx.x, nchunks = gridDim.x;
-  __shared__ float s_mean[64 * 4], s_rstd[64 * 4];
+  __shared__ float s_mean[256], s_rstd[256];
+  __shared__ float s_a[GN_MAX_C], s_b[GN_MAX_C];
   gn_merge_stats(part, n, nchunks, G, eps, s_mean, s_rstd);
   __syncthreads();
   if (chunk == 0)
@@ -182,26 +185,44 @@ __global__ void __launch_bounds__(GN_THREADS)
       rstd_out[n * G + g] = s_rstd[g];
     }
   const int cg = C / G;
+  for (int c = threadIdx.x; c < C; c += GN_THREADS) {
+    const int g = c / cg;
+    const float a = s_rstd[g] * (gamma ? gamma[c] : 1.f);
+    s_a[c] = a;
+    s_b[c] = (gamma ? beta[c] : 0.f) - s_mean[g] * a;
+  }
+  __syncthreads();
   const int CV = C / V;
   const int p0 = chunk * pix_per_chunk;
   const int p1 = min(HW, p0 + pix_per_chunk);
-  const int64_t base = (int64_t)n * HW * C;
-  const int64_t total = (int64_t)(p1 - p0) * CV;
-  for (int64_t i = threadIdx.x; i < total; i += GN_THREADS) {
-    const int64_t p = p0 + i / CV;
-    const int cv = static_cast<int>(i % CV);
-    float f[V];
-    ld16(x + base + p * C + cv * V, f);
+  const T* xs = x + (int64_t)n * HW * C;
+  T* ys = y + (int64_t)n * HW * C;
+  for (int cv0 = 0; cv0 < CV; cv0 += GN_THREADS) {
+    const int width = min(GN_THREADS, CV - cv0);
+    const int rows_par = GN_THREADS / width;
+    const int cv = cv0 + threadIdx.x % width;
+    const int rl = threadIdx.x / width;
+    if (rl >= rows_par) continue;
+    float a[V], b[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-      const int c = cv * V + j;
-      const int g = c / cg;
-      float v = (f[j] - s_mean[g]) * s_rstd[g];
-      if (gamma) v = v * gamma[c] + beta[c];
-      if (silu_on) v = v / (1.f + __expf(-v));
-      f[j] = v;
+      a[j] = s_a[cv * V + j];
+      b[j] = s_b[cv * V + j];
     }
-    st16(y + base + p * C + cv * V, f);
+    const T* xp = xs + (int64_t)(p0 + rl) * C + cv * V;
+    T* yp = ys + (int64_t)(p0 + rl) * C + cv * V;
+    const int64_t step = (int64_t)rows_par * C;
+    for (int p = p0 + rl; p < p1; p += rows_par, xp += step, yp += step) {
+      float f[V];
+      ld16(xp, f);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        float v = fmaf(f[j], a[j], b[j]);
+        if (silu_on) v = v / (1.f + __expf(-v));
+        f[j] = v;
+      }
+      st16(yp, f);
+    }
   }
 }
 
@@ -317,32 +338,45 @@ __global__ void __launch_bounds__(GN_THREADS)
   const int p0 = chunk * pix_per_chunk;
   const int p1 = min(HW, p0 + pix_per_chunk);
   const int64_t base = (int64_t)n * HW * C;
-  const int64_t total = (int64_t)(p1 - p0) * CV;
-  for (int64_t i = threadIdx.x; i < total; i += GN_THREADS) {
-    const int64_t p = p0 + i / CV;
-    const int cv = static_cast<int>(i % CV);
-    const int64_t off = base + p * C + cv * V;
-    float fx[V], fd[V], fo[V];
-    ld16(x + off, fx);
-    ld16(dy + off, fd);
-    if (accumulate) ld16(dx + off, fo);
+  for (int cv0 = 0; cv0 < CV; cv0 += GN_THREADS) {
+    const int width = min(GN_THREADS, CV - cv0);
+    const int rows_par = GN_THREADS / width;
+    const int cv = cv0 + threadIdx.x % width;
+    const int rl = threadIdx.x / width;
+    if (rl >= rows_par) continue;
+    float mu[V], rs[V], ga[V], be[V], gA[V], gB[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       const int c = cv * V + j;
       const int g = c / cg;
-      const float mu = mean[n * G + g], rs = rstd[n * G + g];
-      const float xh = (fx[j] - mu) * rs;
-      const float ga = gamma ? gamma[c] : 1.f;
-      float d = fd[j];
-      if (silu_on) {
-        const float y0 = xh * ga + (gamma ? beta[c] : 0.f);
-        const float s = 1.f / (1.f + __expf(-y0));
-        d *= s * (1.f + y0 * (1.f - s));
-      }
-      const float v = rs * (ga * d - s_A[g] - xh * s_B[g]);
-      fo[j] = accumulate ? fo[j] + v : v;
+      mu[j] = mean[n * G + g];
+      rs[j] = rstd[n * G + g];
+      ga[j] = gamma ? gamma[c] : 1.f;
+      be[j] = gamma ? beta[c] : 0.f;
+      gA[j] = s_A[g];
+      gB[j] = s_B[g];
     }
-    st16(dx + off, fo);
+    const int64_t step = (int64_t)rows_par * C;
+    int64_t off = base + (int64_t)(p0 + rl) * C + cv * V;
+    for (int p = p0 + rl; p < p1; p += rows_par, off += step) {
+      float fx[V], fd[V], fo[V];
+      ld16(x + off, fx);
+      ld16(dy + off, fd);
+      if (accumulate) ld16(dx + off, fo);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const float xh = (fx[j] - mu[j]) * rs[j];
+        float d = fd[j];
+        if (silu_on) {
+          const float y0 = fmaf(xh, ga[j], be[j]);
+          const float sg = 1.f / (1.f + __expf(-y0));
+          d *= sg * (1.f + y0 * (1.f - sg));
+        }
+        const float v = rs[j] * (ga[j] * d - gA[j] - xh * gB[j]);
+        fo[j] = accumulate ? fo[j] + v : v;
+      }
+      st16(dx + off, fo);
+    }
   }
 }
 

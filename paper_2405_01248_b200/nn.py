@@ -27,10 +27,11 @@ import zlib
 
 import torch
 
-from . import ops
+from . import ops, telemetry
 from ._lib import DP_ACT_GELU, DP_ACT_GELU_TANH, DP_ACT_SILU
 
 _ALIGN = 64  # elements; keeps every view 128-byte aligned for TMA
+FLASH_ATTENTION = True  # bf16 head-dim-64 attention through the fused tcgen05 kernels
 
 
 # ============================================================================ parameters
@@ -462,6 +463,16 @@ class _AttentionFn(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, q_t, kv_t, heads, causal):
+        with telemetry.site("attn"):
+            return _AttentionFn._fwd(ctx, q_t, kv_t, heads, causal)
+
+    @staticmethod
+    def backward(ctx, do):
+        with telemetry.site("attn"):
+            return _AttentionFn._bwd(ctx, do)
+
+    @staticmethod
+    def _fwd(ctx, q_t, kv_t, heads, causal):
         q_t = _c(q_t)
         kv_t = None if kv_t is None else _c(kv_t)
         B, N = q_t.shape[0], q_t.shape[1]
@@ -475,8 +486,21 @@ class _AttentionFn(torch.autograd.Function):
             q_ld = C
         hd = C // heads
         scale = 1.0 / math.sqrt(hd)
-        ld = -(-Nk // 8) * 8
         dev, dt = q_t.device, q_t.dtype
+        if FLASH_ATTENTION and dt == torch.bfloat16 and hd == 64 and not causal:
+            # fused tcgen05 attention: no score / probability tensors in HBM
+            o = torch.empty(B, N, C, device=dev, dtype=dt)
+            lse = torch.empty(B, heads, N, device=dev, dtype=torch.float32)
+            kp = src_k.view(-1)[k_off:]
+            vp = src_k.view(-1)[v_off:]
+            ops.flash_attn_fwd(q_t, kp, vp, o, B=B, N=N, Nk=Nk, heads=heads, q_ld=q_ld, kv_ld=kv_ld,
+                               o_ld=C, scale=scale, lse=lse)
+            ctx.save_for_backward(q_t, src_k if kv_t is not None else q_t, o, lse)
+            ctx.meta = (kv_t is None, heads, B, N, Nk, C, hd, q_ld, kv_ld, k_off, v_off, scale)
+            ctx.flash = True
+            return o
+        ctx.flash = False
+        ld = -(-Nk // 8) * 8
         S = torch.empty(B, heads, N, ld, device=dev, dtype=torch.float32)
         P = torch.empty(B, heads, N, ld, device=dev, dtype=dt)
         o = torch.empty(B, N, C, device=dev, dtype=dt)
@@ -495,7 +519,20 @@ class _AttentionFn(torch.autograd.Function):
         return o
 
     @staticmethod
-    def backward(ctx, do):
+    def _bwd(ctx, do):
+        if ctx.flash:
+            q_t, src_k, o, lse = ctx.saved_tensors
+            self_attn, heads, B, N, Nk, C, hd, q_ld, kv_ld, k_off, v_off, scale = ctx.meta
+            do = _c(do)
+            dq_t = torch.empty_like(q_t)
+            dkv_t = dq_t if self_attn else torch.empty_like(src_k)
+            ops.flash_attn_bwd(q_t, src_k.view(-1)[k_off:], src_k.view(-1)[v_off:], o, do, dq_t,
+                               dkv_t.view(-1)[k_off:], dkv_t.view(-1)[v_off:], lse, B=B, N=N, Nk=Nk,
+                               heads=heads, q_ld=q_ld, kv_ld=kv_ld, o_ld=C, do_ld=C, dq_ld=q_ld,
+                               dkv_ld=kv_ld, scale=scale)
+            if self_attn:
+                return dq_t, None, None, None
+            return dq_t, dkv_t, None, None
         q_t, src_k, P = ctx.saved_tensors
         self_attn, heads, B, N, Nk, C, hd, ld, q_ld, kv_ld, k_off, v_off, scale = ctx.meta
         do = _c(do)

@@ -70,7 +70,8 @@ def gemm(A, B, D, *, M, N, K, a_ld, b_ld, d_ld, a_mn=False, b_mn=False,
     args.split_k = split_k
     fam = "tcgen05_gemm" if A.dtype == torch.bfloat16 else "simt_gemm"
     flops = 2.0 * M * N * K * max(1, batch[0]) * max(1, batch[1])
-    telemetry.timed(fam, flops, lambda: check(_lib.lib().dp_gemm(ctypes.byref(args), _stream()), "dp_gemm"))
+    telemetry.timed(fam, flops, lambda: check(_lib.lib().dp_gemm(ctypes.byref(args), _stream()), "dp_gemm"),
+                    sub="linear")
     return D
 
 
@@ -190,7 +191,8 @@ def conv2d(x, w, *, stride=1, pad=(1, 1), out_hw=None, bias=None, residual=None,
         Cp = xp.shape[-1]
         a = _conv_args(xp, wp, out, stride, pad, P, Q, bias, residual)
         telemetry.timed("tcgen05_gemm", 2.0 * N * P * Q * K * R * S * C,
-                        lambda: check(_lib.lib().dp_conv_fwd(ctypes.byref(a), _stream()), "dp_conv_fwd"))
+                        lambda: check(_lib.lib().dp_conv_fwd(ctypes.byref(a), _stream()), "dp_conv_fwd"),
+                        sub="conv_fwd")
         return out
     cols = im2col(x, R, S, stride, pad, P, Q)
     linear(cols, w.reshape(K, -1), bias=bias,
@@ -236,7 +238,8 @@ def conv2d_dgrad(dy, w, x_shape, *, stride=1, pad=(1, 1)):
         a = _conv_args(dx, wp, dx, 1, pad, src.shape[1], src.shape[2])
         a.x = _ptr(src)
         telemetry.timed("tcgen05_gemm", 2.0 * N * H * W * C * R * S * K,
-                        lambda: check(_lib.lib().dp_conv_dgrad(ctypes.byref(a), _stream()), "dp_conv_dgrad"))
+                        lambda: check(_lib.lib().dp_conv_dgrad(ctypes.byref(a), _stream()), "dp_conv_dgrad"),
+                        sub="conv_dgrad")
         return _take_last(dx, C)
     dcols = linear_dgrad(dy.reshape(-1, K), w.reshape(K, -1))
     dx = torch.zeros(N, H, W, C, device=dy.device, dtype=dy.dtype)
@@ -260,7 +263,8 @@ def conv2d_wgrad(dy, x, dw, *, stride=1, pad=(1, 1)):
         a.w = _ptr(dyp)  # wgrad reads dy through the `w` slot (see dpipe.h)
         a.K, a.R, a.S = Kp, R, S
         telemetry.timed("tcgen05_gemm", 2.0 * N * P * Q * K * R * S * C,
-                        lambda: check(_lib.lib().dp_conv_wgrad(ctypes.byref(a), _stream()), "dp_conv_wgrad"))
+                        lambda: check(_lib.lib().dp_conv_wgrad(ctypes.byref(a), _stream()), "dp_conv_wgrad"),
+                        sub="conv_wgrad")
         if tgt is not dw:
             dw.add_(tgt[:K, :, :, :C])
         return dw
@@ -521,3 +525,38 @@ def space_to_depth(x, p, inverse=False):
     check(_L().dp_space_to_depth(dtype_code(x), _ptr(x), _ptr(out), N, Hs, Ws, Cs, p, int(inverse), _stream()),
           "dp_space_to_depth")
     return out
+
+
+def _attn_args(q, k, v, o, B, N, Nk, heads, q_ld, kv_ld, o_ld, scale, lse):
+    a = _lib.DpAttnArgs()
+    a.dtype = DP_BF16
+    a.B, a.N, a.Nk, a.heads, a.head_dim = B, N, Nk, heads, 64
+    a.q, a.k, a.v, a.o = _ptr(q), _ptr(k), _ptr(v), _ptr(o)
+    a.q_ld, a.q_bs = q_ld, N * q_ld
+    a.kv_ld, a.kv_bs = kv_ld, Nk * kv_ld
+    a.o_ld, a.o_bs = o_ld, N * o_ld
+    a.scale = scale
+    a.lse = _ptr(lse)
+    return a
+
+
+def flash_attn_fwd(q, k, v, o, *, B, N, Nk, heads, q_ld, kv_ld, o_ld, scale, lse=None):
+    """Fused attention forward (bf16, head dim 64). q/k/v/o are base pointers of
+    [B, N(k), heads*64] column views with token strides *_ld (elements)."""
+    a = _attn_args(q, k, v, o, B, N, Nk, heads, q_ld, kv_ld, o_ld, scale, lse)
+    flops = 4.0 * B * heads * N * Nk * 64
+    telemetry.timed("tcgen05_gemm", flops,
+                    lambda: check(_L().dp_flash_attn_fwd(ctypes.byref(a), _stream()), "dp_flash_attn_fwd"),
+                    sub="flash_fwd")
+    return o
+
+
+def flash_attn_bwd(q, k, v, o, do, dq, dk, dv, lse, *, B, N, Nk, heads, q_ld, kv_ld, o_ld, do_ld, dq_ld,
+                   dkv_ld, scale):
+    a = _attn_args(q, k, v, o, B, N, Nk, heads, q_ld, kv_ld, o_ld, scale, lse)
+    ws = torch.empty(B * heads * N + B * N * heads * 64, device=o.device, dtype=torch.float32)
+    flops = 10.0 * B * heads * N * Nk * 64  # S, dP, dV, dK, dQ recomputation + products
+    telemetry.timed("tcgen05_gemm", flops,
+                    lambda: check(_L().dp_flash_attn_bwd(ctypes.byref(a), _ptr(do), do_ld, _ptr(dq), dq_ld,
+                                                         _ptr(dk), _ptr(dv), dkv_ld, _ptr(ws), _stream()),
+                                  "dp_flash_attn_bwd", 3), sub="flash_bwd")

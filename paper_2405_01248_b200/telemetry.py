@@ -2,24 +2,30 @@
 
 * every libdpipe entry point reports through `_lib.check`, which counts the kernels it
   launched (`launches`) — the bench's `gpu_launches` claim;
-* when `timer.active`, the GEMM/conv wrappers bracket their launch with CUDA events on the
-  launching stream and record (family, algorithmic FLOPs) so bench.py can compute the
-  dominant kernel's achieved TFLOP/s over the timed region.
+* when `timer.active`, every libdpipe call is bracketed by CUDA events on the launching
+  stream (`_lib.lib()` hands out a timing proxy) and recorded under a family name: the
+  tensor-core GEMM/conv wrappers record their algorithmic FLOPs under "tcgen05_gemm[.site]"
+  (site = attn / conv_fwd / conv_dgrad / conv_wgrad / linear), every other entry point under
+  its own name. bench.py turns this into the per-family breakdown and the roofline line.
 """
 
 from __future__ import annotations
 
+import contextlib
+import threading
 from collections import Counter
 
 import torch
 
 launches = Counter()
+_site = threading.local()
 
 
 class _Timer:
     def __init__(self):
         self.active = False
         self.records = []
+        self.depth = 0
 
     def start(self):
         self.records = []
@@ -42,16 +48,50 @@ class _Timer:
 timer = _Timer()
 
 
-def timed(family, flops, fn):
+@contextlib.contextmanager
+def site(name):
+    """Label the GEMM launches issued inside the block (e.g. 'attn')."""
+    prev = getattr(_site, "name", None)
+    _site.name = name
+    try:
+        yield
+    finally:
+        _site.name = prev
+
+
+def timed(family, flops, fn, sub=None):
     if not timer.active:
         return fn()
+    s = getattr(_site, "name", None) or sub
+    fam = f"{family}.{s}" if s else family
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record()
-    r = fn()
+    timer.depth += 1
+    try:
+        r = fn()
+    finally:
+        timer.depth -= 1
     b.record()
-    timer.records.append((family, flops, a, b))
+    timer.records.append((fam, flops, a, b))
     return r
+
+
+class TimedLib:
+    """Proxy over the ctypes library: times every entry point not already inside `timed`."""
+
+    def __init__(self, lib):
+        self._lib = lib
+
+    def __getattr__(self, name):
+        f = getattr(self._lib, name)
+        if not callable(f) or timer.depth > 0 or name in ("dp_last_error", "dp_version",
+                                                         "dp_group_norm_workspace"):
+            return f
+
+        def call(*args):
+            return timed(name, 0.0, lambda: f(*args))
+        return call
 
 
 def count(what, n=1):

@@ -200,3 +200,37 @@ def test_q_sample_mse(dt):
     refl = 0.25 * ((xt.float() - nz.float()) ** 2).sum()
     assert abs(loss.item() - refl.item()) <= 1e-4 * refl.item()
     assert _rel(dp, 0.5 * (xt.float() - nz.float())) < _tol(dt)
+
+
+@pytest.mark.parametrize("B,N,Nk,C,heads,cross", [(2, 1024, 1024, 320, 5, False), (3, 256, 256, 640, 10, False),
+                                                  (2, 64, 64, 1280, 20, False), (4, 16, 16, 1280, 20, False),
+                                                  (2, 1024, 77, 320, 5, True), (2, 200, 77, 128, 2, True),
+                                                  (1, 300, 300, 128, 2, False)])
+def test_flash_attention_vs_torch(B, N, Nk, C, heads, cross):
+    """The fused tcgen05 attention (fwd + bwd) vs fp32 PyTorch SDPA."""
+    from paper_2405_01248_b200 import nn
+    assert nn.FLASH_ATTENTION
+    g = torch.Generator(device="cuda").manual_seed(N + Nk)
+    if cross:
+        q = torch.randn(B, N, C, device="cuda", generator=g).bfloat16().requires_grad_(True)
+        kv = torch.randn(B, Nk, 2 * C, device="cuda", generator=g).bfloat16().requires_grad_(True)
+        o = nn.attention(q, kv, heads)
+        qr, kvr = q.detach().float().requires_grad_(True), kv.detach().float().requires_grad_(True)
+        Q, K, V = qr, kvr[..., :C], kvr[..., C:]
+    else:
+        q = torch.randn(B, N, 3 * C, device="cuda", generator=g).bfloat16().requires_grad_(True)
+        o = nn.attention(q, None, heads)
+        qr = q.detach().float().requires_grad_(True)
+        Q, K, V = qr[..., :C], qr[..., C:2 * C], qr[..., 2 * C:]
+
+    def sp(t, n):
+        return t.reshape(B, n, heads, 64).transpose(1, 2)
+
+    ref = F.scaled_dot_product_attention(sp(Q, N), sp(K, Nk), sp(V, Nk)).transpose(1, 2).reshape(B, N, C)
+    assert _rel(o, ref) < 2e-2
+    do = torch.randn_like(o)
+    o.backward(do)
+    ref.backward(do.float())
+    assert _rel(q.grad, qr.grad) < 3e-2
+    if cross:
+        assert _rel(kv.grad, kvr.grad) < 3e-2
