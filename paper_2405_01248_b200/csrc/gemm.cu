@@ -54,10 +54,11 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr uint32_t A_STAGE_BYTES = BM * BK * 2;
 
-template <int BN>
+template <int BN, int CG>
 struct TcCfg {
-  static constexpr uint32_t B_STAGE_BYTES = BN * BK * 2;
-  // as many 64-deep k-stages as fit in ~200 KB of shared memory (4 at BN=256, 8 at BN=64)
+  static constexpr int BNL = BN / CG;  // B columns staged per CTA (a CTA pair splits N)
+  static constexpr uint32_t B_STAGE_BYTES = BNL * BK * 2;
+  // as many 64-deep k-stages as fit next to the 16 KB epilogue staging buffers
   static constexpr int STAGES_FIT = 209 * 1024 / (A_STAGE_BYTES + B_STAGE_BYTES);
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256 ? 256 : 512);
@@ -186,14 +187,16 @@ DP_DEV void tile_coords(const TcParams& p, int t, Work& w) {
 }
 
 struct WorkIter {
-  int cursor, end;
-  DP_DEV void init(const TcParams& p) {
+  int cursor, end, unit, units;
+  DP_DEV void init(const TcParams& p, int cg) {
+    unit = blockIdx.x / cg;   // one work unit per CTA pair (cg = 2) or per CTA
+    units = gridDim.x / cg;
     if (p.stream_k) {
       const long long tot = (long long)p.tiles_m * p.tiles_n * p.nbatch * p.num_kb;
-      cursor = static_cast<int>(tot * blockIdx.x / gridDim.x);
-      end = static_cast<int>(tot * (blockIdx.x + 1) / gridDim.x);
+      cursor = static_cast<int>(tot * unit / units);
+      end = static_cast<int>(tot * (unit + 1) / units);
     } else {
-      cursor = blockIdx.x;
+      cursor = unit;
       end = p.tiles_m * p.tiles_n * p.nbatch * p.splits;
     }
   }
@@ -211,7 +214,7 @@ struct WorkIter {
       tile_coords(p, cursor - split * tiles, w);
       w.kb0 = split * p.kb_per_split;
       w.kb1 = min(p.num_kb, w.kb0 + p.kb_per_split);
-      cursor += gridDim.x;
+      cursor += units;
     }
     return true;
   }
@@ -270,12 +273,13 @@ DP_DEV void epilogue_math(const TcParams& p, int row, int n, int z1, int z2, con
 
 constexpr int EPI_STAGE_BYTES = 32 * 64;  // one 32 x 32 bf16 chunk
 
-template <int BN>
+template <int BN, int CG>
 __global__ void __launch_bounds__(256, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmD, const TcParams p) {
-  using Cfg = TcCfg<BN>;
+  using Cfg = TcCfg<BN, CG>;
   constexpr int STAGES = Cfg::STAGES;
+  constexpr int BNL = Cfg::BNL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -290,6 +294,10 @@ __global__ void __launch_bounds__(256, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // CTA pair (cta_group::2): rank 0 (leader) issues the M=256 MMAs; each CTA stages its own
+  // 128 rows of A and half of B's N columns, and owns its 128 rows of the accumulator.
+  const int crank = CG == 2 ? static_cast<int>(cluster_ctarank()) : 0;
+  const bool leader = crank == 0;
   if (threadIdx.x == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
@@ -300,26 +308,35 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 4 * CG);  // one arrival per epilogue warp of each CTA
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (CG == 2)
+      tmem_alloc_2sm<Cfg::TMEM_COLS>(tmem_slot);
+    else
+      tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (threadIdx.x == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producer (every CTA)
     int stage = 0;
     uint32_t phase = 0;
     WorkIter it;
-    it.init(p);
+    it.init(p, CG);
     Work wk;
     while (it.next(p, wk)) {
       const int z1 = wk.z1, z2 = wk.z2;
-      const int m0 = wk.m_blk * BM, n0 = wk.n_blk * BN;
+      const int m0 = wk.m_blk * (BM * CG) + crank * BM;
+      const int n0 = wk.n_blk * BN + crank * BNL;
       int cn = 0, ch = 0, cw = 0;
       if (p.a_mode == A_CONV) {
         pixel_origin(m0, p.P, p.Q, cn, ch, cw);
@@ -328,39 +345,45 @@ __global__ void __launch_bounds__(256, 1)
       }
       for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
-        mbar_expect_tx(&full[stage], A_STAGE_BYTES + Cfg::B_STAGE_BYTES);
+        if (leader) mbar_expect_tx(&full[stage], CG * (A_STAGE_BYTES + Cfg::B_STAGE_BYTES));
         uint8_t* a_dst = sA + stage * A_STAGE_BYTES;
         uint8_t* b_dst = sB + stage * Cfg::B_STAGE_BYTES;
+        uint64_t* fb = &full[stage];
+        auto load = [&](const CUtensorMap* m, void* dst, int c0, int c1, int c2, int c3) {
+          if constexpr (CG == 2)
+            tma_load_4d_2sm(m, fb, dst, c0, c1, c2, c3);
+          else
+            tma_load_4d(m, fb, dst, c0, c1, c2, c3);
+        };
         int pn = 0, ph = 0, pw = 0;
         if (p.a_mode == A_WG_DY || p.b_mode == B_WG_X) pixel_origin(kb * BK, p.P, p.Q, pn, ph, pw);
         switch (p.a_mode) {
           case A_KMAJ:
-            tma_load_4d(&tmA, &full[stage], a_dst, kb * BK, m0, z1, z2);
+            load(&tmA, a_dst, kb * BK, m0, z1, z2);
             break;
           case A_MNMAJ:
-            tma_load_4d(&tmA, &full[stage], a_dst, m0, kb * BK, z1, z2);
-            tma_load_4d(&tmA, &full[stage], a_dst + 8192, m0 + 64, kb * BK, z1, z2);
+            load(&tmA, a_dst, m0, kb * BK, z1, z2);
+            load(&tmA, a_dst + 8192, m0 + 64, kb * BK, z1, z2);
             break;
           case A_CONV: {
             const int tap = kb / p.cblk;
             const int cb = kb - tap * p.cblk;
             const int rr = tap / p.S, ss = tap - (tap / p.S) * p.S;
-            tma_load_4d(&tmA, &full[stage], a_dst, cb * BK, cw + ss, ch + rr, cn);
+            load(&tmA, a_dst, cb * BK, cw + ss, ch + rr, cn);
             break;
           }
           default:  // A_WG_DY
-            tma_load_4d(&tmA, &full[stage], a_dst, m0, pw, ph, pn);
-            tma_load_4d(&tmA, &full[stage], a_dst + 8192, m0 + 64, pw, ph, pn);
+            load(&tmA, a_dst, m0, pw, ph, pn);
+            load(&tmA, a_dst + 8192, m0 + 64, pw, ph, pn);
             break;
         }
         switch (p.b_mode) {
           case B_KMAJ:
-            tma_load_4d(&tmB, &full[stage], b_dst, kb * BK, n0, z1, z2);
+            load(&tmB, b_dst, kb * BK, n0, z1, z2);
             break;
           case B_MNMAJ:
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_4d(&tmB, &full[stage], b_dst + j * 8192, n0 + 64 * j, kb * BK, z1, z2);
+            for (int j = 0; j < BNL / 64; ++j) load(&tmB, b_dst + j * 8192, n0 + 64 * j, kb * BK, z1, z2);
             break;
           case B_DGRAD: {
             // B(n = input channel c, k = (tap, filter kk)) = w[kk][R-1-r][S-1-s][c]: the conv
@@ -369,20 +392,19 @@ __global__ void __launch_bounds__(256, 1)
             const int kk = kb - tap * p.cblk;
             const int rr = tap / p.S, ss = tap - (tap / p.S) * p.S;
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_4d(&tmB, &full[stage], b_dst + j * 8192, n0 + 64 * j, p.S - 1 - ss,
-                          p.Rf - 1 - rr, kk * BK);
+            for (int j = 0; j < BNL / 64; ++j)
+              load(&tmB, b_dst + j * 8192, n0 + 64 * j, p.S - 1 - ss, p.Rf - 1 - rr, kk * BK);
             break;
           }
           default: {  // B_WG_X
             const int hin = ph * p.stride - p.pad_h, win = pw * p.stride - p.pad_w;
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) {
+            for (int j = 0; j < BNL / 64; ++j) {
               const int nn = n0 + 64 * j;
               const int tap = nn / p.C;
               const int ci = nn - tap * p.C;
               const int rr = tap / p.S, ss = tap - (tap / p.S) * p.S;
-              tma_load_4d(&tmB, &full[stage], b_dst + j * 8192, ci, win + ss, hin + rr, pn);
+              load(&tmB, b_dst + j * 8192, ci, win + ss, hin + rr, pn);
             }
             break;
           }
@@ -393,17 +415,17 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     }
-  } else if (threadIdx.x == 32) {
-    // ------------------------------------------------------------ MMA issuer
+  } else if (threadIdx.x == 32 && leader) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA)
     const int a_mn = (p.a_mode == A_MNMAJ || p.a_mode == A_WG_DY) ? 1 : 0;
     const int b_mn = (p.b_mode != B_KMAJ) ? 1 : 0;
-    const uint32_t idesc = idesc_bf16_f32(BM, BN, a_mn, b_mn);
+    const uint32_t idesc = idesc_bf16_f32(BM * CG, BN, a_mn, b_mn);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     WorkIter it;
-    it.init(p);
+    it.init(p, CG);
     Work wk;
     while (it.next(p, wk)) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -420,32 +442,43 @@ __global__ void __launch_bounds__(256, 1)
                                       : smem_desc_sw128(a_addr + j * 32, 16, 1024);
           const uint64_t bdesc = b_mn ? smem_desc_sw128(b_addr + j * 2048, 8192, 1024)
                                       : smem_desc_sw128(b_addr + j * 32, 16, 1024);
-          tc_mma_bf16(d_tmem, adesc, bdesc, idesc, (kb > wk.kb0 || j > 0) ? 1u : 0u);
+          const uint32_t accum = (kb > wk.kb0 || j > 0) ? 1u : 0u;
+          if constexpr (CG == 2)
+            tc_mma_bf16_2sm(d_tmem, adesc, bdesc, idesc, accum);
+          else
+            tc_mma_bf16(d_tmem, adesc, bdesc, idesc, accum);
         }
-        tc_commit(&empty[stage]);
+        if constexpr (CG == 2)
+          tc_commit_2sm_mc(&empty[stage]);
+        else
+          tc_commit(&empty[stage]);
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
         }
       }
-      tc_commit(&tfull[acc]);
+      if constexpr (CG == 2)
+        tc_commit_2sm_mc(&tfull[acc]);
+      else
+        tc_commit(&tfull[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
   } else if (warp >= 4) {
-    // ------------------------------------------------------------ epilogue
+    // ------------------------------------------------------------ epilogue (every CTA)
     const int wq = warp - 4;
     int acc = 0;
     uint32_t acc_phase = 0;
     uint8_t* ebuf = sE + wq * 2 * EPI_STAGE_BYTES;
     int chunk_seq = 0;
+    const uint32_t tempty_leader0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
     WorkIter it;
-    it.init(p);
+    it.init(p, CG);
     Work wk;
     while (it.next(p, wk)) {
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row0 = wk.m_blk * BM + wq * 32;
+      const int row0 = wk.m_blk * (BM * CG) + crank * BM + wq * 32;
       const int row = row0 + lane;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
@@ -475,17 +508,29 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 2)
+          mbar_arrive_cluster(tempty_leader0 + acc * 8);
+        else
+          mbar_arrive(&tempty[acc]);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
     if (p.d_tma && lane == 0) bulk_wait_all();
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+    if constexpr (CG == 2)
+      tmem_dealloc_2sm<Cfg::TMEM_COLS>(tmem_base);
+    else
+      tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
   }
 }
 
@@ -555,13 +600,13 @@ static int make_map(CUtensorMap* map, const void* base, const uint64_t dims[4],
   return 0;
 }
 
-template <int BN>
+template <int BN, int CG>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
                      TcParams p, int max_ctas, cudaStream_t st) {
-  using Cfg = TcCfg<BN>;
+  using Cfg = TcCfg<BN, CG>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN>,
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, CG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(Cfg::SMEM));
     if (e != cudaSuccess) {
@@ -570,17 +615,40 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
     }
     attr_set = true;
   }
-  const long long total = p.stream_k ? (long long)p.tiles_m * p.tiles_n * p.nbatch * p.num_kb
+  const long long units = p.stream_k ? (long long)p.tiles_m * p.tiles_n * p.nbatch * p.num_kb
                                      : (long long)p.tiles_m * p.tiles_n * p.splits * p.nbatch;
-  const int grid = static_cast<int>(total < max_ctas ? total : max_ctas);
+  const int max_units = max_ctas / CG;
+  const int grid = CG * static_cast<int>(units < max_units ? units : max_units);
   if (grid <= 0) return 0;
-  tc_gemm_kernel<BN><<<grid, 256, Cfg::SMEM, st>>>(ma, mb, md, p);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, CG>, ma, mb, md, p);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("tc_gemm launch: ") + cudaGetErrorString(e));
     return e;
   }
   return 0;
+}
+
+// CTA pairs (cta_group::2, M = 256 per pair) halve the per-SM shared-memory traffic of B;
+// used when the 256-row tiling wastes no more rows than the 128-row one and each CTA's half
+// of the B tile is a legal TMA box (64-column multiples for MN-major B).
+static int decide_cg(int M, int bn, bool b_mn_major) {
+  if (M < 256) return 1;
+  if (b_mn_major && (bn / 2) % 64) return 1;
+  const long long r1 = (long long)((M + 127) / 128) * 128, r2 = (long long)((M + 255) / 256) * 256;
+  return r2 <= r1 ? 2 : 1;
 }
 
 // Tile width: minimise padded columns plus a per-tile overhead, e.g. N=320 -> 2 x 160,
@@ -619,19 +687,25 @@ static int make_dmap(CUtensorMap* md, TcParams& p, int M, int N, int b1, int b2)
   return 0;
 }
 
-static int launch_bn(int bn, const CUtensorMap& ma, const CUtensorMap& mb, TcParams& p, int M, int N,
-                     int b1, int b2, cudaStream_t st) {
+template <int CG>
+static int launch_cg(int bn, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
+                     TcParams& p, cudaStream_t st) {
+  switch (bn) {
+    case 64: return launch_tc<64, CG>(ma, mb, md, p, kNumSMs, st);
+    case 96: return launch_tc<96, CG>(ma, mb, md, p, kNumSMs, st);
+    case 128: return launch_tc<128, CG>(ma, mb, md, p, kNumSMs, st);
+    case 160: return launch_tc<160, CG>(ma, mb, md, p, kNumSMs, st);
+    case 192: return launch_tc<192, CG>(ma, mb, md, p, kNumSMs, st);
+    case 224: return launch_tc<224, CG>(ma, mb, md, p, kNumSMs, st);
+    default: return launch_tc<256, CG>(ma, mb, md, p, kNumSMs, st);
+  }
+}
+
+static int launch_bn(int bn, int cg, const CUtensorMap& ma, const CUtensorMap& mb, TcParams& p, int M,
+                     int N, int b1, int b2, cudaStream_t st) {
   CUtensorMap md = ma;
   make_dmap(&md, p, M, N, b1, b2);
-  switch (bn) {
-    case 64: return launch_tc<64>(ma, mb, md, p, kNumSMs, st);
-    case 96: return launch_tc<96>(ma, mb, md, p, kNumSMs, st);
-    case 128: return launch_tc<128>(ma, mb, md, p, kNumSMs, st);
-    case 160: return launch_tc<160>(ma, mb, md, p, kNumSMs, st);
-    case 192: return launch_tc<192>(ma, mb, md, p, kNumSMs, st);
-    case 224: return launch_tc<224>(ma, mb, md, p, kNumSMs, st);
-    default: return launch_tc<256>(ma, mb, md, p, kNumSMs, st);
-  }
+  return cg == 2 ? launch_cg<2>(bn, ma, mb, md, p, st) : launch_cg<1>(bn, ma, mb, md, p, st);
 }
 
 static void choose_split(TcParams& p, int requested, bool allowed) {
@@ -690,11 +764,12 @@ int tc_gemm(const DpGemmArgs* a, cudaStream_t st) {
     return DP_ERR_ARGS;
   }
   const int bn = pick_bn(a->N, a->b_mn_major != 0);
+  const int cg = decide_cg(a->M, bn, a->b_mn_major != 0);
   TcParams p{};
   p.M = a->M;
   p.N = a->N;
   p.num_kb = (a->K + BK - 1) / BK;
-  p.tiles_m = (a->M + BM - 1) / BM;
+  p.tiles_m = (a->M + BM * cg - 1) / (BM * cg);
   p.tiles_n = (a->N + bn - 1) / bn;
   p.batch1 = a->batch1 > 0 ? a->batch1 : 1;
   const int batch2 = a->batch2 > 0 ? a->batch2 : 1;
@@ -726,11 +801,11 @@ int tc_gemm(const DpGemmArgs* a, cudaStream_t st) {
       if (int e = make_map(&mb, a->B, d, s, box, ones)) return e;
     } else {
       const uint64_t d[4] = {(uint64_t)a->K, (uint64_t)a->N, (uint64_t)p.batch1, (uint64_t)batch2};
-      const uint32_t box[4] = {BK, (uint32_t)bn, 1, 1};
+      const uint32_t box[4] = {BK, (uint32_t)(bn / cg), 1, 1};
       if (int e = make_map(&mb, a->B, d, s, box, ones)) return e;
     }
   }
-  return launch_bn(bn, ma, mb, p, a->M, a->N, p.batch1, batch2, st);
+  return launch_bn(bn, cg, ma, mb, p, a->M, a->N, p.batch1, batch2, st);
 }
 
 // Tile the output pixels (P x Q per image, N images) with boxes of `pixels`
@@ -773,11 +848,12 @@ int tc_conv_fwd(const DpConvArgs* a, cudaStream_t st) {
     return DP_ERR_UNSUPPORTED;
   }
   const int bn = pick_bn(a->K, false);
+  const int cg = decide_cg(a->N * a->P * a->Q, bn, false);
   p.M = a->N * a->P * a->Q;
   p.N = a->K;
   p.cblk = a->C / 64;
   p.num_kb = a->R * a->S * p.cblk;
-  p.tiles_m = (p.M + BM - 1) / BM;
+  p.tiles_m = (p.M + BM * cg - 1) / (BM * cg);
   p.tiles_n = (a->K + bn - 1) / bn;
   p.batch1 = 1;
   p.nbatch = 1;
@@ -806,11 +882,11 @@ int tc_conv_fwd(const DpConvArgs* a, cudaStream_t st) {
     const int64_t Kdim = (int64_t)a->R * a->S * a->C;
     const uint64_t d[4] = {(uint64_t)Kdim, (uint64_t)a->K, 1, 1};
     const int64_t s[3] = {Kdim, 0, 0};
-    const uint32_t box[4] = {BK, (uint32_t)bn, 1, 1};
+    const uint32_t box[4] = {BK, (uint32_t)(bn / cg), 1, 1};
     const uint32_t ones[4] = {1, 1, 1, 1};
     if (int e = make_map(&mb, a->w, d, s, box, ones)) return e;
   }
-  return launch_bn(bn, ma, mb, p, p.M, p.N, 1, 1, st);
+  return launch_bn(bn, cg, ma, mb, p, p.M, p.N, 1, 1, st);
 }
 
 // Input gradient of a stride-1 convolution as an implicit GEMM over dy with the weights read
@@ -832,11 +908,12 @@ int tc_conv_dgrad(const DpConvArgs* a, cudaStream_t st) {
     return DP_ERR_UNSUPPORTED;
   }
   const int bn = pick_bn(a->C, true);
+  const int cg = decide_cg(a->N * a->H * a->W, bn, true);
   p.M = a->N * a->H * a->W;
   p.N = a->C;
   p.cblk = a->K / 64;
   p.num_kb = a->R * a->S * p.cblk;
-  p.tiles_m = (p.M + BM - 1) / BM;
+  p.tiles_m = (p.M + BM * cg - 1) / (BM * cg);
   p.tiles_n = (a->C + bn - 1) / bn;
   p.batch1 = 1;
   p.nbatch = 1;
@@ -868,7 +945,7 @@ int tc_conv_dgrad(const DpConvArgs* a, cudaStream_t st) {
     const uint32_t ones[4] = {1, 1, 1, 1};
     if (int e = make_map(&mb, a->w, d, s, box, ones)) return e;
   }
-  return launch_bn(bn, ma, mb, p, p.M, p.N, 1, 1, st);
+  return launch_bn(bn, cg, ma, mb, p, p.M, p.N, 1, 1, st);
 }
 
 // dW[k][r][s][c] += sum_{n,p,q} dy[n][p][q][k] * x[n][p*stride+r-pad][q*stride+s-pad][c]
@@ -884,10 +961,11 @@ int tc_conv_wgrad(const DpConvArgs* a, cudaStream_t st) {
   }
   const int Ntot = a->R * a->S * a->C;
   const int bn = pick_bn(Ntot, true);
+  const int cg = decide_cg(a->K, bn, true);
   p.M = a->K;
   p.N = Ntot;
   p.num_kb = (a->N * a->P * a->Q + BK - 1) / BK;
-  p.tiles_m = (a->K + BM - 1) / BM;
+  p.tiles_m = (a->K + BM * cg - 1) / (BM * cg);
   p.tiles_n = (Ntot + bn - 1) / bn;
   p.batch1 = 1;
   p.nbatch = 1;
@@ -919,7 +997,7 @@ int tc_conv_wgrad(const DpConvArgs* a, cudaStream_t st) {
     const uint32_t es[4] = {1, (uint32_t)a->stride, (uint32_t)a->stride, 1};
     if (int e = make_map(&mb, a->x, d, s, box, es)) return e;
   }
-  return launch_bn(bn, ma, mb, p, p.M, p.N, 1, 1, st);
+  return launch_bn(bn, cg, ma, mb, p, p.M, p.N, 1, 1, st);
 }
 
 // ====================================================================== fp32 / generic SIMT GEMM
