@@ -200,6 +200,13 @@ int dp_adamw(float* param, const float* grad, float* exp_avg, float* exp_avg_sq,
              void* param_bf16, int64_t n, float lr, float beta1, float beta2, float eps,
              float weight_decay, int step, float grad_scale, dp_stream_t stream);
 
+/* same update with the step counter on the device (*step_dev is incremented first; bc_dev
+   receives the two bias corrections) so that a captured CUDA graph can replay it */
+int dp_adamw_dev(float* param, const float* grad, float* exp_avg, float* exp_avg_sq,
+                 void* param_bf16, int64_t n, float lr, float beta1, float beta2, float eps,
+                 float weight_decay, int* step_dev, float* bc_dev, float grad_scale,
+                 dp_stream_t stream);
+
 /* ---- normalisation and softmax (norm.cu) ---- */
 /* GroupNorm(+SiLU) over NHWC [N][HW][C]; gamma/beta fp32 (NULL = no affine); mean/rstd fp32
    [N][G] saved for backward; workspace of dp_group_norm_workspace() bytes. */

@@ -103,6 +103,8 @@ _SIGNATURES = {
     "dp_cast": [c_int, c_int, c_void_p, c_void_p, c_i64, c_void_p],
     "dp_adamw": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_float, c_float, c_float,
                  c_float, c_float, c_int, c_float, c_void_p],
+    "dp_adamw_dev": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_float, c_float, c_float,
+                     c_float, c_float, c_void_p, c_void_p, c_float, c_void_p],
     # norm.cu
     "dp_group_norm_workspace": [c_int, c_int, c_int],
     "dp_group_norm_fwd": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,

@@ -406,7 +406,12 @@ __global__ void cast_kernel(const TI* __restrict__ x, TO* __restrict__ y, int64_
 __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
                              float* __restrict__ m, float* __restrict__ v,
                              __nv_bfloat16* __restrict__ p_bf16, int64_t n, float lr, float b1,
-                             float b2, float eps, float wd, float bc1, float bc2, float gscale) {
+                             float b2, float eps, float wd, float bc1, float bc2, float gscale,
+                             const float* __restrict__ bc_dev) {
+  if (bc_dev) {  // bias corrections of a device-side step counter (CUDA-graph replayable)
+    bc1 = bc_dev[0];
+    bc2 = bc_dev[1];
+  }
   const int64_t nv = n / 4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -537,6 +542,13 @@ __global__ void s2d_kernel(const T* __restrict__ x, T* __restrict__ y, int N, in
     else
       y[j] = x[i];
   }
+}
+
+// ++step; bc = (1 - b1^step, 1 - b2^step)   (one thread; precedes adamw_kernel in the stream)
+__global__ void adamw_step_kernel(int* step, float b1, float b2, float* bc) {
+  const int s = ++(*step);
+  bc[0] = 1.f - powf(b1, static_cast<float>(s));
+  bc[1] = 1.f - powf(b2, static_cast<float>(s));
 }
 
 }  // namespace dp
@@ -779,8 +791,25 @@ int dp_adamw(float* param, const float* grad, float* exp_avg, float* exp_avg_sq,
   adamw_kernel<<<ew_grid(n / 4 + 1), 256, 0, ST>>>(param, grad, exp_avg, exp_avg_sq,
                                                     mp<__nv_bfloat16>(param_bf16), n, lr, beta1,
                                                     beta2, eps, weight_decay, bc1, bc2,
-                                                    grad_scale);
+                                                    grad_scale, nullptr);
   return ew_check("adamw");
+}
+
+int dp_adamw_dev(float* param, const float* grad, float* exp_avg, float* exp_avg_sq,
+                 void* param_bf16, int64_t n, float lr, float beta1, float beta2, float eps,
+                 float weight_decay, int* step_dev, float* bc_dev, float grad_scale,
+                 dp_stream_t stream) {
+  if (n <= 0) return 0;
+  if (!aligned16(param) || !aligned16(grad) || !aligned16(exp_avg) || !aligned16(exp_avg_sq)) {
+    set_error("dp_adamw_dev: flat buffers must be 16-byte aligned");
+    return DP_ERR_ARGS;
+  }
+  adamw_step_kernel<<<1, 1, 0, ST>>>(step_dev, beta1, beta2, bc_dev);
+  adamw_kernel<<<ew_grid(n / 4 + 1), 256, 0, ST>>>(param, grad, exp_avg, exp_avg_sq,
+                                                    mp<__nv_bfloat16>(param_bf16), n, lr, beta1,
+                                                    beta2, eps, weight_decay, 1.f, 1.f, grad_scale,
+                                                    bc_dev);
+  return ew_check("adamw_dev");
 }
 
 }  // extern "C"

@@ -210,12 +210,70 @@ class Trainer:
             return pre.pop(i)
         return InputFeed(make_batch(self.data_spec, i), self.device, self.cfg.dtype, self.feed_mode)
 
+    # ------------------------------------------------------------------ CUDA graphs (world 1)
+    def enable_cuda_graph(self):
+        """Capture one steady-state iteration (U-Net fwd/bwd, AdamW, next batch's frozen
+        encoders) into a CUDA graph and replay it from then on. Single GPU only (the pipeline
+        programs of N > 1 interleave NCCL P2P); needs a fixed self-conditioning branch."""
+        from .runtime import _Streams
+        from . import telemetry
+
+        if self.ex.world != 1 or self.cfg.selfcond_p not in (0.0, 1.0):
+            raise ValueError("CUDA-graph replay needs world == 1 and a fixed self-conditioning branch")
+        if self.it == 0 and not self.ex.frozen_ready:
+            self.warmup_frozen()
+        self.ex.streams = _Streams(self.ex.device, single=True)
+        torch.cuda.synchronize()
+        self._g_cur = InputFeed(make_batch(self.data_spec, self.it), self.device, self.cfg.dtype, "device")
+        self._g_nxt = InputFeed(make_batch(self.data_spec, self.it + 1), self.device, self.cfg.dtype, "device")
+        # refresh the eager state so that frozen_ready holds batch `it` (capture executes nothing)
+        g_in = self.ex.frozen_ready
+        cur, nxt = self._g_cur, self._g_nxt
+        gb = self.ex.gb_of()
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        n0 = telemetry.total_launches()
+        with torch.cuda.stream(side):
+            self.ex.inputs = cur
+            with torch.cuda.graph(graph, stream=side):
+                loss = self.ex.run_iteration(lambda f, lo, hi: nxt.get(f, gb + lo, gb + hi),
+                                             cur.selfcond, has_next=True)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        self._graph_launches = telemetry.total_launches() - n0
+        self._graph = graph
+        self._graph_loss = loss
+        self._graph_in = g_in
+        self._graph_out = self.ex.frozen_ready
+        self.ex.frozen_ready = g_in
+
+    def _graph_step(self):
+        from . import telemetry
+
+        cur_b = self._feed(self.it)
+        nxt_b = self._feed(self.it + 1)
+        for k in ("t", "noise"):
+            self._g_cur.f[k].copy_(cur_b.get(k, 0, cur_b.f[k].shape[0]), non_blocking=True)
+        for k in ("images", "ids"):
+            self._g_nxt.f[k].copy_(nxt_b.get(k, 0, nxt_b.f[k].shape[0]), non_blocking=True)
+        self._graph.replay()
+        # frozen outputs of batch it+1 (graph outputs) -> the buffers the next replay reads
+        for c, pieces in self._graph_out.items():
+            for (a, b, st), (a2, b2, st2) in zip(pieces, self._graph_in[c]):
+                for k in st:
+                    st2[k].copy_(st[k], non_blocking=True)
+        telemetry.count("cuda_graph_replay", self._graph_launches)
+        self.it += 1
+        return self._graph_loss
+
     def warmup_frozen(self):
         self._cur = self._feed(self.it)
         self.ex.warmup(lambda f, lo, hi: self._cur.get(f, self.ex.gb_of() + lo, self.ex.gb_of() + hi))
 
     def step(self, has_next=True):
         """One iteration: train on batch `it` (frozen outputs ready), fill batch it+1."""
+        if getattr(self, "_graph", None) is not None and has_next:
+            return self._graph_step()
         if self.it == 0 and not self.ex.frozen_ready:
             self.warmup_frozen()
         cur = self._cur

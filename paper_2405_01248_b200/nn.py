@@ -119,10 +119,19 @@ class ParamStore:
 
     def adamw_step(self, lr=1e-4, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01, grad_scale=1.0,
                    rng=None):
-        """One AdamW step over the flat slice `rng` (default: everything)."""
+        """One AdamW step over the flat slice `rng` (default: everything). The step counter and
+        the bias corrections live on the device so the update is CUDA-graph replayable."""
         self.step += 1
         lo, hi = rng if rng is not None else (0, self.master.numel())
         if hi <= lo:
+            return
+        if self.master.is_cuda:
+            if getattr(self, "step_dev", None) is None:
+                self.step_dev = torch.zeros(1, device=self.master.device, dtype=torch.int32)
+                self.bc_dev = torch.zeros(2, device=self.master.device, dtype=torch.float32)
+            ops.adamw_dev(self.master[lo:hi], self.grad[lo:hi], self.exp_avg[lo:hi], self.exp_avg_sq[lo:hi],
+                          None if self.compute is self.master else self.compute[lo:hi],
+                          lr, betas[0], betas[1], eps, weight_decay, self.step_dev, self.bc_dev, grad_scale)
             return
         ops.adamw(self.master[lo:hi], self.grad[lo:hi], self.exp_avg[lo:hi], self.exp_avg_sq[lo:hi],
                   None if self.compute is self.master else self.compute[lo:hi],

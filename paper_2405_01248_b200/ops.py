@@ -71,7 +71,8 @@ def gemm(A, B, D, *, M, N, K, a_ld, b_ld, d_ld, a_mn=False, b_mn=False,
     fam = "tcgen05_gemm" if A.dtype == torch.bfloat16 else "simt_gemm"
     flops = 2.0 * M * N * K * max(1, batch[0]) * max(1, batch[1])
     telemetry.timed(fam, flops, lambda: check(_lib.lib().dp_gemm(ctypes.byref(args), _stream()), "dp_gemm"),
-                    sub="linear")
+                    sub=f"linear {M}x{N}x{K}{'a' if a_mn else ''}{'b' if b_mn else ''}x{batch[0] * batch[1]}"
+                    if telemetry.SHAPES else "linear")
     return D
 
 
@@ -415,6 +416,13 @@ def adamw(param, grad, exp_avg, exp_avg_sq, param_bf16, lr, beta1, beta2, eps, w
     check(_L().dp_adamw(_ptr(param), _ptr(grad), _ptr(exp_avg), _ptr(exp_avg_sq), _ptr(param_bf16),
                         param.numel(), lr, beta1, beta2, eps, weight_decay, step, grad_scale, _stream()),
           "dp_adamw")
+
+
+def adamw_dev(param, grad, exp_avg, exp_avg_sq, param_bf16, lr, beta1, beta2, eps, weight_decay,
+              step_dev, bc_dev, grad_scale=1.0):
+    check(_L().dp_adamw_dev(_ptr(param), _ptr(grad), _ptr(exp_avg), _ptr(exp_avg_sq), _ptr(param_bf16),
+                            param.numel(), lr, beta1, beta2, eps, weight_decay, _ptr(step_dev), _ptr(bc_dev),
+                            grad_scale, _stream()), "dp_adamw_dev", 2)
 
 
 _GN_WS = {}

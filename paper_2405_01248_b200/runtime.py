@@ -89,8 +89,8 @@ def _cat(parts):
 
 
 class _Streams:
-    def __init__(self, device):
-        self.cuda = device.type == "cuda"
+    def __init__(self, device, single=False):
+        self.cuda = device.type == "cuda" and not single
         if self.cuda:
             self.compute = torch.cuda.Stream(device=device, priority=-1)
             self.fill = torch.cuda.Stream(device=device, priority=0)

@@ -18,6 +18,7 @@ from collections import Counter
 import torch
 
 launches = Counter()
+SHAPES = False  # label GEMM launches by shape (tools/step_breakdown.py)
 _site = threading.local()
 
 
