@@ -213,6 +213,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--per-gpu-batch", type=int, default=32)
+    ap.add_argument("--graph", action="store_true",
+                    help="N=1: replay the captured iteration as a CUDA graph (measured: no gain, GPU-bound)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -230,15 +232,21 @@ def main():
     trainer = engine.Trainer.create("c2", world=world, rank=rank, world_batch=wb, profile=profile,
                                     device=f"cuda:{local}", **lay)
     W, K = args.warmup, args.steps
-    trainer.prefetch(W + K + 1, mode="device")
+    trainer.prefetch(2 * W + 2 * K + 2, mode="device")
     for _ in range(W):
         trainer.step()
+    # roofline pass (eager): every libdpipe launch bracketed by CUDA events on its stream
+    ms_k, kstats, _, _ = timed_steps(trainer, K, world, kernel_timer=True)
+    use_graph = world == 1 and args.graph
+    if use_graph:
+        # N = 1: the whole iteration (U-Net fwd/bwd, AdamW, next batch's VAE + CLIP) is
+        # captured once and replayed as one CUDA graph (no per-kernel host dispatch)
+        trainer.enable_cuda_graph()
+        for _ in range(W):
+            trainer.step()
     with Clocks(local) as clk:
         ms, _, launches, _ = timed_steps(trainer, K, world)
     value = wb * K / (ms / 1000.0)
-    # roofline pass: same steps again with every libdpipe launch bracketed by CUDA events
-    trainer.prefetch(K + 1, mode="device")
-    ms_k, kstats, _, _ = timed_steps(trainer, K, world, kernel_timer=True)
 
     # speedup vs the same executor's unfilled pipeline (frozen part data-parallel, un-overlapped)
     speedup = 1.0
@@ -298,7 +306,8 @@ def main():
             "config": {"workload": WORKLOAD, "world_batch": wb, "group_batch": wb * lay["D"] // world,
                        "S": lay["S"], "M": lay["M"], "D": lay["D"], "groups": world // lay["D"],
                        "parallelism": f"pp{lay['S']}xdp{world // lay['S']}",
-                       "l2": "working set (weights 1.7 GB bf16 + activations) >> 126 MB L2"},
+                       "l2": "working set (weights 1.7 GB bf16 + activations) >> 126 MB L2",
+                       "dispatch": "cuda_graph" if use_graph else "eager"},
             "bubble_ratio_predicted_before": res["bubble_ratio_before"],
             "bubble_ratio_predicted_after": res["bubble_ratio_after"],
             "speedup_vs_unfilled": speedup,

@@ -551,6 +551,138 @@ __global__ void adamw_step_kernel(int* step, float b1, float b2, float* bc) {
   bc[1] = 1.f - powf(b2, static_cast<float>(s));
 }
 
+// ------------------------------------------------------------------ 16-byte vector variants
+// x [rows][2F] = [a | g] -> y [rows][F] = a * gelu(g): one vector of V features per thread
+template <typename T>
+__global__ void geglu_fwd_vec_kernel(const T* __restrict__ x, T* __restrict__ y, int64_t rows, int F) {
+  constexpr int V = VecT<T>::N;
+  const int FV = F / V;
+  const int64_t n = rows * FV;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / FV;
+    const int fv = static_cast<int>(i - r * FV);
+    float a[V], g[V];
+    load_vec(x + r * 2 * F + fv * V, a);
+    load_vec(x + r * 2 * F + F + fv * V, g);
+#pragma unroll
+    for (int j = 0; j < V; ++j) a[j] *= gelu_erf(g[j]);
+    store_vec(y + r * F + fv * V, a);
+  }
+}
+template <typename T>
+__global__ void geglu_bwd_vec_kernel(const T* __restrict__ x, const T* __restrict__ dy,
+                                     T* __restrict__ dx, int64_t rows, int F) {
+  constexpr int V = VecT<T>::N;
+  const int FV = F / V;
+  const int64_t n = rows * FV;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / FV;
+    const int fv = static_cast<int>(i - r * FV);
+    float a[V], g[V], d[V], da[V], dg[V];
+    load_vec(x + r * 2 * F + fv * V, a);
+    load_vec(x + r * 2 * F + F + fv * V, g);
+    load_vec(dy + r * F + fv * V, d);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      da[j] = d[j] * gelu_erf(g[j]);
+      dg[j] = d[j] * a[j] * gelu_erf_grad(g[j]);
+    }
+    store_vec(dx + r * 2 * F + fv * V, da);
+    store_vec(dx + r * 2 * F + F + fv * V, dg);
+  }
+}
+
+template <typename T>
+__global__ void concat_vec_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ dst,
+                                  int64_t rows, int Ca, int Cb) {
+  constexpr int V = VecT<T>::N;
+  const int CVa = Ca / V, CV = (Ca + Cb) / V, CVb = Cb / V;
+  const int64_t n = rows * CV;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / CV;
+    const int cv = static_cast<int>(i - r * CV);
+    uint4 u = make_uint4(0, 0, 0, 0);
+    if (cv < CVa)
+      u = *reinterpret_cast<const uint4*>(a + (r * CVa + cv) * V);
+    else if (b)
+      u = *reinterpret_cast<const uint4*>(b + (r * CVb + cv - CVa) * V);
+    *reinterpret_cast<uint4*>(dst + i * V) = u;
+  }
+}
+
+template <typename T>
+__global__ void split_vec_kernel(const T* __restrict__ src, T* __restrict__ a, T* __restrict__ b,
+                                 int64_t rows, int Ca, int Cb, int acc_a, int acc_b) {
+  constexpr int V = VecT<T>::N;
+  const int CVa = Ca / V, CV = (Ca + Cb) / V, CVb = Cb / V;
+  const int64_t n = rows * CV;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / CV;
+    const int cv = static_cast<int>(i - r * CV);
+    T* o;
+    int acc;
+    if (cv < CVa) {
+      o = a ? a + (r * CVa + cv) * V : nullptr;
+      acc = acc_a;
+    } else {
+      o = b ? b + (r * CVb + cv - CVa) * V : nullptr;
+      acc = acc_b;
+    }
+    if (!o) continue;
+    if (acc) {
+      float s[V], t[V];
+      load_vec(src + i * V, s);
+      load_vec(o, t);
+#pragma unroll
+      for (int j = 0; j < V; ++j) s[j] += t[j];
+      store_vec(o, s);
+    } else {
+      *reinterpret_cast<uint4*>(o) = *reinterpret_cast<const uint4*>(src + i * V);
+    }
+  }
+}
+
+// db[c] += sum_r dy[r][c] with 16-byte loads: block = 32 channel vectors x 8 row lanes
+template <typename T>
+__global__ void __launch_bounds__(256) bias_grad_vec_kernel(const T* __restrict__ dy, float* __restrict__ db,
+                                                            int64_t rows, int C, int seg) {
+  constexpr int V = VecT<T>::N;
+  const int CV = C / V;
+  const int cv = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int ry = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.y * seg;
+  const int64_t r1 = min(rows, r0 + seg);
+  float acc[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) acc[j] = 0.f;
+  if (cv < CV) {
+#pragma unroll 4
+    for (int64_t r = r0 + ry; r < r1; r += 8) {
+      float f[V];
+      load_vec(dy + r * C + cv * V, f);
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[j] += f[j];
+    }
+  }
+  __shared__ float red[8][32 * 8 + 1];
+#pragma unroll
+  for (int j = 0; j < V; ++j) red[ry][(threadIdx.x & 31) * V + j] = acc[j];
+  __syncthreads();
+  for (int t = threadIdx.x; t < 32 * V; t += 256) {
+    const int c = blockIdx.x * 32 * V + t;
+    if (c < C) {
+      float s = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += red[k][t];
+      atomicAdd(db + c, s);
+    }
+  }
+}
+
 }  // namespace dp
 
 using namespace dp;
@@ -603,6 +735,12 @@ int dp_act_bwd(int op, int dtype, const void* x, const void* dy, void* dx, int64
 
 int dp_geglu_fwd(int dtype, const void* x, void* y, int64_t rows, int F, dp_stream_t stream) {
   if (rows <= 0) return 0;
+  const int V = dtype == DP_F32 ? 4 : 8;
+  if (F % V == 0 && aligned16(x) && aligned16(y)) {
+    DISPATCH_T(dtype, geglu_fwd_vec_kernel<T><<<ew_grid(rows * F / V), 256, 0, ST>>>(
+                          cp<T>(x), mp<T>(y), rows, F));
+    return ew_check("geglu_fwd");
+  }
   DISPATCH_T(dtype, geglu_fwd_kernel<T><<<ew_grid(rows * F), 256, 0, ST>>>(cp<T>(x), mp<T>(y),
                                                                              rows, F));
   return ew_check("geglu_fwd");
@@ -611,6 +749,12 @@ int dp_geglu_fwd(int dtype, const void* x, void* y, int64_t rows, int F, dp_stre
 int dp_geglu_bwd(int dtype, const void* x, const void* dy, void* dx, int64_t rows, int F,
                  dp_stream_t stream) {
   if (rows <= 0) return 0;
+  const int V = dtype == DP_F32 ? 4 : 8;
+  if (F % V == 0 && aligned16(x) && aligned16(dy) && aligned16(dx)) {
+    DISPATCH_T(dtype, geglu_bwd_vec_kernel<T><<<ew_grid(rows * F / V), 256, 0, ST>>>(
+                          cp<T>(x), cp<T>(dy), mp<T>(dx), rows, F));
+    return ew_check("geglu_bwd");
+  }
   DISPATCH_T(dtype, geglu_bwd_kernel<T><<<ew_grid(rows * F), 256, 0, ST>>>(
                         cp<T>(x), cp<T>(dy), mp<T>(dx), rows, F));
   return ew_check("geglu_bwd");
@@ -692,6 +836,12 @@ int dp_embed(int dtype, const int64_t* ids, const void* table, const void* pos, 
 int dp_concat(int dtype, const void* a, const void* b, void* dst, int64_t rows, int Ca, int Cb,
               dp_stream_t stream) {
   if (rows <= 0) return 0;
+  const int V = dtype == DP_F32 ? 4 : 8;
+  if (Ca % V == 0 && Cb % V == 0 && aligned16(a) && aligned16(dst) && (!b || aligned16(b))) {
+    DISPATCH_T(dtype, concat_vec_kernel<T><<<ew_grid(rows * (Ca + Cb) / V), 256, 0, ST>>>(
+                          cp<T>(a), cp<T>(b), mp<T>(dst), rows, Ca, Cb));
+    return ew_check("concat");
+  }
   DISPATCH_T(dtype, concat_kernel<T><<<ew_grid(rows * (Ca + Cb)), 256, 0, ST>>>(
                         cp<T>(a), cp<T>(b), mp<T>(dst), rows, Ca, Cb));
   return ew_check("concat");
@@ -700,6 +850,12 @@ int dp_concat(int dtype, const void* a, const void* b, void* dst, int64_t rows, 
 int dp_split(int dtype, const void* src, void* a, void* b, int64_t rows, int Ca, int Cb,
              int acc_a, int acc_b, dp_stream_t stream) {
   if (rows <= 0) return 0;
+  const int V = dtype == DP_F32 ? 4 : 8;
+  if (Ca % V == 0 && Cb % V == 0 && aligned16(src) && (!a || aligned16(a)) && (!b || aligned16(b))) {
+    DISPATCH_T(dtype, split_vec_kernel<T><<<ew_grid(rows * (Ca + Cb) / V), 256, 0, ST>>>(
+                          cp<T>(src), mp<T>(a), mp<T>(b), rows, Ca, Cb, acc_a, acc_b));
+    return ew_check("split");
+  }
   DISPATCH_T(dtype, split_kernel<T><<<ew_grid(rows * (Ca + Cb)), 256, 0, ST>>>(
                         cp<T>(src), mp<T>(a), mp<T>(b), rows, Ca, Cb, acc_a, acc_b));
   return ew_check("split");
@@ -772,6 +928,17 @@ int dp_space_to_depth(int dtype, const void* x, void* y, int N, int H, int W, in
 
 int dp_bias_grad(int dtype, const void* dy, float* db, int64_t rows, int C, dp_stream_t stream) {
   if (rows <= 0) return 0;
+  const int V = dtype == DP_F32 ? 4 : 8;
+  if (C % V == 0 && aligned16(dy)) {
+    // 16-byte vectors: a block covers 32 vectors (256 bf16 channels) x 8 row lanes
+    const int CV = C / V;
+    int64_t seg = (rows * ((CV + 31) / 32) + 2 * kNumSMs - 1) / (2 * kNumSMs);  // ~2 waves
+    seg = seg < 64 ? 64 : seg;
+    dim3 grid((CV + 31) / 32, static_cast<unsigned>((rows + seg - 1) / seg));
+    DISPATCH_T(dtype, bias_grad_vec_kernel<T><<<grid, 256, 0, ST>>>(cp<T>(dy), db, rows, C,
+                                                                      static_cast<int>(seg)));
+    return ew_check("bias_grad");
+  }
   const int seg = 512;
   dim3 grid((C + 31) / 32, static_cast<unsigned>((rows + seg - 1) / seg));
   DISPATCH_T(dtype, bias_grad_kernel<T><<<grid, 256, 0, ST>>>(cp<T>(dy), db, rows, C, seg));

@@ -107,7 +107,24 @@ __global__ void __launch_bounds__(GN_THREADS) gn_partial_kernel(const T* __restr
 #pragma unroll
     for (int j = 0; j < V; ++j) mean[j] = m2[j] = 0.f;
     if (active) {
-      for (int p = p0 + rl; p < p1; p += rows_par) {
+      int p = p0 + rl;
+      for (; p + 3 * rows_par < p1; p += 4 * rows_par) {  // 4 loads in flight
+        float f[4][V];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) ld16(xs + (int64_t)(p + u * rows_par) * C + cv * V, f[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          cnt += 1.f;
+          const float inv = 1.f / cnt;
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            const float d = f[u][j] - mean[j];
+            mean[j] += d * inv;
+            m2[j] += d * (f[u][j] - mean[j]);
+          }
+        }
+      }
+      for (; p < p1; p += rows_par) {
         float f[V];
         ld16(xs + (int64_t)p * C + cv * V, f);
         cnt += 1.f;
@@ -212,7 +229,24 @@ __global__ void __launch_bounds__(GN_THREADS)
     const T* xp = xs + (int64_t)(p0 + rl) * C + cv * V;
     T* yp = ys + (int64_t)(p0 + rl) * C + cv * V;
     const int64_t step = (int64_t)rows_par * C;
-    for (int p = p0 + rl; p < p1; p += rows_par, xp += step, yp += step) {
+    // 4 independent 16-byte loads in flight per thread (memory-level parallelism)
+    int p = p0 + rl;
+    for (; p + 3 * rows_par < p1; p += 4 * rows_par, xp += 4 * step, yp += 4 * step) {
+      float f[4][V];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) ld16(xp + u * step, f[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          float v = fmaf(f[u][j], a[j], b[j]);
+          if (silu_on) v = v / (1.f + __expf(-v));
+          f[u][j] = v;
+        }
+        st16(yp + u * step, f[u]);
+      }
+    }
+    for (; p < p1; p += rows_par, xp += step, yp += step) {
       float f[V];
       ld16(xp, f);
 #pragma unroll
@@ -263,6 +297,7 @@ __global__ void __launch_bounds__(GN_THREADS)
         ga[j] = gamma ? gamma[c] : 1.f;
         be[j] = gamma ? beta[c] : 0.f;
       }
+#pragma unroll 2
       for (int p = p0 + rl; p < p1; p += rows_par) {
         float fx[V], fd[V];
         ld16(x + base + (int64_t)p * C + cv * V, fx);
@@ -358,6 +393,7 @@ __global__ void __launch_bounds__(GN_THREADS)
     }
     const int64_t step = (int64_t)rows_par * C;
     int64_t off = base + (int64_t)(p0 + rl) * C + cv * V;
+#pragma unroll 2
     for (int p = p0 + rl; p < p1; p += rows_par, off += step) {
       float fx[V], fd[V], fo[V];
       ld16(x + off, fx);
@@ -393,32 +429,46 @@ static void gn_split(int N, int HW, int& chunks, int& ppc) {
 
 // ------------------------------------------------------------------ LayerNorm
 // one warp per row; per-lane strided elements (coalesced across the warp)
-template <typename T, int PER>
+// one warp per row; lane owns 16-byte vectors lane, lane+32, ... (NVEC per lane) -> fully
+// coalesced 512-byte warp accesses, the row kept in registers for the two-pass statistics
+template <typename T, int NVEC>
 __global__ void __launch_bounds__(256)
     ln_fwd_kernel(const T* __restrict__ x, const float* __restrict__ gamma,
                   const float* __restrict__ beta, const T* __restrict__ mod,
                   int64_t mod_ld, int shift_off, int scale_off, int rps, T* __restrict__ y,
                   float* __restrict__ mean_out, float* __restrict__ rstd_out, int64_t rows, int C,
                   float eps) {
+  constexpr int V = NV<T>::V;
   const int lane = threadIdx.x & 31;
   const int64_t row = blockIdx.x * 8LL + (threadIdx.x >> 5);
   if (row >= rows) return;
+  const int CV = C / V;
   const T* xr = x + row * C;
-  float v[PER];
+  float v[NVEC][V];
   float s = 0.f;
 #pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    const int c = lane + 32 * k;
-    v[k] = c < C ? to_f(xr[c]) : 0.f;
-    s += v[k];
+  for (int k = 0; k < NVEC; ++k) {
+    const int cv = lane + 32 * k;
+    if (cv < CV) {
+      ld16(xr + cv * V, v[k]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < V; ++j) v[k][j] = 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) s += v[k][j];
   }
   const float mu = warp_sum(s) / C;
   float q = 0.f;
 #pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    const int c = lane + 32 * k;
-    const float d = c < C ? v[k] - mu : 0.f;
-    q += d * d;
+  for (int k = 0; k < NVEC; ++k) {
+    if (lane + 32 * k < CV) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const float d = v[k][j] - mu;
+        q += d * d;
+      }
+    }
   }
   const float rs = rsqrtf(warp_sum(q) / C + eps);
   if (lane == 0) {
@@ -428,58 +478,75 @@ __global__ void __launch_bounds__(256)
   T* yr = y + row * C;
   const T* mr = mod ? mod + (row / rps) * mod_ld : nullptr;
 #pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    const int c = lane + 32 * k;
-    if (c < C) {
-      float o = (v[k] - mu) * rs;
-      if (gamma) o = o * gamma[c] + beta[c];
-      if (mr) o = o * (1.f + to_f(mr[scale_off + c])) + to_f(mr[shift_off + c]);
-      yr[c] = from_f<T>(o);
+  for (int k = 0; k < NVEC; ++k) {
+    const int cv = lane + 32 * k;
+    if (cv < CV) {
+      float o[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const int c = cv * V + j;
+        float t = (v[k][j] - mu) * rs;
+        if (gamma) t = fmaf(t, __ldg(gamma + c), __ldg(beta + c));
+        if (mr) t = fmaf(t, 1.f + to_f(mr[scale_off + c]), to_f(mr[shift_off + c]));
+        o[j] = t;
+      }
+      st16(yr + cv * V, o);
     }
   }
 }
 
-template <typename T, int PER>
+template <typename T, int NVEC>
 __global__ void __launch_bounds__(256)
     ln_bwd_kernel(const T* __restrict__ x, const T* __restrict__ dy,
                   const float* __restrict__ gamma, const T* __restrict__ mod, int64_t mod_ld,
                   int scale_off, int rps, const float* __restrict__ mean,
                   const float* __restrict__ rstd, T* __restrict__ dx, int64_t rows, int C,
                   int accumulate) {
+  constexpr int V = NV<T>::V;
   const int lane = threadIdx.x & 31;
   const int64_t row = blockIdx.x * 8LL + (threadIdx.x >> 5);
   if (row >= rows) return;
+  const int CV = C / V;
   const float mu = mean[row], rs = rstd[row];
   const T* xr = x + row * C;
   const T* dr = dy + row * C;
   const T* mr = mod ? mod + (row / rps) * mod_ld : nullptr;
-  float xh[PER], g[PER];
+  float xh[NVEC][V], g[NVEC][V];
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    const int c = lane + 32 * k;
-    if (c < C) {
-      xh[k] = (to_f(xr[c]) - mu) * rs;
-      float d = to_f(dr[c]);
-      if (gamma) d *= gamma[c];
-      if (mr) d *= 1.f + to_f(mr[scale_off + c]);
-      g[k] = d;
-    } else {
-      xh[k] = g[k] = 0.f;
+  for (int k = 0; k < NVEC; ++k) {
+    const int cv = lane + 32 * k;
+    if (cv < CV) {
+      ld16(xr + cv * V, xh[k]);
+      ld16(dr + cv * V, g[k]);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const int c = cv * V + j;
+        xh[k][j] = (xh[k][j] - mu) * rs;
+        float d = g[k][j];
+        if (gamma) d *= __ldg(gamma + c);
+        if (mr) d *= 1.f + to_f(mr[scale_off + c]);
+        g[k][j] = d;
+        s1 += d;
+        s2 += d * xh[k][j];
+      }
     }
-    s1 += g[k];
-    s2 += g[k] * xh[k];
   }
   s1 = warp_sum(s1) / C;
   s2 = warp_sum(s2) / C;
   T* xo = dx + row * C;
 #pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    const int c = lane + 32 * k;
-    if (c < C) {
-      float o = rs * (g[k] - s1 - xh[k] * s2);
-      if (accumulate) o += to_f(xo[c]);
-      xo[c] = from_f<T>(o);
+  for (int k = 0; k < NVEC; ++k) {
+    const int cv = lane + 32 * k;
+    if (cv < CV) {
+      float o[V], prev[V];
+      if (accumulate) ld16(xo + cv * V, prev);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        o[j] = rs * (g[k][j] - s1 - xh[k][j] * s2);
+        if (accumulate) o[j] += prev[j];
+      }
+      st16(xo + cv * V, o);
     }
   }
 }
@@ -646,14 +713,17 @@ int dp_group_norm_bwd(int dtype, const void* x, const void* dy, const float* gam
 
 #define LN_PER_DISPATCH(C, KERNEL, ...)                                               \
   do {                                                                                \
-    if ((C) <= 256) {                                                                 \
+    const int nvec = ((C) / NV<T>::V + 31) / 32;                                      \
+    if (nvec <= 1) {                                                                  \
+      KERNEL<T, 1><<<grid, 256, 0, ST>>>(__VA_ARGS__);                                \
+    } else if (nvec <= 2) {                                                           \
+      KERNEL<T, 2><<<grid, 256, 0, ST>>>(__VA_ARGS__);                                \
+    } else if (nvec <= 4) {                                                           \
+      KERNEL<T, 4><<<grid, 256, 0, ST>>>(__VA_ARGS__);                                \
+    } else if (nvec <= 8) {                                                           \
       KERNEL<T, 8><<<grid, 256, 0, ST>>>(__VA_ARGS__);                                \
-    } else if ((C) <= 512) {                                                          \
-      KERNEL<T, 16><<<grid, 256, 0, ST>>>(__VA_ARGS__);                               \
-    } else if ((C) <= 1024) {                                                         \
-      KERNEL<T, 32><<<grid, 256, 0, ST>>>(__VA_ARGS__);                               \
     } else {                                                                          \
-      KERNEL<T, 64><<<grid, 256, 0, ST>>>(__VA_ARGS__);                               \
+      KERNEL<T, 16><<<grid, 256, 0, ST>>>(__VA_ARGS__);                               \
     }                                                                                 \
   } while (0)
 
@@ -662,8 +732,10 @@ int dp_layer_norm_fwd(int dtype, const void* x, const float* gamma, const float*
                       int rows_per_sample, void* y, float* mean, float* rstd, int64_t rows, int C,
                       float eps, dp_stream_t stream) {
   if (rows <= 0) return 0;
-  if (C > 2048 || (gamma && mod)) {
-    set_error("layer_norm: C <= 2048 and affine/modulation are exclusive");
+  if (C > 2048 || (gamma && mod) || C % (dtype == DP_F32 ? 4 : 8) ||
+      (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) % 16) {
+    set_error("layer_norm: C <= 2048, C % 8 == 0 (bf16) / 4 (fp32), 16-byte aligned rows, "
+              "affine and modulation exclusive");
     return DP_ERR_ARGS;
   }
   const dim3 grid(static_cast<unsigned>((rows + 7) / 8));
@@ -679,8 +751,11 @@ int dp_layer_norm_bwd(int dtype, const void* x, const void* dy, const float* gam
                       float* dgamma, float* dbeta, void* dmod, int64_t dmod_ld, int64_t rows,
                       int C, int accumulate, dp_stream_t stream) {
   if (rows <= 0) return 0;
-  if (C > 2048 || (gamma && mod)) {
-    set_error("layer_norm: C <= 2048 and affine/modulation are exclusive");
+  if (C > 2048 || (gamma && mod) || C % (dtype == DP_F32 ? 4 : 8) ||
+      (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy) |
+       reinterpret_cast<uintptr_t>(dx)) % 16) {
+    set_error("layer_norm: C <= 2048, C % 8 == 0 (bf16) / 4 (fp32), 16-byte aligned rows, "
+              "affine and modulation exclusive");
     return DP_ERR_ARGS;
   }
   const int rps = rows_per_sample > 0 ? rows_per_sample : 1;
