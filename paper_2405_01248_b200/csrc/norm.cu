@@ -75,163 +75,178 @@ DP_DEV Welford wf_merge(Welford a, Welford b) {
   return r;
 }
 
+// ------------------------------------------------------------------ GroupNorm
+// Grid (pixel chunks, N, channel blocks); a channel block covers whole groups, so one CTA
+// owns the statistics of its groups over its pixel chunk. Small feature maps (U-Net 8x8 /
+// 16x16 levels) get parallelism from channel blocks, large ones (VAE 256x256) from chunks.
+// Stats: per-channel shifted sums (shift = the chunk's first value of that channel) ->
+// (count, mean, M2) per group and chunk; chunks merged with Chan's formula (deterministic).
 constexpr int GN_THREADS = 256;
 constexpr int GN_MAX_C = 2560;
 
-// pixels [p0, p1) of sample n; thread layout: cv = tid % CV (channel vector), rl = tid / CV
+struct GnGeom {
+  int chunks, ppc, nblk, CB;
+};
+
+template <int V>
+static GnGeom gn_geom(int N, int HW, int C, int G) {
+  GnGeom g{};
+  // ~16 waves of CTAs: small per-CTA pixel chunks keep the tail of the last wave short
+  int target = (16 * kNumSMs + N - 1) / N;
+  const int maxc = (HW + 127) / 128;
+  g.chunks = target < maxc ? target : maxc;
+  if (g.chunks < 1) g.chunks = 1;
+  g.ppc = (HW + g.chunks - 1) / g.chunks;
+  g.chunks = (HW + g.ppc - 1) / g.ppc;
+  g.nblk = 1;
+  while ((long long)g.chunks * N * g.nblk < 2 * kNumSMs && g.nblk * 2 <= G && G % (g.nblk * 2) == 0 &&
+         (C / (g.nblk * 2)) % V == 0)
+    g.nblk *= 2;
+  g.CB = C / g.nblk;
+  return g;
+}
+
+// thread layout for a block of CVB channel vectors: vector cv0 + tid % width, pixel lane tid / width
+struct GnLanes {
+  int width, rows_par, cv, rl;
+  DP_DEV GnLanes(int CVB, int cv0) {
+    width = min(GN_THREADS, CVB - cv0);
+    rows_par = GN_THREADS / width;
+    cv = cv0 + threadIdx.x % width;
+    rl = threadIdx.x / width;
+  }
+};
+
 template <typename T>
-__global__ void __launch_bounds__(GN_THREADS) gn_partial_kernel(const T* __restrict__ x, int HW,
-                                                                int C, int G, int pix_per_chunk,
-                                                                float* __restrict__ part) {
+__global__ void __launch_bounds__(GN_THREADS)
+    gn_partial_kernel(const T* __restrict__ x, int HW, int C, int G, int ppc, int CB,
+                      float* __restrict__ part) {
   constexpr int V = NV<T>::V;
-  const int CV = C / V;
   const int n = blockIdx.y, chunk = blockIdx.x, nchunks = gridDim.x;
-  const int p0 = chunk * pix_per_chunk;
-  const int p1 = min(HW, p0 + pix_per_chunk);
-  __shared__ float s_n[GN_MAX_C], s_mean[GN_MAX_C], s_m2[GN_MAX_C];
-  for (int c = threadIdx.x; c < C; c += GN_THREADS) {
-    s_n[c] = 0.f;
-    s_mean[c] = 0.f;
-    s_m2[c] = 0.f;
+  const int c0 = blockIdx.z * CB;  // first channel of this block
+  const int CVB = CB / V;
+  const int p0 = chunk * ppc;
+  const int p1 = min(HW, p0 + ppc);
+  __shared__ float s1s[GN_MAX_C], s2s[GN_MAX_C];
+  __shared__ float shift[GN_MAX_C];
+  for (int c = threadIdx.x; c < CB; c += GN_THREADS) {
+    s1s[c] = 0.f;
+    s2s[c] = 0.f;
+    shift[c] = to_f(x[((int64_t)n * HW + p0) * C + c0 + c]);
   }
   __syncthreads();
-  const T* xs = x + (int64_t)n * HW * C;
-  // Threads loop over channel vectors in rounds so every vector gets covered even when CV > threads.
-  for (int cv0 = 0; cv0 < CV; cv0 += GN_THREADS) {
-    const int width = min(GN_THREADS, CV - cv0);
-    const int rows_par = GN_THREADS / width;
-    const int cv = cv0 + threadIdx.x % width;
-    const int rl = threadIdx.x / width;
-    const bool active = rl < rows_par;
-    float cnt = 0.f, mean[V], m2[V];
+  const T* xs = x + (int64_t)n * HW * C + c0;
+  for (int cv0 = 0; cv0 < CVB; cv0 += GN_THREADS) {
+    const GnLanes L(CVB, cv0);
+    if (L.rl >= L.rows_par) continue;
+    float k[V], a1[V], a2[V];
 #pragma unroll
-    for (int j = 0; j < V; ++j) mean[j] = m2[j] = 0.f;
-    if (active) {
-      int p = p0 + rl;
-      for (; p + 3 * rows_par < p1; p += 4 * rows_par) {  // 4 loads in flight
-        float f[4][V];
+    for (int j = 0; j < V; ++j) {
+      k[j] = shift[L.cv * V + j];
+      a1[j] = a2[j] = 0.f;
+    }
+    const T* xp = xs + (int64_t)(p0 + L.rl) * C + L.cv * V;
+    const int64_t step = (int64_t)L.rows_par * C;
+    int p = p0 + L.rl;
+    for (; p + 3 * L.rows_par < p1; p += 4 * L.rows_par, xp += 4 * step) {
+      float f[4][V];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) ld16(xs + (int64_t)(p + u * rows_par) * C + cv * V, f[u]);
+      for (int u = 0; u < 4; ++u) ld16(xp + u * step, f[u]);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          cnt += 1.f;
-          const float inv = 1.f / cnt;
-#pragma unroll
-          for (int j = 0; j < V; ++j) {
-            const float d = f[u][j] - mean[j];
-            mean[j] += d * inv;
-            m2[j] += d * (f[u][j] - mean[j]);
-          }
-        }
-      }
-      for (; p < p1; p += rows_par) {
-        float f[V];
-        ld16(xs + (int64_t)p * C + cv * V, f);
-        cnt += 1.f;
-        const float inv = 1.f / cnt;
+      for (int u = 0; u < 4; ++u)
 #pragma unroll
         for (int j = 0; j < V; ++j) {
-          const float d = f[j] - mean[j];
-          mean[j] += d * inv;
-          m2[j] += d * (f[j] - mean[j]);
+          const float d = f[u][j] - k[j];
+          a1[j] += d;
+          a2[j] = fmaf(d, d, a2[j]);
         }
+    }
+    for (; p < p1; p += L.rows_par, xp += step) {
+      float f[V];
+      ld16(xp, f);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const float d = f[j] - k[j];
+        a1[j] += d;
+        a2[j] = fmaf(d, d, a2[j]);
       }
     }
-    // merge the rows_par lanes of each channel through shared memory, one lane row at a
-    // time; every thread executes the same barriers (bar.sync is warp-aligned)
-    for (int r = 0; r < rows_par; ++r) {
-      if (active && rl == r && cnt > 0.f) {
 #pragma unroll
-        for (int j = 0; j < V; ++j) {
-          const int c = cv * V + j;
-          Welford a{s_n[c], s_mean[c], s_m2[c]};
-          Welford b{cnt, mean[j], m2[j]};
-          a = wf_merge(a, b);
-          s_n[c] = a.n;
-          s_mean[c] = a.mean;
-          s_m2[c] = a.m2;
-        }
-      }
-      __syncthreads();
+    for (int j = 0; j < V; ++j) {
+      atomicAdd(&s1s[L.cv * V + j], a1[j]);
+      atomicAdd(&s2s[L.cv * V + j], a2[j]);
     }
   }
   __syncthreads();
   const int cg = C / G;
-  for (int g = threadIdx.x; g < G; g += GN_THREADS) {
+  const int g0 = c0 / cg, gb = CB / cg;
+  const float cnt = static_cast<float>(p1 - p0);
+  for (int gi = threadIdx.x; gi < gb; gi += GN_THREADS) {
     Welford a{0.f, 0.f, 0.f};
-    for (int c = g * cg; c < (g + 1) * cg; ++c) a = wf_merge(a, Welford{s_n[c], s_mean[c], s_m2[c]});
-    float* o = part + (((int64_t)n * nchunks + chunk) * G + g) * 3;
+    for (int c = gi * cg; c < (gi + 1) * cg; ++c) {
+      const float m = s1s[c] / cnt;
+      a = wf_merge(a, Welford{cnt, shift[c] + m, fmaxf(s2s[c] - s1s[c] * m, 0.f)});
+    }
+    float* o = part + (((int64_t)n * nchunks + chunk) * G + g0 + gi) * 3;
     o[0] = a.n;
     o[1] = a.mean;
     o[2] = a.m2;
   }
 }
 
-// merge the chunk partials of sample n into s_mean/s_rstd [G]
-DP_DEV void gn_merge_stats(const float* part, int n, int nchunks, int G, float eps, float* s_mean,
-                           float* s_rstd) {
-  for (int g = threadIdx.x; g < G; g += blockDim.x) {
-    Welford a{0.f, 0.f, 0.f};
-    for (int k = 0; k < nchunks; ++k) {
-      const float* q = part + (((int64_t)n * nchunks + k) * G + g) * 3;
-      a = wf_merge(a, Welford{q[0], q[1], q[2]});
-    }
-    s_mean[g] = a.mean;
-    s_rstd[g] = rsqrtf(a.m2 / fmaxf(a.n, 1.f) + eps);
-  }
-}
-
-// Apply: each thread owns one 16-byte channel vector for the whole pixel range (no index
-// arithmetic in the streaming loop) with its per-channel affine folded into y = x*a + b.
 template <typename T>
-__global__ void __launch_bounds__(GN_THREADS)
+__global__ void __launch_bounds__(GN_THREADS, 4)
     gn_apply_kernel(const T* __restrict__ x, const float* __restrict__ gamma,
                     const float* __restrict__ beta, T* __restrict__ y,
                     float* __restrict__ mean_out, float* __restrict__ rstd_out,
-                    const float* __restrict__ part, int HW, int C, int G, int pix_per_chunk,
-                    float eps, int silu_on) {
+                    const float* __restrict__ part, int HW, int C, int G, int ppc, int CB, float eps,
+                    int silu_on) {
   constexpr int V = NV<T>::V;
   const int n = blockIdx.y, chunk = blockIdx.x, nchunks = gridDim.x;
+  const int c0 = blockIdx.z * CB;
+  const int cg = C / G;
+  const int g0 = c0 / cg, gb = CB / cg;
   __shared__ float s_mean[256], s_rstd[256];
   __shared__ float s_a[GN_MAX_C], s_b[GN_MAX_C];
-  gn_merge_stats(part, n, nchunks, G, eps, s_mean, s_rstd);
-  __syncthreads();
-  if (chunk == 0)
-    for (int g = threadIdx.x; g < G; g += GN_THREADS) {
-      mean_out[n * G + g] = s_mean[g];
-      rstd_out[n * G + g] = s_rstd[g];
+  for (int gi = threadIdx.x; gi < gb; gi += GN_THREADS) {
+    Welford a{0.f, 0.f, 0.f};
+    for (int k = 0; k < nchunks; ++k) {
+      const float* q = part + (((int64_t)n * nchunks + k) * G + g0 + gi) * 3;
+      a = wf_merge(a, Welford{q[0], q[1], q[2]});
     }
-  const int cg = C / G;
-  for (int c = threadIdx.x; c < C; c += GN_THREADS) {
-    const int g = c / cg;
-    const float a = s_rstd[g] * (gamma ? gamma[c] : 1.f);
-    s_a[c] = a;
-    s_b[c] = (gamma ? beta[c] : 0.f) - s_mean[g] * a;
+    s_mean[gi] = a.mean;
+    s_rstd[gi] = rsqrtf(a.m2 / fmaxf(a.n, 1.f) + eps);
+    if (chunk == 0) {
+      mean_out[n * G + g0 + gi] = s_mean[gi];
+      rstd_out[n * G + g0 + gi] = s_rstd[gi];
+    }
   }
   __syncthreads();
-  const int CV = C / V;
-  const int p0 = chunk * pix_per_chunk;
-  const int p1 = min(HW, p0 + pix_per_chunk);
-  const T* xs = x + (int64_t)n * HW * C;
-  T* ys = y + (int64_t)n * HW * C;
-  for (int cv0 = 0; cv0 < CV; cv0 += GN_THREADS) {
-    const int width = min(GN_THREADS, CV - cv0);
-    const int rows_par = GN_THREADS / width;
-    const int cv = cv0 + threadIdx.x % width;
-    const int rl = threadIdx.x / width;
-    if (rl >= rows_par) continue;
+  for (int c = threadIdx.x; c < CB; c += GN_THREADS) {
+    const int gi = c / cg;
+    const float a = s_rstd[gi] * (gamma ? gamma[c0 + c] : 1.f);
+    s_a[c] = a;
+    s_b[c] = (gamma ? beta[c0 + c] : 0.f) - s_mean[gi] * a;
+  }
+  __syncthreads();
+  const int CVB = CB / V;
+  const int p0 = chunk * ppc;
+  const int p1 = min(HW, p0 + ppc);
+  const int64_t base = (int64_t)n * HW * C + c0;
+  for (int cv0 = 0; cv0 < CVB; cv0 += GN_THREADS) {
+    const GnLanes L(CVB, cv0);
+    if (L.rl >= L.rows_par) continue;
     float a[V], b[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-      a[j] = s_a[cv * V + j];
-      b[j] = s_b[cv * V + j];
+      a[j] = s_a[L.cv * V + j];
+      b[j] = s_b[L.cv * V + j];
     }
-    const T* xp = xs + (int64_t)(p0 + rl) * C + cv * V;
-    T* yp = ys + (int64_t)(p0 + rl) * C + cv * V;
-    const int64_t step = (int64_t)rows_par * C;
-    // 4 independent 16-byte loads in flight per thread (memory-level parallelism)
-    int p = p0 + rl;
-    for (; p + 3 * rows_par < p1; p += 4 * rows_par, xp += 4 * step, yp += 4 * step) {
+    const int64_t step = (int64_t)L.rows_par * C;
+    const T* xp = x + base + (int64_t)(p0 + L.rl) * C + L.cv * V;
+    T* yp = y + base + (int64_t)(p0 + L.rl) * C + L.cv * V;
+    int p = p0 + L.rl;
+    for (; p + 3 * L.rows_par < p1; p += 4 * L.rows_par, xp += 4 * step, yp += 4 * step) {
       float f[4][V];
 #pragma unroll
       for (int u = 0; u < 4; ++u) ld16(xp + u * step, f[u]);
@@ -240,19 +255,19 @@ __global__ void __launch_bounds__(GN_THREADS)
 #pragma unroll
         for (int j = 0; j < V; ++j) {
           float v = fmaf(f[u][j], a[j], b[j]);
-          if (silu_on) v = v / (1.f + __expf(-v));
+          if (silu_on) v = __fdividef(v, 1.f + __expf(-v));
           f[u][j] = v;
         }
         st16(yp + u * step, f[u]);
       }
     }
-    for (; p < p1; p += rows_par, xp += step, yp += step) {
+    for (; p < p1; p += L.rows_par, xp += step, yp += step) {
       float f[V];
       ld16(xp, f);
 #pragma unroll
       for (int j = 0; j < V; ++j) {
         float v = fmaf(f[j], a[j], b[j]);
-        if (silu_on) v = v / (1.f + __expf(-v));
+        if (silu_on) v = __fdividef(v, 1.f + __expf(-v));
         f[j] = v;
       }
       st16(yp, f);
@@ -260,87 +275,80 @@ __global__ void __launch_bounds__(GN_THREADS)
   }
 }
 
-// backward pass 1: per-channel sums of dy0*xhat and dy0 (-> dgamma, dbeta atomics) and
-// per-group partials A = sum gamma*dy0, B = sum gamma*dy0*xhat
+// backward pass 1: per-channel sums of dy0 and dy0*xhat (dbeta, dgamma atomics) and per-group
+// partials A = sum gamma*dy0, B = sum gamma*dy0*xhat   (dy0 = dy through the optional SiLU)
 template <typename T>
 __global__ void __launch_bounds__(GN_THREADS)
     gn_bwd_partial_kernel(const T* __restrict__ x, const T* __restrict__ dy,
                           const float* __restrict__ gamma, const float* __restrict__ beta,
                           const float* __restrict__ mean, const float* __restrict__ rstd, int HW,
-                          int C, int G, int pix_per_chunk, int silu_on, float* __restrict__ dgamma,
+                          int C, int G, int ppc, int CB, int silu_on, float* __restrict__ dgamma,
                           float* __restrict__ dbeta, float* __restrict__ part) {
   constexpr int V = NV<T>::V;
-  const int CV = C / V;
   const int n = blockIdx.y, chunk = blockIdx.x, nchunks = gridDim.x;
-  const int p0 = chunk * pix_per_chunk;
-  const int p1 = min(HW, p0 + pix_per_chunk);
+  const int c0 = blockIdx.z * CB;
+  const int CVB = CB / V;
+  const int p0 = chunk * ppc;
+  const int p1 = min(HW, p0 + ppc);
   const int cg = C / G;
   __shared__ float s_a[GN_MAX_C], s_b[GN_MAX_C];
-  for (int c = threadIdx.x; c < C; c += GN_THREADS) s_a[c] = s_b[c] = 0.f;
+  for (int c = threadIdx.x; c < CB; c += GN_THREADS) s_a[c] = s_b[c] = 0.f;
   __syncthreads();
-  const int64_t base = (int64_t)n * HW * C;
-  for (int cv0 = 0; cv0 < CV; cv0 += GN_THREADS) {
-    const int width = min(GN_THREADS, CV - cv0);
-    const int rows_par = GN_THREADS / width;
-    const int cv = cv0 + threadIdx.x % width;
-    const int rl = threadIdx.x / width;
-    float sa[V], sb[V];  // sum dy0, sum dy0*xhat
+  const int64_t base = (int64_t)n * HW * C + c0;
+  for (int cv0 = 0; cv0 < CVB; cv0 += GN_THREADS) {
+    const GnLanes L(CVB, cv0);
+    if (L.rl >= L.rows_par) continue;
+    float sa[V], sb[V], mu[V], rs[V], ga[V], be[V];
 #pragma unroll
-    for (int j = 0; j < V; ++j) sa[j] = sb[j] = 0.f;
-    if (rl < rows_par) {
-      float mu[V], rs[V], ga[V], be[V];
+    for (int j = 0; j < V; ++j) {
+      const int c = c0 + L.cv * V + j;
+      mu[j] = mean[n * G + c / cg];
+      rs[j] = rstd[n * G + c / cg];
+      ga[j] = gamma ? gamma[c] : 1.f;
+      be[j] = gamma ? beta[c] : 0.f;
+      sa[j] = sb[j] = 0.f;
+    }
+    const int64_t step = (int64_t)L.rows_par * C;
+    int64_t off = base + (int64_t)(p0 + L.rl) * C + L.cv * V;
+#pragma unroll 4
+    for (int p = p0 + L.rl; p < p1; p += L.rows_par, off += step) {
+      float fx[V], fd[V];
+      ld16(x + off, fx);
+      ld16(dy + off, fd);
 #pragma unroll
       for (int j = 0; j < V; ++j) {
-        const int c = cv * V + j;
-        mu[j] = mean[n * G + c / cg];
-        rs[j] = rstd[n * G + c / cg];
-        ga[j] = gamma ? gamma[c] : 1.f;
-        be[j] = gamma ? beta[c] : 0.f;
-      }
-#pragma unroll 2
-      for (int p = p0 + rl; p < p1; p += rows_par) {
-        float fx[V], fd[V];
-        ld16(x + base + (int64_t)p * C + cv * V, fx);
-        ld16(dy + base + (int64_t)p * C + cv * V, fd);
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-          const float xh = (fx[j] - mu[j]) * rs[j];
-          float d = fd[j];
-          if (silu_on) {
-            const float y0 = xh * ga[j] + be[j];
-            const float s = 1.f / (1.f + __expf(-y0));
-            d *= s * (1.f + y0 * (1.f - s));
-          }
-          sa[j] += d;
-          sb[j] += d * xh;
+        const float xh = (fx[j] - mu[j]) * rs[j];
+        float d = fd[j];
+        if (silu_on) {
+          const float y0 = fmaf(xh, ga[j], be[j]);
+          const float s = __frcp_rn(1.f + __expf(-y0));
+          d *= s * (1.f + y0 * (1.f - s));
         }
+        sa[j] += d;
+        sb[j] = fmaf(d, xh, sb[j]);
       }
     }
-    for (int r = 0; r < rows_par; ++r) {
-      if (rl == r) {
 #pragma unroll
-        for (int j = 0; j < V; ++j) {
-          s_a[cv * V + j] += sa[j];
-          s_b[cv * V + j] += sb[j];
-        }
-      }
-      __syncthreads();
+    for (int j = 0; j < V; ++j) {
+      atomicAdd(&s_a[L.cv * V + j], sa[j]);
+      atomicAdd(&s_b[L.cv * V + j], sb[j]);
     }
   }
   __syncthreads();
   if (dgamma)
-    for (int c = threadIdx.x; c < C; c += GN_THREADS) {
-      atomicAdd(dgamma + c, s_b[c]);
-      atomicAdd(dbeta + c, s_a[c]);
+    for (int c = threadIdx.x; c < CB; c += GN_THREADS) {
+      atomicAdd(dgamma + c0 + c, s_b[c]);
+      atomicAdd(dbeta + c0 + c, s_a[c]);
     }
-  for (int g = threadIdx.x; g < G; g += GN_THREADS) {
+  const int g0 = c0 / cg, gb = CB / cg;
+  for (int gi = threadIdx.x; gi < gb; gi += GN_THREADS) {
     float A = 0.f, B = 0.f;
-    for (int c = g * cg; c < (g + 1) * cg; ++c) {
-      const float ga = gamma ? gamma[c] : 1.f;
+    for (int c = gi * cg; c < (gi + 1) * cg; ++c) {
+      const float ga = gamma ? gamma[c0 + c] : 1.f;
       A += ga * s_a[c];
       B += ga * s_b[c];
     }
-    float* o = part + (((int64_t)n * nchunks + chunk) * G + g) * 2;
+    float* o = part + (((int64_t)n * nchunks + chunk) * G + g0 + gi) * 2;
     o[0] = A;
     o[1] = B;
   }
@@ -351,50 +359,49 @@ __global__ void __launch_bounds__(GN_THREADS)
     gn_bwd_apply_kernel(const T* __restrict__ x, const T* __restrict__ dy,
                         const float* __restrict__ gamma, const float* __restrict__ beta,
                         const float* __restrict__ mean, const float* __restrict__ rstd,
-                        const float* __restrict__ part, int HW, int C, int G, int pix_per_chunk,
+                        const float* __restrict__ part, int HW, int C, int G, int ppc, int CB,
                         int silu_on, T* __restrict__ dx, int accumulate) {
   constexpr int V = NV<T>::V;
   const int n = blockIdx.y, chunk = blockIdx.x, nchunks = gridDim.x;
+  const int c0 = blockIdx.z * CB;
   const int cg = C / G;
+  const int g0 = c0 / cg, gb = CB / cg;
   __shared__ float s_A[256], s_B[256];
   const float inv_m = 1.f / (static_cast<float>(HW) * cg);
-  for (int g = threadIdx.x; g < G; g += GN_THREADS) {
+  for (int gi = threadIdx.x; gi < gb; gi += GN_THREADS) {
     float A = 0.f, B = 0.f;
     for (int k = 0; k < nchunks; ++k) {
-      const float* q = part + (((int64_t)n * nchunks + k) * G + g) * 2;
+      const float* q = part + (((int64_t)n * nchunks + k) * G + g0 + gi) * 2;
       A += q[0];
       B += q[1];
     }
-    s_A[g] = A * inv_m;
-    s_B[g] = B * inv_m;
+    s_A[gi] = A * inv_m;
+    s_B[gi] = B * inv_m;
   }
   __syncthreads();
-  const int CV = C / V;
-  const int p0 = chunk * pix_per_chunk;
-  const int p1 = min(HW, p0 + pix_per_chunk);
-  const int64_t base = (int64_t)n * HW * C;
-  for (int cv0 = 0; cv0 < CV; cv0 += GN_THREADS) {
-    const int width = min(GN_THREADS, CV - cv0);
-    const int rows_par = GN_THREADS / width;
-    const int cv = cv0 + threadIdx.x % width;
-    const int rl = threadIdx.x / width;
-    if (rl >= rows_par) continue;
+  const int CVB = CB / V;
+  const int p0 = chunk * ppc;
+  const int p1 = min(HW, p0 + ppc);
+  const int64_t base = (int64_t)n * HW * C + c0;
+  for (int cv0 = 0; cv0 < CVB; cv0 += GN_THREADS) {
+    const GnLanes L(CVB, cv0);
+    if (L.rl >= L.rows_par) continue;
     float mu[V], rs[V], ga[V], be[V], gA[V], gB[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-      const int c = cv * V + j;
-      const int g = c / cg;
-      mu[j] = mean[n * G + g];
-      rs[j] = rstd[n * G + g];
-      ga[j] = gamma ? gamma[c] : 1.f;
-      be[j] = gamma ? beta[c] : 0.f;
-      gA[j] = s_A[g];
-      gB[j] = s_B[g];
+      const int cl = L.cv * V + j;
+      const int gi = cl / cg;
+      mu[j] = mean[n * G + g0 + gi];
+      rs[j] = rstd[n * G + g0 + gi];
+      ga[j] = gamma ? gamma[c0 + cl] : 1.f;
+      be[j] = gamma ? beta[c0 + cl] : 0.f;
+      gA[j] = s_A[gi];
+      gB[j] = s_B[gi];
     }
-    const int64_t step = (int64_t)rows_par * C;
-    int64_t off = base + (int64_t)(p0 + rl) * C + cv * V;
-#pragma unroll 2
-    for (int p = p0 + rl; p < p1; p += rows_par, off += step) {
+    const int64_t step = (int64_t)L.rows_par * C;
+    int64_t off = base + (int64_t)(p0 + L.rl) * C + L.cv * V;
+#pragma unroll 4
+    for (int p = p0 + L.rl; p < p1; p += L.rows_par, off += step) {
       float fx[V], fd[V], fo[V];
       ld16(x + off, fx);
       ld16(dy + off, fd);
@@ -405,7 +412,7 @@ __global__ void __launch_bounds__(GN_THREADS)
         float d = fd[j];
         if (silu_on) {
           const float y0 = fmaf(xh, ga[j], be[j]);
-          const float sg = 1.f / (1.f + __expf(-y0));
+          const float sg = __frcp_rn(1.f + __expf(-y0));
           d *= sg * (1.f + y0 * (1.f - sg));
         }
         const float v = rs[j] * (ga[j] * d - gA[j] - xh * gB[j]);
@@ -414,17 +421,6 @@ __global__ void __launch_bounds__(GN_THREADS)
       st16(dx + off, fo);
     }
   }
-}
-
-static void gn_split(int N, int HW, int& chunks, int& ppc) {
-  int target = (4 * kNumSMs + N - 1) / N;
-  if (target < 1) target = 1;
-  // keep >= 64 pixels per chunk so partials stay cheap
-  int maxc = (HW + 63) / 64;
-  chunks = target < maxc ? target : maxc;
-  if (chunks < 1) chunks = 1;
-  ppc = (HW + chunks - 1) / chunks;
-  chunks = (HW + ppc - 1) / ppc;
 }
 
 // ------------------------------------------------------------------ LayerNorm
@@ -669,12 +665,16 @@ static int gn_validate(int dtype, int C, int G) {
   return 0;
 }
 
+static GnGeom gn_geom_rt(int dtype, int N, int HW, int C, int G) {
+  return dtype == DP_F32 ? gn_geom<4>(N, HW, C, G) : gn_geom<8>(N, HW, C, G);
+}
+
 extern "C" {
 
 size_t dp_group_norm_workspace(int N, int HW, int G) {
-  int chunks, ppc;
-  gn_split(N, HW, chunks, ppc);
-  return sizeof(float) * 3 * (size_t)N * chunks * G;
+  // chunking depends only on N and HW (channel blocks do not change the partial count)
+  const GnGeom g = gn_geom<8>(N, HW, G * 8, G);
+  return sizeof(float) * 3 * (size_t)N * g.chunks * G;
 }
 
 int dp_group_norm_fwd(int dtype, const void* x, const float* gamma, const float* beta, void* y,
@@ -682,13 +682,12 @@ int dp_group_norm_fwd(int dtype, const void* x, const float* gamma, const float*
                       float* workspace, dp_stream_t stream) {
   if (N <= 0 || HW <= 0) return 0;
   if (int e = gn_validate(dtype, C, G)) return e;
-  int chunks, ppc;
-  gn_split(N, HW, chunks, ppc);
-  dim3 grid(chunks, N);
-  DISPATCH_T(dtype, gn_partial_kernel<T><<<grid, GN_THREADS, 0, ST>>>(cp<T>(x), HW, C, G, ppc,
+  const GnGeom g = gn_geom_rt(dtype, N, HW, C, G);
+  dim3 grid(g.chunks, N, g.nblk);
+  DISPATCH_T(dtype, gn_partial_kernel<T><<<grid, GN_THREADS, 0, ST>>>(cp<T>(x), HW, C, G, g.ppc, g.CB,
                                                                         workspace));
   DISPATCH_T(dtype, gn_apply_kernel<T><<<grid, GN_THREADS, 0, ST>>>(
-                        cp<T>(x), gamma, beta, mp<T>(y), mean, rstd, workspace, HW, C, G, ppc,
+                        cp<T>(x), gamma, beta, mp<T>(y), mean, rstd, workspace, HW, C, G, g.ppc, g.CB,
                         eps, silu));
   return ew_check("group_norm_fwd");
 }
@@ -699,14 +698,13 @@ int dp_group_norm_bwd(int dtype, const void* x, const void* dy, const float* gam
                       int accumulate, float* workspace, dp_stream_t stream) {
   if (N <= 0 || HW <= 0) return 0;
   if (int e = gn_validate(dtype, C, G)) return e;
-  int chunks, ppc;
-  gn_split(N, HW, chunks, ppc);
-  dim3 grid(chunks, N);
+  const GnGeom g = gn_geom_rt(dtype, N, HW, C, G);
+  dim3 grid(g.chunks, N, g.nblk);
   DISPATCH_T(dtype, gn_bwd_partial_kernel<T><<<grid, GN_THREADS, 0, ST>>>(
-                        cp<T>(x), cp<T>(dy), gamma, beta, mean, rstd, HW, C, G, ppc, silu, dgamma,
-                        dbeta, workspace));
+                        cp<T>(x), cp<T>(dy), gamma, beta, mean, rstd, HW, C, G, g.ppc, g.CB, silu,
+                        dgamma, dbeta, workspace));
   DISPATCH_T(dtype, gn_bwd_apply_kernel<T><<<grid, GN_THREADS, 0, ST>>>(
-                        cp<T>(x), cp<T>(dy), gamma, beta, mean, rstd, workspace, HW, C, G, ppc,
+                        cp<T>(x), cp<T>(dy), gamma, beta, mean, rstd, workspace, HW, C, G, g.ppc, g.CB,
                         silu, mp<T>(dx), accumulate));
   return ew_check("group_norm_bwd");
 }
