@@ -123,12 +123,31 @@ class _Streams:
             t.record_stream(self.compute if which == "compute" else self.fill)
 
 
+class _StagedRecv:
+    """Work handle of a host-staged receive: completes the gloo receive, then copies to the device."""
+
+    def __init__(self, work, host, dst):
+        self.work, self.host, self.dst = work, host, dst
+
+    def wait(self):
+        self.work.wait()
+        self.dst.copy_(self.host)
+
+
+def staged():
+    """TEST transport: gloo cannot move CUDA tensors point-to-point, so the multi-process GPU
+    tests (several ranks sharing one GPU) stage P2P and allreduce through host memory. The
+    product transport is NCCL (device buffers, NVLink)."""
+    return dist.is_initialized() and dist.get_backend() == "gloo" and torch.cuda.is_available()
+
+
 class Links:
     """2-rank process groups per (kind, src, dst); kinds: fwd, bwd, fb (self-cond feedback), frz."""
 
     def __init__(self, rank, world, needed):
         self.rank = rank
         self.pg = {}
+        self.staged = world > 1 and staged()
         if world == 1:
             return
         for key in sorted(needed):
@@ -139,11 +158,16 @@ class Links:
     def isend(self, kind, t, dst):
         if _DEBUG:
             print(f"[r{self.rank}] send {kind} -> {dst} {tuple(t.shape)}", flush=True)
+        if self.staged and t.is_cuda:
+            t = t.detach().to("cpu")
         return dist.isend(t.contiguous(), dst=dst, group=self.pg[(kind, self.rank, dst)])
 
     def irecv(self, kind, t, src):
         if _DEBUG:
             print(f"[r{self.rank}] recv {kind} <- {src} {tuple(t.shape)}", flush=True)
+        if self.staged and t.is_cuda:
+            host = torch.empty(t.shape, dtype=t.dtype)
+            return _StagedRecv(dist.irecv(host, src=src, group=self.pg[(kind, src, self.rank)]), host, t)
         return dist.irecv(t, src=src, group=self.pg[(kind, src, self.rank)])
 
 
@@ -512,7 +536,12 @@ class PipelineExecutor:
         if hasattr(store, "pre_allreduce"):
             store.pre_allreduce()
         if self._stage_pg is not None and hi > lo:
-            dist.all_reduce(store.grad[lo:hi], group=self._stage_pg)
+            if self.links.staged and store.grad.is_cuda:
+                host = store.grad[lo:hi].cpu()
+                dist.all_reduce(host, group=self._stage_pg)
+                store.grad[lo:hi].copy_(host)
+            else:
+                dist.all_reduce(store.grad[lo:hi], group=self._stage_pg)
         if self.grad_snapshots is not None:
             self.grad_snapshots.append((lo, hi, store.grad[lo:hi].detach().clone()))
         store.adamw_step(rng=(lo, hi), **self.model.adamw)
@@ -583,5 +612,10 @@ class PipelineExecutor:
     def total_loss(self):
         """Sum of the loss over all ranks (only last-stage ranks contribute)."""
         if self.world > 1:
-            dist.all_reduce(self.loss_buf)
+            if self.links.staged and self.loss_buf.is_cuda:
+                host = self.loss_buf.cpu()
+                dist.all_reduce(host)
+                self.loss_buf.copy_(host)
+            else:
+                dist.all_reduce(self.loss_buf)
         return self.loss_buf
