@@ -112,22 +112,30 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def dist_setup(n):
+def dist_setup(n, share_gpu=False):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != n:
         raise SystemExit(f"--gpus {n} but WORLD_SIZE={world}")
+    if share_gpu:
+        # TEST ONLY: all ranks on cuda:0, gloo with host-staged P2P (exercises the N > 1 code
+        # path on a single-GPU box; the numbers are meaningless)
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     return rank, world, local
 
 
 def max_over_ranks(x, world):
     if world == 1:
         return x
-    t = torch.tensor([x], device="cuda", dtype=torch.float64)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.item()
 
@@ -213,6 +221,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--per-gpu-batch", type=int, default=32)
+    ap.add_argument("--debug-share-gpu", action="store_true",
+                    help="TEST ONLY: run all ranks on cuda:0 over gloo (validates the N>1 path)")
     ap.add_argument("--graph", action="store_true",
                     help="N=1: replay the captured iteration as a CUDA graph (measured: no gain, GPU-bound)")
     args = ap.parse_args()
@@ -220,7 +230,7 @@ def main():
         return reference_arm(args)
     args.warmup = max(args.warmup, 3)
 
-    rank, world, local = dist_setup(args.gpus)
+    rank, world, local = dist_setup(args.gpus, args.debug_share_gpu)
     from paper_2405_01248_b200 import engine
 
     lay = layout(world)
