@@ -16,6 +16,7 @@
 //                       stride-2 from TMA element strides
 //   A_WG_DY / B_WG_X    conv weight gradient: K runs over 64-pixel tiles of dY / shifted X
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <cudaTypedefs.h>
@@ -644,8 +645,19 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
 // CTA pairs (cta_group::2, M = 256 per pair) halve the per-SM shared-memory traffic of B;
 // used when the 256-row tiling wastes no more rows than the 128-row one and each CTA's half
 // of the B tile is a legal TMA box (64-column multiples for MN-major B).
-static int decide_cg(int M, int bn, bool b_mn_major) {
+static int env_int(const char* name) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : 0;
+}
+
+// Measured (tools/tile_sweep.py): pairs help long-K GEMMs, single CTAs win for short K
+// (K <= 512: 32768x320x320 327 vs 273 TF/s, 32768x2560x320 672 vs 596 TF/s).
+static int decide_cg(int M, int bn, bool b_mn_major, int K) {
+  static const int forced = env_int("DP_FORCE_CG");  // experiments only
+  if (forced == 1) return 1;
   if (M < 256) return 1;
+  if (!forced && K <= 512) return 1;
+  if (forced == 2 && !(b_mn_major && (bn / 2) % 64)) return 2;
   if (b_mn_major && (bn / 2) % 64) return 1;
   const long long r1 = (long long)((M + 127) / 128) * 128, r2 = (long long)((M + 255) / 256) * 256;
   return r2 <= r1 ? 2 : 1;
@@ -655,6 +667,8 @@ static int decide_cg(int M, int bn, bool b_mn_major) {
 // N=2880 -> 13 x 224, N=1280 -> 5 x 256. MN-major B operands are loaded in 64-column TMA
 // boxes, so they only use multiples of 64.
 static int pick_bn(int N, bool b_mn_major) {
+  static const int forced = env_int("DP_FORCE_BN");  // experiments only
+  if (forced && (!b_mn_major || forced % 64 == 0)) return forced;
   static const int kAll[] = {64, 96, 128, 160, 192, 224, 256};
   static const int kMn[] = {64, 128, 192, 256};
   const int* cand = b_mn_major ? kMn : kAll;
@@ -764,7 +778,7 @@ int tc_gemm(const DpGemmArgs* a, cudaStream_t st) {
     return DP_ERR_ARGS;
   }
   const int bn = pick_bn(a->N, a->b_mn_major != 0);
-  const int cg = decide_cg(a->M, bn, a->b_mn_major != 0);
+  const int cg = decide_cg(a->M, bn, a->b_mn_major != 0, a->K);
   TcParams p{};
   p.M = a->M;
   p.N = a->N;
@@ -848,7 +862,7 @@ int tc_conv_fwd(const DpConvArgs* a, cudaStream_t st) {
     return DP_ERR_UNSUPPORTED;
   }
   const int bn = pick_bn(a->K, false);
-  const int cg = decide_cg(a->N * a->P * a->Q, bn, false);
+  const int cg = decide_cg(a->N * a->P * a->Q, bn, false, a->R * a->S * a->C);
   p.M = a->N * a->P * a->Q;
   p.N = a->K;
   p.cblk = a->C / 64;
@@ -908,7 +922,7 @@ int tc_conv_dgrad(const DpConvArgs* a, cudaStream_t st) {
     return DP_ERR_UNSUPPORTED;
   }
   const int bn = pick_bn(a->C, true);
-  const int cg = decide_cg(a->N * a->H * a->W, bn, true);
+  const int cg = decide_cg(a->N * a->H * a->W, bn, true, a->R * a->S * a->K);
   p.M = a->N * a->H * a->W;
   p.N = a->C;
   p.cblk = a->K / 64;
@@ -961,7 +975,7 @@ int tc_conv_wgrad(const DpConvArgs* a, cudaStream_t st) {
   }
   const int Ntot = a->R * a->S * a->C;
   const int bn = pick_bn(Ntot, true);
-  const int cg = decide_cg(a->K, bn, true);
+  const int cg = decide_cg(a->K, bn, true, a->N * a->P * a->Q);
   p.M = a->K;
   p.N = Ntot;
   p.num_kb = (a->N * a->P * a->Q + BK - 1) / BK;
