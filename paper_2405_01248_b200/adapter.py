@@ -88,6 +88,7 @@ class GroupProgram:
     deliveries: list            # list[Transfer] (layer = last layer) final outputs -> stage 0
     frozen_layers: list         # per frozen component: number of layers
     selfcond: bool
+    frozen_deps: tuple = ()     # (producer, consumer) frozen component indices
 
     def device_program(self, dev):
         return self.devices[dev]
@@ -115,7 +116,7 @@ def _stage_layout(plan):
     return ranges, group_device_ranges(plan)
 
 
-def build_group_program(result, frozen_layer_counts, selfcond=None):
+def build_group_program(result, frozen_layer_counts, selfcond=None, frozen_deps=()):
     """Adapt one `evaluate_point` result (or an equivalent dict with plan/schedule/fill
     built for the non-activated self-conditioning iterations) into a GroupProgram."""
     plan = result["plan"]
@@ -166,7 +167,7 @@ def build_group_program(result, frozen_layer_counts, selfcond=None):
         fills.append(pieces)
     tail = []
     tail_phase = len(fill.fills)
-    for tw in _topo_tail(fill.tail, frozen_layer_counts):
+    for tw in _topo_tail(fill.tail, frozen_layer_counts, frozen_deps):
         lo = done[tw.component][tw.layer]
         hi = lo + tw.samples
         done[tw.component][tw.layer] = hi
@@ -199,17 +200,30 @@ def build_group_program(result, frozen_layer_counts, selfcond=None):
         instrs.append(("deliver",))
         prog.instrs = instrs
 
-    transfers, deliveries = _data_plan(fills, tail, frozen_layer_counts, B, M, stage_devices)
+    transfers, deliveries = _data_plan(fills, tail, frozen_layer_counts, B, M, stage_devices, frozen_deps)
     return GroupProgram(D=D, S=S, M=M, group_batch=B, micro_batch=B // M, stage_ranges=stage_ranges,
                         stage_devices=stage_devices, devices=devices, fills=fills, tail=tail,
                         transfers=transfers, deliveries=deliveries,
-                        frozen_layers=list(frozen_layer_counts), selfcond=sc)
+                        frozen_layers=list(frozen_layer_counts), selfcond=sc,
+                        frozen_deps=tuple(tuple(d) for d in frozen_deps))
 
 
-def _topo_tail(tail, counts):
-    """Tail work in (component, layer) order; components are independent here (the configs
-    run have no frozen dependency edges), so index order is a valid topological order."""
-    return sorted(tail, key=lambda t: (t.component, t.layer))
+def topo_order(n, deps):
+    """Frozen components in a dependency-respecting order (Kahn, lowest index first): the
+    reference validates the dependency graph as a DAG (profile.py:184-210) but emits the tail
+    in component-index order (filler.py:256-262), which is only safe for sorted DAGs."""
+    preds = {c: {s for s, d in deps if d == c} for c in range(n)}
+    done, order = set(), []
+    while len(order) < n:
+        nxt = min(c for c in range(n) if c not in done and preds[c] <= done)
+        order.append(nxt)
+        done.add(nxt)
+    return order
+
+
+def _topo_tail(tail, counts, deps=()):
+    rank = {c: i for i, c in enumerate(topo_order(len(counts), deps))}
+    return sorted(tail, key=lambda t: (rank[t.component], t.layer))
 
 
 def _overlaps(pieces, lo, hi):
@@ -219,17 +233,30 @@ def _overlaps(pieces, lo, hi):
             yield p, a, b
 
 
-def _data_plan(fills, tail, counts, B, M, stage_devices):
+def input_layers(comp, layer, counts, deps):
+    """(component, layer) outputs a piece of `layer` of `comp` consumes: the previous layer, or
+    for layer 0 the final layers of the components it depends on (e.g. ControlNet's frozen
+    U-Net encoder on the VAE latents and the text context)."""
+    if layer > 0:
+        return [(comp, layer - 1)]
+    return [(s, counts[s] - 1) for s, d in deps if d == comp]
+
+
+def _data_plan(fills, tail, counts, B, M, stage_devices, deps=()):
     """Frozen-activation transfers in production order, and final-output deliveries."""
     produced = {}  # (comp, layer) -> list[Piece]
     order = [p for ps in fills for p in ps] + list(tail)
     transfers = []
     seq = 0
     for p in order:
-        if p.layer > 0:
-            for src, a, b in _overlaps(produced.get((p.comp, p.layer - 1), ()), p.lo, p.hi):
+        for ic, il in input_layers(p.comp, p.layer, counts, deps):
+            got = list(_overlaps(produced.get((ic, il), ()), p.lo, p.hi))
+            if sum(b - a for _, a, b in got) != p.hi - p.lo:
+                raise RuntimeError(f"frozen ({p.comp},{p.layer}) [{p.lo},{p.hi}) runs before its input "
+                                   f"({ic},{il}) is produced")
+            for src, a, b in got:
                 if src.device != p.device:
-                    transfers.append(Transfer(src.device, p.device, p.comp, p.layer - 1, a, b, seq))
+                    transfers.append(Transfer(src.device, p.device, ic, il, a, b, seq))
                     seq += 1
         produced.setdefault((p.comp, p.layer), []).append(p)
     # transfers are discovered in consumption order; re-sort by producer order so that both

@@ -130,22 +130,23 @@ def plan_programs(prof, world, S, M, D, world_batch, frozen_counts, bubble_min_l
     res = planner.evaluate_point(prof, cluster, S, M, D, world_batch, bubble_min_len=bubble_min_len)
     plan = res["plan"]
     group_batch = plan.config.global_batch
+    deps = tuple(prof.frozen_dep_indices())
     programs = {}
     if res["mode"] == planner.MODE_SELFCOND:
-        programs[True] = build_group_program(res, frozen_counts, selfcond=True)
+        programs[True] = build_group_program(res, frozen_counts, selfcond=True, frozen_deps=deps)
         pre = scheduler.build_schedule(plan, prof, cluster, selfcond=False)
         fill = filler.fill_all(scheduler.extract_bubbles(pre, bubble_min_len), prof, group_batch, pre)
         programs[False] = build_group_program(dict(plan=plan, pre_fill_schedule=pre, fill=fill),
-                                              frozen_counts, selfcond=False)
+                                              frozen_counts, selfcond=False, frozen_deps=deps)
     else:
-        programs[False] = build_group_program(res, frozen_counts, selfcond=False)
+        programs[False] = build_group_program(res, frozen_counts, selfcond=False, frozen_deps=deps)
         programs[True] = programs[False]
     pre = res["pre_fill_schedule"]
     warm = filler.fill_all([], prof, group_batch, pre)
     warm_prog = build_group_program(dict(plan=plan, pre_fill_schedule=pre, fill=warm), frozen_counts,
-                                    selfcond=False)
+                                    selfcond=False, frozen_deps=deps)
     unfilled = build_group_program(dict(plan=plan, pre_fill_schedule=pre, fill=warm), frozen_counts,
-                                   selfcond=False)
+                                   selfcond=False, frozen_deps=deps)
     return res, programs, warm_prog, unfilled
 
 

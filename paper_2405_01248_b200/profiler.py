@@ -38,17 +38,28 @@ def _bytes_per_sample(spec, grad_only=False):
 
 
 def probe_specs(model, batch_fn, device):
-    """Run one sample through every layer; returns (live_specs, frozen_specs, frozen_outputs)."""
-    frozen_specs = []
+    """Run one sample through every layer; returns (live_specs, frozen_specs). Frozen components
+    run in dependency order; a dependent component's first layer also sees its producers'
+    final outputs (model.frozen_deps: (producer, consumer) index pairs)."""
+    from .adapter import topo_order
+
+    deps = getattr(model, "frozen_deps", ())
+    frozen_specs = [None] * len(model.frozen)
+    finals = {}
     fro = {}
-    for f in model.frozen:
+    for c in topo_order(len(model.frozen), deps):
+        f = model.frozen[c]
         st = {k: batch_fn(k) for k in f.inputs}
+        for s_, d in deps:
+            if d == c:
+                st.update(finals[s_])
         specs = []
         with torch.no_grad():
             for layer in f.component.layers:
                 st = layer(st)
                 specs.append({k: (tuple(v.shape[1:]), v.dtype) for k, v in st.items()})
-        frozen_specs.append(specs)
+        frozen_specs[c] = specs
+        finals[c] = st
         fro.update(st)
     t = batch_fn("t")
     noise = batch_fn("noise")
@@ -115,7 +126,9 @@ def synthetic_profile(model, live_specs, frozen_specs, *, group_batch, D, M, fwd
             ))
         nm = (names or {}).get(c, getattr(f.component, "name", f"frozen{c}"))
         frozen.append(ComponentProfile(name=nm, layers=fl, trainable=False))
-    return ModelProfile(backbones=(backbone,), frozen=tuple(frozen), frozen_deps=(),
+    names_ = [c.name for c in frozen]
+    deps = tuple((names_[a], names_[b]) for a, b in getattr(model, "frozen_deps", ()))
+    return ModelProfile(backbones=(backbone,), frozen=tuple(frozen), frozen_deps=deps,
                         selfcond_prob=getattr(model, "selfcond_p", 0.0))
 
 

@@ -32,7 +32,7 @@ from dataclasses import dataclass
 import torch
 import torch.distributed as dist
 
-from .adapter import GroupProgram, backbone_transfers, split_range
+from .adapter import GroupProgram, backbone_transfers, input_layers, split_range
 
 # ============================================================================ model bundle
 
@@ -272,6 +272,8 @@ class PipelineExecutor:
         comp = self.model.frozen[piece.comp]
         if piece.layer == 0:
             st = {f: raw(f, piece.lo, piece.hi) for f in comp.inputs}
+            for ic, il in input_layers(piece.comp, 0, self.prog.frozen_layers, self.prog.frozen_deps):
+                st.update(self._gather_frozen(store, ic, il, piece.lo, piece.hi))
         else:
             st = self._gather_frozen(store, piece.comp, piece.layer - 1, piece.lo, piece.hi)
         with torch.no_grad():
@@ -326,12 +328,12 @@ class PipelineExecutor:
         for piece in pieces:
             if piece.device != self.dev:
                 continue
-            if piece.layer > 0:
-                need = [t.seq for t in prog.transfers
-                        if t.dst == self.dev and t.comp == piece.comp and t.layer == piece.layer - 1
-                        and t.lo < piece.hi and piece.lo < t.hi]
-                if need:
-                    self._recv_frozen_upto(prog, store, max(need), posted, "fill")
+            inputs = set(input_layers(piece.comp, piece.layer, prog.frozen_layers, prog.frozen_deps))
+            need = [t.seq for t in prog.transfers
+                    if t.dst == self.dev and (t.comp, t.layer) in inputs
+                    and t.lo < piece.hi and piece.lo < t.hi]
+            if need:
+                self._recv_frozen_upto(prog, store, max(need), posted, "fill")
             out = self._run_frozen_piece(piece, store, raw)
             self._post_frozen_sends(prog, piece, out, sent)
 
@@ -551,7 +553,7 @@ class PipelineExecutor:
     def warmup(self, raw_next):
         """Iteration-0 warm-up: the frozen part of batch 0 alone, run as a
         data-parallel tail over the group's D devices."""
-        prog = self.warm_program
+        self.prog = prog = self.warm_program
         store, posted, sent = {}, {}, set()
         with self.streams.on("fill"):
             self._run_pieces(prog, prog.tail, store, raw_next, posted, sent)

@@ -92,8 +92,11 @@ class Backbone:
         x = st["x"].reshape(st["x"].shape[0], -1)
         freqs = torch.arange(1, 9, dtype=torch.float32)
         temb = torch.sin(st["t"].float()[:, None] * freqs[None] / 100.0) @ s.w("w_t")
-        h = torch.tanh(x @ s.w("w_in") + st["pooled"] @ s.w("w_pool") + temb)
-        out = {k: v for k, v in st.items() if k not in ("x", "t", "pooled")}
+        pre = x @ s.w("w_in") + st["pooled"] @ s.w("w_pool") + temb
+        if "hint" in st:  # output of a frozen component that depends on two others (ControlNet-like)
+            pre = pre + st["hint"]
+        h = torch.tanh(pre)
+        out = {k: v for k, v in st.items() if k not in ("x", "t", "pooled", "hint")}
         out.update(h=h, temb=temb, s1=h)
         return out
 
@@ -128,6 +131,12 @@ def _vae(s):
             lambda st: {"latent": (st["h"] @ s.w("v2")).view(-1, LAT, LAT, ZC)}]
 
 
+def _enc(s):
+    return [lambda st: {"e": torch.tanh(st["latent"].reshape(st["latent"].shape[0], -1) @ s.w("e0")
+                                        + st["pooled"] @ s.w("e1"))},
+            lambda st: {"hint": st["e"] @ s.w("e2")}]
+
+
 def _text(s):
     return [lambda st: {"e": s.w("emb")[st["ids"]]},
             lambda st: {"ctx": torch.tanh(st["e"] @ s.w("t1")),
@@ -154,15 +163,20 @@ class TorchOps:
         return torch.cat([a, b], -1)
 
 
-def build(selfcond=True, L=6):
+def build(selfcond=True, L=6, deps=False):
     from paper_2405_01248_b200.diffusion import noise_schedule
 
     bb = Backbone(L, selfcond)
     vae = _Frozen("vae", {"v0": (IMG * IMG * 3, 16), "v1": (16, 16), "v2": (16, LAT * LAT * ZC)}, _vae, 2)
     txt = _Frozen("text", {"emb": (VOCAB, 8), "t1": (8, HID), "tp": (HID, HID)}, _text, 3)
+    frozen = [FrozenSpec(vae, ("images",)), FrozenSpec(txt, ("ids",))]
+    if deps:
+        enc = _Frozen("enc", {"e0": (LAT * LAT * ZC, HID), "e1": (HID, HID), "e2": (HID, HID)}, _enc, 4)
+        frozen.append(FrozenSpec(enc, ()))
     sab, s1m = noise_schedule()
-    m = TrainModel(bb, [FrozenSpec(vae, ("images",)), FrozenSpec(txt, ("ids",))], TorchOps, sab, s1m,
+    m = TrainModel(bb, frozen, TorchOps, sab, s1m,
                    selfcond_channels=ZC if selfcond else 0,
                    adamw=dict(lr=1e-2, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01))
     m.selfcond_p = 0.5 if selfcond else 0.0
+    m.frozen_deps = ((0, 2), (1, 2)) if deps else ()
     return m

@@ -29,25 +29,25 @@ def _free_port():
     return p
 
 
-def _make(world, rank, S, M, D, selfcond, wb):
+def _make(world, rank, S, M, D, selfcond, wb, deps=False):
     import cpu_pipeline_model as cm
     from paper_2405_01248_b200 import engine
     from paper_2405_01248_b200.diffusion import DataSpec
 
-    model = cm.build(selfcond)
+    model = cm.build(selfcond, deps=deps)
     ds = DataSpec(7, wb, cm.IMG, cm.LAT, cm.ZC, cm.TL, cm.VOCAB, 1000, 0.5 if selfcond else 0.0)
     cfg = engine.ConfigSpec("toy", torch.float32, cm.IMG, cm.LAT, cm.TL, cm.VOCAB, ds.selfcond_p, 7)
     return engine.Trainer.from_model(model, cfg, ds, world=world, rank=rank, S=S, M=M, D=D, device="cpu")
 
 
-def _worker(rank, world, S, M, D, selfcond, wb, port, outdir):
+def _worker(rank, world, S, M, D, selfcond, wb, port, outdir, deps=False):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.set_num_threads(1)
-    tr = _make(world, rank, S, M, D, selfcond, wb)
+    tr = _make(world, rank, S, M, D, selfcond, wb, deps)
     losses = []
     for i in range(ITERS):
         tr.step(has_next=i < ITERS - 1)
@@ -62,8 +62,8 @@ def _worker(rank, world, S, M, D, selfcond, wb, port, outdir):
     dist.destroy_process_group()
 
 
-def _reference(selfcond, wb):
-    tr = _make(1, 0, 1, 1, 1, selfcond, wb)
+def _reference(selfcond, wb, deps=False):
+    tr = _make(1, 0, 1, 1, 1, selfcond, wb, deps)
     losses = []
     for i in range(ITERS):
         tr.step(has_next=i < ITERS - 1)
@@ -71,19 +71,20 @@ def _reference(selfcond, wb):
     return losses, tr.model.backbone.store.flat.detach().clone()
 
 
-@pytest.mark.parametrize("world,S,M,D,selfcond", [
-    (2, 2, 4, 2, False),
-    (2, 2, 4, 2, True),
-    (4, 2, 2, 2, True),     # 2 pipeline groups (DP across groups)
-    (4, 2, 4, 4, False),    # 2 replicas per stage (DP inside a stage)
+@pytest.mark.parametrize("world,S,M,D,selfcond,deps", [
+    (2, 2, 4, 2, False, False),
+    (2, 2, 4, 2, True, False),
+    (4, 2, 2, 2, True, False),     # 2 pipeline groups (DP across groups)
+    (4, 2, 4, 4, False, False),    # 2 replicas per stage (DP inside a stage)
+    (2, 2, 4, 2, False, True),     # frozen component depending on two others (ControlNet-like)
 ])
-def test_pipelined_equals_sequential(tmp_path, world, S, M, D, selfcond):
+def test_pipelined_equals_sequential(tmp_path, world, S, M, D, selfcond, deps):
     import torch.multiprocessing as mp
 
     wb = 16 * (world // D)
-    mp.spawn(_worker, args=(world, S, M, D, selfcond, wb, _free_port(), str(tmp_path)), nprocs=world,
+    mp.spawn(_worker, args=(world, S, M, D, selfcond, wb, _free_port(), str(tmp_path), deps), nprocs=world,
              join=True)
-    ref_losses, ref_flat = _reference(selfcond, wb)
+    ref_losses, ref_flat = _reference(selfcond, wb, deps)
     outs = [torch.load(os.path.join(tmp_path, f"r{r}.pt")) for r in range(world)]
     for o in outs:
         for a, b in zip(o["losses"], ref_losses):
