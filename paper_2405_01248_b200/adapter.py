@@ -7,10 +7,12 @@ reference planner.py:141-187): the PartitionPlan, the simulated Schedule
 (scheduler.py:320-332) and the FillPlan (filler.py:245-276). Output, per
 group-local device:
 
-  ("fwd" | "fwd_sc" | "bwd", micro, stage)   compute tasks in simulated start order
+  ("fwd" | "fwd_sc" | "bwd", micro, stage, pipe)  compute tasks in simulated start order
+                                             (pipe 0 = "down" backbone, 1 = "up" backbone of a
+                                             bidirectional plan, partitioner.py:402-501)
   ("fill", bubble_idx)                       frozen work of one bubble, placed after the
                                              device's last compute task ending <= bubble.start
-  ("sync", stage)                            per-stage gradient allreduce + AdamW, right after
+  ("sync", stage, pipe)                      per-stage gradient allreduce + AdamW, right after
                                              the stage's final backward (scheduler.py:202-207)
   ("tail",)                                  leftover frozen work over all D devices
   ("deliver",)                               frozen outputs -> stage-0 consumers (next iteration)
@@ -65,9 +67,22 @@ class Transfer:
 @dataclass
 class DeviceProgram:
     device: int
-    stage: int | None
+    stage: int | None              # stage of pipe 0 hosted here
     replica: int | None
     instrs: list = field(default_factory=list)
+    stages: tuple = ()             # per pipe: flow stage hosted on this device (or None)
+
+
+@dataclass(frozen=True)
+class PipeLayout:
+    """One backbone pipeline: flow stage s holds layers stage_ranges[s] on the group-local
+    devices stage_devices[s]. The up pipe of a bidirectional plan runs flow stage j on device
+    group S-1-j (scheduler.py:273-276)."""
+
+    direction: str
+    backbone: int
+    stage_ranges: tuple
+    stage_devices: tuple
 
 
 @dataclass
@@ -89,6 +104,7 @@ class GroupProgram:
     frozen_layers: list         # per frozen component: number of layers
     selfcond: bool
     frozen_deps: tuple = ()     # (producer, consumer) frozen component indices
+    pipes: tuple = ()           # PipeLayout per backbone pipeline (1, or 2 when bidirectional)
 
     def device_program(self, dev):
         return self.devices[dev]
@@ -96,8 +112,8 @@ class GroupProgram:
     def micro_range(self, m):
         return m * self.micro_batch, (m + 1) * self.micro_batch
 
-    def replica_range(self, stage, m, replica):
-        first, last = self.stage_devices[stage]
+    def replica_range(self, stage, m, replica, pipe=0):
+        first, last = self.pipes[pipe].stage_devices[stage]
         lo, hi = self.micro_range(m)
         return split_range(lo, hi, last - first)[replica]
 
@@ -108,12 +124,17 @@ class GroupProgram:
         raise ValueError(dev)
 
 
-def _stage_layout(plan):
-    stages = plan.stages_down
-    if plan.stages_up:
-        raise NotImplementedError("bidirectional (two-backbone) plans are not executed yet")
-    ranges = [tuple(st.layer_range) for st in stages]
-    return ranges, group_device_ranges(plan)
+def _pipes(plan):
+    groups = group_device_ranges(plan)
+    down = plan.stages_down
+    pipes = [PipeLayout("down", down[0].backbone, tuple(tuple(st.layer_range) for st in down),
+                        tuple(groups))]
+    up = plan.stages_up
+    if up:
+        n = len(up)
+        pipes.append(PipeLayout("up", up[0].backbone, tuple(tuple(st.layer_range) for st in up),
+                                tuple(groups[n - 1 - j] for j in range(n))))
+    return tuple(pipes)
 
 
 def build_group_program(result, frozen_layer_counts, selfcond=None, frozen_deps=()):
@@ -124,16 +145,22 @@ def build_group_program(result, frozen_layer_counts, selfcond=None, frozen_deps=
     fill = result["fill"]
     cfg = plan.config
     D, S, M, B = cfg.group_size, cfg.num_stages, cfg.num_microbatches, cfg.global_batch
-    stage_ranges, stage_devices = _stage_layout(plan)
+    pipes = _pipes(plan)
+    stage_ranges, stage_devices = list(pipes[0].stage_ranges), list(pipes[0].stage_devices)
     sc = cfg.selfcond if selfcond is None else selfcond
+    pipe_of = {p.direction: i for i, p in enumerate(pipes)}
 
     devices = []
     for dev in range(D):
-        stage = rep = None
-        for s, (a, b) in enumerate(stage_devices):
-            if a <= dev < b:
-                stage, rep = s, dev - a
-        devices.append(DeviceProgram(dev, stage, rep))
+        stages = []
+        rep = None
+        for pl in pipes:
+            st = None
+            for s_, (a, b) in enumerate(pl.stage_devices):
+                if a <= dev < b:
+                    st, rep = s_, dev - a
+            stages.append(st)
+        devices.append(DeviceProgram(dev, stages[0], rep, stages=tuple(stages)))
 
     # ---- compute tasks per device, in the simulator's per-device order
     compute = {dev: [] for dev in range(D)}
@@ -185,27 +212,30 @@ def build_group_program(result, frozen_layer_counts, selfcond=None, frozen_deps=
         prog = devices[dev]
         items = []  # (sort_time, tiebreak, instr)
         for t in compute[dev]:
-            items.append((t.start, 1, (t.kind, t.micro_batch, t.stage)))
+            items.append((t.start, 1, (t.kind, t.micro_batch, t.stage, pipe_of[t.direction])))
         for bi, f in enumerate(fill.fills):
             if any(p.device == dev for p in fills[bi]):
                 # after every compute task ending <= bubble.start; before those starting >= it
                 items.append((f.bubble.start, 0, ("fill", bi)))
         items.sort(key=lambda x: (x[0], x[1]))
         instrs = [it[2] for it in items]
-        if prog.stage is not None:
-            last_bwd = max(i for i, ins in enumerate(instrs) if ins[0] == "bwd" and ins[2] == prog.stage)
-            instrs.insert(last_bwd + 1, ("sync", prog.stage))
+        for pi, st in enumerate(prog.stages):
+            if st is not None:
+                last_bwd = max(i for i, ins in enumerate(instrs)
+                               if ins[0] == "bwd" and ins[2] == st and ins[3] == pi)
+                instrs.insert(last_bwd + 1, ("sync", st, pi))
         if any(p.device == dev for p in tail):
             instrs.append(("tail",))
         instrs.append(("deliver",))
         prog.instrs = instrs
 
-    transfers, deliveries = _data_plan(fills, tail, frozen_layer_counts, B, M, stage_devices, frozen_deps)
+    transfers, deliveries = _data_plan(fills, tail, frozen_layer_counts, B, M,
+                                       [pl.stage_devices[0] for pl in pipes], frozen_deps)
     return GroupProgram(D=D, S=S, M=M, group_batch=B, micro_batch=B // M, stage_ranges=stage_ranges,
                         stage_devices=stage_devices, devices=devices, fills=fills, tail=tail,
                         transfers=transfers, deliveries=deliveries,
                         frozen_layers=list(frozen_layer_counts), selfcond=sc,
-                        frozen_deps=tuple(tuple(d) for d in frozen_deps))
+                        frozen_deps=tuple(tuple(d) for d in frozen_deps), pipes=pipes)
 
 
 def topo_order(n, deps):
@@ -242,7 +272,7 @@ def input_layers(comp, layer, counts, deps):
     return [(s, counts[s] - 1) for s, d in deps if d == comp]
 
 
-def _data_plan(fills, tail, counts, B, M, stage_devices, deps=()):
+def _data_plan(fills, tail, counts, B, M, first_groups, deps=()):
     """Frozen-activation transfers in production order, and final-output deliveries."""
     produced = {}  # (comp, layer) -> list[Piece]
     order = [p for ps in fills for p in ps] + list(tail)
@@ -271,27 +301,34 @@ def _data_plan(fills, tail, counts, B, M, stage_devices, deps=()):
 
     transfers.sort(key=lambda t: (prod_index(t), t.seq))
     transfers = [Transfer(t.src, t.dst, t.comp, t.layer, t.lo, t.hi, i) for i, t in enumerate(transfers)]
+    # final frozen outputs -> the first-stage owners of every pipe (each sample to the replica
+    # that runs it; a device owning the first stage of both pipes receives it once)
     deliveries = []
-    first, last = stage_devices[0]
-    r0 = last - first
+    seen = set()
     mb = B // M
     k = 0
-    for c, n in enumerate(counts):
-        final = produced.get((c, n - 1), [])
-        for m in range(M):
-            for rep, (lo, hi) in enumerate(split_range(m * mb, (m + 1) * mb, r0)):
-                for src, a, b in _overlaps(final, lo, hi):
-                    deliveries.append(Transfer(src.device, first + rep, c, n - 1, a, b, k))
-                    k += 1
+    for first, last in first_groups:
+        r0 = last - first
+        for c, n in enumerate(counts):
+            final = produced.get((c, n - 1), [])
+            for m in range(M):
+                for rep, (lo, hi) in enumerate(split_range(m * mb, (m + 1) * mb, r0)):
+                    for src, a, b in _overlaps(final, lo, hi):
+                        key = (src.device, first + rep, c, a, b)
+                        if key in seen:
+                            continue
+                        seen.add(key)
+                        deliveries.append(Transfer(src.device, first + rep, c, n - 1, a, b, k))
+                        k += 1
     return transfers, deliveries
 
 
-def backbone_transfers(prog: GroupProgram, stage, m):
-    """Live-set pieces crossing the cut stage -> stage+1 for micro-batch m:
+def backbone_transfers(prog: GroupProgram, stage, m, pipe=0):
+    """Live-set pieces crossing the cut stage -> stage+1 of a pipe for micro-batch m:
     [(src_replica, dst_replica, lo, hi)] (the reverse for gradients)."""
     out = []
-    a0, a1 = prog.stage_devices[stage]
-    b0, b1 = prog.stage_devices[stage + 1]
+    a0, a1 = prog.pipes[pipe].stage_devices[stage]
+    b0, b1 = prog.pipes[pipe].stage_devices[stage + 1]
     lo, hi = prog.micro_range(m)
     src = split_range(lo, hi, a1 - a0)
     dst = split_range(lo, hi, b1 - b0)

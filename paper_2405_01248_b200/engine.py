@@ -181,7 +181,7 @@ class Trainer:
         world_batch = ds.world_batch
         probe = make_batch(replace(ds, world_batch=1), 10 ** 6)
         pfeed = InputFeed(probe, device, cfg.dtype)
-        live, fspecs = probe_specs(model, lambda k: pfeed.get(k, 0, 1), device)
+        live, fspecs = probe_specs(model, lambda k: pfeed.get(k, 0, 1), device)  # per backbone
         counts = [len(f.component.layers) for f in model.frozen]
         if profile is None:
             profile = synthetic_profile(model, live, fspecs, group_batch=world_batch * D // world, D=D, M=M)

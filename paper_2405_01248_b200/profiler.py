@@ -63,15 +63,17 @@ def probe_specs(model, batch_fn, device):
         fro.update(st)
     t = batch_fn("t")
     noise = batch_fn("noise")
-    st, _ = model.stage0_inputs(fro, t, noise)
-    bb = model.backbone
-    live = [_spec_of(st)]
-    ctx = bb.grad_context() if hasattr(bb, "grad_context") else torch.enable_grad()
-    with ctx:
-        for layer in bb.layers:
-            st = layer(st)
-            live.append(_spec_of(st))
-    return live, frozen_specs
+    live_all = []
+    for pipe, bb in enumerate(getattr(model, "backbones", None) or [model.backbone]):
+        st, _ = model.stage0_inputs(fro, t, noise, pipe=pipe)
+        live = [_spec_of(st)]
+        ctx = bb.grad_context() if hasattr(bb, "grad_context") else torch.enable_grad()
+        with ctx:
+            for layer in bb.layers:
+                st = layer(st)
+                live.append(_spec_of(st))
+        live_all.append(live)
+    return live_all, frozen_specs
 
 
 def _keys(group_batch, D, M, extra=()):
@@ -91,25 +93,31 @@ def _keys(group_batch, D, M, extra=()):
 def synthetic_profile(model, live_specs, frozen_specs, *, group_batch, D, M, fwd_per_sample=1e-3,
                       bwd_factor=2.0, frozen_per_sample=5e-4, backbone_weights=None,
                       frozen_weights=None, names=None):
-    """Costs linear in batch: layer j fwd = w_j * fwd_per_sample * b (bwd = bwd_factor x)."""
+    """Costs linear in batch: layer j fwd = w_j * fwd_per_sample * b (bwd = bwd_factor x).
+    live_specs: per backbone, the probed live sets (a single backbone's list is accepted)."""
     keys = _keys(group_batch, D, M)
-    bb = model.backbone
-    L = len(bb.layers)
-    bw = backbone_weights or [1.0] * L
-    layers = []
-    for j in range(L):
-        out_spec = live_specs[j + 1]
-        fb = _bytes_per_sample(out_spec)
-        gb = _bytes_per_sample(out_spec, grad_only=True)
-        layers.append(LayerCost(
-            fwd_time={k: bw[j] * fwd_per_sample * k for k in keys},
-            bwd_time={k: bw[j] * bwd_factor * fwd_per_sample * k for k in keys},
-            fwd_comm_bytes={k: fb * k for k in keys},
-            bwd_comm_bytes={k: gb * k for k in keys},
-            grad_bytes={k: 0 for k in keys},
-            out_bytes={k: _bytes_per_sample({"out": live_specs[-1]["out"]}) * k for k in keys},
-        ))
-    backbone = ComponentProfile(name=getattr(bb, "name", "backbone"), layers=layers, trainable=True)
+    if live_specs and isinstance(live_specs[0], dict):
+        live_specs = [live_specs]
+    backbones = []
+    for bi, bb in enumerate(getattr(model, "backbones", None) or [model.backbone]):
+        live = live_specs[bi]
+        L = len(bb.layers)
+        bw = backbone_weights or [1.0] * L
+        layers = []
+        for j in range(L):
+            out_spec = live[j + 1]
+            fb = _bytes_per_sample(out_spec)
+            gb = _bytes_per_sample(out_spec, grad_only=True)
+            layers.append(LayerCost(
+                fwd_time={k: bw[j] * fwd_per_sample * k for k in keys},
+                bwd_time={k: bw[j] * bwd_factor * fwd_per_sample * k for k in keys},
+                fwd_comm_bytes={k: fb * k for k in keys},
+                bwd_comm_bytes={k: gb * k for k in keys},
+                grad_bytes={k: 0 for k in keys},
+                out_bytes={k: _bytes_per_sample({"out": live[-1]["out"]}) * k for k in keys},
+            ))
+        backbones.append(ComponentProfile(name=f"{getattr(bb, 'name', 'backbone')}{bi if bi else ''}",
+                                          layers=layers, trainable=True))
     frozen = []
     for c, f in enumerate(model.frozen):
         fw = (frozen_weights or {}).get(c) or [1.0] * len(f.component.layers)
@@ -128,7 +136,7 @@ def synthetic_profile(model, live_specs, frozen_specs, *, group_batch, D, M, fwd
         frozen.append(ComponentProfile(name=nm, layers=fl, trainable=False))
     names_ = [c.name for c in frozen]
     deps = tuple((names_[a], names_[b]) for a, b in getattr(model, "frozen_deps", ()))
-    return ModelProfile(backbones=(backbone,), frozen=tuple(frozen), frozen_deps=deps,
+    return ModelProfile(backbones=tuple(backbones), frozen=tuple(frozen), frozen_deps=deps,
                         selfcond_prob=getattr(model, "selfcond_p", 0.0))
 
 

@@ -35,7 +35,8 @@ def measure(cfg, group_batch, D, M, device, reps=3):
     from .diffusion import DataSpec
     ds = DataSpec(c.config_id, 1, c.image, c.latent, 4, c.text_len, c.vocab, 1000, c.selfcond_p)
     feed = engine.InputFeed(make_batch(ds, 10 ** 6), device, c.dtype)
-    live, fspecs = probe_specs(model, lambda k: feed.get(k, 0, 1), device)
+    live_all, fspecs = probe_specs(model, lambda k: feed.get(k, 0, 1), device)
+    live = live_all[0]
     mb = group_batch // M
     bb_keys = sorted({1} | {max(1, mb // r) for r in range(1, D + 1)} | {-(-mb // r) for r in range(1, D + 1)})
     fr_keys = sorted({1, 2} | set(VALID_LOCAL_SIZES) | {max(1, group_batch // d) for d in range(1, D + 1)}

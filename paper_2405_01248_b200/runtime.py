@@ -51,8 +51,9 @@ class TrainModel:
     """
 
     def __init__(self, backbone, frozen, ops, sqrt_ab, sqrt_1mab, selfcond_channels=0,
-                 grad_scale=1.0, adamw=None):
+                 grad_scale=1.0, adamw=None, backbones=None):
         self.backbone = backbone
+        self.backbones = list(backbones) if backbones else [backbone]
         self.frozen = frozen
         self.ops = ops
         self.sqrt_ab = sqrt_ab
@@ -61,8 +62,10 @@ class TrainModel:
         self.adamw = adamw or {}
 
     # -- stage 0 input construction ------------------------------------------------------
-    def stage0_inputs(self, frozen_out, t, noise, x0_sc=None):
-        """frozen_out: merged dict of frozen outputs (latent, ctx, pooled) for these samples."""
+    def stage0_inputs(self, frozen_out, t, noise, x0_sc=None, pipe=0):
+        """frozen_out: merged dict of frozen outputs (latent, ctx, pooled) for these samples.
+        `pipe` selects the backbone of a two-backbone (bidirectional) model; both backbones of
+        a cascaded model share the frozen outputs and the noise draw."""
         o = self.ops
         x0 = frozen_out["latent"]
         xt = o.q_sample(x0, noise, t, self.sqrt_ab, self.sqrt_1mab)
@@ -181,7 +184,8 @@ class PipelineExecutor:
     def __init__(self, model: TrainModel, programs: dict, *, rank=0, world=1, device="cuda",
                  live_specs=None, frozen_specs=None, loss_scale=1.0, inputs=None):
         """programs: {False: GroupProgram, True: GroupProgram (self-cond activated)} built from
-        the same partition; `inputs` provides host/device batch slices (InputFeed)."""
+        the same partition; `inputs` provides host/device batch slices (InputFeed).
+        live_specs: per pipe (backbone) a list over layer boundaries of {name: (shape, dtype, grad)}."""
         self.model = model
         self.programs = programs
         self.prog0 = programs[False]
@@ -190,25 +194,36 @@ class PipelineExecutor:
         self.group, self.dev = divmod(rank, self.D)
         self.device = torch.device(device)
         self.streams = _Streams(self.device)
-        self.live_specs = live_specs      # list per layer boundary: {name: (shape, dtype, grad)}
+        self.npipes = len(self.prog0.pipes)
+        if live_specs is not None and live_specs and isinstance(live_specs[0], dict):
+            live_specs = [live_specs]  # single-backbone form
+        self.live_specs = live_specs
         self.frozen_specs = frozen_specs  # [comp][layer] -> {name: (shape, dtype)}
         self.loss_scale = loss_scale
         self.inputs = inputs
         p = self.prog0.device_program(self.dev)
-        self.stage, self.replica = p.stage, p.replica
-        if self.stage is not None:
-            lo, hi = self.prog0.stage_ranges[self.stage]
-            self.param_range = model.backbone.stage_slice(lo, hi)
+        self.stages = list(p.stages) if p.stages else [p.stage]
+        self.stage, self.replica = self.stages[0], p.replica
+        self.param_ranges = []
+        for pi, st in enumerate(self.stages):
+            if st is None:
+                self.param_ranges.append(None)
+                continue
+            lo, hi = self.prog0.pipes[pi].stage_ranges[st]
+            self.param_ranges.append(self._backbone(pi).stage_slice(lo, hi))
+        self.param_range = self.param_ranges[0]
         self.links = Links(rank, world, self._needed_links())
-        self._stage_pg = self._make_stage_groups()
+        self._stage_pgs = self._make_stage_groups()
         self.frozen_ready = {}   # for the NEXT iteration: comp -> list[(lo, hi, state)] on stage-0 owners
         self.loss_buf = torch.zeros(1, device=self.device, dtype=torch.float32)
-        self.timeline = []       # (kind, micro, stage, ev_start, ev_end) when tracing
-        self.trace = False
         self.grad_snapshots = None  # list -> flat grad slices captured before each AdamW
         self._frz_sends = []        # in-flight frozen-activation sends (kept alive until deliver)
 
     # ---------------------------------------------------------------- setup
+    def _backbone(self, pipe):
+        bbs = getattr(self.model, "backbones", None) or [self.model.backbone]
+        return bbs[self.prog0.pipes[pipe].backbone]
+
     def gb_of(self):
         """Offset of this rank's pipeline group in the world batch."""
         return self.group * self.prog0.group_batch
@@ -221,40 +236,44 @@ class PipelineExecutor:
         for g in range(self.world // self.D):
             base = g * self.D
             for prog in self.programs.values():
-                for s in range(prog.S - 1):
-                    for m in range(prog.M):
-                        for i, j, a, b in backbone_transfers(prog, s, m):
-                            src = base + prog.stage_devices[s][0] + i
-                            dst = base + prog.stage_devices[s + 1][0] + j
-                            need.add(("fwd", src, dst))
-                            need.add(("bwd", dst, src))
+                for pi, pl in enumerate(prog.pipes):
+                    for s in range(prog.S - 1):
+                        for m in range(prog.M):
+                            for i, j, a, b in backbone_transfers(prog, s, m, pi):
+                                src = base + pl.stage_devices[s][0] + i
+                                dst = base + pl.stage_devices[s + 1][0] + j
+                                need.add((f"fwd{pi}", src, dst))
+                                need.add((f"bwd{pi}", dst, src))
                 if prog.selfcond and prog.S > 1:
-                    for m in range(prog.M):
-                        for i, j, a, b in self._feedback_pieces(prog, m):
-                            need.add(("fb", base + prog.stage_devices[-1][0] + i,
-                                      base + prog.stage_devices[0][0] + j))
+                    for pi, pl in enumerate(prog.pipes):
+                        for m in range(prog.M):
+                            for i, j, a, b in self._feedback_pieces(prog, m, pi):
+                                need.add((f"fb{pi}", base + pl.stage_devices[-1][0] + i,
+                                          base + pl.stage_devices[0][0] + j))
                 for t in list(prog.transfers) + list(prog.deliveries):
                     if t.src != t.dst:
                         need.add(("frz", base + t.src, base + t.dst))
         return need
 
     def _make_stage_groups(self):
+        """Per pipe: the process group over every replica of this device's stage (all groups)."""
+        mine = [None] * self.npipes
         if self.world == 1:
-            return None
-        mine = None
-        for s in range(self.prog0.S):
-            a, b = self.prog0.stage_devices[s]
-            ranks = [g * self.D + d for g in range(self.world // self.D) for d in range(a, b)]
-            pg = dist.new_group(ranks=ranks) if len(ranks) > 1 else None
-            if s == self.stage:
-                mine = pg
+            return mine
+        for pi, pl in enumerate(self.prog0.pipes):
+            for s in range(self.prog0.S):
+                a, b = pl.stage_devices[s]
+                ranks = [g * self.D + d for g in range(self.world // self.D) for d in range(a, b)]
+                pg = dist.new_group(ranks=ranks) if len(ranks) > 1 else None
+                if s == self.stages[pi]:
+                    mine[pi] = pg
         return mine
 
     @staticmethod
-    def _feedback_pieces(prog, m):
+    def _feedback_pieces(prog, m, pi=0):
         lo, hi = prog.micro_range(m)
-        a0, a1 = prog.stage_devices[-1]
-        b0, b1 = prog.stage_devices[0]
+        a0, a1 = prog.pipes[pi].stage_devices[-1]
+        b0, b1 = prog.pipes[pi].stage_devices[0]
         out = []
         for i, (sa, sb) in enumerate(split_range(lo, hi, a1 - a0)):
             for j, (da, db) in enumerate(split_range(lo, hi, b1 - b0)):
@@ -305,7 +324,7 @@ class PipelineExecutor:
                                                             self._grank(t.dst)))
                 sent.add(t.seq)
 
-    def _recv_frozen_upto(self, prog, store, need_seq, posted, stream_which):
+    def _recv_frozen_upto(self, prog, store, need_seq, posted):
         """Post receives (in production order) for every transfer to this device up to
         `need_seq`, wait for them, and add them to `store`."""
         for t in prog.transfers:
@@ -333,14 +352,14 @@ class PipelineExecutor:
                     if t.dst == self.dev and (t.comp, t.layer) in inputs
                     and t.lo < piece.hi and piece.lo < t.hi]
             if need:
-                self._recv_frozen_upto(prog, store, max(need), posted, "fill")
+                self._recv_frozen_upto(prog, store, max(need), posted)
             out = self._run_frozen_piece(piece, store, raw)
             self._post_frozen_sends(prog, piece, out, sent)
 
     def _deliver(self, prog, store, posted):
-        """Final frozen outputs -> stage-0 owners (who use them next iteration)."""
+        """Final frozen outputs -> first-stage owners of every pipe (used next iteration)."""
         if prog.transfers:
-            self._recv_frozen_upto(prog, store, prog.transfers[-1].seq, posted, "compute")
+            self._recv_frozen_upto(prog, store, prog.transfers[-1].seq, posted)
         ready = {}
         sends = []
         recvs = []
@@ -373,22 +392,18 @@ class PipelineExecutor:
                 x, y = max(a, lo), min(b, hi)
                 if y > x:
                     parts.append((x, {k: v[x - a:y - a] for k, v in st.items()}))
+            if not parts:
+                continue
             parts.sort(key=lambda q: q[0])
             for k in parts[0][1]:
                 merged[k] = _cat([p[1][k] for p in parts])
         return merged
 
     # ---------------------------------------------------------------- backbone
-    def _live_recv(self, boundary, n):
-        spec = self.live_specs[boundary]
-        return {k: torch.empty((n,) + tuple(shape), device=self.device, dtype=dt)
-                for k, (shape, dt, g) in sorted(spec.items())}
-
-    def _stage_forward(self, st_in, grad):
-        lo, hi = self.prog.stage_ranges[self.stage]
-        bb = self.model.backbone
+    def _stage_forward(self, pi, st_in, grad):
+        lo, hi = self.prog.pipes[pi].stage_ranges[self.stages[pi]]
+        bb = self._backbone(pi)
         if grad:
-            from . import nn as _nn  # noqa: F401  (anchor helper is optional for test doubles)
             anchor_ctx = getattr(bb, "grad_context", None)
             ctx = anchor_ctx() if anchor_ctx else contextlib.nullcontext()
             with ctx:
@@ -396,36 +411,40 @@ class PipelineExecutor:
         with torch.no_grad():
             return bb.run(st_in, lo, hi)
 
-    def _fwd(self, m, sc_pass):
+    def _spec(self, pi, boundary):
+        return self.live_specs[pi][boundary]
+
+    def _fwd(self, pi, m, sc_pass):
         prog = self.prog
+        pl = prog.pipes[pi]
         S = prog.S
-        s = self.stage
-        lo_r, hi_r = prog.replica_range(s, m, self.replica)
+        s = self.stages[pi]
+        lo_r, hi_r = prog.replica_range(s, m, self.replica, pi)
         n = hi_r - lo_r
-        key = (m, sc_pass)
+        key = (pi, m, sc_pass)
         if s == 0:
             fro = self.frozen_for(self.frozen_cur, lo_r, hi_r)
             t, noise = self.inputs.t(self.gb + lo_r, self.gb + hi_r), self.inputs.noise(self.gb + lo_r,
                                                                                          self.gb + hi_r)
             x0_sc = None
             if not sc_pass and prog.selfcond:
-                eps_sc = self._feedback_in.pop(m)
-                x0_sc = self.model.ops.pred_x0(self._xt[m], eps_sc, t, self.model.sqrt_ab,
+                eps_sc = self._feedback_in.pop((pi, m))
+                x0_sc = self.model.ops.pred_x0(self._xt[(pi, m)], eps_sc, t, self.model.sqrt_ab,
                                                self.model.sqrt_1mab)
-            st_in, xt = self.model.stage0_inputs(fro, t, noise, x0_sc)
+            st_in, xt = self.model.stage0_inputs(fro, t, noise, x0_sc, pipe=pl.backbone)
             if sc_pass:
-                self._xt[m] = xt
+                self._xt[(pi, m)] = xt
         else:
-            st_in = self._recv_live(s, m, n, lo_r, "fwd_sc" if sc_pass else "fwd")
+            st_in = self._recv_live(pi, s, m, n, lo_r)
         if not sc_pass:
+            spec0 = self._spec(pi, pl.stage_ranges[s][0])
             for k, v in st_in.items():
-                if v.is_floating_point() and self.live_specs[prog.stage_ranges[s][0]].get(k, (0, 0, False))[2]:
+                if v.is_floating_point() and spec0.get(k, (0, 0, False))[2]:
                     v.requires_grad_(True)
-        out = self._stage_forward(st_in, grad=not sc_pass)
+        out = self._stage_forward(pi, st_in, grad=not sc_pass)
         if s == S - 1:
             if sc_pass:
-                eps = out["out"].detach()
-                self._send_feedback(m, eps, lo_r)
+                self._send_feedback(pi, m, out["out"].detach(), lo_r)
             else:
                 pred = out["out"]
                 dpred = torch.empty_like(pred)
@@ -434,116 +453,122 @@ class PipelineExecutor:
         else:
             if not sc_pass:
                 self._saved[key] = (st_in, out, None)
-            self._send_live(s, m, out, lo_r, "fwd_sc" if sc_pass else "fwd")
+            self._send_live(pi, s, m, out, lo_r)
 
-    def _bwd(self, m):
+    def _bwd(self, pi, m):
         prog = self.prog
-        s = self.stage
-        st_in, outs, grads = self._saved.pop((m, False))
+        pl = prog.pipes[pi]
+        s = self.stages[pi]
+        st_in, outs, grads = self._saved.pop((pi, m, False))
         if s == prog.S - 1:
             torch.autograd.backward(outs, grads)
         else:
-            lo_r, hi_r = prog.replica_range(s, m, self.replica)
-            spec = self.live_specs[prog.stage_ranges[s][1]]
+            lo_r, hi_r = prog.replica_range(s, m, self.replica, pi)
+            spec = self._spec(pi, pl.stage_ranges[s][1])
             names = [k for k in sorted(spec) if spec[k][2]]
-            gin = self._recv_grads(s, m, hi_r - lo_r, lo_r, names)
+            gin = self._recv_grads(pi, s, m, hi_r - lo_r, lo_r, names)
             ts = [outs[k] for k in names if outs[k].requires_grad]
             gs = [gin[k] for k in names if outs[k].requires_grad]
             if ts:
                 torch.autograd.backward(ts, gs)
         if s > 0:
-            spec = self.live_specs[prog.stage_ranges[s][0]]
+            spec = self._spec(pi, pl.stage_ranges[s][0])
             names = [k for k in sorted(spec) if spec[k][2]]
             grads_in = {k: (st_in[k].grad if st_in[k].grad is not None else torch.zeros_like(st_in[k]))
                         for k in names}
-            lo_r, _ = prog.replica_range(s, m, self.replica)
-            self._send_grads(s, m, grads_in, lo_r)
+            lo_r, _ = prog.replica_range(s, m, self.replica, pi)
+            self._send_grads(pi, s, m, grads_in, lo_r)
 
     # live-set P2P -------------------------------------------------------------------------
-    def _pieces(self, s, m, as_src):
-        """(peer_replica, lo, hi) pieces of micro m crossing cut s -> s+1 for this device."""
+    def _pieces(self, pi, s, m, as_src):
+        """(peer_replica, lo, hi) pieces of micro m crossing cut s -> s+1 of pipe pi for this device."""
         out = []
-        for i, j, a, b in backbone_transfers(self.prog, s, m):
+        for i, j, a, b in backbone_transfers(self.prog, s, m, pi):
             if as_src and i == self.replica:
                 out.append((j, a, b))
             if not as_src and j == self.replica:
                 out.append((i, a, b))
         return out
 
-    def _send_live(self, s, m, out, lo_r, kind):
-        spec = self.live_specs[self.prog.stage_ranges[s][1]]
-        dst0 = self.prog.stage_devices[s + 1][0]
-        for j, a, b in self._pieces(s, m, True):
+    def _send_live(self, pi, s, m, out, lo_r):
+        pl = self.prog.pipes[pi]
+        spec = self._spec(pi, pl.stage_ranges[s][1])
+        dst0 = pl.stage_devices[s + 1][0]
+        for j, a, b in self._pieces(pi, s, m, True):
             for k in sorted(spec):
-                self._pending.append(self.links.isend("fwd", out[k].detach()[a - lo_r:b - lo_r],
+                self._pending.append(self.links.isend(f"fwd{pi}", out[k].detach()[a - lo_r:b - lo_r],
                                                       self._grank(dst0 + j)))
 
-    def _recv_live(self, s, m, n, lo_r, kind):
-        spec_b = self.prog.stage_ranges[s][0]
-        bufs = self._live_recv(spec_b, n)
-        src0 = self.prog.stage_devices[s - 1][0]
+    def _recv_live(self, pi, s, m, n, lo_r):
+        pl = self.prog.pipes[pi]
+        spec = self._spec(pi, pl.stage_ranges[s][0])
+        bufs = {k: torch.empty((n,) + tuple(shape), device=self.device, dtype=dt)
+                for k, (shape, dt, g) in sorted(spec.items())}
+        src0 = pl.stage_devices[s - 1][0]
         works = []
-        for i, a, b in self._pieces(s - 1, m, False):
+        for i, a, b in self._pieces(pi, s - 1, m, False):
             for k in sorted(bufs):
-                works.append(self.links.irecv("fwd", bufs[k][a - lo_r:b - lo_r], self._grank(src0 + i)))
+                works.append(self.links.irecv(f"fwd{pi}", bufs[k][a - lo_r:b - lo_r], self._grank(src0 + i)))
         for w in works:
             w.wait()
         return bufs
 
-    def _send_grads(self, s, m, grads, lo_r):
-        src0 = self.prog.stage_devices[s - 1][0]
-        for i, a, b in self._pieces(s - 1, m, False):
+    def _send_grads(self, pi, s, m, grads, lo_r):
+        src0 = self.prog.pipes[pi].stage_devices[s - 1][0]
+        for i, a, b in self._pieces(pi, s - 1, m, False):
             for k in sorted(grads):
-                self._pending.append(self.links.isend("bwd", grads[k][a - lo_r:b - lo_r],
+                self._pending.append(self.links.isend(f"bwd{pi}", grads[k][a - lo_r:b - lo_r],
                                                       self._grank(src0 + i)))
 
-    def _recv_grads(self, s, m, n, lo_r, names):
-        spec = self.live_specs[self.prog.stage_ranges[s][1]]
+    def _recv_grads(self, pi, s, m, n, lo_r, names):
+        pl = self.prog.pipes[pi]
+        spec = self._spec(pi, pl.stage_ranges[s][1])
         bufs = {k: torch.empty((n,) + tuple(spec[k][0]), device=self.device, dtype=spec[k][1]) for k in names}
-        dst0 = self.prog.stage_devices[s + 1][0]
+        dst0 = pl.stage_devices[s + 1][0]
         works = []
-        for j, a, b in self._pieces(s, m, True):
+        for j, a, b in self._pieces(pi, s, m, True):
             for k in names:
-                works.append(self.links.irecv("bwd", bufs[k][a - lo_r:b - lo_r], self._grank(dst0 + j)))
+                works.append(self.links.irecv(f"bwd{pi}", bufs[k][a - lo_r:b - lo_r], self._grank(dst0 + j)))
         for w in works:
             w.wait()
         return bufs
 
-    def _send_feedback(self, m, eps, lo_r):
+    def _send_feedback(self, pi, m, eps, lo_r):
         prog = self.prog
         if prog.S == 1:
-            self._feedback_in[m] = eps
+            self._feedback_in[(pi, m)] = eps
             return
-        b0 = prog.stage_devices[0][0]
-        for i, j, a, b in self._feedback_pieces(prog, m):
+        b0 = prog.pipes[pi].stage_devices[0][0]
+        for i, j, a, b in self._feedback_pieces(prog, m, pi):
             if i == self.replica:
-                self._pending.append(self.links.isend("fb", eps[a - lo_r:b - lo_r], self._grank(b0 + j)))
+                self._pending.append(self.links.isend(f"fb{pi}", eps[a - lo_r:b - lo_r], self._grank(b0 + j)))
 
-    def _recv_feedback(self, m):
+    def _recv_feedback(self, pi, m):
         prog = self.prog
-        lo_r, hi_r = prog.replica_range(0, m, self.replica)
-        spec = self.live_specs[-1]["out"]
+        lo_r, hi_r = prog.replica_range(0, m, self.replica, pi)
+        spec = self._spec(pi, -1)["out"]
         buf = torch.empty((hi_r - lo_r,) + tuple(spec[0]), device=self.device, dtype=spec[1])
-        a0 = prog.stage_devices[-1][0]
-        works = [self.links.irecv("fb", buf[a - lo_r:b - lo_r], self._grank(a0 + i))
-                 for i, j, a, b in self._feedback_pieces(prog, m) if j == self.replica]
+        a0 = prog.pipes[pi].stage_devices[-1][0]
+        works = [self.links.irecv(f"fb{pi}", buf[a - lo_r:b - lo_r], self._grank(a0 + i))
+                 for i, j, a, b in self._feedback_pieces(prog, m, pi) if j == self.replica]
         for w in works:
             w.wait()
-        self._feedback_in[m] = buf
+        self._feedback_in[(pi, m)] = buf
 
     # ---------------------------------------------------------------- sync
-    def _sync(self):
-        store = self.model.backbone.store
-        lo, hi = self.param_range
+    def _sync(self, pi):
+        store = self._backbone(pi).store
+        lo, hi = self.param_ranges[pi]
         if hasattr(store, "pre_allreduce"):
             store.pre_allreduce()
-        if self._stage_pg is not None and hi > lo:
+        pg = self._stage_pgs[pi]
+        if pg is not None and hi > lo:
             if self.links.staged and store.grad.is_cuda:
                 host = store.grad[lo:hi].cpu()
-                dist.all_reduce(host, group=self._stage_pg)
+                dist.all_reduce(host, group=pg)
                 store.grad[lo:hi].copy_(host)
             else:
-                dist.all_reduce(store.grad[lo:hi], group=self._stage_pg)
+                dist.all_reduce(store.grad[lo:hi], group=pg)
         if self.grad_snapshots is not None:
             self.grad_snapshots.append((lo, hi, store.grad[lo:hi].detach().clone()))
         store.adamw_step(rng=(lo, hi), **self.model.adamw)
@@ -575,15 +600,14 @@ class PipelineExecutor:
         for ins in instrs:
             kind = ins[0]
             if kind in ("fwd", "fwd_sc", "bwd"):
-                _, m, s = ins
+                _, m, s, pi = ins
                 with self.streams.on("compute"):
-                    if kind == "fwd" and s == 0 and prog.selfcond:
-                        if prog.S > 1:
-                            self._recv_feedback(m)
+                    if kind == "fwd" and s == 0 and prog.selfcond and prog.S > 1:
+                        self._recv_feedback(pi, m)
                     if kind == "bwd":
-                        self._bwd(m)
+                        self._bwd(pi, m)
                     else:
-                        self._fwd(m, kind == "fwd_sc")
+                        self._fwd(pi, m, kind == "fwd_sc")
                     last_compute_ev = self.streams.event("compute")
             elif kind == "fill":
                 if not has_next:
@@ -593,7 +617,7 @@ class PipelineExecutor:
                     self._run_pieces(prog, prog.fills[ins[1]], store, raw_next, posted, sent)
             elif kind == "sync":
                 with self.streams.on("compute"):
-                    self._sync()
+                    self._sync(ins[2])
             elif kind == "tail":
                 if not has_next:
                     continue

@@ -163,10 +163,11 @@ class TorchOps:
         return torch.cat([a, b], -1)
 
 
-def build(selfcond=True, L=6, deps=False):
+def build(selfcond=True, L=6, deps=False, two=False):
     from paper_2405_01248_b200.diffusion import noise_schedule
 
     bb = Backbone(L, selfcond)
+    bbs = [bb, Backbone(L, selfcond, seed=11)] if two else None
     vae = _Frozen("vae", {"v0": (IMG * IMG * 3, 16), "v1": (16, 16), "v2": (16, LAT * LAT * ZC)}, _vae, 2)
     txt = _Frozen("text", {"emb": (VOCAB, 8), "t1": (8, HID), "tp": (HID, HID)}, _text, 3)
     frozen = [FrozenSpec(vae, ("images",)), FrozenSpec(txt, ("ids",))]
@@ -176,7 +177,7 @@ def build(selfcond=True, L=6, deps=False):
     sab, s1m = noise_schedule()
     m = TrainModel(bb, frozen, TorchOps, sab, s1m,
                    selfcond_channels=ZC if selfcond else 0,
-                   adamw=dict(lr=1e-2, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01))
+                   adamw=dict(lr=1e-2, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01), backbones=bbs)
     m.selfcond_p = 0.5 if selfcond else 0.0
     m.frozen_deps = ((0, 2), (1, 2)) if deps else ()
     return m

@@ -11,7 +11,8 @@ from paper_2405_01248_b200.adapter import build_group_program, split_range
 from paper_2405_01248_b200.pipefill import filler, planner, profile, scheduler
 
 
-def _profile(seed, L=8, frozen=(5, 3), p=0.0, keys=(1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64, 96, 128)):
+def _profile(seed, L=8, frozen=(5, 3), p=0.0, keys=(1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64, 96, 128),
+             backbones=1):
     rnd = random.Random(seed)
 
     def layer(f, b, frozen_layer=False):
@@ -20,17 +21,18 @@ def _profile(seed, L=8, frozen=(5, 3), p=0.0, keys=(1, 2, 3, 4, 6, 8, 12, 16, 24
             fwd_comm_bytes={k: 1000 * k for k in keys}, bwd_comm_bytes={k: (0 if frozen_layer else 1000 * k) for k in keys},
             grad_bytes={k: 0 if frozen_layer else 4000 for k in keys}, out_bytes={k: 100 * k for k in keys})
 
-    bb = profile.ComponentProfile("bb", [layer(rnd.uniform(0.5, 2) * 1e-3, rnd.uniform(1, 4) * 1e-3)
-                                         for _ in range(L)], True)
+    bbs = tuple(profile.ComponentProfile(f"bb{k}", [layer(rnd.uniform(0.5, 2) * 1e-3, rnd.uniform(1, 4) * 1e-3)
+                                                    for _ in range(L)], True) for k in range(backbones))
     fr = [profile.ComponentProfile(f"f{i}", [layer(rnd.uniform(0.2, 1.5) * 1e-3, 0, True) for _ in range(n)],
                                    False) for i, n in enumerate(frozen)]
-    return profile.ModelProfile((bb,), tuple(fr), (), p)
+    return profile.ModelProfile(bbs, tuple(fr), (), p)
 
 
-@pytest.mark.parametrize("seed,S,M,D,p", [(0, 2, 4, 2, 0.0), (1, 4, 4, 4, 0.0), (2, 4, 8, 4, 0.0),
-                                          (3, 2, 4, 4, 0.0), (4, 4, 4, 4, 0.5), (5, 3, 6, 3, 0.0)])
-def test_programs_replay_schedule_and_fill(seed, S, M, D, p):
-    prof = _profile(seed, p=p)
+@pytest.mark.parametrize("seed,S,M,D,p,nb", [(0, 2, 4, 2, 0.0, 1), (1, 4, 4, 4, 0.0, 1), (2, 4, 8, 4, 0.0, 1),
+                                             (3, 2, 4, 4, 0.0, 1), (4, 4, 4, 4, 0.5, 1), (5, 3, 6, 3, 0.0, 1),
+                                             (6, 2, 4, 2, 0.0, 2), (7, 4, 4, 4, 0.0, 2)])
+def test_programs_replay_schedule_and_fill(seed, S, M, D, p, nb):
+    prof = _profile(seed, p=p, backbones=nb)
     cluster = profile.ClusterConfig(D, profile.CommCosts(2e11, 1e-5, 3e11, 1e-5))
     res = planner.evaluate_point(prof, cluster, S, M, D, 64 * M // 4)
     counts = [len(c.layers) for c in prof.frozen]
@@ -39,15 +41,16 @@ def test_programs_replay_schedule_and_fill(seed, S, M, D, p):
     # 1. compute tasks: exactly the schedule's, per device, in start order
     sched = res["pre_fill_schedule"]
     for dev in range(D):
-        want = [(t.kind, t.micro_batch, t.stage) for t in sorted(
+        want = [(t.kind, t.micro_batch, t.stage, 0 if t.direction == "down" else 1) for t in sorted(
             (t for t in sched.tasks if t.device == dev and t.kind in ("fwd", "bwd", "fwd_sc")),
             key=lambda t: (t.start, t.end))]
         got = [i for i in prog.devices[dev].instrs if i[0] in ("fwd", "bwd", "fwd_sc")]
         assert got == want
         kinds = [i[0] for i in prog.devices[dev].instrs]
-        assert kinds[-1] == "deliver" and kinds.count("sync") == 1
-        last_bwd = max(k for k, i in enumerate(prog.devices[dev].instrs) if i[0] == "bwd")
-        assert prog.devices[dev].instrs[last_bwd + 1][0] == "sync"
+        assert kinds[-1] == "deliver" and kinds.count("sync") == len(prog.pipes)
+        for pi in range(len(prog.pipes)):
+            last_bwd = max(k for k, i in enumerate(prog.devices[dev].instrs) if i[0] == "bwd" and i[3] == pi)
+            assert prog.devices[dev].instrs[last_bwd + 1][:1] == ("sync",)
     # 2. frozen coverage: each (comp, layer) sample range covered exactly once
     for c, n in enumerate(counts):
         for layer in range(n):
