@@ -258,6 +258,13 @@ def main():
         ms, _, launches, _ = timed_steps(trainer, K, world)
     value = wb * K / (ms / 1000.0)
 
+    # measured bubble ratio: one traced iteration after the timed region, task intervals from
+    # CUDA events on their streams, bubbles / ratio by the planner's own definitions
+    barrier(world)
+    trainer.step(trace=True)
+    _, _, br_meas = trainer.measured()
+    br_meas_unf = None
+
     # speedup vs the same executor's unfilled pipeline (frozen part data-parallel, un-overlapped)
     speedup = 1.0
     if lay["S"] > 1:
@@ -268,6 +275,9 @@ def main():
             unf.step()
         ms_u, _, _, _ = timed_steps(unf, K, world)
         speedup = ms_u / ms
+        barrier(world)
+        unf.step(trace=True)
+        _, _, br_meas_unf = unf.measured()
         del unf
 
     e2e = None
@@ -320,6 +330,8 @@ def main():
                        "dispatch": "cuda_graph" if use_graph else "eager"},
             "bubble_ratio_predicted_before": res["bubble_ratio_before"],
             "bubble_ratio_predicted_after": res["bubble_ratio_after"],
+            "bubble_ratio_measured": br_meas,
+            "bubble_ratio_measured_unfilled": br_meas_unf,
             "speedup_vs_unfilled": speedup,
             "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
             "clocks": clk.summary(),

@@ -271,9 +271,10 @@ class Trainer:
         self._cur = self._feed(self.it)
         self.ex.warmup(lambda f, lo, hi: self._cur.get(f, self.ex.gb_of() + lo, self.ex.gb_of() + hi))
 
-    def step(self, has_next=True):
-        """One iteration: train on batch `it` (frozen outputs ready), fill batch it+1."""
-        if getattr(self, "_graph", None) is not None and has_next:
+    def step(self, has_next=True, trace=False):
+        """One iteration: train on batch `it` (frozen outputs ready), fill batch it+1.
+        trace=True records measured task intervals (see `measured`)."""
+        if getattr(self, "_graph", None) is not None and has_next and not trace:
             return self._graph_step()
         if self.it == 0 and not self.ex.frozen_ready:
             self.warmup_frozen()
@@ -282,7 +283,16 @@ class Trainer:
         self.ex.inputs = cur
         gb = self.ex.gb_of()
         raw = (lambda f, lo, hi: nxt.get(f, gb + lo, gb + hi)) if nxt is not None else None
-        loss = self.ex.run_iteration(raw, cur.selfcond, has_next=has_next)
+        loss = self.ex.run_iteration(raw, cur.selfcond, has_next=has_next, trace=trace)
         self._cur = nxt
         self.it += 1
         return loss
+
+    def measured(self, min_len=0.0):
+        """Measured schedule of the last traced step (collective over the job): returns
+        (Schedule, bubbles, bubble_ratio) computed with the planner's own extract_bubbles /
+        bubble_ratio (reference scheduler.py:395,434) on barrier-aligned task times; the tail
+        counts as busy (planner.py:172-175)."""
+        sched = self.ex.measured_schedule()
+        bubbles = scheduler.extract_bubbles(sched, min_len)
+        return sched, bubbles, scheduler.bubble_ratio(sched, bubbles)

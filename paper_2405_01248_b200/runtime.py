@@ -177,6 +177,52 @@ class Links:
 _DEBUG = bool(int(__import__("os").environ.get("DP_DEBUG_P2P", "0")))
 
 
+class _Tracer:
+    """Measured per-task times of one iteration on this rank (SURVEY §8d "measured bubble
+    ratio"): CUDA events on the stream each task runs on (host clock on CPU), relative to an
+    origin recorded on the compute stream when the iteration starts. `tasks()` returns
+    pipefill `Task`s in seconds so the planner's own `extract_bubbles` / `bubble_ratio`
+    (scheduler.py:395,434 of the reference) can be applied to the measured schedule."""
+
+    def __init__(self, streams, dev):
+        self.streams, self.dev = streams, dev
+        self.recs = []
+        self.cuda = streams.cuda
+        if self.cuda:
+            self.t0 = torch.cuda.Event(enable_timing=True)
+            self.t0.record(streams.compute)
+        else:
+            self.t0 = time.perf_counter()
+
+    def _mark(self, which):
+        if not self.cuda:
+            return time.perf_counter()
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(self.streams.compute if which == "compute" else self.streams.fill)
+        return ev
+
+    @contextlib.contextmanager
+    def task(self, which, kind, m=None, s=None, direction="down", tag=""):
+        a = self._mark(which)
+        yield
+        self.recs.append((kind, m, s, direction, tag, a, self._mark(which)))
+
+    def tasks(self):
+        from .pipefill.scheduler import Task
+
+        out = []
+        if self.cuda:
+            self.streams.compute.synchronize()
+            self.streams.fill.synchronize()
+        for kind, m, s, d, tag, a, b in self.recs:
+            if self.cuda:
+                ta, tb = self.t0.elapsed_time(a) * 1e-3, self.t0.elapsed_time(b) * 1e-3
+            else:
+                ta, tb = a - self.t0, b - self.t0
+            out.append(Task(self.dev, kind, m, s, d, max(0.0, ta), max(0.0, tb), tag))
+        return out
+
+
 # ============================================================================ executor
 
 
@@ -586,8 +632,9 @@ class PipelineExecutor:
         with self.streams.on("compute"):
             self.frozen_ready = self._deliver(prog, store, posted)
 
-    def run_iteration(self, raw_next, selfcond, has_next=True):
-        """One training iteration on the current batch; fills compute batch i+1 (`raw_next`)."""
+    def run_iteration(self, raw_next, selfcond, has_next=True, trace=False):
+        """One training iteration on the current batch; fills compute batch i+1 (`raw_next`).
+        trace=True records every task's measured interval (see `measured_tasks`)."""
         self.prog = prog = self.programs[bool(selfcond)]
         self.frozen_cur = self.frozen_ready
         self.frozen_ready = {}
@@ -595,13 +642,15 @@ class PipelineExecutor:
         self._saved, self._xt, self._feedback_in, self._pending = {}, {}, {}, []
         store, posted, sent = {}, {}, set()
         self.loss_buf.zero_()
+        tr = self.tracer = _Tracer(self.streams, self.dev) if trace else None
+        task = tr.task if tr else (lambda *a, **k: contextlib.nullcontext())
         last_compute_ev = None
         instrs = prog.device_program(self.dev).instrs
         for ins in instrs:
             kind = ins[0]
             if kind in ("fwd", "fwd_sc", "bwd"):
                 _, m, s, pi = ins
-                with self.streams.on("compute"):
+                with self.streams.on("compute"), task("compute", kind, m, s, prog.pipes[pi].direction):
                     if kind == "fwd" and s == 0 and prog.selfcond and prog.S > 1:
                         self._recv_feedback(pi, m)
                     if kind == "bwd":
@@ -613,20 +662,22 @@ class PipelineExecutor:
                 if not has_next:
                     continue
                 self.streams.wait("fill", last_compute_ev)
-                with self.streams.on("fill"):
+                with self.streams.on("fill"), task("fill", "fill", tag=f"bubble{ins[1]}"):
                     self._run_pieces(prog, prog.fills[ins[1]], store, raw_next, posted, sent)
             elif kind == "sync":
-                with self.streams.on("compute"):
+                with self.streams.on("compute"), task("compute", "sync", s=self.stages[ins[2]],
+                                                      direction=prog.pipes[ins[2]].direction):
                     self._sync(ins[2])
             elif kind == "tail":
                 if not has_next:
                     continue
                 self.streams.join()
-                with self.streams.on("compute"):
+                # leftover frozen work: busy time (planner.py:172-175), recorded as a fill task
+                with self.streams.on("compute"), task("compute", "fill", tag="tail"):
                     self._run_pieces(prog, prog.tail, store, raw_next, posted, sent)
             elif kind == "deliver":
                 self.streams.join()
-                with self.streams.on("compute"):
+                with self.streams.on("compute"), task("compute", "p2p_comm", tag="deliver"):
                     if has_next:
                         self.frozen_ready = self._deliver(prog, store, posted)
                     for w in self._pending:
@@ -634,6 +685,26 @@ class PipelineExecutor:
         if self.streams.cuda:
             torch.cuda.current_stream(self.device).wait_stream(self.streams.compute)
         return self.loss_buf
+
+    def measured_tasks(self):
+        """Measured tasks of the last traced iteration on this rank (device = local index)."""
+        return self.tracer.tasks() if getattr(self, "tracer", None) else []
+
+    def measured_schedule(self):
+        """Gather every rank's measured tasks of the last traced iteration; returns the
+        measured pipefill `Schedule` of this rank's pipeline group (collective call)."""
+        from .pipefill.scheduler import Schedule
+
+        mine = self.measured_tasks()
+        if self.world > 1:
+            allt = [None] * self.world
+            dist.all_gather_object(allt, mine)
+            allt = allt[self.group * self.D:(self.group + 1) * self.D]
+        else:
+            allt = [mine]
+        tasks = [t for ts in allt for t in ts]
+        makespan = max((t.end for t in tasks), default=0.0)
+        return Schedule(tasks, makespan, self.D)
 
     def total_loss(self):
         """Sum of the loss over all ranks (only last-stage ranks contribute)."""

@@ -50,8 +50,12 @@ def _worker(rank, world, S, M, D, selfcond, wb, port, outdir, deps=False, two=Fa
     tr = _make(world, rank, S, M, D, selfcond, wb, deps, two)
     losses = []
     for i in range(ITERS):
-        tr.step(has_next=i < ITERS - 1)
+        dist.barrier()
+        tr.step(has_next=i < ITERS - 1, trace=i == ITERS - 2)
         losses.append(tr.ex.total_loss().item())
+        if i == ITERS - 2:
+            sched, bubbles, ratio = tr.measured()
+            mine = tr.ex.measured_tasks()
     prog = tr.ex.programs[True]
     params = []
     for pi, rng in enumerate(tr.ex.param_ranges):
@@ -61,7 +65,9 @@ def _worker(rank, world, S, M, D, selfcond, wb, port, outdir, deps=False, two=Fa
             params.append((bi, lo, hi, tr.model.backbones[bi].store.flat.detach()[lo:hi].clone()))
     torch.save(dict(losses=losses, params=params, npipes=len(prog.pipes),
                     transfers=len(prog.transfers), fills=sum(len(f) for f in prog.fills),
-                    tail=len(prog.tail)),
+                    tail=len(prog.tail), ratio=ratio, ntasks=len(sched.tasks), mine=mine,
+                    instrs=[i[0] for i in tr.ex.prog.device_program(tr.ex.dev).instrs],
+                    makespan=sched.makespan),
                os.path.join(outdir, f"r{rank}.pt"))
     dist.barrier()
     dist.destroy_process_group()
@@ -92,7 +98,7 @@ def test_pipelined_equals_sequential(tmp_path, world, S, M, D, selfcond, deps, t
     mp.spawn(_worker, args=(world, S, M, D, selfcond, wb, _free_port(), str(tmp_path), deps, two),
              nprocs=world, join=True)
     ref_losses, ref_flats = _reference(selfcond, wb, deps, two)
-    outs = [torch.load(os.path.join(tmp_path, f"r{r}.pt")) for r in range(world)]
+    outs = [torch.load(os.path.join(tmp_path, f"r{r}.pt"), weights_only=False) for r in range(world)]
     covered = [torch.zeros(f.numel(), dtype=torch.bool) for f in ref_flats]
     for o in outs:
         assert o["npipes"] == (2 if two else 1)
@@ -102,6 +108,15 @@ def test_pipelined_equals_sequential(tmp_path, world, S, M, D, selfcond, deps, t
             assert torch.allclose(p, ref_flats[bi][lo:hi], rtol=1e-5, atol=1e-6)
             covered[bi][lo:hi] = True
     assert all(c.all() for c in covered)
+    # measured schedule of a traced iteration: one task per executed instruction, compute
+    # tasks in program order, a bubble ratio in [0, 1) from the planner's own definitions
+    for o in outs:
+        kinds = [t.kind for t in o["mine"]]
+        assert len(kinds) == len(o["instrs"]), (kinds, o["instrs"])
+        comp = [t for t in o["mine"] if t.kind in ("fwd", "bwd", "fwd_sc")]
+        assert all(a.end <= b.start + 1e-9 for a, b in zip(comp, comp[1:]))
+        assert 0.0 <= o["ratio"] < 1.0 and o["makespan"] > 0
+        assert o["ntasks"] == sum(len(x["mine"]) for x in outs) // (world // D)
     # the fill plan actually exercised bubbles (and, with several devices, frozen transfers)
     # (bidirectional plans leave bubbles too short to fill at this toy size)
     assert two or any(o["fills"] > 0 for o in outs)
