@@ -68,6 +68,13 @@ typedef struct DpGemmArgs {
   int64_t r_ld, r_bs1, r_bs2;
   float alpha;
   int split_k; /* 0 = heuristic */
+  /* optional fp32 workspace (caller-owned, 16-byte aligned). When a bf16 STORE GEMM covers
+     too few tiles to fill the SMs, the kernel accumulates split-K partials into it with fp32
+     atomics and a finish kernel applies bias/residual and writes D. dp_gemm_workspace()
+     returns the bytes that enable this (0: not needed); with a smaller or NULL workspace the
+     GEMM runs unsplit. */
+  float* workspace;
+  int64_t workspace_bytes;
 } DpGemmArgs;
 
 /* 2-D convolution over NHWC activations with weights [K][R][S][C].
@@ -87,6 +94,8 @@ typedef struct DpConvArgs {
   float alpha;
   int out_mode;
   int split_k;
+  float* workspace; /* as DpGemmArgs::workspace (conv fwd / dgrad) */
+  int64_t workspace_bytes;
 } DpConvArgs;
 
 /* Multi-head attention over strided [B][N][heads*head_dim] activations (q, k, v may be
@@ -106,6 +115,11 @@ typedef struct DpAttnArgs {
 } DpAttnArgs;
 
 int dp_gemm(const DpGemmArgs* args, dp_stream_t stream);
+/* bytes of fp32 workspace that let dp_gemm / dp_conv_fwd / dp_conv_dgrad split K over all SMs
+   for an under-filled launch (0 = the launch fills the machine unsplit); host-only query */
+int64_t dp_gemm_workspace(const DpGemmArgs* args);
+int64_t dp_conv_fwd_workspace(const DpConvArgs* args);
+int64_t dp_conv_dgrad_workspace(const DpConvArgs* args);
 /* fused attention forward (tcgen05 S = QK^T and O = PV, online softmax from TMEM);
    bf16, head_dim 64 */
 int dp_flash_attn_fwd(const DpAttnArgs* args, dp_stream_t stream);

@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdpipe.so")
+LIB_PATH = os.environ.get("DP_LIB_PATH") or os.path.join(_HERE, "libdpipe.so")  # override: A/B kernel experiments
 
 DP_F32 = 0
 DP_BF16 = 1
@@ -35,6 +35,7 @@ class DpGemmArgs(ctypes.Structure):
         ("Res", c_void_p), ("r_ld", c_i64), ("r_bs1", c_i64), ("r_bs2", c_i64),
         ("alpha", c_float),
         ("split_k", c_int),
+        ("workspace", c_void_p), ("workspace_bytes", c_i64),
     ]
 
 
@@ -50,6 +51,7 @@ class DpConvArgs(ctypes.Structure):
         ("alpha", c_float),
         ("out_mode", c_int),
         ("split_k", c_int),
+        ("workspace", c_void_p), ("workspace_bytes", c_i64),
     ]
 
 
@@ -65,6 +67,9 @@ class DpAttnArgs(ctypes.Structure):
 # name -> argtypes (restype is always c_int unless listed in _RESTYPES)
 _SIGNATURES = {
     "dp_gemm": [ctypes.POINTER(DpGemmArgs), c_void_p],
+    "dp_gemm_workspace": [ctypes.POINTER(DpGemmArgs)],
+    "dp_conv_fwd_workspace": [ctypes.POINTER(DpConvArgs)],
+    "dp_conv_dgrad_workspace": [ctypes.POINTER(DpConvArgs)],
     "dp_conv_fwd": [ctypes.POINTER(DpConvArgs), c_void_p],
     "dp_conv_wgrad": [ctypes.POINTER(DpConvArgs), c_void_p],
     "dp_conv_dgrad": [ctypes.POINTER(DpConvArgs), c_void_p],
@@ -122,7 +127,8 @@ _SIGNATURES = {
     "dp_last_error": [],
     "dp_version": [],
 }
-_RESTYPES = {"dp_last_error": ctypes.c_char_p, "dp_group_norm_workspace": ctypes.c_size_t}
+_RESTYPES = {"dp_last_error": ctypes.c_char_p, "dp_group_norm_workspace": ctypes.c_size_t,
+             "dp_gemm_workspace": c_i64, "dp_conv_fwd_workspace": c_i64, "dp_conv_dgrad_workspace": c_i64}
 
 _lib = None
 

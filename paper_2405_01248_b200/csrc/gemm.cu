@@ -715,8 +715,100 @@ static int launch_cg(int bn, const CUtensorMap& ma, const CUtensorMap& mb, const
   }
 }
 
+static void choose_split(TcParams& p, int requested, bool allowed);
+
+// ---------------------------------------------------------------- split-K for bf16 outputs
+// A bf16 STORE launch whose tiles cover only a fraction of the SMs (U-Net 4x4 / 8x8 level
+// convs, M = 32 time-embedding linears, ...) is re-run as an fp32 atomic split-K / stream-K
+// GEMM into a caller-provided workspace, then finished (bias, residual, bf16) by one
+// elementwise pass: the tensor cores of every SM work on the long K instead of a few.
+__global__ void __launch_bounds__(256)
+    splitk_finish_kernel(const float* __restrict__ ws, __nv_bfloat16* __restrict__ D, int64_t d_ld,
+                         int64_t d_bs1, int64_t d_bs2, const float* __restrict__ bias,
+                         const __nv_bfloat16* __restrict__ R, int64_t r_ld, int64_t r_bs1,
+                         int64_t r_bs2, int M, int N, int batch1, int64_t total) {
+  const int nv = N / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = static_cast<int>(i % nv);
+    const int64_t r = i / nv;
+    const int m = static_cast<int>(r % M);
+    const int z = static_cast<int>(r / M);
+    const int z1 = z % batch1, z2 = z / batch1;
+    const float4* w = reinterpret_cast<const float4*>(ws + ((int64_t)z * M + m) * N + v * 8);
+    const float4 a = w[0], b = w[1];
+    float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    if (bias) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[j] += __ldg(bias + v * 8 + j);
+    }
+    if (R) {
+      const uint4 u = *reinterpret_cast<const uint4*>(R + z1 * r_bs1 + z2 * r_bs2 + (int64_t)m * r_ld + v * 8);
+      const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[j] += __bfloat162float(rb[j]);
+    }
+    uint4 o;
+    o.x = pack_bf16x2(f[0], f[1]);
+    o.y = pack_bf16x2(f[2], f[3]);
+    o.z = pack_bf16x2(f[4], f[5]);
+    o.w = pack_bf16x2(f[6], f[7]);
+    *reinterpret_cast<uint4*>(D + z1 * d_bs1 + z2 * d_bs2 + (int64_t)m * d_ld + v * 8) = o;
+  }
+}
+
+// fraction of the SMs below which a bf16 launch is split (DP_SPLITK_FRAC, percent; experiments)
+static int splitk_pct() {
+  static const int v = [] {
+    const char* e = getenv("DP_SPLITK_FRAC");
+    return e ? atoi(e) : 50;
+  }();
+  return v;
+}
+
+static int64_t splitk_bytes(const TcParams& p, int cg, int M, int N) {
+  if (p.d_f32 || p.out_mode != DP_OUT_STORE || !p.vec_ok || (N % 8) || p.num_kb < 8) return 0;
+  const long long ctas = (long long)p.tiles_m * p.tiles_n * p.nbatch * cg;
+  if (ctas * 100 >= (long long)kNumSMs * splitk_pct()) return 0;
+  return 4LL * M * N * p.nbatch;
+}
+
 static int launch_bn(int bn, int cg, const CUtensorMap& ma, const CUtensorMap& mb, TcParams& p, int M,
-                     int N, int b1, int b2, cudaStream_t st) {
+                     int N, int b1, int b2, cudaStream_t st, float* ws = nullptr, int64_t ws_bytes = 0) {
+  const int64_t need = splitk_bytes(p, cg, M, N);
+  if (need > 0 && ws && ws_bytes >= need && (reinterpret_cast<uintptr_t>(ws) % 16) == 0) {
+    TcParams q = p;
+    q.D = ws;
+    q.d_f32 = 1;
+    q.out_mode = DP_OUT_ATOMIC_ADD;
+    q.bias = nullptr;
+    q.R = nullptr;
+    q.d_ld = N;
+    q.d_bs1 = (int64_t)M * N;
+    q.d_bs2 = (int64_t)M * N * b1;
+    q.vec_ok = (N % 4) == 0;
+    q.d_tma = 0;
+    choose_split(q, 0, true);
+    cudaError_t e = cudaMemsetAsync(ws, 0, need, st);
+    if (e != cudaSuccess) {
+      set_error(std::string("split-K workspace memset: ") + cudaGetErrorString(e));
+      return e;
+    }
+    int rc = cg == 2 ? launch_cg<2>(bn, ma, mb, ma, q, st) : launch_cg<1>(bn, ma, mb, ma, q, st);
+    if (rc) return rc;
+    const int64_t total = (int64_t)p.nbatch * M * (N / 8);
+    const int64_t want = (total + 255) / 256;
+    const int grid = static_cast<int>(want < 8 * kNumSMs ? want : 8 * kNumSMs);
+    splitk_finish_kernel<<<grid, 256, 0, st>>>(ws, reinterpret_cast<__nv_bfloat16*>(p.D), p.d_ld, p.d_bs1,
+                                               p.d_bs2, p.bias, reinterpret_cast<const __nv_bfloat16*>(p.R),
+                                               p.r_ld, p.r_bs1, p.r_bs2, M, N, b1, total);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      set_error(std::string("split-K finish: ") + cudaGetErrorString(e));
+      return e;
+    }
+    return 0;
+  }
   CUtensorMap md = ma;
   make_dmap(&md, p, M, N, b1, b2);
   return cg == 2 ? launch_cg<2>(bn, ma, mb, md, p, st) : launch_cg<1>(bn, ma, mb, md, p, st);
@@ -771,7 +863,8 @@ static void fill_epilogue(TcParams& p, void* D, int d_dtype, int64_t d_ld, int64
   p.vec_ok = ok ? 1 : 0;
 }
 
-int tc_gemm(const DpGemmArgs* a, cudaStream_t st) {
+int tc_gemm(const DpGemmArgs* a, cudaStream_t st, int64_t* query = nullptr) {
+  if (query) *query = 0;
   if (a->M <= 0 || a->N <= 0 || a->K <= 0) return 0;
   if (a->out_mode == DP_OUT_ATOMIC_ADD && a->d_dtype != DP_F32) {
     set_error("atomic accumulation needs an fp32 output");
@@ -793,6 +886,10 @@ int tc_gemm(const DpGemmArgs* a, cudaStream_t st) {
   choose_split(p, a->split_k, a->out_mode == DP_OUT_ATOMIC_ADD);
   fill_epilogue(p, a->D, a->d_dtype, a->d_ld, a->d_bs1, a->d_bs2, a->out_mode, a->bias, a->Res,
                 a->r_ld, a->r_bs1, a->r_bs2, a->alpha);
+  if (query) {
+    *query = splitk_bytes(p, cg, a->M, a->N);
+    return 0;
+  }
   CUtensorMap ma, mb;
   const uint32_t ones[4] = {1, 1, 1, 1};
   {
@@ -819,7 +916,7 @@ int tc_gemm(const DpGemmArgs* a, cudaStream_t st) {
       if (int e = make_map(&mb, a->B, d, s, box, ones)) return e;
     }
   }
-  return launch_bn(bn, cg, ma, mb, p, a->M, a->N, p.batch1, batch2, st);
+  return launch_bn(bn, cg, ma, mb, p, a->M, a->N, p.batch1, batch2, st, a->workspace, a->workspace_bytes);
 }
 
 // Tile the output pixels (P x Q per image, N images) with boxes of `pixels`
@@ -847,7 +944,8 @@ static bool pixel_box(int P, int Q, int pixels, int& tw, int& th, int& tn) {
   return true;
 }
 
-int tc_conv_fwd(const DpConvArgs* a, cudaStream_t st) {
+int tc_conv_fwd(const DpConvArgs* a, cudaStream_t st, int64_t* query = nullptr) {
+  if (query) *query = 0;
   if (a->C % 64) {
     set_error("implicit conv needs C % 64 == 0");
     return DP_ERR_UNSUPPORTED;
@@ -883,6 +981,10 @@ int tc_conv_fwd(const DpConvArgs* a, cudaStream_t st) {
   choose_split(p, a->split_k, a->out_mode == DP_OUT_ATOMIC_ADD);
   fill_epilogue(p, a->y, a->dtype == DP_BF16 && a->out_mode != DP_OUT_ATOMIC_ADD ? DP_BF16 : DP_F32,
                 a->K, 0, 0, a->out_mode, a->bias, a->Res, a->K, 0, 0, a->alpha);
+  if (query) {
+    *query = splitk_bytes(p, cg, p.M, p.N);
+    return 0;
+  }
   CUtensorMap ma, mb;
   {
     const uint64_t d[4] = {(uint64_t)a->C, (uint64_t)a->W, (uint64_t)a->H, (uint64_t)a->N};
@@ -900,14 +1002,15 @@ int tc_conv_fwd(const DpConvArgs* a, cudaStream_t st) {
     const uint32_t ones[4] = {1, 1, 1, 1};
     if (int e = make_map(&mb, a->w, d, s, box, ones)) return e;
   }
-  return launch_bn(bn, cg, ma, mb, p, p.M, p.N, 1, 1, st);
+  return launch_bn(bn, cg, ma, mb, p, p.M, p.N, 1, 1, st, a->workspace, a->workspace_bytes);
 }
 
 // Input gradient of a stride-1 convolution as an implicit GEMM over dy with the weights read
 // tap-flipped in place (B_DGRAD): dx[n][h][w][c] = sum_{kk,r,s} dy[n][h+r-(R-1-pad_h)]
 // [w+s-(S-1-pad_w)][kk] * w[kk][R-1-r][S-1-s][c]. Args: N,H,W,C describe dx, P,Q dy, x := dy,
 // w := weights [K][R][S][C], y := dx. Strided convolutions zero-dilate dy first (dp_dilate).
-int tc_conv_dgrad(const DpConvArgs* a, cudaStream_t st) {
+int tc_conv_dgrad(const DpConvArgs* a, cudaStream_t st, int64_t* query = nullptr) {
+  if (query) *query = 0;
   if (a->C % 64 || a->K % 64) {
     set_error("implicit dgrad needs C % 64 == 0 and K % 64 == 0");
     return DP_ERR_UNSUPPORTED;
@@ -944,6 +1047,10 @@ int tc_conv_dgrad(const DpConvArgs* a, cudaStream_t st) {
   choose_split(p, a->split_k, a->out_mode == DP_OUT_ATOMIC_ADD);
   fill_epilogue(p, a->y, a->dtype == DP_BF16 && a->out_mode != DP_OUT_ATOMIC_ADD ? DP_BF16 : DP_F32,
                 a->C, 0, 0, a->out_mode, nullptr, a->Res, a->C, 0, 0, a->alpha);
+  if (query) {
+    *query = splitk_bytes(p, cg, p.M, p.N);
+    return 0;
+  }
   CUtensorMap ma, mb;
   {
     const uint64_t d[4] = {(uint64_t)a->K, (uint64_t)a->Q, (uint64_t)a->P, (uint64_t)a->N};
@@ -959,7 +1066,7 @@ int tc_conv_dgrad(const DpConvArgs* a, cudaStream_t st) {
     const uint32_t ones[4] = {1, 1, 1, 1};
     if (int e = make_map(&mb, a->w, d, s, box, ones)) return e;
   }
-  return launch_bn(bn, cg, ma, mb, p, p.M, p.N, 1, 1, st);
+  return launch_bn(bn, cg, ma, mb, p, p.M, p.N, 1, 1, st, a->workspace, a->workspace_bytes);
 }
 
 // dW[k][r][s][c] += sum_{n,p,q} dy[n][p][q][k] * x[n][p*stride+r-pad][q*stride+s-pad][c]
@@ -1144,6 +1251,25 @@ int dp_conv_wgrad(const DpConvArgs* a, dp_stream_t stream) {
     return DP_ERR_UNSUPPORTED;
   }
   return dp::tc_conv_wgrad(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int64_t dp_gemm_workspace(const DpGemmArgs* a) {
+  int64_t q = 0;
+  if (a->dtype != DP_BF16) return 0;
+  dp::tc_gemm(a, nullptr, &q);
+  return q;
+}
+
+int64_t dp_conv_fwd_workspace(const DpConvArgs* a) {
+  int64_t q = 0;
+  if (a->dtype == DP_BF16) dp::tc_conv_fwd(a, nullptr, &q);
+  return q;
+}
+
+int64_t dp_conv_dgrad_workspace(const DpConvArgs* a) {
+  int64_t q = 0;
+  if (a->dtype == DP_BF16) dp::tc_conv_dgrad(a, nullptr, &q);
+  return q;
 }
 
 const char* dp_last_error(void) { return dp::g_last_error.c_str(); }

@@ -77,11 +77,16 @@ DP_DEV Welford wf_merge(Welford a, Welford b) {
 
 // ------------------------------------------------------------------ GroupNorm
 // Grid (pixel chunks, N, channel blocks); a channel block covers whole groups, so one CTA
-// owns the statistics of its groups over its pixel chunk. Small feature maps (U-Net 8x8 /
+// owns the statistics of its groups over its pixel chunk. Small feature maps (U-Net 4x4 ..
 // 16x16 levels) get parallelism from channel blocks, large ones (VAE 256x256) from chunks.
-// Stats: per-channel shifted sums (shift = the chunk's first value of that channel) ->
-// (count, mean, M2) per group and chunk; chunks merged with Chan's formula (deterministic).
+// Every thread keeps a fixed 16-byte channel vector and strides over pixels (coalesced rows);
+// the CTA reduces per channel through shared memory (no atomics), then one warp per group
+// merges the channels with shuffles. Stats are shifted sums (shift = the chunk's first value
+// of each channel) -> (count, mean, M2) per (sample, chunk, group); the apply / backward
+// kernels merge the chunk partials of a group with one warp (lanes over chunks, shuffle
+// Chan merge), so no step of either kernel is a serial chain over chunks or channels.
 constexpr int GN_THREADS = 256;
+constexpr int GN_WARPS = GN_THREADS / 32;
 constexpr int GN_MAX_C = 2560;
 
 struct GnGeom {
@@ -90,10 +95,10 @@ struct GnGeom {
 
 template <int V>
 static GnGeom gn_geom(int N, int HW, int C, int G) {
+  // ~8 waves of CTAs (several resident per SM) with at least 64 pixels per chunk
+  int target = (8 * kNumSMs + N - 1) / N;
+  const int maxc = (HW + 63) / 64;
   GnGeom g{};
-  // ~16 waves of CTAs: small per-CTA pixel chunks keep the tail of the last wave short
-  int target = (16 * kNumSMs + N - 1) / N;
-  const int maxc = (HW + 127) / 128;
   g.chunks = target < maxc ? target : maxc;
   if (g.chunks < 1) g.chunks = 1;
   g.ppc = (HW + g.chunks - 1) / g.chunks;
@@ -117,6 +122,22 @@ struct GnLanes {
   }
 };
 
+// Sum the per-thread vectors red[rl][ch] over the pixel lanes: thread -> channel.
+DP_DEV void gn_lane_sum(const float* red, int rows_par, int nch, int c, float& s) {
+  s = 0.f;
+  for (int r = 0; r < rows_par; ++r) s += red[r * nch + c];
+}
+
+DP_DEV Welford wf_shfl_merge(Welford a) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Welford b{__shfl_xor_sync(0xffffffffu, a.n, o), __shfl_xor_sync(0xffffffffu, a.mean, o),
+              __shfl_xor_sync(0xffffffffu, a.m2, o)};
+    a = wf_merge(a, b);
+  }
+  return a;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(GN_THREADS)
     gn_partial_kernel(const T* __restrict__ x, int HW, int C, int G, int ppc, int CB,
@@ -127,70 +148,83 @@ __global__ void __launch_bounds__(GN_THREADS)
   const int CVB = CB / V;
   const int p0 = chunk * ppc;
   const int p1 = min(HW, p0 + ppc);
-  __shared__ float s1s[GN_MAX_C], s2s[GN_MAX_C];
-  __shared__ float shift[GN_MAX_C];
-  for (int c = threadIdx.x; c < CB; c += GN_THREADS) {
-    s1s[c] = 0.f;
-    s2s[c] = 0.f;
-    shift[c] = to_f(x[((int64_t)n * HW + p0) * C + c0 + c]);
-  }
-  __syncthreads();
+  const float cnt = static_cast<float>(p1 - p0);
+  __shared__ float r1[GN_THREADS * 8], r2[GN_THREADS * 8];
+  __shared__ float cmean[GN_MAX_C], cm2[GN_MAX_C];
   const T* xs = x + (int64_t)n * HW * C + c0;
   for (int cv0 = 0; cv0 < CVB; cv0 += GN_THREADS) {
     const GnLanes L(CVB, cv0);
-    if (L.rl >= L.rows_par) continue;
-    float k[V], a1[V], a2[V];
+    const int nch = L.width * V;
+    if (L.rl < L.rows_par) {
+      float k[V], a1[V], a2[V];
+      ld16(xs + (int64_t)p0 * C + L.cv * V, k);
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-      k[j] = shift[L.cv * V + j];
-      a1[j] = a2[j] = 0.f;
-    }
-    const T* xp = xs + (int64_t)(p0 + L.rl) * C + L.cv * V;
-    const int64_t step = (int64_t)L.rows_par * C;
-    int p = p0 + L.rl;
-    for (; p + 3 * L.rows_par < p1; p += 4 * L.rows_par, xp += 4 * step) {
-      float f[4][V];
+      for (int j = 0; j < V; ++j) a1[j] = a2[j] = 0.f;
+      const T* xp = xs + (int64_t)(p0 + L.rl) * C + L.cv * V;
+      const int64_t step = (int64_t)L.rows_par * C;
+      int p = p0 + L.rl;
+      for (; p + 3 * L.rows_par < p1; p += 4 * L.rows_par, xp += 4 * step) {
+        float f[4][V];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) ld16(xp + u * step, f[u]);
+        for (int u = 0; u < 4; ++u) ld16(xp + u * step, f[u]);
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            const float d = f[u][j] - k[j];
+            a1[j] += d;
+            a2[j] = fmaf(d, d, a2[j]);
+          }
+      }
+      for (; p < p1; p += L.rows_par, xp += step) {
+        float f[V];
+        ld16(xp, f);
 #pragma unroll
         for (int j = 0; j < V; ++j) {
-          const float d = f[u][j] - k[j];
+          const float d = f[j] - k[j];
           a1[j] += d;
           a2[j] = fmaf(d, d, a2[j]);
         }
-    }
-    for (; p < p1; p += L.rows_par, xp += step) {
-      float f[V];
-      ld16(xp, f);
+      }
+      const int o = L.rl * nch + (L.cv - cv0) * V;
 #pragma unroll
       for (int j = 0; j < V; ++j) {
-        const float d = f[j] - k[j];
-        a1[j] += d;
-        a2[j] = fmaf(d, d, a2[j]);
+        r1[o + j] = a1[j];
+        r2[o + j] = a2[j];
       }
     }
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      atomicAdd(&s1s[L.cv * V + j], a1[j]);
-      atomicAdd(&s2s[L.cv * V + j], a2[j]);
+    __syncthreads();
+    for (int c = threadIdx.x; c < nch; c += GN_THREADS) {
+      float s1, s2;
+      gn_lane_sum(r1, L.rows_par, nch, c, s1);
+      gn_lane_sum(r2, L.rows_par, nch, c, s2);
+      const float m = s1 / cnt;
+      const int cc = cv0 * V + c;
+      cmean[cc] = to_f(xs[(int64_t)p0 * C + cc]) + m;
+      cm2[cc] = fmaxf(s2 - s1 * m, 0.f);
     }
+    __syncthreads();
   }
-  __syncthreads();
+  // one warp per group: equal-count channels -> group (count, mean, M2)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cg = C / G;
   const int g0 = c0 / cg, gb = CB / cg;
-  const float cnt = static_cast<float>(p1 - p0);
-  for (int gi = threadIdx.x; gi < gb; gi += GN_THREADS) {
-    Welford a{0.f, 0.f, 0.f};
-    for (int c = gi * cg; c < (gi + 1) * cg; ++c) {
-      const float m = s1s[c] / cnt;
-      a = wf_merge(a, Welford{cnt, shift[c] + m, fmaxf(s2s[c] - s1s[c] * m, 0.f)});
+  for (int gi = warp; gi < gb; gi += GN_WARPS) {
+    float sm = 0.f;
+    for (int c = lane; c < cg; c += 32) sm += cmean[gi * cg + c];
+    const float mg = warp_sum(sm) / cg;
+    float s = 0.f;
+    for (int c = lane; c < cg; c += 32) {
+      const float d = cmean[gi * cg + c] - mg;
+      s += cm2[gi * cg + c] + cnt * d * d;
     }
-    float* o = part + (((int64_t)n * nchunks + chunk) * G + g0 + gi) * 3;
-    o[0] = a.n;
-    o[1] = a.mean;
-    o[2] = a.m2;
+    s = warp_sum(s);
+    if (lane == 0) {
+      float* o = part + (((int64_t)n * nchunks + chunk) * G + g0 + gi) * 3;
+      o[0] = cnt * cg;
+      o[1] = mg;
+      o[2] = s;
+    }
   }
 }
 
@@ -208,17 +242,21 @@ __global__ void __launch_bounds__(GN_THREADS, 4)
   const int g0 = c0 / cg, gb = CB / cg;
   __shared__ float s_mean[256], s_rstd[256];
   __shared__ float s_a[GN_MAX_C], s_b[GN_MAX_C];
-  for (int gi = threadIdx.x; gi < gb; gi += GN_THREADS) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int gi = warp; gi < gb; gi += GN_WARPS) {
     Welford a{0.f, 0.f, 0.f};
-    for (int k = 0; k < nchunks; ++k) {
+    for (int k = lane; k < nchunks; k += 32) {
       const float* q = part + (((int64_t)n * nchunks + k) * G + g0 + gi) * 3;
       a = wf_merge(a, Welford{q[0], q[1], q[2]});
     }
-    s_mean[gi] = a.mean;
-    s_rstd[gi] = rsqrtf(a.m2 / fmaxf(a.n, 1.f) + eps);
-    if (chunk == 0) {
-      mean_out[n * G + g0 + gi] = s_mean[gi];
-      rstd_out[n * G + g0 + gi] = s_rstd[gi];
+    a = wf_shfl_merge(a);
+    if (lane == 0) {
+      s_mean[gi] = a.mean;
+      s_rstd[gi] = rsqrtf(a.m2 / fmaxf(a.n, 1.f) + eps);
+      if (chunk == 0) {
+        mean_out[n * G + g0 + gi] = s_mean[gi];
+        rstd_out[n * G + g0 + gi] = s_rstd[gi];
+      }
     }
   }
   __syncthreads();
@@ -275,8 +313,9 @@ __global__ void __launch_bounds__(GN_THREADS, 4)
   }
 }
 
-// backward pass 1: per-channel sums of dy0 and dy0*xhat (dbeta, dgamma atomics) and per-group
-// partials A = sum gamma*dy0, B = sum gamma*dy0*xhat   (dy0 = dy through the optional SiLU)
+// backward pass 1: per-channel sums of dy0 and dy0*xhat (dbeta, dgamma: one atomic per channel
+// and CTA) and per-group partials A = sum gamma*dy0, B = sum gamma*dy0*xhat (dy0 = dy through
+// the optional SiLU)
 template <typename T>
 __global__ void __launch_bounds__(GN_THREADS)
     gn_bwd_partial_kernel(const T* __restrict__ x, const T* __restrict__ dy,
@@ -291,66 +330,81 @@ __global__ void __launch_bounds__(GN_THREADS)
   const int p0 = chunk * ppc;
   const int p1 = min(HW, p0 + ppc);
   const int cg = C / G;
+  __shared__ float r1[GN_THREADS * 8], r2[GN_THREADS * 8];
   __shared__ float s_a[GN_MAX_C], s_b[GN_MAX_C];
-  for (int c = threadIdx.x; c < CB; c += GN_THREADS) s_a[c] = s_b[c] = 0.f;
-  __syncthreads();
   const int64_t base = (int64_t)n * HW * C + c0;
   for (int cv0 = 0; cv0 < CVB; cv0 += GN_THREADS) {
     const GnLanes L(CVB, cv0);
-    if (L.rl >= L.rows_par) continue;
-    float sa[V], sb[V], mu[V], rs[V], ga[V], be[V];
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      const int c = c0 + L.cv * V + j;
-      mu[j] = mean[n * G + c / cg];
-      rs[j] = rstd[n * G + c / cg];
-      ga[j] = gamma ? gamma[c] : 1.f;
-      be[j] = gamma ? beta[c] : 0.f;
-      sa[j] = sb[j] = 0.f;
-    }
-    const int64_t step = (int64_t)L.rows_par * C;
-    int64_t off = base + (int64_t)(p0 + L.rl) * C + L.cv * V;
-#pragma unroll 4
-    for (int p = p0 + L.rl; p < p1; p += L.rows_par, off += step) {
-      float fx[V], fd[V];
-      ld16(x + off, fx);
-      ld16(dy + off, fd);
+    const int nch = L.width * V;
+    if (L.rl < L.rows_par) {
+      float sa[V], sb[V], mu[V], rs[V], ga[V], be[V];
 #pragma unroll
       for (int j = 0; j < V; ++j) {
-        const float xh = (fx[j] - mu[j]) * rs[j];
-        float d = fd[j];
-        if (silu_on) {
-          const float y0 = fmaf(xh, ga[j], be[j]);
-          const float s = __frcp_rn(1.f + __expf(-y0));
-          d *= s * (1.f + y0 * (1.f - s));
+        const int c = c0 + L.cv * V + j;
+        mu[j] = mean[n * G + c / cg];
+        rs[j] = rstd[n * G + c / cg];
+        ga[j] = gamma ? gamma[c] : 1.f;
+        be[j] = gamma ? beta[c] : 0.f;
+        sa[j] = sb[j] = 0.f;
+      }
+      const int64_t step = (int64_t)L.rows_par * C;
+      int64_t off = base + (int64_t)(p0 + L.rl) * C + L.cv * V;
+#pragma unroll 4
+      for (int p = p0 + L.rl; p < p1; p += L.rows_par, off += step) {
+        float fx[V], fd[V];
+        ld16(x + off, fx);
+        ld16(dy + off, fd);
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          const float xh = (fx[j] - mu[j]) * rs[j];
+          float d = fd[j];
+          if (silu_on) {
+            const float y0 = fmaf(xh, ga[j], be[j]);
+            const float s = __frcp_rn(1.f + __expf(-y0));
+            d *= s * (1.f + y0 * (1.f - s));
+          }
+          sa[j] += d;
+          sb[j] = fmaf(d, xh, sb[j]);
         }
-        sa[j] += d;
-        sb[j] = fmaf(d, xh, sb[j]);
+      }
+      const int o = L.rl * nch + (L.cv - cv0) * V;
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        r1[o + j] = sa[j];
+        r2[o + j] = sb[j];
       }
     }
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      atomicAdd(&s_a[L.cv * V + j], sa[j]);
-      atomicAdd(&s_b[L.cv * V + j], sb[j]);
+    __syncthreads();
+    for (int c = threadIdx.x; c < nch; c += GN_THREADS) {
+      float a, b;
+      gn_lane_sum(r1, L.rows_par, nch, c, a);
+      gn_lane_sum(r2, L.rows_par, nch, c, b);
+      const int cc = cv0 * V + c;
+      s_a[cc] = a;
+      s_b[cc] = b;
+      if (dgamma) {
+        atomicAdd(dgamma + c0 + cc, b);
+        atomicAdd(dbeta + c0 + cc, a);
+      }
     }
+    __syncthreads();
   }
-  __syncthreads();
-  if (dgamma)
-    for (int c = threadIdx.x; c < CB; c += GN_THREADS) {
-      atomicAdd(dgamma + c0 + c, s_b[c]);
-      atomicAdd(dbeta + c0 + c, s_a[c]);
-    }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g0 = c0 / cg, gb = CB / cg;
-  for (int gi = threadIdx.x; gi < gb; gi += GN_THREADS) {
+  for (int gi = warp; gi < gb; gi += GN_WARPS) {
     float A = 0.f, B = 0.f;
-    for (int c = gi * cg; c < (gi + 1) * cg; ++c) {
-      const float ga = gamma ? gamma[c0 + c] : 1.f;
-      A += ga * s_a[c];
-      B += ga * s_b[c];
+    for (int c = lane; c < cg; c += 32) {
+      const float ga = gamma ? gamma[c0 + gi * cg + c] : 1.f;
+      A += ga * s_a[gi * cg + c];
+      B += ga * s_b[gi * cg + c];
     }
-    float* o = part + (((int64_t)n * nchunks + chunk) * G + g0 + gi) * 2;
-    o[0] = A;
-    o[1] = B;
+    A = warp_sum(A);
+    B = warp_sum(B);
+    if (lane == 0) {
+      float* o = part + (((int64_t)n * nchunks + chunk) * G + g0 + gi) * 2;
+      o[0] = A;
+      o[1] = B;
+    }
   }
 }
 
@@ -368,15 +422,20 @@ __global__ void __launch_bounds__(GN_THREADS)
   const int g0 = c0 / cg, gb = CB / cg;
   __shared__ float s_A[256], s_B[256];
   const float inv_m = 1.f / (static_cast<float>(HW) * cg);
-  for (int gi = threadIdx.x; gi < gb; gi += GN_THREADS) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int gi = warp; gi < gb; gi += GN_WARPS) {
     float A = 0.f, B = 0.f;
-    for (int k = 0; k < nchunks; ++k) {
+    for (int k = lane; k < nchunks; k += 32) {
       const float* q = part + (((int64_t)n * nchunks + k) * G + g0 + gi) * 2;
       A += q[0];
       B += q[1];
     }
-    s_A[gi] = A * inv_m;
-    s_B[gi] = B * inv_m;
+    A = warp_sum(A);
+    B = warp_sum(B);
+    if (lane == 0) {
+      s_A[gi] = A * inv_m;
+      s_B[gi] = B * inv_m;
+    }
   }
   __syncthreads();
   const int CVB = CB / V;

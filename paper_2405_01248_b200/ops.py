@@ -68,12 +68,29 @@ def gemm(A, B, D, *, M, N, K, a_ld, b_ld, d_ld, a_mn=False, b_mn=False,
     args.r_bs1, args.r_bs2 = d_bs if r_bs is None else r_bs
     args.alpha = alpha
     args.split_k = split_k
+    ws = _splitk_ws(args, "dp_gemm_workspace", A.device)
     fam = "tcgen05_gemm" if A.dtype == torch.bfloat16 else "simt_gemm"
     flops = 2.0 * M * N * K * max(1, batch[0]) * max(1, batch[1])
-    telemetry.timed(fam, flops, lambda: check(_lib.lib().dp_gemm(ctypes.byref(args), _stream()), "dp_gemm"),
+    telemetry.timed(fam, flops, lambda: check(_lib.lib().dp_gemm(ctypes.byref(args), _stream()), "dp_gemm",
+                                              2 if ws is not None else 1),
                     sub=f"linear {M}x{N}x{K}{'a' if a_mn else ''}{'b' if b_mn else ''}x{batch[0] * batch[1]}"
                     if telemetry.SHAPES else "linear")
     return D
+
+
+def _splitk_ws(args, query, device):
+    """fp32 workspace that lets an under-filled bf16 launch split K over every SM (the C ABI
+    decides and sizes it; kernels never allocate). Returns the tensor (kept alive by the
+    caller until the launch is enqueued) or None."""
+    if args.dtype != DP_BF16:
+        return None
+    nbytes = getattr(_lib.lib(), query)(ctypes.byref(args))
+    if nbytes <= 0:
+        return None
+    ws = torch.empty(nbytes // 4, device=device, dtype=torch.float32)
+    args.workspace = ws.data_ptr()
+    args.workspace_bytes = nbytes
+    return ws
 
 
 def linear(x, w, bias=None, residual=None, out=None):
@@ -191,8 +208,10 @@ def conv2d(x, w, *, stride=1, pad=(1, 1), out_hw=None, bias=None, residual=None,
         xp, wp = _pad_last(x), _pad_last(w)
         Cp = xp.shape[-1]
         a = _conv_args(xp, wp, out, stride, pad, P, Q, bias, residual)
+        ws = _splitk_ws(a, "dp_conv_fwd_workspace", x.device)
         telemetry.timed("tcgen05_gemm", 2.0 * N * P * Q * K * R * S * C,
-                        lambda: check(_lib.lib().dp_conv_fwd(ctypes.byref(a), _stream()), "dp_conv_fwd"),
+                        lambda: check(_lib.lib().dp_conv_fwd(ctypes.byref(a), _stream()), "dp_conv_fwd",
+                                      2 if ws is not None else 1),
                         sub="conv_fwd")
         return out
     cols = im2col(x, R, S, stride, pad, P, Q)
@@ -238,8 +257,10 @@ def conv2d_dgrad(dy, w, x_shape, *, stride=1, pad=(1, 1)):
         dx = torch.empty(N, H, W, Cp, device=dy.device, dtype=dy.dtype)
         a = _conv_args(dx, wp, dx, 1, pad, src.shape[1], src.shape[2])
         a.x = _ptr(src)
+        ws = _splitk_ws(a, "dp_conv_dgrad_workspace", dy.device)
         telemetry.timed("tcgen05_gemm", 2.0 * N * H * W * C * R * S * K,
-                        lambda: check(_lib.lib().dp_conv_dgrad(ctypes.byref(a), _stream()), "dp_conv_dgrad"),
+                        lambda: check(_lib.lib().dp_conv_dgrad(ctypes.byref(a), _stream()), "dp_conv_dgrad",
+                                      2 if ws is not None else 1),
                         sub="conv_dgrad")
         return _take_last(dx, C)
     dcols = linear_dgrad(dy.reshape(-1, K), w.reshape(K, -1))

@@ -149,3 +149,47 @@ def test_conv_small_channels_fp32():
     w = torch.randn(32, 3, 3, 8, device="cuda")
     y = ops.conv2d(x, w, stride=1, pad=(1, 1))
     assert _rel(y, _conv_ref(x, w, 1, (1, 1), (16, 16))) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(32, 1280, 1280), (512, 1280, 11520), (200, 640, 2560)])
+def test_splitk_bf16_linear(M, N, K):
+    """Under-filled bf16 launches take the fp32 split-K / stream-K workspace path (the C ABI
+    asks for a workspace) and finish bias + residual in the reduction pass."""
+    ops = _ops()
+    from paper_2405_01248_b200 import _lib
+    import ctypes
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    x = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    w = torch.randn(N, K, device="cuda", generator=g).bfloat16()
+    b = torch.randn(N, device="cuda", generator=g)
+    r = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    a = _lib.DpGemmArgs()
+    a.M, a.N, a.K, a.batch1, a.batch2, a.dtype = M, N, K, 1, 1, _lib.DP_BF16
+    a.A, a.B, a.D = x.data_ptr(), w.data_ptr(), r.data_ptr()
+    a.a_ld = a.b_ld = K
+    a.d_ld = a.r_ld = N
+    a.d_dtype = _lib.DP_BF16
+    a.Res = r.data_ptr()
+    assert _lib.lib().dp_gemm_workspace(ctypes.byref(a)) == 4 * M * N
+    y = ops.linear(x, w, bias=b, residual=r)
+    ref = x.float() @ w.float().t() + b + r.float()
+    assert _rel(y, ref) < 1e-2
+
+
+@pytest.mark.parametrize("N,H,C,K", [(32, 4, 1280, 1280), (8, 8, 640, 1280)])
+def test_splitk_conv_fwd_dgrad(N, H, C, K):
+    ops = _ops()
+    g = torch.Generator(device="cuda").manual_seed(H * C)
+    x = torch.randn(N, H, H, C, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(K, 3, 3, C, device="cuda", generator=g) * 0.05).bfloat16()
+    b = torch.randn(K, device="cuda", generator=g)
+    r = torch.randn(N, H, H, K, device="cuda", generator=g).bfloat16()
+    y = ops.conv2d(x, w, bias=b, residual=r)
+    xr = x.float().permute(0, 3, 1, 2)
+    wr = w.float().permute(0, 3, 1, 2)
+    ref = F.conv2d(xr, wr, b, padding=1).permute(0, 2, 3, 1) + r.float()
+    assert _rel(y, ref) < 1e-2
+    dy = torch.randn(N, H, H, K, device="cuda", generator=g).bfloat16()
+    dx = ops.conv2d_dgrad(dy, w, x.shape)
+    ref_dx = torch.nn.grad.conv2d_input(xr.shape, wr, dy.float().permute(0, 3, 1, 2), padding=1)
+    assert _rel(dx, ref_dx.permute(0, 2, 3, 1)) < 1e-2
