@@ -235,6 +235,9 @@ int dp_group_norm_bwd(int dtype, const void* x, const void* dy, const float* gam
                       int accumulate, float* workspace, dp_stream_t stream);
 /* LayerNorm over rows of C (C <= 2048). Either per-channel affine gamma/beta (fp32) or per-sample
    adaLN modulation y = xhat*(1+mod[b][scale_off+c]) + mod[b][shift_off+c], b = row/rows_per_sample */
+/* T5-style RMSNorm forward (frozen encoders): y = x * rsqrt(mean(x^2) + eps) * gamma, rows of C */
+int dp_rms_norm_fwd(int dtype, const void* x, const float* gamma, void* y, int64_t rows, int C,
+                    float eps, dp_stream_t stream);
 int dp_layer_norm_fwd(int dtype, const void* x, const float* gamma, const float* beta,
                       const void* mod, int64_t mod_ld, int shift_off, int scale_off,
                       int rows_per_sample, void* y, float* mean, float* rstd, int64_t rows, int C,

@@ -216,3 +216,121 @@ def sd_unet(P, x, t, ctx, mc=320, mult=(1, 2, 4, 4), n_res=2, attn_levels=(0, 1,
                 h = conv(P, f"output_blocks.{oidx}.up", h)
             oidx += 1
     return conv(P, "out.conv", group_norm(P, "out.norm", h, eps=1e-5, silu=True))
+
+
+# ----------------------------------------------------------------------------- C3 / C4 / C5
+
+def sd_unet_encoder(P, x, t, ctx, mc=320, mult=(1, 2, 4, 4), n_res=2, attn_levels=(0, 1, 2)):
+    """Input blocks + middle block of sd_unet: returns (h, skips, temb)."""
+    temb = linear(P, "time_embed.2", F.silu(linear(P, "time_embed.0", timestep_embedding(t, mc))))
+    h = conv(P, "input_blocks.0", x)
+    skips = [h]
+    idx = 1
+    for lvl, m in enumerate(mult):
+        for r in range(n_res):
+            h = resblock(P, f"input_blocks.{idx}.res", h, temb, eps=1e-5)
+            if lvl in attn_levels:
+                h = spatial_transformer(P, f"input_blocks.{idx}.tr", h, ctx)
+            skips.append(h)
+            idx += 1
+        if lvl != len(mult) - 1:
+            h = conv(P, f"input_blocks.{idx}.down", h, stride=2)
+            skips.append(h)
+            idx += 1
+    h = resblock(P, "middle.res1", h, temb, eps=1e-5)
+    h = spatial_transformer(P, "middle.tr", h, ctx)
+    h = resblock(P, "middle.res2", h, temb, eps=1e-5)
+    return h, skips, temb
+
+
+def sd_unet_decoder(P, h, skips, temb, ctx, mult=(1, 2, 4, 4), n_res=2, attn_levels=(0, 1, 2)):
+    skips = list(skips)
+    oidx = 0
+    for lvl, m in list(enumerate(mult))[::-1]:
+        for r in range(n_res + 1):
+            h = torch.cat([h, skips.pop()], -1)
+            h = resblock(P, f"output_blocks.{oidx}.res", h, temb, eps=1e-5)
+            if lvl in attn_levels:
+                h = spatial_transformer(P, f"output_blocks.{oidx}.tr", h, ctx)
+            if lvl != 0 and r == n_res:
+                B, H, W, C = h.shape
+                h = h[:, :, None, :, None, :].expand(B, H, 2, W, 2, C).reshape(B, 2 * H, 2 * W, C)
+                h = conv(P, f"output_blocks.{oidx}.up", h)
+            oidx += 1
+    return conv(P, "out.conv", group_norm(P, "out.norm", h, eps=1e-5, silu=True))
+
+
+HINT = ((3, 16, 1), (16, 16, 1), (16, 32, 2), (32, 32, 1), (32, 96, 2), (96, 96, 1), (96, 256, 2))
+
+
+def controlnet(Pc, Pl, x, hint, t, ctx, locked_h, locked_skips, locked_temb, mc=320, mult=(1, 2, 4, 4),
+               n_res=2, attn_levels=(0, 1, 2)):
+    """ControlNet v1.0 branch (params Pc) + locked SD decoder (params Pl) consuming the locked
+    encoder outputs (h, skips, temb) plus the zero-conv residuals."""
+    temb = linear(Pc, "time_embed.2", F.silu(linear(Pc, "time_embed.0", timestep_embedding(t, mc))))
+    g = hint
+    for j, (_, _, s) in enumerate(HINT):
+        g = F.silu(conv(Pc, f"input_hint_block.{2 * j}", g, stride=s, pad=1))
+    g = conv(Pc, f"input_hint_block.{2 * len(HINT)}", g)
+    h = conv(Pc, "input_blocks.0", x) + g
+    res = [conv(Pc, "zero_convs.0", h, pad=0)]
+    idx = 1
+    for lvl, m in enumerate(mult):
+        for r in range(n_res):
+            h = resblock(Pc, f"input_blocks.{idx}.res", h, temb, eps=1e-5)
+            if lvl in attn_levels:
+                h = spatial_transformer(Pc, f"input_blocks.{idx}.tr", h, ctx)
+            res.append(conv(Pc, f"zero_convs.{idx}", h, pad=0))
+            idx += 1
+        if lvl != len(mult) - 1:
+            h = conv(Pc, f"input_blocks.{idx}.down", h, stride=2)
+            res.append(conv(Pc, f"zero_convs.{idx}", h, pad=0))
+            idx += 1
+    h = resblock(Pc, "middle.res1", h, temb, eps=1e-5)
+    h = spatial_transformer(Pc, "middle.tr", h, ctx)
+    h = resblock(Pc, "middle.res2", h, temb, eps=1e-5)
+    mid = conv(Pc, "middle_block_out", h, pad=0)
+    skips = [a + b for a, b in zip(locked_skips, res)]
+    return sd_unet_decoder(Pl, locked_h + mid, skips, locked_temb, ctx, mult, n_res, attn_levels)
+
+
+def t5_buckets(L, num_buckets=32, max_distance=128):
+    """T5 bidirectional relative-position bucket of (query i, key j) (HF T5Attention._relative_position_bucket)."""
+    rel = torch.arange(L)[None, :] - torch.arange(L)[:, None]
+    nb = num_buckets // 2
+    ret = (rel > 0).long() * nb
+    n = rel.abs()
+    max_exact = nb // 2
+    large = max_exact + (torch.log(n.float().clamp(min=1) / max_exact) / math.log(max_distance / max_exact)
+                         * (nb - max_exact)).long()
+    large = large.clamp(max=nb - 1)
+    return ret + torch.where(n < max_exact, n, large)
+
+
+def rms_norm(x, g, eps=1e-6):
+    return x * torch.rsqrt((x * x).mean(-1, keepdim=True) + eps) * g
+
+
+def t5_encoder(P, ids, heads=16, layers=24):
+    h = P["shared"][ids]
+    B, L, D = h.shape
+    hd = D // heads
+    bias = P["rel_bias"][t5_buckets(L)].permute(2, 0, 1)[None]  # [1, H, L, L]
+    for i in range(layers):
+        p = f"block.{i}"
+        qkv = rms_norm(h, P[f"{p}.ln1.weight"]) @ P[f"{p}.attn.qkv.weight"].t()
+        q, k, v = [a.reshape(B, L, heads, hd).transpose(1, 2) for a in qkv.split(D, -1)]
+        s = q @ k.transpose(-1, -2) + bias          # T5: no 1/sqrt(d) scaling
+        o = (torch.softmax(s, -1) @ v).transpose(1, 2).reshape(B, L, D)
+        h = o @ P[f"{p}.attn.o.weight"].t() + h
+        a, gt = (rms_norm(h, P[f"{p}.ln2.weight"]) @ P[f"{p}.ff.wi.weight"].t()).chunk(2, -1)
+        h = (a * F.gelu(gt)) @ P[f"{p}.ff.wo.weight"].t() + h
+    return rms_norm(h, P["final_ln.weight"])
+
+
+def image_pyramid(img, f=4):
+    """(img_sr, base x0 = f x f average pool, nearest f x upsample of it)."""
+    B, H, W, C = img.shape
+    lo = img.reshape(B, H // f, f, W // f, f, C).mean((2, 4))
+    up = lo[:, :, None, :, None, :].expand(B, H // f, f, W // f, f, C).reshape(B, H, W, C)
+    return img, lo, up

@@ -78,3 +78,85 @@ def train(config, params, batches, sab, s1m, adamw=dict(lr=1e-4, betas=(0.9, 0.9
         grads.append({n: v.grad.detach().clone() for n, v in P[bb].items()})
         opt.step()
     return losses, grads, {n: v.detach().clone() for n, v in P[bb].items()}
+
+
+def _q(x0, noise, t, sab, s1m):
+    return sab[t][:, None, None, None] * x0 + s1m[t][:, None, None, None] * noise
+
+
+def c3_forward(P, batch, sab, s1m, clip_layers=23):
+    """ControlNet v1.0 (SURVEY Appendix B.2): frozen VAE / text / hint / locked U-Net encoder;
+    the loss trains the ControlNet branch through the locked decoder."""
+    img = batch.images.float()
+    img = torch.cat([img, torch.zeros(*img.shape[:-1], 5)], -1)
+    x0 = nets.vae_encoder(P["vae"], img, ch=128, mult=(1, 2, 4, 4), n_res=2)
+    ctx, _ = nets.text_encoder(P["text"], batch.ids, heads=16, layers=clip_layers)
+    noise = batch.noise.float()
+    xt = _q(x0, noise, batch.t, sab, s1m)
+    with torch.no_grad():
+        lh, lskips, ltemb = nets.sd_unet_encoder(P["unet_locked"], xt, batch.t, ctx)
+    hint = batch.extra["hint"].float()
+    eps = nets.controlnet(P["controlnet"], P["unet_locked"], xt, hint, batch.t, ctx, lh, lskips, ltemb)
+    loss = ((eps - noise) ** 2).mean()
+    return loss, eps, dict(latent=x0, ctx=ctx)
+
+
+CDM_BASE = dict(mc=192, mult=(1, 2, 3, 4), attn_levels=(1, 2, 3))
+CDM_SR = dict(mc=128, mult=(1, 2, 4, 4), attn_levels=(3,))
+
+
+def c4_forward(P, batch, sab, s1m, t5_layers=24, factor=4):
+    """Cascaded model: base (64 px) and super-resolution (256 px, conditioned on the upsampled
+    low-res image) U-Nets trained independently on shared frozen outputs (PAPER.md:128-130);
+    self-conditioning on both pipes when the iteration's coin is set; loss = sum of the two
+    pipes' mean squared errors. Returns the summed loss (both backbones' params get grads)."""
+    img = batch.images.float()
+    img_sr, lo, up = nets.image_pyramid(img, factor)
+    ctx = nets.t5_encoder(P["t5"], batch.ids, layers=t5_layers)
+    t = batch.t
+    a = sab[t][:, None, None, None]
+    b = s1m[t][:, None, None, None]
+    total = 0.0
+    outs = []
+    for name, x0, noise, cond, kw in (("unet_base", lo, batch.noise.float(), None, CDM_BASE),
+                                      ("unet_sr", img_sr, batch.extra["noise_sr"].float(), up, CDM_SR)):
+        xt = a * x0 + b * noise
+        inp = xt if cond is None else torch.cat([xt, cond], -1)
+        if batch.selfcond:
+            with torch.no_grad():
+                eps_sc = nets.sd_unet(P[name], torch.cat([inp, torch.zeros_like(xt)], -1), t, ctx, **kw)
+                x0_sc = (xt - b * eps_sc) / a
+        else:
+            x0_sc = torch.zeros_like(xt)
+        eps = nets.sd_unet(P[name], torch.cat([inp, x0_sc], -1), t, ctx, **kw)
+        total = total + ((eps - noise) ** 2).mean()
+        outs.append(eps)
+    return total, outs, dict(latent=lo, ctx=ctx)
+
+
+def c5_forward(P, batch, sab, s1m, clip_layers=23):
+    """Scaled-up SD U-Net (model channels 512): same training step as c2."""
+    img = batch.images.float()
+    img = torch.cat([img, torch.zeros(*img.shape[:-1], 5)], -1)
+    x0 = nets.vae_encoder(P["vae"], img, ch=128, mult=(1, 2, 4, 4), n_res=2)
+    ctx, _ = nets.text_encoder(P["text"], batch.ids, heads=16, layers=clip_layers)
+    noise = batch.noise.float()
+    xt = _q(x0, noise, batch.t, sab, s1m)
+    eps = nets.sd_unet(P["unet"], xt, batch.t, ctx, mc=512)
+    loss = ((eps - noise) ** 2).mean()
+    return loss, eps, dict(latent=x0, ctx=ctx)
+
+
+FORWARDS.update({"c3": ("controlnet", c3_forward), "c5": ("unet", c5_forward)})
+
+
+def grads_of(config, params, batch, sab, s1m, trainable, **kw):
+    """Loss and gradients of one iteration (no optimizer state: for the big configs)."""
+    fwd = {"c2": c2_forward, "c3": c3_forward, "c4": c4_forward, "c5": c5_forward}[config]
+    P = {k: {n: v.detach().clone().float() for n, v in d.items()} for k, d in params.items()}
+    for name in trainable:
+        for v in P[name].values():
+            v.requires_grad_(True)
+    loss, _, _ = fwd(P, batch, sab, s1m, **kw)
+    loss.backward()
+    return loss.item(), {name: {n: v.grad.detach().clone() for n, v in P[name].items()} for name in trainable}

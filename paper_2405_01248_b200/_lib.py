@@ -122,6 +122,7 @@ _SIGNATURES = {
     "dp_layer_norm_bwd": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_int, c_int,
                           c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i64,
                           c_int, c_int, c_void_p],
+    "dp_rms_norm_fwd": [c_int, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_float, c_void_p],
     "dp_softmax_fwd": [c_int, c_void_p, c_void_p, c_i64, c_int, c_int, c_float, c_int, c_int, c_void_p],
     "dp_softmax_bwd": [c_int, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_int, c_float, c_void_p],
     "dp_last_error": [],

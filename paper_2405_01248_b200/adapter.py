@@ -219,6 +219,16 @@ def build_group_program(result, frozen_layer_counts, selfcond=None, frozen_deps=
                 items.append((f.bubble.start, 0, ("fill", bi)))
         items.sort(key=lambda x: (x[0], x[1]))
         instrs = [it[2] for it in items]
+        if sc and len(pipes) > 1 and not any(t.kind == "fwd_sc" for t in compute[dev]):
+            # The reference's bidirectional simulator has no self-conditioning pass
+            # (planner.py:115-118, scheduler.py:346-347). Run it outside the plan (SURVEY
+            # Appendix B.1): every pipe's no-grad forward of all micro-batches, pipe by pipe in
+            # flow order, before the planned tasks; feedback reaches stage 0 before its fwd.
+            pre = []
+            for pi, st in enumerate(prog.stages):
+                if st is not None:
+                    pre += [("fwd_sc", m, st, pi) for m in range(M)]
+            instrs = pre + instrs
         for pi, st in enumerate(prog.stages):
             if st is not None:
                 last_bwd = max(i for i, ins in enumerate(instrs)

@@ -104,6 +104,9 @@ static GnGeom gn_geom(int N, int HW, int C, int G) {
   g.ppc = (HW + g.chunks - 1) / g.chunks;
   g.chunks = (HW + g.ppc - 1) / g.ppc;
   g.nblk = 1;
+  // wide layers (e.g. 4096 concat channels of a 2B U-Net decoder) are split into channel blocks
+  // of whole groups so that a block's per-channel shared arrays fit (GN_MAX_C)
+  while (C / g.nblk > GN_MAX_C && g.nblk * 2 <= G && G % (g.nblk * 2) == 0) g.nblk *= 2;
   while ((long long)g.chunks * N * g.nblk < 2 * kNumSMs && g.nblk * 2 <= G && G % (g.nblk * 2) == 0 &&
          (C / (g.nblk * 2)) % V == 0)
     g.nblk *= 2;
@@ -486,6 +489,46 @@ __global__ void __launch_bounds__(GN_THREADS)
 // one warp per row; per-lane strided elements (coalesced across the warp)
 // one warp per row; lane owns 16-byte vectors lane, lane+32, ... (NVEC per lane) -> fully
 // coalesced 512-byte warp accesses, the row kept in registers for the two-pass statistics
+// RMSNorm (T5 layer norm: no mean subtraction, no bias): y = x * rsqrt(mean(x^2) + eps) * gamma.
+// Forward only (the T5 text encoder is frozen); one warp per row like ln_fwd.
+template <typename T, int NVEC>
+__global__ void __launch_bounds__(256)
+    rms_fwd_kernel(const T* __restrict__ x, const float* __restrict__ gamma, T* __restrict__ y,
+                   int64_t rows, int C, float eps) {
+  constexpr int V = NV<T>::V;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = blockIdx.x * 8LL + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int CV = C / V;
+  const T* xr = x + row * C;
+  float v[NVEC][V];
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < NVEC; ++k) {
+    const int cv = lane + 32 * k;
+    if (cv < CV) {
+      ld16(xr + cv * V, v[k]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < V; ++j) v[k][j] = 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) q = fmaf(v[k][j], v[k][j], q);
+  }
+  const float rs = rsqrtf(warp_sum(q) / C + eps);
+  T* yr = y + row * C;
+#pragma unroll
+  for (int k = 0; k < NVEC; ++k) {
+    const int cv = lane + 32 * k;
+    if (cv < CV) {
+      float o[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) o[j] = v[k][j] * rs * __ldg(gamma + cv * V + j);
+      st16(yr + cv * V, o);
+    }
+  }
+}
+
 template <typename T, int NVEC>
 __global__ void __launch_bounds__(256)
     ln_fwd_kernel(const T* __restrict__ x, const float* __restrict__ gamma,
@@ -717,8 +760,14 @@ static T* mp(void* p) {
 
 static int gn_validate(int dtype, int C, int G) {
   const int V = dtype == DP_F32 ? 4 : 8;
-  if (G <= 0 || C % G || C % V || C > GN_MAX_C || G > 256) {
-    set_error("group_norm: need C % G == 0, C % 8 == 0 (bf16) / 4 (fp32), C <= 2560, G <= 256");
+  if (G <= 0 || C % G || C % V || G > 256) {
+    set_error("group_norm: need C % G == 0, C % 8 == 0 (bf16) / 4 (fp32), G <= 256");
+    return DP_ERR_ARGS;
+  }
+  int nb = 1;
+  while (C / nb > GN_MAX_C && nb * 2 <= G && G % (nb * 2) == 0) nb *= 2;
+  if (C / nb > GN_MAX_C || (C / nb) % V) {
+    set_error("group_norm: channels per group block exceed 2560");
     return DP_ERR_ARGS;
   }
   return 0;
@@ -800,6 +849,19 @@ int dp_layer_norm_fwd(int dtype, const void* x, const float* gamma, const float*
                                     shift_off, scale_off, rows_per_sample > 0 ? rows_per_sample : 1,
                                     mp<T>(y), mean, rstd, rows, C, eps));
   return ew_check("layer_norm_fwd");
+}
+
+int dp_rms_norm_fwd(int dtype, const void* x, const float* gamma, void* y, int64_t rows, int C,
+                    float eps, dp_stream_t stream) {
+  if (rows <= 0) return 0;
+  const int V = dtype == DP_F32 ? 4 : 8;
+  if (C % V || C > 32 * 8 * V) {
+    set_error("rms_norm: need C % 8 == 0 (bf16) / 4 (fp32) and C <= 256 vectors");
+    return DP_ERR_ARGS;
+  }
+  dim3 grid(static_cast<unsigned>((rows + 7) / 8));
+  DISPATCH_T(dtype, LN_PER_DISPATCH(C, rms_fwd_kernel, cp<T>(x), gamma, mp<T>(y), rows, C, eps));
+  return ew_check("rms_norm_fwd");
 }
 
 int dp_layer_norm_bwd(int dtype, const void* x, const void* dy, const float* gamma,

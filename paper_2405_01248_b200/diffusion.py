@@ -14,6 +14,7 @@ from dataclasses import dataclass
 import torch
 
 STREAM_IMAGES, STREAM_IDS, STREAM_T, STREAM_NOISE, STREAM_COIN = range(5)
+STREAM_EXTRA0 = 5  # extra fields (ControlNet hint, second-pipe noise) use streams 5, 6, ...
 
 
 def noise_schedule(T=1000, beta_start=0.00085, beta_end=0.012):
@@ -36,9 +37,14 @@ class Batch:
     t: torch.Tensor        # [WB] int64 in [0, T)
     noise: torch.Tensor    # [WB, h, w, zc] ~ N(0, 1)
     selfcond: bool         # per-iteration coin shared by all ranks
+    extra: dict = None     # config-specific fields: "hint" (ControlNet), "noise_sr" (cascaded SR pipe)
 
     def slice(self, lo, hi):
-        return Batch(self.images[lo:hi], self.ids[lo:hi], self.t[lo:hi], self.noise[lo:hi], self.selfcond)
+        return Batch(self.images[lo:hi], self.ids[lo:hi], self.t[lo:hi], self.noise[lo:hi], self.selfcond,
+                     {k: v[lo:hi] for k, v in (self.extra or {}).items()})
+
+    def fields(self):
+        return dict(images=self.images, ids=self.ids, t=self.t, noise=self.noise, **(self.extra or {}))
 
 
 @dataclass(frozen=True)
@@ -52,6 +58,9 @@ class DataSpec:
     vocab: int = 1000
     T: int = 1000
     selfcond_p: float = 0.0
+    # extra per-sample fields: (name, kind, H, C) with kind "bernoulli" (ControlNet hint ~ B(0.1),
+    # SURVEY.md §8d) or "noise" (N(0,1), e.g. the super-resolution pipe of a cascaded model)
+    extra: tuple = ()
 
 
 def make_batch(spec: DataSpec, iteration: int) -> Batch:
@@ -67,4 +76,13 @@ def make_batch(spec: DataSpec, iteration: int) -> Batch:
     noise = torch.randn(WB, spec.latent, spec.latent, spec.zc, generator=g)
     g = _gen(spec.config_id, iteration, STREAM_COIN)
     coin = bool(torch.rand(1, generator=g).item() < spec.selfcond_p)
-    return Batch(images, ids, t, noise, coin)
+    extra = {}
+    for i, (name, kind, H, C) in enumerate(spec.extra):
+        g = _gen(spec.config_id, iteration, STREAM_EXTRA0 + i)
+        if kind == "bernoulli":
+            extra[name] = (torch.rand(WB, H, H, C, generator=g) < 0.1).float()
+        elif kind == "noise":
+            extra[name] = torch.randn(WB, H, H, C, generator=g)
+        else:
+            raise ValueError(kind)
+    return Batch(images, ids, t, noise, coin, extra)

@@ -9,6 +9,14 @@ Configurations (BASELINE.json configs):
   c1  tiny DiT (4 blocks, d=256) + tiny VAE encoder + tiny text encoder, 128 px, fp32,
       self-conditioning p=0.5
   c2  SD v2.1 U-Net + OpenCLIP ViT-H text (23 layers) + SD VAE encoder, 256 px, bf16
+  c3  ControlNet v1.0: trainable ControlNet branch -> locked SD v2.1 decoder (one backbone
+      chain); frozen VAE, OpenCLIP-H text, hint map and the LOCKED U-Net encoder (frozen
+      dependencies vae->enc, text->enc), 512 px, bf16
+  c4  cascaded two-backbone model (CDM): 64 px base U-Net + 256 px super-resolution U-Net
+      (bidirectional pipelines), frozen T5-large-shaped encoder (128 tokens) and image pyramid,
+      self-conditioning p=0.5 on both pipes, pixel space, bf16
+  c5  scaled-up SD U-Net (model channels 512 -> 2.2B parameters) + OpenCLIP-H + SD VAE, 256 px
+  *-small  reduced resolution / encoder depth variants of c3..c5 for the parity tests
 """
 
 from __future__ import annotations
@@ -21,8 +29,8 @@ import torch
 from . import ops as kops
 from .adapter import build_group_program
 from .diffusion import DataSpec, make_batch, noise_schedule
-from .networks import (CLIPTextEncoder, SDUNet, SDVAEEncoder, TinyDiT, TinyTextEncoder,
-                       TinyVAEEncoder)
+from .networks import (CLIPTextEncoder, ControlNet, HintImage, ImagePyramid, LockedUNetEncoder, SDUNet,
+                       SDVAEEncoder, T5Encoder, TinyDiT, TinyTextEncoder, TinyVAEEncoder)
 from .nn import grad_anchor
 from .pipefill import filler, planner, profile as pprof, scheduler
 from .profiler import probe_specs, synthetic_profile
@@ -39,12 +47,30 @@ class ConfigSpec:
     vocab: int
     selfcond_p: float
     config_id: int
+    zc: int = 4
+    extra: tuple = ()   # extra batch fields (diffusion.DataSpec.extra)
+    family: str = ""    # model family (defaults to name)
+    depth: int = 0      # text-encoder depth override (small variants)
 
 
+_C = torch.bfloat16
 CONFIGS = {
     "c1": ConfigSpec("c1", torch.float32, 128, 32, 16, 1000, 0.5, 1),
-    "c2": ConfigSpec("c2", torch.bfloat16, 256, 32, 77, 49408, 0.0, 2),
+    "c2": ConfigSpec("c2", _C, 256, 32, 77, 49408, 0.0, 2),
+    "c3": ConfigSpec("c3", _C, 512, 64, 77, 49408, 0.0, 3, extra=(("hint", "bernoulli", 512, 3),)),
+    "c4": ConfigSpec("c4", _C, 256, 64, 128, 32128, 0.5, 4, zc=3, extra=(("noise_sr", "noise", 256, 3),)),
+    "c5": ConfigSpec("c5", _C, 256, 32, 77, 49408, 0.0, 5),
+    "c3-small": ConfigSpec("c3-small", _C, 128, 16, 77, 49408, 0.0, 3, extra=(("hint", "bernoulli", 128, 3),),
+                           family="c3", depth=2),
+    "c4-small": ConfigSpec("c4-small", _C, 64, 16, 16, 32128, 0.5, 4, zc=3,
+                           extra=(("noise_sr", "noise", 64, 3),), family="c4", depth=2),
+    "c5-small": ConfigSpec("c5-small", _C, 128, 16, 77, 49408, 0.0, 5, family="c5", depth=2),
 }
+
+# model-size parameters of the cascaded configuration (c4): pixel-space U-Nets
+CDM_BASE = dict(mc=192, mult=(1, 2, 3, 4), attn_levels=(1, 2, 3))
+CDM_SR = dict(mc=128, mult=(1, 2, 4, 4), attn_levels=(3,))
+C5_MC = 512
 
 
 def _attach_grad_context(comp, device):
@@ -57,6 +83,9 @@ def build_model(cfg: str | ConfigSpec, device="cuda", seed=0, states=None, small
     `states` optionally maps component name -> parameter dict (e.g. for parity tests)."""
     c = CONFIGS[cfg] if isinstance(cfg, str) else cfg
     states = states or {}
+    fam = c.family or c.name
+    if fam in ("c3", "c4", "c5"):
+        return _build_ext(c, fam, device, seed, states)
     if c.name == "c1":
         bb = TinyDiT(c.dtype, img=c.latent, cin=8, cout=4)
         vae = TinyVAEEncoder(c.dtype)
@@ -81,6 +110,52 @@ def build_model(cfg: str | ConfigSpec, device="cuda", seed=0, states=None, small
     return model
 
 
+def _finish(model, c, device, comps, seed, states):
+    for comp in comps:
+        comp.materialize(device, seed, states.get(comp.name))
+    for bb in model.backbones:
+        _attach_grad_context(bb, device)
+    model.cfg = c
+    model.selfcond_p = c.selfcond_p
+    return model
+
+
+def _build_ext(c, fam, device, seed, states):
+    """c3 (ControlNet), c4 (cascaded two-backbone), c5 (2.2B U-Net)."""
+    sab, s1m = noise_schedule()
+    sab, s1m = sab.to(device), s1m.to(device)
+    adam = dict(lr=1e-4, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01)
+    depth = c.depth or 23
+    if fam == "c5":
+        bb = SDUNet(c.dtype, mc=C5_MC)
+        vae, txt = SDVAEEncoder(c.dtype), CLIPTextEncoder(c.dtype, layers=depth)
+        model = TrainModel(bb, [FrozenSpec(vae, ("images",)), FrozenSpec(txt, ("ids",))], kops, sab, s1m,
+                           adamw=adam)
+        return _finish(model, c, device, (bb, vae, txt), seed, states)
+    if fam == "c3":
+        locked = SDUNet(c.dtype, trainable=False, name="unet_locked")
+        enc = LockedUNetEncoder(locked)
+        enc.sqrt_ab, enc.sqrt_1mab = sab, s1m
+        bb = ControlNet(locked, c.dtype)
+        vae, txt, hint = SDVAEEncoder(c.dtype), CLIPTextEncoder(c.dtype, layers=depth), HintImage(c.dtype)
+        frozen = [FrozenSpec(vae, ("images",)), FrozenSpec(txt, ("ids",)), FrozenSpec(hint, ("hint",)),
+                  FrozenSpec(enc, ("t", "noise"))]
+        model = TrainModel(bb, frozen, kops, sab, s1m, adamw=adam)
+        model.frozen_deps = ((0, 3), (1, 3))
+        return _finish(model, c, device, (bb, vae, txt, hint, enc), seed, states)
+    # c4: cascaded diffusion, two backbones sharing the frozen outputs (PAPER.md:128-130)
+    sc = 3 if c.selfcond_p > 0 else 0
+    base = SDUNet(c.dtype, cin=3 + sc, cout=3, name="unet_base", **CDM_BASE)
+    sr = SDUNet(c.dtype, cin=6 + sc, cout=3, name="unet_sr", **CDM_SR)
+    t5 = T5Encoder(c.dtype, vocab=c.vocab, L=c.text_len, layers=c.depth or 24)
+    pyr = ImagePyramid(c.dtype, factor=c.image // c.latent)
+    io = [dict(latent="latent", noise="noise", cond=None, drop=("img_sr", "lowres")),
+          dict(latent="img_sr", noise="noise_sr", cond="lowres", drop=("latent",))]
+    model = TrainModel(base, [FrozenSpec(pyr, ("images",)), FrozenSpec(t5, ("ids",))], kops, sab, s1m,
+                       selfcond_channels=sc, adamw=adam, backbones=[base, sr], pipe_io=io)
+    return _finish(model, c, device, (base, sr, pyr, t5), seed, states)
+
+
 class InputFeed:
     """Batch fields for one iteration. mode 'device': the whole world batch is resident on
     the device (bench `value`); mode 'host': slices are copied from pinned host memory
@@ -94,7 +169,7 @@ class InputFeed:
         self.dtype = dtype
         self.mode = mode
         self.h2d_bytes = 0
-        fields = dict(images=batch.images, ids=batch.ids, t=batch.t, noise=batch.noise)
+        fields = batch.fields()
         if mode == "device":
             self.f = {k: self._cast(k, v.to(self.device, non_blocking=True)) for k, v in fields.items()}
         else:
@@ -102,7 +177,7 @@ class InputFeed:
         self.selfcond = batch.selfcond
 
     def _cast(self, k, v):
-        if k in ("images", "noise") and v.dtype != self.dtype:
+        if v.is_floating_point() and k != "t" and v.dtype != self.dtype:
             return v.to(self.dtype)
         return v
 
@@ -132,7 +207,12 @@ def plan_programs(prof, world, S, M, D, world_batch, frozen_counts, bubble_min_l
     group_batch = plan.config.global_batch
     deps = tuple(prof.frozen_dep_indices())
     programs = {}
-    if res["mode"] == planner.MODE_SELFCOND:
+    if res["mode"] == planner.MODE_BIDIRECTIONAL and prof.selfcond_prob > 0:
+        # two backbones with self-conditioning: the planner's bidirectional schedule has no
+        # fwd_sc tasks; the adapter runs the pass ahead of the planned tasks (outside the plan)
+        programs[True] = build_group_program(res, frozen_counts, selfcond=True, frozen_deps=deps)
+        programs[False] = build_group_program(res, frozen_counts, selfcond=False, frozen_deps=deps)
+    elif res["mode"] == planner.MODE_SELFCOND:
         programs[True] = build_group_program(res, frozen_counts, selfcond=True, frozen_deps=deps)
         pre = scheduler.build_schedule(plan, prof, cluster, selfcond=False)
         fill = filler.fill_all(scheduler.extract_bubbles(pre, bubble_min_len), prof, group_batch, pre)
@@ -168,8 +248,8 @@ class Trainer:
         device = device or (f"cuda:{torch.cuda.current_device()}" if torch.cuda.is_available() else "cpu")
         model = build_model(c, device, seed, states, small=small)
         world_batch = world_batch or 8 * world
-        ds = DataSpec(c.config_id, world_batch, c.image, c.latent, 4, c.text_len, c.vocab, 1000,
-                      c.selfcond_p)
+        ds = DataSpec(c.config_id, world_batch, c.image, c.latent, c.zc, c.text_len, c.vocab, 1000,
+                      c.selfcond_p, extra=c.extra)
         return cls.from_model(model, c, ds, world=world, rank=rank, S=S, M=M, D=D, device=device,
                               profile=profile, filled=filled, feed_mode=feed_mode,
                               bubble_min_len=bubble_min_len)
@@ -189,9 +269,11 @@ class Trainer:
                                                       bubble_min_len, comm)
         if not filled:
             programs = {False: unfilled, True: unfilled}
-        elems = ds.latent * ds.latent * ds.zc
+        # per pipe: mean squared error over that pipe's noise tensor (two-backbone models sum them)
+        scales = [1.0 / (world_batch * pfeed.get(model.noise_field(p), 0, 1).numel())
+                  for p in range(len(model.backbones))]
         ex = PipelineExecutor(model, programs, rank=rank, world=world, device=device, live_specs=live,
-                              frozen_specs=fspecs, loss_scale=1.0 / (world_batch * elems))
+                              frozen_specs=fspecs, loss_scale=scales if len(scales) > 1 else scales[0])
         ex.warm_program = warm
         ex.plan_result = res
         t = cls(model, cfg, ex, ds, device, feed_mode)

@@ -377,9 +377,12 @@ class SDUNet(Component):
     name = "unet"
 
     def __init__(self, dtype=torch.bfloat16, cin=4, cout=4, mc=320, mult=(1, 2, 4, 4), n_res=2,
-                 attn_levels=(0, 1, 2), ctx_dim=1024, head_dim=64):
-        super().__init__(dtype, trainable=True)
+                 attn_levels=(0, 1, 2), ctx_dim=1024, head_dim=64, trainable=True, name=None):
+        super().__init__(dtype, trainable=trainable)
+        if name:
+            self.name = name
         s = self.store
+        self.in_mods, self.out_mods = [], []  # per layer: the modules (reused by ControlNet)
         self.mc = mc
         ted = 4 * mc
         self.ted = ted
@@ -397,11 +400,13 @@ class SDUNet(Component):
                 tr = SpatialTransformer(s, f"input_blocks.{idx}.tr", ch, ctx_dim, head_dim) \
                     if lvl in attn_levels else None
                 self.add_layer(f"in.{idx}", self._in_block(res, tr, idx), (f"input_blocks.{idx}",))
+                self.in_mods.append(("res", res, tr))
                 chans.append(ch)
                 idx += 1
             if lvl != len(mult) - 1:
                 ds = nn.Conv2d(s, f"input_blocks.{idx}.down", ch, ch, 3, stride=2)
                 self.add_layer(f"in.{idx}", self._down(ds, idx), (f"input_blocks.{idx}",))
+                self.in_mods.append(("down", ds, None))
                 chans.append(ch)
                 idx += 1
         self.n_skips = idx
@@ -409,6 +414,8 @@ class SDUNet(Component):
         mtr = SpatialTransformer(s, "middle.tr", ch, ctx_dim, head_dim)
         mres2 = ResBlock(s, "middle.res2", ch, ch, ted, eps=1e-5)
         self.add_layer("mid", self._mid(mres1, mtr, mres2), ("middle",))
+        self.mid_mods = (mres1, mtr, mres2)
+        self.chans = list(chans)
         oidx = 0
         skip_i = idx - 1
         for lvl, m in list(enumerate(mult))[::-1]:
@@ -422,6 +429,7 @@ class SDUNet(Component):
                     if (lvl != 0 and r == n_res) else None
                 self.add_layer(f"out.{oidx}", self._out_block(res, tr, up, skip_i),
                                (f"output_blocks.{oidx}",))
+                self.out_mods.append((res, tr, up, skip_i))
                 skip_i -= 1
                 oidx += 1
         self.norm_out = nn.GroupNorm(s, "out.norm", ch, 32, 1e-5, silu=True)
@@ -484,3 +492,327 @@ class SDUNet(Component):
         out = {k: v for k, v in st.items() if k not in ("h", "temb", "ctx")}
         out["out"] = eps
         return out
+
+
+# ============================================================================ C3: ControlNet v1.0
+
+class HintImage(Component):
+    """Frozen pre-processing of the ControlNet condition: the raw hint map -> compute dtype.
+    (ControlNet v1.0 trains on hint maps produced by a frozen detector; the synthetic hint is
+    already a map, so the detector is the identity here.)"""
+
+    name = "hint"
+
+    def __init__(self, dtype=torch.bfloat16):
+        super().__init__(dtype, trainable=False)
+        self.add_layer("hint", lambda st: {"hint": ops.cast(st["hint"], self.dtype)}, ())
+
+    def layer_of_param(self, pname):
+        return 0
+
+
+class LockedUNetEncoder:
+    """The locked (frozen) SD U-Net's input blocks + middle block as a FROZEN component of the
+    ControlNet configuration: it consumes the VAE latent and the text
+    context (frozen dependencies vae->enc, text->enc) plus the batch's t and noise,
+    and produces the decoder's inputs (skip stack lk_s*, middle output lk_h, time embedding
+    lk_temb). It shares its parameter store with the locked decoder inside the backbone."""
+
+    def __init__(self, unet: "SDUNet"):
+        self.unet = unet
+        self.name = unet.name
+        self.store = unet.store
+        self.dtype = unet.dtype
+        self.sqrt_ab = self.sqrt_1mab = None   # noise-schedule tables (set by the config builder)
+        n = unet.n_skips
+        self.layers = [self._l0] + [self._block(i) for i in range(1, n)] + [self._mid]
+        self.layer_names = ["lk.in.0"] + [f"lk.in.{i}" for i in range(1, n)] + ["lk.mid"]
+
+    def materialize(self, device, seed=0, state=None):
+        self.unet.materialize(device, seed, state)
+        return self
+
+    def _l0(self, st):
+        u = self.unet
+        xt = ops.q_sample(st["latent"], st["noise"], st["t"], self.sqrt_ab, self.sqrt_1mab)
+        temb = u.t2(nn.silu(u.t1(ops.timestep_embed(st["t"], u.mc, u.dtype))))
+        h = u.conv_in(xt)
+        return {"h": h, "temb": temb, "ctx": st["ctx"], "lk_s0": h}
+
+    def _block(self, i):
+        kind, m, tr = self.unet.in_mods[i - 1]
+
+        def f(st):
+            if kind == "down":
+                h = m(st["h"])
+            else:
+                h = m(st["h"], nn.silu(st["temb"]))
+                if tr is not None:
+                    h = tr(h, st["ctx"])
+            out = dict(st)
+            out["h"], out[f"lk_s{i}"] = h, h
+            return out
+        return f
+
+    def _mid(self, st):
+        r1, tr, r2 = self.unet.mid_mods
+        ta = nn.silu(st["temb"])
+        h = r2(tr(r1(st["h"], ta), st["ctx"]), ta)
+        out = {k: v for k, v in st.items() if k.startswith("lk_s")}
+        out["lk_h"], out["lk_temb"] = h, st["temb"]
+        return out
+
+
+class ControlNet(Component):
+    """ControlNet v1.0 training backbone: the trainable ControlNet branch (hint encoder, a copy
+    of the U-Net input blocks + middle block, zero 1x1 convs on every skip and on the middle
+    output) followed by the LOCKED SD U-Net decoder (frozen weights: input gradients only, no
+    weight gradients) that consumes the locked encoder's frozen outputs plus the ControlNet
+    residuals. One backbone chain, per SURVEY Appendix B.2.
+
+    Planner layers: c.in, c.1..c.11, c.mid, lk.out.0..lk.out.11, lk.final (26).
+    Live set: ch / ctemb (branch), c0..c11, cmid (residuals), lk_* (locked encoder outputs),
+    ctx, noise, then h through the decoder."""
+
+    name = "controlnet"
+    HINT = ((3, 16, 1), (16, 16, 1), (16, 32, 2), (32, 32, 1), (32, 96, 2), (96, 96, 1), (96, 256, 2))
+
+    def __init__(self, locked: SDUNet, dtype=torch.bfloat16, cin=4, ctx_dim=1024, head_dim=64,
+                 attn_levels=(0, 1, 2), mult=(1, 2, 4, 4), n_res=2):
+        super().__init__(dtype, trainable=True)
+        s = self.store
+        self.locked = locked
+        mc = locked.mc
+        self.mc = mc
+        ted = 4 * mc
+        self.t1 = nn.Linear(s, "time_embed.0", mc, ted)
+        self.t2 = nn.Linear(s, "time_embed.2", ted, ted)
+        self.conv_in = nn.Conv2d(s, "input_blocks.0", cin, mc, 3)
+        self.hint = []
+        for j, (a, b, st_) in enumerate(self.HINT):
+            self.hint.append(nn.Conv2d(s, f"input_hint_block.{2 * j}", a, b, 3, stride=st_))
+        self.hint_out = nn.Conv2d(s, f"input_hint_block.{2 * len(self.HINT)}", 256, mc, 3, init="z")
+        self.zero = [nn.Conv2d(s, "zero_convs.0", mc, mc, 1, pad=(0, 0), init="z")]
+        self.add_layer("c.in", self._cin, ("time_embed", "input_blocks.0", "input_hint_block", "zero_convs.0"))
+        ch = mc
+        idx = 1
+        for lvl, m in enumerate(mult):
+            for r in range(n_res):
+                res = ResBlock(s, f"input_blocks.{idx}.res", ch, m * mc, ted, eps=1e-5)
+                ch = m * mc
+                tr = SpatialTransformer(s, f"input_blocks.{idx}.tr", ch, ctx_dim, head_dim) \
+                    if lvl in attn_levels else None
+                z = nn.Conv2d(s, f"zero_convs.{idx}", ch, ch, 1, pad=(0, 0), init="z")
+                self.add_layer(f"c.{idx}", self._cblock(res, tr, z, idx), (f"input_blocks.{idx}", f"zero_convs.{idx}"))
+                idx += 1
+            if lvl != len(mult) - 1:
+                ds = nn.Conv2d(s, f"input_blocks.{idx}.down", ch, ch, 3, stride=2)
+                z = nn.Conv2d(s, f"zero_convs.{idx}", ch, ch, 1, pad=(0, 0), init="z")
+                self.add_layer(f"c.{idx}", self._cdown(ds, z, idx), (f"input_blocks.{idx}", f"zero_convs.{idx}"))
+                idx += 1
+        mres1 = ResBlock(s, "middle.res1", ch, ch, ted, eps=1e-5)
+        mtr = SpatialTransformer(s, "middle.tr", ch, ctx_dim, head_dim)
+        mres2 = ResBlock(s, "middle.res2", ch, ch, ted, eps=1e-5)
+        mz = nn.Conv2d(s, "middle_block_out", ch, ch, 1, pad=(0, 0), init="z")
+        self.add_layer("c.mid", self._cmid(mres1, mtr, mres2, mz), ("middle", "middle_block_out"))
+        for j, (res, tr, up, skip_i) in enumerate(locked.out_mods):
+            self.add_layer(f"lk.out.{j}", self._dec(j, res, tr, up, skip_i), ())
+        self.add_layer("lk.final", self._final, ())
+
+    def layer_of_param(self, pname):
+        return Component.layer_of_param(self, pname)
+
+    def _cin(self, st):
+        temb = self.t2(nn.silu(self.t1(ops.timestep_embed(st["t"], self.mc, self.dtype))))
+        g = st["hint"]
+        for cv in self.hint:
+            g = nn.silu(cv(g))
+        h = self.conv_in(st["x"], residual=self.hint_out(g))
+        out = {k: v for k, v in st.items() if k not in ("x", "t", "pooled", "hint")}
+        out["ch"], out["ctemb"], out["c0"] = h, temb, self.zero[0](h)
+        return out
+
+    @staticmethod
+    def _cblock(res, tr, z, idx):
+        def f(st):
+            h = res(st["ch"], nn.silu(st["ctemb"]))
+            if tr is not None:
+                h = tr(h, st["ctx"])
+            out = dict(st)
+            out["ch"], out[f"c{idx}"] = h, z(h)
+            return out
+        return f
+
+    @staticmethod
+    def _cdown(ds, z, idx):
+        def f(st):
+            h = ds(st["ch"])
+            out = dict(st)
+            out["ch"], out[f"c{idx}"] = h, z(h)
+            return out
+        return f
+
+    @staticmethod
+    def _cmid(r1, tr, r2, z):
+        def f(st):
+            ta = nn.silu(st["ctemb"])
+            h = r2(tr(r1(st["ch"], ta), st["ctx"]), ta)
+            out = {k: v for k, v in st.items() if k not in ("ch", "ctemb")}
+            out["cmid"] = z(h)
+            return out
+        return f
+
+    @staticmethod
+    def _dec(j, res, tr, up, skip_i):
+        def f(st):
+            drop = {f"lk_s{skip_i}", f"c{skip_i}"} | ({"lk_h", "cmid"} if j == 0 else set())
+            out = {k: v for k, v in st.items() if k not in drop}
+            h = nn.add(st["lk_h"], st["cmid"]) if j == 0 else st["h"]
+            h = nn.concat(h, nn.add(st[f"lk_s{skip_i}"], st[f"c{skip_i}"]))
+            h = res(h, nn.silu(st["lk_temb"]))
+            if tr is not None:
+                h = tr(h, st["ctx"])
+            if up is not None:
+                h = up(nn.upsample2x(h))
+            out["h"] = h
+            return out
+        return f
+
+    def _final(self, st):
+        u = self.locked
+        eps = u.conv_out(u.norm_out(st["h"]))
+        out = {k: v for k, v in st.items() if k not in ("h", "lk_temb", "ctx")}
+        out["out"] = eps
+        return out
+
+
+# ============================================================================ C4: cascaded model
+
+def t5_buckets(L, num_buckets=32, max_distance=128):
+    """T5 bidirectional relative-position buckets [L, L] (query i, key j)."""
+    ctx = torch.arange(L)[:, None]
+    mem = torch.arange(L)[None, :]
+    rel = mem - ctx
+    nb = num_buckets // 2
+    ret = (rel > 0).long() * nb
+    n = rel.abs()
+    max_exact = nb // 2
+    large = max_exact + (torch.log(n.float().clamp(min=1) / max_exact) / math.log(max_distance / max_exact)
+                         * (nb - max_exact)).long()
+    large = large.clamp(max=nb - 1)
+    return ret + torch.where(n < max_exact, n, large)
+
+
+class T5Encoder(Component):
+    """T5 v1.1-large-shaped text encoder (frozen): shared token embedding; per block RMSNorm ->
+    self-attention with the relative-position bias of block 0 (no 1/sqrt(d) scaling) ->
+    residual, RMSNorm -> gated-GELU FF -> residual; final RMSNorm -> ctx [B, L, D].
+    Attention runs as QK^T GEMM with the position bias fused as an fp32 residual (batch stride
+    0) in the GEMM epilogue, row softmax, P.V GEMM."""
+
+    name = "t5"
+
+    def __init__(self, dtype=torch.bfloat16, vocab=32128, L=128, D=1024, heads=16, layers=24, ff=2816):
+        super().__init__(dtype, trainable=False)
+        s = self.store
+        self.L, self.D, self.heads, self.ff = L, D, heads, ff
+        self.tok = s.add("shared", (vocab, D), init="e")
+        self.rel = s.add("rel_bias", (32, heads), fp32=True, init="e")
+        self.blocks = []
+        for i in range(layers):
+            p = f"block.{i}"
+            blk = dict(ln1=s.add(f"{p}.ln1.weight", (D,), fp32=True, init="g"),
+                       qkv=nn.Linear(s, f"{p}.attn.qkv", D, 3 * D, bias=False),
+                       o=nn.Linear(s, f"{p}.attn.o", D, D, bias=False),
+                       ln2=s.add(f"{p}.ln2.weight", (D,), fp32=True, init="g"),
+                       wi=nn.Linear(s, f"{p}.ff.wi", D, 2 * ff, bias=False),
+                       wo=nn.Linear(s, f"{p}.ff.wo", ff, D, bias=False))
+            self.blocks.append(blk)
+            pre = (p, "shared", "rel_bias") if i == 0 else (p,)
+            if i == layers - 1:
+                pre = pre + ("final_ln",)
+            self.add_layer(p, self._make_block(i, layers), pre)
+        self.final_ln = s.add("final_ln.weight", (D,), fp32=True, init="g")
+
+    def _post_materialize(self):
+        # the position bias is a function of the frozen table only: expand it once (init time)
+        L = self.L
+        self.ld = -(-L // 8) * 8
+        idx = t5_buckets(L).to(self.rel.w.device)
+        bias = torch.zeros(self.heads, L, self.ld, device=self.rel.w.device, dtype=torch.float32)
+        bias[:, :, :L] = self.rel.w.float()[idx].permute(2, 0, 1)
+        self.pos_bias = bias
+
+    def _rms(self, x, g):
+        y = torch.empty_like(x)
+        ops.rms_norm(x, g.w, y, 1e-6)
+        return y
+
+    def _attn(self, x, blk):
+        B, L, D = x.shape
+        H, hd, ld = self.heads, D // self.heads, self.ld
+        qkv = ops.linear(self._rms(x, blk["ln1"]).view(-1, D), blk["qkv"].weight.w)
+        S = torch.empty(B, H, L, ld, device=x.device, dtype=torch.float32)
+        ops.gemm(qkv, qkv.view(-1)[D:], S, M=L, N=L, K=hd, a_ld=3 * D, b_ld=3 * D, d_ld=ld, batch=(H, B),
+                 a_bs=(hd, L * 3 * D), b_bs=(hd, L * 3 * D), d_bs=(L * ld, H * L * ld),
+                 residual=self.pos_bias, r_ld=ld, r_bs=(L * ld, 0))
+        P = torch.empty(B, H, L, ld, device=x.device, dtype=x.dtype)
+        ops.softmax(S, P, 1.0, L)
+        o = torch.empty(B, L, D, device=x.device, dtype=x.dtype)
+        ops.gemm(P, qkv.view(-1)[2 * D:], o, M=L, N=hd, K=L, a_ld=ld, b_ld=3 * D, b_mn=True, d_ld=D,
+                 batch=(H, B), a_bs=(L * ld, H * L * ld), b_bs=(hd, L * 3 * D), d_bs=(hd, L * D))
+        return ops.linear(o.view(-1, D), blk["o"].weight.w, residual=x.view(-1, D)).view(B, L, D)
+
+    def _make_block(self, i, n):
+        blk = self.blocks[i]
+
+        def f(st):
+            x = ops.embed(st["ids"], self.tok.w) if i == 0 else st["h"]
+            B, L, D = x.shape
+            x = self._attn(x, blk)
+            m = ops.geglu(ops.linear(self._rms(x, blk["ln2"]).view(-1, D), blk["wi"].weight.w))
+            x = ops.linear(m, blk["wo"].weight.w, residual=x.view(-1, D)).view(B, L, D)
+            if i == n - 1:
+                return {"ctx": self._rms(x, self.final_ln)}
+            return {"h": x}
+        return f
+
+
+class ImagePyramid(Component):
+    """Frozen pre-processing of the cascaded model (CDM): the 256 px image is the x0 of the
+    super-resolution pipe ("img_sr"); its 4x4 average pool is the 64 px x0 of the base pipe
+    ("latent"); the nearest 4x upsample of that is the SR pipe's low-resolution condition
+    ("lowres"). Average pooling = space-to-depth(4) + a constant [3, 48] averaging GEMM."""
+
+    name = "pyramid"
+
+    def __init__(self, dtype=torch.bfloat16, factor=4):
+        super().__init__(dtype, trainable=False)
+        self.f = factor
+        self.add_layer("pool", self._pool, ())
+        self.add_layer("lowres", self._lowres, ())
+
+    def layer_of_param(self, pname):
+        return 0
+
+    def _post_materialize(self):
+        f2 = self.f * self.f
+        w = torch.zeros(3, f2 * 3)
+        for c in range(3):
+            w[c, c::3] = 1.0 / f2
+        self.avg_w = w.to(self.device, self.dtype)
+
+    def _pool(self, st):
+        img = ops.cast(st["images"], self.dtype)
+        B, H, W, _ = img.shape
+        sd = ops.space_to_depth(img, self.f)            # [B, H/f, W/f, f*f*3]
+        lo = ops.linear(sd.view(-1, sd.shape[-1]), self.avg_w).view(B, H // self.f, W // self.f, 3)
+        return {"img_sr": img, "latent": lo}
+
+    def _lowres(self, st):
+        up = st["latent"]
+        f = self.f
+        while f > 1:
+            up = ops.upsample2x(up)
+            f //= 2
+        return {"img_sr": st["img_sr"], "latent": st["latent"], "lowres": up}

@@ -494,6 +494,14 @@ def layer_norm(x, gamma, beta, eps, mod=None, mod_ld=0, shift_off=0, scale_off=0
     return y, mean, rstd
 
 
+def rms_norm(x, gamma, y, eps):
+    """T5 RMSNorm forward (frozen encoders): y = x * rsqrt(mean(x^2) + eps) * gamma."""
+    C = x.shape[-1]
+    check(_L().dp_rms_norm_fwd(dtype_code(x), _ptr(x), _ptr(gamma), _ptr(y), x.numel() // C, C, eps,
+                               _stream()), "dp_rms_norm_fwd")
+    return y
+
+
 def layer_norm_bwd(x, dy, gamma, mean, rstd, dgamma=None, dbeta=None, mod=None, mod_ld=0, shift_off=0,
                    scale_off=0, rows_per_sample=1, dmod=None, dmod_ld=0):
     C = x.shape[-1]

@@ -62,10 +62,10 @@ def probe_specs(model, batch_fn, device):
         finals[c] = st
         fro.update(st)
     t = batch_fn("t")
-    noise = batch_fn("noise")
     live_all = []
     for pipe, bb in enumerate(getattr(model, "backbones", None) or [model.backbone]):
-        st, _ = model.stage0_inputs(fro, t, noise, pipe=pipe)
+        nf = model.noise_field(pipe) if hasattr(model, "noise_field") else "noise"
+        st, _ = model.stage0_inputs(fro, t, batch_fn(nf), pipe=pipe)
         live = [_spec_of(st)]
         ctx = bb.grad_context() if hasattr(bb, "grad_context") else torch.enable_grad()
         with ctx:

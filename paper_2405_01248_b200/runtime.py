@@ -51,9 +51,12 @@ class TrainModel:
     """
 
     def __init__(self, backbone, frozen, ops, sqrt_ab, sqrt_1mab, selfcond_channels=0,
-                 grad_scale=1.0, adamw=None, backbones=None):
+                 grad_scale=1.0, adamw=None, backbones=None, pipe_io=None):
         self.backbone = backbone
         self.backbones = list(backbones) if backbones else [backbone]
+        # per backbone: which frozen output is x0, which batch field is its noise and which
+        # frozen output (if any) is concatenated as conditioning (cascaded super-resolution)
+        self.pipe_io = pipe_io or [dict(latent="latent", noise="noise", cond=None)] * len(self.backbones)
         self.frozen = frozen
         self.ops = ops
         self.sqrt_ab = sqrt_ab
@@ -67,18 +70,24 @@ class TrainModel:
         `pipe` selects the backbone of a two-backbone (bidirectional) model; both backbones of
         a cascaded model share the frozen outputs and the noise draw."""
         o = self.ops
-        x0 = frozen_out["latent"]
+        io = self.pipe_io[pipe]
+        x0 = frozen_out[io["latent"]]
         xt = o.q_sample(x0, noise, t, self.sqrt_ab, self.sqrt_1mab)
+        x = xt
+        if io.get("cond"):
+            x = o.concat_last(x, frozen_out[io["cond"]])
         if self.sc_ch:
             sc = x0_sc if x0_sc is not None else torch.zeros_like(xt)
-            x = o.concat_last(xt, sc)
-        else:
-            x = xt
+            x = o.concat_last(x, sc)
         st = {"x": x, "t": t, "noise": noise}
+        skip = {io["latent"], io.get("cond")} | set(io.get("drop", ()))
         for k, v in frozen_out.items():
-            if k != "latent":
+            if k not in skip:
                 st[k] = v
         return st, xt
+
+    def noise_field(self, pipe=0):
+        return self.pipe_io[pipe]["noise"]
 
 
 # ============================================================================ helpers
@@ -263,6 +272,7 @@ class PipelineExecutor:
         self.frozen_ready = {}   # for the NEXT iteration: comp -> list[(lo, hi, state)] on stage-0 owners
         self.loss_buf = torch.zeros(1, device=self.device, dtype=torch.float32)
         self.grad_snapshots = None  # list -> flat grad slices captured before each AdamW
+        self.grad_snapshot_pipes = []  # backbone index of each snapshot
         self._frz_sends = []        # in-flight frozen-activation sends (kept alive until deliver)
 
     # ---------------------------------------------------------------- setup
@@ -470,8 +480,8 @@ class PipelineExecutor:
         key = (pi, m, sc_pass)
         if s == 0:
             fro = self.frozen_for(self.frozen_cur, lo_r, hi_r)
-            t, noise = self.inputs.t(self.gb + lo_r, self.gb + hi_r), self.inputs.noise(self.gb + lo_r,
-                                                                                         self.gb + hi_r)
+            t = self.inputs.t(self.gb + lo_r, self.gb + hi_r)
+            noise = self.inputs.get(self.model.noise_field(pl.backbone), self.gb + lo_r, self.gb + hi_r)
             x0_sc = None
             if not sc_pass and prog.selfcond:
                 eps_sc = self._feedback_in.pop((pi, m))
@@ -494,7 +504,8 @@ class PipelineExecutor:
             else:
                 pred = out["out"]
                 dpred = torch.empty_like(pred)
-                self.model.ops.mse(pred.detach(), out["noise"], self.loss_buf, self.loss_scale, dpred)
+                ls = self.loss_scale[pl.backbone] if isinstance(self.loss_scale, (list, tuple)) else self.loss_scale
+                self.model.ops.mse(pred.detach(), out["noise"], self.loss_buf, ls, dpred)
                 self._saved[key] = (st_in, [pred], [dpred])
         else:
             if not sc_pass:
@@ -617,6 +628,7 @@ class PipelineExecutor:
                 dist.all_reduce(store.grad[lo:hi], group=pg)
         if self.grad_snapshots is not None:
             self.grad_snapshots.append((lo, hi, store.grad[lo:hi].detach().clone()))
+            self.grad_snapshot_pipes.append(self.prog.pipes[pi].backbone)
         store.adamw_step(rng=(lo, hi), **self.model.adamw)
         store.zero_grad((lo, hi))
 
