@@ -81,6 +81,37 @@ __global__ void flip_kernel(const T* __restrict__ w, T* __restrict__ wt, int K, 
   }
 }
 
+// Tiled flip-transpose (bf16, K % 8 == 0, C % 8 == 0): per tap, a 64 x 64 block of w[k][tap][c]
+// is read with 16-byte row loads (coalesced in c), staged in shared memory, and written as
+// 16-byte vectors of 8 consecutive k (coalesced in k) to wt[c][flipped tap][k]. The scalar
+// flip_kernel above scatters its writes with stride K (one 2-byte store per 128-byte line).
+__global__ void __launch_bounds__(256)
+    flip_t_kernel(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ wt, int K, int R, int S,
+                  int C) {
+  __shared__ __nv_bfloat16 tile[64][64 + 8];
+  const int c0 = blockIdx.x * 64, k0 = blockIdx.y * 64, tap = blockIdx.z;
+  const int RS = R * S;
+  const int r = tap / S, s = tap - (tap / S) * S;
+  const int ftap = (R - 1 - r) * S + (S - 1 - s);
+  for (int i = threadIdx.x; i < 64 * 8; i += 256) {
+    const int kk = i >> 3, cv = (i & 7) * 8;
+    const int k = k0 + kk, c = c0 + cv;
+    uint4 u = make_uint4(0, 0, 0, 0);
+    if (k < K && c < C) u = *reinterpret_cast<const uint4*>(w + ((int64_t)k * RS + tap) * C + c);
+    *reinterpret_cast<uint4*>(&tile[kk][cv]) = u;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 64 * 8; i += 256) {
+    const int cc = i >> 3, kv = (i & 7) * 8;
+    const int c = c0 + cc, k = k0 + kv;
+    if (c >= C || k >= K) continue;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = tile[kv + j][cc];
+    *reinterpret_cast<uint4*>(wt + ((int64_t)c * RS + ftap) * K + k) = *reinterpret_cast<const uint4*>(v);
+  }
+}
+
 template <typename T>
 __global__ void dilate_kernel(const T* __restrict__ dy, T* __restrict__ out, int N, int P, int Q,
                               int C, int stride) {
@@ -154,7 +185,10 @@ int dp_conv_weight_flip(int dtype, const void* w, void* wt, int K, int R, int S,
   const int64_t total = (int64_t)K * R * S * C;
   if (total == 0) return 0;
   auto st = reinterpret_cast<cudaStream_t>(stream);
-  if (dtype == DP_F32)
+  if (dtype != DP_F32 && K % 8 == 0 && C % 8 == 0) {
+    dim3 grid((C + 63) / 64, (K + 63) / 64, R * S);
+    flip_t_kernel<<<grid, 256, 0, st>>>((const __nv_bfloat16*)w, (__nv_bfloat16*)wt, K, R, S, C);
+  } else if (dtype == DP_F32)
     flip_kernel<float><<<grid_for(total), 256, 0, st>>>((const float*)w, (float*)wt, K, R, S, C);
   else
     flip_kernel<__nv_bfloat16><<<grid_for(total), 256, 0, st>>>(

@@ -244,7 +244,9 @@ def conv2d_dgrad(dy, w, x_shape, *, stride=1, pad=(1, 1)):
     _, H, W, _ = x_shape
     if R == 1 and S == 1 and stride == 1 and pad == (0, 0):
         return linear_dgrad(dy.reshape(-1, K), w.reshape(K, C)).view(N, H, W, C)
-    if dy.dtype == torch.bfloat16 and _tiles(H, W, 128):
+    if dy.dtype == torch.bfloat16 and _tiles(H, W, 128) and N * H * W < 8192:
+        # small feature maps (U-Net 8x8 / 4x4 levels): the weights dominate the traffic, read
+        # them tap-flipped in place (MN-major B_DGRAD operand mode, no transposed copy)
         src = _pad_last(dy)
         Kp = src.shape[-1]
         wp = _pad_first(_pad_last(w))
@@ -260,6 +262,30 @@ def conv2d_dgrad(dy, w, x_shape, *, stride=1, pad=(1, 1)):
         ws = _splitk_ws(a, "dp_conv_dgrad_workspace", dy.device)
         telemetry.timed("tcgen05_gemm", 2.0 * N * H * W * C * R * S * K,
                         lambda: check(_lib.lib().dp_conv_dgrad(ctypes.byref(a), _stream()), "dp_conv_dgrad",
+                                      2 if ws is not None else 1),
+                        sub="conv_dgrad")
+        return _take_last(dx, C)
+    if dy.dtype == torch.bfloat16 and _tiles(H, W, 128):
+        # dx = conv(dy (zero-dilated for stride 2), flip-transposed w, pad R-1-pad): the forward
+        # implicit GEMM with K-major weights (CTA pairs, 32-column tile widths) instead of the
+        # MN-major B_DGRAD operand mode (64-column boxes, single CTAs)
+        src = _pad_last(dy)
+        Kp = src.shape[-1]
+        wp = _pad_first(_pad_last(w))
+        Cp = wp.shape[-1]
+        if stride > 1:
+            dil = torch.empty(N, P * stride, Q * stride, Kp, device=dy.device, dtype=dy.dtype)
+            check(_lib.lib().dp_dilate(dtype_code(dy), _ptr(src), _ptr(dil), N, P, Q, Kp, stride,
+                                       _stream()), "dp_dilate")
+            src = dil
+        wt = torch.empty(Cp, R, S, Kp, device=dy.device, dtype=dy.dtype)
+        check(_lib.lib().dp_conv_weight_flip(dtype_code(wp), _ptr(wp), _ptr(wt), Kp, R, S, Cp, _stream()),
+              "dp_conv_weight_flip")
+        dx = torch.empty(N, H, W, Cp, device=dy.device, dtype=dy.dtype)
+        a = _conv_args(src, wt, dx, 1, (R - 1 - pad[0], S - 1 - pad[1]), H, W)
+        ws = _splitk_ws(a, "dp_conv_fwd_workspace", dy.device)
+        telemetry.timed("tcgen05_gemm", 2.0 * N * H * W * C * R * S * K,
+                        lambda: check(_lib.lib().dp_conv_fwd(ctypes.byref(a), _stream()), "dp_conv_fwd",
                                       2 if ws is not None else 1),
                         sub="conv_dgrad")
         return _take_last(dx, C)
