@@ -593,59 +593,94 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-template <typename T, int NVEC>
+// Backward of LayerNorm: warps stride over rows (grid sized to the SMs); with affine params
+// each lane also accumulates dgamma (dy * xhat) and dbeta (dy) of its channels over its rows in
+// registers, the 8 warps of a block merge them in shared memory and the block adds them to the
+// fp32 gradients with one atomic per channel (no second pass over x and dy).
+template <typename T, int NVEC, bool PG>
 __global__ void __launch_bounds__(256)
     ln_bwd_kernel(const T* __restrict__ x, const T* __restrict__ dy,
                   const float* __restrict__ gamma, const T* __restrict__ mod, int64_t mod_ld,
                   int scale_off, int rps, const float* __restrict__ mean,
                   const float* __restrict__ rstd, T* __restrict__ dx, int64_t rows, int C,
-                  int accumulate) {
+                  int accumulate, float* __restrict__ dgamma, float* __restrict__ dbeta) {
   constexpr int V = NV<T>::V;
   const int lane = threadIdx.x & 31;
-  const int64_t row = blockIdx.x * 8LL + (threadIdx.x >> 5);
-  if (row >= rows) return;
+  const int warp = threadIdx.x >> 5;
   const int CV = C / V;
-  const float mu = mean[row], rs = rstd[row];
-  const T* xr = x + row * C;
-  const T* dr = dy + row * C;
-  const T* mr = mod ? mod + (row / rps) * mod_ld : nullptr;
-  float xh[NVEC][V], g[NVEC][V];
-  float s1 = 0.f, s2 = 0.f;
+  constexpr bool pg = PG;
+  float ag[PG ? NVEC : 1][V], ab[PG ? NVEC : 1][V];
 #pragma unroll
-  for (int k = 0; k < NVEC; ++k) {
-    const int cv = lane + 32 * k;
-    if (cv < CV) {
-      ld16(xr + cv * V, xh[k]);
-      ld16(dr + cv * V, g[k]);
+  for (int k = 0; k < (PG ? NVEC : 1); ++k)
 #pragma unroll
-      for (int j = 0; j < V; ++j) {
-        const int c = cv * V + j;
-        xh[k][j] = (xh[k][j] - mu) * rs;
-        float d = g[k][j];
-        if (gamma) d *= __ldg(gamma + c);
-        if (mr) d *= 1.f + to_f(mr[scale_off + c]);
-        g[k][j] = d;
-        s1 += d;
-        s2 += d * xh[k][j];
+    for (int j = 0; j < V; ++j) ag[k][j] = ab[k][j] = 0.f;
+  for (int64_t row = blockIdx.x * 8LL + warp; row < rows; row += gridDim.x * 8LL) {
+    const float mu = mean[row], rs = rstd[row];
+    const T* xr = x + row * C;
+    const T* dr = dy + row * C;
+    const T* mr = mod ? mod + (row / rps) * mod_ld : nullptr;
+    float xh[NVEC][V], g[NVEC][V];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NVEC; ++k) {
+      const int cv = lane + 32 * k;
+      if (cv < CV) {
+        ld16(xr + cv * V, xh[k]);
+        ld16(dr + cv * V, g[k]);
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          const int c = cv * V + j;
+          xh[k][j] = (xh[k][j] - mu) * rs;
+          float d = g[k][j];
+          if constexpr (PG) {
+            ag[k][j] = fmaf(d, xh[k][j], ag[k][j]);
+            ab[k][j] += d;
+          }
+          if (gamma) d *= __ldg(gamma + c);
+          if (mr) d *= 1.f + to_f(mr[scale_off + c]);
+          g[k][j] = d;
+          s1 += d;
+          s2 += d * xh[k][j];
+        }
+      }
+    }
+    s1 = warp_sum(s1) / C;
+    s2 = warp_sum(s2) / C;
+    T* xo = dx + row * C;
+#pragma unroll
+    for (int k = 0; k < NVEC; ++k) {
+      const int cv = lane + 32 * k;
+      if (cv < CV) {
+        float o[V], prev[V];
+        if (accumulate) ld16(xo + cv * V, prev);
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          o[j] = rs * (g[k][j] - s1 - xh[k][j] * s2);
+          if (accumulate) o[j] += prev[j];
+        }
+        st16(xo + cv * V, o);
       }
     }
   }
-  s1 = warp_sum(s1) / C;
-  s2 = warp_sum(s2) / C;
-  T* xo = dx + row * C;
+  if constexpr (!PG) return;
+  __shared__ float sg[PG ? 2048 : 1], sb[PG ? 2048 : 1];
+  for (int c = threadIdx.x; c < C; c += 256) sg[c] = sb[c] = 0.f;
+  __syncthreads();
 #pragma unroll
-  for (int k = 0; k < NVEC; ++k) {
+  for (int k = 0; k < (PG ? NVEC : 1); ++k) {
     const int cv = lane + 32 * k;
     if (cv < CV) {
-      float o[V], prev[V];
-      if (accumulate) ld16(xo + cv * V, prev);
 #pragma unroll
       for (int j = 0; j < V; ++j) {
-        o[j] = rs * (g[k][j] - s1 - xh[k][j] * s2);
-        if (accumulate) o[j] += prev[j];
+        atomicAdd(&sg[cv * V + j], ag[k][j]);
+        atomicAdd(&sb[cv * V + j], ab[k][j]);
       }
-      st16(xo + cv * V, o);
     }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += 256) {
+    atomicAdd(dgamma + c, sg[c]);
+    atomicAdd(dbeta + c, sb[c]);
   }
 }
 
@@ -660,29 +695,45 @@ __global__ void __launch_bounds__(256)
                          int64_t rows, int C, int rows_per_seg, float* __restrict__ dgamma,
                          float* __restrict__ dbeta, T* __restrict__ dmod, int64_t dmod_ld,
                          int shift_off, int scale_off) {
-  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  // 16-byte vectors: a block covers 32 channel vectors x 8 row lanes of one row segment
+  constexpr int V = NV<T>::V;
+  const int CV = C / V;
+  const int cv = blockIdx.x * 32 + (threadIdx.x & 31);
   const int ry = threadIdx.x >> 5;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_seg;
   const int64_t r1 = min(rows, r0 + rows_per_seg);
-  float a = 0.f, b = 0.f;
-  if (c < C) {
+  float a[V], b[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) a[j] = b[j] = 0.f;
+  if (cv < CV) {
+#pragma unroll 2
     for (int64_t r = r0 + ry; r < r1; r += 8) {
-      const float xh = (to_f(x[r * C + c]) - mean[r]) * rstd[r];
-      const float d = to_f(dy[r * C + c]);
-      a += d * xh;
-      b += d;
+      float fx[V], fd[V];
+      ld16(x + r * C + cv * V, fx);
+      ld16(dy + r * C + cv * V, fd);
+      const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        a[j] = fmaf(fd[j], (fx[j] - mu) * rs, a[j]);
+        b[j] += fd[j];
+      }
     }
   }
-  __shared__ float ra[8][33], rb[8][33];
-  ra[ry][threadIdx.x & 31] = a;
-  rb[ry][threadIdx.x & 31] = b;
+  __shared__ float ra[8][32 * 8 + 1], rb[8][32 * 8 + 1];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    ra[ry][(threadIdx.x & 31) * V + j] = a[j];
+    rb[ry][(threadIdx.x & 31) * V + j] = b[j];
+  }
   __syncthreads();
-  if (ry == 0 && c < C) {
+  for (int t = threadIdx.x; t < 32 * V; t += 256) {
+    const int c = blockIdx.x * 32 * V + t;
+    if (c >= C) continue;
     float sa = 0.f, sb = 0.f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      sa += ra[k][threadIdx.x];
-      sb += rb[k][threadIdx.x];
+      sa += ra[k][t];
+      sb += rb[k][t];
     }
     if (dmod) {
       dmod[blockIdx.y * dmod_ld + scale_off + c] = from_f<T>(sa);
@@ -878,19 +929,41 @@ int dp_layer_norm_bwd(int dtype, const void* x, const void* dy, const float* gam
     return DP_ERR_ARGS;
   }
   const int rps = rows_per_sample > 0 ? rows_per_sample : 1;
-  const dim3 grid(static_cast<unsigned>((rows + 7) / 8));
-  DISPATCH_T(dtype, LN_PER_DISPATCH(C, ln_bwd_kernel, cp<T>(x), cp<T>(dy), gamma, cp<T>(mod),
-                                    mod_ld, scale_off, rps, mean, rstd, mp<T>(dx), rows, C,
-                                    accumulate));
-  if (gamma && dgamma) {
-    const int seg = 256;
-    dim3 g2((C + 31) / 32, static_cast<unsigned>((rows + seg - 1) / seg));
+  const int nvec = (C / (dtype == DP_F32 ? 4 : 8) + 31) / 32;
+  // affine parameter grads fused into the row pass while the per-lane partials fit in registers
+  // (C <= 1024 bf16): few fat blocks, each merging its rows' partials once
+  const bool pg = gamma && dgamma && nvec <= 4;
+  const int64_t want = (rows + 7) / 8;
+  const int64_t cap = pg ? 2 * kNumSMs : want;
+  const dim3 grid(static_cast<unsigned>(want < cap ? want : cap));
+#define LN_BWD_ARGS cp<T>(x), cp<T>(dy), gamma, cp<T>(mod), mod_ld, scale_off, rps, mean, rstd, mp<T>(dx), \
+                    rows, C, accumulate, dgamma, dbeta
+  DISPATCH_T(dtype, {
+    if (pg) {
+      if (nvec <= 1) ln_bwd_kernel<T, 1, true><<<grid, 256, 0, ST>>>(LN_BWD_ARGS);
+      else if (nvec <= 2) ln_bwd_kernel<T, 2, true><<<grid, 256, 0, ST>>>(LN_BWD_ARGS);
+      else ln_bwd_kernel<T, 4, true><<<grid, 256, 0, ST>>>(LN_BWD_ARGS);
+    } else {
+      if (nvec <= 1) ln_bwd_kernel<T, 1, false><<<grid, 256, 0, ST>>>(LN_BWD_ARGS);
+      else if (nvec <= 2) ln_bwd_kernel<T, 2, false><<<grid, 256, 0, ST>>>(LN_BWD_ARGS);
+      else if (nvec <= 4) ln_bwd_kernel<T, 4, false><<<grid, 256, 0, ST>>>(LN_BWD_ARGS);
+      else if (nvec <= 8) ln_bwd_kernel<T, 8, false><<<grid, 256, 0, ST>>>(LN_BWD_ARGS);
+      else ln_bwd_kernel<T, 16, false><<<grid, 256, 0, ST>>>(LN_BWD_ARGS);
+    }
+  });
+#undef LN_BWD_ARGS
+  if (gamma && dgamma && !pg) {
+    const int CVn = C / (dtype == DP_F32 ? 4 : 8);
+    const int64_t cb = (CVn + 31) / 32;
+    int64_t seg = (rows * cb + 2 * kNumSMs - 1) / (2 * kNumSMs);  // ~2 waves
+    seg = seg < 64 ? 64 : seg;
+    dim3 g2(static_cast<unsigned>(cb), static_cast<unsigned>((rows + seg - 1) / seg));
     DISPATCH_T(dtype, ln_param_grad_kernel<T><<<g2, 256, 0, ST>>>(
                           cp<T>(x), cp<T>(dy), mean, rstd, rows, C, seg, dgamma, dbeta, nullptr, 0,
                           0, 0));
   }
   if (mod && dmod) {
-    dim3 g2((C + 31) / 32, static_cast<unsigned>(rows / rps));
+    dim3 g2(static_cast<unsigned>((C / (dtype == DP_F32 ? 4 : 8) + 31) / 32), static_cast<unsigned>(rows / rps));
     DISPATCH_T(dtype, ln_param_grad_kernel<T><<<g2, 256, 0, ST>>>(
                           cp<T>(x), cp<T>(dy), mean, rstd, rows, C, rps, nullptr, nullptr,
                           mp<T>(dmod), dmod_ld, shift_off, scale_off));
