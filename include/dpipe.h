@@ -216,6 +216,13 @@ int dp_adamw(float* param, const float* grad, float* exp_avg, float* exp_avg_sq,
 
 /* same update with the step counter on the device (*step_dev is incremented first; bc_dev
    receives the two bias corrections) so that a captured CUDA graph can replay it */
+/* chunked AdamW: advance the device step counter / bias corrections once per iteration, then
+   update flat slices (e.g. layer by layer while the backward pass still runs) */
+int dp_adamw_advance(int* step_dev, float beta1, float beta2, float* bc_dev, dp_stream_t stream);
+int dp_adamw_apply(float* param, const float* grad, float* exp_avg, float* exp_avg_sq,
+                   void* param_bf16, int64_t n, float lr, float beta1, float beta2, float eps,
+                   float weight_decay, const float* bc_dev, float grad_scale, int max_ctas,
+                   int zero_grad, dp_stream_t stream);
 int dp_adamw_dev(float* param, const float* grad, float* exp_avg, float* exp_avg_sq,
                  void* param_bf16, int64_t n, float lr, float beta1, float beta2, float eps,
                  float weight_decay, int* step_dev, float* bc_dev, float grad_scale,

@@ -108,6 +108,9 @@ _SIGNATURES = {
     "dp_cast": [c_int, c_int, c_void_p, c_void_p, c_i64, c_void_p],
     "dp_adamw": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_float, c_float, c_float,
                  c_float, c_float, c_int, c_float, c_void_p],
+    "dp_adamw_advance": [c_void_p, c_float, c_float, c_void_p, c_void_p],
+    "dp_adamw_apply": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_float, c_float, c_float,
+                       c_float, c_float, c_void_p, c_float, c_int, c_int, c_void_p],
     "dp_adamw_dev": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_float, c_float, c_float,
                      c_float, c_float, c_void_p, c_void_p, c_float, c_void_p],
     # norm.cu

@@ -407,7 +407,7 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
                              float* __restrict__ m, float* __restrict__ v,
                              __nv_bfloat16* __restrict__ p_bf16, int64_t n, float lr, float b1,
                              float b2, float eps, float wd, float bc1, float bc2, float gscale,
-                             const float* __restrict__ bc_dev) {
+                             const float* __restrict__ bc_dev, int zero_g) {
   if (bc_dev) {  // bias corrections of a device-side step counter (CUDA-graph replayable)
     bc1 = bc_dev[0];
     bc2 = bc_dev[1];
@@ -435,6 +435,7 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
     reinterpret_cast<float4*>(p)[i] = pp;
     reinterpret_cast<float4*>(m)[i] = mm;
     reinterpret_cast<float4*>(v)[i] = vv;
+    if (zero_g) reinterpret_cast<float4*>(const_cast<float*>(g))[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (p_bf16) {
       uint2 o;
       o.x = pack_bf16x2(pa[0], pa[1]);
@@ -454,6 +455,7 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
     m[i] = mj;
     v[i] = vj;
     if (p_bf16) p_bf16[i] = __float2bfloat16_rn(pj);
+    if (zero_g) const_cast<float*>(g)[i] = 0.f;
   }
 }
 
@@ -958,8 +960,35 @@ int dp_adamw(float* param, const float* grad, float* exp_avg, float* exp_avg_sq,
   adamw_kernel<<<ew_grid(n / 4 + 1), 256, 0, ST>>>(param, grad, exp_avg, exp_avg_sq,
                                                     mp<__nv_bfloat16>(param_bf16), n, lr, beta1,
                                                     beta2, eps, weight_decay, bc1, bc2,
-                                                    grad_scale, nullptr);
+                                                    grad_scale, nullptr, 0);
   return ew_check("adamw");
+}
+
+// Chunked AdamW (optimizer overlapped with the backward pass): advance the device step counter
+// and bias corrections once per iteration, then update any number of flat slices with them.
+int dp_adamw_advance(int* step_dev, float beta1, float beta2, float* bc_dev, dp_stream_t stream) {
+  adamw_step_kernel<<<1, 1, 0, ST>>>(step_dev, beta1, beta2, bc_dev);
+  return ew_check("adamw_advance");
+}
+
+int dp_adamw_apply(float* param, const float* grad, float* exp_avg, float* exp_avg_sq,
+                   void* param_bf16, int64_t n, float lr, float beta1, float beta2, float eps,
+                   float weight_decay, const float* bc_dev, float grad_scale, int max_ctas,
+                   int zero_grad, dp_stream_t stream) {
+  if (n <= 0) return 0;
+  if (!aligned16(param) || !aligned16(grad) || !aligned16(exp_avg) || !aligned16(exp_avg_sq)) {
+    set_error("dp_adamw_apply: flat buffers must be 16-byte aligned");
+    return DP_ERR_ARGS;
+  }
+  // max_ctas > 0 caps the grid (grid-stride loop): a background update running next to the
+  // backward pass must leave thread slots for the persistent GEMM CTAs on every SM
+  int grid = ew_grid(n / 4 + 1);
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  adamw_kernel<<<grid, 256, 0, ST>>>(param, grad, exp_avg, exp_avg_sq,
+                                                    mp<__nv_bfloat16>(param_bf16), n, lr, beta1,
+                                                    beta2, eps, weight_decay, 1.f, 1.f, grad_scale,
+                                                    bc_dev, zero_grad);
+  return ew_check("adamw_apply");
 }
 
 int dp_adamw_dev(float* param, const float* grad, float* exp_avg, float* exp_avg_sq,
@@ -975,7 +1004,7 @@ int dp_adamw_dev(float* param, const float* grad, float* exp_avg, float* exp_avg
   adamw_kernel<<<ew_grid(n / 4 + 1), 256, 0, ST>>>(param, grad, exp_avg, exp_avg_sq,
                                                     mp<__nv_bfloat16>(param_bf16), n, lr, beta1,
                                                     beta2, eps, weight_decay, 1.f, 1.f, grad_scale,
-                                                    bc_dev);
+                                                    bc_dev, 0);
   return ew_check("adamw_dev");
 }
 

@@ -71,12 +71,21 @@ class Component:
         return self
 
     def stage_slice(self, lo, hi):
-        """[start, end) element range of layers [lo, hi) in the flat buffers."""
-        ps = [p for p in self.store.params.values() if lo <= self.layer_of_param(p.name) < hi]
-        if not ps:
+        """[start, end) element range of layers [lo, hi) in the flat buffers (per-layer ranges
+        are computed once: this is called per layer group on the backward's critical path)."""
+        rng = getattr(self, "_layer_rng", None)
+        if rng is None:
+            rng = {}
+            for p in self.store.params.values():
+                j = self.layer_of_param(p.name)
+                a, b = rng.get(j, (p.offset, p.offset + p.numel))
+                rng[j] = (min(a, p.offset), max(b, p.offset + p.numel))
+            self._layer_rng = rng
+        parts = [rng[j] for j in range(lo, hi) if j in rng]
+        if not parts:
             return (0, 0)
-        start = min(p.offset for p in ps)
-        end = max(p.offset + p.numel for p in ps)
+        start = min(a for a, _ in parts)
+        end = max(b for _, b in parts)
         end = -(-end // nn._ALIGN) * nn._ALIGN
         return (start, end)
 

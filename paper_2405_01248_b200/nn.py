@@ -117,6 +117,26 @@ class ParamStore:
             lo, hi = rng if rng is not None else (0, self.grad.numel())
             self.grad[lo:hi].zero_()
 
+    def adamw_begin(self, betas=(0.9, 0.999), **_):
+        """Chunked AdamW, part 1: advance the step counter (host and device) once per iteration."""
+        self.step += 1
+        if getattr(self, "step_dev", None) is None:
+            self.step_dev = torch.zeros(1, device=self.master.device, dtype=torch.int32)
+            self.bc_dev = torch.zeros(2, device=self.master.device, dtype=torch.float32)
+        ops.adamw_advance(self.step_dev, self.bc_dev, betas[0], betas[1])
+
+    def adamw_apply(self, rng, lr=1e-4, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01, grad_scale=1.0,
+                    max_ctas=0, zero_grad=False):
+        """(zero_grad: the kernel clears the gradient slice after reading it — no separate fill.)"""
+        """Chunked AdamW, part 2: update the flat slice `rng` with this iteration's corrections."""
+        lo, hi = rng
+        if hi <= lo:
+            return
+        ops.adamw_apply(self.master[lo:hi], self.grad[lo:hi], self.exp_avg[lo:hi], self.exp_avg_sq[lo:hi],
+                        None if self.compute is self.master else self.compute[lo:hi],
+                        lr, betas[0], betas[1], eps, weight_decay, self.bc_dev, grad_scale, max_ctas,
+                        zero_grad)
+
     def adamw_step(self, lr=1e-4, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01, grad_scale=1.0,
                    rng=None):
         """One AdamW step over the flat slice `rng` (default: everything). The step counter and

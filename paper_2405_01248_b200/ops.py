@@ -472,6 +472,17 @@ def adamw_dev(param, grad, exp_avg, exp_avg_sq, param_bf16, lr, beta1, beta2, ep
                             grad_scale, _stream()), "dp_adamw_dev", 2)
 
 
+def adamw_advance(step_dev, bc_dev, beta1, beta2):
+    check(_L().dp_adamw_advance(_ptr(step_dev), beta1, beta2, _ptr(bc_dev), _stream()), "dp_adamw_advance")
+
+
+def adamw_apply(param, grad, exp_avg, exp_avg_sq, param_bf16, lr, beta1, beta2, eps, weight_decay, bc_dev,
+                grad_scale=1.0, max_ctas=0, zero_grad=False):
+    check(_L().dp_adamw_apply(_ptr(param), _ptr(grad), _ptr(exp_avg), _ptr(exp_avg_sq), _ptr(param_bf16),
+                              param.numel(), lr, beta1, beta2, eps, weight_decay, _ptr(bc_dev), grad_scale,
+                              max_ctas, int(zero_grad), _stream()), "dp_adamw_apply")
+
+
 _GN_WS = {}
 
 

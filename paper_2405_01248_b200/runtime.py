@@ -184,6 +184,7 @@ class Links:
 
 
 _DEBUG = bool(int(__import__("os").environ.get("DP_DEBUG_P2P", "0")))
+_OVL_SIDE = __import__("os").environ.get("DP_OVL_STREAM", "opt") == "opt"  # experiments: "compute"
 
 
 class _Tracer:
@@ -236,6 +237,7 @@ class _Tracer:
 
 
 class PipelineExecutor:
+    OVERLAP_CTAS = int(__import__("os").environ.get("DP_OVL_CTAS", "296"))  # grid cap of AdamW chunks next to the backward
     def __init__(self, model: TrainModel, programs: dict, *, rank=0, world=1, device="cuda",
                  live_specs=None, frozen_specs=None, loss_scale=1.0, inputs=None):
         """programs: {False: GroupProgram, True: GroupProgram (self-cond activated)} built from
@@ -271,6 +273,11 @@ class PipelineExecutor:
         self._stage_pgs = self._make_stage_groups()
         self.frozen_ready = {}   # for the NEXT iteration: comp -> list[(lo, hi, state)] on stage-0 owners
         self.loss_buf = torch.zeros(1, device=self.device, dtype=torch.float32)
+        # optimizer overlapped with the stage's final backward (the planner's sync task starts
+        # with the final backward, scheduler.py:202-207): layer-group allreduce + AdamW chunks on a
+        # side stream as soon as autograd has finished their gradients (CUDA, NCCL or world 1)
+        self.overlap_sync = self.streams.cuda and not (world > 1 and staged())
+        self.opt_stream = torch.cuda.Stream(device=self.device, priority=0) if self.streams.cuda else None
         self.grad_snapshots = None  # list -> flat grad slices captured before each AdamW
         self.grad_snapshot_pipes = []  # backbone index of each snapshot
         self._frz_sends = []        # in-flight frozen-activation sends (kept alive until deliver)
@@ -456,16 +463,74 @@ class PipelineExecutor:
         return merged
 
     # ---------------------------------------------------------------- backbone
-    def _stage_forward(self, pi, st_in, grad):
+    def _stage_forward(self, pi, st_in, grad, hooks=False):
         lo, hi = self.prog.pipes[pi].stage_ranges[self.stages[pi]]
         bb = self._backbone(pi)
         if grad:
             anchor_ctx = getattr(bb, "grad_context", None)
             ctx = anchor_ctx() if anchor_ctx else contextlib.nullcontext()
             with ctx:
+                if hooks:
+                    return self._run_hooked(pi, bb, st_in, lo, hi)
                 return bb.run(st_in, lo, hi)
         with torch.no_grad():
             return bb.run(st_in, lo, hi)
+
+    # ---------------------------------------------------------------- optimizer overlap
+    def _run_hooked(self, pi, bb, st, lo, hi):
+        """Forward of the stage's LAST micro-batch layer by layer, with a gradient hook on every
+        layer's input hidden state: when autograd completes grad(h_j), layers > j have finished
+        their backward (one layer of lag covers side branches such as the time embedding), so
+        their parameter slice can be reduced and updated while layers <= j still run backward."""
+        self._ovl_top[pi] = hi
+        for j in range(lo, hi):
+            h = st.get("h") if isinstance(st, dict) else None
+            if j > lo and torch.is_tensor(h) and h.requires_grad:
+                h.register_hook(self._layer_hook(pi, j + 1))
+            st = bb.layers[j](st)
+        return st
+
+    def _layer_hook(self, pi, new_top):
+        def hook(_g):
+            self._update_layers(pi, new_top)
+        return hook
+
+    def _update_layers(self, pi, new_top, final=False):
+        """Allreduce + AdamW of the parameter slice of layers [new_top, top) on the optimizer
+        stream, ordered after everything the compute stream has enqueued so far."""
+        top = self._ovl_top.get(pi)
+        if top is None or new_top >= top:
+            return
+        bb = self._backbone(pi)
+        store = bb.store
+        a, b = bb.stage_slice(new_top, top)
+        lo, hi = self.param_ranges[pi]
+        a, b = max(a, lo), min(b, hi)
+        self._ovl_top[pi] = new_top
+        if b <= a and not final:
+            return
+        st = self.opt_stream if _OVL_SIDE else self.streams.compute
+        if st is not self.streams.compute:
+            ev = torch.cuda.Event()
+            ev.record(self.streams.compute)
+            st.wait_event(ev)
+        with torch.cuda.stream(st):
+            if not self._ovl_begun.get(pi):
+                store.adamw_begin(**self.model.adamw)
+                self._ovl_begun[pi] = True
+            if b > a:
+                pg = self._stage_pgs[pi]
+                if pg is not None:
+                    dist.all_reduce(store.grad[a:b], group=pg)
+                # background chunks: one CTA per SM at most (see dp_adamw_apply); the final chunk
+                # at the sync point has the machine to itself
+                store.adamw_apply((a, b), max_ctas=0 if final else self.OVERLAP_CTAS, zero_grad=True,
+                                  **self.model.adamw)
+
+    def _sync_overlapped(self, pi):
+        lo_l, _ = self.prog.pipes[pi].stage_ranges[self.stages[pi]]
+        self._update_layers(pi, lo_l, final=True)
+        self.streams.compute.wait_stream(self.opt_stream)
 
     def _spec(self, pi, boundary):
         return self.live_specs[pi][boundary]
@@ -497,7 +562,8 @@ class PipelineExecutor:
             for k, v in st_in.items():
                 if v.is_floating_point() and spec0.get(k, (0, 0, False))[2]:
                     v.requires_grad_(True)
-        out = self._stage_forward(pi, st_in, grad=not sc_pass)
+        hooks = (not sc_pass and self._ovl_on and self._last_m.get(pi) == m)
+        out = self._stage_forward(pi, st_in, grad=not sc_pass, hooks=hooks)
         if s == S - 1:
             if sc_pass:
                 self._send_feedback(pi, m, out["out"].detach(), lo_r)
@@ -614,6 +680,8 @@ class PipelineExecutor:
 
     # ---------------------------------------------------------------- sync
     def _sync(self, pi):
+        if self._ovl_on and pi in self._ovl_top:
+            return self._sync_overlapped(pi)
         store = self._backbone(pi).store
         lo, hi = self.param_ranges[pi]
         if hasattr(store, "pre_allreduce"):
@@ -655,6 +723,12 @@ class PipelineExecutor:
         store, posted, sent = {}, {}, set()
         self.loss_buf.zero_()
         tr = self.tracer = _Tracer(self.streams, self.dev) if trace else None
+        # optimizer overlap: the micro-batch of each pipe's final backward on this device
+        self._ovl_on = self.overlap_sync and self.grad_snapshots is None and self.streams.cuda
+        self._ovl_top, self._ovl_begun, self._last_m = {}, {}, {}
+        for ins in prog.device_program(self.dev).instrs:
+            if ins[0] == "bwd":
+                self._last_m[ins[3]] = ins[1]
         task = tr.task if tr else (lambda *a, **k: contextlib.nullcontext())
         last_compute_ev = None
         instrs = prog.device_program(self.dev).instrs

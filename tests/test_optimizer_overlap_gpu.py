@@ -1,0 +1,29 @@
+"""The optimizer overlapped with the final backward (layer-group AdamW on a side stream, driven
+by gradient hooks) must match the sequential sync: same kernels and per-element arithmetic, only
+the launch order changes. Run-to-run differences come only from fp32 atomic accumulation order
+(split-K / stream-K), as in the CUDA-graph test."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("cfg,kw", [("c1", {}), ("c2", dict(small=True)), ("c4-small", {})])
+def test_overlapped_optimizer_matches_sequential(cfg, kw):
+    from paper_2405_01248_b200 import engine
+
+    runs = []
+    for overlap in (False, True):
+        tr = engine.Trainer.create(cfg, world=1, rank=0, S=1, M=1, D=1, world_batch=4, **kw)
+        tr.ex.overlap_sync = overlap
+        losses = [tr.step().item() for _ in range(3)]
+        torch.cuda.synchronize()
+        runs.append((losses, [bb.store.master.detach().clone() for bb in tr.model.backbones],
+                     tr.ex._ovl_top))
+    (l0, p0, _), (l1, p1, top1) = runs
+    assert top1, "overlap path did not run"
+    for a, b in zip(l0, l1):
+        assert abs(a - b) <= 1e-3 * abs(b), (l0, l1)
+    for a, b in zip(p0, p1):
+        assert ((a - b).norm() / a.norm()).item() < 1e-3
