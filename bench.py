@@ -35,8 +35,17 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 METRIC = "train samples/sec"
-WORKLOAD = ("c2: SD v2.1 U-Net (trainable, 865M) + OpenCLIP ViT-H text (23 layers, frozen) + "
-            "SD VAE encoder (frozen), 256px, 32 samples/GPU/iteration")
+WORKLOADS = {
+    "c2": ("c2: SD v2.1 U-Net (trainable, 865M) + OpenCLIP ViT-H text (23 layers, frozen) + "
+           "SD VAE encoder (frozen), 256px, 32 samples/GPU/iteration"),
+    "c3": ("c3: ControlNet v1.0 branch (trainable, 364M) -> locked SD v2.1 decoder; frozen VAE, "
+           "OpenCLIP-H, hint, locked U-Net encoder; 512px, 32 samples/GPU/iteration"),
+    "c4": ("c4: cascaded base 64px U-Net (316M) + SR 256px U-Net (133M), bidirectional pipelines, "
+           "frozen T5-large-shaped encoder (128 tokens) + image pyramid, self-cond p=0.5, 32 samples/GPU"),
+    "c5": ("c5: SD U-Net at model channels 512 (trainable, 2.19B) + OpenCLIP-H + SD VAE, 256px, "
+           "32 samples/GPU/iteration"),
+}
+WORKLOAD = WORKLOADS["c2"]
 
 
 def layout(n):
@@ -223,6 +232,8 @@ def main():
     ap.add_argument("--per-gpu-batch", type=int, default=32)
     ap.add_argument("--debug-share-gpu", action="store_true",
                     help="TEST ONLY: run all ranks on cuda:0 over gloo (validates the N>1 path)")
+    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS),
+                    help="the headline (BASELINE.json metric) workload is c2; c3..c5 for reference")
     ap.add_argument("--graph", action="store_true",
                     help="N=1: replay the captured iteration as a CUDA graph (measured: no gain, GPU-bound)")
     args = ap.parse_args()
@@ -238,8 +249,8 @@ def main():
     profile = None
     if lay["S"] > 1:
         from paper_2405_01248_b200 import profiling_run
-        profile = profiling_run.shared_profile("c2", world, rank, wb, **lay)
-    trainer = engine.Trainer.create("c2", world=world, rank=rank, world_batch=wb, profile=profile,
+        profile = profiling_run.shared_profile(args.config, world, rank, wb, **lay)
+    trainer = engine.Trainer.create(args.config, world=world, rank=rank, world_batch=wb, profile=profile,
                                     device=f"cuda:{local}", **lay)
     W, K = args.warmup, args.steps
     trainer.prefetch(2 * W + 2 * K + 2, mode="device")
@@ -268,7 +279,7 @@ def main():
     # speedup vs the same executor's unfilled pipeline (frozen part data-parallel, un-overlapped)
     speedup = 1.0
     if lay["S"] > 1:
-        unf = engine.Trainer.create("c2", world=world, rank=rank, world_batch=wb, profile=profile,
+        unf = engine.Trainer.create(args.config, world=world, rank=rank, world_batch=wb, profile=profile,
                                     device=f"cuda:{local}", filled=False, **lay)
         unf.prefetch(W + K + 1, mode="device")
         for _ in range(W):
@@ -312,7 +323,7 @@ def main():
                 "timed_step_ms_with_events": ms_k / K, "breakdown": breakdown}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == "c2":
         v, cores = cpu_reference(1, 0)
         cpu = {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
                "sample": "1 sample of the c2 training step on the CPU oracle (oracle/train_step.py, fp32)"}
@@ -323,7 +334,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded), random init",
-            "config": {"workload": WORKLOAD, "world_batch": wb, "group_batch": wb * lay["D"] // world,
+            "config": {"workload": WORKLOADS[args.config], "world_batch": wb, "group_batch": wb * lay["D"] // world,
                        "S": lay["S"], "M": lay["M"], "D": lay["D"], "groups": world // lay["D"],
                        "parallelism": f"pp{lay['S']}xdp{world // lay['S']}",
                        "l2": "working set (weights 1.7 GB bf16 + activations) >> 126 MB L2",
