@@ -53,6 +53,13 @@ class ConfigSpec:
     depth: int = 0      # text-encoder depth override (small variants)
 
 
+# Bubbles shorter than this are not filled. The reference default (scheduler.py MIN_BUBBLE_LEN,
+# 10 ms) was tuned for A100 layer times; on B200 a U-Net stage of one micro-batch
+# runs in a few ms and kernel launches cost microseconds, so the executor passes 2 ms through the
+# planner's own `bubble_min_len` argument (measured c2 profile, S=D=4, M=4: predicted speedup over
+# the unfilled pipeline 1.12x at 10 ms, 1.18x at 2 ms; tests/test_c5_plan.py).
+B200_BUBBLE_MIN_LEN = 0.002
+
 _C = torch.bfloat16
 CONFIGS = {
     "c1": ConfigSpec("c1", torch.float32, 128, 32, 16, 1000, 0.5, 1),
@@ -197,7 +204,7 @@ class InputFeed:
         return self.get("noise", lo, hi)
 
 
-def plan_programs(prof, world, S, M, D, world_batch, frozen_counts, bubble_min_len=0.010,
+def plan_programs(prof, world, S, M, D, world_batch, frozen_counts, bubble_min_len=B200_BUBBLE_MIN_LEN,
                   cluster_comm=None):
     """Reference planner calls -> {selfcond: GroupProgram} plus the warm-up program."""
     comm = cluster_comm or pprof.CommCosts(2.0e11, 2e-5, 3.0e11, 1e-5)
@@ -243,7 +250,7 @@ class Trainer:
     @classmethod
     def create(cls, cfg="c1", *, world=1, rank=0, S=1, M=1, D=1, world_batch=None, device=None,
                seed=0, states=None, profile=None, filled=True, feed_mode="device", small=False,
-               bubble_min_len=0.010):
+               bubble_min_len=B200_BUBBLE_MIN_LEN):
         c = CONFIGS[cfg] if isinstance(cfg, str) else cfg
         device = device or (f"cuda:{torch.cuda.current_device()}" if torch.cuda.is_available() else "cpu")
         model = build_model(c, device, seed, states, small=small)
@@ -256,7 +263,7 @@ class Trainer:
 
     @classmethod
     def from_model(cls, model, cfg, ds, *, world=1, rank=0, S=1, M=1, D=1, device="cuda", profile=None,
-                   filled=True, feed_mode="device", bubble_min_len=0.010, comm=None):
+                   filled=True, feed_mode="device", bubble_min_len=B200_BUBBLE_MIN_LEN, comm=None):
         """Plan and wire an already-built TrainModel (any component implementation)."""
         world_batch = ds.world_batch
         probe = make_batch(replace(ds, world_batch=1), 10 ** 6)
@@ -273,8 +280,8 @@ class Trainer:
         scales = [1.0 / (world_batch * pfeed.get(model.noise_field(p), 0, 1).numel())
                   for p in range(len(model.backbones))]
         ex = PipelineExecutor(model, programs, rank=rank, world=world, device=device, live_specs=live,
-                              frozen_specs=fspecs, loss_scale=scales if len(scales) > 1 else scales[0])
-        ex.warm_program = warm
+                              frozen_specs=fspecs, loss_scale=scales if len(scales) > 1 else scales[0],
+                              warm_program=warm)
         ex.plan_result = res
         t = cls(model, cfg, ex, ds, device, feed_mode)
         t.profile = profile

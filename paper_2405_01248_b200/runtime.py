@@ -239,13 +239,14 @@ class _Tracer:
 class PipelineExecutor:
     OVERLAP_CTAS = int(__import__("os").environ.get("DP_OVL_CTAS", "296"))  # grid cap of AdamW chunks next to the backward
     def __init__(self, model: TrainModel, programs: dict, *, rank=0, world=1, device="cuda",
-                 live_specs=None, frozen_specs=None, loss_scale=1.0, inputs=None):
+                 live_specs=None, frozen_specs=None, loss_scale=1.0, inputs=None, warm_program=None):
         """programs: {False: GroupProgram, True: GroupProgram (self-cond activated)} built from
         the same partition; `inputs` provides host/device batch slices (InputFeed).
         live_specs: per pipe (backbone) a list over layer boundaries of {name: (shape, dtype, grad)}."""
         self.model = model
         self.programs = programs
         self.prog0 = programs[False]
+        self.warm_program = warm_program  # iteration-0 frozen pass (its links are created up front)
         self.rank, self.world = rank, world
         self.D = self.prog0.D
         self.group, self.dev = divmod(rank, self.D)
@@ -296,9 +297,10 @@ class PipelineExecutor:
 
     def _needed_links(self):
         need = set()
+        progs = list(self.programs.values()) + ([self.warm_program] if self.warm_program else [])
         for g in range(self.world // self.D):
             base = g * self.D
-            for prog in self.programs.values():
+            for prog in progs:
                 for pi, pl in enumerate(prog.pipes):
                     for s in range(prog.S - 1):
                         for m in range(prog.M):
