@@ -13,6 +13,35 @@ namespace dp {
 
 constexpr int kNumSMs = 148;
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every libdpipe kernel is launched with cudaLaunchAttributeProgrammaticStreamSerialization
+// (launch_k below) and starts with DP_PDL_ENTRY(): the kernel's launch and CTA rasterisation
+// overlap the previous kernel's tail, while `griddepcontrol.wait` still orders every global
+// memory access after the previous grid has completed and flushed; `launch_dependents` then lets
+// the next kernel in the stream begin launching. Non-PDL predecessors (torch kernels, memsets)
+// keep normal stream order.
+#define DP_PDL_ENTRY()                                     \
+  do {                                                      \
+    asm volatile("griddepcontrol.wait;" ::: "memory");     \
+    asm volatile("griddepcontrol.launch_dependents;");     \
+  } while (0)
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                   cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 DP_DEV uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

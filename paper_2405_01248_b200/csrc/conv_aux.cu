@@ -12,6 +12,7 @@ template <typename T>
 __global__ void im2col_kernel(const T* __restrict__ x, T* __restrict__ cols, int N, int H, int W,
                               int C, int R, int S, int stride, int ph, int pw, int P, int Q,
                               int64_t total) {
+  DP_PDL_ENTRY();
   const int64_t ncol = (int64_t)R * S * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -36,6 +37,7 @@ template <typename T>
 __global__ void col2im_kernel(const T* __restrict__ cols, T* __restrict__ dx, int N, int H, int W,
                               int C, int R, int S, int stride, int ph, int pw, int P, int Q,
                               int64_t total) {
+  DP_PDL_ENTRY();
   const int64_t ncol = (int64_t)R * S * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -67,6 +69,7 @@ __global__ void col2im_kernel(const T* __restrict__ cols, T* __restrict__ dx, in
 template <typename T>
 __global__ void flip_kernel(const T* __restrict__ w, T* __restrict__ wt, int K, int R, int S,
                             int C) {
+  DP_PDL_ENTRY();
   const int64_t total = (int64_t)K * R * S * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -88,6 +91,7 @@ __global__ void flip_kernel(const T* __restrict__ w, T* __restrict__ wt, int K, 
 __global__ void __launch_bounds__(256)
     flip_t_kernel(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ wt, int K, int R, int S,
                   int C) {
+  DP_PDL_ENTRY();
   __shared__ __nv_bfloat16 tile[64][64 + 8];
   const int c0 = blockIdx.x * 64, k0 = blockIdx.y * 64, tap = blockIdx.z;
   const int RS = R * S;
@@ -115,6 +119,7 @@ __global__ void __launch_bounds__(256)
 template <typename T>
 __global__ void dilate_kernel(const T* __restrict__ dy, T* __restrict__ out, int N, int P, int Q,
                               int C, int stride) {
+  DP_PDL_ENTRY();
   const int Ho = P * stride, Wo = Q * stride;
   const int64_t total = (int64_t)N * Ho * Wo * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -156,10 +161,10 @@ int dp_im2col(int dtype, const void* x, void* cols, int N, int H, int W, int C, 
   if (total == 0) return 0;
   auto st = reinterpret_cast<cudaStream_t>(stream);
   if (dtype == DP_F32)
-    im2col_kernel<float><<<grid_for(total), 256, 0, st>>>(
+    launch_k(im2col_kernel<float>, dim3(grid_for(total)), dim3(256), 0, st, 
         (const float*)x, (float*)cols, N, H, W, C, R, S, stride, pad_h, pad_w, P, Q, total);
   else
-    im2col_kernel<__nv_bfloat16><<<grid_for(total), 256, 0, st>>>(
+    launch_k(im2col_kernel<__nv_bfloat16>, dim3(grid_for(total)), dim3(256), 0, st, 
         (const __nv_bfloat16*)x, (__nv_bfloat16*)cols, N, H, W, C, R, S, stride, pad_h, pad_w, P,
         Q, total);
   return check("im2col");
@@ -171,10 +176,10 @@ int dp_col2im(int dtype, const void* cols, void* dx, int N, int H, int W, int C,
   if (total == 0) return 0;
   auto st = reinterpret_cast<cudaStream_t>(stream);
   if (dtype == DP_F32)
-    col2im_kernel<float><<<grid_for(total), 256, 0, st>>>(
+    launch_k(col2im_kernel<float>, dim3(grid_for(total)), dim3(256), 0, st, 
         (const float*)cols, (float*)dx, N, H, W, C, R, S, stride, pad_h, pad_w, P, Q, total);
   else
-    col2im_kernel<__nv_bfloat16><<<grid_for(total), 256, 0, st>>>(
+    launch_k(col2im_kernel<__nv_bfloat16>, dim3(grid_for(total)), dim3(256), 0, st, 
         (const __nv_bfloat16*)cols, (__nv_bfloat16*)dx, N, H, W, C, R, S, stride, pad_h, pad_w, P,
         Q, total);
   return check("col2im");
@@ -187,11 +192,11 @@ int dp_conv_weight_flip(int dtype, const void* w, void* wt, int K, int R, int S,
   auto st = reinterpret_cast<cudaStream_t>(stream);
   if (dtype != DP_F32 && K % 8 == 0 && C % 8 == 0) {
     dim3 grid((C + 63) / 64, (K + 63) / 64, R * S);
-    flip_t_kernel<<<grid, 256, 0, st>>>((const __nv_bfloat16*)w, (__nv_bfloat16*)wt, K, R, S, C);
+    launch_k(flip_t_kernel, dim3(grid), dim3(256), 0, st, (const __nv_bfloat16*)w, (__nv_bfloat16*)wt, K, R, S, C);
   } else if (dtype == DP_F32)
-    flip_kernel<float><<<grid_for(total), 256, 0, st>>>((const float*)w, (float*)wt, K, R, S, C);
+    launch_k(flip_kernel<float>, dim3(grid_for(total)), dim3(256), 0, st, (const float*)w, (float*)wt, K, R, S, C);
   else
-    flip_kernel<__nv_bfloat16><<<grid_for(total), 256, 0, st>>>(
+    launch_k(flip_kernel<__nv_bfloat16>, dim3(grid_for(total)), dim3(256), 0, st, 
         (const __nv_bfloat16*)w, (__nv_bfloat16*)wt, K, R, S, C);
   return check("conv_weight_flip");
 }
@@ -202,10 +207,10 @@ int dp_dilate(int dtype, const void* dy, void* out, int N, int P, int Q, int C, 
   if (total == 0) return 0;
   auto st = reinterpret_cast<cudaStream_t>(stream);
   if (dtype == DP_F32)
-    dilate_kernel<float><<<grid_for(total), 256, 0, st>>>((const float*)dy, (float*)out, N, P, Q,
+    launch_k(dilate_kernel<float>, dim3(grid_for(total)), dim3(256), 0, st, (const float*)dy, (float*)out, N, P, Q,
                                                            C, stride);
   else
-    dilate_kernel<__nv_bfloat16><<<grid_for(total), 256, 0, st>>>(
+    launch_k(dilate_kernel<__nv_bfloat16>, dim3(grid_for(total)), dim3(256), 0, st, 
         (const __nv_bfloat16*)dy, (__nv_bfloat16*)out, N, P, Q, C, stride);
   return check("dilate");
 }

@@ -106,6 +106,7 @@ DP_DEV float act_g(int op, float x) {
 
 template <typename T>
 __global__ void act_fwd_kernel(int op, const T* __restrict__ x, T* __restrict__ y, int64_t n) {
+  DP_PDL_ENTRY();
   constexpr int V = VecT<T>::N;
   const int64_t nv = n / V;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
@@ -125,6 +126,7 @@ __global__ void act_fwd_kernel(int op, const T* __restrict__ x, T* __restrict__ 
 template <typename T>
 __global__ void act_bwd_kernel(int op, const T* __restrict__ x, const T* __restrict__ dy,
                                T* __restrict__ dx, int64_t n, int accumulate) {
+  DP_PDL_ENTRY();
   constexpr int V = VecT<T>::N;
   const int64_t nv = n / V;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
@@ -149,6 +151,7 @@ __global__ void act_bwd_kernel(int op, const T* __restrict__ x, const T* __restr
 // x [rows][2F] = [a | g];  y [rows][F] = a * gelu(g)
 template <typename T>
 __global__ void geglu_fwd_kernel(const T* __restrict__ x, T* __restrict__ y, int64_t rows, int F) {
+  DP_PDL_ENTRY();
   const int64_t n = rows * F;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -162,6 +165,7 @@ __global__ void geglu_fwd_kernel(const T* __restrict__ x, T* __restrict__ y, int
 template <typename T>
 __global__ void geglu_bwd_kernel(const T* __restrict__ x, const T* __restrict__ dy,
                                  T* __restrict__ dx, int64_t rows, int F) {
+  DP_PDL_ENTRY();
   const int64_t n = rows * F;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -180,6 +184,7 @@ __global__ void geglu_bwd_kernel(const T* __restrict__ x, const T* __restrict__ 
 template <typename T>
 __global__ void axpby_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ y,
                              int64_t n, float alpha, float beta) {
+  DP_PDL_ENTRY();
   constexpr int V = VecT<T>::N;
   const int64_t nv = n / V;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
@@ -202,6 +207,7 @@ template <typename T>
 __global__ void gate_res_fwd_kernel(const T* __restrict__ x, const T* __restrict__ g, int64_t g_ld,
                                     const T* __restrict__ h, T* __restrict__ y, int64_t rows, int C,
                                     int rps) {
+  DP_PDL_ENTRY();
   const int64_t n = rows * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -216,6 +222,7 @@ template <typename T>
 __global__ void gate_res_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ g, int64_t g_ld,
                                     const T* __restrict__ h, T* __restrict__ dh,
                                     T* __restrict__ dg, int64_t dg_ld, int B, int C, int rps) {
+  DP_PDL_ENTRY();
   const int b = blockIdx.y;
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);
   const int ry = threadIdx.x >> 5;  // 8 row lanes
@@ -247,6 +254,7 @@ __global__ void q_sample_kernel(const T* __restrict__ x0, const T* __restrict__ 
                                 const int64_t* __restrict__ t, const float* __restrict__ sab,
                                 const float* __restrict__ s1mab, T* __restrict__ xt, int64_t n,
                                 int64_t per_sample) {
+  DP_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t ts = t[i / per_sample];
@@ -260,6 +268,7 @@ __global__ void pred_x0_kernel(const T* __restrict__ xt, const T* __restrict__ e
                                const int64_t* __restrict__ t, const float* __restrict__ sab,
                                const float* __restrict__ s1mab, T* __restrict__ out,
                                int64_t n, int64_t per_sample) {
+  DP_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t ts = t[i / per_sample];
@@ -271,6 +280,7 @@ __global__ void pred_x0_kernel(const T* __restrict__ xt, const T* __restrict__ e
 template <typename T>
 __global__ void mse_kernel(const T* __restrict__ p, const T* __restrict__ y, T* __restrict__ dp,
                            float* __restrict__ loss, int64_t n, float scale) {
+  DP_PDL_ENTRY();
   float acc = 0.f;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -294,6 +304,7 @@ __global__ void mse_kernel(const T* __restrict__ p, const T* __restrict__ y, T* 
 template <typename T>
 __global__ void timestep_embed_kernel(const int64_t* __restrict__ t, T* __restrict__ out, int B,
                                       int dim, float max_period) {
+  DP_PDL_ENTRY();
   const int half = dim / 2;
   const int64_t n = (int64_t)B * half;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -312,6 +323,7 @@ template <typename T>
 __global__ void embed_kernel(const int64_t* __restrict__ ids, const T* __restrict__ table,
                              const T* __restrict__ pos, T* __restrict__ out, int64_t rows, int L,
                              int C) {
+  DP_PDL_ENTRY();
   const int64_t n = rows * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -327,6 +339,7 @@ __global__ void embed_kernel(const int64_t* __restrict__ ids, const T* __restric
 template <typename T>
 __global__ void concat_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ dst,
                               int64_t rows, int Ca, int Cb) {
+  DP_PDL_ENTRY();
   const int C = Ca + Cb;
   const int64_t n = rows * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -340,6 +353,7 @@ __global__ void concat_kernel(const T* __restrict__ a, const T* __restrict__ b, 
 template <typename T>
 __global__ void split_kernel(const T* __restrict__ src, T* __restrict__ a, T* __restrict__ b,
                              int64_t rows, int Ca, int Cb, int acc_a, int acc_b) {
+  DP_PDL_ENTRY();
   const int C = Ca + Cb;
   const int64_t n = rows * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -363,6 +377,7 @@ __global__ void split_kernel(const T* __restrict__ src, T* __restrict__ a, T* __
 template <typename T>
 __global__ void upsample2x_kernel(const T* __restrict__ x, T* __restrict__ y, int N, int H, int W,
                                   int C) {
+  DP_PDL_ENTRY();
   const int64_t n = (int64_t)N * 2 * H * 2 * W * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -378,6 +393,7 @@ __global__ void upsample2x_kernel(const T* __restrict__ x, T* __restrict__ y, in
 template <typename T>
 __global__ void upsample2x_bwd_kernel(const T* __restrict__ dy, T* __restrict__ dx, int N, int H,
                                       int W, int C) {
+  DP_PDL_ENTRY();
   const int64_t n = (int64_t)N * H * W * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -396,6 +412,7 @@ __global__ void upsample2x_bwd_kernel(const T* __restrict__ dy, T* __restrict__ 
 
 template <typename TI, typename TO>
 __global__ void cast_kernel(const TI* __restrict__ x, TO* __restrict__ y, int64_t n) {
+  DP_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     y[i] = from_f<TO>(to_f(x[i]));
@@ -408,6 +425,7 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
                              __nv_bfloat16* __restrict__ p_bf16, int64_t n, float lr, float b1,
                              float b2, float eps, float wd, float bc1, float bc2, float gscale,
                              const float* __restrict__ bc_dev, int zero_g) {
+  DP_PDL_ENTRY();
   if (bc_dev) {  // bias corrections of a device-side step counter (CUDA-graph replayable)
     bc1 = bc_dev[0];
     bc2 = bc_dev[1];
@@ -463,6 +481,7 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
 template <typename T>
 __global__ void __launch_bounds__(256) bias_grad_kernel(const T* __restrict__ dy, float* __restrict__ db,
                                                         int64_t rows, int C, int seg) {
+  DP_PDL_ENTRY();
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);
   const int ry = threadIdx.x >> 5;
   const int64_t r0 = (int64_t)blockIdx.y * seg;
@@ -485,6 +504,7 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(const T* __restrict__ dy
 template <typename T>
 __global__ void row_bias_fwd_kernel(const T* __restrict__ x, const T* __restrict__ e, int64_t e_ld,
                                     T* __restrict__ y, int64_t rows, int C, int rps) {
+  DP_PDL_ENTRY();
   constexpr int V = VecT<T>::N;
   const int CV = C / V;
   const int64_t n = rows * CV;
@@ -506,6 +526,7 @@ __global__ void row_bias_fwd_kernel(const T* __restrict__ x, const T* __restrict
 template <typename T>
 __global__ void __launch_bounds__(256) row_bias_bwd_kernel(const T* __restrict__ dy, T* __restrict__ de,
                                                            int64_t de_ld, int C, int rps) {
+  DP_PDL_ENTRY();
   const int b = blockIdx.y;
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);
   const int ry = threadIdx.x >> 5;
@@ -527,6 +548,7 @@ __global__ void __launch_bounds__(256) row_bias_bwd_kernel(const T* __restrict__
 template <typename T>
 __global__ void s2d_kernel(const T* __restrict__ x, T* __restrict__ y, int N, int H, int W, int C,
                            int p, int inverse) {
+  DP_PDL_ENTRY();
   const int64_t n = (int64_t)N * H * W * C;
   const int h = H / p, w = W / p;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -548,6 +570,7 @@ __global__ void s2d_kernel(const T* __restrict__ x, T* __restrict__ y, int N, in
 
 // ++step; bc = (1 - b1^step, 1 - b2^step)   (one thread; precedes adamw_kernel in the stream)
 __global__ void adamw_step_kernel(int* step, float b1, float b2, float* bc) {
+  DP_PDL_ENTRY();
   const int s = ++(*step);
   bc[0] = 1.f - powf(b1, static_cast<float>(s));
   bc[1] = 1.f - powf(b2, static_cast<float>(s));
@@ -557,6 +580,7 @@ __global__ void adamw_step_kernel(int* step, float b1, float b2, float* bc) {
 // x [rows][2F] = [a | g] -> y [rows][F] = a * gelu(g): one vector of V features per thread
 template <typename T>
 __global__ void geglu_fwd_vec_kernel(const T* __restrict__ x, T* __restrict__ y, int64_t rows, int F) {
+  DP_PDL_ENTRY();
   constexpr int V = VecT<T>::N;
   const int FV = F / V;
   const int64_t n = rows * FV;
@@ -575,6 +599,7 @@ __global__ void geglu_fwd_vec_kernel(const T* __restrict__ x, T* __restrict__ y,
 template <typename T>
 __global__ void geglu_bwd_vec_kernel(const T* __restrict__ x, const T* __restrict__ dy,
                                      T* __restrict__ dx, int64_t rows, int F) {
+  DP_PDL_ENTRY();
   constexpr int V = VecT<T>::N;
   const int FV = F / V;
   const int64_t n = rows * FV;
@@ -599,6 +624,7 @@ __global__ void geglu_bwd_vec_kernel(const T* __restrict__ x, const T* __restric
 template <typename T>
 __global__ void concat_vec_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ dst,
                                   int64_t rows, int Ca, int Cb) {
+  DP_PDL_ENTRY();
   constexpr int V = VecT<T>::N;
   const int CVa = Ca / V, CV = (Ca + Cb) / V, CVb = Cb / V;
   const int64_t n = rows * CV;
@@ -618,6 +644,7 @@ __global__ void concat_vec_kernel(const T* __restrict__ a, const T* __restrict__
 template <typename T>
 __global__ void split_vec_kernel(const T* __restrict__ src, T* __restrict__ a, T* __restrict__ b,
                                  int64_t rows, int Ca, int Cb, int acc_a, int acc_b) {
+  DP_PDL_ENTRY();
   constexpr int V = VecT<T>::N;
   const int CVa = Ca / V, CV = (Ca + Cb) / V, CVb = Cb / V;
   const int64_t n = rows * CV;
@@ -652,6 +679,7 @@ __global__ void split_vec_kernel(const T* __restrict__ src, T* __restrict__ a, T
 template <typename T>
 __global__ void __launch_bounds__(256) bias_grad_vec_kernel(const T* __restrict__ dy, float* __restrict__ db,
                                                             int64_t rows, int C, int seg) {
+  DP_PDL_ENTRY();
   constexpr int V = VecT<T>::N;
   const int CV = C / V;
   const int cv = blockIdx.x * 32 + (threadIdx.x & 31);
@@ -739,11 +767,11 @@ int dp_geglu_fwd(int dtype, const void* x, void* y, int64_t rows, int F, dp_stre
   if (rows <= 0) return 0;
   const int V = dtype == DP_F32 ? 4 : 8;
   if (F % V == 0 && aligned16(x) && aligned16(y)) {
-    DISPATCH_T(dtype, geglu_fwd_vec_kernel<T><<<ew_grid(rows * F / V), 256, 0, ST>>>(
+    DISPATCH_T(dtype, launch_k(geglu_fwd_vec_kernel<T>, dim3(ew_grid(rows * F / V)), dim3(256), 0, ST, 
                           cp<T>(x), mp<T>(y), rows, F));
     return ew_check("geglu_fwd");
   }
-  DISPATCH_T(dtype, geglu_fwd_kernel<T><<<ew_grid(rows * F), 256, 0, ST>>>(cp<T>(x), mp<T>(y),
+  DISPATCH_T(dtype, launch_k(geglu_fwd_kernel<T>, dim3(ew_grid(rows * F)), dim3(256), 0, ST, cp<T>(x), mp<T>(y),
                                                                              rows, F));
   return ew_check("geglu_fwd");
 }
@@ -753,11 +781,11 @@ int dp_geglu_bwd(int dtype, const void* x, const void* dy, void* dx, int64_t row
   if (rows <= 0) return 0;
   const int V = dtype == DP_F32 ? 4 : 8;
   if (F % V == 0 && aligned16(x) && aligned16(dy) && aligned16(dx)) {
-    DISPATCH_T(dtype, geglu_bwd_vec_kernel<T><<<ew_grid(rows * F / V), 256, 0, ST>>>(
+    DISPATCH_T(dtype, launch_k(geglu_bwd_vec_kernel<T>, dim3(ew_grid(rows * F / V)), dim3(256), 0, ST, 
                           cp<T>(x), cp<T>(dy), mp<T>(dx), rows, F));
     return ew_check("geglu_bwd");
   }
-  DISPATCH_T(dtype, geglu_bwd_kernel<T><<<ew_grid(rows * F), 256, 0, ST>>>(
+  DISPATCH_T(dtype, launch_k(geglu_bwd_kernel<T>, dim3(ew_grid(rows * F)), dim3(256), 0, ST, 
                         cp<T>(x), cp<T>(dy), mp<T>(dx), rows, F));
   return ew_check("geglu_bwd");
 }
@@ -777,7 +805,7 @@ int dp_axpby(int dtype, const void* a, const void* b, void* y, int64_t n, float 
 int dp_gate_residual_fwd(int dtype, const void* x, const void* g, int64_t g_ld, const void* h,
                          void* y, int64_t rows, int C, int rows_per_sample, dp_stream_t stream) {
   if (rows <= 0) return 0;
-  DISPATCH_T(dtype, gate_res_fwd_kernel<T><<<ew_grid(rows * C), 256, 0, ST>>>(
+  DISPATCH_T(dtype, launch_k(gate_res_fwd_kernel<T>, dim3(ew_grid(rows * C)), dim3(256), 0, ST, 
                         cp<T>(x), cp<T>(g), g_ld, cp<T>(h), mp<T>(y), rows, C, rows_per_sample));
   return ew_check("gate_residual_fwd");
 }
@@ -787,7 +815,7 @@ int dp_gate_residual_bwd(int dtype, const void* dy, const void* g, int64_t g_ld,
                          dp_stream_t stream) {
   if (B <= 0) return 0;
   dim3 grid((C + 31) / 32, B);
-  DISPATCH_T(dtype, gate_res_bwd_kernel<T><<<grid, 256, 0, ST>>>(
+  DISPATCH_T(dtype, launch_k(gate_res_bwd_kernel<T>, dim3(grid), dim3(256), 0, ST, 
                         cp<T>(dy), cp<T>(g), g_ld, cp<T>(h), mp<T>(dh), mp<T>(dg), dg_ld, B, C,
                         rows_per_sample));
   return ew_check("gate_residual_bwd");
@@ -797,7 +825,7 @@ int dp_q_sample(int dtype, const void* x0, const void* noise, const int64_t* t,
                 const float* sqrt_ab, const float* sqrt_1mab, void* xt, int64_t n,
                 int64_t per_sample, dp_stream_t stream) {
   if (n <= 0) return 0;
-  DISPATCH_T(dtype, q_sample_kernel<T><<<ew_grid(n), 256, 0, ST>>>(
+  DISPATCH_T(dtype, launch_k(q_sample_kernel<T>, dim3(ew_grid(n)), dim3(256), 0, ST, 
                         cp<T>(x0), cp<T>(noise), t, sqrt_ab, sqrt_1mab, mp<T>(xt), n, per_sample));
   return ew_check("q_sample");
 }
@@ -806,7 +834,7 @@ int dp_pred_x0(int dtype, const void* xt, const void* eps, const int64_t* t, con
                const float* sqrt_1mab, void* out, int64_t n, int64_t per_sample,
                dp_stream_t stream) {
   if (n <= 0) return 0;
-  DISPATCH_T(dtype, pred_x0_kernel<T><<<ew_grid(n), 256, 0, ST>>>(
+  DISPATCH_T(dtype, launch_k(pred_x0_kernel<T>, dim3(ew_grid(n)), dim3(256), 0, ST, 
                         cp<T>(xt), cp<T>(eps), t, sqrt_ab, sqrt_1mab, mp<T>(out), n, per_sample));
   return ew_check("pred_x0");
 }
@@ -814,7 +842,7 @@ int dp_pred_x0(int dtype, const void* xt, const void* eps, const int64_t* t, con
 int dp_mse(int dtype, const void* pred, const void* target, void* dpred, float* loss_acc,
            int64_t n, float scale, dp_stream_t stream) {
   if (n <= 0) return 0;
-  DISPATCH_T(dtype, mse_kernel<T><<<ew_grid(n), 256, 0, ST>>>(cp<T>(pred), cp<T>(target),
+  DISPATCH_T(dtype, launch_k(mse_kernel<T>, dim3(ew_grid(n)), dim3(256), 0, ST, cp<T>(pred), cp<T>(target),
                                                                 mp<T>(dpred), loss_acc, n, scale));
   return ew_check("mse");
 }
@@ -822,7 +850,7 @@ int dp_mse(int dtype, const void* pred, const void* target, void* dpred, float* 
 int dp_timestep_embed(int dtype, const int64_t* t, void* out, int B, int dim, float max_period,
                       dp_stream_t stream) {
   if (B <= 0) return 0;
-  DISPATCH_T(dtype, timestep_embed_kernel<T><<<ew_grid((int64_t)B * dim / 2), 256, 0, ST>>>(
+  DISPATCH_T(dtype, launch_k(timestep_embed_kernel<T>, dim3(ew_grid((int64_t)B * dim / 2)), dim3(256), 0, ST, 
                         t, mp<T>(out), B, dim, max_period));
   return ew_check("timestep_embed");
 }
@@ -830,7 +858,7 @@ int dp_timestep_embed(int dtype, const int64_t* t, void* out, int B, int dim, fl
 int dp_embed(int dtype, const int64_t* ids, const void* table, const void* pos, void* out,
              int64_t rows, int L, int C, dp_stream_t stream) {
   if (rows <= 0) return 0;
-  DISPATCH_T(dtype, embed_kernel<T><<<ew_grid(rows * C), 256, 0, ST>>>(
+  DISPATCH_T(dtype, launch_k(embed_kernel<T>, dim3(ew_grid(rows * C)), dim3(256), 0, ST, 
                         ids, cp<T>(table), cp<T>(pos), mp<T>(out), rows, L, C));
   return ew_check("embed");
 }
@@ -840,11 +868,11 @@ int dp_concat(int dtype, const void* a, const void* b, void* dst, int64_t rows, 
   if (rows <= 0) return 0;
   const int V = dtype == DP_F32 ? 4 : 8;
   if (Ca % V == 0 && Cb % V == 0 && aligned16(a) && aligned16(dst) && (!b || aligned16(b))) {
-    DISPATCH_T(dtype, concat_vec_kernel<T><<<ew_grid(rows * (Ca + Cb) / V), 256, 0, ST>>>(
+    DISPATCH_T(dtype, launch_k(concat_vec_kernel<T>, dim3(ew_grid(rows * (Ca + Cb) / V)), dim3(256), 0, ST, 
                           cp<T>(a), cp<T>(b), mp<T>(dst), rows, Ca, Cb));
     return ew_check("concat");
   }
-  DISPATCH_T(dtype, concat_kernel<T><<<ew_grid(rows * (Ca + Cb)), 256, 0, ST>>>(
+  DISPATCH_T(dtype, launch_k(concat_kernel<T>, dim3(ew_grid(rows * (Ca + Cb))), dim3(256), 0, ST, 
                         cp<T>(a), cp<T>(b), mp<T>(dst), rows, Ca, Cb));
   return ew_check("concat");
 }
@@ -854,11 +882,11 @@ int dp_split(int dtype, const void* src, void* a, void* b, int64_t rows, int Ca,
   if (rows <= 0) return 0;
   const int V = dtype == DP_F32 ? 4 : 8;
   if (Ca % V == 0 && Cb % V == 0 && aligned16(src) && (!a || aligned16(a)) && (!b || aligned16(b))) {
-    DISPATCH_T(dtype, split_vec_kernel<T><<<ew_grid(rows * (Ca + Cb) / V), 256, 0, ST>>>(
+    DISPATCH_T(dtype, launch_k(split_vec_kernel<T>, dim3(ew_grid(rows * (Ca + Cb) / V)), dim3(256), 0, ST, 
                           cp<T>(src), mp<T>(a), mp<T>(b), rows, Ca, Cb, acc_a, acc_b));
     return ew_check("split");
   }
-  DISPATCH_T(dtype, split_kernel<T><<<ew_grid(rows * (Ca + Cb)), 256, 0, ST>>>(
+  DISPATCH_T(dtype, launch_k(split_kernel<T>, dim3(ew_grid(rows * (Ca + Cb))), dim3(256), 0, ST, 
                         cp<T>(src), mp<T>(a), mp<T>(b), rows, Ca, Cb, acc_a, acc_b));
   return ew_check("split");
 }
@@ -866,7 +894,7 @@ int dp_split(int dtype, const void* src, void* a, void* b, int64_t rows, int Ca,
 int dp_upsample2x(int dtype, const void* x, void* y, int N, int H, int W, int C,
                   dp_stream_t stream) {
   if (N <= 0) return 0;
-  DISPATCH_T(dtype, upsample2x_kernel<T><<<ew_grid((int64_t)N * 4 * H * W * C), 256, 0, ST>>>(
+  DISPATCH_T(dtype, launch_k(upsample2x_kernel<T>, dim3(ew_grid((int64_t)N * 4 * H * W * C)), dim3(256), 0, ST, 
                         cp<T>(x), mp<T>(y), N, H, W, C));
   return ew_check("upsample2x");
 }
@@ -874,7 +902,7 @@ int dp_upsample2x(int dtype, const void* x, void* y, int N, int H, int W, int C,
 int dp_upsample2x_bwd(int dtype, const void* dy, void* dx, int N, int H, int W, int C,
                       dp_stream_t stream) {
   if (N <= 0) return 0;
-  DISPATCH_T(dtype, upsample2x_bwd_kernel<T><<<ew_grid((int64_t)N * H * W * C), 256, 0, ST>>>(
+  DISPATCH_T(dtype, launch_k(upsample2x_bwd_kernel<T>, dim3(ew_grid((int64_t)N * H * W * C)), dim3(256), 0, ST, 
                         cp<T>(dy), mp<T>(dx), N, H, W, C));
   return ew_check("upsample2x_bwd");
 }
@@ -883,13 +911,13 @@ int dp_cast(int src_dtype, int dst_dtype, const void* x, void* y, int64_t n, dp_
   if (n <= 0) return 0;
   const int g = ew_grid(n);
   if (src_dtype == DP_F32 && dst_dtype == DP_BF16)
-    cast_kernel<float, __nv_bfloat16><<<g, 256, 0, ST>>>(cp<float>(x), mp<__nv_bfloat16>(y), n);
+    launch_k(cast_kernel<float, __nv_bfloat16>, dim3(g), dim3(256), 0, ST, cp<float>(x), mp<__nv_bfloat16>(y), n);
   else if (src_dtype == DP_BF16 && dst_dtype == DP_F32)
-    cast_kernel<__nv_bfloat16, float><<<g, 256, 0, ST>>>(cp<__nv_bfloat16>(x), mp<float>(y), n);
+    launch_k(cast_kernel<__nv_bfloat16, float>, dim3(g), dim3(256), 0, ST, cp<__nv_bfloat16>(x), mp<float>(y), n);
   else if (src_dtype == DP_F32)
-    cast_kernel<float, float><<<g, 256, 0, ST>>>(cp<float>(x), mp<float>(y), n);
+    launch_k(cast_kernel<float, float>, dim3(g), dim3(256), 0, ST, cp<float>(x), mp<float>(y), n);
   else
-    cast_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, ST>>>(cp<__nv_bfloat16>(x),
+    launch_k(cast_kernel<__nv_bfloat16, __nv_bfloat16>, dim3(g), dim3(256), 0, ST, cp<__nv_bfloat16>(x),
                                                                   mp<__nv_bfloat16>(y), n);
   return ew_check("cast");
 }
@@ -902,7 +930,7 @@ int dp_row_bias_fwd(int dtype, const void* x, const void* e, int64_t e_ld, void*
     set_error("dp_row_bias_fwd: C must be a multiple of the vector width and x/y 16-byte aligned");
     return DP_ERR_ARGS;
   }
-  DISPATCH_T(dtype, row_bias_fwd_kernel<T><<<ew_grid(rows * C / V), 256, 0, ST>>>(
+  DISPATCH_T(dtype, launch_k(row_bias_fwd_kernel<T>, dim3(ew_grid(rows * C / V)), dim3(256), 0, ST, 
                         cp<T>(x), cp<T>(e), e_ld, mp<T>(y), rows, C, rows_per_sample));
   return ew_check("row_bias_fwd");
 }
@@ -911,7 +939,7 @@ int dp_row_bias_bwd(int dtype, const void* dy, void* de, int64_t de_ld, int B, i
                     int rows_per_sample, dp_stream_t stream) {
   if (B <= 0) return 0;
   dim3 grid((C + 31) / 32, B);
-  DISPATCH_T(dtype, row_bias_bwd_kernel<T><<<grid, 256, 0, ST>>>(cp<T>(dy), mp<T>(de), de_ld, C,
+  DISPATCH_T(dtype, launch_k(row_bias_bwd_kernel<T>, dim3(grid), dim3(256), 0, ST, cp<T>(dy), mp<T>(de), de_ld, C,
                                                                    rows_per_sample));
   return ew_check("row_bias_bwd");
 }
@@ -923,7 +951,7 @@ int dp_space_to_depth(int dtype, const void* x, void* y, int N, int H, int W, in
     set_error("dp_space_to_depth: H and W must be multiples of p");
     return DP_ERR_ARGS;
   }
-  DISPATCH_T(dtype, s2d_kernel<T><<<ew_grid((int64_t)N * H * W * C), 256, 0, ST>>>(
+  DISPATCH_T(dtype, launch_k(s2d_kernel<T>, dim3(ew_grid((int64_t)N * H * W * C)), dim3(256), 0, ST, 
                         cp<T>(x), mp<T>(y), N, H, W, C, p, inverse));
   return ew_check("space_to_depth");
 }
@@ -937,13 +965,13 @@ int dp_bias_grad(int dtype, const void* dy, float* db, int64_t rows, int C, dp_s
     int64_t seg = (rows * ((CV + 31) / 32) + 2 * kNumSMs - 1) / (2 * kNumSMs);  // ~2 waves
     seg = seg < 64 ? 64 : seg;
     dim3 grid((CV + 31) / 32, static_cast<unsigned>((rows + seg - 1) / seg));
-    DISPATCH_T(dtype, bias_grad_vec_kernel<T><<<grid, 256, 0, ST>>>(cp<T>(dy), db, rows, C,
+    DISPATCH_T(dtype, launch_k(bias_grad_vec_kernel<T>, dim3(grid), dim3(256), 0, ST, cp<T>(dy), db, rows, C,
                                                                       static_cast<int>(seg)));
     return ew_check("bias_grad");
   }
   const int seg = 512;
   dim3 grid((C + 31) / 32, static_cast<unsigned>((rows + seg - 1) / seg));
-  DISPATCH_T(dtype, bias_grad_kernel<T><<<grid, 256, 0, ST>>>(cp<T>(dy), db, rows, C, seg));
+  DISPATCH_T(dtype, launch_k(bias_grad_kernel<T>, dim3(grid), dim3(256), 0, ST, cp<T>(dy), db, rows, C, seg));
   return ew_check("bias_grad");
 }
 
@@ -957,7 +985,7 @@ int dp_adamw(float* param, const float* grad, float* exp_avg, float* exp_avg_sq,
   }
   const float bc1 = 1.f - powf(beta1, static_cast<float>(step));
   const float bc2 = 1.f - powf(beta2, static_cast<float>(step));
-  adamw_kernel<<<ew_grid(n / 4 + 1), 256, 0, ST>>>(param, grad, exp_avg, exp_avg_sq,
+  launch_k(adamw_kernel, dim3(ew_grid(n / 4 + 1)), dim3(256), 0, ST, param, grad, exp_avg, exp_avg_sq,
                                                     mp<__nv_bfloat16>(param_bf16), n, lr, beta1,
                                                     beta2, eps, weight_decay, bc1, bc2,
                                                     grad_scale, nullptr, 0);
@@ -967,7 +995,7 @@ int dp_adamw(float* param, const float* grad, float* exp_avg, float* exp_avg_sq,
 // Chunked AdamW (optimizer overlapped with the backward pass): advance the device step counter
 // and bias corrections once per iteration, then update any number of flat slices with them.
 int dp_adamw_advance(int* step_dev, float beta1, float beta2, float* bc_dev, dp_stream_t stream) {
-  adamw_step_kernel<<<1, 1, 0, ST>>>(step_dev, beta1, beta2, bc_dev);
+  launch_k(adamw_step_kernel, dim3(1), dim3(1), 0, ST, step_dev, beta1, beta2, bc_dev);
   return ew_check("adamw_advance");
 }
 
@@ -984,7 +1012,7 @@ int dp_adamw_apply(float* param, const float* grad, float* exp_avg, float* exp_a
   // backward pass must leave thread slots for the persistent GEMM CTAs on every SM
   int grid = ew_grid(n / 4 + 1);
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  adamw_kernel<<<grid, 256, 0, ST>>>(param, grad, exp_avg, exp_avg_sq,
+  launch_k(adamw_kernel, dim3(grid), dim3(256), 0, ST, param, grad, exp_avg, exp_avg_sq,
                                                     mp<__nv_bfloat16>(param_bf16), n, lr, beta1,
                                                     beta2, eps, weight_decay, 1.f, 1.f, grad_scale,
                                                     bc_dev, zero_grad);
@@ -1000,8 +1028,8 @@ int dp_adamw_dev(float* param, const float* grad, float* exp_avg, float* exp_avg
     set_error("dp_adamw_dev: flat buffers must be 16-byte aligned");
     return DP_ERR_ARGS;
   }
-  adamw_step_kernel<<<1, 1, 0, ST>>>(step_dev, beta1, beta2, bc_dev);
-  adamw_kernel<<<ew_grid(n / 4 + 1), 256, 0, ST>>>(param, grad, exp_avg, exp_avg_sq,
+  launch_k(adamw_step_kernel, dim3(1), dim3(1), 0, ST, step_dev, beta1, beta2, bc_dev);
+  launch_k(adamw_kernel, dim3(ew_grid(n / 4 + 1)), dim3(256), 0, ST, param, grad, exp_avg, exp_avg_sq,
                                                     mp<__nv_bfloat16>(param_bf16), n, lr, beta1,
                                                     beta2, eps, weight_decay, 1.f, 1.f, grad_scale,
                                                     bc_dev, 0);

@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(128, 2)
     fa_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                   const Params p) {
+  DP_PDL_ENTRY();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -236,6 +237,7 @@ constexpr size_t SMEM = 1024 + 6 * TILE_BYTES + 64;
 __global__ void fa_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
                                    float* __restrict__ Dv, int B, int N, int heads, int64_t o_ld,
                                    int64_t do_ld) {
+  DP_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t r = blockIdx.x * 8LL + (threadIdx.x >> 5);  // (b, h, n) flattened
   const int64_t total = (int64_t)B * heads * N;
@@ -256,6 +258,7 @@ __global__ void fa_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __
 // out[b][n][h*64+d] (bf16, token stride out_ld) = alpha * acc[b][n][h][d] (fp32, dense)
 __global__ void fa_dq_cast_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ out,
                                   int64_t rows, int C, int64_t out_ld, float alpha) {
+  DP_PDL_ENTRY();
   const int64_t n = rows * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n / 2;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -287,6 +290,7 @@ __global__ void __launch_bounds__(128, 1)
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                   const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmDV,
                   const BwdParams p) {
+  DP_PDL_ENTRY();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -605,11 +609,11 @@ extern "C" int dp_flash_attn_bwd(const DpAttnArgs* a, const void* dout, int64_t 
   }
   fa::BwdParams p{a->N, a->Nk, a->heads, a->scale * 1.4426950408889634f, a->scale, a->lse, Dv, dq_acc};
   dim3 grid((a->Nk + fa::BKV - 1) / fa::BKV, a->heads, a->B);
-  fa::fa_bwd_kernel<<<grid, 128, fa::BWD_SMEM, st>>>(mq, mk, mv, mdo, mdk, mdv, p);
+  launch_k(fa::fa_bwd_kernel, dim3(grid), dim3(128), fa::BWD_SMEM, st, mq, mk, mv, mdo, mdk, mdv, p);
   const int64_t n2 = rows * C / 2;
   int g = static_cast<int>((n2 + 255) / 256);
   if (g > 148 * 8) g = 148 * 8;
-  fa::fa_dq_cast_kernel<<<g, 256, 0, st>>>(dq_acc, reinterpret_cast<__nv_bfloat16*>(dq), rows, C, dq_ld,
+  launch_k(fa::fa_dq_cast_kernel, dim3(g), dim3(256), 0, st, dq_acc, reinterpret_cast<__nv_bfloat16*>(dq), rows, C, dq_ld,
                                            a->scale);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -326,6 +326,10 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: everything above (barrier init, TMEM allocation, descriptor
+  // prefetch) overlaps the tail of the previous kernel in the stream; no global memory is read
+  // or written before the previous grid has completed and flushed.
+  DP_PDL_ENTRY();
 
   if (threadIdx.x == 0) {
     // ------------------------------------------------------------ TMA producer (every CTA)
@@ -601,6 +605,14 @@ static int make_map(CUtensorMap* map, const void* base, const uint64_t dims[4],
   return 0;
 }
 
+static bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DP_PDL");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return on;
+}
+
 template <int BN, int CG>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
                      TcParams p, int max_ctas, cudaStream_t st) {
@@ -626,13 +638,15 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, CG>, ma, mb, md, p);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -727,6 +741,7 @@ __global__ void __launch_bounds__(256)
                          int64_t d_bs1, int64_t d_bs2, const float* __restrict__ bias,
                          const __nv_bfloat16* __restrict__ R, int64_t r_ld, int64_t r_bs1,
                          int64_t r_bs2, int M, int N, int batch1, int64_t total) {
+  DP_PDL_ENTRY();
   const int nv = N / 8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -799,7 +814,7 @@ static int launch_bn(int bn, int cg, const CUtensorMap& ma, const CUtensorMap& m
     const int64_t total = (int64_t)p.nbatch * M * (N / 8);
     const int64_t want = (total + 255) / 256;
     const int grid = static_cast<int>(want < 8 * kNumSMs ? want : 8 * kNumSMs);
-    splitk_finish_kernel<<<grid, 256, 0, st>>>(ws, reinterpret_cast<__nv_bfloat16*>(p.D), p.d_ld, p.d_bs1,
+    launch_k(splitk_finish_kernel, dim3(grid), dim3(256), 0, st, ws, reinterpret_cast<__nv_bfloat16*>(p.D), p.d_ld, p.d_bs1,
                                                p.d_bs2, p.bias, reinterpret_cast<const __nv_bfloat16*>(p.R),
                                                p.r_ld, p.r_bs1, p.r_bs2, M, N, b1, total);
     e = cudaGetLastError();
@@ -1126,6 +1141,7 @@ int tc_conv_wgrad(const DpConvArgs* a, cudaStream_t st) {
 // Arbitrary strides on both operands (any major), batch, epilogue identical to the TC path.
 template <typename TI>
 __global__ void __launch_bounds__(256) simt_gemm_kernel(DpGemmArgs a) {
+  DP_PDL_ENTRY();
   __shared__ float As[16][64 + 4];
   __shared__ float Bs[16][64 + 4];
   const int z = blockIdx.z;
@@ -1202,9 +1218,9 @@ int simt_gemm(const DpGemmArgs* in, cudaStream_t st) {
   if (a.batch2 <= 0) a.batch2 = 1;
   dim3 grid((a.N + 63) / 64, (a.M + 63) / 64, a.batch1 * a.batch2);
   if (a.dtype == DP_F32)
-    simt_gemm_kernel<float><<<grid, 256, 0, st>>>(a);
+    launch_k(simt_gemm_kernel<float>, dim3(grid), dim3(256), 0, st, a);
   else
-    simt_gemm_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(a);
+    launch_k(simt_gemm_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, st, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) set_error(std::string("simt_gemm: ") + cudaGetErrorString(e));
   return e;

@@ -145,6 +145,7 @@ template <typename T>
 __global__ void __launch_bounds__(GN_THREADS)
     gn_partial_kernel(const T* __restrict__ x, int HW, int C, int G, int ppc, int CB,
                       float* __restrict__ part) {
+  DP_PDL_ENTRY();
   constexpr int V = NV<T>::V;
   const int n = blockIdx.y, chunk = blockIdx.x, nchunks = gridDim.x;
   const int c0 = blockIdx.z * CB;  // first channel of this block
@@ -238,6 +239,7 @@ __global__ void __launch_bounds__(GN_THREADS, 4)
                     float* __restrict__ mean_out, float* __restrict__ rstd_out,
                     const float* __restrict__ part, int HW, int C, int G, int ppc, int CB, float eps,
                     int silu_on) {
+  DP_PDL_ENTRY();
   constexpr int V = NV<T>::V;
   const int n = blockIdx.y, chunk = blockIdx.x, nchunks = gridDim.x;
   const int c0 = blockIdx.z * CB;
@@ -326,6 +328,7 @@ __global__ void __launch_bounds__(GN_THREADS)
                           const float* __restrict__ mean, const float* __restrict__ rstd, int HW,
                           int C, int G, int ppc, int CB, int silu_on, float* __restrict__ dgamma,
                           float* __restrict__ dbeta, float* __restrict__ part) {
+  DP_PDL_ENTRY();
   constexpr int V = NV<T>::V;
   const int n = blockIdx.y, chunk = blockIdx.x, nchunks = gridDim.x;
   const int c0 = blockIdx.z * CB;
@@ -418,6 +421,7 @@ __global__ void __launch_bounds__(GN_THREADS)
                         const float* __restrict__ mean, const float* __restrict__ rstd,
                         const float* __restrict__ part, int HW, int C, int G, int ppc, int CB,
                         int silu_on, T* __restrict__ dx, int accumulate) {
+  DP_PDL_ENTRY();
   constexpr int V = NV<T>::V;
   const int n = blockIdx.y, chunk = blockIdx.x, nchunks = gridDim.x;
   const int c0 = blockIdx.z * CB;
@@ -495,6 +499,7 @@ template <typename T, int NVEC>
 __global__ void __launch_bounds__(256)
     rms_fwd_kernel(const T* __restrict__ x, const float* __restrict__ gamma, T* __restrict__ y,
                    int64_t rows, int C, float eps) {
+  DP_PDL_ENTRY();
   constexpr int V = NV<T>::V;
   const int lane = threadIdx.x & 31;
   const int64_t row = blockIdx.x * 8LL + (threadIdx.x >> 5);
@@ -536,6 +541,7 @@ __global__ void __launch_bounds__(256)
                   int64_t mod_ld, int shift_off, int scale_off, int rps, T* __restrict__ y,
                   float* __restrict__ mean_out, float* __restrict__ rstd_out, int64_t rows, int C,
                   float eps) {
+  DP_PDL_ENTRY();
   constexpr int V = NV<T>::V;
   const int lane = threadIdx.x & 31;
   const int64_t row = blockIdx.x * 8LL + (threadIdx.x >> 5);
@@ -604,6 +610,7 @@ __global__ void __launch_bounds__(256)
                   int scale_off, int rps, const float* __restrict__ mean,
                   const float* __restrict__ rstd, T* __restrict__ dx, int64_t rows, int C,
                   int accumulate, float* __restrict__ dgamma, float* __restrict__ dbeta) {
+  DP_PDL_ENTRY();
   constexpr int V = NV<T>::V;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -695,6 +702,7 @@ __global__ void __launch_bounds__(256)
                          int64_t rows, int C, int rows_per_seg, float* __restrict__ dgamma,
                          float* __restrict__ dbeta, T* __restrict__ dmod, int64_t dmod_ld,
                          int shift_off, int scale_off) {
+  DP_PDL_ENTRY();
   // 16-byte vectors: a block covers 32 channel vectors x 8 row lanes of one row segment
   constexpr int V = NV<T>::V;
   const int CV = C / V;
@@ -751,6 +759,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
     softmax_fwd_kernel(const float* __restrict__ S, T* __restrict__ P, int64_t rows, int cols,
                        int ld, float scale, int causal, int Lq) {
+  DP_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t row = blockIdx.x * 8LL + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -772,6 +781,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
     softmax_bwd_kernel(const T* __restrict__ P, const float* __restrict__ dP, T* __restrict__ dS,
                        int64_t rows, int cols, int ld, float scale) {
+  DP_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t row = blockIdx.x * 8LL + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -843,9 +853,9 @@ int dp_group_norm_fwd(int dtype, const void* x, const float* gamma, const float*
   if (int e = gn_validate(dtype, C, G)) return e;
   const GnGeom g = gn_geom_rt(dtype, N, HW, C, G);
   dim3 grid(g.chunks, N, g.nblk);
-  DISPATCH_T(dtype, gn_partial_kernel<T><<<grid, GN_THREADS, 0, ST>>>(cp<T>(x), HW, C, G, g.ppc, g.CB,
+  DISPATCH_T(dtype, launch_k(gn_partial_kernel<T>, dim3(grid), dim3(GN_THREADS), 0, ST, cp<T>(x), HW, C, G, g.ppc, g.CB,
                                                                         workspace));
-  DISPATCH_T(dtype, gn_apply_kernel<T><<<grid, GN_THREADS, 0, ST>>>(
+  DISPATCH_T(dtype, launch_k(gn_apply_kernel<T>, dim3(grid), dim3(GN_THREADS), 0, ST, 
                         cp<T>(x), gamma, beta, mp<T>(y), mean, rstd, workspace, HW, C, G, g.ppc, g.CB,
                         eps, silu));
   return ew_check("group_norm_fwd");
@@ -859,10 +869,10 @@ int dp_group_norm_bwd(int dtype, const void* x, const void* dy, const float* gam
   if (int e = gn_validate(dtype, C, G)) return e;
   const GnGeom g = gn_geom_rt(dtype, N, HW, C, G);
   dim3 grid(g.chunks, N, g.nblk);
-  DISPATCH_T(dtype, gn_bwd_partial_kernel<T><<<grid, GN_THREADS, 0, ST>>>(
+  DISPATCH_T(dtype, launch_k(gn_bwd_partial_kernel<T>, dim3(grid), dim3(GN_THREADS), 0, ST, 
                         cp<T>(x), cp<T>(dy), gamma, beta, mean, rstd, HW, C, G, g.ppc, g.CB, silu,
                         dgamma, dbeta, workspace));
-  DISPATCH_T(dtype, gn_bwd_apply_kernel<T><<<grid, GN_THREADS, 0, ST>>>(
+  DISPATCH_T(dtype, launch_k(gn_bwd_apply_kernel<T>, dim3(grid), dim3(GN_THREADS), 0, ST, 
                         cp<T>(x), cp<T>(dy), gamma, beta, mean, rstd, workspace, HW, C, G, g.ppc, g.CB,
                         silu, mp<T>(dx), accumulate));
   return ew_check("group_norm_bwd");
@@ -872,15 +882,15 @@ int dp_group_norm_bwd(int dtype, const void* x, const void* dy, const float* gam
   do {                                                                                \
     const int nvec = ((C) / NV<T>::V + 31) / 32;                                      \
     if (nvec <= 1) {                                                                  \
-      KERNEL<T, 1><<<grid, 256, 0, ST>>>(__VA_ARGS__);                                \
+      launch_k(KERNEL<T, 1>, dim3(grid), dim3(256), 0, ST, __VA_ARGS__);                                \
     } else if (nvec <= 2) {                                                           \
-      KERNEL<T, 2><<<grid, 256, 0, ST>>>(__VA_ARGS__);                                \
+      launch_k(KERNEL<T, 2>, dim3(grid), dim3(256), 0, ST, __VA_ARGS__);                                \
     } else if (nvec <= 4) {                                                           \
-      KERNEL<T, 4><<<grid, 256, 0, ST>>>(__VA_ARGS__);                                \
+      launch_k(KERNEL<T, 4>, dim3(grid), dim3(256), 0, ST, __VA_ARGS__);                                \
     } else if (nvec <= 8) {                                                           \
-      KERNEL<T, 8><<<grid, 256, 0, ST>>>(__VA_ARGS__);                                \
+      launch_k(KERNEL<T, 8>, dim3(grid), dim3(256), 0, ST, __VA_ARGS__);                                \
     } else {                                                                          \
-      KERNEL<T, 16><<<grid, 256, 0, ST>>>(__VA_ARGS__);                               \
+      launch_k(KERNEL<T, 16>, dim3(grid), dim3(256), 0, ST, __VA_ARGS__);                               \
     }                                                                                 \
   } while (0)
 
@@ -940,15 +950,15 @@ int dp_layer_norm_bwd(int dtype, const void* x, const void* dy, const float* gam
                     rows, C, accumulate, dgamma, dbeta
   DISPATCH_T(dtype, {
     if (pg) {
-      if (nvec <= 1) ln_bwd_kernel<T, 1, true><<<grid, 256, 0, ST>>>(LN_BWD_ARGS);
-      else if (nvec <= 2) ln_bwd_kernel<T, 2, true><<<grid, 256, 0, ST>>>(LN_BWD_ARGS);
-      else ln_bwd_kernel<T, 4, true><<<grid, 256, 0, ST>>>(LN_BWD_ARGS);
+      if (nvec <= 1) launch_k(ln_bwd_kernel<T, 1, true>, dim3(grid), dim3(256), 0, ST, LN_BWD_ARGS);
+      else if (nvec <= 2) launch_k(ln_bwd_kernel<T, 2, true>, dim3(grid), dim3(256), 0, ST, LN_BWD_ARGS);
+      else launch_k(ln_bwd_kernel<T, 4, true>, dim3(grid), dim3(256), 0, ST, LN_BWD_ARGS);
     } else {
-      if (nvec <= 1) ln_bwd_kernel<T, 1, false><<<grid, 256, 0, ST>>>(LN_BWD_ARGS);
-      else if (nvec <= 2) ln_bwd_kernel<T, 2, false><<<grid, 256, 0, ST>>>(LN_BWD_ARGS);
-      else if (nvec <= 4) ln_bwd_kernel<T, 4, false><<<grid, 256, 0, ST>>>(LN_BWD_ARGS);
-      else if (nvec <= 8) ln_bwd_kernel<T, 8, false><<<grid, 256, 0, ST>>>(LN_BWD_ARGS);
-      else ln_bwd_kernel<T, 16, false><<<grid, 256, 0, ST>>>(LN_BWD_ARGS);
+      if (nvec <= 1) launch_k(ln_bwd_kernel<T, 1, false>, dim3(grid), dim3(256), 0, ST, LN_BWD_ARGS);
+      else if (nvec <= 2) launch_k(ln_bwd_kernel<T, 2, false>, dim3(grid), dim3(256), 0, ST, LN_BWD_ARGS);
+      else if (nvec <= 4) launch_k(ln_bwd_kernel<T, 4, false>, dim3(grid), dim3(256), 0, ST, LN_BWD_ARGS);
+      else if (nvec <= 8) launch_k(ln_bwd_kernel<T, 8, false>, dim3(grid), dim3(256), 0, ST, LN_BWD_ARGS);
+      else launch_k(ln_bwd_kernel<T, 16, false>, dim3(grid), dim3(256), 0, ST, LN_BWD_ARGS);
     }
   });
 #undef LN_BWD_ARGS
@@ -958,13 +968,13 @@ int dp_layer_norm_bwd(int dtype, const void* x, const void* dy, const float* gam
     int64_t seg = (rows * cb + 2 * kNumSMs - 1) / (2 * kNumSMs);  // ~2 waves
     seg = seg < 64 ? 64 : seg;
     dim3 g2(static_cast<unsigned>(cb), static_cast<unsigned>((rows + seg - 1) / seg));
-    DISPATCH_T(dtype, ln_param_grad_kernel<T><<<g2, 256, 0, ST>>>(
+    DISPATCH_T(dtype, launch_k(ln_param_grad_kernel<T>, dim3(g2), dim3(256), 0, ST, 
                           cp<T>(x), cp<T>(dy), mean, rstd, rows, C, seg, dgamma, dbeta, nullptr, 0,
                           0, 0));
   }
   if (mod && dmod) {
     dim3 g2(static_cast<unsigned>((C / (dtype == DP_F32 ? 4 : 8) + 31) / 32), static_cast<unsigned>(rows / rps));
-    DISPATCH_T(dtype, ln_param_grad_kernel<T><<<g2, 256, 0, ST>>>(
+    DISPATCH_T(dtype, launch_k(ln_param_grad_kernel<T>, dim3(g2), dim3(256), 0, ST, 
                           cp<T>(x), cp<T>(dy), mean, rstd, rows, C, rps, nullptr, nullptr,
                           mp<T>(dmod), dmod_ld, shift_off, scale_off));
   }
@@ -975,7 +985,7 @@ int dp_softmax_fwd(int dtype, const float* S, void* P, int64_t rows, int cols, i
                    float scale, int causal, int Lq, dp_stream_t stream) {
   if (rows <= 0) return 0;
   const dim3 grid(static_cast<unsigned>((rows + 7) / 8));
-  DISPATCH_T(dtype, softmax_fwd_kernel<T><<<grid, 256, 0, ST>>>(S, mp<T>(P), rows, cols, ld, scale,
+  DISPATCH_T(dtype, launch_k(softmax_fwd_kernel<T>, dim3(grid), dim3(256), 0, ST, S, mp<T>(P), rows, cols, ld, scale,
                                                                   causal, Lq > 0 ? Lq : 1));
   return ew_check("softmax_fwd");
 }
@@ -984,7 +994,7 @@ int dp_softmax_bwd(int dtype, const void* P, const float* dP, void* dS, int64_t 
                    int ld, float scale, dp_stream_t stream) {
   if (rows <= 0) return 0;
   const dim3 grid(static_cast<unsigned>((rows + 7) / 8));
-  DISPATCH_T(dtype, softmax_bwd_kernel<T><<<grid, 256, 0, ST>>>(cp<T>(P), dP, mp<T>(dS), rows,
+  DISPATCH_T(dtype, launch_k(softmax_bwd_kernel<T>, dim3(grid), dim3(256), 0, ST, cp<T>(P), dP, mp<T>(dS), rows,
                                                                   cols, ld, scale));
   return ew_check("softmax_bwd");
 }
