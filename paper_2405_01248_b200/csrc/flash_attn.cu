@@ -285,7 +285,7 @@ struct BwdParams {
 // (TMEM accumulators across query tiles), dQ_i = dS K (TMEM) -> fp32 atomics into dq_acc.
 constexpr uint32_t BWD_SMEM_TILES = 10;  // K, V, Q[2], dO[2], P^T (2), dS^T (2)
 
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(256, 1)
     fa_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                   const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmDV,
@@ -309,8 +309,12 @@ __global__ void __launch_bounds__(128, 1)
   uint64_t* bar_acc = bar + 4;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 5);
 
+  // 8 warps: warps w and w+4 share TMEM lanes 32*(w%4).. (key rows) and split the 128 query
+  // columns of every S^T / dP^T tile (and the 64 dQ / dK / dV columns) between them
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
+  const int row = tid & 127;   // key row (TMEM lane) of this thread
+  const int half = tid >> 7;   // column half
   const int kt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int k0 = kt * BKV;
   const int nq = (p.N + BQ - 1) / BQ;
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_st = tmem, t_dpt = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 320, t_dq = tmem + 384;
-  const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+  const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
 
   auto load_q = [&](int i, int buf) {
     mbar_expect_tx(&bar_q[buf], 2 * TILE_BYTES);
@@ -346,15 +350,16 @@ __global__ void __launch_bounds__(128, 1)
   }
   // lse / D of the first query tile (rows >= N: lse = +inf -> P = 0)
   auto load_rows = [&](int i, int buf) {
-    const int q = i * BQ + tid;
-    sLse[buf * 128 + tid] = q < p.N ? p.lse[bh * p.N + q] : INFINITY;
-    sD[buf * 128 + tid] = q < p.N ? p.Dv[bh * p.N + q] : 0.f;
+    if (half) return;
+    const int q = i * BQ + row;
+    sLse[buf * 128 + row] = q < p.N ? p.lse[bh * p.N + q] : INFINITY;
+    sD[buf * 128 + row] = q < p.N ? p.Dv[bh * p.N + q] : 0.f;
   };
   load_rows(0, 0);
   const uint32_t id_sq = idesc_bf16_f32(BKV, BQ, 0, 0);  // S^T / dP^T: M=keys, N=queries, K=64
   const uint32_t id_acc = idesc_bf16_f32(BKV, HD, 0, 1); // dV / dK: M=keys, N=64, K=queries
   const uint32_t id_dq = idesc_bf16_f32(BQ, HD, 1, 1);   // dQ: M=queries (A MN-major), N=64
-  const bool key_valid = k0 + tid < p.Nk;
+  const bool key_valid = k0 + row < p.Nk;
 
   for (int i = 0; i < nq; ++i) {
     const int qb = i & 1;
@@ -380,7 +385,7 @@ __global__ void __launch_bounds__(128, 1)
     const float* lse = sLse + qb * 128;
     const float* Dq = sD + qb * 128;
 #pragma unroll 1
-    for (int c = 0; c < BQ / 32; ++c) {
+    for (int c = half * 2; c < half * 2 + 2; ++c) {
       uint32_t sv[32], dv[32];
       tmem_ld_32x32(t_st + lane_off + c * 32, sv);
       tmem_ld_32x32(t_dpt + lane_off + c * 32, dv);
@@ -397,7 +402,7 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
         const int chunk = (c & 1) * 4 + q4;
-        const int off = blk * TILE_BYTES + tid * 128 + ((chunk ^ (tid & 7)) * 16);
+        const int off = blk * TILE_BYTES + row * 128 + ((chunk ^ (row & 7)) * 16);
         uint4 u;
         u.x = pack_bf16x2(pt[q4 * 8 + 0], pt[q4 * 8 + 1]);
         u.y = pack_bf16x2(pt[q4 * 8 + 2], pt[q4 * 8 + 3]);
@@ -440,10 +445,10 @@ __global__ void __launch_bounds__(128, 1)
     mbar_wait(bar_acc, i & 1);
     tc_fence_after();
     if (tid == 0 && i + 2 < nq) load_q(i + 2, qb);  // Q/dO buffer qb is free again
-    // dQ rows of this query tile -> fp32 atomics (thread = query row)
-    const int q = i * BQ + tid;
-#pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
+    // dQ rows of this query tile -> fp32 atomics (thread = query row, half = 32-column chunk)
+    const int q = i * BQ + row;
+    {
+      const int c = half;
       uint32_t v[32];
       tmem_ld_32x32(t_dq + lane_off + c * 32, v);
       tmem_ld_wait();
@@ -463,8 +468,8 @@ __global__ void __launch_bounds__(128, 1)
   // dK (scaled), dV -> bf16 -> shared (reuse the Q buffers) -> TMA stores (thread = key row)
   uint8_t* sdk = sQ;
   uint8_t* sdv = sQ + TILE_BYTES;
-#pragma unroll
-  for (int c = 0; c < HD / 32; ++c) {
+  {
+    const int c = half;
     uint32_t vk[32], vv[32];
     tmem_ld_32x32(t_dk + lane_off + c * 32, vk);
     tmem_ld_32x32(t_dv + lane_off + c * 32, vv);
@@ -472,7 +477,7 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
     for (int q4 = 0; q4 < 4; ++q4) {
       const int chunk = c * 4 + q4;
-      const int off = tid * 128 + ((chunk ^ (tid & 7)) * 16);
+      const int off = row * 128 + ((chunk ^ (row & 7)) * 16);
       uint4 u;
       u.x = pack_bf16x2(p.scale * __uint_as_float(vk[q4 * 8 + 0]), p.scale * __uint_as_float(vk[q4 * 8 + 1]));
       u.y = pack_bf16x2(p.scale * __uint_as_float(vk[q4 * 8 + 2]), p.scale * __uint_as_float(vk[q4 * 8 + 3]));
@@ -609,7 +614,7 @@ extern "C" int dp_flash_attn_bwd(const DpAttnArgs* a, const void* dout, int64_t 
   }
   fa::BwdParams p{a->N, a->Nk, a->heads, a->scale * 1.4426950408889634f, a->scale, a->lse, Dv, dq_acc};
   dim3 grid((a->Nk + fa::BKV - 1) / fa::BKV, a->heads, a->B);
-  launch_k(fa::fa_bwd_kernel, dim3(grid), dim3(128), fa::BWD_SMEM, st, mq, mk, mv, mdo, mdk, mdv, p);
+  launch_k(fa::fa_bwd_kernel, dim3(grid), dim3(256), fa::BWD_SMEM, st, mq, mk, mv, mdo, mdk, mdv, p);
   const int64_t n2 = rows * C / 2;
   int g = static_cast<int>((n2 + 255) / 256);
   if (g > 148 * 8) g = 148 * 8;
