@@ -361,24 +361,30 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t id_dq = idesc_bf16_f32(BQ, HD, 1, 1);   // dQ: M=queries (A MN-major), N=64
   const bool key_valid = k0 + row < p.Nk;
 
+  // S^T / dP^T of query tile i: issued by thread 0 right after tile i-1's accumulator MMAs, so
+  // the tensor pipe computes them while the warps drain tile i-1's dQ (in-order MMA pipe: they
+  // complete after the dV/dK/dQ MMAs that still read P^T / dS^T from shared memory)
+  auto issue_sdp = [&](int i) {
+    const int qb = i & 1;
+    if (i == 0) mbar_wait(bar_kv, 0);
+    mbar_wait(&bar_q[qb], (i >> 1) & 1);
+    tc_fence_after();
+    const uint32_t ka = smem_u32(sK), va = smem_u32(sV);
+    const uint32_t qa = smem_u32(sQ + qb * TILE_BYTES), da = smem_u32(sDO + qb * TILE_BYTES);
+#pragma unroll
+    for (int k = 0; k < HD / 16; ++k) {
+      tc_mma_bf16(t_st, smem_desc_sw128(ka + k * 32, 16, 1024), smem_desc_sw128(qa + k * 32, 16, 1024),
+                  id_sq, k > 0 ? 1u : 0u);
+      tc_mma_bf16(t_dpt, smem_desc_sw128(va + k * 32, 16, 1024), smem_desc_sw128(da + k * 32, 16, 1024),
+                  id_sq, k > 0 ? 1u : 0u);
+    }
+    tc_commit(bar_sp);
+  };
+  if (tid == 0) issue_sdp(0);
+
   for (int i = 0; i < nq; ++i) {
     const int qb = i & 1;
     __syncthreads();  // sLse/sD of tile i visible; previous tile's smem/TMEM consumers done
-    if (tid == 0) {
-      if (i == 0) mbar_wait(bar_kv, 0);
-      mbar_wait(&bar_q[qb], (i >> 1) & 1);
-      tc_fence_after();
-      const uint32_t ka = smem_u32(sK), va = smem_u32(sV);
-      const uint32_t qa = smem_u32(sQ + qb * TILE_BYTES), da = smem_u32(sDO + qb * TILE_BYTES);
-#pragma unroll
-      for (int k = 0; k < HD / 16; ++k) {
-        tc_mma_bf16(t_st, smem_desc_sw128(ka + k * 32, 16, 1024), smem_desc_sw128(qa + k * 32, 16, 1024),
-                    id_sq, k > 0 ? 1u : 0u);
-        tc_mma_bf16(t_dpt, smem_desc_sw128(va + k * 32, 16, 1024), smem_desc_sw128(da + k * 32, 16, 1024),
-                    id_sq, k > 0 ? 1u : 0u);
-      }
-      tc_commit(bar_sp);
-    }
     if (i + 1 < nq) load_rows(i + 1, qb ^ 1);
     mbar_wait(bar_sp, i & 1);
     tc_fence_after();
@@ -441,6 +447,7 @@ __global__ void __launch_bounds__(256, 1)
                     smem_desc_sw128(ka + k * 2048, 8192, 1024), id_dq, k > 0 ? 1u : 0u);
       }
       tc_commit(bar_acc);
+      if (i + 1 < nq) issue_sdp(i + 1);
     }
     mbar_wait(bar_acc, i & 1);
     tc_fence_after();
