@@ -364,10 +364,13 @@ def _h2d_bytes_per_step(trainer):
 
 
 def _ncu_traffic(fam):
+    """DRAM bytes per launch of the family's representative kernel from one committed ncu --set full
+    capture (profiles/ncu_traffic.json), or None."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(fam)
+            v = json.load(fh).get(fam)
+        return v if isinstance(v, (int, float)) else None
     except (OSError, ValueError):
         return None
 
