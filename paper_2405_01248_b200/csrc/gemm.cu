@@ -42,6 +42,7 @@ struct TcParams {
   int Rf;          // filter height (B_DGRAD flips taps)
   int stream_k;    // 1: contiguous k-iteration ranges per CTA (fp32 atomic outputs)
   int d_tma;       // 1: bf16 output written by TMA tensor stores (tmD)
+  int halo;        // 1: 3x3 stride-1 conv with one input strip per filter row (TcCfg HALO)
   void* D;
   int64_t d_ld, d_bs1, d_bs2;
   int d_f32, out_mode, vec_ok;
@@ -55,15 +56,24 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr uint32_t A_STAGE_BYTES = BM * BK * 2;
 
-template <int BN, int CG>
+// HALO (3x3 stride-1 convs whose 128-pixel tiles lie in one image row): a stage holds ONE input
+// strip of 130 pixels x 64 channels for a filter row r and the three taps s = 0..2 read it as
+// row-shifted views (UMMA descriptor base offset), with the three matching weight blocks: the
+// A operand crosses L2 -> SM once per filter row instead of once per tap.
+constexpr int HALO_ROWS = BM + 2;
+constexpr uint32_t HALO_A_BYTES = HALO_ROWS * BK * 2;   // bytes the halo TMA box delivers
+template <int BN, int CG, bool HALO = false>
 struct TcCfg {
   static constexpr int BNL = BN / CG;  // B columns staged per CTA (a CTA pair splits N)
-  static constexpr uint32_t B_STAGE_BYTES = BNL * BK * 2;
+  static constexpr uint32_t B_SUB = BNL * BK * 2;
+  static constexpr uint32_t B_STAGE_BYTES = (HALO ? 3 : 1) * B_SUB;
+  static constexpr uint32_t A_BYTES = HALO ? ((HALO_A_BYTES + 1023) / 1024) * 1024 : A_STAGE_BYTES;
+  static constexpr uint32_t A_TX = HALO ? HALO_A_BYTES : A_STAGE_BYTES;
   // as many 64-deep k-stages as fit next to the 16 KB epilogue staging buffers
-  static constexpr int STAGES_FIT = 209 * 1024 / (A_STAGE_BYTES + B_STAGE_BYTES);
+  static constexpr int STAGES_FIT = 209 * 1024 / (A_BYTES + B_STAGE_BYTES);
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256 ? 256 : 512);
-  static constexpr size_t SMEM = 1024 + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 8 * 2048 + 256;
+  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_STAGE_BYTES) + 8 * 2048 + 256;
 };
 
 DP_DEV void pixel_origin(int pix0, int P, int Q, int& n, int& h, int& w) {
@@ -274,18 +284,18 @@ DP_DEV void epilogue_math(const TcParams& p, int row, int n, int z1, int z2, con
 
 constexpr int EPI_STAGE_BYTES = 32 * 64;  // one 32 x 32 bf16 chunk
 
-template <int BN, int CG>
+template <int BN, int CG, bool HALO>
 __global__ void __launch_bounds__(256, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmD, const TcParams p) {
-  using Cfg = TcCfg<BN, CG>;
+  using Cfg = TcCfg<BN, CG, HALO>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int BNL = Cfg::BNL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
   uint8_t* sE = sB + STAGES * Cfg::B_STAGE_BYTES;            // 4 warps x 2 x 2 KB, 1 KB aligned
   uint64_t* full = reinterpret_cast<uint64_t*>(sE + 8 * EPI_STAGE_BYTES);
   uint64_t* empty = full + STAGES;
@@ -350,8 +360,8 @@ __global__ void __launch_bounds__(256, 1)
       }
       for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
-        if (leader) mbar_expect_tx(&full[stage], CG * (A_STAGE_BYTES + Cfg::B_STAGE_BYTES));
-        uint8_t* a_dst = sA + stage * A_STAGE_BYTES;
+        if (leader) mbar_expect_tx(&full[stage], CG * (Cfg::A_TX + Cfg::B_STAGE_BYTES));
+        uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
         uint8_t* b_dst = sB + stage * Cfg::B_STAGE_BYTES;
         uint64_t* fb = &full[stage];
         auto load = [&](const CUtensorMap* m, void* dst, int c0, int c1, int c2, int c3) {
@@ -361,6 +371,20 @@ __global__ void __launch_bounds__(256, 1)
             tma_load_4d(m, fb, dst, c0, c1, c2, c3);
         };
         int pn = 0, ph = 0, pw = 0;
+        if constexpr (HALO) {
+          // kb = (filter row r, 64-channel block): one 130-pixel strip, three tap weight blocks
+          const int rr = kb / p.cblk;
+          const int cb = kb - rr * p.cblk;
+          load(&tmA, a_dst, cb * BK, cw, ch + rr, cn);
+#pragma unroll
+          for (int ss = 0; ss < 3; ++ss)
+            load(&tmB, b_dst + ss * Cfg::B_SUB, ((rr * 3 + ss) * p.cblk + cb) * BK, n0, z1, z2);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+          continue;
+        }
         if (p.a_mode == A_WG_DY || p.b_mode == B_WG_X) pixel_origin(kb * BK, p.P, p.Q, pn, ph, pw);
         switch (p.a_mode) {
           case A_KMAJ:
@@ -439,8 +463,25 @@ __global__ void __launch_bounds__(256, 1)
       for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t a_addr = smem_u32(sA + stage * A_STAGE_BYTES);
+        const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
         const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_STAGE_BYTES);
+        if constexpr (HALO) {
+#pragma unroll
+          for (int ss = 0; ss < 3; ++ss)
+#pragma unroll
+            for (int j = 0; j < BK / 16; ++j) {
+              // tap ss = the strip shifted by ss pixel rows (128 B): start address mid swizzle atom
+              const uint64_t adesc = smem_desc_sw128(a_addr + ss * 128 + j * 32, 16, 1024);  // no base offset: the
+              // SWIZZLE_128B phase follows the absolute smem address (TMA wrote the strip the same
+              // way), so a row-shifted start is consistent as is (tests/test_gemm_gpu.py::halo)
+              const uint64_t bdesc = smem_desc_sw128(b_addr + ss * Cfg::B_SUB + j * 32, 16, 1024);
+              const uint32_t accum = (kb > wk.kb0 || ss > 0 || j > 0) ? 1u : 0u;
+              if constexpr (CG == 2)
+                tc_mma_bf16_2sm(d_tmem, adesc, bdesc, idesc, accum);
+              else
+                tc_mma_bf16(d_tmem, adesc, bdesc, idesc, accum);
+            }
+        } else
 #pragma unroll
         for (int j = 0; j < BK / 16; ++j) {
           const uint64_t adesc = a_mn ? smem_desc_sw128(a_addr + j * 2048, 8192, 1024)
@@ -605,6 +646,14 @@ static int make_map(CUtensorMap* map, const void* base, const uint64_t dims[4],
   return 0;
 }
 
+static bool halo_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DP_HALO");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return on;
+}
+
 static bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("DP_PDL");
@@ -613,13 +662,13 @@ static bool pdl_enabled() {
   return on;
 }
 
-template <int BN, int CG>
+template <int BN, int CG, bool HALO = false>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
                      TcParams p, int max_ctas, cudaStream_t st) {
-  using Cfg = TcCfg<BN, CG>;
+  using Cfg = TcCfg<BN, CG, HALO>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, CG>,
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, CG, HALO>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(Cfg::SMEM));
     if (e != cudaSuccess) {
@@ -647,7 +696,7 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
   attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, CG>, ma, mb, md, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, CG, HALO>, ma, mb, md, p);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("tc_gemm launch: ") + cudaGetErrorString(e));
@@ -718,6 +767,14 @@ static int make_dmap(CUtensorMap* md, TcParams& p, int M, int N, int b1, int b2)
 template <int CG>
 static int launch_cg(int bn, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
                      TcParams& p, cudaStream_t st) {
+  if (p.halo) {
+    switch (bn) {
+      case 128: return launch_tc<128, CG, true>(ma, mb, md, p, kNumSMs, st);
+      case 160: return launch_tc<160, CG, true>(ma, mb, md, p, kNumSMs, st);
+      case 192: return launch_tc<192, CG, true>(ma, mb, md, p, kNumSMs, st);
+      default: return launch_tc<256, CG, true>(ma, mb, md, p, kNumSMs, st);
+    }
+  }
   switch (bn) {
     case 64: return launch_tc<64, CG>(ma, mb, md, p, kNumSMs, st);
     case 96: return launch_tc<96, CG>(ma, mb, md, p, kNumSMs, st);
@@ -979,7 +1036,10 @@ int tc_conv_fwd(const DpConvArgs* a, cudaStream_t st, int64_t* query = nullptr) 
   p.M = a->N * a->P * a->Q;
   p.N = a->K;
   p.cblk = a->C / 64;
-  p.num_kb = a->R * a->S * p.cblk;
+  // halo strips: 3x3, stride 1, symmetric 1-pixel padding, tiles inside one image row
+  p.halo = (halo_enabled() && a->R == 3 && a->S == 3 && a->stride == 1 && a->pad_w == 1 && p.th == 1 &&
+            p.tn == 1 && (bn == 128 || bn == 160 || bn == 192 || bn == 256)) ? 1 : 0;
+  p.num_kb = p.halo ? a->R * p.cblk : a->R * a->S * p.cblk;
   p.tiles_m = (p.M + BM * cg - 1) / (BM * cg);
   p.tiles_n = (a->K + bn - 1) / bn;
   p.batch1 = 1;
@@ -1004,8 +1064,8 @@ int tc_conv_fwd(const DpConvArgs* a, cudaStream_t st, int64_t* query = nullptr) 
   {
     const uint64_t d[4] = {(uint64_t)a->C, (uint64_t)a->W, (uint64_t)a->H, (uint64_t)a->N};
     const int64_t s[3] = {a->C, (int64_t)a->W * a->C, (int64_t)a->H * a->W * a->C};
-    const uint32_t box[4] = {64, (uint32_t)(p.tw * a->stride), (uint32_t)(p.th * a->stride),
-                             (uint32_t)p.tn};
+    const uint32_t box[4] = {64, (uint32_t)(p.halo ? HALO_ROWS : p.tw * a->stride),
+                             (uint32_t)(p.th * a->stride), (uint32_t)p.tn};
     const uint32_t es[4] = {1, (uint32_t)a->stride, (uint32_t)a->stride, 1};
     if (int e = make_map(&ma, a->x, d, s, box, es)) return e;
   }

@@ -193,3 +193,18 @@ def test_splitk_conv_fwd_dgrad(N, H, C, K):
     dx = ops.conv2d_dgrad(dy, w, x.shape)
     ref_dx = torch.nn.grad.conv2d_input(xr.shape, wr, dy.float().permute(0, 3, 1, 2), padding=1)
     assert _rel(dx, ref_dx.permute(0, 2, 3, 1)) < 1e-2
+
+
+@pytest.mark.parametrize("N,H,W,C,K", [(2, 4, 256, 128, 128), (1, 3, 128, 256, 256), (2, 2, 128, 128, 320),
+                                       (1, 5, 384, 64, 192)])
+def test_conv_halo_strips(N, H, W, C, K):
+    """3x3 stride-1 convs whose 128-pixel tiles lie inside one image row use one input strip per
+    filter row (three row-shifted tap views of it): must equal the reference conv."""
+    ops = _ops()
+    g = torch.Generator(device="cuda").manual_seed(C + K + W)
+    x = torch.randn(N, H, W, C, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(K, 3, 3, C, device="cuda", generator=g) * 0.05).bfloat16()
+    b = torch.randn(K, device="cuda", generator=g)
+    y = ops.conv2d(x, w, bias=b)
+    ref = F.conv2d(x.float().permute(0, 3, 1, 2), w.float().permute(0, 3, 1, 2), b, padding=1).permute(0, 2, 3, 1)
+    assert _rel(y, ref) < 1e-2
