@@ -72,7 +72,13 @@ struct TcCfg {
   // as many 64-deep k-stages as fit next to the 16 KB epilogue staging buffers
   static constexpr int STAGES_FIT = 209 * 1024 / (A_BYTES + B_STAGE_BYTES);
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
-  static constexpr int TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256 ? 256 : 512);
+  // BN > 256 (320: U-Net 320/640-channel layers): two N = BN/2 MMAs per k-step into adjacent TMEM
+  // column ranges, one accumulator buffer (the epilogue is exposed once per long-K tile); each CTA
+  // of a pair stages BNL/2 rows of B for each half
+  static constexpr int NH = BN > 256 ? 2 : 1;
+  static constexpr uint32_t B_HALF = B_SUB / NH;
+  static constexpr int NACC = 2 * BN <= 512 ? 2 : 1;
+  static constexpr int TMEM_COLS = (NACC * BN <= 128) ? 128 : (NACC * BN <= 256 ? 256 : 512);
   static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_STAGE_BYTES) + 8 * 2048 + 256;
 };
 
@@ -408,7 +414,13 @@ __global__ void __launch_bounds__(256, 1)
         }
         switch (p.b_mode) {
           case B_KMAJ:
-            load(&tmB, b_dst, kb * BK, n0, z1, z2);
+            if constexpr (Cfg::NH == 2) {
+              const int nt = wk.n_blk * BN + crank * (BNL / 2);
+              load(&tmB, b_dst, kb * BK, nt, z1, z2);
+              load(&tmB, b_dst + Cfg::B_HALF, kb * BK, nt + BN / 2, z1, z2);
+            } else {
+              load(&tmB, b_dst, kb * BK, n0, z1, z2);
+            }
             break;
           case B_MNMAJ:
 #pragma unroll
@@ -448,7 +460,7 @@ __global__ void __launch_bounds__(256, 1)
     // ------------------------------------------------------------ MMA issuer (leader CTA)
     const int a_mn = (p.a_mode == A_MNMAJ || p.a_mode == A_WG_DY) ? 1 : 0;
     const int b_mn = (p.b_mode != B_KMAJ) ? 1 : 0;
-    const uint32_t idesc = idesc_bf16_f32(BM * CG, BN, a_mn, b_mn);
+    const uint32_t idesc = idesc_bf16_f32(BM * CG, BN / Cfg::NH, a_mn, b_mn);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -481,6 +493,19 @@ __global__ void __launch_bounds__(256, 1)
               else
                 tc_mma_bf16(d_tmem, adesc, bdesc, idesc, accum);
             }
+        } else if constexpr (Cfg::NH == 2) {
+#pragma unroll
+          for (int j = 0; j < BK / 16; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint64_t adesc = smem_desc_sw128(a_addr + j * 32, 16, 1024);
+              const uint64_t bdesc = smem_desc_sw128(b_addr + h * Cfg::B_HALF + j * 32, 16, 1024);
+              const uint32_t accum = (kb > wk.kb0 || j > 0) ? 1u : 0u;
+              if constexpr (CG == 2)
+                tc_mma_bf16_2sm(d_tmem + h * (BN / 2), adesc, bdesc, idesc, accum);
+              else
+                tc_mma_bf16(d_tmem + h * (BN / 2), adesc, bdesc, idesc, accum);
+            }
         } else
 #pragma unroll
         for (int j = 0; j < BK / 16; ++j) {
@@ -507,8 +532,10 @@ __global__ void __launch_bounds__(256, 1)
         tc_commit_2sm_mc(&tfull[acc]);
       else
         tc_commit(&tfull[acc]);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (++acc == Cfg::NACC) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue (every CTA)
@@ -561,8 +588,10 @@ __global__ void __launch_bounds__(256, 1)
         else
           mbar_arrive(&tempty[acc]);
       }
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (++acc == Cfg::NACC) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
     }
     if (p.d_tma && lane == 0) bulk_wait_all();
   }
@@ -750,6 +779,17 @@ static int pick_bn(int N, bool b_mn_major) {
   return best;
 }
 
+// BN = 320 (two N = 160 MMAs per k-step, one accumulator buffer) for N = 320 / 640 / 960 with
+// K-major B, CTA pairs and long K: B traffic per MMA cycle drops from (16 + 10) KB / 320 cycles
+// (BN 160) to (16 + 20) KB / 640 cycles per SM; the single accumulator exposes the epilogue once
+// per tile, which long K (>= 16 k-blocks) amortises.
+static int widen_bn(int bn, int cg, bool b_mn, int N, int num_kb) {
+  static const int off = env_int("DP_NO_BN320");  // experiments only
+  if (off || cg != 2 || b_mn || num_kb < 16) return bn;
+  if (N == 320 || N == 640 || N == 960) return 320;
+  return bn;
+}
+
 // bf16 STORE outputs with TMA-legal strides are written by tensor stores (box 32 x 32,
 // SWIZZLE_64B); fp32 / atomic outputs keep the direct per-thread path.
 static int make_dmap(CUtensorMap* md, TcParams& p, int M, int N, int b1, int b2) {
@@ -782,6 +822,9 @@ static int launch_cg(int bn, const CUtensorMap& ma, const CUtensorMap& mb, const
     case 160: return launch_tc<160, CG>(ma, mb, md, p, kNumSMs, st);
     case 192: return launch_tc<192, CG>(ma, mb, md, p, kNumSMs, st);
     case 224: return launch_tc<224, CG>(ma, mb, md, p, kNumSMs, st);
+    case 320:
+      if constexpr (CG == 2) return launch_tc<320, 2>(ma, mb, md, p, kNumSMs, st);
+      [[fallthrough]];
     default: return launch_tc<256, CG>(ma, mb, md, p, kNumSMs, st);
   }
 }
@@ -942,8 +985,9 @@ int tc_gemm(const DpGemmArgs* a, cudaStream_t st, int64_t* query = nullptr) {
     set_error("atomic accumulation needs an fp32 output");
     return DP_ERR_ARGS;
   }
-  const int bn = pick_bn(a->N, a->b_mn_major != 0);
-  const int cg = decide_cg(a->M, bn, a->b_mn_major != 0, a->K);
+  const int bn0 = pick_bn(a->N, a->b_mn_major != 0);
+  const int cg = decide_cg(a->M, bn0, a->b_mn_major != 0, a->K);
+  const int bn = widen_bn(bn0, cg, a->b_mn_major != 0, a->N, (a->K + BK - 1) / BK);
   TcParams p{};
   p.M = a->M;
   p.N = a->N;
@@ -984,7 +1028,7 @@ int tc_gemm(const DpGemmArgs* a, cudaStream_t st, int64_t* query = nullptr) {
       if (int e = make_map(&mb, a->B, d, s, box, ones)) return e;
     } else {
       const uint64_t d[4] = {(uint64_t)a->K, (uint64_t)a->N, (uint64_t)p.batch1, (uint64_t)batch2};
-      const uint32_t box[4] = {BK, (uint32_t)(bn / cg), 1, 1};
+      const uint32_t box[4] = {BK, (uint32_t)(bn / cg / (bn > 256 ? 2 : 1)), 1, 1};
       if (int e = make_map(&mb, a->B, d, s, box, ones)) return e;
     }
   }
@@ -1031,7 +1075,7 @@ int tc_conv_fwd(const DpConvArgs* a, cudaStream_t st, int64_t* query = nullptr) 
     set_error("output spatial size does not tile into 128-pixel boxes");
     return DP_ERR_UNSUPPORTED;
   }
-  const int bn = pick_bn(a->K, false);
+  int bn = pick_bn(a->K, false);
   const int cg = decide_cg(a->N * a->P * a->Q, bn, false, a->R * a->S * a->C);
   p.M = a->N * a->P * a->Q;
   p.N = a->K;
@@ -1039,6 +1083,7 @@ int tc_conv_fwd(const DpConvArgs* a, cudaStream_t st, int64_t* query = nullptr) 
   // halo strips: 3x3, stride 1, symmetric 1-pixel padding, tiles inside one image row
   p.halo = (halo_enabled() && a->R == 3 && a->S == 3 && a->stride == 1 && a->pad_w == 1 && p.th == 1 &&
             p.tn == 1 && (bn == 128 || bn == 160 || bn == 192 || bn == 256)) ? 1 : 0;
+  if (!p.halo) bn = widen_bn(bn, cg, false, a->K, a->R * a->S * p.cblk);
   p.num_kb = p.halo ? a->R * p.cblk : a->R * a->S * p.cblk;
   p.tiles_m = (p.M + BM * cg - 1) / (BM * cg);
   p.tiles_n = (a->K + bn - 1) / bn;
@@ -1073,7 +1118,7 @@ int tc_conv_fwd(const DpConvArgs* a, cudaStream_t st, int64_t* query = nullptr) 
     const int64_t Kdim = (int64_t)a->R * a->S * a->C;
     const uint64_t d[4] = {(uint64_t)Kdim, (uint64_t)a->K, 1, 1};
     const int64_t s[3] = {Kdim, 0, 0};
-    const uint32_t box[4] = {BK, (uint32_t)(bn / cg), 1, 1};
+    const uint32_t box[4] = {BK, (uint32_t)(bn / cg / (bn > 256 ? 2 : 1)), 1, 1};
     const uint32_t ones[4] = {1, 1, 1, 1};
     if (int e = make_map(&mb, a->w, d, s, box, ones)) return e;
   }

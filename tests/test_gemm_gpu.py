@@ -208,3 +208,31 @@ def test_conv_halo_strips(N, H, W, C, K):
     y = ops.conv2d(x, w, bias=b)
     ref = F.conv2d(x.float().permute(0, 3, 1, 2), w.float().permute(0, 3, 1, 2), b, padding=1).permute(0, 2, 3, 1)
     assert _rel(y, ref) < 1e-2
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 320, 2880), (8192, 640, 2560), (2048, 960, 1280), (512, 320, 4096)])
+def test_linear_bn320(M, N, K):
+    """N = 320 / 640 / 960 with long K: CTA pairs with two N = 160 MMAs per k-step (BN 320)."""
+    ops = _ops()
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    x = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    w = torch.randn(N, K, device="cuda", generator=g).bfloat16()
+    b = torch.randn(N, device="cuda", generator=g)
+    r = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    y = ops.linear(x, w, bias=b, residual=r)
+    assert _rel(y, x.float() @ w.float().t() + b + r.float()) < 1e-2
+
+
+@pytest.mark.parametrize("N,H,C,K", [(8, 32, 320, 320), (8, 16, 640, 640), (4, 32, 640, 320)])
+def test_conv_bn320_fwd_dgrad(N, H, C, K):
+    ops = _ops()
+    g = torch.Generator(device="cuda").manual_seed(C * K)
+    x = torch.randn(N, H, H, C, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(K, 3, 3, C, device="cuda", generator=g) * 0.05).bfloat16()
+    y = ops.conv2d(x, w)
+    xr, wr = x.float().permute(0, 3, 1, 2), w.float().permute(0, 3, 1, 2)
+    assert _rel(y, F.conv2d(xr, wr, padding=1).permute(0, 2, 3, 1)) < 1e-2
+    dy = torch.randn(N, H, H, K, device="cuda", generator=g).bfloat16()
+    dx = ops.conv2d_dgrad(dy, w, x.shape)
+    ref = torch.nn.grad.conv2d_input(xr.shape, wr, dy.float().permute(0, 3, 1, 2), padding=1)
+    assert _rel(dx, ref.permute(0, 2, 3, 1)) < 1e-2
