@@ -255,7 +255,7 @@ DP_DEV void stage_row_bf16(uint8_t* buf, int lane, const float (&f)[32]) {
 
 template <int BN>
 DP_DEV void epilogue_math(const TcParams& p, int row, int n, int z1, int z2, const uint32_t (&v)[32],
-                          float (&f)[32]) {
+                          float (&f)[32], const uint4 (&rpre)[4], bool use_pre) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * p.alpha;
   const int nvalid = min(32, p.N - n);
@@ -269,7 +269,14 @@ DP_DEV void epilogue_math(const TcParams& p, int row, int n, int z1, int z2, con
         if (i < nvalid) f[i] += __ldg(p.bias + n + i);
     }
   }
-  if (p.R && row < p.M) {
+  if (use_pre) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&rpre[q]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f[q * 8 + i] += __bfloat162float(b[i]);
+    }
+  } else if (p.R && row < p.M) {
     const int64_t roff = z1 * p.r_bs1 + z2 * p.r_bs2 + (int64_t)row * p.r_ld + n;
     const __nv_bfloat16* r = reinterpret_cast<const __nv_bfloat16*>(p.R) + roff;
     if (nvalid == 32 && p.vec_ok) {
@@ -290,7 +297,7 @@ DP_DEV void epilogue_math(const TcParams& p, int row, int n, int z1, int z2, con
 
 constexpr int EPI_STAGE_BYTES = 32 * 64;  // one 32 x 32 bf16 chunk
 
-template <int BN, int CG, bool HALO>
+template <int BN, int CG, bool HALO, bool RES>
 __global__ void __launch_bounds__(256, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmD, const TcParams p) {
@@ -548,21 +555,49 @@ __global__ void __launch_bounds__(256, 1)
     WorkIter it;
     it.init(p, CG);
     Work wk;
+    // bf16 residual (TMA-store path): each lane's 64-byte row segments are fetched two chunks
+    // ahead, the first two before the accumulator is ready, so their DRAM latency overlaps the
+    // MMAs and the previous chunks instead of stalling every chunk
+    const bool rpre_on = RES && p.R != nullptr && p.vec_ok && !p.d_f32 && p.d_tma;
+    auto rload = [&](const Work& w, int row, int c, uint4 (&dst)[4]) {
+      const int n = w.n_blk * BN + c * 32;
+      if (rpre_on && row < p.M && c < BN / 32 && n + 32 <= p.N) {
+        const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(p.R) + w.z1 * p.r_bs1 +
+                                  w.z2 * p.r_bs2 + (int64_t)row * p.r_ld + n;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = *reinterpret_cast<const uint4*>(rb + q * 8);
+      }
+    };
     while (it.next(p, wk)) {
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
       const int row0 = wk.m_blk * (BM * CG) + crank * BM + wq * 32;
       const int row = row0 + lane;
+      uint4 r1[4], r2[4];
+      if constexpr (RES) {
+        rload(wk, row, 0, r1);
+        rload(wk, row, 1, r2);
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         const int n = wk.n_blk * BN + c * 32;
         if (n >= p.N) break;  // warp-uniform
+        uint4 rc[4];
+        if constexpr (RES) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            rc[q] = r1[q];
+            r1[q] = r2[q];
+          }
+          rload(wk, row, c + 2, r2);
+        }
+        const bool use_pre = rpre_on && row < p.M && n + 32 <= p.N;
         uint32_t v[32];
         tmem_ld_32x32(tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + acc * BN + c * 32, v);
         tmem_ld_wait();
         if (p.d_tma) {
           float f[32];
-          epilogue_math<BN>(p, row, n, wk.z1, wk.z2, v, f);
+          epilogue_math<BN>(p, row, n, wk.z1, wk.z2, v, f, rc, use_pre);
           uint8_t* buf = ebuf + (chunk_seq & 1) * EPI_STAGE_BYTES;
           if (chunk_seq >= 2) {
             if (lane == 0) bulk_wait_read<1>();
@@ -691,13 +726,13 @@ static bool pdl_enabled() {
   return on;
 }
 
-template <int BN, int CG, bool HALO = false>
+template <int BN, int CG, bool HALO = false, bool RES = false>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
                      TcParams p, int max_ctas, cudaStream_t st) {
   using Cfg = TcCfg<BN, CG, HALO>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, CG, HALO>,
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, CG, HALO, RES>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(Cfg::SMEM));
     if (e != cudaSuccess) {
@@ -725,7 +760,7 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
   attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, CG, HALO>, ma, mb, md, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, CG, HALO, RES>, ma, mb, md, p);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("tc_gemm launch: ") + cudaGetErrorString(e));
@@ -804,9 +839,29 @@ static int make_dmap(CUtensorMap* md, TcParams& p, int M, int N, int b1, int b2)
   return 0;
 }
 
+template <int CG, bool RES>
+static int launch_cg_r(int bn, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
+                       TcParams& p, cudaStream_t st) {
+  switch (bn) {
+    case 64: return launch_tc<64, CG, false, RES>(ma, mb, md, p, kNumSMs, st);
+    case 96: return launch_tc<96, CG, false, RES>(ma, mb, md, p, kNumSMs, st);
+    case 128: return launch_tc<128, CG, false, RES>(ma, mb, md, p, kNumSMs, st);
+    case 160: return launch_tc<160, CG, false, RES>(ma, mb, md, p, kNumSMs, st);
+    case 192: return launch_tc<192, CG, false, RES>(ma, mb, md, p, kNumSMs, st);
+    case 224: return launch_tc<224, CG, false, RES>(ma, mb, md, p, kNumSMs, st);
+    case 320:
+      if constexpr (CG == 2) return launch_tc<320, 2, false, RES>(ma, mb, md, p, kNumSMs, st);
+      [[fallthrough]];
+    default: return launch_tc<256, CG, false, RES>(ma, mb, md, p, kNumSMs, st);
+  }
+}
+
 template <int CG>
 static int launch_cg(int bn, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
                      TcParams& p, cudaStream_t st) {
+  // bf16 residual epilogue through TMA stores: the instantiation with residual prefetch
+  if (!p.halo && p.R && !p.d_f32 && p.vec_ok && p.d_tma) return launch_cg_r<CG, true>(bn, ma, mb, md, p, st);
+  if (!p.halo) return launch_cg_r<CG, false>(bn, ma, mb, md, p, st);
   if (p.halo) {
     switch (bn) {
       case 128: return launch_tc<128, CG, true>(ma, mb, md, p, kNumSMs, st);

@@ -104,11 +104,18 @@ def linear(x, w, bias=None, residual=None, out=None):
 
 
 def linear_dgrad(dy, w, out=None):
-    """dx[M,K] = dy[M,N] @ w[N,K]."""
+    """dx[M,K] = dy[M,N] @ w[N,K]. bf16 with a K-dim multiple of 8: the weight is transposed once
+    (tiled flip-transpose kernel, K x N x 2 B) so that B is K-major and the GEMM can use CTA pairs and
+    32-column tile widths (MN-major B is restricted to 64-column boxes on single CTAs)."""
     M, N = dy.shape
     K = w.shape[1]
     if out is None:
         out = torch.empty(M, K, device=dy.device, dtype=dy.dtype)
+    if dy.dtype == torch.bfloat16 and K % 8 == 0 and N % 8 == 0 and w.is_contiguous() and M >= 1024:
+        wt = torch.empty(K, N, device=w.device, dtype=w.dtype)
+        check(_lib.lib().dp_conv_weight_flip(dtype_code(w), _ptr(w), _ptr(wt), N, 1, 1, K, _stream()),
+              "dp_conv_weight_flip")
+        return gemm(dy, wt, out, M=M, N=K, K=N, a_ld=dy.stride(0), b_ld=N, d_ld=out.stride(0))
     return gemm(dy, w, out, M=M, N=K, K=N, a_ld=dy.stride(0), b_ld=w.stride(0), b_mn=True,
                 d_ld=out.stride(0))
 
@@ -212,7 +219,7 @@ def conv2d(x, w, *, stride=1, pad=(1, 1), out_hw=None, bias=None, residual=None,
         telemetry.timed("tcgen05_gemm", 2.0 * N * P * Q * K * R * S * C,
                         lambda: check(_lib.lib().dp_conv_fwd(ctypes.byref(a), _stream()), "dp_conv_fwd",
                                       2 if ws is not None else 1),
-                        sub="conv_fwd")
+                        sub=f"conv_fwd {N}x{H}x{W}x{C}->{K} r{R}s{stride}" if telemetry.SHAPES else "conv_fwd")
         return out
     cols = im2col(x, R, S, stride, pad, P, Q)
     linear(cols, w.reshape(K, -1), bias=bias,
@@ -263,7 +270,7 @@ def conv2d_dgrad(dy, w, x_shape, *, stride=1, pad=(1, 1)):
         telemetry.timed("tcgen05_gemm", 2.0 * N * H * W * C * R * S * K,
                         lambda: check(_lib.lib().dp_conv_dgrad(ctypes.byref(a), _stream()), "dp_conv_dgrad",
                                       2 if ws is not None else 1),
-                        sub="conv_dgrad")
+                        sub=f"conv_dgrad {N}x{H}x{W}x{C}<-{K} r{R}" if telemetry.SHAPES else "conv_dgrad")
         return _take_last(dx, C)
     if dy.dtype == torch.bfloat16 and _tiles(H, W, 128):
         # dx = conv(dy (zero-dilated for stride 2), flip-transposed w, pad R-1-pad): the forward
@@ -287,7 +294,7 @@ def conv2d_dgrad(dy, w, x_shape, *, stride=1, pad=(1, 1)):
         telemetry.timed("tcgen05_gemm", 2.0 * N * H * W * C * R * S * K,
                         lambda: check(_lib.lib().dp_conv_fwd(ctypes.byref(a), _stream()), "dp_conv_fwd",
                                       2 if ws is not None else 1),
-                        sub="conv_dgrad")
+                        sub=f"conv_dgrad {N}x{H}x{W}x{C}<-{K} r{R}" if telemetry.SHAPES else "conv_dgrad")
         return _take_last(dx, C)
     dcols = linear_dgrad(dy.reshape(-1, K), w.reshape(K, -1))
     dx = torch.zeros(N, H, W, C, device=dy.device, dtype=dy.dtype)
@@ -312,7 +319,7 @@ def conv2d_wgrad(dy, x, dw, *, stride=1, pad=(1, 1)):
         a.K, a.R, a.S = Kp, R, S
         telemetry.timed("tcgen05_gemm", 2.0 * N * P * Q * K * R * S * C,
                         lambda: check(_lib.lib().dp_conv_wgrad(ctypes.byref(a), _stream()), "dp_conv_wgrad"),
-                        sub="conv_wgrad")
+                        sub=f"conv_wgrad {N}x{H}x{W}x{C}->{K} r{R}" if telemetry.SHAPES else "conv_wgrad")
         if tgt is not dw:
             dw.add_(tgt[:K, :, :, :C])
         return dw

@@ -19,6 +19,6 @@ st = telemetry.timer.stop()
 tot = sum(v["ms"] for v in st.values())
 rows = sorted(st.items(), key=lambda kv: -kv[1]["ms"])
 print(f"total {tot:.2f} ms over {sum(v['launches'] for v in st.values())} launches")
-for k, v in rows[:60]:
+for k, v in rows[:90]:
     tf = f"{v['flops'] / max(v['ms'], 1e-9) / 1e9:7.1f} TF/s" if v["flops"] else ""
     print(f"{v['ms']:8.3f} ms {v['launches']:4d}x  {tf}  {k}")
