@@ -825,6 +825,39 @@ static int widen_bn(int bn, int cg, bool b_mn, int N, int num_kb) {
   return bn;
 }
 
+// Tile choice for bf16 STORE GEMMs (linears): a wave-aware cost over (BN, CTA pair) candidates,
+//   cost = waves(units, SMs / cg) * (num_kb * max(2*BN MMA cycles, L2 bytes per k-block / 80 B/clk)
+//          + 2500 [+1500 for the single-accumulator BN 320])
+// (fitted on the device-time sweep tools/tile_sweep2.py: e.g. 2048x1280x1280 prefers 128 single-CTA
+// 128x160 tiles in one wave over 40 pair tiles of 256x256; 8192^3 keeps pairs of 256).
+static void choose_tile(int M, int N, int K, bool b_mn, int& bn_out, int& cg_out) {
+  static const int forced_bn = env_int("DP_FORCE_BN"), forced_cg = env_int("DP_FORCE_CG");
+  const int num_kb = (K + BK - 1) / BK;
+  double best = -1.0;
+  for (int cg = 1; cg <= 2; ++cg) {
+    if (cg == 2 && (M < 256 || num_kb <= 8)) continue;  // short K: pairs measured slower
+    if (forced_cg && cg != forced_cg) continue;
+    for (int bn = 64; bn <= 320; bn += 32) {
+      if (bn == 288) continue;
+      if (b_mn && bn % 64) continue;
+      if (b_mn && cg == 2 && (bn / 2) % 64) continue;
+      if (bn == 320 && (cg != 2 || b_mn || num_kb < 16)) continue;
+      if (forced_bn && bn != forced_bn) continue;
+      const long long units = (long long)((M + 128 * cg - 1) / (128 * cg)) * ((N + bn - 1) / bn);
+      const long long per_wave = kNumSMs / cg;
+      const long long waves = (units + per_wave - 1) / per_wave;
+      const double l2 = (16384.0 + (bn / cg) * 128.0) / 80.0;
+      const double per_kb = (2.0 * bn > l2) ? 2.0 * bn : l2;
+      const double cost = waves * (num_kb * per_kb + 2500.0 + (bn > 256 ? 1500.0 : 0.0));
+      if (best < 0 || cost < best * 0.999 || (cost <= best * 1.001 && bn > bn_out)) {
+        best = cost;
+        bn_out = bn;
+        cg_out = cg;
+      }
+    }
+  }
+}
+
 // bf16 STORE outputs with TMA-legal strides are written by tensor stores (box 32 x 32,
 // SWIZZLE_64B); fp32 / atomic outputs keep the direct per-thread path.
 static int make_dmap(CUtensorMap* md, TcParams& p, int M, int N, int b1, int b2) {
@@ -1040,9 +1073,16 @@ int tc_gemm(const DpGemmArgs* a, cudaStream_t st, int64_t* query = nullptr) {
     set_error("atomic accumulation needs an fp32 output");
     return DP_ERR_ARGS;
   }
-  const int bn0 = pick_bn(a->N, a->b_mn_major != 0);
-  const int cg = decide_cg(a->M, bn0, a->b_mn_major != 0, a->K);
-  const int bn = widen_bn(bn0, cg, a->b_mn_major != 0, a->N, (a->K + BK - 1) / BK);
+  int bn, cg;
+  if (a->out_mode == DP_OUT_STORE && a->d_dtype == DP_BF16 && !env_int("DP_OLD_TILES")) {
+    bn = 64;
+    cg = 1;
+    choose_tile(a->M, a->N, a->K, a->b_mn_major != 0, bn, cg);
+  } else {
+    const int bn0 = pick_bn(a->N, a->b_mn_major != 0);
+    cg = decide_cg(a->M, bn0, a->b_mn_major != 0, a->K);
+    bn = widen_bn(bn0, cg, a->b_mn_major != 0, a->N, (a->K + BK - 1) / BK);
+  }
   TcParams p{};
   p.M = a->M;
   p.N = a->N;
