@@ -170,7 +170,10 @@ def test_splitk_bf16_linear(M, N, K):
     a.d_ld = a.r_ld = N
     a.d_dtype = _lib.DP_BF16
     a.Res = r.data_ptr()
-    assert _lib.lib().dp_gemm_workspace(ctypes.byref(a)) == 4 * M * N
+    ws = _lib.lib().dp_gemm_workspace(ctypes.byref(a))
+    assert ws in (0, 4 * M * N)
+    if M <= 256:  # a handful of tiles: always split
+        assert ws == 4 * M * N
     y = ops.linear(x, w, bias=b, residual=r)
     ref = x.float() @ w.float().t() + b + r.float()
     assert _rel(y, ref) < 1e-2
