@@ -23,7 +23,8 @@ def _rel(a, b):
 @pytest.mark.parametrize("dt", DT)
 @pytest.mark.parametrize("N,H,C,G,silu", [(2, 16, 64, 32, False), (3, 8, 320, 32, True),
                                           (2, 32, 128, 32, True), (1, 4, 2560, 32, True),
-                                          (2, 4, 4096, 32, True)])
+                                          (2, 4, 4096, 32, True), (4, 32, 320, 32, True),
+                                          (3, 16, 640, 32, False), (2, 64, 256, 32, True)])
 def test_group_norm(dt, N, H, C, G, silu):
     from paper_2405_01248_b200 import ops
     x = (torch.randn(N, H, H, C, device="cuda") * 2 + 0.5).to(dt)
