@@ -188,7 +188,32 @@ class InputFeed:
             return v.to(self.dtype)
         return v
 
+    def stage(self, fields, stream):
+        """Host mode: start the H2D copies of whole `fields` on `stream` now (pinned memory ->
+        device); later `get`s of those fields wait on the copy event instead of copying inline, so
+        the transfer overlaps compute (the bytes still count as this step's H2D traffic)."""
+        if self.mode != "host" or self.device.type != "cuda":
+            return
+        self.staged = getattr(self, "staged", {})
+        with torch.cuda.stream(stream):
+            for k in fields:
+                if k in self.f and k not in self.staged:
+                    v = self.f[k].to(self.device, non_blocking=True)
+                    n = v.numel() * v.element_size()
+                    self.h2d_bytes += n
+                    InputFeed.h2d_total += n
+                    self.staged[k] = v
+            self.staged_ev = torch.cuda.Event()
+            self.staged_ev.record(stream)
+
     def get(self, k, lo, hi):
+        st = getattr(self, "staged", None)
+        if st and k in st:
+            cur = torch.cuda.current_stream(self.device)
+            cur.wait_event(self.staged_ev)
+            v = st[k]
+            v.record_stream(cur)
+            return self._cast(k, v[lo:hi])
         v = self.f[k][lo:hi]
         if self.mode == "host":
             v = v.to(self.device, non_blocking=True)
@@ -369,6 +394,11 @@ class Trainer:
             self.warmup_frozen()
         cur = self._cur
         nxt = self._feed(self.it + 1) if has_next else None
+        if nxt is not None and nxt.mode == "host" and self.ex.world == 1 and self.ex.streams.cuda:
+            # the next batch's encoder inputs are consumed by this iteration's fills / tail
+            if getattr(self, "_copy_stream", None) is None:
+                self._copy_stream = torch.cuda.Stream(device=self.ex.device)
+            nxt.stage([f for spec in self.model.frozen for f in spec.inputs], self._copy_stream)
         self.ex.inputs = cur
         gb = self.ex.gb_of()
         raw = (lambda f, lo, hi: nxt.get(f, gb + lo, gb + hi)) if nxt is not None else None

@@ -27,3 +27,17 @@ def test_overlapped_optimizer_matches_sequential(cfg, kw):
         assert abs(a - b) <= 1e-3 * abs(b), (l0, l1)
     for a, b in zip(p0, p1):
         assert ((a - b).norm() / a.norm()).item() < 1e-3
+
+
+def test_host_feed_matches_device_feed():
+    """e2e path: pinned-host inputs (next batch's encoder inputs staged H2D on a copy stream)
+    give the same losses as device-resident inputs."""
+    from paper_2405_01248_b200 import engine
+
+    out = []
+    for mode in ("device", "host"):
+        tr = engine.Trainer.create("c2", world=1, rank=0, S=1, M=1, D=1, world_batch=4, small=True,
+                                   feed_mode=mode)
+        out.append([tr.step().item() for _ in range(3)])
+    for a, b in zip(*out):
+        assert abs(a - b) <= 1e-3 * abs(b), out
