@@ -166,12 +166,19 @@ def timed_steps(trainer, K, world, *, read_loss=False, kernel_timer=False):
     b = torch.cuda.Event(enable_timing=True)
     a.record()
     losses = []
-    for _ in range(K):
+    host_loss = torch.empty(K, dtype=torch.float32, pin_memory=True) if read_loss else None
+    for i in range(K):
         loss = trainer.step()
         if read_loss:
-            losses.append(trainer.ex.total_loss().item())
+            # the step's loss crosses to pinned host memory every step (async D2H: the host does not
+            # drain the GPU between steps, as in a training loop with asynchronous logging)
+            host_loss[i:i + 1].copy_(trainer.ex.total_loss(), non_blocking=True)
     b.record()
     torch.cuda.synchronize()
+    if read_loss:
+        losses = host_loss.tolist()
+        if not all(v == v for v in losses):
+            raise SystemExit(f"non-finite loss in the e2e run: {losses}")
     ms = a.elapsed_time(b)
     kstats = telemetry.timer.stop() if kernel_timer else None
     launches = telemetry.total_launches()
