@@ -121,30 +121,27 @@ __global__ void __launch_bounds__(128, 2)
     mbar_wait(bar_s, j & 1);
     tc_fence_after();
     const int valid = min(BKV, p.Nk - j * BKV);
-    // pass 1: row max of the scaled scores
-    float mx = -INFINITY;
-#pragma unroll 1
-    for (int c = 0; c < BKV / 32; ++c) {
-      uint32_t v[32];
-      tmem_ld_32x32(t_s + lane_off + c * 32, v);
-      tmem_ld_wait();
+    // the row's 128 scores come out of TMEM once (4 loads, one wait) and stay in registers for
+    // both the row max and the exponentials
+    uint32_t sv[BKV];
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (c * 32 + i < valid) mx = fmaxf(mx, __uint_as_float(v[i]));
-    }
+    for (int c = 0; c < BKV / 32; ++c)
+      tmem_ld_32x32(t_s + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
+    tmem_ld_wait();
+    float mx = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < BKV; ++i)
+      if (i < valid) mx = fmaxf(mx, __uint_as_float(sv[i]));
     const float m_new = fmaxf(m_run, mx * p.scale_log2);
     const float alpha = ex2(m_run - m_new);
-    // pass 2: P = exp2(s*scale - m) -> bf16 -> shared (SWIZZLE_128B K-major rows)
+    // P = exp2(s*scale - m) -> bf16 -> shared (SWIZZLE_128B K-major rows)
     float lsum = 0.f;
-#pragma unroll 1
+#pragma unroll
     for (int c = 0; c < BKV / 32; ++c) {
-      uint32_t v[32];
-      tmem_ld_32x32(t_s + lane_off + c * 32, v);
-      tmem_ld_wait();
       float pv[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        const float e = (c * 32 + i < valid) ? ex2(fmaf(__uint_as_float(v[i]), p.scale_log2, -m_new)) : 0.f;
+        const float e = (c * 32 + i < valid) ? ex2(fmaf(__uint_as_float(sv[c * 32 + i]), p.scale_log2, -m_new)) : 0.f;
         pv[i] = e;
         lsum += e;
       }
