@@ -387,12 +387,18 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_after();
     const float* lse = sLse + qb * 128;
     const float* Dq = sD + qb * 128;
-#pragma unroll 1
-    for (int c = half * 2; c < half * 2 + 2; ++c) {
-      uint32_t sv[32], dv[32];
-      tmem_ld_32x32(t_st + lane_off + c * 32, sv);
-      tmem_ld_32x32(t_dpt + lane_off + c * 32, dv);
-      tmem_ld_wait();
+    uint32_t sva[2][32], dva[2][32];  // both 32-query chunks of this half, one TMEM wait
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      tmem_ld_32x32(t_st + lane_off + (half * 2 + u) * 32, sva[u]);
+      tmem_ld_32x32(t_dpt + lane_off + (half * 2 + u) * 32, dva[u]);
+    }
+    tmem_ld_wait();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int c = half * 2 + u;
+      const uint32_t (&sv)[32] = sva[u];
+      const uint32_t (&dv)[32] = dva[u];
       float pt[32], dst[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
