@@ -310,6 +310,13 @@ def main():
         e2e = {"value": wb * K / (ms_e / 1000.0), "unit": "samples/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 4}
 
+    # memory-feasibility model vs the measured peak of this run (memory.py)
+    mem = {"measured_peak_gb": round(torch.cuda.max_memory_allocated() / 1e9, 2)}
+    try:
+        mem["predicted_gb"] = round(trainer.memory_report()[trainer.ex.dev] / 1e9, 2)
+    except Exception as e:  # the report is informative; never fail the bench line on it
+        mem["predicted_error"] = str(e)[:120]
+
     pk, pk_kind = peaks()
     roof = None
     if kstats:
@@ -351,7 +358,7 @@ def main():
             "bubble_ratio_measured": br_meas,
             "bubble_ratio_measured_unfilled": br_meas_unf,
             "speedup_vs_unfilled": speedup,
-            "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "memory": mem,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

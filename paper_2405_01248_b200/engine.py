@@ -407,6 +407,16 @@ class Trainer:
         self.it += 1
         return loss
 
+    def memory_report(self, batch=2):
+        """Predicted bytes per device of this rank's pipeline group (memory.py: parameters, frozen
+        weights, activations kept for the backward x micro-batches in flight, held frozen outputs)."""
+        from . import memory
+
+        probe = make_batch(replace(self.data_spec, world_batch=batch), 10 ** 6 + 1)
+        feed = InputFeed(probe, self.device, self.cfg.dtype)
+        act = memory.measure_layer_activation_bytes(self.model, lambda k, b: feed.get(k, 0, b), self.device, batch)
+        return memory.predict_device_bytes(self.ex.prog0, self.model, act, self.ex.frozen_specs)
+
     def measured(self, min_len=0.0):
         """Measured schedule of the last traced step (collective over the job): returns
         (Schedule, bubbles, bubble_ratio) computed with the planner's own extract_bubbles /
