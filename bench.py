@@ -239,6 +239,7 @@ def main():
     ap.add_argument("--per-gpu-batch", type=int, default=32)
     ap.add_argument("--debug-share-gpu", action="store_true",
                     help="TEST ONLY: run all ranks on cuda:0 over gloo (validates the N>1 path)")
+    ap.add_argument("--trace-out", default=None, help="write the measured schedule as a trace-event JSON")
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS),
                     help="the headline (BASELINE.json metric) workload is c2; c3..c5 for reference")
     ap.add_argument("--graph", action="store_true",
@@ -280,8 +281,12 @@ def main():
     # CUDA events on their streams, bubbles / ratio by the planner's own definitions
     barrier(world)
     trainer.step(trace=True)
-    _, _, br_meas = trainer.measured()
+    sched_meas, _, br_meas = trainer.measured()
     br_meas_unf = None
+    if args.trace_out and rank == 0:
+        # measured schedule in the reference's trace-event format (scheduler.py:483-519)
+        from paper_2405_01248_b200.pipefill import scheduler as psched
+        psched.export_trace(sched_meas, args.trace_out)
 
     # speedup vs the same executor's unfilled pipeline (frozen part data-parallel, un-overlapped)
     speedup = 1.0
