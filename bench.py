@@ -273,6 +273,7 @@ def main():
         trainer.enable_cuda_graph()
         for _ in range(W):
             trainer.step()
+    torch.cuda.reset_peak_memory_stats()  # the memory line reflects training steps only
     with Clocks(local) as clk:
         ms, _, launches, _ = timed_steps(trainer, K, world)
     value = wb * K / (ms / 1000.0)

@@ -9,7 +9,7 @@ Per device of a GroupProgram the model adds
     (`measure_layer_activation_bytes`) x the stage's per-replica micro-batch x the micro-batches in flight at
     the stage under 1F1B (min(M, S - s));
   * frozen outputs held for the next iteration (latents / context of the group batch, twice: being produced
-    and being consumed).
+    and being consumed), plus the largest frozen layer's input + output over the group batch (transient).
 `check_plan` raises MemoryError when a device exceeds the budget; the planner API itself is unchanged.
 """
 
@@ -32,13 +32,12 @@ def _store_bytes(store, trainable):
 def measure_layer_activation_bytes(model, batch_fn, device, batch=2):
     """Per backbone, per layer: bytes per sample allocated (and kept alive for the backward) by the
     layer's forward with autograd recording, measured with torch.cuda.memory_allocated on `device`."""
-    from .profiler import probe_specs  # noqa: F401  (same probing conventions)
+    from .adapter import topo_order
 
     dev = torch.device(device)
     fro = {}
     deps = getattr(model, "frozen_deps", ())
     finals = {}
-    from .adapter import topo_order
     with torch.no_grad():
         for c in topo_order(len(model.frozen), deps):
             f = model.frozen[c]
@@ -83,11 +82,16 @@ def predict_device_bytes(prog, model, act_bytes, frozen_specs=None):
                  if getattr(f.component, "store", None) is not None
                  and f.component.store is not getattr(model.backbone, "store", None))
     held = 0
+    transient = 0
     if frozen_specs:
+        def nbytes(spec):
+            return sum(math.prod(shape) * torch.tensor([], dtype=dt).element_size() for shape, dt in spec.values())
         for c, specs in enumerate(frozen_specs):
-            last = specs[-1]
-            per = sum(math.prod(shape) * torch.tensor([], dtype=dt).element_size() for shape, dt in last.values())
-            held += 2 * per * prog.group_batch
+            held += 2 * nbytes(specs[-1]) * prog.group_batch
+            # a frozen layer's input + output for the largest piece a device runs (<= the group batch)
+            for j in range(1, len(specs)):
+                transient = max(transient, (nbytes(specs[j - 1]) + nbytes(specs[j])) * prog.group_batch)
+    held += transient
     out = {}
     for dev in range(prog.D):
         dp = prog.device_program(dev)
