@@ -126,6 +126,9 @@ int dp_flash_attn_fwd(const DpAttnArgs* args, dp_stream_t stream);
 /* fused attention backward (recomputes P from args->lse): dq (token stride dq_ld), dk/dv
    (token stride dkv_ld) for the o written by dp_flash_attn_fwd; workspace holds
    B*heads*N + B*N*heads*64 floats */
+/* bytes of fp32 workspace dp_flash_attn_bwd needs for these args (D, dQ accumulator and, when the
+   query tiles are split across CTAs, the dK/dV accumulators) */
+int64_t dp_flash_attn_bwd_workspace(const DpAttnArgs* args);
 int dp_flash_attn_bwd(const DpAttnArgs* args, const void* dout, int64_t do_ld, void* dq,
                       int64_t dq_ld, void* dk, void* dv, int64_t dkv_ld, float* workspace,
                       dp_stream_t stream);

@@ -74,6 +74,7 @@ _SIGNATURES = {
     "dp_conv_wgrad": [ctypes.POINTER(DpConvArgs), c_void_p],
     "dp_conv_dgrad": [ctypes.POINTER(DpConvArgs), c_void_p],
     "dp_flash_attn_fwd": [ctypes.POINTER(DpAttnArgs), c_void_p],
+    "dp_flash_attn_bwd_workspace": [ctypes.POINTER(DpAttnArgs)],
     "dp_flash_attn_bwd": [ctypes.POINTER(DpAttnArgs), c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_void_p,
                           c_i64, c_void_p, c_void_p],
     "dp_im2col": [c_int, c_void_p, c_void_p] + [c_int] * 11 + [c_void_p],
@@ -132,7 +133,7 @@ _SIGNATURES = {
     "dp_version": [],
 }
 _RESTYPES = {"dp_last_error": ctypes.c_char_p, "dp_group_norm_workspace": ctypes.c_size_t,
-             "dp_gemm_workspace": c_i64, "dp_conv_fwd_workspace": c_i64, "dp_conv_dgrad_workspace": c_i64}
+             "dp_gemm_workspace": c_i64, "dp_flash_attn_bwd_workspace": c_i64, "dp_conv_fwd_workspace": c_i64, "dp_conv_dgrad_workspace": c_i64}
 
 _lib = None
 

@@ -12,6 +12,7 @@
 //     log-sum-exp saved for the backward pass.
 // Two CTAs fit per SM (96 KB shared memory, 256 TMEM columns each), so one CTA's softmax
 // overlaps the other's MMAs. Keys beyond N_k (cross-attention, 77 tokens) are masked.
+#include <cstdlib>
 #include <string>
 #include <cudaTypedefs.h>
 #include "common.cuh"
@@ -230,42 +231,57 @@ __global__ void __launch_bounds__(128, 2)
 constexpr size_t SMEM = 1024 + 6 * TILE_BYTES + 64;
 
 // ------------------------------------------------------------------ backward
-// D[b][h][n] = sum_d dO[b][n][h*64+d] * O[b][n][h*64+d]   (one warp per (b, n, h) row)
-__global__ void fa_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
-                                   float* __restrict__ Dv, int B, int N, int heads, int64_t o_ld,
-                                   int64_t do_ld) {
+// D[b][h][n] = sum_d dO[b][n][h*64+d] * O[b][n][h*64+d]: rows taken in memory order (b, n, h), eight
+// threads per 128-byte row (16-byte loads), shuffle reduction inside the 8-lane group
+__global__ void __launch_bounds__(256) fa_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
+                                                          const __nv_bfloat16* __restrict__ dout,
+                                                          float* __restrict__ Dv, int B, int N, int heads,
+                                                          int64_t o_ld, int64_t do_ld) {
   DP_PDL_ENTRY();
-  const int lane = threadIdx.x & 31;
-  const int64_t r = blockIdx.x * 8LL + (threadIdx.x >> 5);  // (b, h, n) flattened
-  const int64_t total = (int64_t)B * heads * N;
-  if (r >= total) return;
-  const int n = static_cast<int>(r % N);
-  const int64_t bh = r / N;
-  const int h = static_cast<int>(bh % heads);
-  const int b = static_cast<int>(bh / heads);
-  const __nv_bfloat16* op = o + ((int64_t)b * N + n) * o_ld + h * HD;
-  const __nv_bfloat16* dp = dout + ((int64_t)b * N + n) * do_ld + h * HD;
-  const __nv_bfloat162 a = reinterpret_cast<const __nv_bfloat162*>(op)[lane];
-  const __nv_bfloat162 c = reinterpret_cast<const __nv_bfloat162*>(dp)[lane];
-  float s = __bfloat162float(a.x) * __bfloat162float(c.x) + __bfloat162float(a.y) * __bfloat162float(c.y);
-  s = warp_sum(s);
-  if (lane == 0) Dv[r] = s;
+  const int sub = threadIdx.x & 7;
+  const int64_t total = (int64_t)B * N * heads;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3; r < total;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 3) {
+    const int h = static_cast<int>(r % heads);
+    const int64_t bn = r / heads;
+    const int n = static_cast<int>(bn % N);
+    const int b = static_cast<int>(bn / N);
+    const uint4 a = *reinterpret_cast<const uint4*>(o + ((int64_t)b * N + n) * o_ld + h * HD + sub * 8);
+    const uint4 c = *reinterpret_cast<const uint4*>(dout + ((int64_t)b * N + n) * do_ld + h * HD + sub * 8);
+    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&c);
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 fa = __bfloat1622float2(a2[j]), fc = __bfloat1622float2(c2[j]);
+      s = fmaf(fa.x, fc.x, fmaf(fa.y, fc.y, s));
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (sub == 0) Dv[((int64_t)b * heads + h) * N + n] = s;
+  }
 }
 
-// out[b][n][h*64+d] (bf16, token stride out_ld) = alpha * acc[b][n][h][d] (fp32, dense)
+// out[b][n][h*64+d] (bf16, token stride out_ld) = alpha * acc[b][n][h][d] (fp32, dense): 8 elements
+// per thread (two 16-byte loads, one 16-byte store)
 __global__ void fa_dq_cast_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ out,
                                   int64_t rows, int C, int64_t out_ld, float alpha) {
   DP_PDL_ENTRY();
-  const int64_t n = rows * C;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n / 2;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = 2 * i;
-    const int64_t r = e / C;
-    const int c = static_cast<int>(e - r * C);
-    const float2 v = reinterpret_cast<const float2*>(acc)[i];
-    reinterpret_cast<__nv_bfloat162*>(out + r * out_ld + c)[0] = __floats2bfloat162_rn(alpha * v.x, alpha * v.y);
-  }
-}
+  const int cv = C / 8;
+  const int64_t n = rows * cv;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cv;
+    const int c = static_cast<int>(i - r * cv) * 8;
+    const float4 u = reinterpret_cast<const float4*>(acc)[2 * i];
+    const float4 v = reinterpret_cast<const float4*>(acc)[2 * i + 1];
+    uint4 o;
+    o.x = pack_bf16x2(alpha * u.x, alpha * u.y);
+    o.y = pack_bf16x2(alpha * u.z, alpha * u.w);
+    o.z = pack_bf16x2(alpha * v.x, alpha * v.y);
+    o.w = pack_bf16x2(alpha * v.z, alpha * v.w);
+    *reinterpret_cast<uint4*>(out + r * out_ld + c) = o;
+  }}
 
 struct BwdParams {
   int N, Nk, heads;
@@ -274,6 +290,8 @@ struct BwdParams {
   const float* lse;   // [B][heads][N]
   const float* Dv;    // [B][heads][N]
   float* dq_acc;      // [B][N][heads][64] fp32, zero-initialised
+  int qsplit;         // CTAs per key tile (query tiles split between them)
+  float* dkv_acc;     // qsplit > 1: [2][B][Nk][heads][64] fp32 dK (unscaled), dV, zero-initialised
 };
 
 // One CTA = one 128-key tile of one (batch, head); thread t owns key row t (S^T, dP^T rows).
@@ -312,9 +330,13 @@ __global__ void __launch_bounds__(256, 1)
   const int warp = tid >> 5;
   const int row = tid & 127;   // key row (TMEM lane) of this thread
   const int half = tid >> 7;   // column half
-  const int kt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int kt = blockIdx.x / p.qsplit, h = blockIdx.y, b = blockIdx.z;
   const int k0 = kt * BKV;
   const int nq = (p.N + BQ - 1) / BQ;
+  // query tiles [i0, i1) of this CTA (split when there are too few key tiles to fill the SMs)
+  const int per = (nq + p.qsplit - 1) / p.qsplit;
+  const int i0 = (blockIdx.x % p.qsplit) * per;
+  const int i1 = min(nq, i0 + per);
   const int64_t bh = (int64_t)b * p.heads + h;
 
   if (tid == 0) {
@@ -342,8 +364,8 @@ __global__ void __launch_bounds__(256, 1)
     mbar_expect_tx(bar_kv, 2 * TILE_BYTES);
     tma_load_4d(&tmK, bar_kv, sK, 0, k0, h, b);
     tma_load_4d(&tmV, bar_kv, sV, 0, k0, h, b);
-    load_q(0, 0);
-    if (nq > 1) load_q(1, 1);
+    load_q(i0, 0);
+    if (i0 + 1 < i1) load_q(i0 + 1, 1);
   }
   // lse / D of the first query tile (rows >= N: lse = +inf -> P = 0)
   auto load_rows = [&](int i, int buf) {
@@ -352,7 +374,7 @@ __global__ void __launch_bounds__(256, 1)
     sLse[buf * 128 + row] = q < p.N ? p.lse[bh * p.N + q] : INFINITY;
     sD[buf * 128 + row] = q < p.N ? p.Dv[bh * p.N + q] : 0.f;
   };
-  load_rows(0, 0);
+  load_rows(i0, 0);
   const uint32_t id_sq = idesc_bf16_f32(BKV, BQ, 0, 0);  // S^T / dP^T: M=keys, N=queries, K=64
   const uint32_t id_acc = idesc_bf16_f32(BKV, HD, 0, 1); // dV / dK: M=keys, N=64, K=queries
   const uint32_t id_dq = idesc_bf16_f32(BQ, HD, 1, 1);   // dQ: M=queries (A MN-major), N=64
@@ -361,10 +383,10 @@ __global__ void __launch_bounds__(256, 1)
   // S^T / dP^T of query tile i: issued by thread 0 right after tile i-1's accumulator MMAs, so
   // the tensor pipe computes them while the warps drain tile i-1's dQ (in-order MMA pipe: they
   // complete after the dV/dK/dQ MMAs that still read P^T / dS^T from shared memory)
-  auto issue_sdp = [&](int i) {
-    const int qb = i & 1;
-    if (i == 0) mbar_wait(bar_kv, 0);
-    mbar_wait(&bar_q[qb], (i >> 1) & 1);
+  auto issue_sdp = [&](int li) {  // li: tile index local to this CTA
+    const int qb = li & 1;
+    if (li == 0) mbar_wait(bar_kv, 0);
+    mbar_wait(&bar_q[qb], (li >> 1) & 1);
     tc_fence_after();
     const uint32_t ka = smem_u32(sK), va = smem_u32(sV);
     const uint32_t qa = smem_u32(sQ + qb * TILE_BYTES), da = smem_u32(sDO + qb * TILE_BYTES);
@@ -379,11 +401,12 @@ __global__ void __launch_bounds__(256, 1)
   };
   if (tid == 0) issue_sdp(0);
 
-  for (int i = 0; i < nq; ++i) {
-    const int qb = i & 1;
+  for (int i = i0; i < i1; ++i) {
+    const int li = i - i0;
+    const int qb = li & 1;
     __syncthreads();  // sLse/sD of tile i visible; previous tile's smem/TMEM consumers done
-    if (i + 1 < nq) load_rows(i + 1, qb ^ 1);
-    mbar_wait(bar_sp, i & 1);
+    if (i + 1 < i1) load_rows(i + 1, qb ^ 1);
+    mbar_wait(bar_sp, li & 1);
     tc_fence_after();
     const float* lse = sLse + qb * 128;
     const float* Dq = sD + qb * 128;
@@ -437,10 +460,10 @@ __global__ void __launch_bounds__(256, 1)
         const uint32_t aoff = (k >> 2) * TILE_BYTES + (k & 3) * 32;  // K-major over queries
         // dV += P^T dO    (B(n=d, k=q) = dO[q][d]: MN-major)
         tc_mma_bf16(t_dv, smem_desc_sw128(pta + aoff, 16, 1024), smem_desc_sw128(da + k * 2048, 8192, 1024),
-                    id_acc, (i > 0 || k > 0) ? 1u : 0u);
+                    id_acc, (li > 0 || k > 0) ? 1u : 0u);
         // dK += dS^T Q    (B(n=d, k=q) = Q[q][d]: MN-major)
         tc_mma_bf16(t_dk, smem_desc_sw128(dsa + aoff, 16, 1024), smem_desc_sw128(qa + k * 2048, 8192, 1024),
-                    id_acc, (i > 0 || k > 0) ? 1u : 0u);
+                    id_acc, (li > 0 || k > 0) ? 1u : 0u);
       }
 #pragma unroll
       for (int k = 0; k < BKV / 16; ++k) {
@@ -450,11 +473,11 @@ __global__ void __launch_bounds__(256, 1)
                     smem_desc_sw128(ka + k * 2048, 8192, 1024), id_dq, k > 0 ? 1u : 0u);
       }
       tc_commit(bar_acc);
-      if (i + 1 < nq) issue_sdp(i + 1);
+      if (i + 1 < i1) issue_sdp(li + 1);
     }
-    mbar_wait(bar_acc, i & 1);
+    mbar_wait(bar_acc, li & 1);
     tc_fence_after();
-    if (tid == 0 && i + 2 < nq) load_q(i + 2, qb);  // Q/dO buffer qb is free again
+    if (tid == 0 && i + 2 < i1) load_q(i + 2, qb);  // Q/dO buffer qb is free again
     // dQ rows of this query tile -> fp32 atomics (thread = query row, half = 32-column chunk)
     const int q = i * BQ + row;
     {
@@ -475,6 +498,34 @@ __global__ void __launch_bounds__(256, 1)
   }
   __syncthreads();
   tc_fence_after();
+  if (p.qsplit > 1) {
+    // partial dK / dV over this CTA's query tiles -> fp32 atomics (scale and bf16 cast afterwards)
+    const int c = half;
+    uint32_t vk[32], vv[32];
+    tmem_ld_32x32(t_dk + lane_off + c * 32, vk);
+    tmem_ld_32x32(t_dv + lane_off + c * 32, vv);
+    tmem_ld_wait();
+    if (key_valid) {
+      const int64_t off = (((int64_t)b * p.Nk + k0 + row) * p.heads + h) * HD + c * 32;
+      const int64_t plane = (int64_t)gridDim.z * p.Nk * p.heads * HD;
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        atomicAdd(reinterpret_cast<float4*>(p.dkv_acc + off + j),
+                  make_float4(__uint_as_float(vk[j]), __uint_as_float(vk[j + 1]), __uint_as_float(vk[j + 2]),
+                              __uint_as_float(vk[j + 3])));
+        atomicAdd(reinterpret_cast<float4*>(p.dkv_acc + plane + off + j),
+                  make_float4(__uint_as_float(vv[j]), __uint_as_float(vv[j + 1]), __uint_as_float(vv[j + 2]),
+                              __uint_as_float(vv[j + 3])));
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+      tc_fence_after();
+      tmem_dealloc<512>(tmem);
+    }
+    return;
+  }
   // dK (scaled), dV -> bf16 -> shared (reuse the Q buffers) -> TMA stores (thread = key row)
   uint8_t* sdk = sQ;
   uint8_t* sdv = sQ + TILE_BYTES;
@@ -584,6 +635,32 @@ extern "C" int dp_flash_attn_fwd(const DpAttnArgs* a, dp_stream_t stream) {
   return 0;
 }
 
+// query-tile split of the backward: key-tile CTAs x heads x batch below two per SM -> give each key tile
+// several CTAs (each a contiguous range of query tiles, dK/dV reduced with fp32 atomics)
+static int fa_bwd_qsplit(const DpAttnArgs* a) {
+  using namespace dp;
+  const long long nkt = (a->Nk + fa::BKV - 1) / fa::BKV;
+  const int nq = (a->N + fa::BQ - 1) / fa::BQ;
+  const long long ctas = nkt * a->heads * a->B;
+  static const int forced = [] {
+    const char* e = getenv("DP_FA_QSPLIT");  // experiments only
+    return e ? atoi(e) : 0;
+  }();
+  if (forced > 0) return forced <= nq ? forced : nq;
+  if (ctas >= 2LL * 148 || nq < 2) return 1;
+  int q = static_cast<int>((2LL * 148 + ctas - 1) / ctas);
+  if (q > nq) q = nq;
+  const int per = (nq + q - 1) / q;
+  return (nq + per - 1) / per;  // no empty splits
+}
+
+extern "C" int64_t dp_flash_attn_bwd_workspace(const DpAttnArgs* a) {
+  const int64_t C = (int64_t)a->heads * 64;
+  int64_t floats = (int64_t)a->B * a->heads * a->N + (int64_t)a->B * a->N * C;
+  if (fa_bwd_qsplit(a) > 1) floats += 2 * (int64_t)a->B * a->Nk * C;
+  return floats * 4;
+}
+
 extern "C" int dp_flash_attn_bwd(const DpAttnArgs* a, const void* dout, int64_t do_ld, void* dq,
                                  int64_t dq_ld, void* dk, void* dv, int64_t dkv_ld, float* workspace,
                                  dp_stream_t stream) {
@@ -601,7 +678,9 @@ extern "C" int dp_flash_attn_bwd(const DpAttnArgs* a, const void* dout, int64_t 
   cudaMemsetAsync(dq_acc, 0, sizeof(float) * rows * C, st);
   {
     const int64_t total = (int64_t)a->B * a->heads * a->N;
-    fa::fa_bwd_prep_kernel<<<static_cast<unsigned>((total + 7) / 8), 256, 0, st>>>(
+    int gp = static_cast<int>((total * 8 + 255) / 256);
+    if (gp > 148 * 8) gp = 148 * 8;
+    fa::fa_bwd_prep_kernel<<<gp, 256, 0, st>>>(
         reinterpret_cast<const __nv_bfloat16*>(a->o), reinterpret_cast<const __nv_bfloat16*>(dout), Dv, a->B,
         a->N, a->heads, a->o_ld, do_ld);
   }
@@ -622,10 +701,24 @@ extern "C" int dp_flash_attn_bwd(const DpAttnArgs* a, const void* dout, int64_t 
     }
     attr = true;
   }
-  fa::BwdParams p{a->N, a->Nk, a->heads, a->scale * 1.4426950408889634f, a->scale, a->lse, Dv, dq_acc};
-  dim3 grid((a->Nk + fa::BKV - 1) / fa::BKV, a->heads, a->B);
+  const int qsplit = fa_bwd_qsplit(a);
+  float* dkv_acc = dq_acc + rows * C;  // [2][B][Nk][heads][64] (split only)
+  const int64_t kv_rows = (int64_t)a->B * a->Nk;
+  if (qsplit > 1) cudaMemsetAsync(dkv_acc, 0, sizeof(float) * 2 * kv_rows * C, st);
+  fa::BwdParams p{a->N, a->Nk, a->heads, a->scale * 1.4426950408889634f, a->scale, a->lse, Dv, dq_acc,
+                  qsplit, dkv_acc};
+  dim3 grid((a->Nk + fa::BKV - 1) / fa::BKV * qsplit, a->heads, a->B);
   launch_k(fa::fa_bwd_kernel, dim3(grid), dim3(256), fa::BWD_SMEM, st, mq, mk, mv, mdo, mdk, mdv, p);
-  const int64_t n2 = rows * C / 2;
+  if (qsplit > 1) {
+    const int64_t nk2 = kv_rows * C / 8;
+    int gk = static_cast<int>((nk2 + 255) / 256);
+    if (gk > 148 * 8) gk = 148 * 8;
+    launch_k(fa::fa_dq_cast_kernel, dim3(gk), dim3(256), 0, st, dkv_acc, reinterpret_cast<__nv_bfloat16*>(dk),
+             kv_rows, C, dkv_ld, a->scale);
+    launch_k(fa::fa_dq_cast_kernel, dim3(gk), dim3(256), 0, st, dkv_acc + kv_rows * C,
+             reinterpret_cast<__nv_bfloat16*>(dv), kv_rows, C, dkv_ld, 1.0f);
+  }
+  const int64_t n2 = rows * C / 8;
   int g = static_cast<int>((n2 + 255) / 256);
   if (g > 148 * 8) g = 148 * 8;
   launch_k(fa::fa_dq_cast_kernel, dim3(g), dim3(256), 0, st, dq_acc, reinterpret_cast<__nv_bfloat16*>(dq), rows, C, dq_ld,

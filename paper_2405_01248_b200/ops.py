@@ -635,7 +635,7 @@ def flash_attn_fwd(q, k, v, o, *, B, N, Nk, heads, q_ld, kv_ld, o_ld, scale, lse
 def flash_attn_bwd(q, k, v, o, do, dq, dk, dv, lse, *, B, N, Nk, heads, q_ld, kv_ld, o_ld, do_ld, dq_ld,
                    dkv_ld, scale):
     a = _attn_args(q, k, v, o, B, N, Nk, heads, q_ld, kv_ld, o_ld, scale, lse)
-    ws = torch.empty(B * heads * N + B * N * heads * 64, device=o.device, dtype=torch.float32)
+    ws = torch.empty(_L().dp_flash_attn_bwd_workspace(ctypes.byref(a)) // 4, device=o.device, dtype=torch.float32)
     flops = 10.0 * B * heads * N * Nk * 64  # S, dP, dV, dK, dQ recomputation + products
     telemetry.timed("tcgen05_gemm", flops,
                     lambda: check(_L().dp_flash_attn_bwd(ctypes.byref(a), _ptr(do), do_ld, _ptr(dq), dq_ld,

@@ -88,7 +88,8 @@ class TimedLib:
         f = getattr(self._lib, name)
         if not callable(f) or timer.depth > 0 or name in ("dp_last_error", "dp_version",
                                                          "dp_group_norm_workspace", "dp_gemm_workspace",
-                                                         "dp_conv_fwd_workspace", "dp_conv_dgrad_workspace"):
+                                                         "dp_conv_fwd_workspace", "dp_conv_dgrad_workspace",
+                                                         "dp_flash_attn_bwd_workspace"):
             return f
 
         def call(*args):
