@@ -27,9 +27,15 @@ class _Timer:
         self.active = False
         self.records = []
         self.depth = 0
+        self.pool = []  # pre-created timing events (event creation kept off the timed path)
 
-    def start(self):
+    def event(self):
+        return self.pool.pop() if self.pool else torch.cuda.Event(enable_timing=True)
+
+    def start(self, reserve=0):
         self.records = []
+        if len(self.pool) < reserve:
+            self.pool.extend(torch.cuda.Event(enable_timing=True) for _ in range(reserve - len(self.pool)))
         self.active = True
 
     def stop(self):
@@ -42,6 +48,7 @@ class _Timer:
             f["launches"] += 1
             f["flops"] += flops
             f["ms"] += ms
+            self.pool.extend((a, b))
         self.records = []
         return out
 
@@ -65,8 +72,8 @@ def timed(family, flops, fn, sub=None):
         return fn()
     s = getattr(_site, "name", None) or sub
     fam = f"{family}.{s}" if s else family
-    a = torch.cuda.Event(enable_timing=True)
-    b = torch.cuda.Event(enable_timing=True)
+    a = timer.event()
+    b = timer.event()
     a.record()
     timer.depth += 1
     try:
