@@ -1021,6 +1021,15 @@ static void choose_split(TcParams& p, int requested, bool allowed) {
   const int tiles = p.tiles_m * p.tiles_n * p.nbatch;
   int splits = 1;
   p.stream_k = 0;
+  static const int sk_target = env_int("DP_SK_TARGET");  // experiments: split-K to ~N CTAs
+  if (allowed && requested <= 0 && sk_target > 0) {
+    splits = (sk_target + tiles - 1) / tiles;
+    const int max_split = p.num_kb / 4 > 0 ? p.num_kb / 4 : 1;
+    if (splits > max_split) splits = max_split;
+    p.kb_per_split = (p.num_kb + splits - 1) / splits;
+    p.splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
+    return;
+  }
   if (allowed && requested <= 0 && tiles < 2 * kNumSMs && (long long)tiles * p.num_kb >= 4 * kNumSMs) {
     // fp32 atomic output: balance k-iterations over all SMs (stream-K)
     p.stream_k = 1;
