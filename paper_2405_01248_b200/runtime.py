@@ -185,6 +185,7 @@ class Links:
 
 _DEBUG = bool(int(__import__("os").environ.get("DP_DEBUG_P2P", "0")))
 _OVL_SIDE = __import__("os").environ.get("DP_OVL_STREAM", "opt") == "opt"  # experiments: "compute"
+_EARLY_TAIL = bool(int(__import__("os").environ.get("DP_EARLY_TAIL", "0")))  # experiments
 
 
 class _Tracer:
@@ -734,6 +735,12 @@ class PipelineExecutor:
         task = tr.task if tr else (lambda *a, **k: contextlib.nullcontext())
         last_compute_ev = None
         instrs = prog.device_program(self.dev).instrs
+        early_tail = _EARLY_TAIL and self.world == 1 and self.streams.cuda and has_next and bool(prog.tail)
+        if early_tail:
+            # experiment: the single-device tail (no bubbles) issued on the low-priority fill stream at
+            # the start of the iteration, concurrent with the backbone
+            with self.streams.on("fill"), task("fill", "fill", tag="tail"):
+                self._run_pieces(prog, prog.tail, store, raw_next, posted, sent)
         for ins in instrs:
             kind = ins[0]
             if kind in ("fwd", "fwd_sc", "bwd"):
@@ -757,7 +764,7 @@ class PipelineExecutor:
                                                       direction=prog.pipes[ins[2]].direction):
                     self._sync(ins[2])
             elif kind == "tail":
-                if not has_next:
+                if not has_next or early_tail:
                     continue
                 self.streams.join()
                 # leftover frozen work: busy time (planner.py:172-175), recorded as a fill task
