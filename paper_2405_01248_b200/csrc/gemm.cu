@@ -249,7 +249,10 @@ DP_DEV void stage_row_bf16(uint8_t* buf, int lane, const float (&f)[32]) {
     u.z = pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]);
     u.w = pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]);
     const int qs = q ^ ((lane >> 1) & 3);
-    *reinterpret_cast<uint4*>(buf + lane * 64 + qs * 16) = u;
+    // st.shared (not a generic store): the staging buffer is known to be shared memory
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(buf + lane * 64 + qs * 16)),
+                 "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w)
+                 : "memory");
   }
 }
 
