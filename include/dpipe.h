@@ -112,6 +112,7 @@ typedef struct DpAttnArgs {
   int64_t q_ld, q_bs, kv_ld, kv_bs, o_ld, o_bs;
   float scale;
   float* lse;
+  int causal; /* forward only: key j > query i masked (N == Nk; CLIP's causal text encoder) */
 } DpAttnArgs;
 
 int dp_gemm(const DpGemmArgs* args, dp_stream_t stream);

@@ -60,7 +60,7 @@ class DpAttnArgs(ctypes.Structure):
         ("dtype", c_int), ("B", c_int), ("N", c_int), ("Nk", c_int), ("heads", c_int), ("head_dim", c_int),
         ("q", c_void_p), ("k", c_void_p), ("v", c_void_p), ("o", c_void_p),
         ("q_ld", c_i64), ("q_bs", c_i64), ("kv_ld", c_i64), ("kv_bs", c_i64), ("o_ld", c_i64), ("o_bs", c_i64),
-        ("scale", c_float), ("lse", c_void_p),
+        ("scale", c_float), ("lse", c_void_p), ("causal", c_int),
     ]
 
 

@@ -30,6 +30,7 @@ struct Params {
   int N, Nk, heads;
   float scale_log2;  // softmax scale * log2(e)
   float* lse;        // [B][heads][N] (log2 domain: m + log2(l))
+  int causal;        // key j > query i masked (N == Nk)
 };
 
 DP_DEV float ex2(float x) {
@@ -49,8 +50,9 @@ __global__ void __launch_bounds__(128, 2)
                   const Params p) {
   DP_PDL_ENTRY();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // 1024-byte alignment by an offset from the __shared__ array (not an integer round trip), so the
+  // compiler keeps the shared address space: LDS/STS instead of generic LD/ST on the LSU path
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + TILE_BYTES;          // 2 buffers
   uint8_t* sV = sK + 2 * TILE_BYTES;      // 1 buffer
@@ -67,7 +69,8 @@ __global__ void __launch_bounds__(128, 2)
   const int warp = tid >> 5;
   const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int q0 = qt * BQ;
-  const int ntiles = (p.Nk + BKV - 1) / BKV;
+  int ntiles = (p.Nk + BKV - 1) / BKV;
+  if (p.causal) ntiles = min(ntiles, (q0 + BQ - 1) / BKV + 1);  // tiles past the diagonal are masked
 
   if (tid == 0) {
     tma_prefetch(&tmQ);
@@ -121,7 +124,9 @@ __global__ void __launch_bounds__(128, 2)
     }
     mbar_wait(bar_s, j & 1);
     tc_fence_after();
-    const int valid = min(BKV, p.Nk - j * BKV);
+    // keys of this tile the row may see (key 0 is always visible, so m stays finite)
+    const int valid = p.causal ? min(min(BKV, p.Nk - j * BKV), q0 + row - j * BKV + 1)
+                               : min(BKV, p.Nk - j * BKV);
     // the row's 128 scores come out of TMEM once (4 loads, one wait) and stay in registers for
     // both the row max and the exponentials
     uint32_t sv[BKV];
@@ -307,8 +312,9 @@ __global__ void __launch_bounds__(256, 1)
                   const BwdParams p) {
   DP_PDL_ENTRY();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // 1024-byte alignment by an offset from the __shared__ array (not an integer round trip), so the
+  // compiler keeps the shared address space: LDS/STS instead of generic LD/ST on the LSU path
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sK = smem;
   uint8_t* sV = sK + TILE_BYTES;
   uint8_t* sQ = sV + TILE_BYTES;        // [2]
@@ -608,6 +614,10 @@ extern "C" int dp_flash_attn_fwd(const DpAttnArgs* a, dp_stream_t stream) {
     set_error("dp_flash_attn_fwd: bf16, head_dim 64 only");
     return DP_ERR_UNSUPPORTED;
   }
+  if (a->causal && a->N != a->Nk) {
+    set_error("dp_flash_attn_fwd: causal masking needs N == Nk");
+    return DP_ERR_ARGS;
+  }
   if (a->B <= 0 || a->N <= 0 || a->Nk <= 0) return 0;
   CUtensorMap mq, mk, mv, mo;
   if (int e = fa_map(&mq, a->q, a->N, a->heads, a->B, a->q_ld, a->q_bs)) return e;
@@ -624,7 +634,7 @@ extern "C" int dp_flash_attn_fwd(const DpAttnArgs* a, dp_stream_t stream) {
     }
     attr = true;
   }
-  fa::Params p{a->N, a->Nk, a->heads, a->scale * 1.4426950408889634f, a->lse};
+  fa::Params p{a->N, a->Nk, a->heads, a->scale * 1.4426950408889634f, a->lse, a->causal};
   dim3 grid((a->N + fa::BQ - 1) / fa::BQ, a->heads, a->B);
   fa::fa_fwd_kernel<<<grid, 128, fa::SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(mq, mk, mv, mo, p);
   cudaError_t e = cudaGetLastError();
@@ -665,8 +675,8 @@ extern "C" int dp_flash_attn_bwd(const DpAttnArgs* a, const void* dout, int64_t 
                                  int64_t dq_ld, void* dk, void* dv, int64_t dkv_ld, float* workspace,
                                  dp_stream_t stream) {
   using namespace dp;
-  if (a->head_dim != 64 || a->dtype != DP_BF16) {
-    set_error("dp_flash_attn_bwd: bf16, head_dim 64 only");
+  if (a->head_dim != 64 || a->dtype != DP_BF16 || a->causal) {
+    set_error("dp_flash_attn_bwd: bf16, head_dim 64, non-causal only");
     return DP_ERR_UNSUPPORTED;
   }
   if (a->B <= 0 || a->N <= 0 || a->Nk <= 0) return 0;

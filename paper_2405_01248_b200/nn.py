@@ -516,14 +516,17 @@ class _AttentionFn(torch.autograd.Function):
         hd = C // heads
         scale = 1.0 / math.sqrt(hd)
         dev, dt = q_t.device, q_t.dtype
-        if FLASH_ATTENTION and dt == torch.bfloat16 and hd == 64 and not causal:
+        # causal masking exists in the fused forward only: used where no gradient flows back
+        # (the frozen CLIP text encoder); a trainable causal attention keeps the explicit path
+        grad_needed = ctx.needs_input_grad[0] or ctx.needs_input_grad[1]
+        if FLASH_ATTENTION and dt == torch.bfloat16 and hd == 64 and not (causal and grad_needed):
             # fused tcgen05 attention: no score / probability tensors in HBM
             o = torch.empty(B, N, C, device=dev, dtype=dt)
             lse = torch.empty(B, heads, N, device=dev, dtype=torch.float32)
             kp = src_k.view(-1)[k_off:]
             vp = src_k.view(-1)[v_off:]
             ops.flash_attn_fwd(q_t, kp, vp, o, B=B, N=N, Nk=Nk, heads=heads, q_ld=q_ld, kv_ld=kv_ld,
-                               o_ld=C, scale=scale, lse=lse)
+                               o_ld=C, scale=scale, lse=lse, causal=causal)
             ctx.save_for_backward(q_t, src_k if kv_t is not None else q_t, o, lse)
             ctx.meta = (kv_t is None, heads, B, N, Nk, C, hd, q_ld, kv_ld, k_off, v_off, scale)
             ctx.flash = True

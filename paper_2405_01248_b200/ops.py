@@ -621,11 +621,13 @@ def _attn_args(q, k, v, o, B, N, Nk, heads, q_ld, kv_ld, o_ld, scale, lse):
     return a
 
 
-def flash_attn_fwd(q, k, v, o, *, B, N, Nk, heads, q_ld, kv_ld, o_ld, scale, lse=None):
+def flash_attn_fwd(q, k, v, o, *, B, N, Nk, heads, q_ld, kv_ld, o_ld, scale, lse=None, causal=False):
     """Fused attention forward (bf16, head dim 64). q/k/v/o are base pointers of
-    [B, N(k), heads*64] column views with token strides *_ld (elements)."""
+    [B, N(k), heads*64] column views with token strides *_ld (elements). causal (N == Nk, forward
+    only): key j > query i masked."""
     a = _attn_args(q, k, v, o, B, N, Nk, heads, q_ld, kv_ld, o_ld, scale, lse)
-    flops = 4.0 * B * heads * N * Nk * 64
+    a.causal = int(causal)
+    flops = 4.0 * B * heads * 64 * (N * (N + 1) / 2 if causal else N * Nk)
     telemetry.timed("tcgen05_gemm", flops,
                     lambda: check(_L().dp_flash_attn_fwd(ctypes.byref(a), _stream()), "dp_flash_attn_fwd"),
                     sub="flash_fwd")

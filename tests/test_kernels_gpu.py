@@ -236,3 +236,16 @@ def test_flash_attention_vs_torch(B, N, Nk, C, heads, cross):
     assert _rel(q.grad, qr.grad) < 3e-2
     if cross:
         assert _rel(kv.grad, kvr.grad) < 3e-2
+
+
+@pytest.mark.parametrize("B,N,C,heads", [(4, 77, 1024, 16), (2, 300, 128, 2), (1, 1024, 320, 5)])
+def test_flash_attention_causal_forward(B, N, C, heads):
+    """Causal fused forward (frozen CLIP text encoder: no gradient) vs fp32 PyTorch SDPA."""
+    from paper_2405_01248_b200 import nn
+    g = torch.Generator(device="cuda").manual_seed(N)
+    q = torch.randn(B, N, 3 * C, device="cuda", generator=g).bfloat16()
+    with torch.no_grad():
+        o = nn.attention(q, None, heads, True)
+    Q, K, V = (q.float()[..., i * C:(i + 1) * C].reshape(B, N, heads, 64).transpose(1, 2) for i in range(3))
+    ref = F.scaled_dot_product_attention(Q, K, V, is_causal=True).transpose(1, 2).reshape(B, N, C)
+    assert _rel(o, ref) < 2e-2
