@@ -294,7 +294,7 @@ struct BwdParams {
   float scale;        // softmax scale (dS -> dS_raw)
   const float* lse;   // [B][heads][N]
   const float* Dv;    // [B][heads][N]
-  float* dq_acc;      // [B][N][heads][64] fp32, zero-initialised
+  float* dq_acc;      // [B][N][heads][64] fp32, zero-initialised (reduced into by TMA: tmDQ)
   int qsplit;         // CTAs per key tile (query tiles split between them)
   float* dkv_acc;     // qsplit > 1: [2][B][Nk][heads][64] fp32 dK (unscaled), dV, zero-initialised
 };
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(256, 1)
     fa_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                   const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmDV,
-                  const BwdParams p) {
+                  const __grid_constant__ CUtensorMap tmDQ, const BwdParams p) {
   DP_PDL_ENTRY();
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment by an offset from the __shared__ array (not an integer round trip), so the
@@ -321,7 +321,10 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sDO = sQ + 2 * TILE_BYTES;   // [2]
   uint8_t* sPT = sDO + 2 * TILE_BYTES;  // 2 blocks (queries 0-63, 64-127)
   uint8_t* sDST = sPT + 2 * TILE_BYTES; // 2 blocks
-  float* sLse = reinterpret_cast<float*>(sDST + 2 * TILE_BYTES);  // [2][128]
+  // dQ_i staging (128 query rows x 64 fp32, 256-byte rows): one TMA reduce-add per query tile
+  // instead of 2048 per-thread vector atomics (those saturated the LSU queue, lg_throttle)
+  float* sDQ = reinterpret_cast<float*>(sDST + 2 * TILE_BYTES);
+  float* sLse = sDQ + BQ * HD;                                     // [2][128]
   float* sD = sLse + 256;                                          // [2][128]
   uint64_t* bar = reinterpret_cast<uint64_t*>(sD + 256);
   uint64_t* bar_kv = bar;
@@ -411,6 +414,11 @@ __global__ void __launch_bounds__(256, 1)
     const int li = i - i0;
     const int qb = li & 1;
     __syncthreads();  // sLse/sD of tile i visible; previous tile's smem/TMEM consumers done
+    if (tid == 0 && li > 0) {  // dQ of the previous query tile, staged by every thread
+      tma_reduce_add_4d(&tmDQ, sDQ, h * HD, (i - 1) * BQ, b, 0);
+      tma_reduce_add_4d(&tmDQ, reinterpret_cast<uint8_t*>(sDQ) + BQ * 128, h * HD + 32, (i - 1) * BQ, b, 0);
+      bulk_commit();
+    }
     if (i + 1 < i1) load_rows(i + 1, qb ^ 1);
     mbar_wait(bar_sp, li & 1);
     tc_fence_after();
@@ -456,6 +464,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     fence_async_shared();
     tc_fence_before();
+    if (tid == 0) bulk_wait_read<0>();  // the staging buffer is free once the reduce has read it
     __syncthreads();
     if (tid == 0) {
       tc_fence_after();
@@ -484,25 +493,29 @@ __global__ void __launch_bounds__(256, 1)
     mbar_wait(bar_acc, li & 1);
     tc_fence_after();
     if (tid == 0 && i + 2 < i1) load_q(i + 2, qb);  // Q/dO buffer qb is free again
-    // dQ rows of this query tile -> fp32 atomics (thread = query row, half = 32-column chunk)
-    const int q = i * BQ + row;
+    // dQ rows of this query tile -> staging: half-buffer `half` holds 128 rows x 32 fp32 (128 B) in
+    // the SWIZZLE_128B layout of tmDQ's box (16-byte chunk k of row r at k ^ (r & 7): conflict-free)
     {
-      const int c = half;
       uint32_t v[32];
-      tmem_ld_32x32(t_dq + lane_off + c * 32, v);
+      tmem_ld_32x32(t_dq + lane_off + half * 32, v);
       tmem_ld_wait();
-      if (q < p.N) {
-        float* dst = p.dq_acc + (((int64_t)b * p.N + q) * p.heads + h) * HD + c * 32;
+      uint8_t* dst = reinterpret_cast<uint8_t*>(sDQ) + half * (BQ * 128) + row * 128;
 #pragma unroll
-        for (int j = 0; j < 32; j += 4)
-          atomicAdd(reinterpret_cast<float4*>(dst + j),
-                    make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
-                                __uint_as_float(v[j + 3])));
-      }
+      for (int k = 0; k < 8; ++k)
+        *reinterpret_cast<float4*>(dst + ((k ^ (row & 7)) * 16)) =
+            make_float4(__uint_as_float(v[k * 4]), __uint_as_float(v[k * 4 + 1]), __uint_as_float(v[k * 4 + 2]),
+                        __uint_as_float(v[k * 4 + 3]));
+      fence_async_shared();
     }
     tc_fence_before();
   }
   __syncthreads();
+  if (tid == 0 && i1 > i0) {
+    tma_reduce_add_4d(&tmDQ, sDQ, h * HD, (i1 - 1) * BQ, b, 0);
+    tma_reduce_add_4d(&tmDQ, reinterpret_cast<uint8_t*>(sDQ) + BQ * 128, h * HD + 32, (i1 - 1) * BQ, b, 0);
+    bulk_commit();
+    bulk_wait_all();
+  }
   tc_fence_after();
   if (p.qsplit > 1) {
     // partial dK / dV over this CTA's query tiles -> fp32 atomics (scale and bf16 cast afterwards)
@@ -574,7 +587,7 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
-constexpr size_t BWD_SMEM = 1024 + BWD_SMEM_TILES * TILE_BYTES + 4 * 256 * 4 + 64;
+constexpr size_t BWD_SMEM = 1024 + BWD_SMEM_TILES * TILE_BYTES + BQ * HD * 4 + 4 * 256 * 4 + 64;
 
 }  // namespace fa
 
@@ -711,6 +724,21 @@ extern "C" int dp_flash_attn_bwd(const DpAttnArgs* a, const void* dout, int64_t 
     }
     attr = true;
   }
+  // dq_acc [B][N][C] fp32: dims {C, N, B, 1}, box {32, 128, 1, 1} (128-byte rows, SWIZZLE_128B)
+  CUtensorMap mdq;
+  {
+    auto fn = tensor_map_encoder();
+    cuuint64_t gdim[4] = {(cuuint64_t)C, (cuuint64_t)a->N, (cuuint64_t)a->B, 1};
+    cuuint64_t gstr[3] = {(cuuint64_t)C * 4, (cuuint64_t)a->N * C * 4, (cuuint64_t)a->B * a->N * C * 4};
+    cuuint32_t box[4] = {32, 128, 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (!fn || fn(&mdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dq_acc, gdim, gstr, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      set_error("flash attention bwd: dQ tensor map encode failed");
+      return DP_ERR_DRIVER;
+    }
+  }
   const int qsplit = fa_bwd_qsplit(a);
   float* dkv_acc = dq_acc + rows * C;  // [2][B][Nk][heads][64] (split only)
   const int64_t kv_rows = (int64_t)a->B * a->Nk;
@@ -718,7 +746,7 @@ extern "C" int dp_flash_attn_bwd(const DpAttnArgs* a, const void* dout, int64_t 
   fa::BwdParams p{a->N, a->Nk, a->heads, a->scale * 1.4426950408889634f, a->scale, a->lse, Dv, dq_acc,
                   qsplit, dkv_acc};
   dim3 grid((a->Nk + fa::BKV - 1) / fa::BKV * qsplit, a->heads, a->B);
-  launch_k(fa::fa_bwd_kernel, dim3(grid), dim3(256), fa::BWD_SMEM, st, mq, mk, mv, mdo, mdk, mdv, p);
+  launch_k(fa::fa_bwd_kernel, dim3(grid), dim3(256), fa::BWD_SMEM, st, mq, mk, mv, mdo, mdk, mdv, mdq, p);
   if (qsplit > 1) {
     const int64_t nk2 = kv_rows * C / 8;
     int gk = static_cast<int>((nk2 + 255) / 256);
