@@ -296,6 +296,8 @@ struct BwdParams {
   const float* Dv;    // [B][heads][N]
   float* dq_acc;      // [B][N][heads][64] fp32, zero-initialised (reduced into by TMA: tmDQ)
   int qsplit;         // CTAs per key tile (query tiles split between them)
+  int dq_direct;      // one key tile (Nk <= 128): each dQ tile has one producer -> scaled bf16 written
+                      // by a TMA store through tmDQ (no fp32 accumulator, memset or cast pass)
   float* dkv_acc;     // qsplit > 1: [2][B][Nk][heads][64] fp32 dK (unscaled), dV, zero-initialised
 };
 
@@ -415,8 +417,12 @@ __global__ void __launch_bounds__(256, 1)
     const int qb = li & 1;
     __syncthreads();  // sLse/sD of tile i visible; previous tile's smem/TMEM consumers done
     if (tid == 0 && li > 0) {  // dQ of the previous query tile, staged by every thread
-      tma_reduce_add_4d(&tmDQ, sDQ, h * HD, (i - 1) * BQ, b, 0);
-      tma_reduce_add_4d(&tmDQ, reinterpret_cast<uint8_t*>(sDQ) + BQ * 128, h * HD + 32, (i - 1) * BQ, b, 0);
+      if (p.dq_direct) {
+        tma_store_4d(&tmDQ, sDQ, 0, (i - 1) * BQ, h, b);
+      } else {
+        tma_reduce_add_4d(&tmDQ, sDQ, h * HD, (i - 1) * BQ, b, 0);
+        tma_reduce_add_4d(&tmDQ, reinterpret_cast<uint8_t*>(sDQ) + BQ * 128, h * HD + 32, (i - 1) * BQ, b, 0);
+      }
       bulk_commit();
     }
     if (i + 1 < i1) load_rows(i + 1, qb ^ 1);
@@ -499,20 +505,38 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t v[32];
       tmem_ld_32x32(t_dq + lane_off + half * 32, v);
       tmem_ld_wait();
-      uint8_t* dst = reinterpret_cast<uint8_t*>(sDQ) + half * (BQ * 128) + row * 128;
+      if (p.dq_direct) {
+        // bf16 tile of 128-byte rows (64 dims): this half's 4 chunks, SWIZZLE_128B like tmQ
+        uint8_t* dst = reinterpret_cast<uint8_t*>(sDQ) + row * 128;
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        *reinterpret_cast<float4*>(dst + ((k ^ (row & 7)) * 16)) =
-            make_float4(__uint_as_float(v[k * 4]), __uint_as_float(v[k * 4 + 1]), __uint_as_float(v[k * 4 + 2]),
-                        __uint_as_float(v[k * 4 + 3]));
+        for (int k = 0; k < 4; ++k) {
+          uint4 u;
+          u.x = pack_bf16x2(p.scale * __uint_as_float(v[k * 8 + 0]), p.scale * __uint_as_float(v[k * 8 + 1]));
+          u.y = pack_bf16x2(p.scale * __uint_as_float(v[k * 8 + 2]), p.scale * __uint_as_float(v[k * 8 + 3]));
+          u.z = pack_bf16x2(p.scale * __uint_as_float(v[k * 8 + 4]), p.scale * __uint_as_float(v[k * 8 + 5]));
+          u.w = pack_bf16x2(p.scale * __uint_as_float(v[k * 8 + 6]), p.scale * __uint_as_float(v[k * 8 + 7]));
+          *reinterpret_cast<uint4*>(dst + (((half * 4 + k) ^ (row & 7)) * 16)) = u;
+        }
+      } else {
+        uint8_t* dst = reinterpret_cast<uint8_t*>(sDQ) + half * (BQ * 128) + row * 128;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          *reinterpret_cast<float4*>(dst + ((k ^ (row & 7)) * 16)) =
+              make_float4(__uint_as_float(v[k * 4]), __uint_as_float(v[k * 4 + 1]), __uint_as_float(v[k * 4 + 2]),
+                          __uint_as_float(v[k * 4 + 3]));
+      }
       fence_async_shared();
     }
     tc_fence_before();
   }
   __syncthreads();
   if (tid == 0 && i1 > i0) {
-    tma_reduce_add_4d(&tmDQ, sDQ, h * HD, (i1 - 1) * BQ, b, 0);
-    tma_reduce_add_4d(&tmDQ, reinterpret_cast<uint8_t*>(sDQ) + BQ * 128, h * HD + 32, (i1 - 1) * BQ, b, 0);
+    if (p.dq_direct) {
+      tma_store_4d(&tmDQ, sDQ, 0, (i1 - 1) * BQ, h, b);
+    } else {
+      tma_reduce_add_4d(&tmDQ, sDQ, h * HD, (i1 - 1) * BQ, b, 0);
+      tma_reduce_add_4d(&tmDQ, reinterpret_cast<uint8_t*>(sDQ) + BQ * 128, h * HD + 32, (i1 - 1) * BQ, b, 0);
+    }
     bulk_commit();
     bulk_wait_all();
   }
@@ -698,7 +722,8 @@ extern "C" int dp_flash_attn_bwd(const DpAttnArgs* a, const void* dout, int64_t 
   const int64_t rows = (int64_t)a->B * a->N;
   float* Dv = workspace;                                   // [B][heads][N]
   float* dq_acc = workspace + (int64_t)a->B * a->heads * a->N;  // [B][N][heads][64]
-  cudaMemsetAsync(dq_acc, 0, sizeof(float) * rows * C, st);
+  const bool dq_direct = a->Nk <= fa::BKV;
+  if (!dq_direct) cudaMemsetAsync(dq_acc, 0, sizeof(float) * rows * C, st);
   {
     const int64_t total = (int64_t)a->B * a->heads * a->N;
     int gp = static_cast<int>((total * 8 + 255) / 256);
@@ -724,9 +749,12 @@ extern "C" int dp_flash_attn_bwd(const DpAttnArgs* a, const void* dout, int64_t 
     }
     attr = true;
   }
-  // dq_acc [B][N][C] fp32: dims {C, N, B, 1}, box {32, 128, 1, 1} (128-byte rows, SWIZZLE_128B)
+  // dq_acc [B][N][C] fp32: dims {C, N, B, 1}, box {32, 128, 1, 1} (128-byte rows, SWIZZLE_128B);
+  // dq_direct: the bf16 dq itself, mapped like q
   CUtensorMap mdq;
-  {
+  if (dq_direct) {
+    if (int e = fa_map(&mdq, dq, a->N, a->heads, a->B, dq_ld, a->N * dq_ld)) return e;
+  } else {
     auto fn = tensor_map_encoder();
     cuuint64_t gdim[4] = {(cuuint64_t)C, (cuuint64_t)a->N, (cuuint64_t)a->B, 1};
     cuuint64_t gstr[3] = {(cuuint64_t)C * 4, (cuuint64_t)a->N * C * 4, (cuuint64_t)a->B * a->N * C * 4};
@@ -744,7 +772,7 @@ extern "C" int dp_flash_attn_bwd(const DpAttnArgs* a, const void* dout, int64_t 
   const int64_t kv_rows = (int64_t)a->B * a->Nk;
   if (qsplit > 1) cudaMemsetAsync(dkv_acc, 0, sizeof(float) * 2 * kv_rows * C, st);
   fa::BwdParams p{a->N, a->Nk, a->heads, a->scale * 1.4426950408889634f, a->scale, a->lse, Dv, dq_acc,
-                  qsplit, dkv_acc};
+                  qsplit, dq_direct ? 1 : 0, dkv_acc};
   dim3 grid((a->Nk + fa::BKV - 1) / fa::BKV * qsplit, a->heads, a->B);
   launch_k(fa::fa_bwd_kernel, dim3(grid), dim3(256), fa::BWD_SMEM, st, mq, mk, mv, mdo, mdk, mdv, mdq, p);
   if (qsplit > 1) {
@@ -756,11 +784,13 @@ extern "C" int dp_flash_attn_bwd(const DpAttnArgs* a, const void* dout, int64_t 
     launch_k(fa::fa_dq_cast_kernel, dim3(gk), dim3(256), 0, st, dkv_acc + kv_rows * C,
              reinterpret_cast<__nv_bfloat16*>(dv), kv_rows, C, dkv_ld, 1.0f);
   }
-  const int64_t n2 = rows * C / 8;
-  int g = static_cast<int>((n2 + 255) / 256);
-  if (g > 148 * 8) g = 148 * 8;
-  launch_k(fa::fa_dq_cast_kernel, dim3(g), dim3(256), 0, st, dq_acc, reinterpret_cast<__nv_bfloat16*>(dq), rows, C, dq_ld,
-                                           a->scale);
+  if (!dq_direct) {
+    const int64_t n2 = rows * C / 8;
+    int g = static_cast<int>((n2 + 255) / 256);
+    if (g > 148 * 8) g = 148 * 8;
+    launch_k(fa::fa_dq_cast_kernel, dim3(g), dim3(256), 0, st, dq_acc, reinterpret_cast<__nv_bfloat16*>(dq), rows,
+             C, dq_ld, a->scale);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("flash attention bwd launch: ") + cudaGetErrorString(e));

@@ -634,6 +634,14 @@ def flash_attn_fwd(q, k, v, o, *, B, N, Nk, heads, q_ld, kv_ld, o_ld, scale, lse
     return o
 
 
+def _fa_bwd_launches(B, N, Nk, heads):
+    """Kernels dp_flash_attn_bwd launches: D prep + backward, the dQ cast unless one key tile
+    (dQ stored directly), the dK/dV casts when query tiles are split (mirrors fa_bwd_qsplit)."""
+    nkt = -(-Nk // 128)
+    split = nkt * heads * B < 2 * 148 and -(-N // 128) >= 2
+    return 2 + (0 if nkt == 1 else 1) + (2 if split else 0)
+
+
 def flash_attn_bwd(q, k, v, o, do, dq, dk, dv, lse, *, B, N, Nk, heads, q_ld, kv_ld, o_ld, do_ld, dq_ld,
                    dkv_ld, scale):
     a = _attn_args(q, k, v, o, B, N, Nk, heads, q_ld, kv_ld, o_ld, scale, lse)
@@ -642,4 +650,4 @@ def flash_attn_bwd(q, k, v, o, do, dq, dk, dv, lse, *, B, N, Nk, heads, q_ld, kv
     telemetry.timed("tcgen05_gemm", flops,
                     lambda: check(_L().dp_flash_attn_bwd(ctypes.byref(a), _ptr(do), do_ld, _ptr(dq), dq_ld,
                                                          _ptr(dk), _ptr(dv), dkv_ld, _ptr(ws), _stream()),
-                                  "dp_flash_attn_bwd", 3), sub="flash_bwd")
+                                  "dp_flash_attn_bwd", _fa_bwd_launches(B, N, Nk, heads)), sub="flash_bwd")
