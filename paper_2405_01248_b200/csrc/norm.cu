@@ -88,6 +88,9 @@ DP_DEV Welford wf_merge(Welford a, Welford b) {
 constexpr int GN_THREADS = 256;
 constexpr int GN_WARPS = GN_THREADS / 32;
 constexpr int GN_MAX_C = 2560;
+#ifndef GN_BWD_MINB
+#define GN_BWD_MINB 2  // resident CTAs per SM the backward kernels are register-limited to (3, 4 spill)
+#endif
 
 struct GnGeom {
   int chunks, ppc, nblk, CB;
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__(GN_THREADS, 4)
 // and CTA) and per-group partials A = sum gamma*dy0, B = sum gamma*dy0*xhat (dy0 = dy through
 // the optional SiLU)
 template <typename T>
-__global__ void __launch_bounds__(GN_THREADS)
+__global__ void __launch_bounds__(GN_THREADS, GN_BWD_MINB)
     gn_bwd_partial_kernel(const T* __restrict__ x, const T* __restrict__ dy,
                           const float* __restrict__ gamma, const float* __restrict__ beta,
                           const float* __restrict__ mean, const float* __restrict__ rstd, int HW,
@@ -355,23 +358,37 @@ __global__ void __launch_bounds__(GN_THREADS)
       }
       const int64_t step = (int64_t)L.rows_par * C;
       int64_t off = base + (int64_t)(p0 + L.rl) * C + L.cv * V;
-#pragma unroll 4
-      for (int p = p0 + L.rl; p < p1; p += L.rows_par, off += step) {
-        float fx[V], fd[V];
-        ld16(x + off, fx);
-        ld16(dy + off, fd);
+      auto acc = [&](const float* fx, const float* fd) {
 #pragma unroll
         for (int j = 0; j < V; ++j) {
           const float xh = (fx[j] - mu[j]) * rs[j];
           float d = fd[j];
           if (silu_on) {
             const float y0 = fmaf(xh, ga[j], be[j]);
-            const float s = __frcp_rn(1.f + __expf(-y0));
+            const float s = __fdividef(1.f, 1.f + __expf(-y0));  // MUFU rcp (no IEEE fixup path)
             d *= s * (1.f + y0 * (1.f - s));
           }
           sa[j] += d;
           sb[j] = fmaf(d, xh, sb[j]);
         }
+      };
+      int p = p0 + L.rl;
+      // 4 pixels' x and dy loads issued before any arithmetic (8 x 16 B in flight per thread)
+      for (; p + 3 * L.rows_par < p1; p += 4 * L.rows_par, off += 4 * step) {
+        float fx[4][V], fd[4][V];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ld16(x + off + u * step, fx[u]);
+          ld16(dy + off + u * step, fd[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc(fx[u], fd[u]);
+      }
+      for (; p < p1; p += L.rows_par, off += step) {
+        float fx[V], fd[V];
+        ld16(x + off, fx);
+        ld16(dy + off, fd);
+        acc(fx, fd);
       }
       const int o = L.rl * nch + (L.cv - cv0) * V;
 #pragma unroll
@@ -415,7 +432,7 @@ __global__ void __launch_bounds__(GN_THREADS)
 }
 
 template <typename T>
-__global__ void __launch_bounds__(GN_THREADS)
+__global__ void __launch_bounds__(GN_THREADS, GN_BWD_MINB)
     gn_bwd_apply_kernel(const T* __restrict__ x, const T* __restrict__ dy,
                         const float* __restrict__ gamma, const float* __restrict__ beta,
                         const float* __restrict__ mean, const float* __restrict__ rstd,
@@ -466,24 +483,42 @@ __global__ void __launch_bounds__(GN_THREADS)
     }
     const int64_t step = (int64_t)L.rows_par * C;
     int64_t off = base + (int64_t)(p0 + L.rl) * C + L.cv * V;
-#pragma unroll 4
-    for (int p = p0 + L.rl; p < p1; p += L.rows_par, off += step) {
-      float fx[V], fd[V], fo[V];
-      ld16(x + off, fx);
-      ld16(dy + off, fd);
-      if (accumulate) ld16(dx + off, fo);
+    auto one = [&](const float* fx, const float* fd, float* fo) {
 #pragma unroll
       for (int j = 0; j < V; ++j) {
         const float xh = (fx[j] - mu[j]) * rs[j];
         float d = fd[j];
         if (silu_on) {
           const float y0 = fmaf(xh, ga[j], be[j]);
-          const float sg = __frcp_rn(1.f + __expf(-y0));
+          const float sg = __fdividef(1.f, 1.f + __expf(-y0));
           d *= sg * (1.f + y0 * (1.f - sg));
         }
         const float v = rs[j] * (ga[j] * d - gA[j] - xh * gB[j]);
         fo[j] = accumulate ? fo[j] + v : v;
       }
+    };
+    int p = p0 + L.rl;
+    // 2 pixels' loads (x, dy, optional dx) issued before the arithmetic
+    for (; p + L.rows_par < p1; p += 2 * L.rows_par, off += 2 * step) {
+      float fx[2][V], fd[2][V], fo[2][V];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        ld16(x + off + u * step, fx[u]);
+        ld16(dy + off + u * step, fd[u]);
+        if (accumulate) ld16(dx + off + u * step, fo[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        one(fx[u], fd[u], fo[u]);
+        st16(dx + off + u * step, fo[u]);
+      }
+    }
+    for (; p < p1; p += L.rows_par, off += step) {
+      float fx[V], fd[V], fo[V];
+      ld16(x + off, fx);
+      ld16(dy + off, fd);
+      if (accumulate) ld16(dx + off, fo);
+      one(fx, fd, fo);
       st16(dx + off, fo);
     }
   }
