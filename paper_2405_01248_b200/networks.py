@@ -200,7 +200,8 @@ class ResBlock:
         self.skip = nn.Conv2d(s, f"{p}.skip", cin, cout, 1) if cin != cout else None
 
     def __call__(self, x, temb_act=None):
-        h = self.c1(self.n1(x))
+        hn, x = self.n1.fork(x)  # x's skip-path gradient is accumulated in the GroupNorm backward
+        h = self.c1(hn)
         if self.emb is not None:
             h = nn.add_row_bias(h, self.emb(temb_act))
         sk = x if self.skip is None else self.skip(x)
@@ -366,11 +367,16 @@ class SpatialTransformer:
 
     def __call__(self, x, ctx):
         B, H, W, C = x.shape
+        # pre-norm forks: each norm's backward adds into its residual branch's gradient
+        xn, x = self.norm.fork(x)
         x2 = x.view(B, H * W, C)
-        h = self.proj_in(self.norm(x).view(B, H * W, C))
-        h = self.attn1(self.ln1(h), residual=h)
-        h = self.attn2(self.ln2(h), ctx, residual=h)
-        h = self.ff2(nn.geglu(self.ff1(self.ln3(h))), residual=h)
+        h = self.proj_in(xn.view(B, H * W, C))
+        a, h = self.ln1.fork(h)
+        h = self.attn1(a, residual=h)
+        a, h = self.ln2.fork(h)
+        h = self.attn2(a, ctx, residual=h)
+        a, h = self.ln3.fork(h)
+        h = self.ff2(nn.geglu(self.ff1(a)), residual=h)
         return self.proj_out(h, residual=x2).view(B, H, W, C)
 
 

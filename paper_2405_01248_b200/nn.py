@@ -320,6 +320,65 @@ class _LayerNormFn(torch.autograd.Function):
         return dx, None, None
 
 
+def _identity_grad(g):
+    """Gradient of a fork's identity output as a contiguous buffer the norm backward may add into
+    (autograd hands the consumer's gradient over; every kernel that read it is already enqueued on
+    this stream, so accumulating in place is ordered after them)."""
+    return None if g is None else (g if g.is_contiguous() else g.contiguous())
+
+
+class _GroupNormForkFn(torch.autograd.Function):
+    """(GroupNorm(x), x) for an x with a second consumer (residual / skip): both gradients reach one
+    backward and the GroupNorm backward kernel adds its dx into the identity branch's gradient
+    instead of autograd summing the two with a separate elementwise kernel."""
+
+    @staticmethod
+    def forward(ctx, x, anchor, layer):
+        ctx.set_materialize_grads(False)
+        xc = _c(x)
+        y, mean, rstd = ops.group_norm(xc, layer.gamma.w, layer.beta.w, layer.groups, layer.eps, layer.silu)
+        ctx.save_for_backward(xc, mean, rstd)
+        ctx.layer = layer
+        return y, x.view_as(x)
+
+    @staticmethod
+    def backward(ctx, dy, dres):
+        x, mean, rstd = ctx.saved_tensors
+        L = ctx.layer
+        if dy is None:
+            return dres, None, None
+        dx = ops.group_norm_bwd(x, _c(dy), L.gamma.w, L.beta.w, mean, rstd, L.groups, L.silu,
+                                dgamma=L.gamma.g, dbeta=L.beta.g, accumulate_into=_identity_grad(dres))
+        return dx.view_as(x), None, None
+
+
+class _LayerNormForkFn(torch.autograd.Function):
+    """(LayerNorm(x), x): as _GroupNormForkFn for the transformer's pre-norm residual stream."""
+
+    @staticmethod
+    def forward(ctx, x, anchor, layer):
+        ctx.set_materialize_grads(False)
+        xc = _c(x)
+        g = None if layer.gamma is None else layer.gamma.w
+        b = None if layer.beta is None else layer.beta.w
+        y, mean, rstd = ops.layer_norm(xc, g, b, layer.eps)
+        ctx.save_for_backward(xc, mean, rstd)
+        ctx.layer = layer
+        return y, x.view_as(x)
+
+    @staticmethod
+    def backward(ctx, dy, dres):
+        x, mean, rstd = ctx.saved_tensors
+        L = ctx.layer
+        if dy is None:
+            return dres, None, None
+        dx = ops.layer_norm_bwd(x, _c(dy), None if L.gamma is None else L.gamma.w, mean, rstd,
+                                dgamma=None if L.gamma is None else L.gamma.g,
+                                dbeta=None if L.beta is None else L.beta.g,
+                                accumulate_into=_identity_grad(dres))
+        return dx.view_as(x), None, None
+
+
 class _LayerNormModFn(torch.autograd.Function):
     """adaLN: y = LN(x) * (1 + mod[b, scale_off:+C]) + mod[b, shift_off:+C]."""
 
@@ -642,6 +701,10 @@ class GroupNorm:
     def __call__(self, x):
         return _GroupNormFn.apply(x, _anchor(), self)
 
+    def fork(self, x):
+        """(GroupNorm(x), x-alias): use the alias for x's other consumer (residual / skip)."""
+        return _GroupNormForkFn.apply(x, _anchor(), self)
+
 
 class LayerNorm:
     def __init__(self, store, name, C, eps=1e-5, affine=True):
@@ -651,6 +714,10 @@ class LayerNorm:
 
     def __call__(self, x):
         return _LayerNormFn.apply(x, _anchor(), self)
+
+    def fork(self, x):
+        """(LayerNorm(x), x-alias): use the alias for x's other consumer (the residual add)."""
+        return _LayerNormForkFn.apply(x, _anchor(), self)
 
 
 def ln_modulate(x, mod, shift_off, scale_off, eps=1e-6):

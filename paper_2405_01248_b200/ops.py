@@ -515,14 +515,16 @@ def group_norm(x, gamma, beta, G, eps, silu):
     return y, mean, rstd
 
 
-def group_norm_bwd(x, dy, gamma, beta, mean, rstd, G, silu, dgamma=None, dbeta=None):
+def group_norm_bwd(x, dy, gamma, beta, mean, rstd, G, silu, dgamma=None, dbeta=None, accumulate_into=None):
+    """dx of GroupNorm(+SiLU); accumulate_into: add dx into this contiguous tensor in the kernel
+    (a second consumer's gradient of x) and return it."""
     N, C = x.shape[0], x.shape[-1]
     HW = x.numel() // (N * C)
-    dx = torch.empty_like(x)
+    dx = torch.empty_like(x) if accumulate_into is None else accumulate_into
     ws = _gn_ws(x.device, _L().dp_group_norm_workspace(N, HW, G))
     check(_L().dp_group_norm_bwd(dtype_code(x), _ptr(x), _ptr(dy), _ptr(gamma), _ptr(beta), _ptr(mean),
-                                 _ptr(rstd), _ptr(dx), _ptr(dgamma), _ptr(dbeta), N, HW, C, G, int(silu), 0,
-                                 _ptr(ws), _stream()), "dp_group_norm_bwd", 2)
+                                 _ptr(rstd), _ptr(dx), _ptr(dgamma), _ptr(dbeta), N, HW, C, G, int(silu),
+                                 int(accumulate_into is not None), _ptr(ws), _stream()), "dp_group_norm_bwd", 2)
     return dx
 
 
@@ -547,13 +549,14 @@ def rms_norm(x, gamma, y, eps):
 
 
 def layer_norm_bwd(x, dy, gamma, mean, rstd, dgamma=None, dbeta=None, mod=None, mod_ld=0, shift_off=0,
-                   scale_off=0, rows_per_sample=1, dmod=None, dmod_ld=0):
+                   scale_off=0, rows_per_sample=1, dmod=None, dmod_ld=0, accumulate_into=None):
     C = x.shape[-1]
     rows = x.numel() // C
-    dx = torch.empty_like(x)
+    dx = torch.empty_like(x) if accumulate_into is None else accumulate_into
     check(_L().dp_layer_norm_bwd(dtype_code(x), _ptr(x), _ptr(dy), _ptr(gamma), _ptr(mod), mod_ld,
                                  shift_off, scale_off, rows_per_sample, _ptr(mean), _ptr(rstd), _ptr(dx),
-                                 _ptr(dgamma), _ptr(dbeta), _ptr(dmod), dmod_ld, rows, C, 0, _stream()),
+                                 _ptr(dgamma), _ptr(dbeta), _ptr(dmod), dmod_ld, rows, C,
+                                 int(accumulate_into is not None), _stream()),
           "dp_layer_norm_bwd", 1 + int(gamma is not None and dgamma is not None) + int(mod is not None and dmod is not None))
     return dx
 
