@@ -960,6 +960,22 @@ int dp_rms_norm_fwd(int dtype, const void* x, const float* gamma, void* y, int64
   return ew_check("rms_norm_fwd");
 }
 
+// resident 256-thread blocks per SM of a kernel (cached per function pointer)
+static int ln_blocks_per_sm(const void* kern) {
+  static const void* keys[32];
+  static int vals[32];
+  static int n = 0;
+  for (int i = 0; i < n; ++i)
+    if (keys[i] == kern) return vals[i];
+  int v = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, 256, 0) != cudaSuccess || v < 1) v = 1;
+  if (n < 32) {
+    keys[n] = kern;
+    vals[n++] = v;
+  }
+  return v;
+}
+
 int dp_layer_norm_bwd(int dtype, const void* x, const void* dy, const float* gamma,
                       const void* mod, int64_t mod_ld, int shift_off, int scale_off,
                       int rows_per_sample, const float* mean, const float* rstd, void* dx,
@@ -979,21 +995,26 @@ int dp_layer_norm_bwd(int dtype, const void* x, const void* dy, const float* gam
   // (C <= 1024 bf16): few fat blocks, each merging its rows' partials once
   const bool pg = gamma && dgamma && nvec <= 4;
   const int64_t want = (rows + 7) / 8;
-  const int64_t cap = pg ? 2 * kNumSMs : want;
-  const dim3 grid(static_cast<unsigned>(want < cap ? want : cap));
 #define LN_BWD_ARGS cp<T>(x), cp<T>(dy), gamma, cp<T>(mod), mod_ld, scale_off, rps, mean, rstd, mp<T>(dx), \
                     rows, C, accumulate, dgamma, dbeta
+  // grid = one wave of the instantiation's resident blocks (register-limited: the wide-row variants
+  // fit one 256-thread block per SM, and a second partial wave doubled their time); warps stride
+  // over the remaining rows
   DISPATCH_T(dtype, {
+    auto go = [&](auto kern) {
+      const int64_t cap = (int64_t)ln_blocks_per_sm(reinterpret_cast<const void*>(kern)) * kNumSMs;
+      launch_k(kern, dim3(static_cast<unsigned>(want < cap ? want : cap)), dim3(256), 0, ST, LN_BWD_ARGS);
+    };
     if (pg) {
-      if (nvec <= 1) launch_k(ln_bwd_kernel<T, 1, true>, dim3(grid), dim3(256), 0, ST, LN_BWD_ARGS);
-      else if (nvec <= 2) launch_k(ln_bwd_kernel<T, 2, true>, dim3(grid), dim3(256), 0, ST, LN_BWD_ARGS);
-      else launch_k(ln_bwd_kernel<T, 4, true>, dim3(grid), dim3(256), 0, ST, LN_BWD_ARGS);
+      if (nvec <= 1) go(ln_bwd_kernel<T, 1, true>);
+      else if (nvec <= 2) go(ln_bwd_kernel<T, 2, true>);
+      else go(ln_bwd_kernel<T, 4, true>);
     } else {
-      if (nvec <= 1) launch_k(ln_bwd_kernel<T, 1, false>, dim3(grid), dim3(256), 0, ST, LN_BWD_ARGS);
-      else if (nvec <= 2) launch_k(ln_bwd_kernel<T, 2, false>, dim3(grid), dim3(256), 0, ST, LN_BWD_ARGS);
-      else if (nvec <= 4) launch_k(ln_bwd_kernel<T, 4, false>, dim3(grid), dim3(256), 0, ST, LN_BWD_ARGS);
-      else if (nvec <= 8) launch_k(ln_bwd_kernel<T, 8, false>, dim3(grid), dim3(256), 0, ST, LN_BWD_ARGS);
-      else launch_k(ln_bwd_kernel<T, 16, false>, dim3(grid), dim3(256), 0, ST, LN_BWD_ARGS);
+      if (nvec <= 1) go(ln_bwd_kernel<T, 1, false>);
+      else if (nvec <= 2) go(ln_bwd_kernel<T, 2, false>);
+      else if (nvec <= 4) go(ln_bwd_kernel<T, 4, false>);
+      else if (nvec <= 8) go(ln_bwd_kernel<T, 8, false>);
+      else go(ln_bwd_kernel<T, 16, false>);
     }
   });
 #undef LN_BWD_ARGS
