@@ -21,6 +21,7 @@ tail) and the AdamW step: nothing is skipped inside the timed 
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -160,6 +161,11 @@ def timed_steps(trainer, K, world, *, read_loss=False, kernel_timer=False):
 
     barrier(world)
     telemetry.reset()
+    # automatic garbage collection off inside the timed loop (collected just before, as training
+    # loops with manual GC do): a collection pause stalls the host thread that feeds ~2000 launches
+    # per step and showed up as sporadic 10% dips of the e2e pass
+    gc.collect()
+    gc.disable()
     if kernel_timer:
         telemetry.timer.start(reserve=2 * 2500 * K)
     a = torch.cuda.Event(enable_timing=True)
@@ -175,6 +181,7 @@ def timed_steps(trainer, K, world, *, read_loss=False, kernel_timer=False):
             host_loss[i:i + 1].copy_(trainer.ex.total_loss(), non_blocking=True)
     b.record()
     torch.cuda.synchronize()
+    gc.enable()
     if read_loss:
         losses = host_loss.tolist()
         if not all(v == v for v in losses):

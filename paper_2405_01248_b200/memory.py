@@ -3,7 +3,8 @@ memory model, while the paper hits memory limits).
 
 Per device of a GroupProgram the model adds
   * trainable parameters of the stage(s) it hosts: fp32 master + compute copy (bf16) + fp32 grad + AdamW m, v
-    (18 B/parameter in bf16 configurations, 16 B in fp32 ones where the master is the compute copy);
+    + the cached flip-transposed bf16 copy the dgrads read (nn.FLIP_CACHE; upper bound: every weight)
+    (20 B/parameter in bf16 configurations, 16 B in fp32 ones where the master is the compute copy);
   * frozen components, replicated on every device (fp32 master + compute copy);
   * activations autograd keeps for the backward: per backbone layer, bytes per sample measured on the device
     (`measure_layer_activation_bytes`) x the stage's per-replica micro-batch x the micro-batches in flight at
@@ -26,7 +27,9 @@ def _store_bytes(store, trainable):
     n = store.numel()
     if not trainable:
         return n * (4 + (2 if store.dtype != torch.float32 else 0))
-    return n * (16 + (2 if store.dtype != torch.float32 else 0))
+    from . import nn
+    bf16 = store.dtype != torch.float32
+    return n * (16 + (2 if bf16 else 0) + (2 if bf16 and nn.FLIP_CACHE else 0))
 
 
 def measure_layer_activation_bytes(model, batch_fn, device, batch=2):

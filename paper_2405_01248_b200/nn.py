@@ -22,6 +22,7 @@ encoders; layer shapes follow SD v2.1 / DiT.
 from __future__ import annotations
 
 import math
+import os
 import threading
 import zlib
 
@@ -37,7 +38,7 @@ FLASH_ATTENTION = True  # bf16 head-dim-64 attention through the fused tcgen05 k
 # ============================================================================ parameters
 
 class Param:
-    __slots__ = ("name", "shape", "fp32", "init", "offset", "numel", "w", "g", "master")
+    __slots__ = ("name", "shape", "fp32", "init", "offset", "numel", "w", "g", "master", "wt", "wt_fn")
 
     def __init__(self, name, shape, fp32, init):
         self.name = name
@@ -49,6 +50,14 @@ class Param:
         self.w = None       # compute view (bf16 weights, or fp32)
         self.g = None       # fp32 grad view (None when frozen)
         self.master = None  # fp32 master view
+        self.wt = None      # cached flip-transposed bf16 copy for dgrad (ops.cached_flip)
+        self.wt_fn = None   # recomputes wt in place from w
+
+
+# flip-transposed weight copies for dgrad are cached and refreshed right after each AdamW update
+# of their parameter (on the optimizer's stream, off the backward's critical path); DP_FLIP_CACHE=0
+# flips inside every dgrad instead (the A/B reference)
+FLIP_CACHE = os.environ.get("DP_FLIP_CACHE", "1") != "0"
 
 
 class ParamStore:
@@ -60,6 +69,17 @@ class ParamStore:
         self.params: dict[str, Param] = {}
         self.master = self.grad = self.compute = self.exp_avg = self.exp_avg_sq = None
         self.step = 0
+        self.flip_params = []  # params holding a cached wt, refreshed after their AdamW update
+
+    def register_flip(self, p):
+        self.flip_params.append(p)
+
+    def refresh_flips(self, lo, hi):
+        """Recompute the cached dgrad weight copies of the params inside the flat range [lo, hi)
+        (call right after updating it, on the same stream)."""
+        for p in self.flip_params:
+            if lo <= p.offset < hi:
+                p.wt_fn(p.wt)
 
     def add(self, name, shape, fp32=False, init="w"):
         if name in self.params:
@@ -83,6 +103,9 @@ class ParamStore:
             p.offset = off
             off += -(-p.numel // _ALIGN) * _ALIGN
         total = max(off, _ALIGN)
+        for p in plist:
+            p.wt = p.wt_fn = None
+        self.flip_params = []
         self.master = torch.zeros(total, device=device, dtype=torch.float32)
         if self.dtype != torch.float32:
             self.compute = torch.zeros(total, device=device, dtype=self.dtype)
@@ -136,6 +159,7 @@ class ParamStore:
                         None if self.compute is self.master else self.compute[lo:hi],
                         lr, betas[0], betas[1], eps, weight_decay, self.bc_dev, grad_scale, max_ctas,
                         zero_grad)
+        self.refresh_flips(lo, hi)
 
     def adamw_step(self, lr=1e-4, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01, grad_scale=1.0,
                    rng=None):
@@ -152,6 +176,7 @@ class ParamStore:
             ops.adamw_dev(self.master[lo:hi], self.grad[lo:hi], self.exp_avg[lo:hi], self.exp_avg_sq[lo:hi],
                           None if self.compute is self.master else self.compute[lo:hi],
                           lr, betas[0], betas[1], eps, weight_decay, self.step_dev, self.bc_dev, grad_scale)
+            self.refresh_flips(lo, hi)
             return
         ops.adamw(self.master[lo:hi], self.grad[lo:hi], self.exp_avg[lo:hi], self.exp_avg_sq[lo:hi],
                   None if self.compute is self.master else self.compute[lo:hi],
@@ -221,6 +246,12 @@ def _c(t):
 
 # ============================================================================ Functions
 
+def _flip_cache(layer):
+    """(store, weight param) when the layer's dgrad may reuse a cached flip-transposed weight: a
+    trainable store refreshes it after each AdamW update, a frozen one never changes it."""
+    return (layer.store, layer.weight) if FLIP_CACHE else None
+
+
 class _LinearFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, anchor, residual, layer):
@@ -246,7 +277,7 @@ class _LinearFn(torch.autograd.Function):
         dy2 = _c(dy).view(-1, N)
         dx = None
         if ctx.needs_input_grad[0]:
-            dx = ops.linear_dgrad(dy2, W.w).view(*dy.shape[:-1], W.shape[1])
+            dx = ops.linear_dgrad(dy2, W.w, cache=_flip_cache(layer)).view(*dy.shape[:-1], W.shape[1])
         if W.g is not None:
             ops.linear_wgrad(dy2, x2, W.g)
         if layer.bias is not None and layer.bias.g is not None:
@@ -273,7 +304,8 @@ class _ConvFn(torch.autograd.Function):
         dy = _c(dy)
         dx = None
         if ctx.needs_input_grad[0]:
-            dx = ops.conv2d_dgrad(dy, layer.weight.w, x.shape, stride=layer.stride, pad=layer.pad)
+            dx = ops.conv2d_dgrad(dy, layer.weight.w, x.shape, stride=layer.stride, pad=layer.pad,
+                                  cache=_flip_cache(layer))
         if layer.weight.g is not None:
             ops.conv2d_wgrad(dy, x, layer.weight.g, stride=layer.stride, pad=layer.pad)
         if layer.bias is not None and layer.bias.g is not None:
@@ -663,6 +695,7 @@ def _anchor():
 
 class Linear:
     def __init__(self, store, name, fin, fout, bias=True, init="w"):
+        self.store = store
         self.weight = store.add(f"{name}.weight", (fout, fin), init=init)
         self.bias = store.add(f"{name}.bias", (fout,), fp32=True, init="b") if bias else None
 
@@ -678,6 +711,7 @@ class Conv2d:
         self.k, self.stride = k, stride
         self.pad = (0, 0) if asym else ((k // 2, k // 2) if pad is None else pad)
         self.asym = asym
+        self.store = store
         self.weight = store.add(f"{name}.weight", (cout, k, k, cin), init=init)
         self.bias = store.add(f"{name}.bias", (cout,), fp32=True, init="b") if bias else None
 

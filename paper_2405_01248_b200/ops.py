@@ -103,7 +103,21 @@ def linear(x, w, bias=None, residual=None, out=None):
                 bias=bias, residual=residual)
 
 
-def linear_dgrad(dy, w, out=None):
+def cached_flip(cache, make):
+    """The flip-transposed weight for a dgrad: `make(dst)` writes it from the current weights.
+    cache = (store, param) keeps one persistent copy per parameter, refreshed by the store right
+    after each AdamW update of that parameter (nn.ParamStore.refresh_flips); None flips now."""
+    if cache is None:
+        return make(None)
+    store, p = cache
+    if p.wt is None:
+        p.wt = make(None)
+        p.wt_fn = make
+        store.register_flip(p)
+    return p.wt
+
+
+def linear_dgrad(dy, w, out=None, cache=None):
     """dx[M,K] = dy[M,N] @ w[N,K]. bf16 with a K-dim multiple of 8: the weight is transposed once
     (tiled flip-transpose kernel, K x N x 2 B) so that B is K-major and the GEMM can use CTA pairs and
     32-column tile widths (MN-major B is restricted to 64-column boxes on single CTAs)."""
@@ -112,9 +126,12 @@ def linear_dgrad(dy, w, out=None):
     if out is None:
         out = torch.empty(M, K, device=dy.device, dtype=dy.dtype)
     if dy.dtype == torch.bfloat16 and K % 8 == 0 and N % 8 == 0 and w.is_contiguous() and M >= 1024:
-        wt = torch.empty(K, N, device=w.device, dtype=w.dtype)
-        check(_lib.lib().dp_conv_weight_flip(dtype_code(w), _ptr(w), _ptr(wt), N, 1, 1, K, _stream()),
-              "dp_conv_weight_flip")
+        def make(dst):
+            wt = torch.empty(K, N, device=w.device, dtype=w.dtype) if dst is None else dst
+            check(_lib.lib().dp_conv_weight_flip(dtype_code(w), _ptr(w), _ptr(wt), N, 1, 1, K, _stream()),
+                  "dp_conv_weight_flip")
+            return wt
+        wt = cached_flip(cache, make)
         return gemm(dy, wt, out, M=M, N=K, K=N, a_ld=dy.stride(0), b_ld=N, d_ld=out.stride(0))
     return gemm(dy, w, out, M=M, N=K, K=N, a_ld=dy.stride(0), b_ld=w.stride(0), b_mn=True,
                 d_ld=out.stride(0))
@@ -242,7 +259,7 @@ def col2im(cols, dx, R, S, stride, pad, P, Q):
     return dx
 
 
-def conv2d_dgrad(dy, w, x_shape, *, stride=1, pad=(1, 1)):
+def conv2d_dgrad(dy, w, x_shape, *, stride=1, pad=(1, 1), cache=None):
     """dx [N,H,W,C] of y = conv2d(x, w). bf16: implicit GEMM over dy (zero-dilated for
     stride 2) with the weights read tap-flipped in place (dp_conv_dgrad)."""
     _require_cuda(dy, w)
@@ -250,7 +267,7 @@ def conv2d_dgrad(dy, w, x_shape, *, stride=1, pad=(1, 1)):
     K2, R, S, C = w.shape
     _, H, W, _ = x_shape
     if R == 1 and S == 1 and stride == 1 and pad == (0, 0):
-        return linear_dgrad(dy.reshape(-1, K), w.reshape(K, C)).view(N, H, W, C)
+        return linear_dgrad(dy.reshape(-1, K), w.reshape(K, C), cache=cache).view(N, H, W, C)
     if dy.dtype == torch.bfloat16 and _tiles(H, W, 128) and N * H * W < 8192:
         # small feature maps (U-Net 8x8 / 4x4 levels): the weights dominate the traffic, read
         # them tap-flipped in place (MN-major B_DGRAD operand mode, no transposed copy)
@@ -285,9 +302,13 @@ def conv2d_dgrad(dy, w, x_shape, *, stride=1, pad=(1, 1)):
             check(_lib.lib().dp_dilate(dtype_code(dy), _ptr(src), _ptr(dil), N, P, Q, Kp, stride,
                                        _stream()), "dp_dilate")
             src = dil
-        wt = torch.empty(Cp, R, S, Kp, device=dy.device, dtype=dy.dtype)
-        check(_lib.lib().dp_conv_weight_flip(dtype_code(wp), _ptr(wp), _ptr(wt), Kp, R, S, Cp, _stream()),
-              "dp_conv_weight_flip")
+        def make(dst):
+            wpp = _pad_first(_pad_last(w))  # the current weights (a refresh re-reads them)
+            wt = torch.empty(Cp, R, S, Kp, device=w.device, dtype=w.dtype) if dst is None else dst
+            check(_lib.lib().dp_conv_weight_flip(dtype_code(wpp), _ptr(wpp), _ptr(wt), Kp, R, S, Cp,
+                                                 _stream()), "dp_conv_weight_flip")
+            return wt
+        wt = cached_flip(cache, make)
         dx = torch.empty(N, H, W, Cp, device=dy.device, dtype=dy.dtype)
         a = _conv_args(src, wt, dx, 1, (R - 1 - pad[0], S - 1 - pad[1]), H, W)
         ws = _splitk_ws(a, "dp_conv_fwd_workspace", dy.device)
