@@ -8,6 +8,7 @@
 // All kernels are grid-stride loops over 16-byte vectors (8 x bf16 or 4 x fp32)
 // with a scalar tail, sized to a multiple of the SM count; arithmetic is fp32.
 #include <string>
+#include <cstdlib>
 #include "common.cuh"
 #include "dpipe.h"
 
@@ -713,6 +714,58 @@ __global__ void __launch_bounds__(256) bias_grad_vec_kernel(const T* __restrict_
   }
 }
 
+// db[c] += sum_r dy[r][c], block = CVB channel vectors (all of a row when C <= 256 vectors) x
+// 256/CVB row lanes: no idle lanes for C = 320 / 640 / 1280 (the 32-vector blocks above left
+// 3/4 of a block idle at C = 320); 4 rows' loads in flight per thread
+template <typename T>
+__global__ void __launch_bounds__(256) bias_grad_rows_kernel(const T* __restrict__ dy, float* __restrict__ db,
+                                                             int64_t rows, int C, int CVB, int seg) {
+  DP_PDL_ENTRY();
+  constexpr int V = VecT<T>::N;
+  const int CV = C / V;
+  const int RL = 256 / CVB;
+  const int lane_v = threadIdx.x % CVB, rl = threadIdx.x / CVB;
+  const int cv = blockIdx.x * CVB + lane_v;
+  const int64_t r0 = (int64_t)blockIdx.y * seg;
+  const int64_t r1 = min(rows, r0 + seg);
+  float acc[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) acc[j] = 0.f;
+  if (rl < RL && cv < CV) {
+    const T* p = dy + cv * V;
+    int64_t r = r0 + rl;
+    for (; r + 3 * RL < r1; r += 4 * RL) {
+      float f[4][V];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load_vec(p + (r + u * RL) * C, f[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] += f[u][j];
+    }
+    for (; r < r1; r += RL) {
+      float f[V];
+      load_vec(p + r * C, f);
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[j] += f[j];
+    }
+  }
+  __shared__ float red[256 * 8];
+  if (rl < RL) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) red[rl * CVB * V + lane_v * V + j] = acc[j];
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < CVB * V; t += 256) {
+    const int c = blockIdx.x * CVB * V + t;
+    if (c < C) {
+      float s = 0.f;
+      for (int k = 0; k < RL; ++k) s += red[k * CVB * V + t];
+      atomicAdd(db + c, s);
+    }
+  }
+}
+
 }  // namespace dp
 
 using namespace dp;
@@ -959,6 +1012,25 @@ int dp_space_to_depth(int dtype, const void* x, void* y, int N, int H, int W, in
 int dp_bias_grad(int dtype, const void* dy, float* db, int64_t rows, int C, dp_stream_t stream) {
   if (rows <= 0) return 0;
   const int V = dtype == DP_F32 ? 4 : 8;
+  static const bool old_path = getenv("DP_BIAS_GRAD_OLD") != nullptr;  // A/B experiments
+  if (C % V == 0 && aligned16(dy) && !old_path) {
+    const int CV = C / V;
+    // channel vectors per block: the divisor of CV (<= 256) that keeps the most of 256 threads busy
+    int CVB = 0, best = -1;
+    for (int d = 1; d <= 256 && d <= CV; ++d)
+      if (CV % d == 0 && (256 / d) * d >= best) {
+        best = (256 / d) * d;
+        CVB = d;
+      }
+    const int RL = 256 / CVB;
+    // ~4 resident blocks per SM, at least 4 rows per row lane
+    int64_t seg = (rows + 4 * kNumSMs - 1) / (4 * kNumSMs);
+    if (seg < 4 * RL) seg = 4 * RL;
+    dim3 grid(CV / CVB, static_cast<unsigned>((rows + seg - 1) / seg));
+    DISPATCH_T(dtype, launch_k(bias_grad_rows_kernel<T>, dim3(grid), dim3(256), 0, ST, cp<T>(dy), db, rows, C, CVB,
+                               static_cast<int>(seg)));
+    return ew_check("bias_grad");
+  }
   if (C % V == 0 && aligned16(dy)) {
     // 16-byte vectors: a block covers 32 vectors (256 bf16 channels) x 8 row lanes
     const int CV = C / V;

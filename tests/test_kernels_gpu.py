@@ -249,3 +249,15 @@ def test_flash_attention_causal_forward(B, N, C, heads):
     Q, K, V = (q.float()[..., i * C:(i + 1) * C].reshape(B, N, heads, 64).transpose(1, 2) for i in range(3))
     ref = F.scaled_dot_product_attention(Q, K, V, is_causal=True).transpose(1, 2).reshape(B, N, C)
     assert _rel(o, ref) < 2e-2
+
+
+@pytest.mark.parametrize("dt", DT)
+@pytest.mark.parametrize("rows,C", [(32768, 320), (8192, 640), (2048, 1280), (512, 2560), (100, 8), (77, 1024)])
+def test_bias_grad(dt, rows, C):
+    """db += column sums of dy (bias gradients of linears / convs) vs fp32 torch."""
+    from paper_2405_01248_b200 import ops
+    dy = torch.randn(rows, C, device="cuda").to(dt)
+    db = torch.randn(C, device="cuda")
+    ref = db + dy.float().sum(0)
+    ops.bias_grad(dy, db)
+    assert _rel(db, ref) < 1e-4
