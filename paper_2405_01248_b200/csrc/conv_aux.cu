@@ -137,6 +137,27 @@ __global__ void dilate_kernel(const T* __restrict__ dy, T* __restrict__ out, int
   }
 }
 
+// bf16, C % 8 == 0: one thread per 16-byte channel vector of the dilated map
+__global__ void dilate_vec_kernel(const __nv_bfloat16* __restrict__ dy, __nv_bfloat16* __restrict__ out, int N,
+                                  int P, int Q, int C, int stride) {
+  DP_PDL_ENTRY();
+  const int Ho = P * stride, Wo = Q * stride, CV = C / 8;
+  const int64_t total = (int64_t)N * Ho * Wo * CV;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int cv = static_cast<int>(i % CV);
+    int64_t t = i / CV;
+    const int w = static_cast<int>(t % Wo);
+    t /= Wo;
+    const int h = static_cast<int>(t % Ho);
+    const int n = static_cast<int>(t / Ho);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (h % stride == 0 && w % stride == 0)
+      v = *reinterpret_cast<const uint4*>(dy + (((int64_t)n * P + h / stride) * Q + w / stride) * C + cv * 8);
+    *reinterpret_cast<uint4*>(out + i * 8) = v;
+  }
+}
+
 static inline int grid_for(int64_t total) {
   int64_t g = (total + 255) / 256;
   const int64_t cap = (int64_t)kNumSMs * 16;
@@ -209,6 +230,9 @@ int dp_dilate(int dtype, const void* dy, void* out, int N, int P, int Q, int C, 
   if (dtype == DP_F32)
     launch_k(dilate_kernel<float>, dim3(grid_for(total)), dim3(256), 0, st, (const float*)dy, (float*)out, N, P, Q,
                                                            C, stride);
+  else if (C % 8 == 0 && (reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(out)) % 16 == 0)
+    launch_k(dilate_vec_kernel, dim3(grid_for(total / 8)), dim3(256), 0, st, (const __nv_bfloat16*)dy,
+             (__nv_bfloat16*)out, N, P, Q, C, stride);
   else
     launch_k(dilate_kernel<__nv_bfloat16>, dim3(grid_for(total)), dim3(256), 0, st, 
         (const __nv_bfloat16*)dy, (__nv_bfloat16*)out, N, P, Q, C, stride);

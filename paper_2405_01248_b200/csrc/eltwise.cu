@@ -411,6 +411,56 @@ __global__ void upsample2x_bwd_kernel(const T* __restrict__ dy, T* __restrict__ 
   }
 }
 
+// 16-byte channel vectors (C % V == 0): one thread per output pixel-vector of the 2x map, the
+// source pixel read once per vector (the scalar kernels above divide per element)
+template <typename T>
+__global__ void upsample2x_vec_kernel(const T* __restrict__ x, T* __restrict__ y, int N, int H, int W, int C) {
+  DP_PDL_ENTRY();
+  constexpr int V = VecT<T>::N;
+  const int CV = C / V;
+  const int64_t n = (int64_t)N * 2 * H * 2 * W * CV;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int cv = static_cast<int>(i % CV);
+    const int64_t pix = i / CV;  // (b, h2, w2)
+    const int w2 = static_cast<int>(pix % (2 * W));
+    const int64_t t = pix / (2 * W);
+    const int h2 = static_cast<int>(t % (2 * H));
+    const int b = static_cast<int>(t / (2 * H));
+    *reinterpret_cast<uint4*>(y + i * V) =
+        *reinterpret_cast<const uint4*>(x + (((int64_t)b * H + h2 / 2) * W + w2 / 2) * C + cv * V);
+  }
+}
+template <typename T>
+__global__ void upsample2x_bwd_vec_kernel(const T* __restrict__ dy, T* __restrict__ dx, int N, int H, int W,
+                                          int C) {
+  DP_PDL_ENTRY();
+  constexpr int V = VecT<T>::N;
+  const int CV = C / V;
+  const int64_t n = (int64_t)N * H * W * CV;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int cv = static_cast<int>(i % CV);
+    const int64_t pix = i / CV;  // (b, h, w)
+    const int w = static_cast<int>(pix % W);
+    const int64_t t = pix / W;
+    const int h = static_cast<int>(t % H);
+    const int b = static_cast<int>(t / H);
+    const int64_t W2 = 2 * W;
+    const T* s = dy + (((int64_t)b * 2 * H + 2 * h) * W2 + 2 * w) * C + cv * V;
+    float a[V], f[V];
+    load_vec(s, a);
+    load_vec(s + C, f);
+#pragma unroll
+    for (int j = 0; j < V; ++j) a[j] += f[j];
+    load_vec(s + W2 * C, f);
+#pragma unroll
+    for (int j = 0; j < V; ++j) a[j] += f[j];
+    load_vec(s + W2 * C + C, f);
+#pragma unroll
+    for (int j = 0; j < V; ++j) a[j] += f[j];
+    store_vec(dx + i * V, a);
+  }
+}
+
 template <typename TI, typename TO>
 __global__ void cast_kernel(const TI* __restrict__ x, TO* __restrict__ y, int64_t n) {
   DP_PDL_ENTRY();
@@ -947,6 +997,12 @@ int dp_split(int dtype, const void* src, void* a, void* b, int64_t rows, int Ca,
 int dp_upsample2x(int dtype, const void* x, void* y, int N, int H, int W, int C,
                   dp_stream_t stream) {
   if (N <= 0) return 0;
+  const int V = dtype == DP_F32 ? 4 : 8;
+  if (C % V == 0 && aligned16(x) && aligned16(y)) {
+    DISPATCH_T(dtype, launch_k(upsample2x_vec_kernel<T>, dim3(ew_grid((int64_t)N * 4 * H * W * (C / V))), dim3(256),
+                               0, ST, cp<T>(x), mp<T>(y), N, H, W, C));
+    return ew_check("upsample2x");
+  }
   DISPATCH_T(dtype, launch_k(upsample2x_kernel<T>, dim3(ew_grid((int64_t)N * 4 * H * W * C)), dim3(256), 0, ST, 
                         cp<T>(x), mp<T>(y), N, H, W, C));
   return ew_check("upsample2x");
@@ -955,6 +1011,12 @@ int dp_upsample2x(int dtype, const void* x, void* y, int N, int H, int W, int C,
 int dp_upsample2x_bwd(int dtype, const void* dy, void* dx, int N, int H, int W, int C,
                       dp_stream_t stream) {
   if (N <= 0) return 0;
+  const int V = dtype == DP_F32 ? 4 : 8;
+  if (C % V == 0 && aligned16(dy) && aligned16(dx)) {
+    DISPATCH_T(dtype, launch_k(upsample2x_bwd_vec_kernel<T>, dim3(ew_grid((int64_t)N * H * W * (C / V))), dim3(256),
+                               0, ST, cp<T>(dy), mp<T>(dx), N, H, W, C));
+    return ew_check("upsample2x_bwd");
+  }
   DISPATCH_T(dtype, launch_k(upsample2x_bwd_kernel<T>, dim3(ew_grid((int64_t)N * H * W * C)), dim3(256), 0, ST, 
                         cp<T>(dy), mp<T>(dx), N, H, W, C));
   return ew_check("upsample2x_bwd");

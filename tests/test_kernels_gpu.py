@@ -164,6 +164,12 @@ def test_eltwise_family(dt):
     up = ops.upsample2x(u)
     assert torch.equal(up, u.repeat_interleave(2, 1).repeat_interleave(2, 2))
     assert _rel(ops.upsample2x_bwd(up), 4 * u.float()) < _tol(dt)
+    for C in (64, 3):  # 16-byte channel vectors / scalar path
+        u = torch.randn(2, 4, 5, C, device="cuda").to(dt)
+        assert torch.equal(ops.upsample2x(u), u.repeat_interleave(2, 1).repeat_interleave(2, 2))
+        g = torch.randn(2, 8, 10, C, device="cuda").to(dt)
+        ref = g.float().view(2, 4, 2, 5, 2, C).sum((2, 4))
+        assert _rel(ops.upsample2x_bwd(g), ref) < _tol(dt)
 
 
 def test_adamw_matches_torch():
