@@ -350,6 +350,29 @@ __global__ void concat_kernel(const T* __restrict__ a, const T* __restrict__ b, 
     dst[i] = c < Ca ? a[r * Ca + c] : (b ? b[r * Cb + (c - Ca)] : from_f<T>(0.f));
   }
 }
+// row-vector variant for narrow unaligned inputs (3 / 4-channel images and latents padded with
+// zeros or joined with a channel block): one thread per 16-byte vector of a dst row, gathered from
+// a / b element-wise and stored as one vector
+template <typename T>
+__global__ void concat_rowvec_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ dst,
+                                     int64_t rows, int Ca, int Cb) {
+  DP_PDL_ENTRY();
+  constexpr int V = VecT<T>::N;
+  const int C = Ca + Cb, CV = C / V;
+  const int64_t n = rows * CV;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / CV;
+    const int c0 = static_cast<int>(i - r * CV) * V;
+    float f[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int c = c0 + j;
+      f[j] = c < Ca ? to_f(a[r * Ca + c]) : (b ? to_f(b[r * Cb + (c - Ca)]) : 0.f);
+    }
+    store_vec(dst + i * V, f);
+  }
+}
+
 // a[r] (+)= src[r][0:Ca], b[r] (+)= src[r][Ca:]   (either output may be null)
 template <typename T>
 __global__ void split_kernel(const T* __restrict__ src, T* __restrict__ a, T* __restrict__ b,
@@ -849,8 +872,8 @@ int dp_act_fwd(int op, int dtype, const void* x, void* y, int64_t n, dp_stream_t
     set_error("dp_act_fwd: pointers must be 16-byte aligned");
     return DP_ERR_ARGS;
   }
-  DISPATCH_T(dtype, act_fwd_kernel<T><<<ew_grid(n / VecT<T>::N + 1), 256, 0, ST>>>(
-                        op, cp<T>(x), mp<T>(y), n));
+  DISPATCH_T(dtype, launch_k(act_fwd_kernel<T>, dim3(ew_grid(n / VecT<T>::N + 1)), dim3(256), 0, ST,
+                             op, cp<T>(x), mp<T>(y), n));
   return ew_check("act_fwd");
 }
 
@@ -861,8 +884,8 @@ int dp_act_bwd(int op, int dtype, const void* x, const void* dy, void* dx, int64
     set_error("dp_act_bwd: pointers must be 16-byte aligned");
     return DP_ERR_ARGS;
   }
-  DISPATCH_T(dtype, act_bwd_kernel<T><<<ew_grid(n / VecT<T>::N + 1), 256, 0, ST>>>(
-                        op, cp<T>(x), cp<T>(dy), mp<T>(dx), n, accumulate));
+  DISPATCH_T(dtype, launch_k(act_bwd_kernel<T>, dim3(ew_grid(n / VecT<T>::N + 1)), dim3(256), 0, ST,
+                             op, cp<T>(x), cp<T>(dy), mp<T>(dx), n, accumulate));
   return ew_check("act_bwd");
 }
 
@@ -900,8 +923,8 @@ int dp_axpby(int dtype, const void* a, const void* b, void* y, int64_t n, float 
     set_error("dp_axpby: pointers must be 16-byte aligned");
     return DP_ERR_ARGS;
   }
-  DISPATCH_T(dtype, axpby_kernel<T><<<ew_grid(n / VecT<T>::N + 1), 256, 0, ST>>>(
-                        cp<T>(a), cp<T>(b), mp<T>(y), n, alpha, beta));
+  DISPATCH_T(dtype, launch_k(axpby_kernel<T>, dim3(ew_grid(n / VecT<T>::N + 1)), dim3(256), 0, ST,
+                             cp<T>(a), cp<T>(b), mp<T>(y), n, alpha, beta));
   return ew_check("axpby");
 }
 
@@ -973,6 +996,11 @@ int dp_concat(int dtype, const void* a, const void* b, void* dst, int64_t rows, 
   if (Ca % V == 0 && Cb % V == 0 && aligned16(a) && aligned16(dst) && (!b || aligned16(b))) {
     DISPATCH_T(dtype, launch_k(concat_vec_kernel<T>, dim3(ew_grid(rows * (Ca + Cb) / V)), dim3(256), 0, ST, 
                           cp<T>(a), cp<T>(b), mp<T>(dst), rows, Ca, Cb));
+    return ew_check("concat");
+  }
+  if ((Ca + Cb) % V == 0 && aligned16(dst)) {
+    DISPATCH_T(dtype, launch_k(concat_rowvec_kernel<T>, dim3(ew_grid(rows * (Ca + Cb) / V)), dim3(256), 0, ST,
+                               cp<T>(a), cp<T>(b), mp<T>(dst), rows, Ca, Cb));
     return ew_check("concat");
   }
   DISPATCH_T(dtype, launch_k(concat_kernel<T>, dim3(ew_grid(rows * (Ca + Cb))), dim3(256), 0, ST, 

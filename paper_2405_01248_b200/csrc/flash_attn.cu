@@ -673,7 +673,8 @@ extern "C" int dp_flash_attn_fwd(const DpAttnArgs* a, dp_stream_t stream) {
   }
   fa::Params p{a->N, a->Nk, a->heads, a->scale * 1.4426950408889634f, a->lse, a->causal};
   dim3 grid((a->N + fa::BQ - 1) / fa::BQ, a->heads, a->B);
-  fa::fa_fwd_kernel<<<grid, 128, fa::SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(mq, mk, mv, mo, p);
+  launch_k(fa::fa_fwd_kernel, dim3(grid), dim3(128), fa::SMEM, reinterpret_cast<cudaStream_t>(stream), mq, mk, mv,
+           mo, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("flash attention launch: ") + cudaGetErrorString(e));
@@ -728,7 +729,7 @@ extern "C" int dp_flash_attn_bwd(const DpAttnArgs* a, const void* dout, int64_t 
     const int64_t total = (int64_t)a->B * a->heads * a->N;
     int gp = static_cast<int>((total * 8 + 255) / 256);
     if (gp > 148 * 8) gp = 148 * 8;
-    fa::fa_bwd_prep_kernel<<<gp, 256, 0, st>>>(
+    launch_k(fa::fa_bwd_prep_kernel, dim3(gp), dim3(256), 0, st,
         reinterpret_cast<const __nv_bfloat16*>(a->o), reinterpret_cast<const __nv_bfloat16*>(dout), Dv, a->B,
         a->N, a->heads, a->o_ld, do_ld);
   }

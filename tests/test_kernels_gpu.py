@@ -267,3 +267,16 @@ def test_bias_grad(dt, rows, C):
     ref = db + dy.float().sum(0)
     ops.bias_grad(dy, db)
     assert _rel(db, ref) < 1e-4
+
+
+@pytest.mark.parametrize("dt", DT)
+@pytest.mark.parametrize("Ca,Cb,zeros", [(3, 5, True), (4, 60, True), (4, 4, False), (320, 320, False),
+                                         (5, 6, False)])
+def test_concat_last(dt, Ca, Cb, zeros):
+    """Channel concat (U-Net skips, self-conditioning input, zero channel padding) vs torch.cat."""
+    from paper_2405_01248_b200 import ops
+    a = torch.randn(7, 9, Ca, device="cuda").to(dt)
+    b = None if zeros else torch.randn(7, 9, Cb, device="cuda").to(dt)
+    out = ops.concat_last(a, b, Cb)
+    ref = torch.cat([a, torch.zeros(7, 9, Cb, device="cuda", dtype=dt) if zeros else b], -1)
+    assert torch.equal(out, ref)
