@@ -52,18 +52,21 @@ __global__ void __launch_bounds__(128, 2)
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment by an offset from the __shared__ array (not an integer round trip), so the
   // compiler keeps the shared address space: LDS/STS instead of generic LD/ST on the LSU path
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  uint8_t* smem = smem_raw + pad;
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + TILE_BYTES;          // 2 buffers
-  uint8_t* sV = sK + 2 * TILE_BYTES;      // 1 buffer
-  uint8_t* sP = sV + TILE_BYTES;          // 2 x 16 KB (keys 0-63, 64-127)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 2 * TILE_BYTES);
+  uint8_t* sV = sK + 2 * TILE_BYTES;      // 2 buffers
+  uint8_t* sP = sV + 2 * TILE_BYTES;      // 2 x 16 KB (keys 0-63, 64-127)
+  // barriers in the alignment slack when it has room, else after the tiles: the request is exactly
+  // 7 tiles + 1 KB, so two CTAs (+ 1 KB system reservation each) fill the SM's 228 KB
+  uint64_t* bar = reinterpret_cast<uint64_t*>(pad >= 64 ? smem_raw : sP + 2 * TILE_BYTES);
   uint64_t* bar_q = bar;
   uint64_t* bar_k = bar + 1;  // [2]
-  uint64_t* bar_v = bar + 3;
-  uint64_t* bar_s = bar + 4;
-  uint64_t* bar_o = bar + 5;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 6);
+  uint64_t* bar_v = bar + 3;  // [2]
+  uint64_t* bar_s = bar + 5;
+  uint64_t* bar_o = bar + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 7);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(128, 2)
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
-    for (int i = 0; i < 6; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < 7; ++i) mbar_init(&bar[i], 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc<256>(tmem_slot);
@@ -87,60 +90,76 @@ __global__ void __launch_bounds__(128, 2)
   const uint32_t t_s = tmem;          // S: columns [0, 128)
   const uint32_t t_o = tmem + 128;    // O_j: columns [128, 192)
   const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+  const uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, 0, 0);
+  const uint32_t idesc_o = idesc_bf16_f32(BQ, HD, 0, 1);
 
+  // Pipeline per key tile j (one MMA-issuing thread, in-order tensor pipe):
+  //   PV(j) and S(j+1) are issued back to back after P(j) is in shared memory, so one wait on
+  //   S(j+1) also covers PV(j): O_j and S_{j+1} leave TMEM under a single tcgen05.wait, and O_j is
+  //   folded into the register accumulator one iteration late (with alpha_j kept from tile j).
+  //   K and V are double-buffered (V(j+1) streams in while tile j's softmax runs).
+  auto issue_s = [&](int j) {
+    const int kb = j & 1;
+    mbar_wait(&bar_k[kb], (j >> 1) & 1);
+    tc_fence_after();
+    const uint32_t qa = smem_u32(sQ), ka = smem_u32(sK + kb * TILE_BYTES);
+#pragma unroll
+    for (int k = 0; k < HD / 16; ++k)
+      tc_mma_bf16(t_s, smem_desc_sw128(qa + k * 32, 16, 1024), smem_desc_sw128(ka + k * 32, 16, 1024),
+                  idesc_s, k > 0 ? 1u : 0u);
+    tc_commit(bar_s);
+  };
   if (tid == 0) {
     mbar_expect_tx(bar_q, TILE_BYTES);
     tma_load_4d_(&tmQ, bar_q, sQ, 0, q0, h, b);
-    mbar_expect_tx(&bar_k[0], TILE_BYTES);
-    tma_load_4d_(&tmK, &bar_k[0], sK, 0, 0, h, b);
-    mbar_expect_tx(bar_v, TILE_BYTES);
-    tma_load_4d_(&tmV, bar_v, sV, 0, 0, h, b);
-    if (ntiles > 1) {
-      mbar_expect_tx(&bar_k[1], TILE_BYTES);
-      tma_load_4d_(&tmK, &bar_k[1], sK + TILE_BYTES, 0, BKV, h, b);
+    for (int t = 0; t < 2 && t < ntiles; ++t) {
+      mbar_expect_tx(&bar_k[t], TILE_BYTES);
+      tma_load_4d_(&tmK, &bar_k[t], sK + t * TILE_BYTES, 0, t * BKV, h, b);
+      mbar_expect_tx(&bar_v[t], TILE_BYTES);
+      tma_load_4d_(&tmV, &bar_v[t], sV + t * TILE_BYTES, 0, t * BKV, h, b);
     }
+    mbar_wait(bar_q, 0);
+    issue_s(0);
   }
-  const uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, 0, 0);
-  const uint32_t idesc_o = idesc_bf16_f32(BQ, HD, 0, 1);
 
   float o[HD];
 #pragma unroll
   for (int i = 0; i < HD; ++i) o[i] = 0.f;
-  float m_run = -INFINITY, l_run = 0.f;
+  float m_run = -INFINITY, l_run = 0.f, alpha_prev = 1.f;
   const int row = tid;  // query row inside the tile
 
-  for (int j = 0; j < ntiles; ++j) {
-    const int kb = j & 1;
-    if (tid == 0) {
-      if (j == 0) mbar_wait(bar_q, 0);
-      mbar_wait(&bar_k[kb], (j >> 1) & 1);
-      tc_fence_after();
-      const uint32_t qa = smem_u32(sQ), ka = smem_u32(sK + kb * TILE_BYTES);
+  auto fold_o = [&](const uint32_t (&v)[HD], float alpha) {
 #pragma unroll
-      for (int k = 0; k < HD / 16; ++k)
-        tc_mma_bf16(t_s, smem_desc_sw128(qa + k * 32, 16, 1024), smem_desc_sw128(ka + k * 32, 16, 1024),
-                    idesc_s, k > 0 ? 1u : 0u);
-      tc_commit(bar_s);
-    }
-    mbar_wait(bar_s, j & 1);
+    for (int i = 0; i < HD; ++i) o[i] = fmaf(o[i], alpha, __uint_as_float(v[i]));
+  };
+
+  for (int j = 0; j < ntiles; ++j) {
+    mbar_wait(bar_s, j & 1);  // S(j) done, and (in-order) PV(j-1) too
     tc_fence_after();
-    // keys of this tile the row may see (key 0 is always visible, so m stays finite)
     const int valid = p.causal ? min(min(BKV, p.Nk - j * BKV), q0 + row - j * BKV + 1)
                                : min(BKV, p.Nk - j * BKV);
-    // the row's 128 scores come out of TMEM once (4 loads, one wait) and stay in registers for
-    // both the row max and the exponentials
+    // the row's 128 scores (and O_{j-1}) come out of TMEM under one wait
     uint32_t sv[BKV];
 #pragma unroll
     for (int c = 0; c < BKV / 32; ++c)
       tmem_ld_32x32(t_s + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
-    tmem_ld_wait();
+    if (j > 0) {
+      uint32_t ov[HD];
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c)
+        tmem_ld_32x32(t_o + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&ov[c * 32]));
+      tmem_ld_wait();
+      fold_o(ov, alpha_prev);
+    } else {
+      tmem_ld_wait();
+    }
     float mx = -INFINITY;
 #pragma unroll
     for (int i = 0; i < BKV; ++i)
       if (i < valid) mx = fmaxf(mx, __uint_as_float(sv[i]));
     const float m_new = fmaxf(m_run, mx * p.scale_log2);
     const float alpha = ex2(m_run - m_new);
-    // P = exp2(s*scale - m) -> bf16 -> shared (SWIZZLE_128B K-major rows)
+    // P = exp2(s*scale - m) -> bf16 -> shared (SWIZZLE_128B K-major rows); PV(j-1) has read sP
     float lsum = 0.f;
 #pragma unroll
     for (int c = 0; c < BKV / 32; ++c) {
@@ -165,17 +184,13 @@ __global__ void __launch_bounds__(128, 2)
     }
     fence_async_shared();
     tc_fence_before();
-    __syncthreads();
+    __syncthreads();  // P(j) in shared memory; every thread has read S(j) and O_{j-1} from TMEM
     if (tid == 0) {
       tc_fence_after();
-      // S MMA of tile j has completed (bar_s), so K buffer kb can be refilled
-      if (j + 2 < ntiles) {
-        mbar_expect_tx(&bar_k[kb], TILE_BYTES);
-        tma_load_4d_(&tmK, &bar_k[kb], sK + kb * TILE_BYTES, 0, (j + 2) * BKV, h, b);
-      }
-      mbar_wait(bar_v, j & 1);
+      const int vb = j & 1;
+      mbar_wait(&bar_v[vb], (j >> 1) & 1);
       tc_fence_after();
-      const uint32_t pa = smem_u32(sP), va = smem_u32(sV);
+      const uint32_t pa = smem_u32(sP), va = smem_u32(sV + vb * TILE_BYTES);
 #pragma unroll
       for (int k = 0; k < BKV / 16; ++k) {
         const uint64_t ad = smem_desc_sw128(pa + (k >> 2) * TILE_BYTES + (k & 3) * 32, 16, 1024);
@@ -183,25 +198,35 @@ __global__ void __launch_bounds__(128, 2)
         tc_mma_bf16(t_o, ad, bd, idesc_o, k > 0 ? 1u : 0u);
       }
       tc_commit(bar_o);
-    }
-    mbar_wait(bar_o, j & 1);
-    tc_fence_after();
-    if (tid == 0 && j + 1 < ntiles) {
-      mbar_expect_tx(bar_v, TILE_BYTES);
-      tma_load_4d_(&tmV, bar_v, sV, 0, (j + 1) * BKV, h, b);
-    }
-#pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
-      uint32_t v[32];
-      tmem_ld_32x32(t_o + lane_off + c * 32, v);
-      tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 32; ++i) o[c * 32 + i] = fmaf(o[c * 32 + i], alpha, __uint_as_float(v[i]));
+      if (j + 1 < ntiles) {
+        issue_s(j + 1);
+        // S(j) finished before S(j+1) was issued: K buffer j&1 is free for tile j+2; V buffer
+        // (j+1)&1 held V(j-1), read by PV(j-1), which finished before S(j)
+        if (j + 2 < ntiles) {
+          mbar_expect_tx(&bar_k[j & 1], TILE_BYTES);
+          tma_load_4d_(&tmK, &bar_k[j & 1], sK + (j & 1) * TILE_BYTES, 0, (j + 2) * BKV, h, b);
+        }
+      }
     }
     l_run = l_run * alpha + lsum;
     m_run = m_new;
-    tc_fence_before();
-    __syncthreads();
+    alpha_prev = alpha;
+    if (tid == 0 && j + 1 < ntiles && j >= 1) {
+      // V(j+1) into buffer (j+1)&1 (V(j-1) there was consumed by PV(j-1), complete before S(j))
+      mbar_expect_tx(&bar_v[(j + 1) & 1], TILE_BYTES);
+      tma_load_4d_(&tmV, &bar_v[(j + 1) & 1], sV + ((j + 1) & 1) * TILE_BYTES, 0, (j + 1) * BKV, h, b);
+    }
+  }
+  // the last PV
+  mbar_wait(bar_o, (ntiles - 1) & 1);
+  tc_fence_after();
+  {
+    uint32_t ov[HD];
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c)
+      tmem_ld_32x32(t_o + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&ov[c * 32]));
+    tmem_ld_wait();
+    fold_o(ov, alpha_prev);
   }
 
   // epilogue: O / l -> shared (SWIZZLE_128B rows of 64 bf16) -> one TMA store
@@ -233,7 +258,7 @@ __global__ void __launch_bounds__(128, 2)
   }
 }
 
-constexpr size_t SMEM = 1024 + 6 * TILE_BYTES + 64;
+constexpr size_t SMEM = 1024 + 7 * TILE_BYTES;
 
 // ------------------------------------------------------------------ backward
 // D[b][h][n] = sum_d dO[b][n][h*64+d] * O[b][n][h*64+d]: rows taken in memory order (b, n, h), eight
