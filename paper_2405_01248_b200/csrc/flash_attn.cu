@@ -13,6 +13,7 @@
 // Two CTAs fit per SM (96 KB shared memory, 256 TMEM columns each), so one CTA's softmax
 // overlaps the other's MMAs. Keys beyond N_k (cross-attention, 77 tokens) are masked.
 #include <cstdlib>
+#include <type_traits>
 #include <string>
 #include <cudaTypedefs.h>
 #include "common.cuh"
@@ -153,35 +154,44 @@ __global__ void __launch_bounds__(128, 2)
     } else {
       tmem_ld_wait();
     }
-    float mx = -INFINITY;
+    // full tiles (every row of the warp sees all 128 keys: the common case) run a copy of the
+    // softmax without the per-element key mask
+    float m_new, alpha, lsum = 0.f;
+    auto softmax_tile = [&](auto full_t) {
+      constexpr bool FULL = decltype(full_t)::value;
+      float mx = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < BKV; ++i)
-      if (i < valid) mx = fmaxf(mx, __uint_as_float(sv[i]));
-    const float m_new = fmaxf(m_run, mx * p.scale_log2);
-    const float alpha = ex2(m_run - m_new);
-    // P = exp2(s*scale - m) -> bf16 -> shared (SWIZZLE_128B K-major rows); PV(j-1) has read sP
-    float lsum = 0.f;
+      for (int i = 0; i < BKV; ++i)
+        if (FULL || i < valid) mx = fmaxf(mx, __uint_as_float(sv[i]));
+      m_new = fmaxf(m_run, mx * p.scale_log2);
+      alpha = ex2(m_run - m_new);
+      // P = exp2(s*scale - m) -> bf16 -> shared (SWIZZLE_128B K-major rows); PV(j-1) has read sP
 #pragma unroll
-    for (int c = 0; c < BKV / 32; ++c) {
-      float pv[32];
+      for (int c = 0; c < BKV / 32; ++c) {
+        float pv[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float e = (c * 32 + i < valid) ? ex2(fmaf(__uint_as_float(sv[c * 32 + i]), p.scale_log2, -m_new)) : 0.f;
-        pv[i] = e;
-        lsum += e;
+        for (int i = 0; i < 32; ++i) {
+          const float e = ex2(fmaf(__uint_as_float(sv[c * 32 + i]), p.scale_log2, -m_new));
+          pv[i] = (FULL || c * 32 + i < valid) ? e : 0.f;
+          lsum += pv[i];
+        }
+        uint8_t* blk = sP + (c >> 1) * TILE_BYTES + row * 128;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int chunk = (c & 1) * 4 + q;  // 16-byte chunk of the 128-byte row
+          uint4 u;
+          u.x = pack_bf16x2(pv[q * 8 + 0], pv[q * 8 + 1]);
+          u.y = pack_bf16x2(pv[q * 8 + 2], pv[q * 8 + 3]);
+          u.z = pack_bf16x2(pv[q * 8 + 4], pv[q * 8 + 5]);
+          u.w = pack_bf16x2(pv[q * 8 + 6], pv[q * 8 + 7]);
+          *reinterpret_cast<uint4*>(blk + ((chunk ^ (row & 7)) * 16)) = u;
+        }
       }
-      uint8_t* blk = sP + (c >> 1) * TILE_BYTES + row * 128;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int chunk = (c & 1) * 4 + q;  // 16-byte chunk of the 128-byte row
-        uint4 u;
-        u.x = pack_bf16x2(pv[q * 8 + 0], pv[q * 8 + 1]);
-        u.y = pack_bf16x2(pv[q * 8 + 2], pv[q * 8 + 3]);
-        u.z = pack_bf16x2(pv[q * 8 + 4], pv[q * 8 + 5]);
-        u.w = pack_bf16x2(pv[q * 8 + 6], pv[q * 8 + 7]);
-        *reinterpret_cast<uint4*>(blk + ((chunk ^ (row & 7)) * 16)) = u;
-      }
-    }
+    };
+    if (__all_sync(0xffffffffu, valid >= BKV))
+      softmax_tile(std::true_type{});
+    else
+      softmax_tile(std::false_type{});
     fence_async_shared();
     tc_fence_before();
     __syncthreads();  // P(j) in shared memory; every thread has read S(j) and O_{j-1} from TMEM
