@@ -161,13 +161,24 @@ def _bind(lib, name):
     fn.restype = _RESTYPES.get(name, ctypes.c_int)
 
 
+_telemetry = None
+
+
+def _tele():
+    global _telemetry
+    if _telemetry is None:
+        from . import telemetry
+
+        _telemetry = telemetry
+    return _telemetry
+
+
 def lib():
     """Load libdpipe.so once; raise loudly when it is missing. While the bench's kernel timer
     is active, calls go through a proxy that brackets each launch with CUDA events."""
     global _lib
     if _lib is not None:
-        from . import telemetry
-
+        telemetry = _tele()
         if telemetry.timer.active:
             return telemetry.TimedLib(_lib)
         return _lib
@@ -185,9 +196,7 @@ def lib():
 
 
 def check(rc: int, what: str, kernels: int = 1) -> None:
-    from . import telemetry
-
-    telemetry.count(what, kernels)
+    _tele().count(what, kernels)
     if rc != 0:
         msg = lib().dp_last_error().decode(errors="replace")
         raise DpipeError(f"{what} failed (code {rc}): {msg}")
