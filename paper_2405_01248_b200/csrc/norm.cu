@@ -16,6 +16,7 @@
 // y = xhat * (1 + scale[b]) + shift[b] (b = row / rows_per_sample).
 // Softmax over fp32 score rows (scale, optional causal mask) -> P in T, and its
 // backward dS = scale * P * (dP - rowsum(dP * P)).
+#include <cstdlib>
 #include <string>
 #include "common.cuh"
 #include "dpipe.h"
@@ -579,9 +580,31 @@ __global__ void __launch_bounds__(256)
   DP_PDL_ENTRY();
   constexpr int V = NV<T>::V;
   const int lane = threadIdx.x & 31;
-  const int64_t row = blockIdx.x * 8LL + (threadIdx.x >> 5);
-  if (row >= rows) return;
   const int CV = C / V;
+  // per-lane affine parameters loaded once (16-byte loads) for all the warp's rows: per-element
+  // scalar gamma/beta loads had been 8x the row's own load instructions
+  // (rows of <= 4 vectors per lane; wider rows load them per vector inside the row loop)
+  constexpr bool HOIST = NVEC <= 4;
+  float ga[HOIST ? NVEC : 1][V], be[HOIST ? NVEC : 1][V];
+  if (HOIST && gamma) {
+#pragma unroll
+    for (int k = 0; k < NVEC; ++k) {
+      const int cv = lane + 32 * k;
+      if (cv < CV) {
+#pragma unroll
+        for (int j = 0; j < V; j += 4) {
+          const float4 g4 = __ldg(reinterpret_cast<const float4*>(gamma + cv * V + j));
+          const float4 b4 = __ldg(reinterpret_cast<const float4*>(beta + cv * V + j));
+          ga[HOIST ? k : 0][j] = g4.x; ga[HOIST ? k : 0][j + 1] = g4.y;
+          ga[HOIST ? k : 0][j + 2] = g4.z; ga[HOIST ? k : 0][j + 3] = g4.w;
+          be[HOIST ? k : 0][j] = b4.x; be[HOIST ? k : 0][j + 1] = b4.y;
+          be[HOIST ? k : 0][j + 2] = b4.z; be[HOIST ? k : 0][j + 3] = b4.w;
+        }
+      }
+    }
+  }
+  // warps stride over rows: the grid is one wave of resident blocks (dp_layer_norm_fwd)
+  for (int64_t row = blockIdx.x * 8LL + (threadIdx.x >> 5); row < rows; row += gridDim.x * 8LL) {
   const T* xr = x + row * C;
   float v[NVEC][V];
   float s = 0.f;
@@ -620,17 +643,35 @@ __global__ void __launch_bounds__(256)
   for (int k = 0; k < NVEC; ++k) {
     const int cv = lane + 32 * k;
     if (cv < CV) {
-      float o[V];
+      float o[V], gv[V], bv[V];
+      if (gamma) {
+        if constexpr (HOIST) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            gv[j] = ga[HOIST ? k : 0][j];
+            bv[j] = be[HOIST ? k : 0][j];
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < V; j += 4) {
+            const float4 g4 = __ldg(reinterpret_cast<const float4*>(gamma + cv * V + j));
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(beta + cv * V + j));
+            gv[j] = g4.x; gv[j + 1] = g4.y; gv[j + 2] = g4.z; gv[j + 3] = g4.w;
+            bv[j] = b4.x; bv[j + 1] = b4.y; bv[j + 2] = b4.z; bv[j + 3] = b4.w;
+          }
+        }
+      }
 #pragma unroll
       for (int j = 0; j < V; ++j) {
         const int c = cv * V + j;
         float t = (v[k][j] - mu) * rs;
-        if (gamma) t = fmaf(t, __ldg(gamma + c), __ldg(beta + c));
+        if (gamma) t = fmaf(t, gv[j], bv[j]);
         if (mr) t = fmaf(t, 1.f + to_f(mr[scale_off + c]), to_f(mr[shift_off + c]));
         o[j] = t;
       }
       st16(yr + cv * V, o);
     }
+  }
   }
 }
 
@@ -669,6 +710,14 @@ __global__ void __launch_bounds__(256)
       if (cv < CV) {
         ld16(xr + cv * V, xh[k]);
         ld16(dr + cv * V, g[k]);
+        float gv[V];  // gamma of this vector: 16-byte loads (not one scalar load per element)
+        if (gamma) {
+#pragma unroll
+          for (int j = 0; j < V; j += 4) {
+            const float4 g4 = __ldg(reinterpret_cast<const float4*>(gamma + cv * V + j));
+            gv[j] = g4.x; gv[j + 1] = g4.y; gv[j + 2] = g4.z; gv[j + 3] = g4.w;
+          }
+        }
 #pragma unroll
         for (int j = 0; j < V; ++j) {
           const int c = cv * V + j;
@@ -678,7 +727,7 @@ __global__ void __launch_bounds__(256)
             ag[k][j] = fmaf(d, xh[k][j], ag[k][j]);
             ab[k][j] += d;
           }
-          if (gamma) d *= __ldg(gamma + c);
+          if (gamma) d *= gv[j];
           if (mr) d *= 1.f + to_f(mr[scale_off + c]);
           g[k][j] = d;
           s1 += d;
@@ -929,37 +978,6 @@ int dp_group_norm_bwd(int dtype, const void* x, const void* dy, const float* gam
     }                                                                                 \
   } while (0)
 
-int dp_layer_norm_fwd(int dtype, const void* x, const float* gamma, const float* beta,
-                      const void* mod, int64_t mod_ld, int shift_off, int scale_off,
-                      int rows_per_sample, void* y, float* mean, float* rstd, int64_t rows, int C,
-                      float eps, dp_stream_t stream) {
-  if (rows <= 0) return 0;
-  if (C > 2048 || (gamma && mod) || C % (dtype == DP_F32 ? 4 : 8) ||
-      (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) % 16) {
-    set_error("layer_norm: C <= 2048, C % 8 == 0 (bf16) / 4 (fp32), 16-byte aligned rows, "
-              "affine and modulation exclusive");
-    return DP_ERR_ARGS;
-  }
-  const dim3 grid(static_cast<unsigned>((rows + 7) / 8));
-  DISPATCH_T(dtype, LN_PER_DISPATCH(C, ln_fwd_kernel, cp<T>(x), gamma, beta, cp<T>(mod), mod_ld,
-                                    shift_off, scale_off, rows_per_sample > 0 ? rows_per_sample : 1,
-                                    mp<T>(y), mean, rstd, rows, C, eps));
-  return ew_check("layer_norm_fwd");
-}
-
-int dp_rms_norm_fwd(int dtype, const void* x, const float* gamma, void* y, int64_t rows, int C,
-                    float eps, dp_stream_t stream) {
-  if (rows <= 0) return 0;
-  const int V = dtype == DP_F32 ? 4 : 8;
-  if (C % V || C > 32 * 8 * V) {
-    set_error("rms_norm: need C % 8 == 0 (bf16) / 4 (fp32) and C <= 256 vectors");
-    return DP_ERR_ARGS;
-  }
-  dim3 grid(static_cast<unsigned>((rows + 7) / 8));
-  DISPATCH_T(dtype, LN_PER_DISPATCH(C, rms_fwd_kernel, cp<T>(x), gamma, mp<T>(y), rows, C, eps));
-  return ew_check("rms_norm_fwd");
-}
-
 // resident 256-thread blocks per SM of a kernel (cached per function pointer)
 static int ln_blocks_per_sm(const void* kern) {
   static const void* keys[32];
@@ -974,6 +992,47 @@ static int ln_blocks_per_sm(const void* kern) {
     vals[n++] = v;
   }
   return v;
+}
+
+int dp_layer_norm_fwd(int dtype, const void* x, const float* gamma, const float* beta,
+                      const void* mod, int64_t mod_ld, int shift_off, int scale_off,
+                      int rows_per_sample, void* y, float* mean, float* rstd, int64_t rows, int C,
+                      float eps, dp_stream_t stream) {
+  if (rows <= 0) return 0;
+  if (C > 2048 || (gamma && mod) || C % (dtype == DP_F32 ? 4 : 8) ||
+      (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) % 16) {
+    set_error("layer_norm: C <= 2048, C % 8 == 0 (bf16) / 4 (fp32), 16-byte aligned rows, "
+              "affine and modulation exclusive");
+    return DP_ERR_ARGS;
+  }
+  const int64_t want = (rows + 7) / 8;
+  static const bool one_block_per_8_rows = getenv("DP_LN_FWD_BLOCKS") != nullptr;  // A/B experiments
+  DISPATCH_T(dtype, {
+    const int nvec = (C / NV<T>::V + 31) / 32;
+    const void* kern = nvec <= 1   ? (const void*)ln_fwd_kernel<T, 1>
+                       : nvec <= 2 ? (const void*)ln_fwd_kernel<T, 2>
+                       : nvec <= 4 ? (const void*)ln_fwd_kernel<T, 4>
+                       : nvec <= 8 ? (const void*)ln_fwd_kernel<T, 8>
+                                   : (const void*)ln_fwd_kernel<T, 16>;
+    const int64_t cap = one_block_per_8_rows ? want : (int64_t)ln_blocks_per_sm(kern) * kNumSMs;
+    const dim3 grid(static_cast<unsigned>(want < cap ? want : cap));
+    LN_PER_DISPATCH(C, ln_fwd_kernel, cp<T>(x), gamma, beta, cp<T>(mod), mod_ld, shift_off, scale_off,
+                    rows_per_sample > 0 ? rows_per_sample : 1, mp<T>(y), mean, rstd, rows, C, eps);
+  });
+  return ew_check("layer_norm_fwd");
+}
+
+int dp_rms_norm_fwd(int dtype, const void* x, const float* gamma, void* y, int64_t rows, int C,
+                    float eps, dp_stream_t stream) {
+  if (rows <= 0) return 0;
+  const int V = dtype == DP_F32 ? 4 : 8;
+  if (C % V || C > 32 * 8 * V) {
+    set_error("rms_norm: need C % 8 == 0 (bf16) / 4 (fp32) and C <= 256 vectors");
+    return DP_ERR_ARGS;
+  }
+  dim3 grid(static_cast<unsigned>((rows + 7) / 8));
+  DISPATCH_T(dtype, LN_PER_DISPATCH(C, rms_fwd_kernel, cp<T>(x), gamma, mp<T>(y), rows, C, eps));
+  return ew_check("rms_norm_fwd");
 }
 
 int dp_layer_norm_bwd(int dtype, const void* x, const void* dy, const float* gamma,

@@ -21,3 +21,10 @@ for rows, C in [(32768, 320), (8192, 640), (2048, 1280), (2464, 1024)]:
     ms = t(lambda: ops.layer_norm_bwd(x, dy, g, m, r, dgamma=dg, dbeta=db, accumulate_into=acc))
     nb = x.numel() * 2 * 4
     print(f"({rows}, {C}) bwd+acc {ms * 1e3:7.1f} us {nb / ms / 1e6:6.0f} GB/s")
+
+for rows, C in [(32768, 320), (8192, 640), (2048, 1280), (2464, 1024)]:
+    x = torch.randn(rows, C, device="cuda").bfloat16()
+    g = torch.randn(C, device="cuda")
+    b = torch.randn(C, device="cuda")
+    ms = t(lambda: ops.layer_norm(x, g, b, 1e-5))
+    print(f"({rows}, {C}) fwd {ms * 1e3:7.1f} us {x.numel() * 4 / ms / 1e6:6.0f} GB/s")
