@@ -97,7 +97,17 @@ DP_DEV void epilogue_store(const TcParams& p, int row, int n, int z1, int z2, co
   for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * p.alpha;
   const int nvalid = min(32, p.N - n);
   if (p.bias) {
-    if (nvalid == 32) {
+    if (nvalid == 32 && (reinterpret_cast<uintptr_t>(p.bias + n) & 15) == 0) {
+      // 8 x 16-byte loads (the 32 scalar loads per chunk were warp-uniform but 32 instructions)
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + n + i));
+        f[i] += b4.x;
+        f[i + 1] += b4.y;
+        f[i + 2] += b4.z;
+        f[i + 3] += b4.w;
+      }
+    } else if (nvalid == 32) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) f[i] += __ldg(p.bias + n + i);
     } else {
@@ -263,7 +273,17 @@ DP_DEV void epilogue_math(const TcParams& p, int row, int n, int z1, int z2, con
   for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * p.alpha;
   const int nvalid = min(32, p.N - n);
   if (p.bias) {
-    if (nvalid == 32) {
+    if (nvalid == 32 && (reinterpret_cast<uintptr_t>(p.bias + n) & 15) == 0) {
+      // 8 x 16-byte loads (the 32 scalar loads per chunk were warp-uniform but 32 instructions)
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + n + i));
+        f[i] += b4.x;
+        f[i + 1] += b4.y;
+        f[i + 2] += b4.z;
+        f[i + 3] += b4.w;
+      }
+    } else if (nvalid == 32) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) f[i] += __ldg(p.bias + n + i);
     } else {
