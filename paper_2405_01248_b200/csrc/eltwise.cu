@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(const T* __restrict__ dy
 }
 
 // y[r][c] = x[r][c] + e[r / rps][c]  (ResBlock time-embedding add, broadcast over pixels)
-template <typename T>
+template <typename T, bool EV>
 __global__ void row_bias_fwd_kernel(const T* __restrict__ x, const T* __restrict__ e, int64_t e_ld,
                                     T* __restrict__ y, int64_t rows, int C, int rps) {
   DP_PDL_ENTRY();
@@ -589,8 +589,12 @@ __global__ void row_bias_fwd_kernel(const T* __restrict__ x, const T* __restrict
     float f[V], g[V];
     load_vec(x + r * C + cv * V, f);
     const T* er = e + (r / rps) * e_ld + cv * V;
+    if constexpr (EV) {
+      load_vec(er, g);  // 16-byte aligned rows of e (checked by the launcher)
+    } else {
 #pragma unroll
-    for (int j = 0; j < V; ++j) g[j] = to_f(er[j]);
+      for (int j = 0; j < V; ++j) g[j] = to_f(er[j]);
+    }
 #pragma unroll
     for (int j = 0; j < V; ++j) f[j] += g[j];
     store_vec(y + r * C + cv * V, f);
@@ -615,6 +619,52 @@ __global__ void __launch_bounds__(256) row_bias_bwd_kernel(const T* __restrict__
 #pragma unroll
     for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x];
     de[(int64_t)b * de_ld + c] = from_f<T>(s);
+  }
+}
+
+// de[b][c] = sum_{r in sample b} dy[r][c], 16-byte vectors: block = CVB channel vectors x 256/CVB row
+// lanes over one sample's rows (grid (CV/CVB, B)), deterministic (no atomics)
+template <typename T>
+__global__ void __launch_bounds__(256) row_bias_bwd_vec_kernel(const T* __restrict__ dy, T* __restrict__ de,
+                                                               int64_t de_ld, int C, int rps, int CVB) {
+  DP_PDL_ENTRY();
+  constexpr int V = VecT<T>::N;
+  const int b = blockIdx.y;
+  const int RL = 256 / CVB;
+  const int lv = threadIdx.x % CVB, rl = threadIdx.x / CVB;
+  const int cv = blockIdx.x * CVB + lv;
+  float acc[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) acc[j] = 0.f;
+  if (rl < RL) {
+    const T* p = dy + (int64_t)b * rps * C + cv * V;
+    int r = rl;
+    for (; r + 3 * RL < rps; r += 4 * RL) {
+      float f[4][V];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load_vec(p + (int64_t)(r + u * RL) * C, f[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] += f[u][j];
+    }
+    for (; r < rps; r += RL) {
+      float f[V];
+      load_vec(p + (int64_t)r * C, f);
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[j] += f[j];
+    }
+  }
+  __shared__ float red[256 * 8];
+  if (rl < RL) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) red[rl * CVB * V + lv * V + j] = acc[j];
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < CVB * V; t += 256) {
+    float s = 0.f;
+    for (int k = 0; k < RL; ++k) s += red[k * CVB * V + t];
+    de[(int64_t)b * de_ld + blockIdx.x * CVB * V + t] = from_f<T>(s);
   }
 }
 
@@ -1073,14 +1123,32 @@ int dp_row_bias_fwd(int dtype, const void* x, const void* e, int64_t e_ld, void*
     set_error("dp_row_bias_fwd: C must be a multiple of the vector width and x/y 16-byte aligned");
     return DP_ERR_ARGS;
   }
-  DISPATCH_T(dtype, launch_k(row_bias_fwd_kernel<T>, dim3(ew_grid(rows * C / V)), dim3(256), 0, ST, 
-                        cp<T>(x), cp<T>(e), e_ld, mp<T>(y), rows, C, rows_per_sample));
+  if (e_ld % V == 0 && aligned16(e))
+    DISPATCH_T(dtype, launch_k(row_bias_fwd_kernel<T, true>, dim3(ew_grid(rows * C / V)), dim3(256), 0, ST,
+                               cp<T>(x), cp<T>(e), e_ld, mp<T>(y), rows, C, rows_per_sample));
+  else
+    DISPATCH_T(dtype, launch_k(row_bias_fwd_kernel<T, false>, dim3(ew_grid(rows * C / V)), dim3(256), 0, ST,
+                               cp<T>(x), cp<T>(e), e_ld, mp<T>(y), rows, C, rows_per_sample));
   return ew_check("row_bias_fwd");
 }
 
 int dp_row_bias_bwd(int dtype, const void* dy, void* de, int64_t de_ld, int B, int C,
                     int rows_per_sample, dp_stream_t stream) {
   if (B <= 0) return 0;
+  const int V = dtype == DP_F32 ? 4 : 8;
+  if (C % V == 0 && de_ld % V == 0 && aligned16(dy) && aligned16(de)) {
+    const int CV = C / V;
+    int CVB = 0, best = -1;  // divisor of CV keeping the most of 256 threads busy (as dp_bias_grad)
+    for (int d = 1; d <= 256 && d <= CV; ++d)
+      if (CV % d == 0 && (256 / d) * d >= best) {
+        best = (256 / d) * d;
+        CVB = d;
+      }
+    dim3 g(CV / CVB, B);
+    DISPATCH_T(dtype, launch_k(row_bias_bwd_vec_kernel<T>, dim3(g), dim3(256), 0, ST, cp<T>(dy), mp<T>(de), de_ld,
+                               C, rows_per_sample, CVB));
+    return ew_check("row_bias_bwd");
+  }
   dim3 grid((C + 31) / 32, B);
   DISPATCH_T(dtype, launch_k(row_bias_bwd_kernel<T>, dim3(grid), dim3(256), 0, ST, cp<T>(dy), mp<T>(de), de_ld, C,
                                                                    rows_per_sample));

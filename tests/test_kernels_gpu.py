@@ -154,6 +154,14 @@ def test_eltwise_family(dt):
     assert _rel(y, h.float() + e.float()[:, None, None, :]) < _tol(dt)
     y.backward(torch.ones_like(y))
     assert _rel(e.grad, torch.full((3, 64), 64.0, device="cuda")) < _tol(dt)
+    for C in (320, 1280, 8):  # U-Net widths and a one-vector row
+        h = torch.randn(4, 16, 16, C, device="cuda").to(dt).requires_grad_(True)
+        e = torch.randn(4, C, device="cuda").to(dt).requires_grad_(True)
+        y = nn.add_row_bias(h, e)
+        assert _rel(y, h.float() + e.float()[:, None, None, :]) < _tol(dt)
+        g = torch.randn_like(y)
+        y.backward(g)
+        assert _rel(e.grad, g.float().sum((1, 2))) < _tol(dt)
     # space_to_depth round trip
     z = torch.randn(2, 8, 8, 4, device="cuda").to(dt)
     assert torch.equal(ops.space_to_depth(ops.space_to_depth(z, 2), 2, inverse=True), z)
