@@ -564,7 +564,13 @@ __global__ void __launch_bounds__(256)
     if (cv < CV) {
       float o[V];
 #pragma unroll
-      for (int j = 0; j < V; ++j) o[j] = v[k][j] * rs * __ldg(gamma + cv * V + j);
+      for (int j = 0; j < V; j += 4) {  // gamma as 16-byte loads
+        const float4 g4 = __ldg(reinterpret_cast<const float4*>(gamma + cv * V + j));
+        o[j] = v[k][j] * rs * g4.x;
+        o[j + 1] = v[k][j + 1] * rs * g4.y;
+        o[j + 2] = v[k][j + 2] * rs * g4.z;
+        o[j + 3] = v[k][j + 3] * rs * g4.w;
+      }
       st16(yr + cv * V, o);
     }
   }
@@ -1000,7 +1006,8 @@ int dp_layer_norm_fwd(int dtype, const void* x, const float* gamma, const float*
                       float eps, dp_stream_t stream) {
   if (rows <= 0) return 0;
   if (C > 2048 || (gamma && mod) || C % (dtype == DP_F32 ? 4 : 8) ||
-      (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) % 16) {
+      (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(gamma) |
+       reinterpret_cast<uintptr_t>(beta)) % 16) {
     set_error("layer_norm: C <= 2048, C % 8 == 0 (bf16) / 4 (fp32), 16-byte aligned rows, "
               "affine and modulation exclusive");
     return DP_ERR_ARGS;
@@ -1026,8 +1033,8 @@ int dp_rms_norm_fwd(int dtype, const void* x, const float* gamma, void* y, int64
                     float eps, dp_stream_t stream) {
   if (rows <= 0) return 0;
   const int V = dtype == DP_F32 ? 4 : 8;
-  if (C % V || C > 32 * 8 * V) {
-    set_error("rms_norm: need C % 8 == 0 (bf16) / 4 (fp32) and C <= 256 vectors");
+  if (C % V || C > 32 * 8 * V || reinterpret_cast<uintptr_t>(gamma) % 16) {
+    set_error("rms_norm: need C % 8 == 0 (bf16) / 4 (fp32), C <= 256 vectors, 16-byte aligned gamma");
     return DP_ERR_ARGS;
   }
   dim3 grid(static_cast<unsigned>((rows + 7) / 8));
@@ -1042,8 +1049,8 @@ int dp_layer_norm_bwd(int dtype, const void* x, const void* dy, const float* gam
                       int C, int accumulate, dp_stream_t stream) {
   if (rows <= 0) return 0;
   if (C > 2048 || (gamma && mod) || C % (dtype == DP_F32 ? 4 : 8) ||
-      (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy) |
-       reinterpret_cast<uintptr_t>(dx)) % 16) {
+      (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(dx) |
+       reinterpret_cast<uintptr_t>(gamma)) % 16) {
     set_error("layer_norm: C <= 2048, C % 8 == 0 (bf16) / 4 (fp32), 16-byte aligned rows, "
               "affine and modulation exclusive");
     return DP_ERR_ARGS;
