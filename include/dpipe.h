@@ -122,11 +122,12 @@ int64_t dp_gemm_workspace(const DpGemmArgs* args);
 int64_t dp_conv_fwd_workspace(const DpConvArgs* args);
 int64_t dp_conv_dgrad_workspace(const DpConvArgs* args);
 /* fused attention forward (tcgen05 S = QK^T and O = PV, online softmax from TMEM);
-   bf16, head_dim 64 */
+   bf16, head_dim 64; args->causal masks key j > query i (N == Nk; no backward) */
 int dp_flash_attn_fwd(const DpAttnArgs* args, dp_stream_t stream);
 /* fused attention backward (recomputes P from args->lse): dq (token stride dq_ld), dk/dv
-   (token stride dkv_ld) for the o written by dp_flash_attn_fwd; workspace holds
-   B*heads*N + B*N*heads*64 floats */
+   (token stride dkv_ld) for the o written by dp_flash_attn_fwd (non-causal); workspace holds
+   B*heads*N + B*N*heads*64 floats (the dQ accumulator is unused when Nk <= 128: dQ is stored
+   directly) */
 /* bytes of fp32 workspace dp_flash_attn_bwd needs for these args (D, dQ accumulator and, when the
    query tiles are split across CTAs, the dK/dV accumulators) */
 int64_t dp_flash_attn_bwd_workspace(const DpAttnArgs* args);
