@@ -99,9 +99,14 @@ struct GnGeom {
 
 template <int V>
 static GnGeom gn_geom(int N, int HW, int C, int G) {
-  // ~8 waves of CTAs (several resident per SM) with at least 64 pixels per chunk
+  // ~8 waves of CTAs (several resident per SM) with at least 512 pixels per chunk; small maps get
+  // their parallelism from channel blocks instead (fewer partials to merge per group)
+  static const int minpix = [] {  // pixels per chunk floor (DP_GN_MINPIX: experiments)
+    const char* e = getenv("DP_GN_MINPIX");
+    return e && atoi(e) > 0 ? atoi(e) : 512;  // swept 32..512 on the VAE / U-Net maps (tools/gn_bench.py)
+  }();
   int target = (8 * kNumSMs + N - 1) / N;
-  const int maxc = (HW + 63) / 64;
+  const int maxc = (HW + minpix - 1) / minpix;
   GnGeom g{};
   g.chunks = target < maxc ? target : maxc;
   if (g.chunks < 1) g.chunks = 1;
