@@ -1138,12 +1138,16 @@ int dp_row_bias_bwd(int dtype, const void* dy, void* de, int64_t de_ld, int B, i
   const int V = dtype == DP_F32 ? 4 : 8;
   if (C % V == 0 && de_ld % V == 0 && aligned16(dy) && aligned16(de)) {
     const int CV = C / V;
-    int CVB = 0, best = -1;  // divisor of CV keeping the most of 256 threads busy (as dp_bias_grad)
-    for (int d = 1; d <= 256 && d <= CV; ++d)
-      if (CV % d == 0 && (256 / d) * d >= best) {
-        best = (256 / d) * d;
+    // channel vectors per block: the largest divisor of CV (<= 256, >= 8 vectors = 128-byte row
+    // runs when CV allows) that still gives >= 2 blocks per SM over (channel blocks x samples)
+    const int lo = CV < 8 ? CV : 8;
+    int CVB = 0;
+    for (int d = (CV < 256 ? CV : 256); d >= lo; --d)
+      if (CV % d == 0) {
         CVB = d;
+        if ((int64_t)(CV / d) * B >= 2 * kNumSMs) break;
       }
+    if (CVB == 0) CVB = CV;
     dim3 g(CV / CVB, B);
     DISPATCH_T(dtype, launch_k(row_bias_bwd_vec_kernel<T>, dim3(g), dim3(256), 0, ST, cp<T>(dy), mp<T>(de), de_ld,
                                C, rows_per_sample, CVB));
