@@ -965,8 +965,15 @@ __global__ void __launch_bounds__(256)
     const float4 a = w[0], b = w[1];
     float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
     if (bias) {
+      if ((reinterpret_cast<uintptr_t>(bias) & 15) == 0) {  // two 16-byte loads
+        const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + v * 8));
+        const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + v * 8 + 4));
+        f[0] += b0.x; f[1] += b0.y; f[2] += b0.z; f[3] += b0.w;
+        f[4] += b1.x; f[5] += b1.y; f[6] += b1.z; f[7] += b1.w;
+      } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) f[j] += __ldg(bias + v * 8 + j);
+        for (int j = 0; j < 8; ++j) f[j] += __ldg(bias + v * 8 + j);
+      }
     }
     if (R) {
       const uint4 u = *reinterpret_cast<const uint4*>(R + z1 * r_bs1 + z2 * r_bs2 + (int64_t)m * r_ld + v * 8);
