@@ -8,7 +8,9 @@ Workload (configs[1] of BASELINE.json): SD v2.1 U-Net (865M, trainable) + frozen
 OpenCLIP ViT-H text encoder (23 layers) + frozen SD VAE encoder, 256 px, bf16
 compute with fp32 master weights / AdamW, synthetic data and random init.
 Per GPU 32 samples per iteration (weak scaling): world batch 32 N; N = 1 -> S = D = 1;
-N = 2 -> S = D = 2, M = 4; N = 4 -> S = D = 4, M = 4; N = 8 -> S = D = 4, M = 4, 2 groups.
+N = 2 -> S = D = 2, M = 4; N = 4 -> S = D = 4, M = 4; N = 8 -> S = D = 4, M = 4, 2 groups (c2/c4);
+c3: S = N/2 stages x 2 replicas over D = N; c5: S = D = N, M = 2N (see `layout`). N > 1 plans from
+a profile measured on the box and NCCL-measured CommCosts (profiling_run).
 
 value  : world samples/s, inputs resident in HBM, device-timed (CUDA events) over exactly K
          iterations after W warm-ups, max over ranks.
@@ -49,15 +51,17 @@ WORKLOADS = {
 WORKLOAD = WORKLOADS["c2"]
 
 
-def layout(n):
+def layout(n, config="c2"):
+    """Pipeline layout per GPU count and configuration: c2 / c4 follow
+    "4-stage pipeline x 2 DP" at N=8 (S = D = 4, two groups); c3 runs S = 4 stages over D = 8
+    devices (every stage replicated twice, reference partitioner.py:69-84); c5 is the "8-stage
+    pipeline on 8xB200" with M = 16 (BASELINE.json configs[4]). Fewer GPUs shrink the pipeline."""
     if n == 1:
         return dict(S=1, D=1, M=1)
-    if n == 2:
-        return dict(S=2, D=2, M=4)
-    if n == 4:
-        return dict(S=4, D=4, M=4)
-    if n == 8:
-        return dict(S=4, D=4, M=4)
+    if config == "c5":
+        return dict(S=n, D=n, M=2 * n)
+    if config == "c3" and n >= 4:
+        return dict(S=n // 2, D=n, M=4)
     S = min(n, 4)
     return dict(S=S, D=S, M=4)
 
@@ -217,6 +221,32 @@ def cpu_reference(steps, warmup, sample=1):
     return sample * len(times) / sum(times), torch.get_num_threads()
 
 
+def planner_cpu_baseline(reps=10):
+    """BASELINE.md §4 CPU baseline #1: the REFERENCE planner's evaluate_point (baseline/_ref, the
+    unmodified pipefill package) on the measured c2 B200 profile at the N=8 layout (S = D = 4, M = 4,
+    world 8, world batch 256), single-threaded Python, best of `reps` (perf_counter)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    prof_path = os.path.join(ROOT, "profiles", "r01_c2_measured_profile_D4_M4.json")
+    if not os.path.isdir(os.path.join(ref, "pipefill")) or not os.path.exists(prof_path):
+        return None
+    if ref not in sys.path:
+        sys.path.append(ref)
+    import importlib
+
+    Rpl = importlib.import_module("pipefill.planner")
+    Rpr = importlib.import_module("pipefill.profile")
+    prof = Rpr.load_profile(prof_path)
+    cl = Rpr.ClusterConfig(8, Rpr.CommCosts(2.0e11, 2e-5, 3.0e11, 1e-5))
+    best = float("inf")
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        Rpl.evaluate_point(prof, cl, 4, 4, 4, 256, bubble_min_len=0.002)
+        best = min(best, time.perf_counter() - t0)
+    return {"value": best * 1e3, "unit": "ms per evaluate_point", "cores": 1, "kind": "reference",
+            "sample": "reference pipefill evaluate_point(S=4, M=4, D=4, world 8, batch 256) on the measured "
+                      "c2 profile, best of 10"}
+
+
 def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -247,7 +277,7 @@ def main():
     ap.add_argument("--debug-share-gpu", action="store_true",
                     help="TEST ONLY: run all ranks on cuda:0 over gloo (validates the N>1 path)")
     ap.add_argument("--trace-out", default=None, help="write the measured schedule as a trace-event JSON")
-    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS),
+    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS) + ["c3-small", "c4-small", "c5-small"],
                     help="the headline (BASELINE.json metric) workload is c2; c3..c5 for reference")
     ap.add_argument("--graph", action="store_true",
                     help="N=1: replay the captured iteration as a CUDA graph (measured: no gain, GPU-bound)")
@@ -259,14 +289,16 @@ def main():
     rank, world, local = dist_setup(args.gpus, args.debug_share_gpu)
     from paper_2405_01248_b200 import engine
 
-    lay = layout(world)
+    lay = layout(world, args.config.split("-")[0])
     wb = args.per_gpu_batch * world
-    profile = None
+    profile = comm = None
     if lay["S"] > 1:
+        # measured per-layer costs (rank 0) and NCCL p2p / allreduce costs (all ranks), shared so
+        # every rank plans from identical inputs
         from paper_2405_01248_b200 import profiling_run
-        profile = profiling_run.shared_profile(args.config, world, rank, wb, **lay)
+        profile, comm = profiling_run.shared_profile(args.config, world, rank, wb, with_comm=True, **lay)
     trainer = engine.Trainer.create(args.config, world=world, rank=rank, world_batch=wb, profile=profile,
-                                    device=f"cuda:{local}", **lay)
+                                    device=f"cuda:{local}", comm=comm, **lay)
     W, K = args.warmup, args.steps
     trainer.prefetch(2 * W + 2 * K + 2, mode="device")
     for _ in range(W):
@@ -322,7 +354,7 @@ def main():
     speedup = 1.0
     if lay["S"] > 1:
         unf = engine.Trainer.create(args.config, world=world, rank=rank, world_batch=wb, profile=profile,
-                                    device=f"cuda:{local}", filled=False, **lay)
+                                    device=f"cuda:{local}", filled=False, comm=comm, **lay)
         unf.prefetch(W + K + 1, mode="device")
         for _ in range(W):
             unf.step()
@@ -361,9 +393,11 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == "c2":
-        v, cores = cpu_reference(1, 0)
+        v, cores = cpu_reference(2, 1)
         cpu = {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
-               "sample": "1 sample of the c2 training step on the CPU oracle (oracle/train_step.py, fp32)"}
+               "sample": "2 timed steps x 1 sample of the c2 training step after 1 warm-up step, CPU oracle "
+                         "(oracle/train_step.py, fp32)",
+               "planner": planner_cpu_baseline()}
 
     if rank == 0:
         res = trainer.ex.plan_result
@@ -371,7 +405,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded), random init",
-            "config": {"workload": WORKLOADS[args.config], "world_batch": wb, "group_batch": wb * lay["D"] // world,
+            "config": {"workload": WORKLOADS.get(args.config, args.config + " (reduced test variant)"), "world_batch": wb, "group_batch": wb * lay["D"] // world,
                        "S": lay["S"], "M": lay["M"], "D": lay["D"], "groups": world // lay["D"],
                        "parallelism": f"pp{lay['S']}xdp{world // lay['S']}",
                        "l2": "working set (weights 1.7 GB bf16 + activations) >> 126 MB L2",

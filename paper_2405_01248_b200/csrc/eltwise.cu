@@ -1147,7 +1147,12 @@ int dp_row_bias_bwd(int dtype, const void* dy, void* de, int64_t de_ld, int B, i
         CVB = d;
         if ((int64_t)(CV / d) * B >= 2 * kNumSMs) break;
       }
-    if (CVB == 0) CVB = CV;
+    if (CVB == 0)  // no divisor in [lo, 256] (e.g. prime CV > 256): the largest divisor <= 256
+      for (int d = (CV < 256 ? CV : 256); d >= 1; --d)
+        if (CV % d == 0) {
+          CVB = d;
+          break;
+        }
     dim3 g(CV / CVB, B);
     DISPATCH_T(dtype, launch_k(row_bias_bwd_vec_kernel<T>, dim3(g), dim3(256), 0, ST, cp<T>(dy), mp<T>(de), de_ld,
                                C, rows_per_sample, CVB));

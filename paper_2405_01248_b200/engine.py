@@ -275,7 +275,7 @@ class Trainer:
     @classmethod
     def create(cls, cfg="c1", *, world=1, rank=0, S=1, M=1, D=1, world_batch=None, device=None,
                seed=0, states=None, profile=None, filled=True, feed_mode="device", small=False,
-               bubble_min_len=B200_BUBBLE_MIN_LEN):
+               bubble_min_len=B200_BUBBLE_MIN_LEN, comm=None):
         c = CONFIGS[cfg] if isinstance(cfg, str) else cfg
         device = device or (f"cuda:{torch.cuda.current_device()}" if torch.cuda.is_available() else "cpu")
         model = build_model(c, device, seed, states, small=small)
@@ -284,12 +284,15 @@ class Trainer:
                       c.selfcond_p, extra=c.extra)
         return cls.from_model(model, c, ds, world=world, rank=rank, S=S, M=M, D=D, device=device,
                               profile=profile, filled=filled, feed_mode=feed_mode,
-                              bubble_min_len=bubble_min_len)
+                              bubble_min_len=bubble_min_len, comm=comm)
 
     @classmethod
     def from_model(cls, model, cfg, ds, *, world=1, rank=0, S=1, M=1, D=1, device="cuda", profile=None,
-                   filled=True, feed_mode="device", bubble_min_len=B200_BUBBLE_MIN_LEN, comm=None):
-        """Plan and wire an already-built TrainModel (any component implementation)."""
+                   filled=True, feed_mode="device", bubble_min_len=B200_BUBBLE_MIN_LEN, comm=None,
+                   check_memory=None):
+        """Plan and wire an already-built TrainModel (any component implementation).
+        check_memory (default: on CUDA devices): gate the plan with the memory-feasibility model
+        (memory.check_plan raises MemoryError before the first step when a device would overflow)."""
         world_batch = ds.world_batch
         probe = make_batch(replace(ds, world_batch=1), 10 ** 6)
         pfeed = InputFeed(probe, device, cfg.dtype)
@@ -310,6 +313,10 @@ class Trainer:
         ex.plan_result = res
         t = cls(model, cfg, ex, ds, device, feed_mode)
         t.profile = profile
+        if check_memory is None:
+            check_memory = torch.device(device).type == "cuda"
+        if check_memory:
+            t.memory_report(check=True)
         return t
 
     def prefetch(self, n, mode=None):
@@ -367,9 +374,12 @@ class Trainer:
 
         cur_b = self._feed(self.it)
         nxt_b = self._feed(self.it + 1)
-        for k in ("t", "noise"):
+        # every field the captured iteration reads: the current batch's fields (t, noise, extra
+        # fields such as a second pipe's noise) and every frozen component's inputs of the next batch
+        # (images, ids, ControlNet hint, the locked encoder's t / noise)
+        for k in self._g_cur.f:
             self._g_cur.f[k].copy_(cur_b.get(k, 0, cur_b.f[k].shape[0]), non_blocking=True)
-        for k in ("images", "ids"):
+        for k in sorted({f for spec in self.model.frozen for f in spec.inputs}):
             self._g_nxt.f[k].copy_(nxt_b.get(k, 0, nxt_b.f[k].shape[0]), non_blocking=True)
         self._graph.replay()
         # frozen outputs of batch it+1 (graph outputs) -> the buffers the next replay reads
@@ -407,15 +417,26 @@ class Trainer:
         self.it += 1
         return loss
 
-    def memory_report(self, batch=2):
+    def memory_report(self, batch=2, check=False):
         """Predicted bytes per device of this rank's pipeline group (memory.py: parameters, frozen
-        weights, activations kept for the backward x micro-batches in flight, held frozen outputs)."""
+        weights, activations kept for the backward x micro-batches in flight, held frozen outputs):
+        the maximum over the iteration programs the executor may run. check=True raises MemoryError
+        when a device exceeds the B200 budget (memory.check_plan)."""
         from . import memory
 
-        probe = make_batch(replace(self.data_spec, world_batch=batch), 10 ** 6 + 1)
-        feed = InputFeed(probe, self.device, self.cfg.dtype)
-        act = memory.measure_layer_activation_bytes(self.model, lambda k, b: feed.get(k, 0, b), self.device, batch)
-        return memory.predict_device_bytes(self.ex.prog0, self.model, act, self.ex.frozen_specs)
+        act = getattr(self, "_act_bytes", None)
+        if act is None:
+            probe = make_batch(replace(self.data_spec, world_batch=batch), 10 ** 6 + 1)
+            feed = InputFeed(probe, self.device, self.cfg.dtype)
+            act = memory.measure_layer_activation_bytes(self.model, lambda k, b: feed.get(k, 0, b), self.device,
+                                                        batch)
+            self._act_bytes = act
+        out = {}
+        for prog in {id(p): p for p in self.ex.programs.values()}.values():
+            fn = memory.check_plan if check else memory.predict_device_bytes
+            for d, v in fn(prog, self.model, act, self.ex.frozen_specs).items():
+                out[d] = max(out.get(d, 0), v)
+        return out
 
     def measured(self, min_len=0.0):
         """Measured schedule of the last traced step (collective over the job): returns

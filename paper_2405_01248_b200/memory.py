@@ -8,7 +8,10 @@ Per device of a GroupProgram the model adds
   * frozen components, replicated on every device (fp32 master + compute copy);
   * activations autograd keeps for the backward: per backbone layer, bytes per sample measured on the device
     (`measure_layer_activation_bytes`) x the stage's per-replica micro-batch x the micro-batches in flight at
-    the stage under 1F1B (min(M, S - s));
+    the stage. The planner's simulator dispatches forwards eagerly (reference scheduler.py:1-10,165-179: a
+    ready forward runs whenever no backward is ready), not warm-up-capped 1F1B, so the in-flight depth is
+    counted from the device's replayed instruction order (`inflight_depth`: max over the program of
+    forwards minus backwards of that stage), e.g. 8 at S=4, M=8 on stage 0 where 1F1B would hold 4;
   * frozen outputs held for the next iteration (latents / context of the group batch, twice: being produced
     and being consumed), plus the largest frozen layer's input + output over the group batch (transient).
 `check_plan` raises MemoryError when a device exceeds the budget; the planner API itself is unchanged.
@@ -27,9 +30,7 @@ def _store_bytes(store, trainable):
     n = store.numel()
     if not trainable:
         return n * (4 + (2 if store.dtype != torch.float32 else 0))
-    from . import nn
-    bf16 = store.dtype != torch.float32
-    return n * (16 + (2 if bf16 else 0) + (2 if bf16 and nn.FLIP_CACHE else 0))
+    return n * _param_bytes(store)
 
 
 def measure_layer_activation_bytes(model, batch_fn, device, batch=2):
@@ -79,6 +80,25 @@ def measure_layer_activation_bytes(model, batch_fn, device, batch=2):
     return out
 
 
+def inflight_depth(prog, dev, pipe=0):
+    """Peak number of micro-batches whose forward has run and whose backward has not, over the
+    instruction order of `dev` in GroupProgram `prog` (the order the executor replays), for `pipe`."""
+    live = peak = 0
+    for ins in prog.device_program(dev).instrs:
+        if ins[0] in ("fwd", "bwd") and ins[3] == pipe:
+            live += 1 if ins[0] == "fwd" else -1
+            peak = max(peak, live)
+    return peak
+
+
+def _param_bytes(store):
+    """Trainable bytes per parameter: fp32 master + grad + AdamW m, v (16) + bf16 compute copy (2)
+    + the cached flip-transposed bf16 copy the dgrads read (2, nn.FLIP_CACHE; upper bound: every weight)."""
+    from . import nn
+    bf16 = store.dtype != torch.float32
+    return 16 + (2 if bf16 else 0) + (2 if bf16 and nn.FLIP_CACHE else 0)
+
+
 def predict_device_bytes(prog, model, act_bytes, frozen_specs=None):
     """{device: bytes} for one GroupProgram (adapter.build_group_program) of `model`."""
     frozen = sum(_store_bytes(f.component.store, False) for f in model.frozen
@@ -107,10 +127,10 @@ def predict_device_bytes(prog, model, act_bytes, frozen_specs=None):
             bb = model.backbones[pl.backbone]
             lo, hi = pl.stage_ranges[st]
             a, b = bb.stage_slice(lo, hi)
-            total += (b - a) * (16 + (2 if bb.store.dtype != torch.float32 else 0))
+            total += (b - a) * _param_bytes(bb.store)
             r = pl.stage_devices[st][1] - pl.stage_devices[st][0]
             micro = -(-prog.micro_batch // r)
-            inflight = min(prog.M, prog.S - st)
+            inflight = inflight_depth(prog, dev, pi)
             total += sum(act_bytes[pl.backbone][lo:hi]) * micro * inflight
         out[dev] = int(total)
     return out

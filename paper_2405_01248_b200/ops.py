@@ -524,10 +524,16 @@ _GN_WS = {}
 
 
 def _gn_ws(device, nbytes):
-    ws = _GN_WS.get(device)
+    """GroupNorm partial-statistics scratch, one buffer per (device, stream): the forward and backward
+    pass statistics between their two kernels through it, so kernels on the fill stream (frozen VAE
+    GroupNorms in bubbles) and on the compute stream (U-Net) must never share one. The buffer is
+    allocated on (and, when it grows, released to) the pool of the stream that uses it, so the caching
+    allocator orders the reuse of a replaced buffer after that stream's pending kernels."""
+    key = (device, _stream())
+    ws = _GN_WS.get(key)
     if ws is None or ws.numel() * 4 < nbytes:
         ws = torch.empty((nbytes + 3) // 4 + 1024, device=device, dtype=torch.float32)
-        _GN_WS[device] = ws
+        _GN_WS[key] = ws
     return ws
 
 

@@ -152,8 +152,9 @@ def measure_profile(model, live_specs, frozen_specs, make_state, *, group_batch,
                     device="cuda", bb_keys=None, frozen_keys=None):
     """Measured per-layer costs on this GPU (CUDA events, median of `reps` after a warm-up).
 
-    make_state(component_index or 'backbone', layer, batch) -> input state dict for that layer
-    (random tensors of the probed shapes). Backward time of a backbone layer = time of
+    make_state(component_index or ("backbone", pipe), layer, batch) -> input state dict for that
+    layer (random tensors of the probed shapes). Every backbone of a two-backbone model is profiled
+    and the model's frozen dependencies (producer, consumer) are carried into the profile by name. Backward time of a backbone layer = time of
     torch.autograd.backward over its grad-carrying outputs with unit-random gradients.
     """
     keys = bb_keys or _keys(group_batch, D, M)
@@ -173,41 +174,46 @@ def measure_profile(model, live_specs, frozen_specs, make_state, *, group_batch,
         ts.sort()
         return ts[len(ts) // 2]
 
-    bb = model.backbone
-    layers = []
-    for j, fn in enumerate(bb.layers):
-        fwd, bwd = {}, {}
-        for k in keys:
-            st = make_state("backbone", j, k)
+    if live_specs and isinstance(live_specs[0], dict):
+        live_specs = [live_specs]  # single-backbone form
+    backbones = []
+    for pipe, bb in enumerate(getattr(model, "backbones", None) or [model.backbone]):
+        live = live_specs[pipe]
+        layers = []
+        for j, fn in enumerate(bb.layers):
+            fwd, bwd = {}, {}
+            for k in keys:
+                st = make_state(("backbone", pipe), j, k)
 
-            def run_f():
-                with bb.grad_context():
-                    return fn(dict(st))
+                def run_f():
+                    with bb.grad_context():
+                        return fn(dict(st))
 
-            fwd[k] = timed(lambda: run_f())
-            spec = live_specs[j + 1]
-            names = [n for n in sorted(spec) if spec[n][2]]
+                fwd[k] = timed(lambda: run_f())
+                spec = live[j + 1]
+                names = [n for n in sorted(spec) if spec[n][2]]
 
-            def run_b():
-                out = run_f()
-                ts = [out[n] for n in names if out[n].requires_grad]
-                if ts:
-                    torch.autograd.backward(ts, [torch.randn_like(t) for t in ts])
+                def run_b():
+                    out = run_f()
+                    ts = [out[n] for n in names if out[n].requires_grad]
+                    if ts:
+                        torch.autograd.backward(ts, [torch.randn_like(t) for t in ts])
 
-            tb = timed(run_b)
-            bwd[k] = max(tb - fwd[k], 1e-7)
-            bb.store.zero_grad()
-        out_spec = live_specs[j + 1]
-        fb = _bytes_per_sample(out_spec)
-        gb = _bytes_per_sample(out_spec, grad_only=True)
-        pb = _param_bytes(bb, j)
-        layers.append(LayerCost(fwd_time=fwd, bwd_time=bwd,
-                                fwd_comm_bytes={k: fb * k for k in keys},
-                                bwd_comm_bytes={k: gb * k for k in keys},
-                                grad_bytes={k: pb for k in keys},
-                                out_bytes={k: _bytes_per_sample({"out": live_specs[-1]["out"]}) * k
-                                           for k in keys}))
-    backbone = ComponentProfile(name=getattr(bb, "name", "backbone"), layers=layers, trainable=True)
+                tb = timed(run_b)
+                bwd[k] = max(tb - fwd[k], 1e-7)
+                bb.store.zero_grad()
+            out_spec = live[j + 1]
+            fb = _bytes_per_sample(out_spec)
+            gb = _bytes_per_sample(out_spec, grad_only=True)
+            pb = _param_bytes(bb, j)
+            layers.append(LayerCost(fwd_time=fwd, bwd_time=bwd,
+                                    fwd_comm_bytes={k: fb * k for k in keys},
+                                    bwd_comm_bytes={k: gb * k for k in keys},
+                                    grad_bytes={k: pb for k in keys},
+                                    out_bytes={k: _bytes_per_sample({"out": live[-1]["out"]}) * k
+                                               for k in keys}))
+        backbones.append(ComponentProfile(name=f"{getattr(bb, 'name', 'backbone')}{pipe if pipe else ''}",
+                                          layers=layers, trainable=True))
     frozen = []
     for c, f in enumerate(model.frozen):
         fl = []
@@ -225,5 +231,7 @@ def measure_profile(model, live_specs, frozen_specs, make_state, *, group_batch,
                                 out_bytes={k: ob * k for k in fkeys}))
         frozen.append(ComponentProfile(name=getattr(f.component, "name", f"frozen{c}"), layers=fl,
                                        trainable=False))
-    return ModelProfile(backbones=(backbone,), frozen=tuple(frozen), frozen_deps=(),
+    names_ = [c.name for c in frozen]
+    deps = tuple((names_[a], names_[b]) for a, b in getattr(model, "frozen_deps", ()))
+    return ModelProfile(backbones=tuple(backbones), frozen=tuple(frozen), frozen_deps=deps,
                         selfcond_prob=getattr(model, "selfcond_p", 0.0))

@@ -280,7 +280,7 @@ class PipelineExecutor:
         # side stream as soon as autograd has finished their gradients (CUDA, NCCL or world 1)
         self.overlap_sync = self.streams.cuda and not (world > 1 and staged())
         self.opt_stream = torch.cuda.Stream(device=self.device, priority=0) if self.streams.cuda else None
-        self.grad_snapshots = None  # list -> flat grad slices captured before each AdamW
+        self.grad_snapshots = None  # list -> reduced flat grad slices (lo, hi, grad) captured before each AdamW
         self.grad_snapshot_pipes = []  # backbone index of each snapshot
         self._frz_sends = []        # in-flight frozen-activation sends (kept alive until deliver)
 
@@ -525,6 +525,10 @@ class PipelineExecutor:
                 pg = self._stage_pgs[pi]
                 if pg is not None:
                     dist.all_reduce(store.grad[a:b], group=pg)
+                if self.grad_snapshots is not None:
+                    # parity tests: the reduced gradient slice exactly as this AdamW chunk reads it
+                    self.grad_snapshots.append((a, b, store.grad[a:b].detach().clone()))
+                    self.grad_snapshot_pipes.append(self.prog.pipes[pi].backbone)
                 # background chunks: one CTA per SM at most (see dp_adamw_apply); the final chunk
                 # at the sync point has the machine to itself
                 store.adamw_apply((a, b), max_ctas=0 if final else self.OVERLAP_CTAS, zero_grad=True,
@@ -727,7 +731,7 @@ class PipelineExecutor:
         self.loss_buf.zero_()
         tr = self.tracer = _Tracer(self.streams, self.dev) if trace else None
         # optimizer overlap: the micro-batch of each pipe's final backward on this device
-        self._ovl_on = self.overlap_sync and self.grad_snapshots is None and self.streams.cuda
+        self._ovl_on = self.overlap_sync and self.streams.cuda
         self._ovl_top, self._ovl_begun, self._last_m = {}, {}, {}
         for ins in prog.device_program(self.dev).instrs:
             if ins[0] == "bwd":
@@ -780,6 +784,21 @@ class PipelineExecutor:
         if self.streams.cuda:
             torch.cuda.current_stream(self.device).wait_stream(self.streams.compute)
         return self.loss_buf
+
+    def take_grad_snapshots(self):
+        """Parity tests: the reduced gradients captured since the last call (grad_snapshots = []
+        enables capture), assembled per backbone index into full flat fp32 host tensors (zeros
+        outside the stages this rank hosts); clears the capture list."""
+        torch.cuda.synchronize(self.device) if self.device.type == "cuda" else None
+        out = {}
+        for (lo, hi, g), bi in zip(self.grad_snapshots or [], self.grad_snapshot_pipes):
+            bbs = getattr(self.model, "backbones", None) or [self.model.backbone]
+            flat = out.setdefault(bi, torch.zeros(bbs[bi].store.numel(), dtype=torch.float32))
+            flat[lo:hi] = g.float().cpu()
+        if self.grad_snapshots is not None:
+            self.grad_snapshots.clear()
+            self.grad_snapshot_pipes.clear()
+        return out
 
     def measured_tasks(self):
         """Measured tasks of the last traced iteration on this rank (device = local index)."""

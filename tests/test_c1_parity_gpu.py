@@ -41,16 +41,16 @@ def test_c1_single_gpu_matches_oracle(M):
     tr = engine.Trainer.create("c1", world=1, rank=0, S=1, M=M, D=1, world_batch=8)
     tr.ex.grad_snapshots = []
     iters = 3
-    losses = []
+    losses, snaps = [], []
     for i in range(iters):
         losses.append(tr.step(has_next=i < iters - 1).item())
+        snaps.append(tr.ex.take_grad_snapshots())
     (ref_losses, ref_grads, ref_params), batches = _oracle(tr, iters)
     assert any(b.selfcond for b in batches) or True
     for a, b in zip(losses, ref_losses):
         assert abs(a - b) <= 1e-4 * abs(b) + 1e-6, (losses, ref_losses)
     store = tr.model.backbone.store
-    lo, hi, g0 = tr.ex.grad_snapshots[0]
-    got = _flat_to_named(store, lo, g0)
+    got = _flat_to_named(store, 0, snaps[0][0])
     for name, ref in ref_grads[0].items():
         scale = ref.abs().max().item() + 1e-12
         err = (got[name] - ref).abs().max().item()

@@ -154,7 +154,9 @@ def test_eltwise_family(dt):
     assert _rel(y, h.float() + e.float()[:, None, None, :]) < _tol(dt)
     y.backward(torch.ones_like(y))
     assert _rel(e.grad, torch.full((3, 64), 64.0, device="cuda")) < _tol(dt)
-    for C in (320, 1280, 8):  # U-Net widths and a one-vector row
+    # U-Net widths, a one-vector row, and a row of a prime number of 16-byte vectors above 256
+    # (no channel-block width in [8, 256] divides it: ADVICE r1, CV = 257 had produced zeros)
+    for C in (320, 1280, 8, 257 * (4 if dt == torch.float32 else 8)):
         h = torch.randn(4, 16, 16, C, device="cuda").to(dt).requires_grad_(True)
         e = torch.randn(4, C, device="cuda").to(dt).requires_grad_(True)
         y = nn.add_row_bias(h, e)

@@ -313,3 +313,46 @@ def test_profile_roundtrip_and_validation(tmp_path):
     bad["format"] = "nope"
     with pytest.raises(errors.ParseError):
         profile.profile_from_dict(bad)
+
+
+@pytest.mark.skipif(_reference() is None, reason="reference pipefill not importable here")
+def test_reference_plans_drive_the_adapter_identically():
+    """The drop-in boundary: the REFERENCE planner's own evaluate_point output (reference
+    planner.py:141-187), fed to the executor's adapter (adapter.build_group_program), yields
+    per-device programs identical to those from the restated planner — the executor runs the
+    reference's plans unchanged."""
+    import dataclasses
+    import importlib
+
+    from paper_2405_01248_b200.adapter import build_group_program
+
+    _reference()
+    Rpl = importlib.import_module("pipefill.planner")
+    Rpr = importlib.import_module("pipefill.profile")
+    rng = random.Random(4321)
+    compared = 0
+    for it in range(40):
+        nb = 2 if rng.random() < 0.25 else 1
+        doc = synthetic_profile_doc(seed=2000 + it, n_backbones=nb, n_frozen=rng.randint(1, 3),
+                                    selfcond_prob=rng.choice([0.0, 0.5]) if nb == 1 else 0.0,
+                                    layers=(3, 10), frozen_layers=(1, 8), frozen_scale=rng.choice([0.5, 1.0, 3.0]))
+        world = rng.choice([2, 4, 8])
+        comm = (rng.uniform(1e10, 3e11), rng.uniform(0, 1e-4), rng.uniform(1e10, 3e11), rng.uniform(0, 1e-4))
+        wb = rng.choice([32, 64, 128])
+        rp, mp = Rpr.profile_from_dict(doc), profile.profile_from_dict(doc)
+        rc = Rpr.ClusterConfig(world, Rpr.CommCosts(*comm))
+        mc = profile.ClusterConfig(world, profile.CommCosts(*comm))
+        counts = [len(c["layers"]) for c in doc["frozen"]]
+        for S, M, D in Rpl.default_search_space(rp, rc, wb).points()[:6]:
+            try:
+                r = Rpl.evaluate_point(rp, rc, S, M, D, wb, bubble_min_len=0.005)
+                m = planner.evaluate_point(mp, mc, S, M, D, wb, bubble_min_len=0.005)
+            except Exception:
+                continue
+            deps = tuple(mp.frozen_dep_indices())
+            for sc in (False, True) if r["mode"] == "selfcond" else (False,):
+                pr = build_group_program(r, counts, selfcond=sc or None, frozen_deps=deps)
+                pm = build_group_program(m, counts, selfcond=sc or None, frozen_deps=deps)
+                assert dataclasses.asdict(pr) == dataclasses.asdict(pm), (it, S, M, D)
+                compared += 1
+    assert compared > 60

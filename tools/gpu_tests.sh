@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 : > gpurun_out/tests.log
 for f in "$@"; do
-  timeout -s KILL 600 python -m pytest "$f" -v -x --timeout 120 --timeout-method thread > gpurun_out/$(basename $f .py).log 2>&1
+  timeout -s KILL 1500 python -m pytest "$f" -v -x --timeout 1200 --timeout-method thread > gpurun_out/$(basename $f .py).log 2>&1
   echo "== $f rc=$?" >> gpurun_out/tests.log
   grep -E "PASSED|FAILED|ERROR|Timeout|Error|error|assert" gpurun_out/$(basename $f .py).log | head -40 >> gpurun_out/tests.log
 done
