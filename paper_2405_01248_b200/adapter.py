@@ -123,6 +123,98 @@ class GroupProgram:
                 return s, dev - a
         raise ValueError(dev)
 
+    # ---- standalone program documents (Fig. 6 step 6: "instruction generation").
+    # The reference's plan document carries task counts only (planner.py:312-317); these carry the
+    # per-device instruction order, the frozen pieces with their sample ranges and every transfer,
+    # so a launcher can ship one file per rank and the executor runs it without re-planning.
+
+    def to_dict(self):
+        return {"format": PROGRAM_FORMAT, "D": self.D, "S": self.S, "M": self.M,
+                "group_batch": self.group_batch, "micro_batch": self.micro_batch,
+                "stage_ranges": [list(r) for r in self.stage_ranges],
+                "stage_devices": [list(r) for r in self.stage_devices],
+                "devices": [{"device": d.device, "stage": d.stage, "replica": d.replica,
+                             "stages": list(d.stages), "instrs": [list(i) for i in d.instrs]}
+                            for d in self.devices],
+                "fills": [[_piece_row(p) for p in ps] for ps in self.fills],
+                "tail": [_piece_row(p) for p in self.tail],
+                "transfers": [_transfer_row(t) for t in self.transfers],
+                "deliveries": [_transfer_row(t) for t in self.deliveries],
+                "frozen_layers": list(self.frozen_layers), "selfcond": bool(self.selfcond),
+                "frozen_deps": [list(d) for d in self.frozen_deps],
+                "pipes": [{"direction": pl.direction, "backbone": pl.backbone,
+                           "stage_ranges": [list(r) for r in pl.stage_ranges],
+                           "stage_devices": [list(r) for r in pl.stage_devices]} for pl in self.pipes]}
+
+    @classmethod
+    def from_dict(cls, d):
+        if d.get("format") != PROGRAM_FORMAT:
+            raise ValueError(f"not a {PROGRAM_FORMAT} document: format={d.get('format')!r}")
+        devices = [DeviceProgram(x["device"], x["stage"], x["replica"], [tuple(i) for i in x["instrs"]],
+                                 tuple(x["stages"])) for x in d["devices"]]
+        return cls(D=d["D"], S=d["S"], M=d["M"], group_batch=d["group_batch"], micro_batch=d["micro_batch"],
+                   stage_ranges=[tuple(r) for r in d["stage_ranges"]],
+                   stage_devices=[tuple(r) for r in d["stage_devices"]], devices=devices,
+                   fills=[[Piece(*r) for r in ps] for ps in d["fills"]], tail=[Piece(*r) for r in d["tail"]],
+                   transfers=[Transfer(*r) for r in d["transfers"]],
+                   deliveries=[Transfer(*r) for r in d["deliveries"]],
+                   frozen_layers=list(d["frozen_layers"]), selfcond=d["selfcond"],
+                   frozen_deps=tuple(tuple(x) for x in d["frozen_deps"]),
+                   pipes=tuple(PipeLayout(p["direction"], p["backbone"], tuple(tuple(r) for r in p["stage_ranges"]),
+                                          tuple(tuple(r) for r in p["stage_devices"])) for p in d["pipes"]))
+
+    def rank_document(self, dev, group=0, rank=None):
+        """The program of group-local device `dev` as a standalone document: the group-level
+        layout (stage ranges / devices, pieces, transfers — every rank of the group needs them to
+        address its peers) plus `device` = the instruction list this rank executes."""
+        doc = self.to_dict()
+        doc["rank"] = {"device": dev, "group": group, "rank": group * self.D + dev if rank is None else rank}
+        return doc
+
+
+PROGRAM_FORMAT = "dpipe-program/v1"
+
+
+def _piece_row(p):
+    return [p.comp, p.layer, p.lo, p.hi, p.device, p.phase]
+
+
+def _transfer_row(t):
+    return [t.src, t.dst, t.comp, t.layer, t.lo, t.hi, t.seq]
+
+
+def save_rank_programs(prog, directory, groups=1, programs=None):
+    """Write one `rank<r>.json` per rank of a `groups`-group job (PROGRAM_FORMAT). `programs` maps
+    an iteration kind ("plain" / "selfcond") to a GroupProgram when self-conditioning makes the
+    executor pick one of two programs per iteration; each rank file then holds both."""
+    import json
+    import os
+
+    os.makedirs(directory, exist_ok=True)
+    progs = programs or {"plain": prog}
+    paths = []
+    for g in range(groups):
+        for dev in range(prog.D):
+            r = g * prog.D + dev
+            doc = {"format": PROGRAM_FORMAT + "+rank", "rank": r, "group": g, "device": dev,
+                   "programs": {k: p.rank_document(dev, g, r) for k, p in progs.items()}}
+            path = os.path.join(directory, f"rank{r}.json")
+            with open(path, "w") as f:
+                json.dump(doc, f, sort_keys=True, separators=(",", ":"))
+            paths.append(path)
+    return paths
+
+
+def load_rank_program(path):
+    """-> (rank, {kind: GroupProgram}) from a file written by save_rank_programs."""
+    import json
+
+    with open(path) as f:
+        doc = json.load(f)
+    if doc.get("format") != PROGRAM_FORMAT + "+rank":
+        raise ValueError(f"{path}: not a {PROGRAM_FORMAT} rank document")
+    return doc["rank"], {k: GroupProgram.from_dict(v) for k, v in doc["programs"].items()}
+
 
 def _pipes(plan):
     groups = group_device_ranges(plan)

@@ -670,6 +670,15 @@ __global__ void __launch_bounds__(256, 1)
 // ====================================================================== host side
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  // The encoder is a driver call that validates the global address against the CURRENT context.
+  // A thread whose first CUDA work is one of our launches (autograd's device worker thread: torch
+  // skips cudaSetDevice when the device index already matches) has no context bound yet and the
+  // encoder would fail with CUDA_ERROR_INVALID_CONTEXT; cudaFree(0) binds the primary context.
+  thread_local bool bound = false;
+  if (!bound) {
+    cudaFree(nullptr);
+    bound = true;
+  }
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {

@@ -275,7 +275,7 @@ class Trainer:
     @classmethod
     def create(cls, cfg="c1", *, world=1, rank=0, S=1, M=1, D=1, world_batch=None, device=None,
                seed=0, states=None, profile=None, filled=True, feed_mode="device", small=False,
-               bubble_min_len=B200_BUBBLE_MIN_LEN, comm=None):
+               bubble_min_len=B200_BUBBLE_MIN_LEN, comm=None, program_file=None):
         c = CONFIGS[cfg] if isinstance(cfg, str) else cfg
         device = device or (f"cuda:{torch.cuda.current_device()}" if torch.cuda.is_available() else "cpu")
         model = build_model(c, device, seed, states, small=small)
@@ -284,12 +284,12 @@ class Trainer:
                       c.selfcond_p, extra=c.extra)
         return cls.from_model(model, c, ds, world=world, rank=rank, S=S, M=M, D=D, device=device,
                               profile=profile, filled=filled, feed_mode=feed_mode,
-                              bubble_min_len=bubble_min_len, comm=comm)
+                              bubble_min_len=bubble_min_len, comm=comm, program_file=program_file)
 
     @classmethod
     def from_model(cls, model, cfg, ds, *, world=1, rank=0, S=1, M=1, D=1, device="cuda", profile=None,
                    filled=True, feed_mode="device", bubble_min_len=B200_BUBBLE_MIN_LEN, comm=None,
-                   check_memory=None):
+                   check_memory=None, program_file=None):
         """Plan and wire an already-built TrainModel (any component implementation).
         check_memory (default: on CUDA devices): gate the plan with the memory-feasibility model
         (memory.check_plan raises MemoryError before the first step when a device would overflow)."""
@@ -300,10 +300,20 @@ class Trainer:
         counts = [len(f.component.layers) for f in model.frozen]
         if profile is None:
             profile = synthetic_profile(model, live, fspecs, group_batch=world_batch * D // world, D=D, M=M)
-        res, programs, warm, unfilled = plan_programs(profile, world, S, M, D, world_batch, counts,
-                                                      bubble_min_len, comm)
-        if not filled:
-            programs = {False: unfilled, True: unfilled}
+        if program_file is not None:
+            # a shipped per-rank program (adapter.save_rank_programs): no planning on this rank
+            from .adapter import load_rank_program
+
+            prank, docs = load_rank_program(program_file)
+            if prank != rank:
+                raise ValueError(f"{program_file} holds the program of rank {prank}, not {rank}")
+            res, warm = None, docs["warmup"]
+            programs = {False: docs["plain"], True: docs["selfcond"]}
+        else:
+            res, programs, warm, unfilled = plan_programs(profile, world, S, M, D, world_batch, counts,
+                                                          bubble_min_len, comm)
+            if not filled:
+                programs = {False: unfilled, True: unfilled}
         # per pipe: mean squared error over that pipe's noise tensor (two-backbone models sum them)
         scales = [1.0 / (world_batch * pfeed.get(model.noise_field(p), 0, 1).numel())
                   for p in range(len(model.backbones))]
@@ -318,6 +328,16 @@ class Trainer:
         if check_memory:
             t.memory_report(check=True)
         return t
+
+    def save_programs(self, directory):
+        """Ship this job's plan as one program file per rank (adapter.PROGRAM_FORMAT: per-device
+        instruction order, frozen pieces with sample ranges, transfers; the plain, self-conditioned
+        and warm-up programs); Trainer.create(..., program_file=<dir>/rank<r>.json) runs it."""
+        from .adapter import save_rank_programs
+
+        ex = self.ex
+        progs = {"plain": ex.programs[False], "selfcond": ex.programs[True], "warmup": ex.warm_program}
+        return save_rank_programs(ex.prog0, directory, groups=ex.world // ex.D, programs=progs)
 
     def prefetch(self, n, mode=None):
         """Pre-build the feeds of iterations [it, it + n] (device-resident or pinned host)

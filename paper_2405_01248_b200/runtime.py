@@ -793,7 +793,7 @@ class PipelineExecutor:
         out = {}
         for (lo, hi, g), bi in zip(self.grad_snapshots or [], self.grad_snapshot_pipes):
             bbs = getattr(self.model, "backbones", None) or [self.model.backbone]
-            flat = out.setdefault(bi, torch.zeros(bbs[bi].store.numel(), dtype=torch.float32))
+            flat = out.setdefault(bi, torch.zeros(bbs[bi].store.grad.numel(), dtype=torch.float32))
             flat[lo:hi] = g.float().cpu()
         if self.grad_snapshots is not None:
             self.grad_snapshots.clear()

@@ -92,3 +92,29 @@ def test_programs_replay_schedule_and_fill(seed, S, M, D, p, nb):
 def test_split_range():
     assert split_range(0, 10, 3) == [(0, 3), (3, 6), (6, 10)]
     assert split_range(5, 7, 4) == [(5, 5), (5, 6), (6, 6), (6, 7)]
+
+
+@pytest.mark.parametrize("seed,S,M,D,p,nb", [(0, 2, 4, 2, 0.0, 1), (4, 4, 4, 4, 0.5, 1), (7, 4, 4, 4, 0.0, 2)])
+def test_program_documents_round_trip(tmp_path, seed, S, M, D, p, nb):
+    """The standalone per-rank program format: to_dict/from_dict and the rank
+    files reproduce the in-memory programs exactly, and reject foreign documents."""
+    import dataclasses
+    import json
+
+    from paper_2405_01248_b200.adapter import GroupProgram, load_rank_program, save_rank_programs
+
+    prof = _profile(seed, p=p, backbones=nb)
+    cluster = profile.ClusterConfig(2 * D, profile.CommCosts(2e11, 1e-5, 3e11, 1e-5))
+    res = planner.evaluate_point(prof, cluster, S, M, D, 64 * M // 4)
+    counts = [len(c.layers) for c in prof.frozen]
+    prog = build_group_program(res, counts, selfcond=bool(p) or None)
+    doc = json.loads(json.dumps(prog.to_dict()))
+    assert dataclasses.asdict(GroupProgram.from_dict(doc)) == dataclasses.asdict(prog)
+    paths = save_rank_programs(prog, str(tmp_path), groups=2, programs={"plain": prog, "selfcond": prog})
+    assert len(paths) == 2 * D
+    for r, path in enumerate(paths):
+        rank, progs = load_rank_program(path)
+        assert rank == r and set(progs) == {"plain", "selfcond"}
+        assert dataclasses.asdict(progs["plain"]) == dataclasses.asdict(prog)
+    with pytest.raises(ValueError):
+        GroupProgram.from_dict({"format": "pipeline-plan/v1"})

@@ -29,7 +29,7 @@ def _free_port():
     return p
 
 
-def _make(world, rank, S, M, D, selfcond, wb, deps=False, two=False):
+def _make(world, rank, S, M, D, selfcond, wb, deps=False, two=False, program_file=None):
     import cpu_pipeline_model as cm
     from paper_2405_01248_b200 import engine
     from paper_2405_01248_b200.diffusion import DataSpec
@@ -37,10 +37,11 @@ def _make(world, rank, S, M, D, selfcond, wb, deps=False, two=False):
     model = cm.build(selfcond, deps=deps, two=two)
     ds = DataSpec(7, wb, cm.IMG, cm.LAT, cm.ZC, cm.TL, cm.VOCAB, 1000, 0.5 if selfcond else 0.0)
     cfg = engine.ConfigSpec("toy", torch.float32, cm.IMG, cm.LAT, cm.TL, cm.VOCAB, ds.selfcond_p, 7)
-    return engine.Trainer.from_model(model, cfg, ds, world=world, rank=rank, S=S, M=M, D=D, device="cpu")
+    return engine.Trainer.from_model(model, cfg, ds, world=world, rank=rank, S=S, M=M, D=D, device="cpu",
+                                     program_file=program_file)
 
 
-def _worker(rank, world, S, M, D, selfcond, wb, port, outdir, deps=False, two=False):
+def _worker(rank, world, S, M, D, selfcond, wb, port, outdir, deps=False, two=False, from_file=False):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -48,6 +49,21 @@ def _worker(rank, world, S, M, D, selfcond, wb, port, outdir, deps=False, two=Fa
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.set_num_threads(1)
     tr = _make(world, rank, S, M, D, selfcond, wb, deps, two)
+    if from_file:
+        # ship the plan as per-rank program files (rank 0 writes them), then run from the files
+        import dataclasses
+
+        pdir = os.path.join(outdir, "programs")
+        if rank == 0:
+            tr.save_programs(pdir)
+        dist.barrier()
+        planned = tr
+        tr = _make(world, rank, S, M, D, selfcond, wb, deps, two,
+                   program_file=os.path.join(pdir, f"rank{rank}.json"))
+        for k in (False, True):
+            assert dataclasses.asdict(tr.ex.programs[k]) == dataclasses.asdict(planned.ex.programs[k])
+        assert dataclasses.asdict(tr.ex.warm_program) == dataclasses.asdict(planned.ex.warm_program)
+        del planned
     losses = []
     for i in range(ITERS):
         dist.barrier()
@@ -91,11 +107,11 @@ def _reference(selfcond, wb, deps=False, two=False):
     (2, 2, 4, 2, False, False, True),     # two backbones, bidirectional pipelines
     (2, 2, 4, 2, True, False, True),      # bidirectional + self-conditioning feedback per pipe
 ])
-def test_pipelined_equals_sequential(tmp_path, world, S, M, D, selfcond, deps, two):
+def test_pipelined_equals_sequential(tmp_path, world, S, M, D, selfcond, deps, two, from_file=False):
     import torch.multiprocessing as mp
 
     wb = 16 * (world // D)
-    mp.spawn(_worker, args=(world, S, M, D, selfcond, wb, _free_port(), str(tmp_path), deps, two),
+    mp.spawn(_worker, args=(world, S, M, D, selfcond, wb, _free_port(), str(tmp_path), deps, two, from_file),
              nprocs=world, join=True)
     ref_losses, ref_flats = _reference(selfcond, wb, deps, two)
     outs = [torch.load(os.path.join(tmp_path, f"r{r}.pt"), weights_only=False) for r in range(world)]
@@ -120,3 +136,11 @@ def test_pipelined_equals_sequential(tmp_path, world, S, M, D, selfcond, deps, t
     # the fill plan actually exercised bubbles (and, with several devices, frozen transfers)
     # (bidirectional plans leave bubbles too short to fill at this toy size)
     assert two or any(o["fills"] > 0 for o in outs)
+
+
+def test_pipelined_from_shipped_program_files(tmp_path):
+    """PAPER.md:266 instruction generation as a standalone artefact: the job runs from per-rank
+    program files (adapter.save_rank_programs / load_rank_program, format dpipe-program/v1) that
+    round-trip the planned programs exactly, with the sequential run's losses and parameters
+    (2 pipeline groups x 2 stages, self-conditioning, fills with frozen transfers)."""
+    test_pipelined_equals_sequential(tmp_path, 4, 2, 2, 2, True, False, False, from_file=True)
