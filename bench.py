@@ -23,6 +23,7 @@ tail) and the AdamW step: nothing is skipped inside the timed 
 from __future__ import annotations
 
 import argparse
+import datetime
 import gc
 import json
 import os
@@ -138,10 +139,15 @@ def dist_setup(n, share_gpu=False):
         local = 0
     torch.cuda.set_device(local)
     if world > 1:
+        # a hung peer fails the job after DP_NCCL_TIMEOUT_S instead of blocking forever (the
+        # NCCL watchdog aborts the communicators; every sub-group inherits the timeout)
+        to = datetime.timedelta(seconds=int(os.environ.get("DP_NCCL_TIMEOUT_S", "600")))
         if share_gpu:
-            dist.init_process_group("gloo")
+            dist.init_process_group("gloo", timeout=to)
         else:
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+            # device_id binds the default group to this GPU: its communicator and every
+            # sub-group's (split from it) are created eagerly at setup, not on the first send
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"), timeout=to)
     return rank, world, local
 
 

@@ -3,6 +3,7 @@
 // header-only and compiled into libdpipe.so.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -26,6 +27,16 @@ constexpr int kNumSMs = 148;
     asm volatile("griddepcontrol.launch_dependents;");     \
   } while (0)
 
+// DP_PDL=0 turns programmatic launches off (tools that interleave event-record nodes between
+// kernels in a captured graph, where a programmatic edge must join two kernel nodes)
+static inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DP_PDL");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return on;
+}
+
 template <typename... KArgs, typename... Args>
 static inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                                    cudaStream_t st, Args&&... args) {
@@ -38,7 +49,7 @@ static inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 blo
   a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   a[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = a;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 

@@ -750,14 +750,6 @@ static bool halo_enabled() {
   return on;
 }
 
-static bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("DP_PDL");
-    return e ? atoi(e) != 0 : true;
-  }();
-  return on;
-}
-
 template <int BN, int CG, bool HALO = false, bool RES = false>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
                      TcParams p, int max_ctas, cudaStream_t st) {

@@ -100,6 +100,45 @@ def _cat(parts):
     return torch.cat(parts, 0)
 
 
+_ALIGN = 16
+
+
+def _seg_bytes(shape, dtype, n):
+    """Bytes of n samples of a per-sample `shape` tensor, padded to the packing alignment."""
+    nb = n * int(torch.Size(shape).numel()) * torch.empty((), dtype=dtype).element_size()
+    return -(-nb // _ALIGN) * _ALIGN
+
+
+def pack(tensors):
+    """One flat byte buffer holding `tensors` back to back (16-byte aligned segments): a live set
+    or a frozen activation crosses a link as ONE message instead of one per tensor."""
+    parts = []
+    for t in tensors:
+        b = t.detach().contiguous().reshape(-1).view(torch.uint8)
+        parts.append(b)
+        pad = -b.numel() % _ALIGN
+        if pad:
+            parts.append(torch.zeros(pad, dtype=torch.uint8, device=t.device))
+    return parts[0] if len(parts) == 1 else torch.cat(parts)
+
+
+def unpack(flat, layout, n):
+    """Views into a received flat buffer: layout = [(name, per-sample shape, dtype)] in packing
+    order, n samples each (no copies)."""
+    out, off = {}, 0
+    for name, shape, dt in layout:
+        nb = _seg_bytes(shape, dt, n)
+        numel = n * int(torch.Size(shape).numel())
+        esz = torch.empty((), dtype=dt).element_size()
+        out[name] = flat[off:off + numel * esz].view(dt).view((n,) + tuple(shape))
+        off += nb
+    return out
+
+
+def packed_bytes(layout, n):
+    return sum(_seg_bytes(shape, dt, n) for _, shape, dt in layout)
+
+
 class _Streams:
     def __init__(self, device, single=False):
         self.cuda = device.type == "cuda" and not single
@@ -349,10 +388,6 @@ class PipelineExecutor:
         return out
 
     # ---------------------------------------------------------------- frozen work
-    def _alloc_like(self, spec, n):
-        return {k: torch.empty((n,) + tuple(shape), device=self.device, dtype=dt)
-                for k, (shape, dt) in sorted(spec.items())}
-
     def _run_frozen_piece(self, piece, store, raw):
         comp = self.model.frozen[piece.comp]
         if piece.layer == 0:
@@ -385,9 +420,8 @@ class PipelineExecutor:
         for t in prog.transfers:
             if (t.src == self.dev and t.comp == piece.comp and t.layer == piece.layer
                     and piece.lo <= t.lo and t.hi <= piece.hi and t.dst != self.dev):
-                for k in sorted(out):
-                    self._frz_sends.append(self.links.isend("frz", out[k][t.lo - piece.lo:t.hi - piece.lo],
-                                                            self._grank(t.dst)))
+                flat = pack([out[k][t.lo - piece.lo:t.hi - piece.lo] for k in sorted(out)])
+                self._frz_sends.append(self.links.isend("frz", flat, self._grank(t.dst)))
                 sent.add(t.seq)
 
     def _recv_frozen_upto(self, prog, store, need_seq, posted):
@@ -398,16 +432,19 @@ class PipelineExecutor:
                 break
             if t.dst != self.dev or t.src == self.dev or t.seq in posted:
                 continue
-            spec = self.frozen_specs[t.comp][t.layer]
-            bufs = self._alloc_like(spec, t.hi - t.lo)
-            works = [self.links.irecv("frz", bufs[k], self._grank(t.src)) for k in sorted(bufs)]
-            posted[t.seq] = (t, bufs, works)
-        for seq, (t, bufs, works) in list(posted.items()):
-            if works is not None and seq <= need_seq:
-                for w in works:
-                    w.wait()
+            layout = self._frozen_layout(t.comp, t.layer)
+            flat = torch.empty(packed_bytes(layout, t.hi - t.lo), device=self.device, dtype=torch.uint8)
+            posted[t.seq] = (t, flat, self.links.irecv("frz", flat, self._grank(t.src)))
+        for seq, (t, flat, work) in list(posted.items()):
+            if work is not None and seq <= need_seq:
+                work.wait()
+                bufs = unpack(flat, self._frozen_layout(t.comp, t.layer), t.hi - t.lo)
                 store.setdefault((t.comp, t.layer), []).append((t.lo, t.hi, bufs))
-                posted[seq] = (t, bufs, None)
+                posted[seq] = (t, flat, None)
+
+    def _frozen_layout(self, comp, layer):
+        spec = self.frozen_specs[comp][layer]
+        return [(k, spec[k][0], spec[k][1]) for k in sorted(spec)]
 
     def _run_pieces(self, prog, pieces, store, raw, posted, sent):
         for piece in pieces:
@@ -435,15 +472,16 @@ class PipelineExecutor:
                 if t.dst == self.dev:
                     ready.setdefault(t.comp, []).append((t.lo, t.hi, comp_out))
                 else:
-                    for k in sorted(comp_out):
-                        sends.append(self.links.isend("frz", comp_out[k], self._grank(t.dst)))
+                    flat = pack([comp_out[k] for k in sorted(comp_out)])
+                    sends.append(self.links.isend("frz", flat, self._grank(t.dst)))
             elif t.dst == self.dev:
-                bufs = self._alloc_like(self.frozen_specs[t.comp][t.layer], t.hi - t.lo)
-                for k in sorted(bufs):
-                    recvs.append(self.links.irecv("frz", bufs[k], self._grank(t.src)))
-                ready.setdefault(t.comp, []).append((t.lo, t.hi, bufs))
-        for w in recvs:
+                layout = self._frozen_layout(t.comp, t.layer)
+                flat = torch.empty(packed_bytes(layout, t.hi - t.lo), device=self.device, dtype=torch.uint8)
+                recvs.append((t, flat, self.links.irecv("frz", flat, self._grank(t.src))))
+        for t, flat, w in recvs:
             w.wait()
+            ready.setdefault(t.comp, []).append(
+                (t.lo, t.hi, unpack(flat, self._frozen_layout(t.comp, t.layer), t.hi - t.lo)))
         for w in sends + self._frz_sends:
             w.wait()
         self._frz_sends = []
@@ -625,43 +663,46 @@ class PipelineExecutor:
         spec = self._spec(pi, pl.stage_ranges[s][1])
         dst0 = pl.stage_devices[s + 1][0]
         for j, a, b in self._pieces(pi, s, m, True):
-            for k in sorted(spec):
-                self._pending.append(self.links.isend(f"fwd{pi}", out[k].detach()[a - lo_r:b - lo_r],
-                                                      self._grank(dst0 + j)))
+            flat = pack([out[k][a - lo_r:b - lo_r] for k in sorted(spec)])
+            self._pending.append(self.links.isend(f"fwd{pi}", flat, self._grank(dst0 + j)))
+
+    def _recv_packed(self, kind, layout, n, pieces, src0, lo_r):
+        """Receive one packed message per piece (peer replica, lo, hi) and return the per-name
+        tensors of all n samples: views of the message when one piece covers them, else
+        assembled from the pieces."""
+        msgs = []
+        for i, a, b in pieces:
+            flat = torch.empty(packed_bytes(layout, b - a), device=self.device, dtype=torch.uint8)
+            msgs.append((a, b, flat, self.links.irecv(kind, flat, self._grank(src0 + i))))
+        for *_, w in msgs:
+            w.wait()
+        if len(msgs) == 1 and msgs[0][1] - msgs[0][0] == n:
+            return unpack(msgs[0][2], layout, n)
+        bufs = {k: torch.empty((n,) + tuple(shape), device=self.device, dtype=dt) for k, shape, dt in layout}
+        for a, b, flat, _ in msgs:
+            for k, v in unpack(flat, layout, b - a).items():
+                bufs[k][a - lo_r:b - lo_r].copy_(v)
+        return bufs
 
     def _recv_live(self, pi, s, m, n, lo_r):
         pl = self.prog.pipes[pi]
         spec = self._spec(pi, pl.stage_ranges[s][0])
-        bufs = {k: torch.empty((n,) + tuple(shape), device=self.device, dtype=dt)
-                for k, (shape, dt, g) in sorted(spec.items())}
-        src0 = pl.stage_devices[s - 1][0]
-        works = []
-        for i, a, b in self._pieces(pi, s - 1, m, False):
-            for k in sorted(bufs):
-                works.append(self.links.irecv(f"fwd{pi}", bufs[k][a - lo_r:b - lo_r], self._grank(src0 + i)))
-        for w in works:
-            w.wait()
-        return bufs
+        layout = [(k, spec[k][0], spec[k][1]) for k in sorted(spec)]
+        return self._recv_packed(f"fwd{pi}", layout, n, self._pieces(pi, s - 1, m, False),
+                                 pl.stage_devices[s - 1][0], lo_r)
 
     def _send_grads(self, pi, s, m, grads, lo_r):
         src0 = self.prog.pipes[pi].stage_devices[s - 1][0]
         for i, a, b in self._pieces(pi, s - 1, m, False):
-            for k in sorted(grads):
-                self._pending.append(self.links.isend(f"bwd{pi}", grads[k][a - lo_r:b - lo_r],
-                                                      self._grank(src0 + i)))
+            flat = pack([grads[k][a - lo_r:b - lo_r] for k in sorted(grads)])
+            self._pending.append(self.links.isend(f"bwd{pi}", flat, self._grank(src0 + i)))
 
     def _recv_grads(self, pi, s, m, n, lo_r, names):
         pl = self.prog.pipes[pi]
         spec = self._spec(pi, pl.stage_ranges[s][1])
-        bufs = {k: torch.empty((n,) + tuple(spec[k][0]), device=self.device, dtype=spec[k][1]) for k in names}
-        dst0 = pl.stage_devices[s + 1][0]
-        works = []
-        for j, a, b in self._pieces(pi, s, m, True):
-            for k in names:
-                works.append(self.links.irecv(f"bwd{pi}", bufs[k][a - lo_r:b - lo_r], self._grank(dst0 + j)))
-        for w in works:
-            w.wait()
-        return bufs
+        layout = [(k, spec[k][0], spec[k][1]) for k in sorted(names)]
+        return self._recv_packed(f"bwd{pi}", layout, n, self._pieces(pi, s, m, True),
+                                 pl.stage_devices[s + 1][0], lo_r)
 
     def _send_feedback(self, pi, m, eps, lo_r):
         prog = self.prog

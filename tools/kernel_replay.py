@@ -20,6 +20,9 @@ import sys
 from collections import defaultdict
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+# programmatic launches must be off: a programmatic edge has to join two kernel nodes, and the
+# replay graph puts a timing event between every pair of launches
+os.environ["DP_PDL"] = "0"
 import torch  # noqa: E402
 
 from paper_2405_01248_b200 import _lib, engine  # noqa: E402
