@@ -240,9 +240,19 @@ def plan_programs(prof, world, S, M, D, world_batch, frozen_counts, bubble_min_l
     deps = tuple(prof.frozen_dep_indices())
     programs = {}
     if res["mode"] == planner.MODE_BIDIRECTIONAL and prof.selfcond_prob > 0:
-        # two backbones with self-conditioning: the planner's bidirectional schedule has no
-        # fwd_sc tasks; the adapter runs the pass ahead of the planned tasks (outside the plan)
-        programs[True] = build_group_program(res, frozen_counts, selfcond=True, frozen_deps=deps)
+        # two backbones with self-conditioning: the reference's bidirectional schedule has no
+        # fwd_sc tasks (planner.py:115-118). Default: the opt-in planner extension simulates both
+        # pipes WITH the pass (planning_ext) so that fills are placed against the
+        # schedule the executor runs; DP_SC_OUTSIDE_PLAN=1 keeps the reference schedule and runs
+        # the pass ahead of the planned tasks instead
+        if os.environ.get("DP_SC_OUTSIDE_PLAN", "0") == "1":
+            programs[True] = build_group_program(res, frozen_counts, selfcond=True, frozen_deps=deps)
+        else:
+            from .planning_ext import evaluate_point_selfcond
+
+            res_sc = evaluate_point_selfcond(prof, cluster, S, M, D, world_batch, bubble_min_len=bubble_min_len)
+            programs[True] = build_group_program(res_sc, frozen_counts, selfcond=True, frozen_deps=deps)
+            programs[True].plan_result = res_sc
         programs[False] = build_group_program(res, frozen_counts, selfcond=False, frozen_deps=deps)
     elif res["mode"] == planner.MODE_SELFCOND:
         programs[True] = build_group_program(res, frozen_counts, selfcond=True, frozen_deps=deps)

@@ -118,3 +118,35 @@ def test_program_documents_round_trip(tmp_path, seed, S, M, D, p, nb):
         assert dataclasses.asdict(progs["plain"]) == dataclasses.asdict(prog)
     with pytest.raises(ValueError):
         GroupProgram.from_dict({"format": "pipeline-plan/v1"})
+
+
+def test_bidirectional_selfcond_extension():
+    """Opt-in planner extension (planning_ext): both pipes of a two-backbone plan
+    carry the self-conditioning forward with the reference simulator's own rules; the
+    programs built from it contain the planned fwd_sc tasks instead of an out-of-plan pass."""
+    from paper_2405_01248_b200.planning_ext import evaluate_point_selfcond
+
+    prof = _profile(11, backbones=2, p=0.5)
+    cluster = profile.ClusterConfig(4, profile.CommCosts(2e11, 1e-5, 3e11, 1e-5))
+    ref = planner.evaluate_point(prof, cluster, 4, 4, 4, 64)
+    ext = evaluate_point_selfcond(prof, cluster, 4, 4, 4, 64)
+    assert ref["mode"] == planner.MODE_BIDIRECTIONAL
+    assert ext["plan"].stages_down == ref["plan"].stages_down and ext["plan"].stages_up == ref["plan"].stages_up
+    sc = [t for t in ext["pre_fill_schedule"].tasks if t.kind == "fwd_sc"]
+    assert not any(t.kind == "fwd_sc" for t in ref["pre_fill_schedule"].tasks)
+    assert len(sc) == 2 * 4 * 4  # both pipes, every stage, every micro-batch
+    assert ext["pre_fill_schedule"].makespan > ref["pre_fill_schedule"].makespan
+    # stage 0 of each pipe runs fwd(m) only after the pass of m left the pipe's last stage
+    for d in ("down", "up"):
+        tasks = [t for t in ext["pre_fill_schedule"].tasks if t.direction == d]
+        for m in range(4):
+            last_sc = max(t.end for t in tasks if t.kind == "fwd_sc" and t.micro_batch == m and t.stage == 3)
+            first = min(t.start for t in tasks if t.kind == "fwd" and t.micro_batch == m and t.stage == 0)
+            assert first >= last_sc - 1e-12
+    counts = [len(c.layers) for c in prof.frozen]
+    prog = build_group_program(ext, counts, selfcond=True)
+    for dp in prog.devices:
+        n_sc = sum(1 for i in dp.instrs if i[0] == "fwd_sc")
+        assert n_sc == 2 * 4 and dp.instrs.index(next(i for i in dp.instrs if i[0] == "fwd_sc")) >= 0
+    # the planned order interleaves the pass with the other pipe's tasks (not a prefix block)
+    assert any(dp.instrs[0][0] != "fwd_sc" or dp.instrs[2 * 4 - 1][0] != "fwd_sc" for dp in prog.devices)

@@ -1,9 +1,8 @@
 """Device time of every libdpipe launch of one training step, without host overhead.
 
 Records every C-ABI call of one step (argument structs copied by value), then replays the
-recorded calls in step order inside ONE CUDA graph with timing events (external event-record
-nodes) around each call, so the per-launch times carry the step's own cache state and PDL overlap
-but none of the ctypes / Python launch cost. Pointers stay valid because the caching allocator
+first call of every distinct signature 10x inside a CUDA graph (device time per call, warm L2,
+none of the ctypes / Python launch cost) and weights it by the signature's launch count. Pointers stay valid because the caching allocator
 keeps its segments mapped (the replay reads stale data; calls that index memory through
 data-dependent ids — embeddings, timestep tables — are skipped).
 
@@ -20,9 +19,6 @@ import sys
 from collections import defaultdict
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-# programmatic launches must be off: a programmatic edge has to join two kernel nodes, and the
-# replay graph puts a timing event between every pair of launches
-os.environ["DP_PDL"] = "0"
 import torch  # noqa: E402
 
 from paper_2405_01248_b200 import _lib, engine  # noqa: E402
@@ -79,48 +75,42 @@ def signature(name, saved):
     return f"{name[3:]} {ints[:6]}", 0.0
 
 
-def replay(calls, reps=2):
+def _args(saved, sh, keep):
+    args = []
+    for k, v in saved:
+        if k == "struct":
+            c = type(v).from_buffer_copy(v)
+            keep.append(c)
+            args.append(ctypes.byref(c))
+        else:
+            args.append(v)
+    args[-1] = sh
+    return args
+
+
+def time_call(name, saved, reps=10):
+    """Device time of one recorded call: `reps` copies captured in one CUDA graph, replayed."""
     stream = torch.cuda.Stream()
     lib = _lib._lib
-    evs = [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
-           for _ in calls]
     keep = []
-
-    def issue(sh):
-        for (name, saved), (a, b) in zip(calls, evs):
-            args = []
-            for k, v in saved:
-                if k == "struct":
-                    c = type(v).from_buffer_copy(v)
-                    keep.append(c)
-                    args.append(ctypes.byref(c))
-                else:
-                    args.append(v)
-            args[-1] = sh
-            a.record(stream)
-            rc = getattr(lib, name)(*args)
-            b.record(stream)
-            if rc:
-                raise RuntimeError(f"{name}: {lib.dp_last_error().decode()}")
-
+    fn = getattr(lib, name)
     with torch.cuda.stream(stream):
-        issue(stream.cuda_stream)  # eager warm-up (module loading, tensor-map caches)
+        for _ in range(2):
+            if fn(*_args(saved, stream.cuda_stream, keep)):
+                raise RuntimeError(f"{name}: {lib.dp_last_error().decode()}")
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=stream):
-        issue(stream.cuda_stream)
-    times = None
-    for _ in range(reps):
-        g.replay()
-        torch.cuda.synchronize()
-        t = [a.elapsed_time(b) for a, b in evs]
-        times = t if times is None else [min(x, y) for x, y in zip(times, t)]
+        for _ in range(reps):
+            fn(*_args(saved, stream.cuda_stream, keep))
+    g.replay()
+    torch.cuda.synchronize()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record()
     g.replay()
     s1.record()
     torch.cuda.synchronize()
-    return times, s0.elapsed_time(s1)
+    return s0.elapsed_time(s1) / reps
 
 
 def cublas_time(M, N, K, a_mn, b_mn, reps=20):
@@ -167,16 +157,21 @@ def main():
     rec.on = False
     _lib._lib = lib
     calls = rec.calls
-    times, total = replay(calls)
     agg = defaultdict(lambda: [0.0, 0, 0.0])
-    for (name, saved), t in zip(calls, times):
+    per_sig = {}
+    for name, saved in calls:
         sig, fl = signature(name, saved)
+        if sig not in per_sig:
+            per_sig[sig] = time_call(name, saved)
         a = agg[sig]
-        a[0] += t
+        a[0] += per_sig[sig]
         a[1] += 1
         a[2] += fl
+    times = [v[0] for v in agg.values()]
+    total = float("nan")
     ssum = sum(times)
-    print(f"{len(calls)} recorded libdpipe calls; graph replay {total:.2f} ms, sum of per-call events {ssum:.2f} ms")
+    print(f"{len(calls)} recorded libdpipe calls, {len(per_sig)} signatures; sum of isolated per-call device "
+          f"times {ssum:.2f} ms")
     fam = defaultdict(lambda: [0.0, 0, 0.0])
     for sig, (t, n, fl) in agg.items():
         f = fam[sig.split(" ")[0]]
