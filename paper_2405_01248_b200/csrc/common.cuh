@@ -239,6 +239,26 @@ DP_DEV void tmem_ld_32x32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 DP_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// wait, then tie every loaded register to the wait so no use of them is scheduled before it
+// (loads are in flight asynchronously until tcgen05.wait::ld)
+DP_DEV void tmem_ld_wait_dep(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) asm volatile("" : "+r"(r[i]));
+}
+// registers -> TMEM, same 32 lanes x 32 columns shape as tmem_ld_32x32
+DP_DEV void tmem_st_32x32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+      ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+        "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]),
+        "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]),
+        "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]),
+        "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+DP_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // Shared-memory matrix descriptor, SWIZZLE_128B canonical layouts (sm_100 "version 1").
 // K-major: rows of 128 B (64 bf16 along K), 8-row atoms 1024 B apart (SBO).
@@ -293,6 +313,30 @@ DP_DEV float from_f<float>(float v) {
 template <>
 DP_DEV __nv_bfloat16 from_f<__nv_bfloat16>(float v) {
   return __float2bfloat16_rn(v);
+}
+
+// One-MUFU sigmoid / SiLU through tanh.approx (max rel. error ~2^-11): used where the result is
+// rounded to bf16 anyway; the fp32 paths keep exp + IEEE division (fp32 parity at rtol 1e-4).
+DP_DEV float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+template <typename T>
+DP_DEV float sigmoid_t(float x) {
+  if constexpr (sizeof(T) == 2)
+    return fmaf(0.5f, tanh_approx(0.5f * x), 0.5f);
+  else
+    return __fdividef(1.f, 1.f + __expf(-x));
+}
+template <typename T>
+DP_DEV float silu_t(float x) {
+  if constexpr (sizeof(T) == 2) {
+    const float h = 0.5f * x;
+    return fmaf(h, tanh_approx(h), h);
+  } else {
+    return __fdividef(x, 1.f + __expf(-x));
+  }
 }
 
 DP_DEV float warp_sum(float v) {

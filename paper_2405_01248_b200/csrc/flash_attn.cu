@@ -1,16 +1,18 @@
 // Fused multi-head attention forward for sm_100a (head dim 64), K4 in SURVEY §2.4.
 //
 // One CTA = one 128-query tile of one (batch, head); 4 warps, thread t owns query row t.
-//   * TMA loads Q once and streams 128-key K/V tiles (K double-buffered, V single-buffered)
-//     from the strided [B, N, heads*64] activations (fused qkv / kv tensors, no copies);
-//   * thread 0 issues tcgen05.mma: S = Q K^T into TMEM (128 fp32 columns), then
-//     O_j = P V_j into TMEM (64 columns) with P read from shared memory;
-//   * all 128 threads run the online softmax on their S row straight from TMEM
-//     (tcgen05.ld), write P = exp2(S*scale*log2e - m) as bf16 into the SWIZZLE_128B K-major
-//     layout the MMA reads, and accumulate O in registers with the running rescale;
-//   * epilogue: O / l staged through shared memory and written by one TMA tensor store,
-//     log-sum-exp saved for the backward pass.
-// Two CTAs fit per SM (96 KB shared memory, 256 TMEM columns each), so one CTA's softmax
+//   * TMA loads Q once and streams 128-key K/V tiles (K and V double-buffered) from the strided
+//     [B, N, heads*64] activations (fused qkv / kv tensors, no copies);
+//   * thread 0 issues tcgen05.mma: S = Q K^T into TMEM (128 fp32 columns) one tile ahead of the
+//     softmax, and O += P V_j into TMEM (64 columns) with P read from shared memory;
+//   * all 128 threads run the online softmax on their S row straight from TMEM (tcgen05.ld) with
+//     packed f32x2 math (FFMA2 / FADD2, three-input FMNMX), part of the exponentials on the FMA
+//     pipe (ex2_poly2), write P = exp2(S*scale*log2e - m) as bf16 into the SWIZZLE_128B K-major
+//     layout the MMA reads; the running max moves only past a threshold, so the O rescale in
+//     TMEM is rare (FA4-style lazy correction);
+//   * epilogue: O / l (TMEM -> registers) staged through shared memory and written by one TMA
+//     tensor store, log-sum-exp saved for the backward pass.
+// Two CTAs fit per SM (113 KB shared memory, 256 TMEM columns each), so one CTA's softmax
 // overlaps the other's MMAs. Keys beyond N_k (cross-attention, 77 tokens) are masked.
 #include <cstdlib>
 #include <type_traits>
@@ -40,11 +42,38 @@ DP_DEV float ex2(float x) {
   return y;
 }
 
+// 2^x for x <= 0 on the FMA pipe (degree-3 minimax on [-0.5, 0.5], max rel. error 7.5e-5, far below
+// bf16's 3.9e-3): round-to-nearest by the 1.5*2^23 magic add, the polynomial on the fraction as packed
+// f32x2 FMAs, the integer part shifted into the exponent field. x is clamped at -126 (2^-126 ~ 0).
+// The forward softmax is bound by MUFU.EX2 (16 / clk / SM against 128-wide tensor MMAs), so a share of
+// the exponentials is computed here instead (the FA4 split of the exp work between MUFU and FMA).
+DP_DEV float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);  // round(x) >= -126: p in [0.7, 1.42] keeps a biased exponent >= 0
+  x.y = fmaxf(x.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 xi = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-xi.x, -xi.y));
+  float2 pp = __ffma2_rn(make_float2(0.05517167f, 0.05517167f), f, make_float2(0.24261114f, 0.24261114f));
+  pp = __ffma2_rn(pp, f, make_float2(0.69326097f, 0.69326097f));
+  pp = __ffma2_rn(pp, f, make_float2(0.99992806f, 0.99992806f));
+  return make_float2(__int_as_float(__float_as_int(pp.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(pp.y) + (__float_as_int(t.y) << 23)));
+}
+
+DP_DEV float max3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
 DP_DEV void tma_load_4d_(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2,
                          int c3) {
   tma_load_4d(map, bar, dst, c0, c1, c2, c3);
 }
 
+// EMU: pairs (of the 16 per 32-key chunk) whose exponentials run on the FMA pipe (ex2_poly2)
+template <int EMU>
 __global__ void __launch_bounds__(128, 2)
     fa_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
@@ -70,7 +99,7 @@ __global__ void __launch_bounds__(128, 2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 7);
 
   const int tid = threadIdx.x;
-  const int warp = tid >> 5;
+  const int warp = tid >> 5, lane = tid & 31;
   const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int q0 = qt * BQ;
   int ntiles = (p.Nk + BKV - 1) / BKV;
@@ -95,9 +124,8 @@ __global__ void __launch_bounds__(128, 2)
   const uint32_t idesc_o = idesc_bf16_f32(BQ, HD, 0, 1);
 
   // Pipeline per key tile j (one MMA-issuing thread, in-order tensor pipe):
-  //   PV(j) and S(j+1) are issued back to back after P(j) is in shared memory, so one wait on
-  //   S(j+1) also covers PV(j): O_j and S_{j+1} leave TMEM under a single tcgen05.wait, and O_j is
-  //   folded into the register accumulator one iteration late (with alpha_j kept from tile j).
+  //   once P(j) is in shared memory, PV(j) (accumulating into O in TMEM) and S(j+1) are issued back
+  //   to back; the wait for S(j+1) covers PV(j), so sP and O are free for softmax(j+1).
   //   K and V are double-buffered (V(j+1) streams in while tile j's softmax runs).
   auto issue_s = [&](int j) {
     const int kb = j & 1;
@@ -123,57 +151,77 @@ __global__ void __launch_bounds__(128, 2)
     issue_s(0);
   }
 
-  float o[HD];
-#pragma unroll
-  for (int i = 0; i < HD; ++i) o[i] = 0.f;
-  float m_run = -INFINITY, l_run = 0.f, alpha_prev = 1.f;
+  // O accumulates across key tiles in TMEM (PV(j) with accumulate = j > 0). The running max is
+  // raised only when a row's max grows by more than RESCALE_T (log2 units, a factor of 256): P then
+  // stays <= 256 (exact enough in bf16, fp32 row sums), and the O rescale (TMEM -> registers ->
+  // TMEM) is skipped on most tiles instead of folding a register accumulator every tile.
+  constexpr float RESCALE_T = 8.f;
+  float m_run = -INFINITY, l_run = 0.f;
   const int row = tid;  // query row inside the tile
-
-  auto fold_o = [&](const uint32_t (&v)[HD], float alpha) {
-#pragma unroll
-    for (int i = 0; i < HD; ++i) o[i] = fmaf(o[i], alpha, __uint_as_float(v[i]));
-  };
 
   for (int j = 0; j < ntiles; ++j) {
     mbar_wait(bar_s, j & 1);  // S(j) done, and (in-order) PV(j-1) too
     tc_fence_after();
     const int valid = p.causal ? min(min(BKV, p.Nk - j * BKV), q0 + row - j * BKV + 1)
                                : min(BKV, p.Nk - j * BKV);
-    // the row's 128 scores (and O_{j-1}) come out of TMEM under one wait
+    // the row's 128 scores leave TMEM under one wait
     uint32_t sv[BKV];
 #pragma unroll
     for (int c = 0; c < BKV / 32; ++c)
       tmem_ld_32x32(t_s + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
-    if (j > 0) {
-      uint32_t ov[HD];
-#pragma unroll
-      for (int c = 0; c < HD / 32; ++c)
-        tmem_ld_32x32(t_o + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&ov[c * 32]));
-      tmem_ld_wait();
-      fold_o(ov, alpha_prev);
-    } else {
-      tmem_ld_wait();
-    }
+    tmem_ld_wait();
     // full tiles (every row of the warp sees all 128 keys: the common case) run a copy of the
     // softmax without the per-element key mask
-    float m_new, alpha, lsum = 0.f;
+    float m_use, alpha, lsum = 0.f;
+    float2 ls2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     auto softmax_tile = [&](auto full_t) {
       constexpr bool FULL = decltype(full_t)::value;
       float mx = -INFINITY;
+      if constexpr (FULL) {
+        // four independent FMNMX3 chains (one or two softmax warps per SMSP: latency, not issue, bound)
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int i = 0; i < BKV; ++i)
-        if (FULL || i < valid) mx = fmaxf(mx, __uint_as_float(sv[i]));
-      m_new = fmaxf(m_run, mx * p.scale_log2);
-      alpha = ex2(m_run - m_new);
-      // P = exp2(s*scale - m) -> bf16 -> shared (SWIZZLE_128B K-major rows); PV(j-1) has read sP
+        for (int i = 0; i < BKV; i += 2)
+          m4[(i / 2) & 3] = max3f(m4[(i / 2) & 3], __uint_as_float(sv[i]), __uint_as_float(sv[i + 1]));
+        mx = max3f(m4[0], m4[1], fmaxf(m4[2], m4[3]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < BKV; ++i)
+          if (i < valid) mx = fmaxf(mx, __uint_as_float(sv[i]));
+      }
+      const float m_cand = fmaxf(m_run, mx * p.scale_log2);
+      if (m_cand - m_run > RESCALE_T) {
+        m_use = m_cand;
+        alpha = ex2(m_run - m_cand);  // 0 on the first tile
+      } else {
+        m_use = m_run;
+        alpha = 1.f;
+      }
+      // P = exp2(s*scale - m) -> bf16 -> shared (SWIZZLE_128B K-major rows); PV(j-1) has read sP.
+      // Packed f32x2 arithmetic (FFMA2 / FADD2) halves the FMA-pipe instructions per score.
+      const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-m_use, -m_use);
 #pragma unroll
       for (int c = 0; c < BKV / 32; ++c) {
         float pv[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float e = ex2(fmaf(__uint_as_float(sv[c * 32 + i]), p.scale_log2, -m_new));
-          pv[i] = (FULL || c * 32 + i < valid) ? e : 0.f;
-          lsum += pv[i];
+        for (int i = 0; i < 32; i += 2) {
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[c * 32 + i]), __uint_as_float(sv[c * 32 + i + 1])),
+                                      sc2, nm2);
+          float2 e;
+          // emulated pairs spread over the chunk (every 16/EMU-th pair) so MUFU and FMA work interleave
+          if (EMU > 0 && ((i / 2) % (16 / (EMU > 0 ? EMU : 1))) == (16 / (EMU > 0 ? EMU : 1)) - 1) {
+            e = ex2_poly2(x);
+          } else {
+            e.x = ex2(x.x);
+            e.y = ex2(x.y);
+          }
+          if constexpr (!FULL) {
+            e.x = (c * 32 + i < valid) ? e.x : 0.f;
+            e.y = (c * 32 + i + 1 < valid) ? e.y : 0.f;
+          }
+          pv[i] = e.x;
+          pv[i + 1] = e.y;
+          ls2[(i / 2) & 3] = __fadd2_rn(ls2[(i / 2) & 3], e);
         }
         uint8_t* blk = sP + (c >> 1) * TILE_BYTES + row * 128;
 #pragma unroll
@@ -192,9 +240,29 @@ __global__ void __launch_bounds__(128, 2)
       softmax_tile(std::true_type{});
     else
       softmax_tile(std::false_type{});
+    lsum = (ls2[0].x + ls2[0].y) + (ls2[1].x + ls2[1].y) + ((ls2[2].x + ls2[2].y) + (ls2[3].x + ls2[3].y));
+    // rescale O (holding PV(0..j-1), complete before S(j)) where the max moved;
+    // warp-collective TMEM access, so a warp rescales when any of its rows needs it
+    if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t ov[32];
+        tmem_ld_32x32(t_o + lane_off + c * 32, ov);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float2 r = __fmul2_rn(make_float2(__uint_as_float(ov[i]), __uint_as_float(ov[i + 1])),
+                                      make_float2(alpha, alpha));
+          ov[i] = __float_as_uint(r.x);
+          ov[i + 1] = __float_as_uint(r.y);
+        }
+        tmem_st_32x32(t_o + lane_off + c * 32, ov);
+      }
+      tmem_st_wait();
+    }
     fence_async_shared();
     tc_fence_before();
-    __syncthreads();  // P(j) in shared memory; every thread has read S(j) and O_{j-1} from TMEM
+    __syncthreads();  // P(j) in shared memory; S(j) read and O rescaled in TMEM by every thread
     if (tid == 0) {
       tc_fence_after();
       const int vb = j & 1;
@@ -205,13 +273,16 @@ __global__ void __launch_bounds__(128, 2)
       for (int k = 0; k < BKV / 16; ++k) {
         const uint64_t ad = smem_desc_sw128(pa + (k >> 2) * TILE_BYTES + (k & 3) * 32, 16, 1024);
         const uint64_t bd = smem_desc_sw128(va + k * 2048, 8192, 1024);
-        tc_mma_bf16(t_o, ad, bd, idesc_o, k > 0 ? 1u : 0u);
+        tc_mma_bf16(t_o, ad, bd, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
       }
       tc_commit(bar_o);
+      // S(j+1) behind PV(j): the wait for S(j+1) then also covers PV(j) (in-order tensor pipe), so
+      // P and O are free for the next softmax without a second barrier. Measured at 32x5x1024^2
+      // against S(j+1) ahead of PV(j) (+ a PV wait before the P store): 86 vs 91 us, and against an
+      // S(j+1) issued before softmax(j) through a per-warp "S consumed" barrier: 92 us.
       if (j + 1 < ntiles) {
         issue_s(j + 1);
-        // S(j) finished before S(j+1) was issued: K buffer j&1 is free for tile j+2; V buffer
-        // (j+1)&1 held V(j-1), read by PV(j-1), which finished before S(j)
+        // S(j) finished: K buffer j&1 is free for tile j+2
         if (j + 2 < ntiles) {
           mbar_expect_tx(&bar_k[j & 1], TILE_BYTES);
           tma_load_4d_(&tmK, &bar_k[j & 1], sK + (j & 1) * TILE_BYTES, 0, (j + 2) * BKV, h, b);
@@ -219,37 +290,33 @@ __global__ void __launch_bounds__(128, 2)
       }
     }
     l_run = l_run * alpha + lsum;
-    m_run = m_new;
-    alpha_prev = alpha;
+    m_run = m_use;
     if (tid == 0 && j + 1 < ntiles && j >= 1) {
       // V(j+1) into buffer (j+1)&1 (V(j-1) there was consumed by PV(j-1), complete before S(j))
       mbar_expect_tx(&bar_v[(j + 1) & 1], TILE_BYTES);
       tma_load_4d_(&tmV, &bar_v[(j + 1) & 1], sV + ((j + 1) & 1) * TILE_BYTES, 0, (j + 1) * BKV, h, b);
     }
   }
-  // the last PV
+  // the last PV, then O / l -> shared (SWIZZLE_128B rows of 64 bf16) -> one TMA store
   mbar_wait(bar_o, (ntiles - 1) & 1);
   tc_fence_after();
-  {
-    uint32_t ov[HD];
-#pragma unroll
-    for (int c = 0; c < HD / 32; ++c)
-      tmem_ld_32x32(t_o + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&ov[c * 32]));
-    tmem_ld_wait();
-    fold_o(ov, alpha_prev);
-  }
-
-  // epilogue: O / l -> shared (SWIZZLE_128B rows of 64 bf16) -> one TMA store
   const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
   uint8_t* so = sP;  // the P buffer is free: the last PV MMA completed
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    uint4 u;
-    u.x = pack_bf16x2(o[q * 8 + 0] * inv, o[q * 8 + 1] * inv);
-    u.y = pack_bf16x2(o[q * 8 + 2] * inv, o[q * 8 + 3] * inv);
-    u.z = pack_bf16x2(o[q * 8 + 4] * inv, o[q * 8 + 5] * inv);
-    u.w = pack_bf16x2(o[q * 8 + 6] * inv, o[q * 8 + 7] * inv);
-    *reinterpret_cast<uint4*>(so + row * 128 + ((q ^ (row & 7)) * 16)) = u;
+  for (int c = 0; c < HD / 32; ++c) {
+    uint32_t ov[32];
+    tmem_ld_32x32(t_o + lane_off + c * 32, ov);
+    tmem_ld_wait();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u;
+      u.x = pack_bf16x2(__uint_as_float(ov[q * 8 + 0]) * inv, __uint_as_float(ov[q * 8 + 1]) * inv);
+      u.y = pack_bf16x2(__uint_as_float(ov[q * 8 + 2]) * inv, __uint_as_float(ov[q * 8 + 3]) * inv);
+      u.z = pack_bf16x2(__uint_as_float(ov[q * 8 + 4]) * inv, __uint_as_float(ov[q * 8 + 5]) * inv);
+      u.w = pack_bf16x2(__uint_as_float(ov[q * 8 + 6]) * inv, __uint_as_float(ov[q * 8 + 7]) * inv);
+      const int chunk = c * 4 + q;
+      *reinterpret_cast<uint4*>(so + row * 128 + ((chunk ^ (row & 7)) * 16)) = u;
+    }
   }
   if (p.lse && q0 + row < p.N)
     p.lse[((int64_t)b * p.heads + h) * p.N + q0 + row] = m_run + log2f(l_run);
@@ -696,9 +763,18 @@ extern "C" int dp_flash_attn_fwd(const DpAttnArgs* a, dp_stream_t stream) {
   if (int e = fa_map(&mk, a->k, a->Nk, a->heads, a->B, a->kv_ld, a->kv_bs)) return e;
   if (int e = fa_map(&mv, a->v, a->Nk, a->heads, a->B, a->kv_ld, a->kv_bs)) return e;
   if (int e = fa_map(&mo, a->o, a->N, a->heads, a->B, a->o_ld, a->o_bs)) return e;
+  // share of the softmax exponentials emulated on the FMA pipe: EMU of every 16 pairs (DP_FA_EMU:
+  // experiments; 0, 1, 2, 4 or 8)
+  static const int emu = [] {
+    const char* e = getenv("DP_FA_EMU");
+    const int v = e ? atoi(e) : 4;
+    return (v == 0 || v == 1 || v == 2 || v == 4 || v == 8) ? v : 4;
+  }();
+  auto kern = emu == 0 ? fa::fa_fwd_kernel<0> : emu == 1 ? fa::fa_fwd_kernel<1> : emu == 2 ? fa::fa_fwd_kernel<2>
+            : emu == 8 ? fa::fa_fwd_kernel<8> : fa::fa_fwd_kernel<4>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(fa::fa_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(fa::SMEM));
     if (e != cudaSuccess) {
       set_error(std::string("flash attention attr: ") + cudaGetErrorString(e));
@@ -708,7 +784,7 @@ extern "C" int dp_flash_attn_fwd(const DpAttnArgs* a, dp_stream_t stream) {
   }
   fa::Params p{a->N, a->Nk, a->heads, a->scale * 1.4426950408889634f, a->lse, a->causal};
   dim3 grid((a->N + fa::BQ - 1) / fa::BQ, a->heads, a->B);
-  launch_k(fa::fa_fwd_kernel, dim3(grid), dim3(128), fa::SMEM, reinterpret_cast<cudaStream_t>(stream), mq, mk, mv,
+  launch_k(kern, dim3(grid), dim3(128), fa::SMEM, reinterpret_cast<cudaStream_t>(stream), mq, mk, mv,
            mo, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

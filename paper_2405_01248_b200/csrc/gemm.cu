@@ -6,8 +6,9 @@
 //   warp 0 (1 thread)   TMA producer: fills a STAGES-deep smem ring (A 128x64, B BNx64)
 //   warp 1 (1 thread)   MMA issuer: 4 x tcgen05.mma (128 x BN x 16) per k-block into TMEM
 //   warp 2              TMEM allocator (2 accumulator buffers of BN fp32 columns)
-//   warps 4-7           epilogue: tcgen05.ld -> alpha/bias/residual -> global store or
-//                       fp32 atomic accumulate (split-K, gradient accumulation)
+//   warps 4-11          epilogue, two warps per TMEM lane quadrant (even / odd 32-column chunks):
+//                       tcgen05.ld -> alpha/bias/residual -> bf16 TMA tensor store, or fp32 atomic
+//                       accumulate (split-K, gradient accumulation)
 // Operand "modes" only change how the producer addresses global memory:
 //   A_KMAJ / B_KMAJ     row-major [rows][K]                      (linear fwd, QK^T)
 //   A_MNMAJ / B_MNMAJ   [K][rows]                                (dgrad/wgrad, P.V)
@@ -54,6 +55,11 @@ struct TcParams {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
+// warps 0-3: TMA producer, MMA issuer, TMEM allocator, idle; warps 4-11: epilogue (two per TMEM lane
+// quadrant), each with two 2 KB bf16 staging buffers for the TMA stores
+constexpr int EPI_WARPS = 8;
+constexpr int GEMM_THREADS = 32 * (4 + EPI_WARPS);
+constexpr int EPI_SMEM = EPI_WARPS * 2 * 32 * 64;
 constexpr uint32_t A_STAGE_BYTES = BM * BK * 2;
 
 // HALO (3x3 stride-1 convs whose 128-pixel tiles lie in one image row): a stage holds ONE input
@@ -69,8 +75,8 @@ struct TcCfg {
   static constexpr uint32_t B_STAGE_BYTES = (HALO ? 3 : 1) * B_SUB;
   static constexpr uint32_t A_BYTES = HALO ? ((HALO_A_BYTES + 1023) / 1024) * 1024 : A_STAGE_BYTES;
   static constexpr uint32_t A_TX = HALO ? HALO_A_BYTES : A_STAGE_BYTES;
-  // as many 64-deep k-stages as fit next to the 16 KB epilogue staging buffers
-  static constexpr int STAGES_FIT = 209 * 1024 / (A_BYTES + B_STAGE_BYTES);
+  // as many 64-deep k-stages as fit next to the epilogue staging buffers
+  static constexpr int STAGES_FIT = (225 * 1024 - EPI_SMEM) / (A_BYTES + B_STAGE_BYTES);
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   // BN > 256 (320: U-Net 320/640-channel layers): two N = BN/2 MMAs per k-step into adjacent TMEM
   // column ranges, one accumulator buffer (the epilogue is exposed once per long-K tile); each CTA
@@ -79,7 +85,7 @@ struct TcCfg {
   static constexpr uint32_t B_HALF = B_SUB / NH;
   static constexpr int NACC = 2 * BN <= 512 ? 2 : 1;
   static constexpr int TMEM_COLS = (NACC * BN <= 128) ? 128 : (NACC * BN <= 256 ? 256 : 512);
-  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_STAGE_BYTES) + 8 * 2048 + 256;
+  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_STAGE_BYTES) + EPI_SMEM + 256;
 };
 
 DP_DEV void pixel_origin(int pix0, int P, int Q, int& n, int& h, int& w) {
@@ -94,7 +100,11 @@ template <int BN>
 DP_DEV void epilogue_store(const TcParams& p, int row, int n, int z1, int z2, const uint32_t (&v)[32]) {
   float f[32];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * p.alpha;
+  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+  if (p.alpha != 1.f) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) f[i] *= p.alpha;
+  }
   const int nvalid = min(32, p.N - n);
   if (p.bias) {
     if (nvalid == 32 && (reinterpret_cast<uintptr_t>(p.bias + n) & 15) == 0) {
@@ -266,11 +276,27 @@ DP_DEV void stage_row_bf16(uint8_t* buf, int lane, const float (&f)[32]) {
   }
 }
 
+// fp32 half chunk (16 columns, 64-byte row) in the SWIZZLE_64B layout of the 16 x 32 reduce box
+DP_DEV void stage_row_f32(uint8_t* buf, int lane, const float (&f)[32], int hh) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int qs = q ^ ((lane >> 1) & 3);
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(buf + lane * 64 + qs * 16)),
+                 "f"(f[hh * 16 + q * 4 + 0]), "f"(f[hh * 16 + q * 4 + 1]), "f"(f[hh * 16 + q * 4 + 2]),
+                 "f"(f[hh * 16 + q * 4 + 3])
+                 : "memory");
+  }
+}
+
 template <int BN>
 DP_DEV void epilogue_math(const TcParams& p, int row, int n, int z1, int z2, const uint32_t (&v)[32],
                           float (&f)[32], const uint4 (&rpre)[4], bool use_pre) {
 #pragma unroll
-  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * p.alpha;
+  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+  if (p.alpha != 1.f) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) f[i] *= p.alpha;
+  }
   const int nvalid = min(32, p.N - n);
   if (p.bias) {
     if (nvalid == 32 && (reinterpret_cast<uintptr_t>(p.bias + n) & 15) == 0) {
@@ -321,7 +347,7 @@ DP_DEV void epilogue_math(const TcParams& p, int row, int n, int z1, int z2, con
 constexpr int EPI_STAGE_BYTES = 32 * 64;  // one 32 x 32 bf16 chunk
 
 template <int BN, int CG, bool HALO, bool RES>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmD, const TcParams p) {
   using Cfg = TcCfg<BN, CG, HALO>;
@@ -333,7 +359,7 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
   uint8_t* sE = sB + STAGES * Cfg::B_STAGE_BYTES;            // 4 warps x 2 x 2 KB, 1 KB aligned
-  uint64_t* full = reinterpret_cast<uint64_t*>(sE + 8 * EPI_STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sE + 2 * EPI_WARPS * EPI_STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -355,7 +381,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4 * CG);  // one arrival per epilogue warp of each CTA
+      mbar_init(&tempty[a], EPI_WARPS * CG);  // one arrival per epilogue warp of each CTA
     }
     fence_barrier_init();
   }
@@ -569,10 +595,11 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue (every CTA)
-    const int wq = warp - 4;
+    const int wq = warp & 3;            // TMEM lane quadrant (rows wq*32 .. +32 of the tile)
+    const int half = (warp - 4) >> 2;   // chunk parity this warp stores
     int acc = 0;
     uint32_t acc_phase = 0;
-    uint8_t* ebuf = sE + wq * 2 * EPI_STAGE_BYTES;
+    uint8_t* ebuf = sE + (warp - 4) * 2 * EPI_STAGE_BYTES;
     int chunk_seq = 0;
     const uint32_t tempty_leader0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
     WorkIter it;
@@ -596,15 +623,21 @@ __global__ void __launch_bounds__(256, 1)
       const int row = row0 + lane;
       uint4 r1[4], r2[4];
       if constexpr (RES) {
-        rload(wk, row, 0, r1);
-        rload(wk, row, 1, r2);
+        rload(wk, row, half, r1);
+        rload(wk, row, half + 2, r2);
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      // two warps per TMEM lane quadrant split the accumulator's 32-column chunks (even / odd):
+      // the epilogue (TMEM load, bias / residual, bf16 staging, TMA store per chunk) is latency
+      // bound per warp and had bounded short-K GEMMs with one warp per quadrant
+      const int nch = min(BN / 32, (p.N - wk.n_blk * BN + 31) / 32);  // warp-uniform
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + acc * BN;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half; c < nch; c += 2) {
         const int n = wk.n_blk * BN + c * 32;
-        if (n >= p.N) break;  // warp-uniform
+        uint32_t v[32];
+        tmem_ld_32x32(tbase + c * 32, v);
         uint4 rc[4];
         if constexpr (RES) {
 #pragma unroll
@@ -612,13 +645,31 @@ __global__ void __launch_bounds__(256, 1)
             rc[q] = r1[q];
             r1[q] = r2[q];
           }
-          rload(wk, row, c + 2, r2);
+          rload(wk, row, c + 4, r2);
         }
+        tmem_ld_wait_dep(v);
         const bool use_pre = rpre_on && row < p.M && n + 32 <= p.N;
-        uint32_t v[32];
-        tmem_ld_32x32(tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + acc * BN + c * 32, v);
-        tmem_ld_wait();
-        if (p.d_tma) {
+        if (p.d_tma == 2) {
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * p.alpha;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            uint8_t* buf = ebuf + (chunk_seq & 1) * EPI_STAGE_BYTES;
+            if (chunk_seq >= 2) {
+              if (lane == 0) bulk_wait_read<1>();
+              __syncwarp();
+            }
+            stage_row_f32(buf, lane, f, hh);
+            fence_async_shared();
+            __syncwarp();
+            if (lane == 0 && row0 < p.M) {
+              tma_reduce_add_4d(&tmD, buf, n + 16 * hh, row0, wk.z1, wk.z2);
+              bulk_commit();
+            }
+            ++chunk_seq;
+          }
+        } else if (p.d_tma) {
           float f[32];
           epilogue_math<BN>(p, row, n, wk.z1, wk.z2, v, f, rc, use_pre);
           uint8_t* buf = ebuf + (chunk_seq & 1) * EPI_STAGE_BYTES;
@@ -697,7 +748,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() { return encode_fn(); }
 // 4-D bf16 map. dims innermost-first; strides in ELEMENTS for dims 1..3.
 static int make_map(CUtensorMap* map, const void* base, const uint64_t dims[4],
                     const int64_t strides_el[3], const uint32_t box[4], const uint32_t estr[4],
-                    CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+                    CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B, int esize = 2) {
   auto fn = encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -707,7 +758,7 @@ static int make_map(CUtensorMap* map, const void* base, const uint64_t dims[4],
   cuuint64_t gstr[3];
   for (int i = 0; i < 4; ++i) gdim[i] = dims[i] ? dims[i] : 1;
   for (int i = 0; i < 3; ++i) {
-    int64_t s = strides_el[i] * 2;
+    int64_t s = strides_el[i] * esize;
     if (gdim[i + 1] == 1 && (s <= 0 || s % 16)) {
       // degenerate dimension: any legal stride works
       s = 16;
@@ -727,7 +778,8 @@ static int make_map(CUtensorMap* map, const void* base, const uint64_t dims[4],
     bx[i] = box[i];
     es[i] = estr[i];
   }
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), gdim, gstr,
+  CUresult r = fn(map, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                  const_cast<void*>(base), gdim, gstr,
                   bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -772,7 +824,7 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
   if (grid <= 0) return 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
@@ -884,15 +936,21 @@ static void choose_tile(int M, int N, int K, bool b_mn, int& bn_out, int& cg_out
 
 // bf16 STORE outputs with TMA-legal strides are written by tensor stores (box 32 x 32,
 // SWIZZLE_64B); fp32 / atomic outputs keep the direct per-thread path.
+// fp32 ATOMIC_ADD outputs (weight gradients, split-K partials) are added by TMA reduce-add of 32 x 16
+// fp32 boxes staged in shared memory (d_tma = 2): bulk L2 reductions instead of one red.v4 per lane
+// and 16 bytes.
 static int make_dmap(CUtensorMap* md, TcParams& p, int M, int N, int b1, int b2) {
+  static const int no_red = env_int("DP_NO_TMA_REDUCE");  // experiments: per-thread atomics
   p.d_tma = 0;
-  if (p.d_f32 || p.out_mode != DP_OUT_STORE || !p.vec_ok) return 0;
+  if (!p.vec_ok) return 0;
+  const bool red = p.d_f32 && p.out_mode == DP_OUT_ATOMIC_ADD && !no_red;
+  if (!red && (p.d_f32 || p.out_mode != DP_OUT_STORE)) return 0;
   const uint64_t d[4] = {(uint64_t)N, (uint64_t)M, (uint64_t)b1, (uint64_t)b2};
   const int64_t s[3] = {p.d_ld, b1 > 1 ? p.d_bs1 : (int64_t)M * p.d_ld,
                         b2 > 1 ? p.d_bs2 : (int64_t)M * p.d_ld * b1};
-  const uint32_t box[4] = {32, 32, 1, 1};
+  const uint32_t box[4] = {red ? 16u : 32u, 32, 1, 1};
   const uint32_t ones[4] = {1, 1, 1, 1};
-  if (make_map(md, p.D, d, s, box, ones, CU_TENSOR_MAP_SWIZZLE_64B) == 0) p.d_tma = 1;
+  if (make_map(md, p.D, d, s, box, ones, CU_TENSOR_MAP_SWIZZLE_64B, red ? 4 : 2) == 0) p.d_tma = red ? 2 : 1;
   return 0;
 }
 
@@ -1023,12 +1081,14 @@ static int launch_bn(int bn, int cg, const CUtensorMap& ma, const CUtensorMap& m
     q.vec_ok = (N % 4) == 0;
     q.d_tma = 0;
     choose_split(q, 0, true);
+    CUtensorMap mq = ma;
+    make_dmap(&mq, q, M, N, b1, b2);
     cudaError_t e = cudaMemsetAsync(ws, 0, need, st);
     if (e != cudaSuccess) {
       set_error(std::string("split-K workspace memset: ") + cudaGetErrorString(e));
       return e;
     }
-    int rc = cg == 2 ? launch_cg<2>(bn, ma, mb, ma, q, st) : launch_cg<1>(bn, ma, mb, ma, q, st);
+    int rc = cg == 2 ? launch_cg<2>(bn, ma, mb, mq, q, st) : launch_cg<1>(bn, ma, mb, mq, q, st);
     if (rc) return rc;
     const int64_t total = (int64_t)p.nbatch * M * (N / 8);
     const int64_t want = (total + 255) / 256;

@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(GN_THREADS, 4)
 #pragma unroll
         for (int j = 0; j < V; ++j) {
           float v = fmaf(f[u][j], a[j], b[j]);
-          if (silu_on) v = __fdividef(v, 1.f + __expf(-v));
+          if (silu_on) v = silu_t<T>(v);
           f[u][j] = v;
         }
         st16(yp + u * step, f[u]);
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(GN_THREADS, 4)
 #pragma unroll
       for (int j = 0; j < V; ++j) {
         float v = fmaf(f[j], a[j], b[j]);
-        if (silu_on) v = __fdividef(v, 1.f + __expf(-v));
+        if (silu_on) v = silu_t<T>(v);
         f[j] = v;
       }
       st16(yp, f);
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(GN_THREADS, GN_BWD_MINB)
           float d = fd[j];
           if (silu_on) {
             const float y0 = fmaf(xh, ga[j], be[j]);
-            const float s = __fdividef(1.f, 1.f + __expf(-y0));  // MUFU rcp (no IEEE fixup path)
+            const float s = sigmoid_t<T>(y0);  // one MUFU (bf16) / MUFU rcp without the IEEE fixup (fp32)
             d *= s * (1.f + y0 * (1.f - s));
           }
           sa[j] += d;
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(GN_THREADS, GN_BWD_MINB)
         float d = fd[j];
         if (silu_on) {
           const float y0 = fmaf(xh, ga[j], be[j]);
-          const float sg = __fdividef(1.f, 1.f + __expf(-y0));
+          const float sg = sigmoid_t<T>(y0);
           d *= sg * (1.f + y0 * (1.f - sg));
         }
         const float v = rs[j] * (ga[j] * d - gA[j] - xh * gB[j]);

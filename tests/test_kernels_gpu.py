@@ -254,6 +254,30 @@ def test_flash_attention_vs_torch(B, N, Nk, C, heads, cross):
         assert _rel(kv.grad, kvr.grad) < 3e-2
 
 
+@pytest.mark.parametrize("N,ramp", [(1024, 6.0), (4096, 3.0), (1000, 12.0)])
+def test_flash_attention_growing_max(N, ramp):
+    """Keys whose norm grows along the sequence: the running row max rises by far more than the forward's
+    lazy-rescale threshold (2^8) across key tiles, so the O-in-TMEM rescale path runs; also the 4096-token
+    (512 px level-0) shape. Forward and backward vs fp32 PyTorch SDPA."""
+    from paper_2405_01248_b200 import nn
+    B, C, heads = 1, 128, 2
+    g = torch.Generator(device="cuda").manual_seed(N)
+    base = torch.randn(B, N, 3 * C, device="cuda", generator=g)
+    gain = 1.0 + ramp * torch.arange(N, device="cuda", dtype=torch.float32) / N
+    base[..., C:2 * C] *= gain[None, :, None]
+    base[..., :C] *= 2.0
+    q = base.bfloat16().requires_grad_(True)
+    o = nn.attention(q, None, heads)
+    qr = q.detach().float().requires_grad_(True)
+    Q, K, V = (qr[..., i * C:(i + 1) * C].reshape(B, N, heads, 64).transpose(1, 2) for i in range(3))
+    ref = F.scaled_dot_product_attention(Q, K, V).transpose(1, 2).reshape(B, N, C)
+    assert _rel(o, ref) < 2e-2
+    do = torch.randn_like(o)
+    o.backward(do)
+    ref.backward(do.float())
+    assert _rel(q.grad, qr.grad) < 3e-2
+
+
 @pytest.mark.parametrize("B,N,C,heads", [(4, 77, 1024, 16), (2, 300, 128, 2), (1, 1024, 320, 5)])
 def test_flash_attention_causal_forward(B, N, C, heads):
     """Causal fused forward (frozen CLIP text encoder: no gradient) vs fp32 PyTorch SDPA."""
