@@ -29,8 +29,8 @@ namespace dp {
 thread_local std::string g_last_error;
 void set_error(const std::string& s) { g_last_error = s; }
 
-enum { A_KMAJ = 0, A_MNMAJ = 1, A_CONV = 2, A_WG_DY = 3 };
-enum { B_KMAJ = 0, B_MNMAJ = 1, B_WG_X = 2, B_DGRAD = 3 };
+enum { A_KMAJ = 0, A_MNMAJ = 1, A_CONV = 2, A_WG_DY = 3, A_WG_X = 4 };
+enum { B_KMAJ = 0, B_MNMAJ = 1, B_WG_X = 2, B_DGRAD = 3, B_WG_DY = 4 };
 
 struct TcParams {
   int M, N;
@@ -365,7 +365,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  const int warp = threadIdx.x >> 5;
+  // warp index through a shuffle from lane 0: the compiler then knows it is warp-uniform, so the role
+  // branches below are uniform and the producer / MMA bookkeeping lives in uniform registers (no
+  // per-instruction uniformity waterfall around every UTMALDG / UTCHMMA)
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   // CTA pair (cta_group::2): rank 0 (leader) issues the M=256 MMAs; each CTA stages its own
   // 128 rows of A and half of B's N columns, and owns its 128 rows of the accumulator.
@@ -403,13 +406,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // or written before the previous grid has completed and flushed.
   DP_PDL_ENTRY();
 
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (every CTA)
+    // The whole warp walks the work list (lane 0 issues). Per-tile invariants (weight-gradient
+    // channel / tap of every 64-column box) are computed once per tile and the per-k-block
+    // coordinates (conv tap + channel block, pixel tile) advance incrementally: the divisions the
+    // producer used to do per k-block (~330 instructions) had made it, not the tensor core, the
+    // bound of the conv wgrad mainloop.
+    const bool issuer = lane == 0;
     int stage = 0;
     uint32_t phase = 0;
     WorkIter it;
     it.init(p, CG);
     Work wk;
+    const bool wg = p.a_mode == A_WG_DY || p.a_mode == A_WG_X;
     while (it.next(p, wk)) {
       const int z1 = wk.z1, z2 = wk.z2;
       const int m0 = wk.m_blk * (BM * CG) + crank * BM;
@@ -420,90 +430,126 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         ch = ch * p.stride - p.pad_h;
         cw = cw * p.stride - p.pad_w;
       }
+      // weight-gradient window boxes: (channel, filter row, filter column) of each 64-wide box of the
+      // x operand (B for B_WG_X: columns n0 + 64 j; A for A_WG_X: rows m0 + 64 j)
+      constexpr int NXB = (BNL / 64) > 2 ? (BNL / 64) : 2;
+      int xci[NXB], xrr[NXB], xss[NXB];
+      if (p.b_mode == B_WG_X || p.a_mode == A_WG_X) {
+        const int base = p.a_mode == A_WG_X ? m0 : n0;
+#pragma unroll
+        for (int j = 0; j < NXB; ++j) {
+          const int nn = base + 64 * j;
+          const int tap = nn / p.C;
+          xci[j] = nn - tap * p.C;
+          xrr[j] = tap / p.S;
+          xss[j] = tap - xrr[j] * p.S;
+        }
+      }
+      // k-block counters: (filter row, filter column, channel block) for the conv modes, pixel tile
+      // origin for the weight-gradient modes
+      int kr = 0, ks = 0, kc = 0, pn = 0, ph = 0, pw = 0;
+      if (p.a_mode == A_CONV) {
+        const int per_r = HALO ? p.cblk : p.S * p.cblk;
+        kr = wk.kb0 / per_r;
+        const int rem = wk.kb0 - kr * per_r;
+        ks = HALO ? 0 : rem / p.cblk;
+        kc = rem - ks * p.cblk;
+      } else if (wg) {
+        pixel_origin(wk.kb0 * BK, p.P, p.Q, pn, ph, pw);
+      }
       for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
-        if (leader) mbar_expect_tx(&full[stage], CG * (Cfg::A_TX + Cfg::B_STAGE_BYTES));
+        if (leader && issuer) mbar_expect_tx(&full[stage], CG * (Cfg::A_TX + Cfg::B_STAGE_BYTES));
         uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
         uint8_t* b_dst = sB + stage * Cfg::B_STAGE_BYTES;
         uint64_t* fb = &full[stage];
         auto load = [&](const CUtensorMap* m, void* dst, int c0, int c1, int c2, int c3) {
+          if (!issuer) return;
           if constexpr (CG == 2)
             tma_load_4d_2sm(m, fb, dst, c0, c1, c2, c3);
           else
             tma_load_4d(m, fb, dst, c0, c1, c2, c3);
         };
-        int pn = 0, ph = 0, pw = 0;
         if constexpr (HALO) {
           // kb = (filter row r, 64-channel block): one 130-pixel strip, three tap weight blocks
-          const int rr = kb / p.cblk;
-          const int cb = kb - rr * p.cblk;
-          load(&tmA, a_dst, cb * BK, cw, ch + rr, cn);
+          load(&tmA, a_dst, kc * BK, cw, ch + kr, cn);
 #pragma unroll
           for (int ss = 0; ss < 3; ++ss)
-            load(&tmB, b_dst + ss * Cfg::B_SUB, ((rr * 3 + ss) * p.cblk + cb) * BK, n0, z1, z2);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-          continue;
-        }
-        if (p.a_mode == A_WG_DY || p.b_mode == B_WG_X) pixel_origin(kb * BK, p.P, p.Q, pn, ph, pw);
-        switch (p.a_mode) {
-          case A_KMAJ:
-            load(&tmA, a_dst, kb * BK, m0, z1, z2);
-            break;
-          case A_MNMAJ:
-            load(&tmA, a_dst, m0, kb * BK, z1, z2);
-            load(&tmA, a_dst + 8192, m0 + 64, kb * BK, z1, z2);
-            break;
-          case A_CONV: {
-            const int tap = kb / p.cblk;
-            const int cb = kb - tap * p.cblk;
-            const int rr = tap / p.S, ss = tap - (tap / p.S) * p.S;
-            load(&tmA, a_dst, cb * BK, cw + ss, ch + rr, cn);
-            break;
-          }
-          default:  // A_WG_DY
-            load(&tmA, a_dst, m0, pw, ph, pn);
-            load(&tmA, a_dst + 8192, m0 + 64, pw, ph, pn);
-            break;
-        }
-        switch (p.b_mode) {
-          case B_KMAJ:
-            if constexpr (Cfg::NH == 2) {
-              const int nt = wk.n_blk * BN + crank * (BNL / 2);
-              load(&tmB, b_dst, kb * BK, nt, z1, z2);
-              load(&tmB, b_dst + Cfg::B_HALF, kb * BK, nt + BN / 2, z1, z2);
-            } else {
-              load(&tmB, b_dst, kb * BK, n0, z1, z2);
+            load(&tmB, b_dst + ss * Cfg::B_SUB, ((kr * 3 + ss) * p.cblk + kc) * BK, n0, z1, z2);
+        } else {
+          switch (p.a_mode) {
+            case A_KMAJ:
+              load(&tmA, a_dst, kb * BK, m0, z1, z2);
+              break;
+            case A_MNMAJ:
+              load(&tmA, a_dst, m0, kb * BK, z1, z2);
+              load(&tmA, a_dst + 8192, m0 + 64, kb * BK, z1, z2);
+              break;
+            case A_CONV:
+              load(&tmA, a_dst, kc * BK, cw + ks, ch + kr, cn);
+              break;
+            case A_WG_X: {  // rows = (tap, channel): shifted input windows, MN-major
+              const int hin = ph * p.stride - p.pad_h, win = pw * p.stride - p.pad_w;
+#pragma unroll
+              for (int j = 0; j < 2; ++j) load(&tmA, a_dst + j * 8192, xci[j], win + xss[j], hin + xrr[j], pn);
+              break;
             }
-            break;
-          case B_MNMAJ:
-#pragma unroll
-            for (int j = 0; j < BNL / 64; ++j) load(&tmB, b_dst + j * 8192, n0 + 64 * j, kb * BK, z1, z2);
-            break;
-          case B_DGRAD: {
-            // B(n = input channel c, k = (tap, filter kk)) = w[kk][R-1-r][S-1-s][c]: the conv
-            // weights [K][R][S][C] read tap-flipped in place (no transposed copy)
-            const int tap = kb / p.cblk;
-            const int kk = kb - tap * p.cblk;
-            const int rr = tap / p.S, ss = tap - (tap / p.S) * p.S;
-#pragma unroll
-            for (int j = 0; j < BNL / 64; ++j)
-              load(&tmB, b_dst + j * 8192, n0 + 64 * j, p.S - 1 - ss, p.Rf - 1 - rr, kk * BK);
-            break;
+            default:  // A_WG_DY
+              load(&tmA, a_dst, m0, pw, ph, pn);
+              load(&tmA, a_dst + 8192, m0 + 64, pw, ph, pn);
+              break;
           }
-          default: {  // B_WG_X
-            const int hin = ph * p.stride - p.pad_h, win = pw * p.stride - p.pad_w;
+          switch (p.b_mode) {
+            case B_KMAJ:
+              if constexpr (Cfg::NH == 2) {
+                const int nt = wk.n_blk * BN + crank * (BNL / 2);
+                load(&tmB, b_dst, kb * BK, nt, z1, z2);
+                load(&tmB, b_dst + Cfg::B_HALF, kb * BK, nt + BN / 2, z1, z2);
+              } else {
+                load(&tmB, b_dst, kb * BK, n0, z1, z2);
+              }
+              break;
+            case B_MNMAJ:
 #pragma unroll
-            for (int j = 0; j < BNL / 64; ++j) {
-              const int nn = n0 + 64 * j;
-              const int tap = nn / p.C;
-              const int ci = nn - tap * p.C;
-              const int rr = tap / p.S, ss = tap - (tap / p.S) * p.S;
-              load(&tmB, b_dst + j * 8192, ci, win + ss, hin + rr, pn);
+              for (int j = 0; j < BNL / 64; ++j) load(&tmB, b_dst + j * 8192, n0 + 64 * j, kb * BK, z1, z2);
+              break;
+            case B_DGRAD:
+              // B(n = input channel c, k = (tap, filter kk)) = w[kk][R-1-r][S-1-s][c]: the conv
+              // weights [K][R][S][C] read tap-flipped in place (no transposed copy)
+#pragma unroll
+              for (int j = 0; j < BNL / 64; ++j)
+                load(&tmB, b_dst + j * 8192, n0 + 64 * j, p.S - 1 - ks, p.Rf - 1 - kr, kc * BK);
+              break;
+            case B_WG_DY:  // dy [pixels][K] MN-major (swapped weight gradient)
+#pragma unroll
+              for (int j = 0; j < BNL / 64; ++j) load(&tmB, b_dst + j * 8192, n0 + 64 * j, pw, ph, pn);
+              break;
+            default: {  // B_WG_X
+              const int hin = ph * p.stride - p.pad_h, win = pw * p.stride - p.pad_w;
+#pragma unroll
+              for (int j = 0; j < BNL / 64; ++j) load(&tmB, b_dst + j * 8192, xci[j], win + xss[j], hin + xrr[j], pn);
+              break;
             }
-            break;
+          }
+        }
+        __syncwarp();
+        if (p.a_mode == A_CONV) {
+          if (++kc == p.cblk) {
+            kc = 0;
+            if (HALO || ++ks == p.S) {
+              ks = 0;
+              ++kr;
+            }
+          }
+        } else if (wg) {
+          pw += p.tw;
+          if (pw >= p.Q) {
+            pw = 0;
+            ph += p.th;
+            if (ph >= p.P) {
+              ph = 0;
+              pn += p.tn;
+            }
           }
         }
         if (++stage == STAGES) {
@@ -512,11 +558,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
       }
     }
-  } else if (threadIdx.x == 32 && leader) {
+  } else if (warp == 1 && leader) {
     // ------------------------------------------------------------ MMA issuer (leader CTA)
-    const int a_mn = (p.a_mode == A_MNMAJ || p.a_mode == A_WG_DY) ? 1 : 0;
+    // warp-wide bookkeeping (uniform registers), lane 0 issues the MMAs and commits
+    const int a_mn = (p.a_mode == A_MNMAJ || p.a_mode == A_WG_DY || p.a_mode == A_WG_X) ? 1 : 0;
     const int b_mn = (p.b_mode != B_KMAJ) ? 1 : 0;
     const uint32_t idesc = idesc_bf16_f32(BM * CG, BN / Cfg::NH, a_mn, b_mn);
+    const bool issuer = lane == 0;
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -544,7 +592,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               // way), so a row-shifted start is consistent as is (tests/test_gemm_gpu.py::halo)
               const uint64_t bdesc = smem_desc_sw128(b_addr + ss * Cfg::B_SUB + j * 32, 16, 1024);
               const uint32_t accum = (kb > wk.kb0 || ss > 0 || j > 0) ? 1u : 0u;
-              if constexpr (CG == 2)
+              if (!issuer) {
+              } else if constexpr (CG == 2)
                 tc_mma_bf16_2sm(d_tmem, adesc, bdesc, idesc, accum);
               else
                 tc_mma_bf16(d_tmem, adesc, bdesc, idesc, accum);
@@ -557,7 +606,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               const uint64_t adesc = smem_desc_sw128(a_addr + j * 32, 16, 1024);
               const uint64_t bdesc = smem_desc_sw128(b_addr + h * Cfg::B_HALF + j * 32, 16, 1024);
               const uint32_t accum = (kb > wk.kb0 || j > 0) ? 1u : 0u;
-              if constexpr (CG == 2)
+              if (!issuer) {
+              } else if constexpr (CG == 2)
                 tc_mma_bf16_2sm(d_tmem + h * (BN / 2), adesc, bdesc, idesc, accum);
               else
                 tc_mma_bf16(d_tmem + h * (BN / 2), adesc, bdesc, idesc, accum);
@@ -570,24 +620,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const uint64_t bdesc = b_mn ? smem_desc_sw128(b_addr + j * 2048, 8192, 1024)
                                       : smem_desc_sw128(b_addr + j * 32, 16, 1024);
           const uint32_t accum = (kb > wk.kb0 || j > 0) ? 1u : 0u;
-          if constexpr (CG == 2)
+          if (!issuer) {
+          } else if constexpr (CG == 2)
             tc_mma_bf16_2sm(d_tmem, adesc, bdesc, idesc, accum);
           else
             tc_mma_bf16(d_tmem, adesc, bdesc, idesc, accum);
         }
-        if constexpr (CG == 2)
+        if (!issuer) {
+        } else if constexpr (CG == 2)
           tc_commit_2sm_mc(&empty[stage]);
         else
           tc_commit(&empty[stage]);
+        __syncwarp();
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
         }
       }
-      if constexpr (CG == 2)
+      if (!issuer) {
+      } else if constexpr (CG == 2)
         tc_commit_2sm_mc(&tfull[acc]);
       else
         tc_commit(&tfull[acc]);
+      __syncwarp();
       if (++acc == Cfg::NACC) {
         acc = 0;
         acc_phase ^= 1;
@@ -649,7 +704,30 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         tmem_ld_wait_dep(v);
         const bool use_pre = rpre_on && row < p.M && n + 32 <= p.N;
-        if (p.d_tma == 2) {
+        if (p.d_tma == 3) {
+          // transposed fp32 reduce (swapped weight gradient: D rows are the contiguous dimension of the
+          // output): stage [16 columns][32 rows] with lane = row, one TMA reduce-add per 16 columns
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            uint8_t* buf = ebuf + (chunk_seq & 1) * EPI_STAGE_BYTES;
+            if (chunk_seq >= 2) {
+              if (lane == 0) bulk_wait_read<1>();
+              __syncwarp();
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(smem_u32(buf + i * 128 + lane * 4)),
+                           "f"(__uint_as_float(v[hh * 16 + i]) * p.alpha)
+                           : "memory");
+            fence_async_shared();
+            __syncwarp();
+            if (lane == 0 && row0 < p.M) {
+              tma_reduce_add_4d(&tmD, buf, row0, n + 16 * hh, wk.z1, wk.z2);
+              bulk_commit();
+            }
+            ++chunk_seq;
+          }
+        } else if (p.d_tma == 2) {
           float f[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * p.alpha;
@@ -1384,6 +1462,66 @@ int tc_conv_dgrad(const DpConvArgs* a, cudaStream_t st, int64_t* query = nullptr
   return launch_bn(bn, cg, ma, mb, p, p.M, p.N, 1, 1, st, a->workspace, a->workspace_bytes);
 }
 
+// Swapped weight gradient: dW^T[(r,s,c)][k] = sum_pixels x_window[p][(r,s,c)] * dy[p][k], i.e. M = R*S*C
+// (shifted input windows, MN-major A) and N = K (dy, MN-major B), so the long dimension takes the
+// 256-row CTA-pair tiles and the output-channel count (a multiple of 128) the tile width; the fp32
+// result is added into dW[k][(r,s,c)] by transposed TMA reduce boxes. The classic orientation
+// (M = K) leaves K = 640 / 1280 layers on single CTAs or 17%-padded pairs.
+static int conv_wgrad_swapped(const DpConvArgs* a, TcParams& p, cudaStream_t st) {
+  const int Ntot = a->R * a->S * a->C;
+  const int bn = (a->K % 256 == 0) ? 256 : 128;
+  const int cg = 2;
+  p.M = Ntot;
+  p.N = a->K;
+  p.num_kb = (a->N * a->P * a->Q + BK - 1) / BK;
+  p.tiles_m = (Ntot + BM * cg - 1) / (BM * cg);
+  p.tiles_n = a->K / bn;
+  p.batch1 = 1;
+  p.nbatch = 1;
+  p.a_mode = A_WG_X;
+  p.b_mode = B_WG_DY;
+  p.P = a->P;
+  p.Q = a->Q;
+  p.stride = a->stride;
+  p.pad_h = a->pad_h;
+  p.pad_w = a->pad_w;
+  p.S = a->S;
+  p.C = a->C;
+  choose_split(p, a->split_k, true);
+  fill_epilogue(p, a->y, DP_F32, Ntot, 0, 0, DP_OUT_ATOMIC_ADD, nullptr, nullptr, 0, 0, 0, a->alpha);
+  CUtensorMap ma, mb, md;
+  const uint32_t ones[4] = {1, 1, 1, 1};
+  {  // x windows as the A operand (the B_WG_X map)
+    const uint64_t d[4] = {(uint64_t)a->C, (uint64_t)a->W, (uint64_t)a->H, (uint64_t)a->N};
+    const int64_t s[3] = {a->C, (int64_t)a->W * a->C, (int64_t)a->H * a->W * a->C};
+    const uint32_t box[4] = {64, (uint32_t)(p.tw * a->stride), (uint32_t)(p.th * a->stride), (uint32_t)p.tn};
+    const uint32_t es[4] = {1, (uint32_t)a->stride, (uint32_t)a->stride, 1};
+    if (int e = make_map(&ma, a->x, d, s, box, es)) return e;
+  }
+  {  // dy [pixels][K] as the B operand
+    const uint64_t d[4] = {(uint64_t)a->K, (uint64_t)a->Q, (uint64_t)a->P, (uint64_t)a->N};
+    const int64_t s[3] = {a->K, (int64_t)a->Q * a->K, (int64_t)a->P * a->Q * a->K};
+    const uint32_t box[4] = {64, (uint32_t)p.tw, (uint32_t)p.th, (uint32_t)p.tn};
+    if (int e = make_map(&mb, a->w, d, s, box, ones)) return e;
+  }
+  {  // dW [K][R*S*C] fp32: (m = r,s,c contiguous, n = k) boxes of 32 m x 16 n
+    const uint64_t d[4] = {(uint64_t)Ntot, (uint64_t)a->K, 1, 1};
+    const int64_t s[3] = {Ntot, (int64_t)Ntot * a->K, (int64_t)Ntot * a->K};
+    const uint32_t box[4] = {32, 16, 1, 1};
+    if (int e = make_map(&md, a->y, d, s, box, ones, CU_TENSOR_MAP_SWIZZLE_NONE, 4)) return e;
+    p.d_tma = 3;
+  }
+  return bn == 256 ? launch_tc<256, 2>(ma, mb, md, p, kNumSMs, st) : launch_tc<128, 2>(ma, mb, md, p, kNumSMs, st);
+}
+
+static bool wgrad_swap_enabled() {
+  static const int v = [] {
+    const char* e = getenv("DP_WGRAD_SWAP");  // experiments: 0 = classic orientation only
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 // dW[k][r][s][c] += sum_{n,p,q} dy[n][p][q][k] * x[n][p*stride+r-pad][q*stride+s-pad][c]
 int tc_conv_wgrad(const DpConvArgs* a, cudaStream_t st) {
   if (a->C % 64 || a->K % 64) {
@@ -1396,6 +1534,9 @@ int tc_conv_wgrad(const DpConvArgs* a, cudaStream_t st) {
     return DP_ERR_UNSUPPORTED;
   }
   const int Ntot = a->R * a->S * a->C;
+  if (wgrad_swap_enabled() && a->K % 128 == 0 && Ntot >= 256 &&
+      reinterpret_cast<uintptr_t>(a->y) % 16 == 0 && (Ntot * 4) % 16 == 0)
+    return conv_wgrad_swapped(a, p, st);
   const int bn = pick_bn(Ntot, true);
   const int cg = decide_cg(a->K, bn, true, a->N * a->P * a->Q);
   p.M = a->K;

@@ -117,6 +117,10 @@ def _conv_ref(x, w, stride, pad, out_hw):
     (4, 32, 320, 4, 1, (1, 1)),      # U-Net conv_out (4 filters)
     (2, 64, 8, 128, 1, (1, 1)),      # VAE conv_in (RGB padded to 8)
     (2, 16, 192, 320, 1, (1, 1)),    # C not a multiple of 64
+    (4, 16, 640, 640, 1, (1, 1)),    # swapped weight gradient (K % 128 == 0): U-Net 16x16 level
+    (3, 8, 1280, 1280, 1, (1, 1)),   # 8x8 level, pairs of BN 256
+    (5, 4, 2560, 1280, 1, (1, 1)),   # 4x4 level, 2560-channel concat input
+    (2, 16, 640, 640, 2, (1, 1)),    # strided downsample (swapped wgrad with element strides)
 ])
 def test_conv_implicit(N, H, C, K, stride, pad):
     ops = _ops()
