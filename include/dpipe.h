@@ -267,6 +267,12 @@ int dp_softmax_fwd(int dtype, const float* S, void* P, int64_t rows, int cols, i
 int dp_softmax_bwd(int dtype, const void* P, const float* dP, void* dS, int64_t rows, int cols,
                    int ld, float scale, dp_stream_t stream);
 
+/* Launch timing (bench roofline pass): a pool of >= n CUDA events, recorded by index on a stream;
+   elapsed milliseconds between two recorded events (-1 on error). */
+int dp_timing_events(int n);
+int dp_timing_record(int i, dp_stream_t stream);
+float dp_timing_elapsed(int i, int j);
+
 const char* dp_last_error(void);
 int dp_version(void);
 

@@ -129,10 +129,14 @@ _SIGNATURES = {
     "dp_rms_norm_fwd": [c_int, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_float, c_void_p],
     "dp_softmax_fwd": [c_int, c_void_p, c_void_p, c_i64, c_int, c_int, c_float, c_int, c_int, c_void_p],
     "dp_softmax_bwd": [c_int, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_int, c_float, c_void_p],
+    # timing.cu
+    "dp_timing_events": [c_int],
+    "dp_timing_record": [c_int, c_void_p],
+    "dp_timing_elapsed": [c_int, c_int],
     "dp_last_error": [],
     "dp_version": [],
 }
-_RESTYPES = {"dp_last_error": ctypes.c_char_p, "dp_group_norm_workspace": ctypes.c_size_t,
+_RESTYPES = {"dp_last_error": ctypes.c_char_p, "dp_timing_elapsed": c_float, "dp_group_norm_workspace": ctypes.c_size_t,
              "dp_gemm_workspace": c_i64, "dp_flash_attn_bwd_workspace": c_i64, "dp_conv_fwd_workspace": c_i64, "dp_conv_dgrad_workspace": c_i64}
 
 _lib = None

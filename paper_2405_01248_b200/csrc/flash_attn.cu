@@ -404,10 +404,11 @@ struct BwdParams {
 };
 
 // One CTA = one 128-key tile of one (batch, head); thread t owns key row t (S^T, dP^T rows).
-// Per 128-query tile: S^T = K Q^T, dP^T = V dO^T (TMEM); P^T = exp2(S^T*sl - lse),
-// dS^T = P^T (dP^T - D) -> shared (bf16, K-major over queries); dV += P^T dO, dK += dS^T Q
-// (TMEM accumulators across query tiles), dQ_i = dS K (TMEM) -> fp32 atomics into dq_acc.
-constexpr uint32_t BWD_SMEM_TILES = 10;  // K, V, Q[2], dO[2], P^T (2), dS^T (2)
+// Per 128-query tile: S^T = K Q^T, dP^T = V dO^T (TMEM); P^T = exp2(S^T*sl - lse) -> TMEM (bf16,
+// the A operand of dV += P^T dO), dS^T = P^T (dP^T - D) -> shared (bf16, K-major over queries);
+// dK += dS^T Q (TMEM accumulators across query tiles), dQ_i = dS K (TMEM) -> staged, TMA reduce-add.
+constexpr uint32_t BWD_SMEM_TILES = 10;  // K, V, Q[3], dO[3], dS^T (2)
+constexpr int NQB = 3;                   // Q / dO buffers: tile li+1 is loaded a full tile ahead
 
 __global__ void __launch_bounds__(256, 1)
     fa_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -421,10 +422,9 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sK = smem;
   uint8_t* sV = sK + TILE_BYTES;
-  uint8_t* sQ = sV + TILE_BYTES;        // [2]
-  uint8_t* sDO = sQ + 2 * TILE_BYTES;   // [2]
-  uint8_t* sPT = sDO + 2 * TILE_BYTES;  // 2 blocks (queries 0-63, 64-127)
-  uint8_t* sDST = sPT + 2 * TILE_BYTES; // 2 blocks
+  uint8_t* sQ = sV + TILE_BYTES;          // [NQB]
+  uint8_t* sDO = sQ + NQB * TILE_BYTES;   // [NQB]
+  uint8_t* sDST = sDO + NQB * TILE_BYTES; // 2 blocks (queries 0-63, 64-127)
   // dQ_i staging (128 query rows x 64 fp32, 256-byte rows): one TMA reduce-add per query tile
   // instead of 2048 per-thread vector atomics (those saturated the LSU queue, lg_throttle)
   float* sDQ = reinterpret_cast<float*>(sDST + 2 * TILE_BYTES);
@@ -432,10 +432,10 @@ __global__ void __launch_bounds__(256, 1)
   float* sD = sLse + 256;                                          // [2][128]
   uint64_t* bar = reinterpret_cast<uint64_t*>(sD + 256);
   uint64_t* bar_kv = bar;
-  uint64_t* bar_q = bar + 1;   // [2]
-  uint64_t* bar_sp = bar + 3;
-  uint64_t* bar_acc = bar + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 5);
+  uint64_t* bar_q = bar + 1;   // [NQB]
+  uint64_t* bar_sp = bar + 1 + NQB;
+  uint64_t* bar_acc = bar + 2 + NQB;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 3 + NQB);
 
   // 8 warps: warps w and w+4 share TMEM lanes 32*(w%4).. (key rows) and split the 128 query
   // columns of every S^T / dP^T tile (and the 64 dQ / dK / dV columns) between them
@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(256, 1)
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     tma_prefetch(&tmDO);
-    for (int i = 0; i < 5; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < 3 + NQB; ++i) mbar_init(&bar[i], 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc<512>(tmem_slot);
@@ -466,6 +466,7 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_st = tmem, t_dpt = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 320, t_dq = tmem + 384;
+  const uint32_t t_p = tmem + 448;  // P^T of the tile in flight, bf16 pairs (64 columns = 128 queries)
   const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
 
   auto load_q = [&](int i, int buf) {
@@ -477,8 +478,7 @@ __global__ void __launch_bounds__(256, 1)
     mbar_expect_tx(bar_kv, 2 * TILE_BYTES);
     tma_load_4d(&tmK, bar_kv, sK, 0, k0, h, b);
     tma_load_4d(&tmV, bar_kv, sV, 0, k0, h, b);
-    load_q(i0, 0);
-    if (i0 + 1 < i1) load_q(i0 + 1, 1);
+    for (int t = 0; t < NQB && i0 + t < i1; ++t) load_q(i0 + t, t);
   }
   // lse / D of the first query tile (rows >= N: lse = +inf -> P = 0)
   auto load_rows = [&](int i, int buf) {
@@ -489,17 +489,21 @@ __global__ void __launch_bounds__(256, 1)
   };
   load_rows(i0, 0);
   const uint32_t id_sq = idesc_bf16_f32(BKV, BQ, 0, 0);  // S^T / dP^T: M=keys, N=queries, K=64
-  const uint32_t id_acc = idesc_bf16_f32(BKV, HD, 0, 1); // dV / dK: M=keys, N=64, K=queries
+  const uint32_t id_acc = idesc_bf16_f32(BKV, HD, 0, 1); // dV / dK: M=keys, N=64, K=queries (dV: A in TMEM)
   const uint32_t id_dq = idesc_bf16_f32(BQ, HD, 1, 1);   // dQ: M=queries (A MN-major), N=64
   const bool key_valid = k0 + row < p.Nk;
 
-  // S^T / dP^T of query tile i: issued by thread 0 right after tile i-1's accumulator MMAs, so
-  // the tensor pipe computes them while the warps drain tile i-1's dQ (in-order MMA pipe: they
-  // complete after the dV/dK/dQ MMAs that still read P^T / dS^T from shared memory)
+  // Pipeline (one issuing thread, in-order tensor pipe): at the end of tile li's softmax thread 0
+  // issues S^T / dP^T of tile li+1 FIRST and then tile li's accumulator MMAs (dV, dK += ..., dQ_li),
+  // so the next softmax starts after 512 MMA cycles and runs while the accumulators (768 cycles)
+  // drain; it waits for them only before it overwrites P^T / dS^T in shared memory, and then drains
+  // dQ_li from TMEM (a tile late). The previous order (accumulators, then the next S^T / dP^T, and
+  // every warp waiting for the accumulators before the next tile) left the softmax warps idle a
+  // third of the kernel (ncu: the bar_acc wait was the top stall).
   auto issue_sdp = [&](int li) {  // li: tile index local to this CTA
-    const int qb = li & 1;
+    const int qb = li % NQB;
     if (li == 0) mbar_wait(bar_kv, 0);
-    mbar_wait(&bar_q[qb], (li >> 1) & 1);
+    mbar_wait(&bar_q[qb], (li / NQB) & 1);
     tc_fence_after();
     const uint32_t ka = smem_u32(sK), va = smem_u32(sV);
     const uint32_t qa = smem_u32(sQ + qb * TILE_BYTES), da = smem_u32(sDO + qb * TILE_BYTES);
@@ -512,22 +516,81 @@ __global__ void __launch_bounds__(256, 1)
     }
     tc_commit(bar_sp);
   };
+  auto issue_acc = [&](int li) {
+    const int qb = li % NQB;
+    const uint32_t dsa = smem_u32(sDST), ka = smem_u32(sK);
+    const uint32_t qa = smem_u32(sQ + qb * TILE_BYTES), da = smem_u32(sDO + qb * TILE_BYTES);
+#pragma unroll
+    for (int k = 0; k < BQ / 16; ++k) {
+      const uint32_t aoff = (k >> 2) * TILE_BYTES + (k & 3) * 32;  // K-major over queries
+      // dV += P^T dO    (A = P^T from TMEM: 16 queries = 8 columns; B(n=d, k=q) = dO[q][d]: MN-major)
+      tc_mma_bf16_ts(t_dv, t_p + k * 8, smem_desc_sw128(da + k * 2048, 8192, 1024), id_acc,
+                     (li > 0 || k > 0) ? 1u : 0u);
+      // dK += dS^T Q    (B(n=d, k=q) = Q[q][d]: MN-major)
+      tc_mma_bf16(t_dk, smem_desc_sw128(dsa + aoff, 16, 1024), smem_desc_sw128(qa + k * 2048, 8192, 1024),
+                  id_acc, (li > 0 || k > 0) ? 1u : 0u);
+    }
+#pragma unroll
+    for (int k = 0; k < BKV / 16; ++k) {
+      // dQ_i = dS K: A(m=q, k=key) = dS^T[key][q] (MN-major, 64-query chunks 16 KB apart),
+      //              B(n=d, k=key) = K[key][d] (MN-major)
+      tc_mma_bf16(t_dq, smem_desc_sw128(dsa + k * 2048, TILE_BYTES, 1024),
+                  smem_desc_sw128(ka + k * 2048, 8192, 1024), id_dq, k > 0 ? 1u : 0u);
+    }
+    tc_commit(bar_acc);
+  };
+  // dQ of query tile `i` (TMEM, complete) -> the staging buffer: half-buffer `half` holds 128 rows x
+  // 32 fp32 (128 B) in the SWIZZLE_128B layout of tmDQ's box (16-byte chunk k of row r at k ^ (r & 7))
+  auto drain_dq = [&]() {
+    uint32_t v[32];
+    tmem_ld_32x32(t_dq + lane_off + half * 32, v);
+    tmem_ld_wait();
+    if (p.dq_direct) {
+      // bf16 tile of 128-byte rows (64 dims): this half's 4 chunks, SWIZZLE_128B like tmQ
+      uint8_t* dst = reinterpret_cast<uint8_t*>(sDQ) + row * 128;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint4 u;
+        u.x = pack_bf16x2(p.scale * __uint_as_float(v[k * 8 + 0]), p.scale * __uint_as_float(v[k * 8 + 1]));
+        u.y = pack_bf16x2(p.scale * __uint_as_float(v[k * 8 + 2]), p.scale * __uint_as_float(v[k * 8 + 3]));
+        u.z = pack_bf16x2(p.scale * __uint_as_float(v[k * 8 + 4]), p.scale * __uint_as_float(v[k * 8 + 5]));
+        u.w = pack_bf16x2(p.scale * __uint_as_float(v[k * 8 + 6]), p.scale * __uint_as_float(v[k * 8 + 7]));
+        *reinterpret_cast<uint4*>(dst + (((half * 4 + k) ^ (row & 7)) * 16)) = u;
+      }
+    } else {
+      uint8_t* dst = reinterpret_cast<uint8_t*>(sDQ) + half * (BQ * 128) + row * 128;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        *reinterpret_cast<float4*>(dst + ((k ^ (row & 7)) * 16)) =
+            make_float4(__uint_as_float(v[k * 4]), __uint_as_float(v[k * 4 + 1]), __uint_as_float(v[k * 4 + 2]),
+                        __uint_as_float(v[k * 4 + 3]));
+    }
+  };
+  auto emit_dq = [&](int i) {  // thread 0: the staged dQ of query tile i -> global
+    if (p.dq_direct) {
+      tma_store_4d(&tmDQ, sDQ, 0, i * BQ, h, b);
+    } else {
+      tma_reduce_add_4d(&tmDQ, sDQ, h * HD, i * BQ, b, 0);
+      tma_reduce_add_4d(&tmDQ, reinterpret_cast<uint8_t*>(sDQ) + BQ * 128, h * HD + 32, i * BQ, b, 0);
+    }
+    bulk_commit();
+  };
   if (tid == 0) issue_sdp(0);
+  // lse / D rows of the tile after next, loaded a tile ahead of their shared-memory store so the
+  // global load latency is not exposed inside the loop
+  float nxt_lse = INFINITY, nxt_d = 0.f;
+  auto fetch_rows = [&](int i) {
+    if (half || i >= i1) return;
+    const int q = i * BQ + row;
+    nxt_lse = q < p.N ? p.lse[bh * p.N + q] : INFINITY;
+    nxt_d = q < p.N ? p.Dv[bh * p.N + q] : 0.f;
+  };
+  fetch_rows(i0 + 1);
+  __syncthreads();  // sLse/sD of the first tile
 
   for (int i = i0; i < i1; ++i) {
     const int li = i - i0;
     const int qb = li & 1;
-    __syncthreads();  // sLse/sD of tile i visible; previous tile's smem/TMEM consumers done
-    if (tid == 0 && li > 0) {  // dQ of the previous query tile, staged by every thread
-      if (p.dq_direct) {
-        tma_store_4d(&tmDQ, sDQ, 0, (i - 1) * BQ, h, b);
-      } else {
-        tma_reduce_add_4d(&tmDQ, sDQ, h * HD, (i - 1) * BQ, b, 0);
-        tma_reduce_add_4d(&tmDQ, reinterpret_cast<uint8_t*>(sDQ) + BQ * 128, h * HD + 32, (i - 1) * BQ, b, 0);
-      }
-      bulk_commit();
-    }
-    if (i + 1 < i1) load_rows(i + 1, qb ^ 1);
     mbar_wait(bar_sp, li & 1);
     tc_fence_after();
     const float* lse = sLse + qb * 128;
@@ -539,108 +602,79 @@ __global__ void __launch_bounds__(256, 1)
       tmem_ld_32x32(t_dpt + lane_off + (half * 2 + u) * 32, dva[u]);
     }
     tmem_ld_wait();
+    // P^T and dS^T of this thread's 64 queries, packed to bf16 in registers until the previous
+    // tile's accumulator MMAs have released the shared-memory operands
+    uint32_t ppk[2][16], dpk[2][16];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int c = half * 2 + u;
-      const uint32_t (&sv)[32] = sva[u];
-      const uint32_t (&dv)[32] = dva[u];
-      float pt[32], dst[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
+      for (int j = 0; j < 32; j += 2) {
         const int q = c * 32 + j;
-        const float pp = key_valid ? ex2(fmaf(__uint_as_float(sv[j]), p.scale_log2, -lse[q])) : 0.f;
-        pt[j] = pp;
-        dst[j] = pp * (__uint_as_float(dv[j]) - Dq[q]);
+        const float2 x = __ffma2_rn(make_float2(__uint_as_float(sva[u][j]), __uint_as_float(sva[u][j + 1])),
+                                    make_float2(p.scale_log2, p.scale_log2), make_float2(-lse[q], -lse[q + 1]));
+        const float p0 = key_valid ? ex2(x.x) : 0.f, p1 = key_valid ? ex2(x.y) : 0.f;
+        const float2 ds = __fmul2_rn(make_float2(p0, p1),
+                                     __fadd2_rn(make_float2(__uint_as_float(dva[u][j]), __uint_as_float(dva[u][j + 1])),
+                                                make_float2(-Dq[q], -Dq[q + 1])));
+        ppk[u][j / 2] = pack_bf16x2(p0, p1);
+        dpk[u][j / 2] = pack_bf16x2(ds.x, ds.y);
       }
+    }
+    if (li > 0) {
+      mbar_wait(bar_acc, (li - 1) & 1);  // tile li-1's dV / dK / dQ MMAs done (they read P^T / sDST)
+      tc_fence_after();
+      if (tid == 0) {
+        // the Q/dO buffer of tile li-1 is free: tile li+2 goes there (tile li+1 arrived a tile ago)
+        if (i + 2 < i1) load_q(i + 2, (li + 2) % NQB);
+        bulk_wait_read<0>();  // the staged dQ of tile li-2 has been read
+      }
+      __syncthreads();
+      drain_dq();
+    }
+    // P^T -> TMEM (this thread's key row, its 64 queries = 32 columns), dS^T -> shared memory
+    tmem_st_32x32(t_p + lane_off + half * 32, *reinterpret_cast<uint32_t(*)[32]>(&ppk[0][0]));
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int c = half * 2 + u;
       const int blk = c >> 1;
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
         const int chunk = (c & 1) * 4 + q4;
         const int off = blk * TILE_BYTES + row * 128 + ((chunk ^ (row & 7)) * 16);
-        uint4 u;
-        u.x = pack_bf16x2(pt[q4 * 8 + 0], pt[q4 * 8 + 1]);
-        u.y = pack_bf16x2(pt[q4 * 8 + 2], pt[q4 * 8 + 3]);
-        u.z = pack_bf16x2(pt[q4 * 8 + 4], pt[q4 * 8 + 5]);
-        u.w = pack_bf16x2(pt[q4 * 8 + 6], pt[q4 * 8 + 7]);
-        *reinterpret_cast<uint4*>(sPT + off) = u;
-        u.x = pack_bf16x2(dst[q4 * 8 + 0], dst[q4 * 8 + 1]);
-        u.y = pack_bf16x2(dst[q4 * 8 + 2], dst[q4 * 8 + 3]);
-        u.z = pack_bf16x2(dst[q4 * 8 + 4], dst[q4 * 8 + 5]);
-        u.w = pack_bf16x2(dst[q4 * 8 + 6], dst[q4 * 8 + 7]);
-        *reinterpret_cast<uint4*>(sDST + off) = u;
+        *reinterpret_cast<uint4*>(sDST + off) =
+            make_uint4(dpk[u][q4 * 4], dpk[u][q4 * 4 + 1], dpk[u][q4 * 4 + 2], dpk[u][q4 * 4 + 3]);
       }
     }
+    tmem_st_wait();
+    if (!half && i + 1 < i1) {  // rows of tile i+1 (loaded a tile ago) -> the other buffer
+      sLse[(qb ^ 1) * 128 + row] = nxt_lse;
+      sD[(qb ^ 1) * 128 + row] = nxt_d;
+    }
+    fetch_rows(i + 2);
     fence_async_shared();
     tc_fence_before();
-    if (tid == 0) bulk_wait_read<0>();  // the staging buffer is free once the reduce has read it
-    __syncthreads();
+    __syncthreads();  // P^T / dS^T (and dQ of tile li-1) staged; S^T / dP^T of tile li read
     if (tid == 0) {
       tc_fence_after();
-      const uint32_t pta = smem_u32(sPT), dsa = smem_u32(sDST), ka = smem_u32(sK);
-      const uint32_t qa = smem_u32(sQ + qb * TILE_BYTES), da = smem_u32(sDO + qb * TILE_BYTES);
-#pragma unroll
-      for (int k = 0; k < BQ / 16; ++k) {
-        const uint32_t aoff = (k >> 2) * TILE_BYTES + (k & 3) * 32;  // K-major over queries
-        // dV += P^T dO    (B(n=d, k=q) = dO[q][d]: MN-major)
-        tc_mma_bf16(t_dv, smem_desc_sw128(pta + aoff, 16, 1024), smem_desc_sw128(da + k * 2048, 8192, 1024),
-                    id_acc, (li > 0 || k > 0) ? 1u : 0u);
-        // dK += dS^T Q    (B(n=d, k=q) = Q[q][d]: MN-major)
-        tc_mma_bf16(t_dk, smem_desc_sw128(dsa + aoff, 16, 1024), smem_desc_sw128(qa + k * 2048, 8192, 1024),
-                    id_acc, (li > 0 || k > 0) ? 1u : 0u);
-      }
-#pragma unroll
-      for (int k = 0; k < BKV / 16; ++k) {
-        // dQ_i = dS K: A(m=q, k=key) = dS^T[key][q] (MN-major, 64-query chunks 16 KB apart),
-        //              B(n=d, k=key) = K[key][d] (MN-major)
-        tc_mma_bf16(t_dq, smem_desc_sw128(dsa + k * 2048, TILE_BYTES, 1024),
-                    smem_desc_sw128(ka + k * 2048, 8192, 1024), id_dq, k > 0 ? 1u : 0u);
-      }
-      tc_commit(bar_acc);
+      if (li > 0) emit_dq(i - 1);
       if (i + 1 < i1) issue_sdp(li + 1);
+      issue_acc(li);
     }
-    mbar_wait(bar_acc, li & 1);
-    tc_fence_after();
-    if (tid == 0 && i + 2 < i1) load_q(i + 2, qb);  // Q/dO buffer qb is free again
-    // dQ rows of this query tile -> staging: half-buffer `half` holds 128 rows x 32 fp32 (128 B) in
-    // the SWIZZLE_128B layout of tmDQ's box (16-byte chunk k of row r at k ^ (r & 7): conflict-free)
-    {
-      uint32_t v[32];
-      tmem_ld_32x32(t_dq + lane_off + half * 32, v);
-      tmem_ld_wait();
-      if (p.dq_direct) {
-        // bf16 tile of 128-byte rows (64 dims): this half's 4 chunks, SWIZZLE_128B like tmQ
-        uint8_t* dst = reinterpret_cast<uint8_t*>(sDQ) + row * 128;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          uint4 u;
-          u.x = pack_bf16x2(p.scale * __uint_as_float(v[k * 8 + 0]), p.scale * __uint_as_float(v[k * 8 + 1]));
-          u.y = pack_bf16x2(p.scale * __uint_as_float(v[k * 8 + 2]), p.scale * __uint_as_float(v[k * 8 + 3]));
-          u.z = pack_bf16x2(p.scale * __uint_as_float(v[k * 8 + 4]), p.scale * __uint_as_float(v[k * 8 + 5]));
-          u.w = pack_bf16x2(p.scale * __uint_as_float(v[k * 8 + 6]), p.scale * __uint_as_float(v[k * 8 + 7]));
-          *reinterpret_cast<uint4*>(dst + (((half * 4 + k) ^ (row & 7)) * 16)) = u;
-        }
-      } else {
-        uint8_t* dst = reinterpret_cast<uint8_t*>(sDQ) + half * (BQ * 128) + row * 128;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          *reinterpret_cast<float4*>(dst + ((k ^ (row & 7)) * 16)) =
-              make_float4(__uint_as_float(v[k * 4]), __uint_as_float(v[k * 4 + 1]), __uint_as_float(v[k * 4 + 2]),
-                          __uint_as_float(v[k * 4 + 3]));
-      }
-      fence_async_shared();
-    }
-    tc_fence_before();
   }
-  __syncthreads();
-  if (tid == 0 && i1 > i0) {
-    if (p.dq_direct) {
-      tma_store_4d(&tmDQ, sDQ, 0, (i1 - 1) * BQ, h, b);
-    } else {
-      tma_reduce_add_4d(&tmDQ, sDQ, h * HD, (i1 - 1) * BQ, b, 0);
-      tma_reduce_add_4d(&tmDQ, reinterpret_cast<uint8_t*>(sDQ) + BQ * 128, h * HD + 32, (i1 - 1) * BQ, b, 0);
+  // the last tile's accumulators, then its dQ
+  if (i1 > i0) {
+    mbar_wait(bar_acc, (i1 - 1 - i0) & 1);
+    tc_fence_after();
+    if (tid == 0) bulk_wait_read<0>();
+    __syncthreads();
+    drain_dq();
+    fence_async_shared();
+    __syncthreads();
+    if (tid == 0) {
+      emit_dq(i1 - 1);
+      bulk_wait_all();
     }
-    bulk_commit();
-    bulk_wait_all();
   }
   tc_fence_after();
   if (p.qsplit > 1) {

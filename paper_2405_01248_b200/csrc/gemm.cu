@@ -1127,19 +1127,27 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// fraction of the SMs below which a bf16 launch is split (DP_SPLITK_FRAC, percent; experiments)
+// wave efficiency (percent) below which a bf16 launch is split (DP_SPLITK_FRAC; experiments)
 static int splitk_pct() {
   static const int v = [] {
     const char* e = getenv("DP_SPLITK_FRAC");
-    return e ? atoi(e) : 50;
+    return e ? atoi(e) : 75;
   }();
   return v;
 }
 
+// A bf16 STORE launch whose tiles fill their waves poorly (efficiency = tiles / (waves x tile slots),
+// e.g. 40 CTA-pair tiles of an 8x8-map conv on 74 pair slots: 54%) and whose K is long enough for the
+// fp32 stream-K pass plus the finish pass to pay: the whole-K tiles were leaving up to half the SMs
+// idle (previous rule: split only below half of the SMs).
 static int64_t splitk_bytes(const TcParams& p, int cg, int M, int N) {
   if (p.d_f32 || p.out_mode != DP_OUT_STORE || !p.vec_ok || (N % 8) || p.num_kb < 8) return 0;
-  const long long ctas = (long long)p.tiles_m * p.tiles_n * p.nbatch * cg;
-  if (ctas * 100 >= (long long)kNumSMs * splitk_pct()) return 0;
+  const long long units = (long long)p.tiles_m * p.tiles_n * p.nbatch;
+  const long long slots = kNumSMs / cg;
+  const long long waves = (units + slots - 1) / slots;
+  const bool under_half = units * cg * 100 < (long long)kNumSMs * 50;
+  const bool poor_waves = p.num_kb >= 16 && units * 100 < waves * slots * splitk_pct();
+  if (!under_half && !poor_waves) return 0;
   return 4LL * M * N * p.nbatch;
 }
 

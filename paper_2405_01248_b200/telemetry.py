@@ -22,20 +22,53 @@ SHAPES = False  # label GEMM launches by shape (tools/step_breakdown.py)
 _site = threading.local()
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+_cur_device = getattr(torch._C, "_cuda_getDevice", None)
+
+
+def _stream_ptr():
+    if _raw_stream is not None and _cur_device is not None:
+        return _raw_stream(_cur_device())
+    return torch.cuda.current_stream().cuda_stream
+
+
 class _Timer:
+    """Event pairs from libdpipe's native pool (dp_timing_record: one C call per record on the
+    launching stream; the torch Event path cost enough host time per record to make the bracketed
+    pass host-bound, so brackets measured launch latency rather than kernels)."""
+
     def __init__(self):
         self.active = False
         self.records = []
         self.depth = 0
-        self.pool = []  # pre-created timing events (event creation kept off the timed path)
+        self.next = 0
+        self.capacity = 0
+
+    @staticmethod
+    def _lib():
+        from . import _lib
+
+        return _lib.lib()  # the raw handle: called while the timer is still inactive
 
     def event(self):
-        return self.pool.pop() if self.pool else torch.cuda.Event(enable_timing=True)
+        i = self.next
+        if i >= self.capacity:
+            raise RuntimeError("telemetry: timing event pool exhausted (raise `reserve`)")
+        self.next += 1
+        return i
+
+    def record(self, i):
+        self.native.dp_timing_record(i, _stream_ptr())
 
     def start(self, reserve=0):
         self.records = []
-        if len(self.pool) < reserve:
-            self.pool.extend(torch.cuda.Event(enable_timing=True) for _ in range(reserve - len(self.pool)))
+        self.active = False
+        self.native = self._lib()
+        if reserve > self.capacity:
+            if self.native.dp_timing_events(reserve) != 0:
+                raise RuntimeError("dp_timing_events failed")
+            self.capacity = reserve
+        self.next = 0
         self.active = True
 
     def stop(self):
@@ -43,13 +76,13 @@ class _Timer:
         torch.cuda.synchronize()
         out = {}
         for fam, flops, a, b in self.records:
-            ms = a.elapsed_time(b)
+            ms = self.native.dp_timing_elapsed(a, b)
             f = out.setdefault(fam, dict(launches=0, flops=0.0, ms=0.0))
             f["launches"] += 1
             f["flops"] += flops
             f["ms"] += ms
-            self.pool.extend((a, b))
         self.records = []
+        self.next = 0
         return out
 
 
@@ -74,13 +107,13 @@ def timed(family, flops, fn, sub=None):
     fam = f"{family}.{s}" if s else family
     a = timer.event()
     b = timer.event()
-    a.record()
+    timer.record(a)
     timer.depth += 1
     try:
         r = fn()
     finally:
         timer.depth -= 1
-    b.record()
+    timer.record(b)
     timer.records.append((fam, flops, a, b))
     return r
 
