@@ -369,8 +369,16 @@ def main():
 
     # roofline pass (eager, after the timed ones): every libdpipe launch bracketed by CUDA events on
     # its stream (the events break programmatic dependent launch, so this pass runs slower), each step
-    # behind a 60 ms lead spin so the GPU never waits on the host inside a bracket
-    ms_k, kstats, _, _ = timed_steps(trainer, K, world, kernel_timer=True, lead_ms=60.0)
+    # behind a 60 ms lead spin so the GPU does not wait on the host inside a bracket
+    # The optimizer's overlap with the final backward is switched off for this pass only: the AdamW slices
+    # otherwise run concurrently on the optimizer stream and every bracketed GEMM of the last backward
+    # shares the SMs with them, so its interval is not that kernel's duration.
+    ovl = trainer.ex.overlap_sync
+    trainer.ex.overlap_sync = False
+    try:
+        ms_k, kstats, _, _ = timed_steps(trainer, K, world, kernel_timer=True, lead_ms=60.0)
+    finally:
+        trainer.ex.overlap_sync = ovl
 
     # measured bubble ratio: one traced iteration after the timed region, task intervals from
     # CUDA events on their streams, bubbles / ratio by the planner's own definitions
