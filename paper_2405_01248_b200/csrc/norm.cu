@@ -933,6 +933,233 @@ static GnGeom gn_geom_rt(int dtype, int N, int HW, int C, int G) {
   return dtype == DP_F32 ? gn_geom<4>(N, HW, C, G) : gn_geom<8>(N, HW, C, G);
 }
 
+// ------------------------------------------------------------------ LayerNorm, row groups (bf16)
+// LPR = 2^lpr_log2 lanes per row, so a warp normalises 32/LPR rows at once with NV 16-byte vectors per lane
+// (C = 320: 8 lanes x 5 vectors, 4 rows per warp; 640: 16 x 5; 1280: 32 x 5). The warp-per-row kernels
+// above kept one row in flight per warp and left most lanes of the second vector idle for C = 320;
+// with 4 rows' loads in flight per warp the U-Net LayerNorms run at a multiple of their bandwidth.
+// The raw bf16 rows stay in registers across both passes (no fp32 copy); shuffles stay inside a
+// row group (xor offsets < LPR).
+DP_DEV void unpack8(const uint4& u, float (&f)[8]) {
+  const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = __bfloat162float(b[i]);
+}
+DP_DEV float group_sum(float v, int lpr) {
+  for (int o = lpr >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+DP_DEV void load8f(const float* p, float (&f)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p + 4));
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256, 3)
+    lnq_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ gamma,
+                   const float* __restrict__ beta, __nv_bfloat16* __restrict__ y,
+                   float* __restrict__ mean_out, float* __restrict__ rstd_out, int64_t rows, int C,
+                   int lpr_log2, float eps) {
+  DP_PDL_ENTRY();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lpr = 1 << lpr_log2, sub = lane & (lpr - 1), rsub = lane >> lpr_log2;
+  const int rpw = 32 >> lpr_log2;
+  const int CV = C >> 3;
+  const float inv_c = 1.f / C;
+  for (int64_t r0 = ((int64_t)blockIdx.x * 8 + warp) * rpw; r0 < rows; r0 += (int64_t)gridDim.x * 8 * rpw) {
+    const int64_t row = r0 + rsub;
+    const bool rv = row < rows;
+    uint4 raw[NV];
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int cv = sub + k * lpr;
+      raw[k] = make_uint4(0, 0, 0, 0);
+      if (rv && cv < CV) raw[k] = *reinterpret_cast<const uint4*>(x + row * C + cv * 8);
+    }
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      float f[8];
+      unpack8(raw[k], f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += f[j];
+    }
+    const float mu = group_sum(s, lpr) * inv_c;
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      if (sub + k * lpr < CV) {
+        float f[8];
+        unpack8(raw[k], f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float d = f[j] - mu;
+          q = fmaf(d, d, q);
+        }
+      }
+    }
+    const float rs = rsqrtf(group_sum(q, lpr) * inv_c + eps);
+    if (rv && sub == 0) {
+      mean_out[row] = mu;
+      rstd_out[row] = rs;
+    }
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int cv = sub + k * lpr;
+      if (rv && cv < CV) {
+        float f[8], o[8];
+        unpack8(raw[k], f);
+        if (gamma) {
+          float g[8], b[8];
+          load8f(gamma + cv * 8, g);
+          load8f(beta + cv * 8, b);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] = fmaf((f[j] - mu) * rs, g[j], b[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] = (f[j] - mu) * rs;
+        }
+        st16(y + row * C + cv * 8, o);
+      }
+    }
+  }
+}
+
+template <int NV, bool PG>
+__global__ void __launch_bounds__(128, PG ? 2 : 4)
+    lnq_bwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ dy,
+                   const float* __restrict__ gamma, const float* __restrict__ mean,
+                   const float* __restrict__ rstd, __nv_bfloat16* __restrict__ dx, int64_t rows, int C,
+                   int lpr_log2, int accumulate, float* __restrict__ dgamma, float* __restrict__ dbeta) {
+  DP_PDL_ENTRY();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lpr = 1 << lpr_log2, sub = lane & (lpr - 1), rsub = lane >> lpr_log2;
+  const int rpw = 32 >> lpr_log2;
+  const int CV = C >> 3;
+  const float inv_c = 1.f / C;
+  float ag[PG ? NV : 1][8], ab[PG ? NV : 1][8];
+#pragma unroll
+  for (int k = 0; k < (PG ? NV : 1); ++k)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ag[k][j] = ab[k][j] = 0.f;
+  for (int64_t r0 = ((int64_t)blockIdx.x * 4 + warp) * rpw; r0 < rows; r0 += (int64_t)gridDim.x * 4 * rpw) {
+    const int64_t row = r0 + rsub;
+    const bool rv = row < rows;
+    uint4 rx[NV], rd[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int cv = sub + k * lpr;
+      rx[k] = rd[k] = make_uint4(0, 0, 0, 0);
+      if (rv && cv < CV) {
+        rx[k] = *reinterpret_cast<const uint4*>(x + row * C + cv * 8);
+        rd[k] = *reinterpret_cast<const uint4*>(dy + row * C + cv * 8);
+      }
+    }
+    const float mu = rv ? mean[row] : 0.f, rs = rv ? rstd[row] : 0.f;
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int cv = sub + k * lpr;
+      if (cv < CV) {
+        float fx[8], fd[8], g[8];
+        unpack8(rx[k], fx);
+        unpack8(rd[k], fd);
+        if (gamma) load8f(gamma + cv * 8, g);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float xh = (fx[j] - mu) * rs;
+          if constexpr (PG) {
+            ag[k][j] = fmaf(fd[j], xh, ag[k][j]);
+            ab[k][j] += fd[j];
+          }
+          const float d = gamma ? fd[j] * g[j] : fd[j];
+          s1 += d;
+          s2 = fmaf(d, xh, s2);
+        }
+      }
+    }
+    s1 = group_sum(s1, lpr) * inv_c;
+    s2 = group_sum(s2, lpr) * inv_c;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int cv = sub + k * lpr;
+      if (rv && cv < CV) {
+        float fx[8], fd[8], g[8], o[8];
+        unpack8(rx[k], fx);
+        unpack8(rd[k], fd);
+        if (gamma) load8f(gamma + cv * 8, g);
+        __nv_bfloat16* xo = dx + row * C + cv * 8;
+        float prev[8];
+        if (accumulate) ld16(xo, prev);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float xh = (fx[j] - mu) * rs;
+          const float d = gamma ? fd[j] * g[j] : fd[j];
+          o[j] = rs * (d - s1 - xh * s2);
+          if (accumulate) o[j] += prev[j];
+        }
+        st16(xo, o);
+      }
+    }
+  }
+  if constexpr (PG) {
+    // lanes with the same `sub` own the same channels: merge the row groups by shuffles, then one
+    // shared-memory add per channel per warp and one global atomic per channel per block
+    __shared__ float sg[2048], sb[2048];
+    for (int c = threadIdx.x; c < C; c += 128) sg[c] = sb[c] = 0.f;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        for (int o = lpr; o < 32; o <<= 1) {
+          ag[k][j] += __shfl_xor_sync(0xffffffffu, ag[k][j], o);
+          ab[k][j] += __shfl_xor_sync(0xffffffffu, ab[k][j], o);
+        }
+    if (rsub == 0) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int cv = sub + k * lpr;
+        if (cv < CV)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            atomicAdd(&sg[cv * 8 + j], ag[k][j]);
+            atomicAdd(&sb[cv * 8 + j], ab[k][j]);
+          }
+      }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < C; c += 128) {
+      atomicAdd(dgamma + c, sg[c]);
+      atomicAdd(dbeta + c, sb[c]);
+    }
+  }
+}
+
+// lanes per row (log2) and vectors per lane for the row-group LayerNorm (bf16, C % 8 == 0): NV in
+// {4, 5, 8}, LPR <= 32; 0 = not covered (the warp-per-row kernels)
+static int lnq_plan(int C, int& nv) {
+  const int CV = C / 8;
+  for (int cand : {5, 4, 8}) {
+    for (int l = 0; l <= 5; ++l) {
+      const int lpr = 1 << l;
+      if (lpr * cand >= CV && lpr * (cand - 1) < CV && (lpr * cand - CV) * 5 <= lpr * cand) {
+        nv = cand;
+        return l + 1;
+      }
+    }
+  }
+  return 0;
+}
+static bool lnq_enabled() {
+  static const int v = [] {
+    const char* e = getenv("DP_LN_GROUPS");  // experiments: 0 = warp-per-row kernels
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 extern "C" {
 
 size_t dp_group_norm_workspace(int N, int HW, int G) {
@@ -1005,6 +1232,22 @@ static int ln_blocks_per_sm(const void* kern) {
   return v;
 }
 
+// resident 128-thread blocks per SM (the row-group backward)
+static int ln_blocks_per_sm128(const void* kern) {
+  static const void* keys[16];
+  static int vals[16];
+  static int n = 0;
+  for (int i = 0; i < n; ++i)
+    if (keys[i] == kern) return vals[i];
+  int v = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, 128, 0) != cudaSuccess || v < 1) v = 1;
+  if (n < 16) {
+    keys[n] = kern;
+    vals[n++] = v;
+  }
+  return v;
+}
+
 int dp_layer_norm_fwd(int dtype, const void* x, const float* gamma, const float* beta,
                       const void* mod, int64_t mod_ld, int shift_off, int scale_off,
                       int rows_per_sample, void* y, float* mean, float* rstd, int64_t rows, int C,
@@ -1016,6 +1259,29 @@ int dp_layer_norm_fwd(int dtype, const void* x, const float* gamma, const float*
     set_error("layer_norm: C <= 2048, C % 8 == 0 (bf16) / 4 (fp32), 16-byte aligned rows, "
               "affine and modulation exclusive");
     return DP_ERR_ARGS;
+  }
+  if (dtype == DP_BF16 && !mod && lnq_enabled()) {
+    int nv = 0;
+    const int plan = lnq_plan(C, nv);
+    // full-warp rows (C >= 1024): the warp-per-row forward measured as fast or faster (tools/ln_bench.py)
+    if (plan && plan - 1 < 5) {
+      const int l = plan - 1;
+      const int64_t groups = (rows + (32 >> l) - 1) / (32 >> l);
+      const void* kern = nv == 4 ? (const void*)lnq_fwd_kernel<4> : nv == 5 ? (const void*)lnq_fwd_kernel<5>
+                                                                           : (const void*)lnq_fwd_kernel<8>;
+      const int64_t want = (groups + 7) / 8;
+      static const bool full = getenv("DP_LNQ_FULLGRID") != nullptr;  // experiments: one block per 8 row groups
+      const int64_t cap = full ? want : (int64_t)ln_blocks_per_sm(kern) * kNumSMs;
+      const dim3 grid(static_cast<unsigned>(want < cap ? want : cap));
+      auto go = [&](auto k) {
+        launch_k(k, grid, dim3(256), 0, ST, cp<__nv_bfloat16>(x), gamma, beta, mp<__nv_bfloat16>(y), mean, rstd,
+                 rows, C, l, eps);
+      };
+      if (nv == 4) go(lnq_fwd_kernel<4>);
+      else if (nv == 5) go(lnq_fwd_kernel<5>);
+      else go(lnq_fwd_kernel<8>);
+      return ew_check("layer_norm_fwd");
+    }
   }
   const int64_t want = (rows + 7) / 8;
   static const bool one_block_per_8_rows = getenv("DP_LN_FWD_BLOCKS") != nullptr;  // A/B experiments
@@ -1060,6 +1326,50 @@ int dp_layer_norm_bwd(int dtype, const void* x, const void* dy, const float* gam
               "affine and modulation exclusive");
     return DP_ERR_ARGS;
   }
+  if (dtype == DP_BF16 && !mod && lnq_enabled()) {
+    int nv = 0;
+    const int plan = lnq_plan(C, nv);
+    if (plan) {
+      const int l = plan - 1;
+      // parameter grads: a separate vectorised pass by default (the fused per-lane partials take ~80
+      // registers and halve the row kernel's occupancy; DP_LNQ_PG=1: fused, experiments)
+      static const bool fuse_pg = [] {
+        const char* e = getenv("DP_LNQ_PG");
+        return e && atoi(e) != 0;
+      }();
+      const bool pgq = gamma && dgamma && fuse_pg;
+      if (pgq && nv > 5) goto warp_rows;  // the fused parameter partials would spill: warp-per-row kernels
+      const int64_t groups = (rows + (32 >> l) - 1) / (32 >> l);
+      const int64_t want = (groups + 3) / 4;
+      auto go = [&](auto k) {
+        static const bool full = getenv("DP_LNQ_FULLGRID") != nullptr;
+        const int64_t cap = full ? want : (int64_t)ln_blocks_per_sm128(reinterpret_cast<const void*>(k)) * kNumSMs;
+        launch_k(k, dim3(static_cast<unsigned>(want < cap ? want : cap)), dim3(128), 0, ST, cp<__nv_bfloat16>(x),
+                 cp<__nv_bfloat16>(dy), gamma, mean, rstd, mp<__nv_bfloat16>(dx), rows, C, l, accumulate, dgamma,
+                 dbeta);
+      };
+      if (pgq) {
+        if (nv == 4) go(lnq_bwd_kernel<4, true>);
+        else go(lnq_bwd_kernel<5, true>);
+        return ew_check("layer_norm_bwd");
+      }
+      if (nv == 4) go(lnq_bwd_kernel<4, false>);
+      else if (nv == 5) go(lnq_bwd_kernel<5, false>);
+      else go(lnq_bwd_kernel<8, false>);
+      if (gamma && dgamma) {
+        const int CVn = C / 8;
+        const int64_t cb = (CVn + 31) / 32;
+        int64_t seg = (rows * cb + 2 * kNumSMs - 1) / (2 * kNumSMs);  // ~2 waves
+        seg = seg < 64 ? 64 : seg;
+        dim3 g2(static_cast<unsigned>(cb), static_cast<unsigned>((rows + seg - 1) / seg));
+        launch_k(ln_param_grad_kernel<__nv_bfloat16>, dim3(g2), dim3(256), 0, ST, cp<__nv_bfloat16>(x),
+                 cp<__nv_bfloat16>(dy), mean, rstd, rows, C, static_cast<int>(seg), dgamma, dbeta,
+                 static_cast<__nv_bfloat16*>(nullptr), (int64_t)0, 0, 0);
+      }
+      return ew_check("layer_norm_bwd");
+    }
+  }
+warp_rows:
   const int rps = rows_per_sample > 0 ? rows_per_sample : 1;
   const int nvec = (C / (dtype == DP_F32 ? 4 : 8) + 31) / 32;
   // affine parameter grads fused into the row pass while the per-lane partials fit in registers

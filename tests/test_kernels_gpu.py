@@ -49,7 +49,8 @@ def test_group_norm(dt, N, H, C, G, silu):
 
 
 @pytest.mark.parametrize("dt", DT)
-@pytest.mark.parametrize("rows,C", [(77, 1024), (300, 320), (64, 256), (10, 1280)])
+@pytest.mark.parametrize("rows,C", [(77, 1024), (300, 320), (64, 256), (10, 1280), (32768, 320), (8192, 640),
+                                    (2048, 1280), (333, 640)])
 def test_layer_norm_affine(dt, rows, C):
     from paper_2405_01248_b200 import ops
     x = (torch.randn(rows, C, device="cuda") * 3 - 1).to(dt)
@@ -68,6 +69,23 @@ def test_layer_norm_affine(dt, rows, C):
     assert _rel(dx, xr.grad) < 2 * _tol(dt)
     assert _rel(dg, gr.grad) < 2 * _tol(dt)
     assert _rel(db, br.grad) < 2 * _tol(dt)
+
+
+@pytest.mark.parametrize("rows,C", [(1000, 320), (257, 640), (99, 1280)])
+def test_layer_norm_bwd_accumulate_no_affine(rows, C):
+    """Backward accumulated into an existing gradient (norm forks) and the affine-free form (bf16 row groups)."""
+    from paper_2405_01248_b200 import ops
+    x = (torch.randn(rows, C, device="cuda") * 2 + 0.5).bfloat16()
+    y, mean, rstd = ops.layer_norm(x, None, None, 1e-6)
+    xr = x.float().requires_grad_(True)
+    yr = F.layer_norm(xr, (C,), eps=1e-6)
+    assert _rel(y, yr) < _tol(torch.bfloat16)
+    dy = torch.randn_like(y)
+    yr.backward(dy.float())
+    base = torch.randn_like(x)
+    acc = base.clone()
+    ops.layer_norm_bwd(x, dy, None, mean, rstd, accumulate_into=acc)
+    assert _rel(acc, base.float() + xr.grad) < 2 * _tol(torch.bfloat16)
 
 
 @pytest.mark.parametrize("dt", DT)
