@@ -52,8 +52,11 @@ class _Timer:
 
     def event(self):
         i = self.next
-        if i >= self.capacity:
-            raise RuntimeError("telemetry: timing event pool exhausted (raise `reserve`)")
+        if i >= self.capacity:  # grow the native pool (event creation is host-side only)
+            cap = max(2 * self.capacity, 1024)
+            if self.native.dp_timing_events(cap) != 0:
+                raise RuntimeError("dp_timing_events failed")
+            self.capacity = cap
         self.next += 1
         return i
 

@@ -71,6 +71,8 @@ def main():
             cache = (_Store(), _P(wt))
             r["dgrad_us"] = timeit(lambda: ops.linear_dgrad(dy, w, out=dx, cache=cache))
             r["dgrad_cublas_us"] = timeit(lambda: torch.mm(dy, w, out=dx))
+            # the weight read MN-major in place (no flip-transposed copy)
+            r["dgrad_mn_us"] = timeit(lambda: ops.gemm(dy, w, dx, M=M, N=K, K=N, a_ld=N, b_ld=K, b_mn=True, d_ld=K))
         if "wgrad" in passes and M >= 1024:
             r["wgrad_us"] = timeit(lambda: ops.linear_wgrad(dy, x, dw))
             r["wgrad_cublas_us"] = timeit(lambda: torch.mm(dy.t(), x, out_dtype=torch.float32))
