@@ -986,6 +986,8 @@ static int widen_bn(int bn, int cg, bool b_mn, int N, int num_kb) {
 // 128x160 tiles in one wave over 40 pair tiles of 256x256; 8192^3 keeps pairs of 256).
 static void choose_tile(int M, int N, int K, bool b_mn, int& bn_out, int& cg_out) {
   static const int forced_bn = env_int("DP_FORCE_BN"), forced_cg = env_int("DP_FORCE_CG");
+  // sustainable L2 -> SM operand feed per SM (bytes per clock) in the cost model (DP_TILE_FEED: experiments)
+  static const double feed = env_int("DP_TILE_FEED") > 0 ? env_int("DP_TILE_FEED") : 80.0;
   const int num_kb = (K + BK - 1) / BK;
   double best = -1.0;
   for (int cg = 1; cg <= 2; ++cg) {
@@ -1000,7 +1002,7 @@ static void choose_tile(int M, int N, int K, bool b_mn, int& bn_out, int& cg_out
       const long long units = (long long)((M + 128 * cg - 1) / (128 * cg)) * ((N + bn - 1) / bn);
       const long long per_wave = kNumSMs / cg;
       const long long waves = (units + per_wave - 1) / per_wave;
-      const double l2 = (16384.0 + (bn / cg) * 128.0) / 80.0;
+      const double l2 = (16384.0 + (bn / cg) * 128.0) / feed;
       const double per_kb = (2.0 * bn > l2) ? 2.0 * bn : l2;
       const double cost = waves * (num_kb * per_kb + 2500.0 + (bn > 256 ? 1500.0 : 0.0));
       if (best < 0 || cost < best * 0.999 || (cost <= best * 1.001 && bn > bn_out)) {
@@ -1268,6 +1270,17 @@ int tc_gemm(const DpGemmArgs* a, cudaStream_t st, int64_t* query = nullptr) {
     const int bn0 = pick_bn(a->N, a->b_mn_major != 0);
     cg = decide_cg(a->M, bn0, a->b_mn_major != 0, a->K);
     bn = widen_bn(bn0, cg, a->b_mn_major != 0, a->N, (a->K + BK - 1) / BK);
+    // weight gradients (fp32 accumulate, both operands MN-major, long K): 256 x 256 CTA-pair tiles
+    // for M >= 1024, N >= 512, padding included (8192x5120x640: 67 -> 52 us, 8192x1920x640: 31 -> 27). These GEMMs are bound by the TMA feed (L2 -> SM
+    // bytes per MMA cycle), not the tensor core: 128 x 128 single-CTA tiles move 128 B per SM per MMA
+    // cycle, pairs of 256 x 256 62.5 (the swapped conv weight gradient measured 85 -> 59 us at
+    // 16x16x640 with the same change; DP_WG_NARROW=1: previous choice, experiments)
+    static const bool narrow = env_int("DP_WG_NARROW") != 0;
+    if (!narrow && a->out_mode == DP_OUT_ATOMIC_ADD && a->a_mn_major && a->b_mn_major && a->M >= 1024 &&
+        a->N >= 512 && a->K >= 1024) {  // (M = 640 measured slower with the padded pairs)
+      bn = 256;
+      cg = 2;
+    }
   }
   TcParams p{};
   p.M = a->M;
@@ -1477,13 +1490,17 @@ int tc_conv_dgrad(const DpConvArgs* a, cudaStream_t st, int64_t* query = nullptr
 // (M = K) leaves K = 640 / 1280 layers on single CTAs or 17%-padded pairs.
 static int conv_wgrad_swapped(const DpConvArgs* a, TcParams& p, cudaStream_t st) {
   const int Ntot = a->R * a->S * a->C;
-  const int bn = (a->K % 256 == 0) ? 256 : 128;
+  // 256-wide tiles also for K = 640 (three tiles, the last half empty): per-CTA L2->SM bytes per MMA
+  // cycle drop by a third against 128-wide tiles, and the swapped weight gradient is bound by the TMA
+  // feed, not by the tensor core (DP_WGRAD_BN128=1: 128-wide tiles, experiments)
+  static const bool bn128 = getenv("DP_WGRAD_BN128") != nullptr;
+  const int bn = (a->K % 256 == 0 || (!bn128 && a->K >= 512)) ? 256 : 128;
   const int cg = 2;
   p.M = Ntot;
   p.N = a->K;
   p.num_kb = (a->N * a->P * a->Q + BK - 1) / BK;
   p.tiles_m = (Ntot + BM * cg - 1) / (BM * cg);
-  p.tiles_n = a->K / bn;
+  p.tiles_n = (a->K + bn - 1) / bn;
   p.batch1 = 1;
   p.nbatch = 1;
   p.a_mode = A_WG_X;
