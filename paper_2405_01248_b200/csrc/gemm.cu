@@ -987,7 +987,7 @@ static int widen_bn(int bn, int cg, bool b_mn, int N, int num_kb) {
 static void choose_tile(int M, int N, int K, bool b_mn, int& bn_out, int& cg_out) {
   static const int forced_bn = env_int("DP_FORCE_BN"), forced_cg = env_int("DP_FORCE_CG");
   // sustainable L2 -> SM operand feed per SM (bytes per clock) in the cost model (DP_TILE_FEED: experiments)
-  static const double feed = env_int("DP_TILE_FEED") > 0 ? env_int("DP_TILE_FEED") : 80.0;
+  static const double feed = env_int("DP_TILE_FEED") > 0 ? env_int("DP_TILE_FEED") : 64.0;
   const int num_kb = (K + BK - 1) / BK;
   double best = -1.0;
   for (int cg = 1; cg <= 2; ++cg) {
