@@ -75,6 +75,17 @@ typedef struct DpGemmArgs {
      GEMM runs unsplit. */
   float* workspace;
   int64_t workspace_bytes;
+  /* optional GEGLU epilogues (bf16, K-major operands, no residual / batch):
+     geglu_mode 1 (forward of the FF input projection, N = 2F): B rows [0, F) produce a and [F, 2F) g of
+       the pre-activation D = [a | g] (stored as usual, it is the backward's input); geglu_out[m][f] =
+       a * gelu_erf(g) (row stride geglu_ld) is written by the same epilogue;
+     geglu_mode 2 (input gradient of the FF output projection, N = F): the GEMM result is dy = dL/dy of
+       the GEGLU output; with h = geglu_out ([M][2F] pre-activation, row stride geglu_ld) the epilogue
+       writes D[m][f] = dy * gelu(g) and D[m][F + f] = dy * a * gelu'(g) (D is [M][2F], row stride d_ld).
+     0: off. */
+  void* geglu_out;
+  int64_t geglu_ld;
+  int geglu_mode;
 } DpGemmArgs;
 
 /* 2-D convolution over NHWC activations with weights [K][R][S][C].
@@ -153,6 +164,15 @@ int dp_col2im(int dtype, const void* cols, void* dx, int N, int H, int W, int C,
 int dp_conv_weight_flip(int dtype, const void* w, void* wt, int K, int R, int S, int C,
                         dp_stream_t stream);
 /* out[n][p*stride][q*stride][c] = dy[n][p][q][c]; other positions 0. out: [N][P*stride][Q*stride][C] */
+/* Batched dgrad weight-copy refresh (bf16): for every job, wt[c][R-1-r][S-1-s][k] = w[k][r][s][c]
+   (dp_conv_weight_flip's layout), all jobs in one launch per DP_FLIP_BATCH_MAX jobs. */
+#define DP_FLIP_BATCH_MAX 48
+typedef struct DpFlipJob {
+  const void* w;
+  void* wt;
+  int K, R, S, C;
+} DpFlipJob;
+int dp_conv_weight_flip_batch(const DpFlipJob* jobs, int n, dp_stream_t stream);
 int dp_dilate(int dtype, const void* dy, void* out, int N, int P, int Q, int C, int stride,
               dp_stream_t stream);
 

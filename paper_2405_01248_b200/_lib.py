@@ -36,6 +36,7 @@ class DpGemmArgs(ctypes.Structure):
         ("alpha", c_float),
         ("split_k", c_int),
         ("workspace", c_void_p), ("workspace_bytes", c_i64),
+        ("geglu_out", c_void_p), ("geglu_ld", c_i64), ("geglu_mode", c_int),
     ]
 
 
@@ -62,6 +63,10 @@ class DpAttnArgs(ctypes.Structure):
         ("q_ld", c_i64), ("q_bs", c_i64), ("kv_ld", c_i64), ("kv_bs", c_i64), ("o_ld", c_i64), ("o_bs", c_i64),
         ("scale", c_float), ("lse", c_void_p), ("causal", c_int),
     ]
+
+
+class DpFlipJob(ctypes.Structure):
+    _fields_ = [("w", c_void_p), ("wt", c_void_p), ("K", c_int), ("R", c_int), ("S", c_int), ("C", c_int)]
 
 
 # name -> argtypes (restype is always c_int unless listed in _RESTYPES)
@@ -129,6 +134,7 @@ _SIGNATURES = {
     "dp_rms_norm_fwd": [c_int, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_float, c_void_p],
     "dp_softmax_fwd": [c_int, c_void_p, c_void_p, c_i64, c_int, c_int, c_float, c_int, c_int, c_void_p],
     "dp_softmax_bwd": [c_int, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_int, c_float, c_void_p],
+    "dp_conv_weight_flip_batch": [ctypes.POINTER(DpFlipJob), c_int, c_void_p],
     # timing.cu
     "dp_timing_events": [c_int],
     "dp_timing_record": [c_int, c_void_p],

@@ -116,6 +116,51 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Batched refresh of the cached dgrad weight copies (after an optimizer slice): one launch over
+// every job's 64x64 tiles instead of one launch per parameter (~150 per step).
+struct FlipBatch {
+  const __nv_bfloat16* w[DP_FLIP_BATCH_MAX];
+  __nv_bfloat16* wt[DP_FLIP_BATCH_MAX];
+  int K[DP_FLIP_BATCH_MAX], R[DP_FLIP_BATCH_MAX], S[DP_FLIP_BATCH_MAX], C[DP_FLIP_BATCH_MAX];
+  int tile0[DP_FLIP_BATCH_MAX + 1];  // prefix sums of the jobs' tile counts
+  int n;
+};
+
+__global__ void __launch_bounds__(256) flip_t_batch_kernel(const __grid_constant__ FlipBatch fb) {
+  DP_PDL_ENTRY();
+  __shared__ __nv_bfloat16 tile[64][64 + 8];
+  int j = 0;
+  while (j + 1 < fb.n && static_cast<int>(blockIdx.x) >= fb.tile0[j + 1]) ++j;
+  const int K = fb.K[j], R = fb.R[j], S = fb.S[j], C = fb.C[j];
+  const int ct = (C + 63) / 64, kt = (K + 63) / 64;
+  int t = blockIdx.x - fb.tile0[j];
+  const int tap = t / (ct * kt);
+  t -= tap * ct * kt;
+  const int k0 = (t / ct) * 64, c0 = (t - (t / ct) * ct) * 64;
+  const __nv_bfloat16* w = fb.w[j];
+  __nv_bfloat16* wt = fb.wt[j];
+  const int RS = R * S;
+  const int r = tap / S, s = tap - (tap / S) * S;
+  const int ftap = (R - 1 - r) * S + (S - 1 - s);
+  for (int i = threadIdx.x; i < 64 * 8; i += 256) {
+    const int kk = i >> 3, cv = (i & 7) * 8;
+    const int k = k0 + kk, c = c0 + cv;
+    uint4 u = make_uint4(0, 0, 0, 0);
+    if (k < K && c < C) u = *reinterpret_cast<const uint4*>(w + ((int64_t)k * RS + tap) * C + c);
+    *reinterpret_cast<uint4*>(&tile[kk][cv]) = u;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 64 * 8; i += 256) {
+    const int cc = i >> 3, kv = (i & 7) * 8;
+    const int c = c0 + cc, k = k0 + kv;
+    if (c >= C || k >= K) continue;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = tile[kv + q][cc];
+    *reinterpret_cast<uint4*>(wt + ((int64_t)c * RS + ftap) * K + k) = *reinterpret_cast<const uint4*>(v);
+  }
+}
+
 template <typename T>
 __global__ void dilate_kernel(const T* __restrict__ dy, T* __restrict__ out, int N, int P, int Q,
                               int C, int stride) {
@@ -220,6 +265,34 @@ int dp_conv_weight_flip(int dtype, const void* w, void* wt, int K, int R, int S,
     launch_k(flip_kernel<__nv_bfloat16>, dim3(grid_for(total)), dim3(256), 0, st, 
         (const __nv_bfloat16*)w, (__nv_bfloat16*)wt, K, R, S, C);
   return check("conv_weight_flip");
+}
+
+int dp_conv_weight_flip_batch(const DpFlipJob* jobs, int n, dp_stream_t stream) {
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  for (int base = 0; base < n; base += DP_FLIP_BATCH_MAX) {
+    FlipBatch fb{};
+    fb.n = n - base < DP_FLIP_BATCH_MAX ? n - base : DP_FLIP_BATCH_MAX;
+    int tiles = 0;
+    for (int i = 0; i < fb.n; ++i) {
+      const DpFlipJob& jb = jobs[base + i];
+      if (jb.K % 8 || jb.C % 8 || (reinterpret_cast<uintptr_t>(jb.w) | reinterpret_cast<uintptr_t>(jb.wt)) % 16) {
+        dp::set_error("dp_conv_weight_flip_batch: bf16 jobs with K % 8 == 0, C % 8 == 0, 16-byte aligned");
+        return DP_ERR_ARGS;
+      }
+      fb.w[i] = static_cast<const __nv_bfloat16*>(jb.w);
+      fb.wt[i] = static_cast<__nv_bfloat16*>(jb.wt);
+      fb.K[i] = jb.K;
+      fb.R[i] = jb.R;
+      fb.S[i] = jb.S;
+      fb.C[i] = jb.C;
+      fb.tile0[i] = tiles;
+      tiles += ((jb.C + 63) / 64) * ((jb.K + 63) / 64) * jb.R * jb.S;
+    }
+    fb.tile0[fb.n] = tiles;
+    if (tiles == 0) continue;
+    launch_k(flip_t_batch_kernel, dim3(tiles), dim3(256), 0, st, fb);
+  }
+  return check("conv_weight_flip_batch");
 }
 
 int dp_dilate(int dtype, const void* dy, void* out, int N, int P, int Q, int C, int stride,

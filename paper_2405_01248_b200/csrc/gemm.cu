@@ -17,6 +17,7 @@
 //                       stride-2 from TMA element strides
 //   A_WG_DY / B_WG_X    conv weight gradient: K runs over 64-pixel tiles of dY / shifted X
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -44,6 +45,10 @@ struct TcParams {
   int stream_k;    // 1: contiguous k-iteration ranges per CTA (fp32 atomic outputs)
   int d_tma;       // 1: bf16 output written by TMA tensor stores (tmD)
   int halo;        // 1: 3x3 stride-1 conv with one input strip per filter row (TcCfg HALO)
+  int geglu, F;    // GEGLU epilogues: 1 = forward (N = 2F, tile = [a cols | g cols] of one BN/2-wide
+                   // output range), 2 = backward through the FF output projection's dgrad (N = F)
+  const void* gh;  // geglu 2: the pre-activation h = [a | g], bf16 [M][2F], row stride gh_ld
+  int64_t gh_ld;
   void* D;
   int64_t d_ld, d_bs1, d_bs2;
   int d_f32, out_mode, vec_ok;
@@ -346,10 +351,13 @@ DP_DEV void epilogue_math(const TcParams& p, int row, int n, int z1, int z2, con
 
 constexpr int EPI_STAGE_BYTES = 32 * 64;  // one 32 x 32 bf16 chunk
 
-template <int BN, int CG, bool HALO, bool RES>
+// GEG: GEGLU epilogue instantiations (0 = none, 1 = FF input projection forward, 2 = FF output projection
+// input gradient); kept out of the other instantiations so their epilogue registers stay as they were
+template <int BN, int CG, bool HALO, bool RES, int GEG = 0>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmD, const TcParams p) {
+                   const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmD2,
+                   const TcParams p) {
   using Cfg = TcCfg<BN, CG, HALO>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int BNL = Cfg::BNL;
@@ -378,6 +386,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     if (p.d_tma) tma_prefetch(&tmD);
+    if constexpr (GEG == 1) tma_prefetch(&tmD2);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -501,7 +510,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           switch (p.b_mode) {
             case B_KMAJ:
-              if constexpr (Cfg::NH == 2) {
+              if constexpr (GEG == 1) {
+                // [a rows | g rows] of output range n_blk*BN/2: a pair's CTAs hold one half each,
+                // a single CTA stacks both (two BN/2-row boxes)
+                const int na = wk.n_blk * (BN / 2);
+                if constexpr (CG == 2) {
+                  load(&tmB, b_dst, kb * BK, crank ? p.F + na : na, z1, z2);
+                } else {
+                  load(&tmB, b_dst, kb * BK, na, z1, z2);
+                  load(&tmB, b_dst + (BN / 2) * BK * 2, kb * BK, p.F + na, z1, z2);
+                }
+              } else if constexpr (Cfg::NH == 2) {
                 const int nt = wk.n_blk * BN + crank * (BNL / 2);
                 load(&tmB, b_dst, kb * BK, nt, z1, z2);
                 load(&tmB, b_dst + Cfg::B_HALF, kb * BK, nt + BN / 2, z1, z2);
@@ -686,8 +705,95 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // two warps per TMEM lane quadrant split the accumulator's 32-column chunks (even / odd):
       // the epilogue (TMEM load, bias / residual, bf16 staging, TMA store per chunk) is latency
       // bound per warp and had bounded short-K GEMMs with one warp per quadrant
-      const int nch = min(BN / 32, (p.N - wk.n_blk * BN + 31) / 32);  // warp-uniform
+      const int nch = GEG == 1 ? 0 : min(BN / 32, (p.N - wk.n_blk * BN + 31) / 32);  // warp-uniform
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + acc * BN;
+      if constexpr (GEG == 1) {
+        // chunk pair (a cols c, g cols c + BN/64): bias, bf16 rounding (the stored pre-activation, which
+        // the backward reads), y = a * gelu_erf(g) from the rounded values, three TMA stores
+#pragma unroll 1
+        for (int c = half; c < BN / 64; c += 2) {
+          const int na = wk.n_blk * (BN / 2) + c * 32;
+          uint32_t va[32], vg[32];
+          tmem_ld_32x32(tbase + c * 32, va);
+          tmem_ld_32x32(tbase + BN / 2 + c * 32, vg);
+          tmem_ld_wait_dep(va);
+          tmem_ld_wait_dep(vg);
+          // a and g rows: bias, bf16 rounding, staged and stored (the stored pre-activation is what the
+          // backward reads); y is then computed from the staged bf16 rows (same inputs as the unfused
+          // geglu kernel) and stored once the first staging buffer has been read by its TMA store
+          auto stage_pre = [&](const uint32_t (&v)[32], const float* bias, int col) -> uint8_t* {
+            uint8_t* buf = ebuf + (chunk_seq & 1) * EPI_STAGE_BYTES;
+            if (chunk_seq >= 2) {
+              if (lane == 0) bulk_wait_read<1>();
+              __syncwarp();
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + q * 8));
+              const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + q * 8 + 4));
+              uint4 u;
+              u.x = pack_bf16x2(__uint_as_float(v[q * 8 + 0]) + b0.x, __uint_as_float(v[q * 8 + 1]) + b0.y);
+              u.y = pack_bf16x2(__uint_as_float(v[q * 8 + 2]) + b0.z, __uint_as_float(v[q * 8 + 3]) + b0.w);
+              u.z = pack_bf16x2(__uint_as_float(v[q * 8 + 4]) + b1.x, __uint_as_float(v[q * 8 + 5]) + b1.y);
+              u.w = pack_bf16x2(__uint_as_float(v[q * 8 + 6]) + b1.z, __uint_as_float(v[q * 8 + 7]) + b1.w);
+              const int qs = q ^ ((lane >> 1) & 3);
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(buf + lane * 64 + qs * 16)),
+                           "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w)
+                           : "memory");
+            }
+            fence_async_shared();
+            __syncwarp();
+            if (lane == 0 && row0 < p.M) {
+              tma_store_4d(&tmD, buf, col, row0, 0, 0);
+              bulk_commit();
+            }
+            ++chunk_seq;
+            return buf;
+          };
+          const uint8_t* ba = stage_pre(va, p.bias + na, na);
+          const uint8_t* bg = stage_pre(vg, p.bias + p.F + na, p.F + na);
+          uint32_t yp[16];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int qs = q ^ ((lane >> 1) & 3);
+            uint4 ua, ug;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(ua.x), "=r"(ua.y), "=r"(ua.z), "=r"(ua.w)
+                         : "r"(smem_u32(ba + lane * 64 + qs * 16)));
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(ug.x), "=r"(ug.y), "=r"(ug.z), "=r"(ug.w)
+                         : "r"(smem_u32(bg + lane * 64 + qs * 16)));
+            const uint32_t* pa = &ua.x;
+            const uint32_t* pg = &ug.x;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(pa + i));
+              const float2 fg = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(pg + i));
+              yp[q * 4 + i] = pack_bf16x2(fa.x * (0.5f * fg.x * (1.f + erff(fg.x * 0.70710678118654752f))),
+                                          fa.y * (0.5f * fg.y * (1.f + erff(fg.y * 0.70710678118654752f))));
+            }
+          }
+          {
+            uint8_t* buf = ebuf + (chunk_seq & 1) * EPI_STAGE_BYTES;  // = the a buffer: wait for its store
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int qs = q ^ ((lane >> 1) & 3);
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(buf + lane * 64 + qs * 16)),
+                           "r"(yp[q * 4]), "r"(yp[q * 4 + 1]), "r"(yp[q * 4 + 2]), "r"(yp[q * 4 + 3])
+                           : "memory");
+            }
+            fence_async_shared();
+            __syncwarp();
+            if (lane == 0 && row0 < p.M) {
+              tma_store_4d(&tmD2, buf, na, row0, 0, 0);
+              bulk_commit();
+            }
+            ++chunk_seq;
+          }
+        }
+      }
 #pragma unroll 1
       for (int c = half; c < nch; c += 2) {
         const int n = wk.n_blk * BN + c * 32;
@@ -702,9 +808,54 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           rload(wk, row, c + 4, r2);
         }
+        // GEGLU backward: this chunk's a / g rows of h are loaded while the TMEM load is in flight
+        uint4 ua[4], ug[4];
+        if constexpr (GEG == 2) {
+          const __nv_bfloat16* hr = reinterpret_cast<const __nv_bfloat16*>(p.gh) + (int64_t)row * p.gh_ld + n;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            ua[q] = row < p.M ? *reinterpret_cast<const uint4*>(hr + q * 8) : make_uint4(0, 0, 0, 0);
+            ug[q] = row < p.M ? *reinterpret_cast<const uint4*>(hr + p.F + q * 8) : make_uint4(0, 0, 0, 0);
+          }
+        }
         tmem_ld_wait_dep(v);
         const bool use_pre = rpre_on && row < p.M && n + 32 <= p.N;
-        if (p.d_tma == 3) {
+        if constexpr (GEG == 2) {
+          // dy (rounded to bf16, as the unfused dgrad stores it) -> da = dy * gelu(g), dg = dy * a * gelu'(g)
+          // from h's a / g rows of this chunk; two TMA stores into dh = [da | dg]
+          float da[32], dg[32];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const __nv_bfloat16* pa = reinterpret_cast<const __nv_bfloat16*>(&ua[q]);
+            const __nv_bfloat16* pg = reinterpret_cast<const __nv_bfloat16*>(&ug[q]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float d = __bfloat162float(__float2bfloat16_rn(__uint_as_float(v[q * 8 + i])));
+              const float a = __bfloat162float(pa[i]), g = __bfloat162float(pg[i]);
+              const float cdf = 0.5f * (1.f + erff(g * 0.70710678118654752f));
+              const float pdf = 0.39894228040143268f * __expf(-0.5f * g * g);
+              da[q * 8 + i] = d * (g * cdf);
+              dg[q * 8 + i] = d * a * (cdf + g * pdf);
+            }
+          }
+          auto put = [&](const float (&f)[32], int col) {
+            uint8_t* buf = ebuf + (chunk_seq & 1) * EPI_STAGE_BYTES;
+            if (chunk_seq >= 2) {
+              if (lane == 0) bulk_wait_read<1>();
+              __syncwarp();
+            }
+            stage_row_bf16(buf, lane, f);
+            fence_async_shared();
+            __syncwarp();
+            if (lane == 0 && row0 < p.M) {
+              tma_store_4d(&tmD, buf, col, row0, 0, 0);
+              bulk_commit();
+            }
+            ++chunk_seq;
+          };
+          put(da, n);
+          put(dg, p.F + n);
+        } else if (p.d_tma == 3) {
           // transposed fp32 reduce (swapped weight gradient: D rows are the contiguous dimension of the
           // output): stage [16 columns][32 rows] with lane = row, one TMA reduce-add per 16 columns
 #pragma unroll
@@ -856,10 +1007,50 @@ static int make_map(CUtensorMap* map, const void* base, const uint64_t dims[4],
     bx[i] = box[i];
     es[i] = estr[i];
   }
+  // Encoded maps are cached per host thread: the caching allocator hands the same addresses back every
+  // iteration, so after the first step almost every launch finds its (address, geometry) maps here
+  // instead of re-encoding three descriptors per GEMM on the host's critical path.
+  struct Key {
+    const void* base;
+    cuuint64_t gdim[4], gstr[3];
+    cuuint32_t bx[4], es[4];
+    int swz, esize;
+  };
+  struct Slot {
+    Key k;
+    CUtensorMap m;
+    bool used;
+  };
+  constexpr int kSlots = 8192;
+  thread_local Slot* cache = nullptr;
+  if (!cache) cache = new Slot[kSlots]();
+  Key k{};
+  k.base = base;
+  for (int i = 0; i < 4; ++i) {
+    k.gdim[i] = gdim[i];
+    k.bx[i] = bx[i];
+    k.es[i] = es[i];
+  }
+  for (int i = 0; i < 3; ++i) k.gstr[i] = gstr[i];
+  k.swz = static_cast<int>(swz);
+  k.esize = esize;
+  uint64_t hsh = 1469598103934665603ull;
+  const unsigned char* kb = reinterpret_cast<const unsigned char*>(&k);
+  for (size_t i = 0; i < sizeof(Key); ++i) hsh = (hsh ^ kb[i]) * 1099511628211ull;
+  Slot& slot = cache[hsh & (kSlots - 1)];
+  if (slot.used && memcmp(&slot.k, &k, sizeof(Key)) == 0) {
+    *map = slot.m;
+    return 0;
+  }
   CUresult r = fn(map, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
                   const_cast<void*>(base), gdim, gstr,
                   bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r == CUDA_SUCCESS) {
+    slot.k = k;
+    slot.m = *map;
+    slot.used = true;
+  }
   if (r != CUDA_SUCCESS) {
     char buf[256];
     snprintf(buf, sizeof(buf),
@@ -880,13 +1071,13 @@ static bool halo_enabled() {
   return on;
 }
 
-template <int BN, int CG, bool HALO = false, bool RES = false>
+template <int BN, int CG, bool HALO = false, bool RES = false, int GEG = 0>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
-                     TcParams p, int max_ctas, cudaStream_t st) {
+                     TcParams p, int max_ctas, cudaStream_t st, const CUtensorMap* md2 = nullptr) {
   using Cfg = TcCfg<BN, CG, HALO>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, CG, HALO, RES>,
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, CG, HALO, RES, GEG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(Cfg::SMEM));
     if (e != cudaSuccess) {
@@ -914,7 +1105,7 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
   attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, CG, HALO, RES>, ma, mb, md, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, CG, HALO, RES, GEG>, ma, mb, md, md2 ? *md2 : md, p);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("tc_gemm launch: ") + cudaGetErrorString(e));
@@ -1254,9 +1445,82 @@ static void fill_epilogue(TcParams& p, void* D, int d_dtype, int64_t d_ld, int64
   p.vec_ok = ok ? 1 : 0;
 }
 
+// Linear forward with the GEGLU epilogue (see DpGemmArgs::geglu_out): tile = BN/2 output columns of
+// both halves, CTA pairs for M >= 256 with each CTA staging one half of B.
+static int tc_gemm_geglu(const DpGemmArgs* a, cudaStream_t st) {
+  const int F = a->N / 2;
+  if (a->d_dtype != DP_BF16 || a->dtype != DP_BF16 || a->out_mode != DP_OUT_STORE || a->Res || !a->bias ||
+      a->a_mn_major || a->b_mn_major || (a->batch1 > 1) || (a->batch2 > 1) || a->N % 128 || F % 64 ||
+      a->alpha != 1.f) {
+    set_error("gemm geglu epilogue: bf16 K-major linear with bias, N = 2F, F % 64 == 0, no residual/batch");
+    return DP_ERR_UNSUPPORTED;
+  }
+  const int bn = (F % 128 == 0) ? 256 : 128;
+  const int cg = a->M >= 256 ? 2 : 1;
+  TcParams p{};
+  p.M = a->M;
+  p.N = a->N;
+  p.F = F;
+  p.geglu = 1;
+  p.num_kb = (a->K + BK - 1) / BK;
+  p.tiles_m = (a->M + BM * cg - 1) / (BM * cg);
+  p.tiles_n = F / (bn / 2);
+  p.batch1 = 1;
+  p.nbatch = 1;
+  p.a_mode = A_KMAJ;
+  p.b_mode = B_KMAJ;
+  choose_split(p, 0, false);
+  fill_epilogue(p, a->D, DP_BF16, a->d_ld, 0, 0, DP_OUT_STORE, a->bias, nullptr, 0, 0, 0, 1.f);
+  if (!p.vec_ok || reinterpret_cast<uintptr_t>(a->geglu_out) % 16 || (a->geglu_ld * 2) % 16 ||
+      reinterpret_cast<uintptr_t>(a->bias) % 16) {
+    set_error("gemm geglu epilogue: 16-byte aligned outputs, bias and row strides");
+    return DP_ERR_ARGS;
+  }
+  CUtensorMap ma, mb, md, md2;
+  const uint32_t ones[4] = {1, 1, 1, 1};
+  {
+    const uint64_t d[4] = {(uint64_t)a->K, (uint64_t)a->M, 1, 1};
+    const int64_t s[3] = {a->a_ld, (int64_t)a->M * a->a_ld, (int64_t)a->M * a->a_ld};
+    const uint32_t box[4] = {BK, BM, 1, 1};
+    if (int e = make_map(&ma, a->A, d, s, box, ones)) return e;
+  }
+  {
+    const uint64_t d[4] = {(uint64_t)a->K, (uint64_t)a->N, 1, 1};
+    const int64_t s[3] = {a->b_ld, (int64_t)a->N * a->b_ld, (int64_t)a->N * a->b_ld};
+    const uint32_t box[4] = {BK, (uint32_t)(bn / 2), 1, 1};
+    if (int e = make_map(&mb, a->B, d, s, box, ones)) return e;
+  }
+  make_dmap(&md, p, a->M, a->N, 1, 1);
+  if (!p.d_tma) {
+    set_error("gemm geglu epilogue: output not TMA-storable");
+    return DP_ERR_ARGS;
+  }
+  {
+    const uint64_t d[4] = {(uint64_t)F, (uint64_t)a->M, 1, 1};
+    const int64_t s[3] = {a->geglu_ld, (int64_t)a->M * a->geglu_ld, (int64_t)a->M * a->geglu_ld};
+    const uint32_t box[4] = {32, 32, 1, 1};
+    if (int e = make_map(&md2, a->geglu_out, d, s, box, ones, CU_TENSOR_MAP_SWIZZLE_64B)) return e;
+  }
+  if (cg == 2)
+    return bn == 256 ? launch_tc<256, 2, false, false, 1>(ma, mb, md, p, kNumSMs, st, &md2)
+                     : launch_tc<128, 2, false, false, 1>(ma, mb, md, p, kNumSMs, st, &md2);
+  return bn == 256 ? launch_tc<256, 1, false, false, 1>(ma, mb, md, p, kNumSMs, st, &md2)
+                   : launch_tc<128, 1, false, false, 1>(ma, mb, md, p, kNumSMs, st, &md2);
+}
+
 int tc_gemm(const DpGemmArgs* a, cudaStream_t st, int64_t* query = nullptr) {
   if (query) *query = 0;
   if (a->M <= 0 || a->N <= 0 || a->K <= 0) return 0;
+  if (a->geglu_mode == 1) return query ? 0 : tc_gemm_geglu(a, st);
+  if (a->geglu_mode == 2) {
+    if (query) return 0;
+    if (a->d_dtype != DP_BF16 || a->out_mode != DP_OUT_STORE || a->Res || a->bias || a->a_mn_major ||
+        a->b_mn_major || a->batch1 > 1 || a->batch2 > 1 || a->N % 32 || a->alpha != 1.f ||
+        reinterpret_cast<uintptr_t>(a->geglu_out) % 16 || a->geglu_ld % 8) {
+      set_error("gemm geglu backward epilogue: bf16 K-major dgrad, N % 32 == 0, aligned h, no bias/residual");
+      return DP_ERR_UNSUPPORTED;
+    }
+  }
   if (a->out_mode == DP_OUT_ATOMIC_ADD && a->d_dtype != DP_F32) {
     set_error("atomic accumulation needs an fp32 output");
     return DP_ERR_ARGS;
@@ -1271,8 +1535,8 @@ int tc_gemm(const DpGemmArgs* a, cudaStream_t st, int64_t* query = nullptr) {
     cg = decide_cg(a->M, bn0, a->b_mn_major != 0, a->K);
     bn = widen_bn(bn0, cg, a->b_mn_major != 0, a->N, (a->K + BK - 1) / BK);
     // weight gradients (fp32 accumulate, both operands MN-major, long K): 256 x 256 CTA-pair tiles
-    // for M >= 1024, N >= 512, padding included (8192x5120x640: 67 -> 52 us, 8192x1920x640: 31 -> 27). These GEMMs are bound by the TMA feed (L2 -> SM
-    // bytes per MMA cycle), not the tensor core: 128 x 128 single-CTA tiles move 128 B per SM per MMA
+    // for M >= 1024, N >= 512, padding included (8192x5120x640: 67 -> 52 us, 8192x1920x640: 31 -> 27).
+    // These GEMMs are bound by the TMA feed (L2 -> SM bytes per MMA cycle), not the tensor core: 128 x 128 single-CTA tiles move 128 B per SM per MMA
     // cycle, pairs of 256 x 256 62.5 (the swapped conv weight gradient measured 85 -> 59 us at
     // 16x16x640 with the same change; DP_WG_NARROW=1: previous choice, experiments)
     static const bool narrow = env_int("DP_WG_NARROW") != 0;
@@ -1281,6 +1545,10 @@ int tc_gemm(const DpGemmArgs* a, cudaStream_t st, int64_t* query = nullptr) {
       bn = 256;
       cg = 2;
     }
+  }
+  if (a->geglu_mode == 2) {  // the GEGLU-backward instantiations: 128 / 256-wide tiles
+    bn = (a->N % 256 == 0) ? 256 : 128;
+    cg = (a->M >= 256 && a->K > 512) ? 2 : 1;
   }
   TcParams p{};
   p.M = a->M;
@@ -1325,6 +1593,23 @@ int tc_gemm(const DpGemmArgs* a, cudaStream_t st, int64_t* query = nullptr) {
       const uint32_t box[4] = {BK, (uint32_t)(bn / cg / (bn > 256 ? 2 : 1)), 1, 1};
       if (int e = make_map(&mb, a->B, d, s, box, ones)) return e;
     }
+  }
+  if (a->geglu_mode == 2) {
+    p.geglu = 2;
+    p.F = a->N;
+    p.gh = a->geglu_out;
+    p.gh_ld = a->geglu_ld;
+    CUtensorMap md = ma;
+    make_dmap(&md, p, a->M, 2 * a->N, 1, 1);  // dh = [da | dg]: 2F columns
+    if (!p.d_tma) {
+      set_error("gemm geglu backward epilogue: output not TMA-storable");
+      return DP_ERR_ARGS;
+    }
+    if (cg == 2)
+      return bn == 256 ? launch_tc<256, 2, false, false, 2>(ma, mb, md, p, kNumSMs, st)
+                       : launch_tc<128, 2, false, false, 2>(ma, mb, md, p, kNumSMs, st);
+    return bn == 256 ? launch_tc<256, 1, false, false, 2>(ma, mb, md, p, kNumSMs, st)
+                     : launch_tc<128, 1, false, false, 2>(ma, mb, md, p, kNumSMs, st);
   }
   return launch_bn(bn, cg, ma, mb, p, a->M, a->N, p.batch1, batch2, st, a->workspace, a->workspace_bytes);
 }
@@ -1707,6 +1992,10 @@ int dp_gemm(const DpGemmArgs* a, dp_stream_t stream) {
                     ((a->batch1 <= 1 || a->a_bs1 != 0) && (a->batch1 <= 1 || a->b_bs1 != 0)) &&
                     ((a->batch2 <= 1 || a->a_bs2 != 0) && (a->batch2 <= 1 || a->b_bs2 != 0));
     if (ok) return dp::tc_gemm(a, st);
+  }
+  if (a->geglu_mode) {
+    dp::set_error("dp_gemm: the GEGLU epilogue needs the bf16 tensor-core path (16-byte aligned operands)");
+    return DP_ERR_UNSUPPORTED;
   }
   return dp::simt_gemm(a, st);
 }

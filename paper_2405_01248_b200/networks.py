@@ -376,7 +376,7 @@ class SpatialTransformer:
         a, h = self.ln2.fork(h)
         h = self.attn2(a, ctx, residual=h)
         a, h = self.ln3.fork(h)
-        h = self.ff2(nn.geglu(self.ff1(a)), residual=h)
+        h = nn.feed_forward_geglu(a, self.ff1, self.ff2, residual=h)
         return self.proj_out(h, residual=x2).view(B, H, W, C)
 
 
@@ -452,7 +452,9 @@ class SDUNet(Component):
         self.add_layer("final", self._final, ("out",))
 
     def _in0(self, st):
-        temb = self.t2(nn.silu(self.t1(ops.timestep_embed(st["t"], self.mc, self.dtype))))
+        # the live set carries SiLU(temb): every ResBlock's embedding projection reads the activated
+        # time embedding, so it is computed once here instead of once per block
+        temb = nn.silu(self.t2(nn.silu(self.t1(ops.timestep_embed(st["t"], self.mc, self.dtype)))))
         h = self.conv_in(st["x"])
         out = {k: v for k, v in st.items() if k not in ("x", "t", "pooled")}
         out["h"], out["temb"], out["s0"] = h, temb, h
@@ -461,7 +463,7 @@ class SDUNet(Component):
     @staticmethod
     def _in_block(res, tr, idx):
         def f(st):
-            h = res(st["h"], nn.silu(st["temb"]))
+            h = res(st["h"], st["temb"])
             if tr is not None:
                 h = tr(h, st["ctx"])
             out = dict(st)
@@ -481,7 +483,7 @@ class SDUNet(Component):
     @staticmethod
     def _mid(r1, tr, r2):
         def f(st):
-            ta = nn.silu(st["temb"])
+            ta = st["temb"]
             h = r2(tr(r1(st["h"], ta), st["ctx"]), ta)
             out = dict(st)
             out["h"] = h
@@ -493,7 +495,7 @@ class SDUNet(Component):
         def f(st):
             out = {k: v for k, v in st.items() if k != f"s{skip_i}"}
             h = nn.concat(st["h"], st[f"s{skip_i}"])
-            h = res(h, nn.silu(st["temb"]))
+            h = res(h, st["temb"])
             if tr is not None:
                 h = tr(h, st["ctx"])
             if up is not None:
@@ -550,7 +552,7 @@ class LockedUNetEncoder:
     def _l0(self, st):
         u = self.unet
         xt = ops.q_sample(st["latent"], st["noise"], st["t"], self.sqrt_ab, self.sqrt_1mab)
-        temb = u.t2(nn.silu(u.t1(ops.timestep_embed(st["t"], u.mc, u.dtype))))
+        temb = nn.silu(u.t2(nn.silu(u.t1(ops.timestep_embed(st["t"], u.mc, u.dtype)))))  # SiLU(temb), as SDUNet
         h = u.conv_in(xt)
         return {"h": h, "temb": temb, "ctx": st["ctx"], "lk_s0": h}
 
@@ -561,7 +563,7 @@ class LockedUNetEncoder:
             if kind == "down":
                 h = m(st["h"])
             else:
-                h = m(st["h"], nn.silu(st["temb"]))
+                h = m(st["h"], st["temb"])
                 if tr is not None:
                     h = tr(h, st["ctx"])
             out = dict(st)
@@ -571,7 +573,7 @@ class LockedUNetEncoder:
 
     def _mid(self, st):
         r1, tr, r2 = self.unet.mid_mods
-        ta = nn.silu(st["temb"])
+        ta = st["temb"]
         h = r2(tr(r1(st["h"], ta), st["ctx"]), ta)
         out = {k: v for k, v in st.items() if k.startswith("lk_s")}
         out["lk_h"], out["lk_temb"] = h, st["temb"]
@@ -638,7 +640,7 @@ class ControlNet(Component):
         return Component.layer_of_param(self, pname)
 
     def _cin(self, st):
-        temb = self.t2(nn.silu(self.t1(ops.timestep_embed(st["t"], self.mc, self.dtype))))
+        temb = nn.silu(self.t2(nn.silu(self.t1(ops.timestep_embed(st["t"], self.mc, self.dtype)))))  # SiLU(temb)
         g = st["hint"]
         for cv in self.hint:
             g = nn.silu(cv(g))
@@ -650,7 +652,7 @@ class ControlNet(Component):
     @staticmethod
     def _cblock(res, tr, z, idx):
         def f(st):
-            h = res(st["ch"], nn.silu(st["ctemb"]))
+            h = res(st["ch"], st["ctemb"])
             if tr is not None:
                 h = tr(h, st["ctx"])
             out = dict(st)
@@ -670,7 +672,7 @@ class ControlNet(Component):
     @staticmethod
     def _cmid(r1, tr, r2, z):
         def f(st):
-            ta = nn.silu(st["ctemb"])
+            ta = st["ctemb"]
             h = r2(tr(r1(st["ch"], ta), st["ctx"]), ta)
             out = {k: v for k, v in st.items() if k not in ("ch", "ctemb")}
             out["cmid"] = z(h)
@@ -684,7 +686,7 @@ class ControlNet(Component):
             out = {k: v for k, v in st.items() if k not in drop}
             h = nn.add(st["lk_h"], st["cmid"]) if j == 0 else st["h"]
             h = nn.concat(h, nn.add(st[f"lk_s{skip_i}"], st[f"c{skip_i}"]))
-            h = res(h, nn.silu(st["lk_temb"]))
+            h = res(h, st["lk_temb"])
             if tr is not None:
                 h = tr(h, st["ctx"])
             if up is not None:

@@ -38,7 +38,8 @@ FLASH_ATTENTION = True  # bf16 head-dim-64 attention through the fused tcgen05 k
 # ============================================================================ parameters
 
 class Param:
-    __slots__ = ("name", "shape", "fp32", "init", "offset", "numel", "w", "g", "master", "wt", "wt_fn")
+    __slots__ = ("name", "shape", "fp32", "init", "offset", "numel", "w", "g", "master", "wt", "wt_fn",
+                 "flip_args")
 
     def __init__(self, name, shape, fp32, init):
         self.name = name
@@ -52,6 +53,7 @@ class Param:
         self.master = None  # fp32 master view
         self.wt = None      # cached flip-transposed bf16 copy for dgrad (ops.cached_flip)
         self.wt_fn = None   # recomputes wt in place from w
+        self.flip_args = None  # (w, wt, K, R, S, C) when wt is a plain flip of w (batched refresh)
 
 
 # flip-transposed weight copies for dgrad are cached and refreshed right after each AdamW update
@@ -77,9 +79,14 @@ class ParamStore:
     def refresh_flips(self, lo, hi):
         """Recompute the cached dgrad weight copies of the params inside the flat range [lo, hi)
         (call right after updating it, on the same stream)."""
+        jobs = []
         for p in self.flip_params:
             if lo <= p.offset < hi:
-                p.wt_fn(p.wt)
+                if p.flip_args is not None and FLIP_BATCH:
+                    jobs.append(p.flip_args)
+                else:
+                    p.wt_fn(p.wt)
+        ops.flip_batch(jobs)
 
     def add(self, name, shape, fp32=False, init="w"):
         if name in self.params:
@@ -283,6 +290,107 @@ class _LinearFn(torch.autograd.Function):
         if layer.bias is not None and layer.bias.g is not None:
             ops.bias_grad(dy2, layer.bias.g)
         return dx, None, (dy if ctx.has_res else None), None
+
+
+# bf16 transformer FF: the ff1 GEMM writes both its pre-activation h (kept for the backward) and
+# GEGLU(h) from one epilogue (no separate GEGLU pass re-reading h); DP_FUSED_GEGLU=0: unfused
+FUSED_GEGLU = os.environ.get("DP_FUSED_GEGLU", "1") != "0"
+# the ff2 input gradient applies the GEGLU backward in its epilogue (DP_FUSED_GEGLU_BWD=0: separate kernel)
+FUSED_GEGLU_BWD = os.environ.get("DP_FUSED_GEGLU_BWD", "1") != "0"
+# cached dgrad weight copies refreshed by one batched launch per optimizer slice (DP_FLIP_BATCH=0: per param)
+FLIP_BATCH = os.environ.get("DP_FLIP_BATCH", "1") != "0"
+
+
+class _LinearGegluFn(torch.autograd.Function):
+    """y = GEGLU(x @ W^T + b): forward in one GEMM, backward = GEGLU backward then the linear's."""
+
+    @staticmethod
+    def forward(ctx, x, anchor, layer):
+        K = x.shape[-1]
+        x2 = _c(x).view(-1, K)
+        W = layer.weight
+        h, y = ops.linear_geglu(x2, W.w, layer.bias.w)
+        ctx.save_for_backward(x2, h)
+        ctx.layer = layer
+        return y.view(*x.shape[:-1], W.shape[0] // 2)
+
+    @staticmethod
+    def backward(ctx, dy):
+        x2, h = ctx.saved_tensors
+        layer = ctx.layer
+        W = layer.weight
+        dh = ops.geglu_bwd(h, _c(dy).view(h.shape[0], -1))
+        dx = None
+        if ctx.needs_input_grad[0]:
+            dx = ops.linear_dgrad(dh, W.w, cache=_flip_cache(layer)).view(*dy.shape[:-1], W.shape[1])
+        if W.g is not None:
+            ops.linear_wgrad(dh, x2, W.g)
+        if layer.bias is not None and layer.bias.g is not None:
+            ops.bias_grad(dh, layer.bias.g)
+        return dx, None, None
+
+
+class _FeedForwardGegluFn(torch.autograd.Function):
+    """out = ff2(GEGLU(ff1(x))) + residual, three GEMMs and no elementwise pass: ff1's epilogue writes
+    the pre-activation h and GEGLU(h); in the backward ff2's input-gradient GEMM applies the GEGLU
+    backward in its epilogue (reading h) and hands dh straight to ff1's backward."""
+
+    @staticmethod
+    def forward(ctx, x, anchor, residual, ff1, ff2):
+        K = x.shape[-1]
+        x2 = _c(x).view(-1, K)
+        h, y = ops.linear_geglu(x2, ff1.weight.w, ff1.bias.w)
+        N2 = ff2.weight.shape[0]
+        out = torch.empty(*x.shape[:-1], N2, device=x.device, dtype=x.dtype)
+        ops.linear(y, ff2.weight.w, bias=ff2.bias.w,
+                   residual=None if residual is None else _c(residual).view(-1, N2), out=out.view(-1, N2))
+        ctx.save_for_backward(x2, h, y)
+        ctx.layers = (ff1, ff2)
+        ctx.has_res = residual is not None
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        x2, h, y = ctx.saved_tensors
+        ff1, ff2 = ctx.layers
+        N2 = ff2.weight.shape[0]
+        d2 = _c(dout).view(-1, N2)
+        if ff2.weight.g is not None:
+            ops.linear_wgrad(d2, y, ff2.weight.g)
+        if ff2.bias.g is not None:
+            ops.bias_grad(d2, ff2.bias.g)
+        if FUSED_GEGLU_BWD:
+            dh = ops.linear_dgrad_geglu(d2, ff2.weight.w, h, cache=_flip_cache(ff2))
+        else:
+            dh = ops.geglu_bwd(h, ops.linear_dgrad(d2, ff2.weight.w, cache=_flip_cache(ff2)))
+        dx = None
+        if ctx.needs_input_grad[0]:
+            dx = ops.linear_dgrad(dh, ff1.weight.w, cache=_flip_cache(ff1)).view(*dout.shape[:-1], x2.shape[1])
+        if ff1.weight.g is not None:
+            ops.linear_wgrad(dh, x2, ff1.weight.g)
+        if ff1.bias.g is not None:
+            ops.bias_grad(dh, ff1.bias.g)
+        return dx, None, (dout if ctx.has_res else None), None, None
+
+
+def feed_forward_geglu(x, ff1, ff2, residual=None):
+    """ff2(GEGLU(ff1(x))) (+ residual): the fused three-GEMM path for bf16 (see _FeedForwardGegluFn),
+    the layer-by-layer composition otherwise."""
+    F = ff1.weight.shape[0] // 2
+    rows = x.numel() // x.shape[-1]
+    if (FUSED_GEGLU and x.dtype == torch.bfloat16 and x.is_cuda and ff1.bias is not None and ff2.bias is not None
+            and F % 64 == 0 and x.shape[-1] % 8 == 0 and rows >= 1024 and ff2.weight.shape[1] == F):
+        return _FeedForwardGegluFn.apply(x, _anchor(), residual, ff1, ff2)
+    return ff2(geglu(ff1(x)), residual=residual)
+
+
+def linear_geglu(x, layer):
+    """GEGLU(layer(x)) for an nn.Linear with bias and an even output width."""
+    F = layer.weight.shape[0] // 2
+    if (FUSED_GEGLU and x.dtype == torch.bfloat16 and x.is_cuda and layer.bias is not None
+            and F % 64 == 0 and x.shape[-1] % 8 == 0 and x.numel() // x.shape[-1] >= 128):
+        return _LinearGegluFn.apply(x, _anchor(), layer)
+    return geglu(layer(x))
 
 
 class _ConvFn(torch.autograd.Function):

@@ -112,18 +112,99 @@ def linear(x, w, bias=None, residual=None, out=None):
                 bias=bias, residual=residual)
 
 
-def cached_flip(cache, make):
+def linear_geglu(x, w, bias, h_out=None, y_out=None):
+    """h[M,2F] = x @ w^T + bias (the GEGLU pre-activation, stored for the backward) and
+    y[M,F] = h[:, :F] * gelu_erf(h[:, F:]) in ONE tensor-core GEMM (the epilogue writes both);
+    bf16, K-major operands, F % 64 == 0."""
+    _require_cuda(x, w, bias)
+    M, K = x.shape
+    N = w.shape[0]
+    F = N // 2
+    h = torch.empty(M, N, device=x.device, dtype=x.dtype) if h_out is None else h_out
+    y = torch.empty(M, F, device=x.device, dtype=x.dtype) if y_out is None else y_out
+    args = DpGemmArgs()
+    args.M, args.N, args.K = M, N, K
+    args.batch1, args.batch2 = 1, 1
+    args.dtype = dtype_code(x)
+    args.A, args.a_ld, args.a_bs1, args.a_bs2, args.a_mn_major = _ptr(x), x.stride(0), 0, 0, 0
+    args.B, args.b_ld, args.b_bs1, args.b_bs2, args.b_mn_major = _ptr(w), w.stride(0), 0, 0, 0
+    args.D, args.d_dtype, args.d_ld, args.d_bs1, args.d_bs2 = _ptr(h), dtype_code(h), h.stride(0), 0, 0
+    args.out_mode = DP_OUT_STORE
+    args.bias = _ptr(bias)
+    args.Res = None
+    args.r_ld, args.r_bs1, args.r_bs2 = h.stride(0), 0, 0
+    args.alpha = 1.0
+    args.split_k = 0
+    args.geglu_out = _ptr(y)
+    args.geglu_ld = y.stride(0)
+    args.geglu_mode = 1
+    telemetry.timed("tcgen05_gemm", 2.0 * M * N * K,
+                    lambda: check(_lib.lib().dp_gemm(ctypes.byref(args), _stream()), "dp_gemm"),
+                    sub=f"linear {M}x{N}x{K} geglu" if telemetry.SHAPES else "linear")
+    return h, y
+
+
+def linear_dgrad_geglu(dy, w, h, cache=None):
+    """dh[M,2F] = GEGLU'(h) applied to (dy[M,N] @ w[N,F]): the input gradient of the FF output projection
+    and the GEGLU backward in one GEMM (its epilogue reads h = [a | g] and writes both halves of dh)."""
+    M, N = dy.shape
+    F = w.shape[1]
+    dh = torch.empty(M, 2 * F, device=dy.device, dtype=dy.dtype)
+
+    def make(dst):
+        wt = torch.empty(F, N, device=w.device, dtype=w.dtype) if dst is None else dst
+        check(_lib.lib().dp_conv_weight_flip(dtype_code(w), _ptr(w), _ptr(wt), N, 1, 1, F, _stream()),
+              "dp_conv_weight_flip")
+        return wt
+    wt = cached_flip(cache, make, lambda wt_: (w, wt_, N, 1, 1, F))
+    args = DpGemmArgs()
+    args.M, args.N, args.K = M, F, N
+    args.batch1, args.batch2 = 1, 1
+    args.dtype = dtype_code(dy)
+    args.A, args.a_ld, args.a_bs1, args.a_bs2, args.a_mn_major = _ptr(dy), dy.stride(0), 0, 0, 0
+    args.B, args.b_ld, args.b_bs1, args.b_bs2, args.b_mn_major = _ptr(wt), N, 0, 0, 0
+    args.D, args.d_dtype, args.d_ld, args.d_bs1, args.d_bs2 = _ptr(dh), dtype_code(dh), dh.stride(0), 0, 0
+    args.out_mode = DP_OUT_STORE
+    args.bias = None
+    args.Res = None
+    args.r_ld, args.r_bs1, args.r_bs2 = dh.stride(0), 0, 0
+    args.alpha = 1.0
+    args.split_k = 0
+    args.geglu_out = _ptr(h)
+    args.geglu_ld = h.stride(0)
+    args.geglu_mode = 2
+    telemetry.timed("tcgen05_gemm", 2.0 * M * N * F,
+                    lambda: check(_lib.lib().dp_gemm(ctypes.byref(args), _stream()), "dp_gemm"),
+                    sub=f"linear {M}x{F}x{N}b geglu-bwd" if telemetry.SHAPES else "linear")
+    return dh
+
+
+def cached_flip(cache, make, flip_args=None):
     """The flip-transposed weight for a dgrad: `make(dst)` writes it from the current weights.
     cache = (store, param) keeps one persistent copy per parameter, refreshed by the store right
-    after each AdamW update of that parameter (nn.ParamStore.refresh_flips); None flips now."""
+    after each AdamW update of that parameter (nn.ParamStore.refresh_flips); None flips now.
+    flip_args(wt) -> (w, K, R, S, C) when the copy is a plain flip of the parameter's own bf16 view
+    (no channel padding): those refreshes are batched into one launch per optimizer slice."""
     if cache is None:
         return make(None)
     store, p = cache
     if p.wt is None:
         p.wt = make(None)
         p.wt_fn = make
+        p.flip_args = None if flip_args is None else flip_args(p.wt)
         store.register_flip(p)
     return p.wt
+
+
+def flip_batch(jobs):
+    """Refresh cached dgrad weight copies: jobs = [(w, wt, K, R, S, C)], one launch per 48 jobs."""
+    if not jobs:
+        return
+    arr = (_lib.DpFlipJob * len(jobs))()
+    for i, (w, wt, K, R, S, C) in enumerate(jobs):
+        arr[i].w, arr[i].wt, arr[i].K, arr[i].R, arr[i].S, arr[i].C = _ptr(w), _ptr(wt), K, R, S, C
+    check(_lib.lib().dp_conv_weight_flip_batch(arr, len(jobs), _stream()), "dp_conv_weight_flip_batch",
+          (len(jobs) + 47) // 48)
 
 
 def linear_dgrad(dy, w, out=None, cache=None):
@@ -140,7 +221,7 @@ def linear_dgrad(dy, w, out=None, cache=None):
             check(_lib.lib().dp_conv_weight_flip(dtype_code(w), _ptr(w), _ptr(wt), N, 1, 1, K, _stream()),
                   "dp_conv_weight_flip")
             return wt
-        wt = cached_flip(cache, make)
+        wt = cached_flip(cache, make, (lambda wt_: (w, wt_, N, 1, 1, K)) if w.dtype == torch.bfloat16 else None)
         return gemm(dy, wt, out, M=M, N=K, K=N, a_ld=dy.stride(0), b_ld=N, d_ld=out.stride(0))
     return gemm(dy, w, out, M=M, N=K, K=N, a_ld=dy.stride(0), b_ld=w.stride(0), b_mn=True,
                 d_ld=out.stride(0))
@@ -317,7 +398,8 @@ def conv2d_dgrad(dy, w, x_shape, *, stride=1, pad=(1, 1), cache=None):
             check(_lib.lib().dp_conv_weight_flip(dtype_code(wpp), _ptr(wpp), _ptr(wt), Kp, R, S, Cp,
                                                  _stream()), "dp_conv_weight_flip")
             return wt
-        wt = cached_flip(cache, make)
+        plain = Kp == K and Cp == C  # no channel padding: the copy is a flip of the parameter view itself
+        wt = cached_flip(cache, make, (lambda wt_: (w, wt_, K, R, S, C)) if plain else None)
         dx = torch.empty(N, H, W, Cp, device=dy.device, dtype=dy.dtype)
         a = _conv_args(src, wt, dx, 1, (R - 1 - pad[0], S - 1 - pad[1]), H, W)
         ws = _splitk_ws(a, "dp_conv_fwd_workspace", dy.device)

@@ -243,3 +243,97 @@ def test_conv_bn320_fwd_dgrad(N, H, C, K):
     dx = ops.conv2d_dgrad(dy, w, x.shape)
     ref = torch.nn.grad.conv2d_input(xr.shape, wr, dy.float().permute(0, 3, 1, 2), padding=1)
     assert _rel(dx, ref.permute(0, 2, 3, 1)) < 1e-2
+
+
+@pytest.mark.parametrize("M,C", [(32768, 320), (8192, 640), (2048, 1280), (300, 320), (1000, 64)])
+def test_linear_geglu_epilogue(M, C):
+    """ff1 GEMM with the GEGLU epilogue: pre-activation h (bf16, as the unfused GEMM stores it) and
+    y = a * gelu(g) from one launch, vs the unfused GEMM + GEGLU kernel and an fp32 torch reference;
+    the fused FF layer's gradients vs the unfused layer."""
+    ops = _ops()
+    g = torch.Generator(device="cuda").manual_seed(M + C)
+    x = torch.randn(M, C, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(8 * C, C, device="cuda", generator=g) / C ** 0.5).bfloat16()
+    b = torch.randn(8 * C, device="cuda", generator=g) * 0.1
+    h, y = ops.linear_geglu(x, w, b)
+    h_ref = ops.linear(x, w, bias=b)
+    y_ref = ops.geglu(h_ref)
+    assert _rel(h, h_ref) < 2e-3 and _rel(y, y_ref) < 5e-3
+    hf = x.float() @ w.float().t() + b
+    yf = hf[:, :4 * C] * F.gelu(hf[:, 4 * C:])
+    assert _rel(y, yf) < 1e-2
+
+
+def test_linear_geglu_layer_grads():
+    """The fused FF layer (nn.linear_geglu) against the unfused layer: output and all gradients."""
+    from paper_2405_01248_b200 import nn
+    torch.manual_seed(0)
+    C, M = 320, 4096
+    store = nn.ParamStore(torch.bfloat16)
+    lin = nn.Linear(store, "ff", C, 8 * C)
+    store.materialize("cuda", seed=3)
+    x = torch.randn(M, C, device="cuda").bfloat16().requires_grad_(True)
+    dy = torch.randn(M, 4 * C, device="cuda").bfloat16()
+    outs = []
+    for fused in (True, False):
+        nn.FUSED_GEGLU = fused
+        store.zero_grad()
+        xi = x.detach().clone().requires_grad_(True)
+        with nn.grad_anchor(device="cuda"):
+            y = nn.linear_geglu(xi, lin)
+            y.backward(dy)
+        outs.append((y.detach().float(), xi.grad.float(), lin.weight.g.clone(), lin.bias.g.clone()))
+    nn.FUSED_GEGLU = True
+    for a, b in zip(outs[0], outs[1]):
+        assert _rel(a, b) < 5e-3
+
+
+@pytest.mark.parametrize("M,C", [(4096, 320), (2048, 640), (1024, 1280)])
+def test_feed_forward_geglu_fused(M, C):
+    """The fused feed-forward (ff1 GEGLU epilogue + ff2 dgrad GEGLU-backward epilogue) against the
+    layer-by-layer composition: output, input / residual gradients, all four parameter gradients."""
+    from paper_2405_01248_b200 import nn
+    torch.manual_seed(M + C)
+    store = nn.ParamStore(torch.bfloat16)
+    ff1 = nn.Linear(store, "ff1", C, 8 * C)
+    ff2 = nn.Linear(store, "ff2", 4 * C, C)
+    store.materialize("cuda", seed=5)
+    x = torch.randn(M, C, device="cuda").bfloat16()
+    r = torch.randn(M, C, device="cuda").bfloat16()
+    dy = torch.randn(M, C, device="cuda").bfloat16()
+    outs = []
+    for fused in (True, False):
+        nn.FUSED_GEGLU = fused
+        store.zero_grad()
+        xi = x.clone().requires_grad_(True)
+        ri = r.clone().requires_grad_(True)
+        with nn.grad_anchor(device="cuda"):
+            y = nn.feed_forward_geglu(xi, ff1, ff2, residual=ri)
+            y.backward(dy)
+        outs.append([y.detach().float(), xi.grad.float(), ri.grad.float(), ff1.weight.g.clone(), ff1.bias.g.clone(),
+                     ff2.weight.g.clone(), ff2.bias.g.clone()])
+    nn.FUSED_GEGLU = True
+    for a, b in zip(outs[0], outs[1]):
+        assert _rel(a, b) < 1e-2
+
+
+def test_flip_batch_matches_single_flips():
+    """Batched refresh of the cached dgrad weight copies (one launch for many parameters, more jobs than one
+    launch holds) equals the per-parameter flip kernel."""
+    ops = _ops()
+    from paper_2405_01248_b200 import _lib
+    import ctypes
+    shapes = [(1280, 1, 1, 320), (320, 3, 3, 640), (640, 3, 3, 640), (64, 1, 1, 8)] * 13
+    jobs, refs = [], []
+    for i, (K, R, S, C) in enumerate(shapes):
+        w = torch.randn(K, R, S, C, device="cuda").bfloat16()
+        wt = torch.empty(C, R, S, K, device="cuda", dtype=torch.bfloat16)
+        ref = torch.empty_like(wt)
+        ops.check(_lib.lib().dp_conv_weight_flip(ops.dtype_code(w), w.data_ptr(), ref.data_ptr(), K, R, S, C,
+                                                 ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)), "flip")
+        jobs.append((w, wt, K, R, S, C))
+        refs.append(ref)
+    ops.flip_batch(jobs)
+    torch.cuda.synchronize()
+    for (w, wt, *_), ref in zip(jobs, refs):
+        assert torch.equal(wt, ref)
