@@ -374,7 +374,11 @@ class Trainer:
             raise ValueError("CUDA-graph replay needs world == 1 and a fixed self-conditioning branch")
         if self.it == 0 and not self.ex.frozen_ready:
             self.warmup_frozen()
-        self.ex.streams = _Streams(self.ex.device, single=True)
+        # multi-stream capture: the executor's compute stream forks from the capturing stream and the
+        # optimizer stream from compute events, so the AdamW slices stay overlapped with the backward
+        # inside the graph (DP_GRAPH_SINGLE_STREAM=1: everything on the capture stream)
+        if os.environ.get("DP_GRAPH_SINGLE_STREAM", "0") != "0":
+            self.ex.streams = _Streams(self.ex.device, single=True)
         torch.cuda.synchronize()
         self._g_cur = InputFeed(make_batch(self.data_spec, self.it), self.device, self.cfg.dtype, "device")
         self._g_nxt = InputFeed(make_batch(self.data_spec, self.it + 1), self.device, self.cfg.dtype, "device")

@@ -295,8 +295,10 @@ class _LinearFn(torch.autograd.Function):
 # bf16 transformer FF: the ff1 GEMM writes both its pre-activation h (kept for the backward) and
 # GEGLU(h) from one epilogue (no separate GEGLU pass re-reading h); DP_FUSED_GEGLU=0: unfused
 FUSED_GEGLU = os.environ.get("DP_FUSED_GEGLU", "1") != "0"
-# the ff2 input gradient applies the GEGLU backward in its epilogue (DP_FUSED_GEGLU_BWD=0: separate kernel)
-FUSED_GEGLU_BWD = os.environ.get("DP_FUSED_GEGLU_BWD", "1") != "0"
+# the ff2 input gradient applying the GEGLU backward in its epilogue (DP_FUSED_GEGLU_BWD=1) measured slower
+# than the dgrad GEMM + the vectorised GEGLU-backward kernel (140 vs 125 us at 32768x320: the epilogue's
+# per-row reads of h), so it is off by default
+FUSED_GEGLU_BWD = os.environ.get("DP_FUSED_GEGLU_BWD", "0") != "0"
 # cached dgrad weight copies refreshed by one batched launch per optimizer slice (DP_FLIP_BATCH=0: per param)
 FLIP_BATCH = os.environ.get("DP_FLIP_BATCH", "1") != "0"
 

@@ -225,6 +225,9 @@ class Links:
 _DEBUG = bool(int(__import__("os").environ.get("DP_DEBUG_P2P", "0")))
 _OVL_SIDE = __import__("os").environ.get("DP_OVL_STREAM", "opt") == "opt"  # experiments: "compute"
 _EARLY_TAIL = bool(int(__import__("os").environ.get("DP_EARLY_TAIL", "0")))  # experiments
+# single-device frozen tail (no transfers) replayed as one CUDA graph per (program, tail): the ~350 launches of
+# the next batch's VAE + text-encoder forwards leave the host's critical path (DP_TAIL_GRAPH=0: eager)
+_TAIL_GRAPH = bool(int(__import__("os").environ.get("DP_TAIL_GRAPH", "1")))
 
 
 class _Tracer:
@@ -458,6 +461,45 @@ class PipelineExecutor:
                 self._recv_frozen_upto(prog, store, max(need), posted)
             out = self._run_frozen_piece(piece, store, raw)
             self._post_frozen_sends(prog, piece, out, sent)
+
+    def _tail_graphable(self, prog):
+        from . import telemetry
+
+        # not inside another capture (whole-iteration graphs), not while the bench brackets every launch
+        return (_TAIL_GRAPH and self.world == 1 and self.streams.cuda and not prog.transfers
+                and all(piece.device == self.dev for piece in prog.tail)
+                and not telemetry.timer.active and not torch.cuda.is_current_stream_capturing())
+
+    def _run_tail_graphed(self, prog, store, raw):
+        """The frozen tail of a single-device program as one CUDA graph: the next batch's raw fields are
+        copied into static buffers, the graph replays every piece, and the outputs the delivery reads
+        (the last layer of each component) are cloned out of the graph's memory pool (the next replay
+        overwrites it while this iteration's successor still consumes them)."""
+        key = id(prog)
+        ent = self._tail_graphs.get(key) if hasattr(self, "_tail_graphs") else None
+        if ent is None:
+            if not hasattr(self, "_tail_graphs"):
+                self._tail_graphs = {}
+            fields = sorted({f for piece in prog.tail if piece.layer == 0
+                             for f in self.model.frozen[piece.comp].inputs})
+            lo0 = min(piece.lo for piece in prog.tail)
+            hi0 = max(piece.hi for piece in prog.tail)
+            static = {f: raw(f, lo0, hi0).clone() for f in fields}
+            sraw = lambda f, lo, hi: static[f][lo - lo0:hi - lo0]  # noqa: E731
+            finals = {(t.comp, t.layer) for t in prog.deliveries}
+            cap_store = {}
+            g = torch.cuda.CUDAGraph()
+            cur = torch.cuda.current_stream(self.device)
+            with torch.cuda.graph(g, stream=cur):
+                self._run_pieces(prog, prog.tail, cap_store, sraw, {}, set())
+            ent = dict(graph=g, static=static, lo0=lo0, hi0=hi0, fields=fields,
+                       outs={k: v for k, v in cap_store.items() if k in finals})
+            self._tail_graphs[key] = ent
+        for f in ent["fields"]:
+            ent["static"][f].copy_(raw(f, ent["lo0"], ent["hi0"]), non_blocking=True)
+        ent["graph"].replay()
+        for k, parts in ent["outs"].items():
+            store.setdefault(k, []).extend((a, b, {n: v.clone() for n, v in st.items()}) for a, b, st in parts)
 
     def _deliver(self, prog, store, posted):
         """Final frozen outputs -> first-stage owners of every pipe (used next iteration)."""
@@ -779,6 +821,14 @@ class PipelineExecutor:
                 self._last_m[ins[3]] = ins[1]
         task = tr.task if tr else (lambda *a, **k: contextlib.nullcontext())
         last_compute_ev = None
+        if self.streams.cuda:
+            # every stream of the iteration is forked from the caller's stream: ordered after its work, and
+            # part of a CUDA-graph capture that runs on it (a join with a never-forked stream would make the
+            # capture depend on uncaptured work)
+            cur = torch.cuda.current_stream(self.device)
+            for st in (self.streams.compute, self.streams.fill, self.opt_stream):
+                if st is not None:
+                    st.wait_stream(cur)
         instrs = prog.device_program(self.dev).instrs
         early_tail = _EARLY_TAIL and self.world == 1 and self.streams.cuda and has_next and bool(prog.tail)
         if early_tail:
@@ -814,7 +864,10 @@ class PipelineExecutor:
                 self.streams.join()
                 # leftover frozen work: busy time (planner.py:172-175), recorded as a fill task
                 with self.streams.on("compute"), task("compute", "fill", tag="tail"):
-                    self._run_pieces(prog, prog.tail, store, raw_next, posted, sent)
+                    if self._tail_graphable(prog) and not trace:
+                        self._run_tail_graphed(prog, store, raw_next)
+                    else:
+                        self._run_pieces(prog, prog.tail, store, raw_next, posted, sent)
             elif kind == "deliver":
                 self.streams.join()
                 with self.streams.on("compute"), task("compute", "p2p_comm", tag="deliver"):
