@@ -3,16 +3,16 @@
 // One CTA = one 128-query tile of one (batch, head); 4 warps, thread t owns query row t.
 //   * TMA loads Q once and streams 128-key K/V tiles (K and V double-buffered) from the strided
 //     [B, N, heads*64] activations (fused qkv / kv tensors, no copies);
-//   * thread 0 issues tcgen05.mma: S = Q K^T into TMEM (128 fp32 columns) one tile ahead of the
-//     softmax, and O += P V_j into TMEM (64 columns) with P read from shared memory;
+//   * thread 0 issues tcgen05.mma: S = Q K^T into TMEM (128 fp32 columns), and O += P V_j into TMEM
+//     (64 columns) with P read from TMEM (64 columns of bf16 pairs, the MMA's A operand);
 //   * all 128 threads run the online softmax on their S row straight from TMEM (tcgen05.ld) with
 //     packed f32x2 math (FFMA2 / FADD2, three-input FMNMX), part of the exponentials on the FMA
-//     pipe (ex2_poly2), write P = exp2(S*scale*log2e - m) as bf16 into the SWIZZLE_128B K-major
-//     layout the MMA reads; the running max moves only past a threshold, so the O rescale in
+//     pipe (ex2_poly2), write P = exp2(S*scale*log2e - m) as bf16 pairs back into TMEM (no
+//     shared-memory round trip); the running max moves only past a threshold, so the O rescale in
 //     TMEM is rare (FA4-style lazy correction);
 //   * epilogue: O / l (TMEM -> registers) staged through shared memory and written by one TMA
 //     tensor store, log-sum-exp saved for the backward pass.
-// Two CTAs fit per SM (113 KB shared memory, 256 TMEM columns each), so one CTA's softmax
+// Two CTAs fit per SM (81 KB shared memory, 256 TMEM columns each), so one CTA's softmax
 // overlaps the other's MMAs. Keys beyond N_k (cross-attention, 77 tokens) are masked.
 #include <cstdlib>
 #include <type_traits>
@@ -87,10 +87,8 @@ __global__ void __launch_bounds__(128, 2)
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + TILE_BYTES;          // 2 buffers
   uint8_t* sV = sK + 2 * TILE_BYTES;      // 2 buffers
-  uint8_t* sP = sV + 2 * TILE_BYTES;      // 2 x 16 KB (keys 0-63, 64-127)
-  // barriers in the alignment slack when it has room, else after the tiles: the request is exactly
-  // 7 tiles + 1 KB, so two CTAs (+ 1 KB system reservation each) fill the SM's 228 KB
-  uint64_t* bar = reinterpret_cast<uint64_t*>(pad >= 64 ? smem_raw : sP + 2 * TILE_BYTES);
+  // barriers in the alignment slack when it has room, else after the tiles (5 tiles + 1 KB requested)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(pad >= 64 ? smem_raw : sV + 2 * TILE_BYTES);
   uint64_t* bar_q = bar;
   uint64_t* bar_k = bar + 1;  // [2]
   uint64_t* bar_v = bar + 3;  // [2]
@@ -118,14 +116,15 @@ __global__ void __launch_bounds__(128, 2)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_s = tmem;          // S: columns [0, 128)
-  const uint32_t t_o = tmem + 128;    // O_j: columns [128, 192)
+  const uint32_t t_o = tmem + 128;    // O: columns [128, 192)
+  const uint32_t t_p = tmem + 192;    // P (bf16 pairs, 128 keys): columns [192, 256), A operand of PV
   const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
   const uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, 0, 0);
   const uint32_t idesc_o = idesc_bf16_f32(BQ, HD, 0, 1);
 
   // Pipeline per key tile j (one MMA-issuing thread, in-order tensor pipe):
   //   once P(j) is in shared memory, PV(j) (accumulating into O in TMEM) and S(j+1) are issued back
-  //   to back; the wait for S(j+1) covers PV(j), so sP and O are free for softmax(j+1).
+  //   to back; the wait for S(j+1) covers PV(j), so P and O are free for softmax(j+1).
   //   K and V are double-buffered (V(j+1) streams in while tile j's softmax runs).
   auto issue_s = [&](int j) {
     const int kb = j & 1;
@@ -197,9 +196,11 @@ __global__ void __launch_bounds__(128, 2)
         m_use = m_run;
         alpha = 1.f;
       }
-      // P = exp2(s*scale - m) -> bf16 -> shared (SWIZZLE_128B K-major rows); PV(j-1) has read sP.
+      // P = exp2(s*scale - m) -> bf16 pairs -> TMEM (the A operand of PV: no shared-memory round trip);
+      // PV(j-1) has read it (complete before S(j)).
       // Packed f32x2 arithmetic (FFMA2 / FADD2) halves the FMA-pipe instructions per score.
       const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-m_use, -m_use);
+      uint32_t pk[32];  // 64 keys of P as bf16 pairs (one TMEM store per 64 keys)
 #pragma unroll
       for (int c = 0; c < BKV / 32; ++c) {
         float pv[32];
@@ -223,17 +224,9 @@ __global__ void __launch_bounds__(128, 2)
           pv[i + 1] = e.y;
           ls2[(i / 2) & 3] = __fadd2_rn(ls2[(i / 2) & 3], e);
         }
-        uint8_t* blk = sP + (c >> 1) * TILE_BYTES + row * 128;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int chunk = (c & 1) * 4 + q;  // 16-byte chunk of the 128-byte row
-          uint4 u;
-          u.x = pack_bf16x2(pv[q * 8 + 0], pv[q * 8 + 1]);
-          u.y = pack_bf16x2(pv[q * 8 + 2], pv[q * 8 + 3]);
-          u.z = pack_bf16x2(pv[q * 8 + 4], pv[q * 8 + 5]);
-          u.w = pack_bf16x2(pv[q * 8 + 6], pv[q * 8 + 7]);
-          *reinterpret_cast<uint4*>(blk + ((chunk ^ (row & 7)) * 16)) = u;
-        }
+        for (int i = 0; i < 16; ++i) pk[(c & 1) * 16 + i] = pack_bf16x2(pv[2 * i], pv[2 * i + 1]);
+        if (c & 1) tmem_st_32x32(t_p + lane_off + (c >> 1) * 32, pk);  // keys 64*(c>>1) .. +64
       }
     };
     if (__all_sync(0xffffffffu, valid >= BKV))
@@ -260,20 +253,19 @@ __global__ void __launch_bounds__(128, 2)
       }
       tmem_st_wait();
     }
-    fence_async_shared();
+    tmem_st_wait();
     tc_fence_before();
-    __syncthreads();  // P(j) in shared memory; S(j) read and O rescaled in TMEM by every thread
+    __syncthreads();  // P(j) in TMEM; S(j) read and O rescaled in TMEM by every thread
     if (tid == 0) {
       tc_fence_after();
       const int vb = j & 1;
       mbar_wait(&bar_v[vb], (j >> 1) & 1);
       tc_fence_after();
-      const uint32_t pa = smem_u32(sP), va = smem_u32(sV + vb * TILE_BYTES);
+      const uint32_t va = smem_u32(sV + vb * TILE_BYTES);
 #pragma unroll
       for (int k = 0; k < BKV / 16; ++k) {
-        const uint64_t ad = smem_desc_sw128(pa + (k >> 2) * TILE_BYTES + (k & 3) * 32, 16, 1024);
         const uint64_t bd = smem_desc_sw128(va + k * 2048, 8192, 1024);
-        tc_mma_bf16(t_o, ad, bd, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+        tc_mma_bf16_ts(t_o, t_p + k * 8, bd, idesc_o, (j > 0 || k > 0) ? 1u : 0u);  // 16 keys = 8 columns
       }
       tc_commit(bar_o);
       // S(j+1) behind PV(j): the wait for S(j+1) then also covers PV(j) (in-order tensor pipe), so
@@ -301,7 +293,7 @@ __global__ void __launch_bounds__(128, 2)
   mbar_wait(bar_o, (ntiles - 1) & 1);
   tc_fence_after();
   const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-  uint8_t* so = sP;  // the P buffer is free: the last PV MMA completed
+  uint8_t* so = sQ;  // Q is free: the last S MMA completed before the last PV
 #pragma unroll
   for (int c = 0; c < HD / 32; ++c) {
     uint32_t ov[32];
@@ -335,7 +327,7 @@ __global__ void __launch_bounds__(128, 2)
   }
 }
 
-constexpr size_t SMEM = 1024 + 7 * TILE_BYTES;
+constexpr size_t SMEM = 1024 + 5 * TILE_BYTES;
 
 // ------------------------------------------------------------------ backward
 // D[b][h][n] = sum_d dO[b][n][h*64+d] * O[b][n][h*64+d]: rows taken in memory order (b, n, h), eight
