@@ -228,6 +228,9 @@ _EARLY_TAIL = bool(int(__import__("os").environ.get("DP_EARLY_TAIL", "0")))  # e
 # single-device frozen tail (no transfers) replayed as one CUDA graph per (program, tail): the ~350 launches of
 # the next batch's VAE + text-encoder forwards leave the host's critical path (DP_TAIL_GRAPH=0: eager)
 _TAIL_GRAPH = bool(int(__import__("os").environ.get("DP_TAIL_GRAPH", "1")))
+# the compute stream joins the optimizer stream at the end of the iteration instead of at the sync task
+# (DP_LATE_OPT_JOIN=0: at the sync task, the previous behaviour)
+_LATE_OPT_JOIN = bool(int(__import__("os").environ.get("DP_LATE_OPT_JOIN", "1")))
 
 
 class _Tracer:
@@ -611,13 +614,19 @@ class PipelineExecutor:
                     self.grad_snapshot_pipes.append(self.prog.pipes[pi].backbone)
                 # background chunks: one CTA per SM at most (see dp_adamw_apply); the final chunk
                 # at the sync point has the machine to itself
-                store.adamw_apply((a, b), max_ctas=0 if final else self.OVERLAP_CTAS, zero_grad=True,
+                store.adamw_apply((a, b), max_ctas=0 if (final and not _LATE_OPT_JOIN) else self.OVERLAP_CTAS,
+                                  zero_grad=True,
                                   **self.model.adamw)
 
     def _sync_overlapped(self, pi):
         lo_l, _ = self.prog.pipes[pi].stage_ranges[self.stages[pi]]
         self._update_layers(pi, lo_l, final=True)
-        self.streams.compute.wait_stream(self.opt_stream)
+        if not _LATE_OPT_JOIN:
+            self.streams.compute.wait_stream(self.opt_stream)
+        # else: the compute stream joins the optimizer stream at the END of the iteration, so the last AdamW
+        # slices (HBM-bound) run under the frozen tail / fills that follow the sync (tensor-bound VAE convs,
+        # text-encoder GEMMs), which never read the backbone's parameters; the next iteration's forward
+        # is ordered after every update by that join
 
     def _spec(self, pi, boundary):
         return self.live_specs[pi][boundary]
@@ -876,6 +885,8 @@ class PipelineExecutor:
                     for w in self._pending:
                         w.wait()
         if self.streams.cuda:
+            if self.opt_stream is not None:
+                self.streams.compute.wait_stream(self.opt_stream)
             torch.cuda.current_stream(self.device).wait_stream(self.streams.compute)
         return self.loss_buf
 
