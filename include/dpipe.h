@@ -91,6 +91,7 @@ typedef struct DpGemmArgs {
 /* 2-D convolution over NHWC activations with weights [K][R][S][C].
  * Output y is NHWC [N][P][Q][K]. pad_h/pad_w are the top/left paddings;
  * the bottom/right padding is implied by P, Q (zero outside the input). */
+#define DP_GN_SLOTS 16
 typedef struct DpConvArgs {
   int dtype;
   int N, H, W, C;
@@ -107,6 +108,12 @@ typedef struct DpConvArgs {
   int split_k;
   float* workspace; /* as DpGemmArgs::workspace (conv fwd / dgrad) */
   int64_t workspace_bytes;
+  /* conv fwd, bf16: GroupNorm statistics of the output for its consumer (gn_groups groups, K / gn_groups a
+     power of two in [4, 32], P*Q % 32 == 0): gn_sums[slot][n][g] = partial {sum, sum of squares} over the
+     stored (bf16) values in DP_GN_SLOTS copies (spreads the reductions), zeroed and accumulated by the
+     launch; read by dp_group_norm_fwd_sums. NULL: off. */
+  float* gn_sums;
+  int gn_groups;
 } DpConvArgs;
 
 /* Multi-head attention over strided [B][N][heads*head_dim] activations (q, k, v may be
@@ -260,6 +267,10 @@ size_t dp_group_norm_workspace(int N, int HW, int G);
 int dp_group_norm_fwd(int dtype, const void* x, const float* gamma, const float* beta, void* y,
                       float* mean, float* rstd, int N, int HW, int C, int G, float eps, int silu,
                       float* workspace, dp_stream_t stream);
+/* GroupNorm(+SiLU) forward from statistics the producer accumulated (DpConvArgs::gn_sums): one pass over x */
+int dp_group_norm_fwd_sums(int dtype, const void* x, const float* gamma, const float* beta, void* y,
+                           float* mean, float* rstd, int N, int HW, int C, int G, float eps, int silu,
+                           const float* sums, dp_stream_t stream);
 /* dx (+)= ..., dgamma/dbeta fp32 accumulated (may be NULL) */
 int dp_group_norm_bwd(int dtype, const void* x, const void* dy, const float* gamma,
                       const float* beta, const float* mean, const float* rstd, void* dx,

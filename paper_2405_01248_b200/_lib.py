@@ -53,6 +53,7 @@ class DpConvArgs(ctypes.Structure):
         ("out_mode", c_int),
         ("split_k", c_int),
         ("workspace", c_void_p), ("workspace_bytes", c_i64),
+        ("gn_sums", c_void_p), ("gn_groups", c_int),
     ]
 
 
@@ -123,6 +124,8 @@ _SIGNATURES = {
     "dp_group_norm_workspace": [c_int, c_int, c_int],
     "dp_group_norm_fwd": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
                           c_int, c_int, c_int, c_float, c_int, c_void_p, c_void_p],
+    "dp_group_norm_fwd_sums": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
+                               c_int, c_int, c_int, c_float, c_int, c_void_p, c_void_p],
     "dp_group_norm_bwd": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                           c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
                           c_void_p, c_void_p],

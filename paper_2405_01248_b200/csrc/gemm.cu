@@ -49,6 +49,8 @@ struct TcParams {
                    // output range), 2 = backward through the FF output projection's dgrad (N = F)
   const void* gh;  // geglu 2: the pre-activation h = [a | g], bf16 [M][2F], row stride gh_ld
   int64_t gh_ld;
+  float* gn_sums;  // GroupNorm statistics epilogue (GEG == 3): [samples][G][2] {sum, sum of squares}
+  int gn_lg, gn_hw, gn_G;  // log2(channels per group), output pixels per sample, groups
   void* D;
   int64_t d_ld, d_bs1, d_bs2;
   int d_f32, out_mode, vec_ok;
@@ -278,6 +280,50 @@ DP_DEV void stage_row_bf16(uint8_t* buf, int lane, const float (&f)[32]) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(buf + lane * 64 + qs * 16)),
                  "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w)
                  : "memory");
+  }
+}
+
+// GroupNorm statistics of one 32 x 32 output chunk (GEG == 3 conv launches): the bf16-rounded values (what
+// the consumer reads) summed per group of 2^lg consecutive channels inside each lane's row by a fixed
+// tree, reduced over the warp's 32 rows (one sample: P*Q % 32 == 0), one atomic pair per group and chunk.
+// The GroupNorm that follows then reads x once (dp_group_norm_fwd_sums) instead of twice.
+DP_DEV void gn_stats_chunk(const TcParams& p, const float (&f)[32], int row, int row0, int n, int lane) {
+  if (row0 >= p.M) return;  // warp-uniform
+  const bool live = row < p.M;
+  float s1[16], q1[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float a = live ? __bfloat162float(__float2bfloat16_rn(f[2 * j])) : 0.f;
+    const float b = live ? __bfloat162float(__float2bfloat16_rn(f[2 * j + 1])) : 0.f;
+    s1[j] = a + b;
+    q1[j] = fmaf(a, a, b * b);
+  }
+  // pairwise tree up to 2^lg channels per group: s1 holds groups of 2, then 4, 8, 16, 32
+#pragma unroll
+  for (int lvl = 1; lvl < 5; ++lvl) {
+    if (lvl >= p.gn_lg) break;  // uniform
+#pragma unroll
+    for (int j = 0; j < (16 >> lvl); ++j) {
+      s1[j] = s1[2 * j] + s1[2 * j + 1];
+      q1[j] = q1[2 * j] + q1[2 * j + 1];
+    }
+  }
+  const int m = 32 >> p.gn_lg;  // groups in this chunk
+  const int sample = row0 / p.gn_hw;
+  // DP_GN_SLOTS copies of the table (CTA b adds into copy b % slots): thousands of tiles add into the
+  // same few (sample, group) entries, and same-address reductions serialise in L2
+  const int slot = blockIdx.x % DP_GN_SLOTS;
+  float* out = p.gn_sums + (((int64_t)slot * (p.M / p.gn_hw) + sample) * p.gn_G + (n >> p.gn_lg)) * 2;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (j >= m) break;
+    float a = s1[j], b = q1[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (lane == 0) atomicAdd(reinterpret_cast<float2*>(out + 2 * j), make_float2(a, b));
   }
 }
 
@@ -901,6 +947,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         } else if (p.d_tma) {
           float f[32];
           epilogue_math<BN>(p, row, n, wk.z1, wk.z2, v, f, rc, use_pre);
+          if constexpr (GEG == 3) gn_stats_chunk(p, f, row, row0, n, lane);
           uint8_t* buf = ebuf + (chunk_seq & 1) * EPI_STAGE_BYTES;
           if (chunk_seq >= 2) {
             if (lane == 0) bulk_wait_read<1>();
@@ -1700,6 +1747,45 @@ int tc_conv_fwd(const DpConvArgs* a, cudaStream_t st, int64_t* query = nullptr) 
     const uint32_t box[4] = {BK, (uint32_t)(bn / cg / (bn > 256 ? 2 : 1)), 1, 1};
     const uint32_t ones[4] = {1, 1, 1, 1};
     if (int e = make_map(&mb, a->w, d, s, box, ones)) return e;
+  }
+  if (a->gn_sums) {
+    // GroupNorm statistics epilogue (GEG == 3 instantiations: 128 / 256-wide tiles, no split-K)
+    const int G = a->gn_groups;
+    const int cpg = G > 0 ? a->K / G : 0;
+    int lg = 0;
+    while ((1 << lg) < cpg) ++lg;
+    if (a->dtype != DP_BF16 || a->out_mode != DP_OUT_STORE || G <= 0 || a->K % G || (1 << lg) != cpg || lg < 2 ||
+        lg > 5 || (a->P * a->Q) % 32 || (bn != 128 && bn != 256) || reinterpret_cast<uintptr_t>(a->gn_sums) % 16) {
+      set_error("conv gn_sums: bf16 store, K / gn_groups a power of two in [4, 32], P*Q % 32 == 0, 128/256 tiles");
+      return DP_ERR_UNSUPPORTED;
+    }
+    p.gn_sums = a->gn_sums;
+    p.gn_lg = lg;
+    p.gn_hw = a->P * a->Q;
+    p.gn_G = G;
+    cudaError_t e = cudaMemsetAsync(a->gn_sums, 0, sizeof(float) * 2 * (size_t)DP_GN_SLOTS * a->N * G, st);
+    if (e != cudaSuccess) {
+      set_error(std::string("gn_sums memset: ") + cudaGetErrorString(e));
+      return e;
+    }
+    CUtensorMap md = ma;
+    make_dmap(&md, p, p.M, p.N, 1, 1);
+    if (p.d_tma != 1) {
+      set_error("conv gn_sums: output not TMA-storable");
+      return DP_ERR_UNSUPPORTED;
+    }
+    if (p.halo) {
+      if (cg == 2)
+        return bn == 256 ? launch_tc<256, 2, true, false, 3>(ma, mb, md, p, kNumSMs, st)
+                         : launch_tc<128, 2, true, false, 3>(ma, mb, md, p, kNumSMs, st);
+      return bn == 256 ? launch_tc<256, 1, true, false, 3>(ma, mb, md, p, kNumSMs, st)
+                       : launch_tc<128, 1, true, false, 3>(ma, mb, md, p, kNumSMs, st);
+    }
+    if (cg == 2)
+      return bn == 256 ? launch_tc<256, 2, false, false, 3>(ma, mb, md, p, kNumSMs, st)
+                       : launch_tc<128, 2, false, false, 3>(ma, mb, md, p, kNumSMs, st);
+    return bn == 256 ? launch_tc<256, 1, false, false, 3>(ma, mb, md, p, kNumSMs, st)
+                     : launch_tc<128, 1, false, false, 3>(ma, mb, md, p, kNumSMs, st);
   }
   return launch_bn(bn, cg, ma, mb, p, p.M, p.N, 1, 1, st, a->workspace, a->workspace_bytes);
 }

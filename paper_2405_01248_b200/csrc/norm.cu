@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(GN_THREADS, 4)
                     const float* __restrict__ beta, T* __restrict__ y,
                     float* __restrict__ mean_out, float* __restrict__ rstd_out,
                     const float* __restrict__ part, int HW, int C, int G, int ppc, int CB, float eps,
-                    int silu_on) {
+                    int silu_on, const float* __restrict__ sums) {
   DP_PDL_ENTRY();
   constexpr int V = NV<T>::V;
   const int n = blockIdx.y, chunk = blockIdx.x, nchunks = gridDim.x;
@@ -259,11 +259,26 @@ __global__ void __launch_bounds__(GN_THREADS, 4)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int gi = warp; gi < gb; gi += GN_WARPS) {
     Welford a{0.f, 0.f, 0.f};
-    for (int k = lane; k < nchunks; k += 32) {
-      const float* q = part + (((int64_t)n * nchunks + k) * G + g0 + gi) * 3;
-      a = wf_merge(a, Welford{q[0], q[1], q[2]});
+    if (sums) {
+      // (sum, sum of squares) accumulated by the producing conv's epilogue
+      const float cnt = static_cast<float>(HW) * cg;
+      float s1 = 0.f, s2 = 0.f;
+      const int nsamp = gridDim.y;
+      for (int k = 0; k < DP_GN_SLOTS; ++k) {
+        const float* q = sums + (((int64_t)k * nsamp + n) * G + g0 + gi) * 2;
+        s1 += q[0];
+        s2 += q[1];
+      }
+      a.n = cnt;
+      a.mean = s1 / cnt;
+      a.m2 = fmaxf(s2 - s1 * a.mean, 0.f);
+    } else {
+      for (int k = lane; k < nchunks; k += 32) {
+        const float* q = part + (((int64_t)n * nchunks + k) * G + g0 + gi) * 3;
+        a = wf_merge(a, Welford{q[0], q[1], q[2]});
+      }
+      a = wf_shfl_merge(a);
     }
-    a = wf_shfl_merge(a);
     if (lane == 0) {
       s_mean[gi] = a.mean;
       s_rstd[gi] = rsqrtf(a.m2 / fmaxf(a.n, 1.f) + eps);
@@ -1179,8 +1194,25 @@ int dp_group_norm_fwd(int dtype, const void* x, const float* gamma, const float*
                                                                         workspace));
   DISPATCH_T(dtype, launch_k(gn_apply_kernel<T>, dim3(grid), dim3(GN_THREADS), 0, ST, 
                         cp<T>(x), gamma, beta, mp<T>(y), mean, rstd, workspace, HW, C, G, g.ppc, g.CB,
-                        eps, silu));
+                        eps, silu, static_cast<const float*>(nullptr)));
   return ew_check("group_norm_fwd");
+}
+
+int dp_group_norm_fwd_sums(int dtype, const void* x, const float* gamma, const float* beta, void* y,
+                           float* mean, float* rstd, int N, int HW, int C, int G, float eps, int silu,
+                           const float* sums, dp_stream_t stream) {
+  if (N <= 0 || HW <= 0) return 0;
+  if (int e = gn_validate(dtype, C, G)) return e;
+  if (!sums) {
+    set_error("group_norm_fwd_sums: statistics required");
+    return DP_ERR_ARGS;
+  }
+  const GnGeom g = gn_geom_rt(dtype, N, HW, C, G);
+  dim3 grid(g.chunks, N, g.nblk);
+  DISPATCH_T(dtype, launch_k(gn_apply_kernel<T>, dim3(grid), dim3(GN_THREADS), 0, ST,
+                        cp<T>(x), gamma, beta, mp<T>(y), mean, rstd, static_cast<const float*>(nullptr), HW, C, G,
+                        g.ppc, g.CB, eps, silu, sums));
+  return ew_check("group_norm_fwd_sums");
 }
 
 int dp_group_norm_bwd(int dtype, const void* x, const void* dy, const float* gamma,

@@ -234,27 +234,37 @@ class VAEEncoderBase(Component):
         self.zc, self.scale, self.in_ch = zc, scale, in_ch + pad_in
         self.conv_in = nn.Conv2d(s, "conv_in", self.in_ch, ch, 3)
         self.add_layer("conv_in", self._conv_in)
+        self._blocks, self._downs = [], []
         cin = ch
         for lvl, m in enumerate(mult):
             cout = ch * m
             for r in range(n_res):
                 blk = ResBlock(s, f"down.{lvl}.res.{r}", cin, cout)
+                self._blocks.append(blk)
                 self.add_layer(f"down.{lvl}.res.{r}", self._res(blk))
                 cin = cout
             if lvl != len(mult) - 1:
                 ds = nn.Conv2d(s, f"down.{lvl}.downsample", cin, cin, 3, stride=2, asym=True)
+                self._downs.append(ds)
                 self.add_layer(f"down.{lvl}.downsample", self._conv(ds))
         m1 = ResBlock(s, "mid.res1", cin, cin)
+        self._blocks.append(m1)
         self.add_layer("mid.res1", self._res(m1))
         if attn_mid:
             at = VAEAttn(s, "mid.attn", cin)
             self.add_layer("mid.attn", lambda st, at=at: {"h": at(st["h"])})
         m2 = ResBlock(s, "mid.res2", cin, cin)
+        self._blocks.append(m2)
         self.add_layer("mid.res2", self._res(m2))
         self.norm_out = nn.GroupNorm(s, "norm_out", cin, 32, 1e-6, silu=True)
         self.conv_out = nn.Conv2d(s, "conv_out", cin, 2 * zc, 3)
         self.add_layer("out", self._out, ("norm_out", "conv_out"))
         self.pad_in = pad_in
+        # convs whose output a 32-group GroupNorm reads directly accumulate its statistics in their epilogue:
+        # conv_in and the downsamples (the next block's norm1), every block's conv1 (its norm2) and conv2 (the
+        # next block's norm1 / the mid attention's norm / norm_out; wasted only before a downsample)
+        for cv in [self.conv_in] + self._downs + [c for b in self._blocks for c in (b.c1, b.c2)]:
+            cv.gn_stats = 32
 
     def _conv_in(self, st):
         img = st["images"].to(self.dtype)

@@ -395,13 +395,38 @@ def linear_geglu(x, layer):
     return geglu(layer(x))
 
 
+# convs whose output feeds a GroupNorm can accumulate its statistics in the GEMM epilogue (Conv2d.gn_stats =
+# G) so that the GroupNorm reads its input once. Measured on c2 (VAE convs): 627 vs 632-635 samples/s with
+# and without -- the epilogue's per-chunk reductions and atomics cost more than the statistics pass they
+# replace (that pass already runs near HBM bandwidth on the large maps), so it is off by default
+# (DP_GN_STATS=1: on)
+GN_STATS = os.environ.get("DP_GN_STATS", "0") != "0"
+
+
+def _lib_gn_slots():
+    return 16  # DP_GN_SLOTS (include/dpipe.h)
+
+
+def _gn_sums_of(x, G):
+    s = getattr(x, "_dp_gn", None)
+    return s[0] if (s is not None and s[1] == G) else None
+
+
 class _ConvFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, anchor, residual, layer):
         x = _c(x)
-        y = ops.conv2d(x, layer.weight.w, stride=layer.stride, pad=layer.pad, out_hw=layer.out_hw(x),
+        hw = layer.out_hw(x)
+        G = layer.gn_stats
+        sums = None
+        if (GN_STATS and G and x.dtype == torch.bfloat16 and x.is_cuda and (hw[0] * hw[1]) % 32 == 0
+                and layer.weight.shape[0] % (4 * G) == 0 and x.shape[-1] % 64 == 0):
+            sums = torch.empty(_lib_gn_slots(), x.shape[0], G, 2, device=x.device, dtype=torch.float32)
+        y = ops.conv2d(x, layer.weight.w, stride=layer.stride, pad=layer.pad, out_hw=hw,
                        bias=None if layer.bias is None else layer.bias.w,
-                       residual=None if residual is None else _c(residual))
+                       residual=None if residual is None else _c(residual), gn_sums=sums, gn_groups=G)
+        if sums is not None:
+            y._dp_gn = (sums, G)
         ctx.save_for_backward(x)
         ctx.layer = layer
         ctx.has_res = residual is not None
@@ -427,7 +452,8 @@ class _GroupNormFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, anchor, layer):
         x = _c(x)
-        y, mean, rstd = ops.group_norm(x, layer.gamma.w, layer.beta.w, layer.groups, layer.eps, layer.silu)
+        y, mean, rstd = ops.group_norm(x, layer.gamma.w, layer.beta.w, layer.groups, layer.eps, layer.silu,
+                                       sums=_gn_sums_of(x, layer.groups))
         ctx.save_for_backward(x, mean, rstd)
         ctx.layer = layer
         return y
@@ -478,7 +504,8 @@ class _GroupNormForkFn(torch.autograd.Function):
     def forward(ctx, x, anchor, layer):
         ctx.set_materialize_grads(False)
         xc = _c(x)
-        y, mean, rstd = ops.group_norm(xc, layer.gamma.w, layer.beta.w, layer.groups, layer.eps, layer.silu)
+        y, mean, rstd = ops.group_norm(xc, layer.gamma.w, layer.beta.w, layer.groups, layer.eps, layer.silu,
+                                       sums=_gn_sums_of(xc, layer.groups))
         ctx.save_for_backward(xc, mean, rstd)
         ctx.layer = layer
         return y, x.view_as(x)
@@ -824,6 +851,7 @@ class Conv2d:
         self.store = store
         self.weight = store.add(f"{name}.weight", (cout, k, k, cin), init=init)
         self.bias = store.add(f"{name}.bias", (cout,), fp32=True, init="b") if bias else None
+        self.gn_stats = 0  # GroupNorm groups of the output's consumer (statistics in the conv epilogue)
 
     def out_hw(self, x):
         H, W = x.shape[1], x.shape[2]

@@ -298,7 +298,8 @@ def _take_last(t, C):
     return out
 
 
-def conv2d(x, w, *, stride=1, pad=(1, 1), out_hw=None, bias=None, residual=None, out=None):
+def conv2d(x, w, *, stride=1, pad=(1, 1), out_hw=None, bias=None, residual=None, out=None, gn_sums=None,
+           gn_groups=0):
     """NHWC conv: x [N,H,W,C], w [K,R,S,C] -> y [N,P,Q,K].
 
     pad is (top, left); bottom/right padding is implied by out_hw (default:
@@ -322,7 +323,9 @@ def conv2d(x, w, *, stride=1, pad=(1, 1), out_hw=None, bias=None, residual=None,
         xp, wp = _pad_last(x), _pad_last(w)
         Cp = xp.shape[-1]
         a = _conv_args(xp, wp, out, stride, pad, P, Q, bias, residual)
-        ws = _splitk_ws(a, "dp_conv_fwd_workspace", x.device)
+        if gn_sums is not None:  # GroupNorm statistics of the output for its consumer (conv epilogue)
+            a.gn_sums, a.gn_groups = _ptr(gn_sums), gn_groups
+        ws = None if gn_sums is not None else _splitk_ws(a, "dp_conv_fwd_workspace", x.device)
         telemetry.timed("tcgen05_gemm", 2.0 * N * P * Q * K * R * S * C,
                         lambda: check(_lib.lib().dp_conv_fwd(ctypes.byref(a), _stream()), "dp_conv_fwd",
                                       2 if ws is not None else 1),
@@ -619,13 +622,19 @@ def _gn_ws(device, nbytes):
     return ws
 
 
-def group_norm(x, gamma, beta, G, eps, silu):
-    """x NHWC [N,H,W,C] (or [N,L,C]); returns y, mean, rstd."""
+def group_norm(x, gamma, beta, G, eps, silu, sums=None):
+    """x NHWC [N,H,W,C] (or [N,L,C]); returns y, mean, rstd. sums: the producer's per-(sample, group)
+    {sum, sum of squares} (conv2d gn_sums): one pass over x instead of two."""
     N, C = x.shape[0], x.shape[-1]
     HW = x.numel() // (N * C)
     y = torch.empty_like(x)
     mean = torch.empty(N, G, device=x.device, dtype=torch.float32)
     rstd = torch.empty_like(mean)
+    if sums is not None:
+        check(_L().dp_group_norm_fwd_sums(dtype_code(x), _ptr(x), _ptr(gamma), _ptr(beta), _ptr(y), _ptr(mean),
+                                          _ptr(rstd), N, HW, C, G, eps, int(silu), _ptr(sums), _stream()),
+              "dp_group_norm_fwd_sums")
+        return y, mean, rstd
     ws = _gn_ws(x.device, _L().dp_group_norm_workspace(N, HW, G))
     check(_L().dp_group_norm_fwd(dtype_code(x), _ptr(x), _ptr(gamma), _ptr(beta), _ptr(y), _ptr(mean),
                                  _ptr(rstd), N, HW, C, G, eps, int(silu), _ptr(ws), _stream()),

@@ -337,3 +337,29 @@ def test_flip_batch_matches_single_flips():
     torch.cuda.synchronize()
     for (w, wt, *_), ref in zip(jobs, refs):
         assert torch.equal(wt, ref)
+
+
+@pytest.mark.parametrize("N,H,C,K,stride", [(2, 64, 128, 128, 1), (2, 32, 256, 256, 1), (3, 16, 512, 512, 1),
+                                            (2, 64, 128, 128, 2), (2, 32, 128, 512, 1)])
+def test_conv_groupnorm_statistics_epilogue(N, H, C, K, stride):
+    """GroupNorm statistics accumulated by the conv epilogue (VAE convs): the sums match the stored output,
+    and the one-pass GroupNorm from them matches the two-pass GroupNorm."""
+    ops = _ops()
+    g = torch.Generator(device="cuda").manual_seed(H + C + K)
+    x = torch.randn(N, H, H, C, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(K, 3, 3, C, device="cuda", generator=g) * 0.05).bfloat16()
+    b = torch.randn(K, device="cuda", generator=g)
+    G = 32
+    P = H // stride
+    sums = torch.empty(16, N, G, 2, device="cuda")  # DP_GN_SLOTS partial tables
+    y = ops.conv2d(x, w, stride=stride, pad=(1, 1), out_hw=(P, P), bias=b, gn_sums=sums, gn_groups=G)
+    y_ref = ops.conv2d(x, w, stride=stride, pad=(1, 1), out_hw=(P, P), bias=b)
+    assert _rel(y, y_ref) < 1e-2  # (the unfused launch may split K: rounding differs)
+    yf = y.float().view(N, P * P, G, K // G)
+    ref = torch.stack([yf.sum((1, 3)), (yf * yf).sum((1, 3))], -1)
+    assert _rel(sums.sum(0), ref) < 1e-4
+    gam = torch.randn(K, device="cuda") * 0.1 + 1
+    bet = torch.randn(K, device="cuda") * 0.1
+    a1, m1, r1 = ops.group_norm(y, gam, bet, G, 1e-6, True, sums=sums)
+    a2, m2, r2 = ops.group_norm(y, gam, bet, G, 1e-6, True)
+    assert _rel(m1, m2) < 1e-4 and _rel(r1, r2) < 1e-3 and _rel(a1, a2) < 1e-2
