@@ -81,7 +81,9 @@ typedef struct DpGemmArgs {
        a * gelu_erf(g) (row stride geglu_ld) is written by the same epilogue;
      geglu_mode 2 (input gradient of the FF output projection, N = F): the GEMM result is dy = dL/dy of
        the GEGLU output; with h = geglu_out ([M][2F] pre-activation, row stride geglu_ld) the epilogue
-       writes D[m][f] = dy * gelu(g) and D[m][F + f] = dy * a * gelu'(g) (D is [M][2F], row stride d_ld).
+       writes D[m][f] = dy * gelu(g) and D[m][F + f] = dy * a * gelu'(g) (D is [M][2F], row stride d_ld);
+     geglu_mode 3 (GELU activation epilogue, bf16 K-major store, N % 128 == 0, no residual / batch):
+       D = gelu_erf(A B^T + bias) (geglu_out unused).
      0: off. */
   void* geglu_out;
   int64_t geglu_ld;
@@ -193,6 +195,10 @@ int dp_act_bwd(int op, int dtype, const void* x, const void* dy, void* dx, int64
 int dp_geglu_fwd(int dtype, const void* x, void* y, int64_t rows, int F, dp_stream_t stream);
 int dp_geglu_bwd(int dtype, const void* x, const void* dy, void* dx, int64_t rows, int F,
                  dp_stream_t stream);
+/* GEGLU backward fused with the producing projection's bias gradient: db[0..2F) += column sums of
+   dx (fp32 accumulate; db NULL -> dp_geglu_bwd) */
+int dp_geglu_bwd_db(int dtype, const void* x, const void* dy, void* dx, int64_t rows, int F, float* db,
+                    dp_stream_t stream);
 /* y = alpha*a + beta*b  (b may be NULL) */
 int dp_axpby(int dtype, const void* a, const void* b, void* y, int64_t n, float alpha, float beta,
              dp_stream_t stream);
@@ -233,6 +239,11 @@ int dp_row_bias_fwd(int dtype, const void* x, const void* e, int64_t e_ld, void*
                     int C, int rows_per_sample, dp_stream_t stream);
 int dp_row_bias_bwd(int dtype, const void* dy, void* de, int64_t de_ld, int B, int C,
                     int rows_per_sample, dp_stream_t stream);
+/* as dp_row_bias_bwd, and db[c] += sum over all rows of dy (the bias gradient of the layer that
+   produced x, e.g. a ResBlock's first conv) and db2[c] += the same sum (the bias gradient of the layer
+   that produced e, e.g. the temb projection: sum_b de[b]) from the same per-sample sums; fp32, NULL -> none */
+int dp_row_bias_bwd_db(int dtype, const void* dy, void* de, int64_t de_ld, int B, int C,
+                       int rows_per_sample, float* db, float* db2, dp_stream_t stream);
 /* NHWC image [N][H][W][C] <-> patches [N][H/p][W/p][p*p*C] (DiT patchify/unpatchify);
    H, W, C describe the image side in both directions */
 int dp_space_to_depth(int dtype, const void* x, void* y, int N, int H, int W, int C, int p,

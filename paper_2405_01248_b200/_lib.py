@@ -92,6 +92,7 @@ _SIGNATURES = {
     "dp_act_bwd": [c_int, c_int, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_void_p],
     "dp_geglu_fwd": [c_int, c_void_p, c_void_p, c_i64, c_int, c_void_p],
     "dp_geglu_bwd": [c_int, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_void_p],
+    "dp_geglu_bwd_db": [c_int, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_void_p, c_void_p],
     "dp_axpby": [c_int, c_void_p, c_void_p, c_void_p, c_i64, c_float, c_float, c_void_p],
     "dp_gate_residual_fwd": [c_int, c_void_p, c_void_p, c_i64, c_void_p, c_void_p, c_i64, c_int,
                              c_int, c_void_p],
@@ -110,6 +111,7 @@ _SIGNATURES = {
     "dp_upsample2x_bwd": [c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p],
     "dp_row_bias_fwd": [c_int, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_int, c_int, c_void_p],
     "dp_row_bias_bwd": [c_int, c_void_p, c_void_p, c_i64, c_int, c_int, c_int, c_void_p],
+    "dp_row_bias_bwd_db": [c_int, c_void_p, c_void_p, c_i64, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p],
     "dp_space_to_depth": [c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p],
     "dp_bias_grad": [c_int, c_void_p, c_void_p, c_i64, c_int, c_void_p],
     "dp_cast": [c_int, c_int, c_void_p, c_void_p, c_i64, c_void_p],

@@ -603,7 +603,8 @@ __global__ void row_bias_fwd_kernel(const T* __restrict__ x, const T* __restrict
 // de[b][c] = sum_{r in sample b} dy[r][c] : grid (ceil(C/32), B), deterministic
 template <typename T>
 __global__ void __launch_bounds__(256) row_bias_bwd_kernel(const T* __restrict__ dy, T* __restrict__ de,
-                                                           int64_t de_ld, int C, int rps) {
+                                                           int64_t de_ld, int C, int rps, float* __restrict__ db,
+                                                           float* __restrict__ db2) {
   DP_PDL_ENTRY();
   const int b = blockIdx.y;
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);
@@ -619,6 +620,8 @@ __global__ void __launch_bounds__(256) row_bias_bwd_kernel(const T* __restrict__
 #pragma unroll
     for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x];
     de[(int64_t)b * de_ld + c] = from_f<T>(s);
+    if (db) atomicAdd(db + c, s);
+    if (db2) atomicAdd(db2 + c, s);
   }
 }
 
@@ -626,7 +629,8 @@ __global__ void __launch_bounds__(256) row_bias_bwd_kernel(const T* __restrict__
 // lanes over one sample's rows (grid (CV/CVB, B)), deterministic (no atomics)
 template <typename T>
 __global__ void __launch_bounds__(256) row_bias_bwd_vec_kernel(const T* __restrict__ dy, T* __restrict__ de,
-                                                               int64_t de_ld, int C, int rps, int CVB) {
+                                                               int64_t de_ld, int C, int rps, int CVB,
+                                                               float* __restrict__ db, float* __restrict__ db2) {
   DP_PDL_ENTRY();
   constexpr int V = VecT<T>::N;
   const int b = blockIdx.y;
@@ -665,6 +669,10 @@ __global__ void __launch_bounds__(256) row_bias_bwd_vec_kernel(const T* __restri
     float s = 0.f;
     for (int k = 0; k < RL; ++k) s += red[k * CVB * V + t];
     de[(int64_t)b * de_ld + blockIdx.x * CVB * V + t] = from_f<T>(s);
+    // the producing conv's bias gradient is the sum of the per-sample sums (fp32, before rounding)
+    if (db) atomicAdd(db + blockIdx.x * CVB * V + t, s);
+    // ... and, for a temb projection, that linear's bias gradient too (the same sum over every row)
+    if (db2) atomicAdd(db2 + blockIdx.x * CVB * V + t, s);
   }
 }
 
@@ -742,6 +750,79 @@ __global__ void geglu_bwd_vec_kernel(const T* __restrict__ x, const T* __restric
     }
     store_vec(dx + r * 2 * F + fv * V, da);
     store_vec(dx + r * 2 * F + F + fv * V, dg);
+  }
+}
+
+// GEGLU backward fused with the bias gradient of the projection that produced x (the FF input
+// projection ff1): db[0..2F) += column sums of dx = [da | dg]. Block = CVB vectors of the F half x
+// 256/CVB row lanes over one row segment (grid (FV/CVB, segments)), two rows' loads in flight per
+// thread, one fp32 atomic per column and block. Replaces the separate bias-gradient pass that
+// re-read dx (2F columns) from HBM.
+template <typename T>
+__global__ void __launch_bounds__(256) geglu_bwd_bias_kernel(const T* __restrict__ x, const T* __restrict__ dy,
+                                                             T* __restrict__ dx, float* __restrict__ db,
+                                                             int64_t rows, int F, int CVB, int64_t seg) {
+  DP_PDL_ENTRY();
+  constexpr int V = VecT<T>::N;
+  const int RL = 256 / CVB;
+  const int lv = threadIdx.x % CVB, rl = threadIdx.x / CVB;
+  const int cv = blockIdx.x * CVB + lv;
+  const int64_t r0 = (int64_t)blockIdx.y * seg;
+  const int64_t r1 = min(rows, r0 + seg);
+  float sa[V], sg[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) sa[j] = sg[j] = 0.f;
+  auto row = [&](int64_t r, const float (&a)[V], const float (&g)[V], const float (&d)[V]) {
+    float da[V], dg[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      da[j] = d[j] * gelu_erf(g[j]);
+      dg[j] = d[j] * a[j] * gelu_erf_grad(g[j]);
+    }
+    store_vec(dx + r * 2 * F + cv * V, da);
+    store_vec(dx + r * 2 * F + F + cv * V, dg);
+    // the bias gradient sums what the consumer reads: the rounded stored values
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      sa[j] += to_f(from_f<T>(da[j]));
+      sg[j] += to_f(from_f<T>(dg[j]));
+    }
+  };
+  if (rl < RL) {
+    int64_t r = r0 + rl;
+    for (; r + RL < r1; r += 2 * RL) {
+      float a0[V], g0[V], d0[V], a1[V], g1[V], d1[V];
+      load_vec(x + r * 2 * F + cv * V, a0);
+      load_vec(x + r * 2 * F + F + cv * V, g0);
+      load_vec(dy + r * F + cv * V, d0);
+      load_vec(x + (r + RL) * 2 * F + cv * V, a1);
+      load_vec(x + (r + RL) * 2 * F + F + cv * V, g1);
+      load_vec(dy + (r + RL) * F + cv * V, d1);
+      row(r, a0, g0, d0);
+      row(r + RL, a1, g1, d1);
+    }
+    for (; r < r1; r += RL) {
+      float a0[V], g0[V], d0[V];
+      load_vec(x + r * 2 * F + cv * V, a0);
+      load_vec(x + r * 2 * F + F + cv * V, g0);
+      load_vec(dy + r * F + cv * V, d0);
+      row(r, a0, g0, d0);
+    }
+  }
+  __shared__ float red[2][256 * 8];
+  if (rl < RL) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      red[0][rl * CVB * V + lv * V + j] = sa[j];
+      red[1][rl * CVB * V + lv * V + j] = sg[j];
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 2 * CVB * V; t += 256) {
+    const int h = t / (CVB * V), u = t - h * (CVB * V);
+    float s = 0.f;
+    for (int k = 0; k < RL; ++k) s += red[h][k * CVB * V + u];
+    atomicAdd(db + h * F + blockIdx.x * CVB * V + u, s);
   }
 }
 
@@ -952,6 +1033,32 @@ int dp_geglu_fwd(int dtype, const void* x, void* y, int64_t rows, int F, dp_stre
   return ew_check("geglu_fwd");
 }
 
+int dp_geglu_bwd_db(int dtype, const void* x, const void* dy, void* dx, int64_t rows, int F, float* db,
+                    dp_stream_t stream) {
+  if (rows <= 0) return 0;
+  const int V = dtype == DP_F32 ? 4 : 8;
+  if (!db) return dp_geglu_bwd(dtype, x, dy, dx, rows, F, stream);
+  if (F % V || !aligned16(x) || !aligned16(dy) || !aligned16(dx)) {
+    set_error("dp_geglu_bwd_db: F must be a multiple of the 16-byte vector and the rows 16-byte aligned");
+    return DP_ERR_ARGS;
+  }
+  const int FV = F / V;
+  int CVB = 1;
+  for (int d = 32; d >= 1; --d)
+    if (FV % d == 0) {
+      CVB = d;
+      break;
+    }
+  // ~2 blocks per SM over (channel blocks x row segments): few atomics per column
+  const int64_t want = 2 * kNumSMs / (FV / CVB) > 0 ? 2 * kNumSMs / (FV / CVB) : 1;
+  int64_t seg = (rows + want - 1) / want;
+  if (seg < 2 * (256 / CVB)) seg = 2 * (256 / CVB);
+  dim3 grid(FV / CVB, static_cast<unsigned>((rows + seg - 1) / seg));
+  DISPATCH_T(dtype, launch_k(geglu_bwd_bias_kernel<T>, dim3(grid), dim3(256), 0, ST, cp<T>(x), cp<T>(dy),
+                             mp<T>(dx), db, rows, F, CVB, seg));
+  return ew_check("geglu_bwd_db");
+}
+
 int dp_geglu_bwd(int dtype, const void* x, const void* dy, void* dx, int64_t rows, int F,
                  dp_stream_t stream) {
   if (rows <= 0) return 0;
@@ -1132,8 +1239,8 @@ int dp_row_bias_fwd(int dtype, const void* x, const void* e, int64_t e_ld, void*
   return ew_check("row_bias_fwd");
 }
 
-int dp_row_bias_bwd(int dtype, const void* dy, void* de, int64_t de_ld, int B, int C,
-                    int rows_per_sample, dp_stream_t stream) {
+int dp_row_bias_bwd_db(int dtype, const void* dy, void* de, int64_t de_ld, int B, int C,
+                       int rows_per_sample, float* db, float* db2, dp_stream_t stream) {
   if (B <= 0) return 0;
   const int V = dtype == DP_F32 ? 4 : 8;
   if (C % V == 0 && de_ld % V == 0 && aligned16(dy) && aligned16(de)) {
@@ -1155,13 +1262,18 @@ int dp_row_bias_bwd(int dtype, const void* dy, void* de, int64_t de_ld, int B, i
         }
     dim3 g(CV / CVB, B);
     DISPATCH_T(dtype, launch_k(row_bias_bwd_vec_kernel<T>, dim3(g), dim3(256), 0, ST, cp<T>(dy), mp<T>(de), de_ld,
-                               C, rows_per_sample, CVB));
+                               C, rows_per_sample, CVB, db, db2));
     return ew_check("row_bias_bwd");
   }
   dim3 grid((C + 31) / 32, B);
   DISPATCH_T(dtype, launch_k(row_bias_bwd_kernel<T>, dim3(grid), dim3(256), 0, ST, cp<T>(dy), mp<T>(de), de_ld, C,
-                                                                   rows_per_sample));
+                                                                   rows_per_sample, db, db2));
   return ew_check("row_bias_bwd");
+}
+
+int dp_row_bias_bwd(int dtype, const void* dy, void* de, int64_t de_ld, int B, int C,
+                    int rows_per_sample, dp_stream_t stream) {
+  return dp_row_bias_bwd_db(dtype, dy, de, de_ld, B, C, rows_per_sample, nullptr, nullptr, stream);
 }
 
 int dp_space_to_depth(int dtype, const void* x, void* y, int N, int H, int W, int C, int p,

@@ -335,12 +335,28 @@ constexpr size_t SMEM = 1024 + 5 * TILE_BYTES;
 __global__ void __launch_bounds__(256) fa_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
                                                           const __nv_bfloat16* __restrict__ dout,
                                                           float* __restrict__ Dv, int B, int N, int heads,
-                                                          int64_t o_ld, int64_t do_ld) {
+                                                          int64_t o_ld, int64_t do_ld, float* __restrict__ dq_zero,
+                                                          float* __restrict__ dkv_zero, int64_t dkv_rows) {
   DP_PDL_ENTRY();
   const int sub = threadIdx.x & 7;
   const int64_t total = (int64_t)B * N * heads;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  // the fp32 dQ (and split dK / dV) accumulators the backward kernel reduce-adds into are zeroed here,
+  // 64-float rows, 8 floats per thread (no separate memset node between the PDL kernels)
+  if (dkv_zero)
+    for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3; r < dkv_rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 3) {
+      float4* d = reinterpret_cast<float4*>(dkv_zero + r * HD + sub * 8);
+      d[0] = z4;
+      d[1] = z4;
+    }
   for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3; r < total;
        r += ((int64_t)gridDim.x * blockDim.x) >> 3) {
+    if (dq_zero) {  // row r = (b, n, h) of [B][N][heads][64]: the same index order as the loop
+      float4* d = reinterpret_cast<float4*>(dq_zero + r * HD + sub * 8);
+      d[0] = z4;
+      d[1] = z4;
+    }
     const int h = static_cast<int>(r % heads);
     const int64_t bn = r / heads;
     const int n = static_cast<int>(bn % N);
@@ -861,14 +877,24 @@ extern "C" int dp_flash_attn_bwd(const DpAttnArgs* a, const void* dout, int64_t 
   float* Dv = workspace;                                   // [B][heads][N]
   float* dq_acc = workspace + (int64_t)a->B * a->heads * a->N;  // [B][N][heads][64]
   const bool dq_direct = a->Nk <= fa::BKV;
-  if (!dq_direct) cudaMemsetAsync(dq_acc, 0, sizeof(float) * rows * C, st);
+  const int qsplit = fa_bwd_qsplit(a);
+  float* dkv_acc = dq_acc + rows * C;  // [2][B][Nk][heads][64] (split only)
+  const int64_t kv_rows = (int64_t)a->B * a->Nk;
+  // accumulators zeroed by the prep kernel (16-byte stores) when aligned, else by memsets
+  const bool zero_in_prep = (reinterpret_cast<uintptr_t>(dq_acc) & 15) == 0;
+  if (!zero_in_prep) {
+    if (!dq_direct) cudaMemsetAsync(dq_acc, 0, sizeof(float) * rows * C, st);
+    if (qsplit > 1) cudaMemsetAsync(dkv_acc, 0, sizeof(float) * 2 * kv_rows * C, st);
+  }
   {
     const int64_t total = (int64_t)a->B * a->heads * a->N;
     int gp = static_cast<int>((total * 8 + 255) / 256);
     if (gp > 148 * 8) gp = 148 * 8;
     launch_k(fa::fa_bwd_prep_kernel, dim3(gp), dim3(256), 0, st,
         reinterpret_cast<const __nv_bfloat16*>(a->o), reinterpret_cast<const __nv_bfloat16*>(dout), Dv, a->B,
-        a->N, a->heads, a->o_ld, do_ld);
+        a->N, a->heads, a->o_ld, do_ld, (dq_direct || !zero_in_prep) ? nullptr : dq_acc,
+        (qsplit > 1 && zero_in_prep) ? dkv_acc : nullptr,
+        2 * kv_rows * a->heads);
   }
   CUtensorMap mq, mk, mv, mdo, mdk, mdv;
   if (int e = fa_map(&mq, a->q, a->N, a->heads, a->B, a->q_ld, a->q_bs)) return e;
@@ -905,10 +931,6 @@ extern "C" int dp_flash_attn_bwd(const DpAttnArgs* a, const void* dout, int64_t 
       return DP_ERR_DRIVER;
     }
   }
-  const int qsplit = fa_bwd_qsplit(a);
-  float* dkv_acc = dq_acc + rows * C;  // [2][B][Nk][heads][64] (split only)
-  const int64_t kv_rows = (int64_t)a->B * a->Nk;
-  if (qsplit > 1) cudaMemsetAsync(dkv_acc, 0, sizeof(float) * 2 * kv_rows * C, st);
   fa::BwdParams p{a->N, a->Nk, a->heads, a->scale * 1.4426950408889634f, a->scale, a->lse, Dv, dq_acc,
                   qsplit, dq_direct ? 1 : 0, dkv_acc};
   dim3 grid((a->Nk + fa::BKV - 1) / fa::BKV * qsplit, a->heads, a->B);

@@ -948,6 +948,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           float f[32];
           epilogue_math<BN>(p, row, n, wk.z1, wk.z2, v, f, rc, use_pre);
           if constexpr (GEG == 3) gn_stats_chunk(p, f, row, row0, n, lane);
+          if constexpr (GEG == 4) {  // GELU (erf) of the biased result: the frozen text encoders' MLP fc1
+#pragma unroll
+            for (int i = 0; i < 32; ++i) f[i] = 0.5f * f[i] * (1.f + erff(f[i] * 0.70710678118654752f));
+          }
           uint8_t* buf = ebuf + (chunk_seq & 1) * EPI_STAGE_BYTES;
           if (chunk_seq >= 2) {
             if (lane == 0) bulk_wait_read<1>();
@@ -1367,6 +1371,20 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// zero the split-K workspace as a programmatic-dependent-launch kernel: a cudaMemsetAsync node between
+// two PDL kernels serialises the stream twice (the memset waits for the previous kernel to drain and the
+// split GEMM cannot overlap its prologue with the memset), 16-byte stores
+__global__ void __launch_bounds__(256) ws_zero_kernel(float4* __restrict__ ws, int64_t n4) {
+  DP_PDL_ENTRY();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x)
+    ws[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+static bool splitk_memset() {  // DP_SPLITK_MEMSET=1: the cudaMemsetAsync path (A/B)
+  static const bool v = env_int("DP_SPLITK_MEMSET") > 0;
+  return v;
+}
+
 // wave efficiency (percent) below which a bf16 launch is split (DP_SPLITK_FRAC; experiments)
 static int splitk_pct() {
   static const int v = [] {
@@ -1409,7 +1427,16 @@ static int launch_bn(int bn, int cg, const CUtensorMap& ma, const CUtensorMap& m
     choose_split(q, 0, true);
     CUtensorMap mq = ma;
     make_dmap(&mq, q, M, N, b1, b2);
-    cudaError_t e = cudaMemsetAsync(ws, 0, need, st);
+    cudaError_t e = cudaSuccess;
+    if (splitk_memset() || (need % 16) != 0) {
+      e = cudaMemsetAsync(ws, 0, need, st);
+    } else {
+      const int64_t n4 = need / 16;
+      const int64_t zb = (n4 + 255) / 256;
+      launch_k(ws_zero_kernel, dim3(static_cast<unsigned>(zb < 4 * kNumSMs ? zb : 4 * kNumSMs)), dim3(256), 0, st,
+               reinterpret_cast<float4*>(ws), n4);
+      e = cudaGetLastError();
+    }
     if (e != cudaSuccess) {
       set_error(std::string("split-K workspace memset: ") + cudaGetErrorString(e));
       return e;
@@ -1597,6 +1624,15 @@ int tc_gemm(const DpGemmArgs* a, cudaStream_t st, int64_t* query = nullptr) {
     bn = (a->N % 256 == 0) ? 256 : 128;
     cg = (a->M >= 256 && a->K > 512) ? 2 : 1;
   }
+  if (a->geglu_mode == 3) {  // GELU epilogue instantiations (GEG = 4): 128 / 256-wide tiles, no split-K
+    if (a->dtype != DP_BF16 || a->d_dtype != DP_BF16 || a->out_mode != DP_OUT_STORE || a->Res ||
+        a->a_mn_major || a->b_mn_major || a->batch1 > 1 || a->batch2 > 1 || a->N % 128 || a->alpha != 1.f) {
+      set_error("gemm gelu epilogue: bf16 K-major linear store, N % 128 == 0, no residual / batch / alpha");
+      return DP_ERR_UNSUPPORTED;
+    }
+    bn = (a->N % 256 == 0) ? 256 : 128;
+    cg = a->M >= 256 ? 2 : 1;
+  }
   TcParams p{};
   p.M = a->M;
   p.N = a->N;
@@ -1612,7 +1648,7 @@ int tc_gemm(const DpGemmArgs* a, cudaStream_t st, int64_t* query = nullptr) {
   fill_epilogue(p, a->D, a->d_dtype, a->d_ld, a->d_bs1, a->d_bs2, a->out_mode, a->bias, a->Res,
                 a->r_ld, a->r_bs1, a->r_bs2, a->alpha);
   if (query) {
-    *query = splitk_bytes(p, cg, a->M, a->N);
+    *query = a->geglu_mode == 3 ? 0 : splitk_bytes(p, cg, a->M, a->N);
     return 0;
   }
   CUtensorMap ma, mb;
@@ -1657,6 +1693,19 @@ int tc_gemm(const DpGemmArgs* a, cudaStream_t st, int64_t* query = nullptr) {
                        : launch_tc<128, 2, false, false, 2>(ma, mb, md, p, kNumSMs, st);
     return bn == 256 ? launch_tc<256, 1, false, false, 2>(ma, mb, md, p, kNumSMs, st)
                      : launch_tc<128, 1, false, false, 2>(ma, mb, md, p, kNumSMs, st);
+  }
+  if (a->geglu_mode == 3) {
+    CUtensorMap md = ma;
+    make_dmap(&md, p, a->M, a->N, 1, 1);
+    if (!p.d_tma) {
+      set_error("gemm gelu epilogue: output not TMA-storable");
+      return DP_ERR_ARGS;
+    }
+    if (cg == 2)
+      return bn == 256 ? launch_tc<256, 2, false, false, 4>(ma, mb, md, p, kNumSMs, st)
+                       : launch_tc<128, 2, false, false, 4>(ma, mb, md, p, kNumSMs, st);
+    return bn == 256 ? launch_tc<256, 1, false, false, 4>(ma, mb, md, p, kNumSMs, st)
+                     : launch_tc<128, 1, false, false, 4>(ma, mb, md, p, kNumSMs, st);
   }
   return launch_bn(bn, cg, ma, mb, p, a->M, a->N, p.batch1, batch2, st, a->workspace, a->workspace_bytes);
 }

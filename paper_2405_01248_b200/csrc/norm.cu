@@ -801,7 +801,9 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Parameter gradients of LayerNorm: grid (ceil(C/32), nseg). Segment = rows_per_seg rows.
+// Parameter gradients of LayerNorm: grid (CV/CVB, nseg). Segment = rows_per_seg rows; block = CVB channel
+// vectors (a divisor of the row's CV vectors: no idle lanes at C = 320 / 640 / 1280, where 32-vector blocks
+// left up to 3/8 of the lanes idle) x 256/CVB row lanes.
 // affine: dgamma[c] += sum dy*xhat, dbeta[c] += sum dy (fp32 atomics)
 // mod:    dmod[b][scale_off+c] = sum_{rows of b} dy*gamma?*xhat_aff, dmod[b][shift_off+c] = sum dy
 //         (segment = sample b; stored, not accumulated)
@@ -811,21 +813,20 @@ __global__ void __launch_bounds__(256)
                          const float* __restrict__ mean, const float* __restrict__ rstd,
                          int64_t rows, int C, int rows_per_seg, float* __restrict__ dgamma,
                          float* __restrict__ dbeta, T* __restrict__ dmod, int64_t dmod_ld,
-                         int shift_off, int scale_off) {
+                         int shift_off, int scale_off, int CVB) {
   DP_PDL_ENTRY();
-  // 16-byte vectors: a block covers 32 channel vectors x 8 row lanes of one row segment
   constexpr int V = NV<T>::V;
-  const int CV = C / V;
-  const int cv = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int ry = threadIdx.x >> 5;
+  const int RL = 256 / CVB;
+  const int lv = threadIdx.x % CVB, ry = threadIdx.x / CVB;
+  const int cv = blockIdx.x * CVB + lv;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_seg;
   const int64_t r1 = min(rows, r0 + rows_per_seg);
   float a[V], b[V];
 #pragma unroll
   for (int j = 0; j < V; ++j) a[j] = b[j] = 0.f;
-  if (cv < CV) {
+  if (ry < RL) {
 #pragma unroll 2
-    for (int64_t r = r0 + ry; r < r1; r += 8) {
+    for (int64_t r = r0 + ry; r < r1; r += RL) {
       float fx[V], fd[V];
       ld16(x + r * C + cv * V, fx);
       ld16(dy + r * C + cv * V, fd);
@@ -837,21 +838,21 @@ __global__ void __launch_bounds__(256)
       }
     }
   }
-  __shared__ float ra[8][32 * 8 + 1], rb[8][32 * 8 + 1];
+  __shared__ float ra[256 * 8], rb[256 * 8];
+  if (ry < RL) {
 #pragma unroll
-  for (int j = 0; j < V; ++j) {
-    ra[ry][(threadIdx.x & 31) * V + j] = a[j];
-    rb[ry][(threadIdx.x & 31) * V + j] = b[j];
+    for (int j = 0; j < V; ++j) {
+      ra[ry * CVB * V + lv * V + j] = a[j];
+      rb[ry * CVB * V + lv * V + j] = b[j];
+    }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < 32 * V; t += 256) {
-    const int c = blockIdx.x * 32 * V + t;
-    if (c >= C) continue;
+  for (int t = threadIdx.x; t < CVB * V; t += 256) {
+    const int c = blockIdx.x * CVB * V + t;
     float sa = 0.f, sb = 0.f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      sa += ra[k][t];
-      sb += rb[k][t];
+    for (int k = 0; k < RL; ++k) {
+      sa += ra[k * CVB * V + t];
+      sb += rb[k * CVB * V + t];
     }
     if (dmod) {
       dmod[blockIdx.y * dmod_ld + scale_off + c] = from_f<T>(sa);
@@ -861,6 +862,17 @@ __global__ void __launch_bounds__(256)
       atomicAdd(dbeta + c, sb);
     }
   }
+}
+
+// channel vectors per ln_param_grad block: the divisor of CV (<= 64) that keeps the most of 256 threads busy
+static int ln_pg_cvb(int CV) {
+  int best = -1, cvb = 1;
+  for (int d = 1; d <= 64 && d <= CV; ++d)
+    if (CV % d == 0 && (256 / d) * d >= best) {
+      best = (256 / d) * d;
+      cvb = d;
+    }
+  return cvb;
 }
 
 // ------------------------------------------------------------------ softmax (attention)
@@ -1390,13 +1402,14 @@ int dp_layer_norm_bwd(int dtype, const void* x, const void* dy, const float* gam
       else go(lnq_bwd_kernel<8, false>);
       if (gamma && dgamma) {
         const int CVn = C / 8;
-        const int64_t cb = (CVn + 31) / 32;
+        const int cvb = ln_pg_cvb(CVn);
+        const int64_t cb = CVn / cvb;
         int64_t seg = (rows * cb + 2 * kNumSMs - 1) / (2 * kNumSMs);  // ~2 waves
         seg = seg < 64 ? 64 : seg;
         dim3 g2(static_cast<unsigned>(cb), static_cast<unsigned>((rows + seg - 1) / seg));
         launch_k(ln_param_grad_kernel<__nv_bfloat16>, dim3(g2), dim3(256), 0, ST, cp<__nv_bfloat16>(x),
                  cp<__nv_bfloat16>(dy), mean, rstd, rows, C, static_cast<int>(seg), dgamma, dbeta,
-                 static_cast<__nv_bfloat16*>(nullptr), (int64_t)0, 0, 0);
+                 static_cast<__nv_bfloat16*>(nullptr), (int64_t)0, 0, 0, cvb);
       }
       return ew_check("layer_norm_bwd");
     }
@@ -1433,19 +1446,22 @@ warp_rows:
 #undef LN_BWD_ARGS
   if (gamma && dgamma && !pg) {
     const int CVn = C / (dtype == DP_F32 ? 4 : 8);
-    const int64_t cb = (CVn + 31) / 32;
+    const int cvb = ln_pg_cvb(CVn);
+    const int64_t cb = CVn / cvb;
     int64_t seg = (rows * cb + 2 * kNumSMs - 1) / (2 * kNumSMs);  // ~2 waves
     seg = seg < 64 ? 64 : seg;
     dim3 g2(static_cast<unsigned>(cb), static_cast<unsigned>((rows + seg - 1) / seg));
     DISPATCH_T(dtype, launch_k(ln_param_grad_kernel<T>, dim3(g2), dim3(256), 0, ST, 
                           cp<T>(x), cp<T>(dy), mean, rstd, rows, C, seg, dgamma, dbeta, nullptr, 0,
-                          0, 0));
+                          0, 0, cvb));
   }
   if (mod && dmod) {
-    dim3 g2(static_cast<unsigned>((C / (dtype == DP_F32 ? 4 : 8) + 31) / 32), static_cast<unsigned>(rows / rps));
+    const int CVn = C / (dtype == DP_F32 ? 4 : 8);
+    const int cvb = ln_pg_cvb(CVn);
+    dim3 g2(static_cast<unsigned>(CVn / cvb), static_cast<unsigned>(rows / rps));
     DISPATCH_T(dtype, launch_k(ln_param_grad_kernel<T>, dim3(g2), dim3(256), 0, ST, 
                           cp<T>(x), cp<T>(dy), mean, rstd, rows, C, rps, nullptr, nullptr,
-                          mp<T>(dmod), dmod_ld, shift_off, scale_off));
+                          mp<T>(dmod), dmod_ld, shift_off, scale_off, cvb));
   }
   return ew_check("layer_norm_bwd");
 }

@@ -198,12 +198,18 @@ class ResBlock:
         self.n2 = nn.GroupNorm(s, f"{p}.norm2", cout, groups, eps, silu=True)
         self.c2 = nn.Conv2d(s, f"{p}.conv2", cout, cout, 3, init="z")
         self.skip = nn.Conv2d(s, f"{p}.skip", cin, cout, 1) if cin != cout else None
+        # conv1's bias gradient comes from the temb row bias's per-sample sums (no separate pass)
+        self.c1.bias_grad_by_row = self.emb is not None and nn.ROW_BIAS_DB
+        if self.emb is not None:
+            self.emb.bias_grad_by_row = nn.ROW_BIAS_DB  # its bias gradient = sum_b de[b]: the same sums
 
     def __call__(self, x, temb_act=None):
         hn, x = self.n1.fork(x)  # x's skip-path gradient is accumulated in the GroupNorm backward
         h = self.c1(hn)
         if self.emb is not None:
-            h = nn.add_row_bias(h, self.emb(temb_act))
+            by_row = self.c1.bias_grad_by_row
+            h = nn.add_row_bias(h, self.emb(temb_act), bias=self.c1.bias if by_row else None,
+                                e_bias=self.emb.bias if by_row else None)
         sk = x if self.skip is None else self.skip(x)
         return self.c2(self.n2(h), residual=sk)
 
@@ -325,7 +331,9 @@ class TextEncoderBase(Component):
         def block(st):
             h = st["h"]
             h = blk["attn"](blk["ln1"](h), residual=h)
-            h = blk["fc2"](nn.gelu(blk["fc1"](blk["ln2"](h)), tanh=gelu_tanh), residual=h)
+            x = blk["ln2"](h)
+            a = nn.gelu(blk["fc1"](x), tanh=True) if gelu_tanh else nn.linear_gelu(x, blk["fc1"])
+            h = blk["fc2"](a, residual=h)
             return {"h": h}
         return block
 

@@ -287,7 +287,7 @@ class _LinearFn(torch.autograd.Function):
             dx = ops.linear_dgrad(dy2, W.w, cache=_flip_cache(layer)).view(*dy.shape[:-1], W.shape[1])
         if W.g is not None:
             ops.linear_wgrad(dy2, x2, W.g)
-        if layer.bias is not None and layer.bias.g is not None:
+        if layer.bias is not None and layer.bias.g is not None and not layer.bias_grad_by_row:
             ops.bias_grad(dy2, layer.bias.g)
         return dx, None, (dy if ctx.has_res else None), None
 
@@ -299,6 +299,8 @@ FUSED_GEGLU = os.environ.get("DP_FUSED_GEGLU", "1") != "0"
 # than the dgrad GEMM + the vectorised GEGLU-backward kernel (140 vs 125 us at 32768x320: the epilogue's
 # per-row reads of h), so it is off by default
 FUSED_GEGLU_BWD = os.environ.get("DP_FUSED_GEGLU_BWD", "0") != "0"
+# ff1's bias gradient accumulated by the GEGLU-backward pass (DP_GEGLU_BIAS_DB=0: separate pass, A/B)
+GEGLU_BIAS_DB = os.environ.get("DP_GEGLU_BIAS_DB", "1") != "0"
 # cached dgrad weight copies refreshed by one batched launch per optimizer slice (DP_FLIP_BATCH=0: per param)
 FLIP_BATCH = os.environ.get("DP_FLIP_BATCH", "1") != "0"
 
@@ -321,13 +323,14 @@ class _LinearGegluFn(torch.autograd.Function):
         x2, h = ctx.saved_tensors
         layer = ctx.layer
         W = layer.weight
-        dh = ops.geglu_bwd(h, _c(dy).view(h.shape[0], -1))
+        db = layer.bias.g if (layer.bias is not None and GEGLU_BIAS_DB) else None
+        dh = ops.geglu_bwd(h, _c(dy).view(h.shape[0], -1), db=db)
         dx = None
         if ctx.needs_input_grad[0]:
             dx = ops.linear_dgrad(dh, W.w, cache=_flip_cache(layer)).view(*dy.shape[:-1], W.shape[1])
         if W.g is not None:
             ops.linear_wgrad(dh, x2, W.g)
-        if layer.bias is not None and layer.bias.g is not None:
+        if layer.bias is not None and layer.bias.g is not None and db is None:
             ops.bias_grad(dh, layer.bias.g)
         return dx, None, None
 
@@ -361,16 +364,19 @@ class _FeedForwardGegluFn(torch.autograd.Function):
             ops.linear_wgrad(d2, y, ff2.weight.g)
         if ff2.bias.g is not None:
             ops.bias_grad(d2, ff2.bias.g)
+        db1 = None
         if FUSED_GEGLU_BWD:
             dh = ops.linear_dgrad_geglu(d2, ff2.weight.w, h, cache=_flip_cache(ff2))
         else:
-            dh = ops.geglu_bwd(h, ops.linear_dgrad(d2, ff2.weight.w, cache=_flip_cache(ff2)))
+            # ff1's bias gradient in the GEGLU-backward pass (no separate re-read of dh)
+            db1 = ff1.bias.g if GEGLU_BIAS_DB else None
+            dh = ops.geglu_bwd(h, ops.linear_dgrad(d2, ff2.weight.w, cache=_flip_cache(ff2)), db=db1)
         dx = None
         if ctx.needs_input_grad[0]:
             dx = ops.linear_dgrad(dh, ff1.weight.w, cache=_flip_cache(ff1)).view(*dout.shape[:-1], x2.shape[1])
         if ff1.weight.g is not None:
             ops.linear_wgrad(dh, x2, ff1.weight.g)
-        if ff1.bias.g is not None:
+        if ff1.bias.g is not None and db1 is None:
             ops.bias_grad(dh, ff1.bias.g)
         return dx, None, (dout if ctx.has_res else None), None, None
 
@@ -384,6 +390,22 @@ def feed_forward_geglu(x, ff1, ff2, residual=None):
             and F % 64 == 0 and x.shape[-1] % 8 == 0 and rows >= 1024 and ff2.weight.shape[1] == F):
         return _FeedForwardGegluFn.apply(x, _anchor(), residual, ff1, ff2)
     return ff2(geglu(ff1(x)), residual=residual)
+
+
+# frozen (no-grad) bf16 MLPs: GELU in the fc1 GEMM epilogue (DP_GELU_EPI=0: separate activation pass)
+GELU_EPI = os.environ.get("DP_GELU_EPI", "1") != "0"
+
+
+def linear_gelu(x, layer):
+    """gelu_erf(layer(x)): one GEMM with the activation in its epilogue when no gradient is recorded
+    (frozen encoders), the linear + activation pair otherwise."""
+    N = layer.weight.shape[0]
+    if (GELU_EPI and not torch.is_grad_enabled() and x.dtype == torch.bfloat16 and x.is_cuda
+            and layer.bias is not None and N % 128 == 0 and x.shape[-1] % 8 == 0):
+        K = x.shape[-1]
+        y = ops.linear_gelu(_c(x).view(-1, K), layer.weight.w, layer.bias.w)
+        return y.view(*x.shape[:-1], N)
+    return gelu(layer(x))
 
 
 def linear_geglu(x, layer):
@@ -443,7 +465,7 @@ class _ConvFn(torch.autograd.Function):
                                   cache=_flip_cache(layer))
         if layer.weight.g is not None:
             ops.conv2d_wgrad(dy, x, layer.weight.g, stride=layer.stride, pad=layer.pad)
-        if layer.bias is not None and layer.bias.g is not None:
+        if layer.bias is not None and layer.bias.g is not None and not layer.bias_grad_by_row:
             ops.bias_grad(dy, layer.bias.g)
         return dx, None, (dy if ctx.has_res else None), None
 
@@ -639,18 +661,22 @@ class _RowBiasFn(torch.autograd.Function):
     """y = x + e[b] broadcast over the pixels/tokens of sample b."""
 
     @staticmethod
-    def forward(ctx, x, e):
+    def forward(ctx, x, e, bias, e_bias):
         x = _c(x)
         B = e.shape[0]
         rps = x.numel() // x.shape[-1] // B
         ctx.meta = (B, rps)
+        ctx.biases = (bias, e_bias)
         return ops.row_bias(x, e, rps)
 
     @staticmethod
     def backward(ctx, dy):
         B, rps = ctx.meta
         dy = _c(dy)
-        return dy, ops.row_bias_bwd(dy, B, rps)
+        # the producing conv's and the temb projection's bias gradients (both = sum of dy over every row)
+        # from the same per-sample sums
+        db, db2 = (b.g if b is not None else None for b in ctx.biases)
+        return dy, ops.row_bias_bwd(dy, B, rps, db=db, db2=db2), None, None
 
 
 class _ConcatFn(torch.autograd.Function):
@@ -835,6 +861,8 @@ class Linear:
         self.store = store
         self.weight = store.add(f"{name}.weight", (fout, fin), init=init)
         self.bias = store.add(f"{name}.bias", (fout,), fp32=True, init="b") if bias else None
+        # True when the output feeds only a per-sample row bias whose backward produces this bias gradient
+        self.bias_grad_by_row = False
 
     def __call__(self, x, residual=None):
         return _LinearFn.apply(x, _anchor(), residual, self)
@@ -852,6 +880,9 @@ class Conv2d:
         self.weight = store.add(f"{name}.weight", (cout, k, k, cin), init=init)
         self.bias = store.add(f"{name}.bias", (cout,), fp32=True, init="b") if bias else None
         self.gn_stats = 0  # GroupNorm groups of the output's consumer (statistics in the conv epilogue)
+        # True when the output's only consumer is a per-sample row bias (ResBlock conv1 + temb) whose
+        # backward also produces this conv's bias gradient (add_row_bias(..., bias=...))
+        self.bias_grad_by_row = False
 
     def out_hw(self, x):
         H, W = x.shape[1], x.shape[2]
@@ -916,8 +947,14 @@ def add(a, b):
     return _AddFn.apply(a, b)
 
 
-def add_row_bias(x, e):
-    return _RowBiasFn.apply(x, e)
+# DP_ROW_BIAS_DB=0: ResBlock conv1's bias gradient by its own pass over dy (A/B)
+ROW_BIAS_DB = os.environ.get("DP_ROW_BIAS_DB", "1") != "0"
+
+
+def add_row_bias(x, e, bias=None, e_bias=None):
+    """x + e[sample]; `bias` / `e_bias` (Params whose layers have bias_grad_by_row set: the layer that
+    produced x / e) each also receive sum(dy) over every row in the backward."""
+    return _RowBiasFn.apply(x, e, bias, e_bias)
 
 
 def concat(a, b):

@@ -112,6 +112,33 @@ def linear(x, w, bias=None, residual=None, out=None):
                 bias=bias, residual=residual)
 
 
+def linear_gelu(x, w, bias, out=None):
+    """y[M,N] = gelu_erf(x @ w^T + bias) in one tensor-core GEMM (GELU in the epilogue, no separate
+    activation pass); bf16, K-major operands, N % 128 == 0 (the frozen text encoders' MLP fc1)."""
+    _require_cuda(x, w, bias)
+    M, K = x.shape
+    N = w.shape[0]
+    y = torch.empty(M, N, device=x.device, dtype=x.dtype) if out is None else out
+    args = DpGemmArgs()
+    args.M, args.N, args.K = M, N, K
+    args.batch1, args.batch2 = 1, 1
+    args.dtype = dtype_code(x)
+    args.A, args.a_ld, args.a_bs1, args.a_bs2, args.a_mn_major = _ptr(x), x.stride(0), 0, 0, 0
+    args.B, args.b_ld, args.b_bs1, args.b_bs2, args.b_mn_major = _ptr(w), w.stride(0), 0, 0, 0
+    args.D, args.d_dtype, args.d_ld, args.d_bs1, args.d_bs2 = _ptr(y), dtype_code(y), y.stride(0), 0, 0
+    args.out_mode = DP_OUT_STORE
+    args.bias = _ptr(bias)
+    args.Res = None
+    args.r_ld, args.r_bs1, args.r_bs2 = y.stride(0), 0, 0
+    args.alpha = 1.0
+    args.split_k = 0
+    args.geglu_mode = 3
+    telemetry.timed("tcgen05_gemm", 2.0 * M * N * K,
+                    lambda: check(_lib.lib().dp_gemm(ctypes.byref(args), _stream()), "dp_gemm"),
+                    sub=f"linear {M}x{N}x{K} gelu" if telemetry.SHAPES else "linear")
+    return y
+
+
 def linear_geglu(x, w, bias, h_out=None, y_out=None):
     """h[M,2F] = x @ w^T + bias (the GEGLU pre-activation, stored for the backward) and
     y[M,F] = h[:, :F] * gelu_erf(h[:, F:]) in ONE tensor-core GEMM (the epilogue writes both);
@@ -276,8 +303,7 @@ def _pad_last(t, mult=64):
     pad = -C % mult
     if not pad:
         return t
-    z = torch.zeros(*t.shape[:-1], pad, device=t.device, dtype=t.dtype)
-    return concat_last(t.contiguous(), z)
+    return concat_last(t.contiguous(), None, pad)  # the concat kernel writes the zero channels itself
 
 
 def _pad_first(w, mult=64):
@@ -468,9 +494,15 @@ def geglu(x):
     return y
 
 
-def geglu_bwd(x, dy):
+def geglu_bwd(x, dy, db=None):
+    """dx = GEGLU'(x) dy; with db (fp32 [2F]) also db += column sums of dx (the bias gradient of the
+    projection that produced x, fused into the same pass)."""
     rows, F2 = x.numel() // x.shape[-1], x.shape[-1]
     dx = torch.empty_like(x)
+    if db is not None:
+        check(_L().dp_geglu_bwd_db(dtype_code(x), _ptr(x), _ptr(dy), _ptr(dx), rows, F2 // 2, _ptr(db),
+                                   _stream()), "dp_geglu_bwd_db")
+        return dx
     check(_L().dp_geglu_bwd(dtype_code(x), _ptr(x), _ptr(dy), _ptr(dx), rows, F2 // 2, _stream()),
           "dp_geglu_bwd")
     return dx
@@ -714,9 +746,15 @@ def row_bias(x, e, rows_per_sample):
     return y
 
 
-def row_bias_bwd(dy, B, rows_per_sample):
+def row_bias_bwd(dy, B, rows_per_sample, db=None, db2=None):
+    """de[b] = sum of dy over sample b; with db / db2 (fp32 [C]) also db += sum of dy over all rows and
+    db2 += the same (the bias gradients of the layers that produced x and e, from the same per-sample sums)."""
     C = dy.shape[-1]
     de = torch.empty(B, C, device=dy.device, dtype=dy.dtype)
+    if db is not None or db2 is not None:
+        check(_L().dp_row_bias_bwd_db(dtype_code(dy), _ptr(dy), _ptr(de), C, B, C, rows_per_sample, _ptr(db),
+                                      _ptr(db2), _stream()), "dp_row_bias_bwd_db")
+        return de
     check(_L().dp_row_bias_bwd(dtype_code(dy), _ptr(dy), _ptr(de), C, B, C, rows_per_sample, _stream()),
           "dp_row_bias_bwd")
     return de

@@ -228,9 +228,12 @@ _EARLY_TAIL = bool(int(__import__("os").environ.get("DP_EARLY_TAIL", "0")))  # e
 # single-device frozen tail (no transfers) replayed as one CUDA graph per (program, tail): the ~350 launches of
 # the next batch's VAE + text-encoder forwards leave the host's critical path (DP_TAIL_GRAPH=0: eager)
 _TAIL_GRAPH = bool(int(__import__("os").environ.get("DP_TAIL_GRAPH", "1")))
-# the compute stream joins the optimizer stream at the end of the iteration instead of at the sync task
-# (DP_LATE_OPT_JOIN=0: at the sync task, the previous behaviour)
-_LATE_OPT_JOIN = bool(int(__import__("os").environ.get("DP_LATE_OPT_JOIN", "1")))
+# DP_LATE_OPT_JOIN=1: the compute stream joins the optimizer stream at the end of the iteration instead of
+# at the sync task. Off by default: measured neutral at N=1, and with per-slice gradient snapshots on (the
+# parity tests) c2 iterations hung in the device synchronize with it on (tools/hang_probe.py: 2 of 3 snapshot
+# runs, and the c2 parity / optimizer-overlap test files; the run with it off completed;
+# profiles/r02_hang_probe.txt)
+_LATE_OPT_JOIN = bool(int(__import__("os").environ.get("DP_LATE_OPT_JOIN", "0")))
 
 
 class _Tracer:
@@ -610,8 +613,7 @@ class PipelineExecutor:
                     dist.all_reduce(store.grad[a:b], group=pg)
                 if self.grad_snapshots is not None:
                     # parity tests: the reduced gradient slice exactly as this AdamW chunk reads it
-                    self.grad_snapshots.append((a, b, store.grad[a:b].detach().clone()))
-                    self.grad_snapshot_pipes.append(self.prog.pipes[pi].backbone)
+                    self._snapshot(store, a, b, self.prog.pipes[pi].backbone)
                 # background chunks: one CTA per SM at most (see dp_adamw_apply); the final chunk
                 # at the sync point has the machine to itself
                 store.adamw_apply((a, b), max_ctas=0 if (final and not _LATE_OPT_JOIN) else self.OVERLAP_CTAS,
@@ -794,8 +796,7 @@ class PipelineExecutor:
             else:
                 dist.all_reduce(store.grad[lo:hi], group=pg)
         if self.grad_snapshots is not None:
-            self.grad_snapshots.append((lo, hi, store.grad[lo:hi].detach().clone()))
-            self.grad_snapshot_pipes.append(self.prog.pipes[pi].backbone)
+            self._snapshot(store, lo, hi, self.prog.pipes[pi].backbone)
         store.adamw_step(rng=(lo, hi), **self.model.adamw)
         store.zero_grad((lo, hi))
 
@@ -821,6 +822,8 @@ class PipelineExecutor:
         self._saved, self._xt, self._feedback_in, self._pending = {}, {}, {}, []
         store, posted, sent = {}, {}, set()
         self.loss_buf.zero_()
+        if self.grad_snapshots is not None:
+            self._alloc_snapshot_bufs()
         tr = self.tracer = _Tracer(self.streams, self.dev) if trace else None
         # optimizer overlap: the micro-batch of each pipe's final backward on this device
         self._ovl_on = self.overlap_sync and self.streams.cuda
@@ -889,6 +892,23 @@ class PipelineExecutor:
                 self.streams.compute.wait_stream(self.opt_stream)
             torch.cuda.current_stream(self.device).wait_stream(self.streams.compute)
         return self.loss_buf
+
+    def _snapshot(self, store, a, b, backbone):
+        """Copy grad[a:b] into the store's preallocated snapshot buffer on the current stream (no
+        allocation inside the backward: a cudaMalloc / cudaFree there synchronises the device from
+        the autograd thread)."""
+        buf = self._snap_bufs[id(store)]
+        buf[a:b].copy_(store.grad[a:b])
+        self.grad_snapshots.append((a, b, buf[a:b]))
+        self.grad_snapshot_pipes.append(backbone)
+
+    def _alloc_snapshot_bufs(self):
+        if not hasattr(self, "_snap_bufs"):
+            self._snap_bufs = {}
+        for pi in range(len(self.prog0.pipes)):
+            st = self._backbone(pi).store
+            if id(st) not in self._snap_bufs and getattr(st, "grad", None) is not None:
+                self._snap_bufs[id(st)] = torch.empty_like(st.grad)
 
     def take_grad_snapshots(self):
         """Parity tests: the reduced gradients captured since the last call (grad_snapshots = []

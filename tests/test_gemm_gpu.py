@@ -363,3 +363,20 @@ def test_conv_groupnorm_statistics_epilogue(N, H, C, K, stride):
     a1, m1, r1 = ops.group_norm(y, gam, bet, G, 1e-6, True, sums=sums)
     a2, m2, r2 = ops.group_norm(y, gam, bet, G, 1e-6, True)
     assert _rel(m1, m2) < 1e-4 and _rel(r1, r2) < 1e-3 and _rel(a1, a2) < 1e-2
+
+
+@pytest.mark.parametrize("M,N,K", [(2464, 4096, 1024), (200, 4096, 1024), (300, 384, 136), (1000, 256, 64)])
+def test_linear_gelu_epilogue(M, N, K):
+    """Frozen-MLP fc1 with GELU (erf) in the GEMM epilogue vs the unfused GEMM + activation kernel and an
+    fp32 torch reference; nn.linear_gelu takes the fused path only without autograd."""
+    ops = _ops()
+    from paper_2405_01248_b200 import nn
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    x = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    b = torch.randn(N, device="cuda", generator=g) * 0.1
+    y = ops.linear_gelu(x, w, b)
+    y_ref = ops.act(ops.linear(x, w, bias=b), nn.DP_ACT_GELU)
+    assert _rel(y, y_ref) < 5e-3
+    yf = F.gelu(x.float() @ w.float().t() + b)
+    assert _rel(y, yf) < 1e-2

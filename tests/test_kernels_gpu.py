@@ -332,3 +332,43 @@ def test_concat_last(dt, Ca, Cb, zeros):
     out = ops.concat_last(a, b, Cb)
     ref = torch.cat([a, torch.zeros(7, 9, Cb, device="cuda", dtype=dt) if zeros else b], -1)
     assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("dt", DT)
+@pytest.mark.parametrize("rows,F", [(32768, 1280), (8192, 2560), (2048, 5120), (512, 5120), (100, 64), (77, 40)])
+def test_geglu_bwd_bias_fused(dt, rows, F):
+    """GEGLU backward with the FF input projection's bias gradient fused (db += column sums of dx) vs
+    fp32 torch autograd; dx identical to the unfused kernel."""
+    from paper_2405_01248_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(rows + F)
+    x = torch.randn(rows, 2 * F, device="cuda", generator=g).to(dt)
+    dy = torch.randn(rows, F, device="cuda", generator=g).to(dt)
+    db0 = torch.randn(2 * F, device="cuda", generator=g)
+    db = db0.clone()
+    dx = ops.geglu_bwd(x, dy, db=db)
+    assert torch.equal(dx, ops.geglu_bwd(x, dy))
+    xr = x.float().requires_grad_(True)
+    a, gg = xr[:, :F], xr[:, F:]
+    (a * torch.nn.functional.gelu(gg)).backward(dy.float())
+    tol = 1e-4 if dt == torch.float32 else 2e-2
+    assert _rel(dx, xr.grad) < tol
+    assert _rel(db - db0, dx.float().sum(0)) < 1e-4
+
+
+@pytest.mark.parametrize("dt", DT)
+@pytest.mark.parametrize("B,rps,C", [(32, 1024, 320), (32, 256, 640), (32, 64, 1280), (32, 16, 1280), (3, 7, 12),
+                                     (2, 5, 2056)])
+def test_row_bias_bwd_conv_bias(dt, B, rps, C):
+    """Per-sample row-bias backward that also accumulates the producing conv's bias gradient
+    (db += sum of dy over all rows) vs fp32 torch; de identical to the plain kernel."""
+    from paper_2405_01248_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(B * rps + C)
+    dy = torch.randn(B * rps, C, device="cuda", generator=g).to(dt)
+    db0 = torch.randn(C, device="cuda", generator=g)
+    db = db0.clone()
+    db2 = -db0
+    de = ops.row_bias_bwd(dy, B, rps, db=db, db2=db2)
+    assert torch.equal(de, ops.row_bias_bwd(dy, B, rps))
+    assert _rel(de, dy.float().view(B, rps, C).sum(1)) < (1e-5 if dt == torch.float32 else 1e-2)
+    assert _rel(db - db0, dy.float().sum(0)) < 1e-4
+    assert _rel(db2 + db0, dy.float().sum(0)) < 1e-4  # the temb projection's bias gradient (same sums)
