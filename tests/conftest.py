@@ -25,3 +25,21 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+@pytest.fixture(autouse=True)
+def _release_cuda_memory(request):
+    """After each GPU test: drop the test's tensors and return the caching allocator's free blocks, so a
+    long single-process `-m gpu` run (the full-size c2 / c3 / c5 trainers back to back) starts every test
+    from an unfragmented pool instead of reaching cudaMalloc / cudaFree in the middle of a backward."""
+    yield
+    if "gpu" not in request.keywords:
+        return
+    import gc
+
+    import torch
+
+    if torch.cuda.is_available():
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
