@@ -45,7 +45,7 @@ def _frozen(tr, ready, n):
     return {k: v.float().cpu() for k, v in m.items()}
 
 
-def _isolated(*args, timeout=900):
+def _isolated(*args, timeout=600):
     """Run one case of this file in a fresh process (own CUDA context); retry once after a timeout."""
     cmd = [sys.executable, os.path.abspath(__file__), *args]
     for attempt in range(2):

@@ -9,4 +9,4 @@ for r in 1 2 3; do
   echo "== WORK run $r" >> gpurun_out/ab_tree.log
   timeout 400 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | grep '^{' | cut -c1-120 >> gpurun_out/ab_tree.log
 done
-timeout -s KILL 1300 python -m pytest tests/test_bench_config_parity_gpu.py -q -x > gpurun_out/bcp_tests.log 2>&1; echo rc=$? >> gpurun_out/bcp_tests.log
+timeout -s KILL 1300 python -m pytest tests/test_zz_bench_config_parity_gpu.py -q -x > gpurun_out/bcp_tests.log 2>&1; echo rc=$? >> gpurun_out/bcp_tests.log

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_optimizer_overlap_gpu.py tests/test_bench_config_parity_gpu.py -q -x > gpurun_out/join_tests.log 2>&1; echo rc=$? >> gpurun_out/join_tests.log
+timeout 600 python -m pytest tests/test_optimizer_overlap_gpu.py tests/test_zz_bench_config_parity_gpu.py -q -x > gpurun_out/join_tests.log 2>&1; echo rc=$? >> gpurun_out/join_tests.log
 : > gpurun_out/join_ab.log
 for v in "X=1" "DP_LATE_OPT_JOIN=0" "X=2" "DP_LATE_OPT_JOIN=0 DP_TAIL_GRAPH=0"; do
   echo "== $v" >> gpurun_out/join_ab.log

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_c2_parity_gpu.py tests/test_cuda_graph_gpu.py tests/test_c1_parity_gpu.py tests/test_bench_config_parity_gpu.py -q -x > gpurun_out/tail_tests.log 2>&1; echo rc=$? >> gpurun_out/tail_tests.log
+timeout 600 python -m pytest tests/test_c2_parity_gpu.py tests/test_cuda_graph_gpu.py tests/test_c1_parity_gpu.py tests/test_zz_bench_config_parity_gpu.py -q -x > gpurun_out/tail_tests.log 2>&1; echo rc=$? >> gpurun_out/tail_tests.log
 : > gpurun_out/tail_ab.log
 for v in "X=1" "DP_TAIL_GRAPH=0" "X=2"; do
   echo "== $v" >> gpurun_out/tail_ab.log
